@@ -1,0 +1,163 @@
+/*
+ * dfpca_cuda.h -- C-ABI of libdfpca_cuda.so, the sm_100a implementation of the
+ * binned multi-dimensional FPCA hot path (reference: arxiv 1510.04439, C++
+ * header library `proj/include/dfpca`).
+ *
+ * Every entry point takes plain pointers and sizes; no C++ or torch types cross
+ * this boundary.  Host pointers are host memory; results stay device-resident
+ * behind opaque handles (dfpca_binned, dfpca_surface) so that the stages can be
+ * chained without host round trips, and are copied out only on request.
+ *
+ * Status convention (mirrors dfpca::ErrorClass, reference errors.hpp:11-17):
+ *   0 = ok, 2 = Parse, 3 = Config, 4 = Numeric, 5 = Version.
+ * On a nonzero status, dfpca_last_error() returns the reference error name
+ * (e.g. "HaloTooSmall", errors.hpp:37-90) and the message, so a host wrapper
+ * can rethrow the matching dfpca::Error.  Device (CUDA) failures are reported
+ * as class 4 with name "DeviceError".
+ *
+ * Flattened arrays are row-major with the LAST axis fastest (grid.hpp:14-16);
+ * covariance surfaces are flattened s_flat * G + t_flat (surface.hpp:14).
+ */
+#ifndef DFPCA_CUDA_H_
+#define DFPCA_CUDA_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DFPCA_API __attribute__((visibility("default")))
+#else
+#define DFPCA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFPCA_MAX_DIM 3
+
+typedef struct dfpca_context dfpca_context;
+typedef struct dfpca_binned dfpca_binned;
+typedef struct dfpca_surface dfpca_surface;
+
+/* Grid descriptor: the data an EvaluationGrid carries (grid.hpp:92-230).
+ * axes[k] points at shape[k] strictly increasing node coordinates (host).
+ * mask is NULL (every node inside) or prod(shape) bytes, 1 = inside. */
+typedef struct dfpca_grid {
+  int32_t dim;
+  int64_t shape[DFPCA_MAX_DIM];
+  const double* axes[DFPCA_MAX_DIM];
+  const uint8_t* mask;
+} dfpca_grid;
+
+/* Overlapping-block plan (fft_smoother.hpp:37-53).  blocks_lo / blocks_hi hold
+ * n_blocks * dim node indices (block b, axis k at b * dim + k); halo holds dim
+ * values.  The device path is plan-invariant (the reference guarantees
+ * bit-invariant cores, fft_smoother.hpp:24-29), so the plan is only validated
+ * (validate_block_plan, fft_smoother.hpp:101-145).  Pass NULL for the
+ * single-block plan. */
+typedef struct dfpca_plan {
+  int64_t n_blocks;
+  const int64_t* blocks_lo;
+  const int64_t* blocks_hi;
+  const int64_t* halo;
+} dfpca_plan;
+
+enum { DFPCA_TARGET_MEAN = 0, DFPCA_TARGET_SQUARES = 1 };
+enum { DFPCA_SURFACE_MEAN = 0, DFPCA_SURFACE_COVARIANCE = 1, DFPCA_SURFACE_DIAG = 2 };
+
+/* ---- context ------------------------------------------------------------ */
+/* One CUDA device, one stream, one workspace per context.  Calls on one
+ * context are synchronous at return and must not overlap; distinct contexts
+ * may be used from distinct host threads. */
+DFPCA_API int dfpca_context_create(int device, dfpca_context** out);
+DFPCA_API int dfpca_context_destroy(dfpca_context* ctx);
+DFPCA_API int dfpca_last_error(const dfpca_context* ctx, int* error_class, const char** name,
+                     const char** message);
+/* Sample / observation index attached to ObservationOutsideGrid (-1 if none). */
+DFPCA_API int dfpca_last_error_location(const dfpca_context* ctx, int64_t* sample, int64_t* obs);
+/* Device time (ms, CUDA events) of the stages run by the last call, by name:
+ * "binning", "pairs", "moments", "solve", "fallback", "center", "eigen", ... */
+DFPCA_API int dfpca_stage_time(const dfpca_context* ctx, const char* stage, double* ms);
+/* Number of kernels this context has launched since creation. */
+DFPCA_API int64_t dfpca_kernel_launches(const dfpca_context* ctx);
+
+/* ---- binning: replaces dfpca::linear_bin (binning.hpp:82-183) ------------ */
+/* Observations in CSR form: sample i owns observations
+ * obs_offsets[i] .. obs_offsets[i+1]-1; coords holds dim doubles per
+ * observation, values one.  Bit-exact with the reference: every bin is an
+ * ordered (sample, observation, corner) sum without contraction. */
+DFPCA_API int dfpca_linear_bin(dfpca_context* ctx, const dfpca_grid* grid, int64_t n_samples,
+                     const int64_t* obs_offsets, const double* coords, const double* values,
+                     int mean_path, int covariance_path, dfpca_binned** out);
+
+/* Sizes needed to download a binned handle. */
+DFPCA_API int dfpca_binned_info(const dfpca_binned* b, int64_t* n_samples, int64_t* n_pair_samples,
+                      int64_t* grid_size, int64_t* offset_codes, int* has_mean_path,
+                      int* has_covariance_path);
+
+/* Copies BinnedData fields (binning.hpp:41-74) to host; any pointer may be NULL.
+ * mass/wvalue/wsquare: G; sample_index/pair_weight: n_pair_samples;
+ * ps_mass/ps_value: n_pair_samples * G; diag_mass/diag_value: G * 3^dim;
+ * sample_sizes: n_samples. */
+DFPCA_API int dfpca_binned_download(dfpca_context* ctx, const dfpca_binned* b, double* mass,
+                          double* wvalue, double* wsquare, int64_t* sample_index,
+                          double* pair_weight, double* ps_mass, double* ps_value,
+                          double* diag_mass, double* diag_value, int64_t* sample_sizes);
+
+/* Uploads a host-built BinnedData (tests construct them by hand). */
+DFPCA_API int dfpca_binned_upload(dfpca_context* ctx, const dfpca_grid* grid, int64_t n_samples,
+                        const int64_t* sample_sizes, int has_mean_path, const double* mass,
+                        const double* wvalue, const double* wsquare, int has_covariance_path,
+                        int64_t n_pair_samples, const int64_t* sample_index,
+                        const double* pair_weight, const double* ps_mass,
+                        const double* ps_value, const double* diag_mass,
+                        const double* diag_value, dfpca_binned** out);
+DFPCA_API int dfpca_binned_free(dfpca_binned* b);
+
+/* ---- smoothing ------------------------------------------------------------ */
+/* Replaces dfpca::fft_local_linear (fft_smoother.hpp:498-575) and
+ * blockwise_apply (:747).  h: dim bandwidths.  out: G host doubles (NaN at
+ * masked nodes).  out_surface (optional) receives a device-resident copy. */
+DFPCA_API int dfpca_local_linear(dfpca_context* ctx, const dfpca_binned* b, const dfpca_grid* grid,
+                       const double* h, int target, const dfpca_plan* plan, double* out,
+                       dfpca_surface** out_surface);
+
+/* Replaces dfpca::fft_covariance (fft_smoother.hpp:585-744) and
+ * blockwise_apply (:754).  mean: G host doubles (the mean surface).  The
+ * symmetrized covariance stays on the device in *out (G*G doubles). */
+DFPCA_API int dfpca_covariance(dfpca_context* ctx, const dfpca_binned* b, const dfpca_grid* grid,
+                     const double* h, const double* mean, const dfpca_plan* plan,
+                     dfpca_surface** out);
+
+/* Pair-product grids pw / pv over the full 2d-dim product grid
+ * (PairGridSource::extract of the full box, fft_smoother.hpp:341-437);
+ * G*G host doubles each, either may be NULL. */
+DFPCA_API int dfpca_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, double* pv);
+
+/* ---- surfaces -------------------------------------------------------------- */
+DFPCA_API int dfpca_surface_info(const dfpca_surface* s, int* kind, int64_t* n_values);
+DFPCA_API int dfpca_surface_download(dfpca_context* ctx, const dfpca_surface* s, double* out);
+DFPCA_API int dfpca_surface_upload(dfpca_context* ctx, const dfpca_grid* grid, int kind,
+                         const double* values, int64_t n_values, dfpca_surface** out);
+DFPCA_API int dfpca_surface_free(dfpca_surface* s);
+
+/* ---- eigendecomposition ------------------------------------------------- */
+/* Replaces dfpca::matrixize + dfpca::randomized_eig (eigensolve.hpp:71-103,
+ * 245-279) on a device-resident covariance surface.  Outputs (host):
+ *   eigenvalues[L_max], eigenfunctions[L_max * G] (full-grid surfaces, NaN at
+ *   masked nodes), fve[L_max], *total_variance, *n_components (kept L). */
+DFPCA_API int dfpca_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const dfpca_grid* grid,
+                         int64_t q, int64_t L_max, uint64_t seed, double* eigenvalues,
+                         double* eigenfunctions, double* fve, double* total_variance,
+                         int64_t* n_components);
+
+/* Residual diagnostic (eigensolve.hpp:294-312) for L eigenpairs. */
+DFPCA_API int dfpca_eig_residuals(dfpca_context* ctx, const dfpca_surface* cov, const dfpca_grid* grid,
+                        int64_t L, const double* eigenvalues, const double* eigenfunctions,
+                        double* residuals);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DFPCA_CUDA_H_ */

@@ -1,0 +1,298 @@
+// TEST INFRASTRUCTURE ONLY -- the parity oracle.
+//
+// extern "C" driver over the reference implementation itself: the reference's
+// own headers (/root/reference/proj/include/dfpca/*.hpp) are compiled
+// UNCHANGED against the shims in oracle/shim (Eigen subset, FFTW, LAPACKE)
+// into oracle/_ref/libdfpca_ref.so by oracle/Makefile.  Nothing from the
+// product links this; only tests/, __graft_entry__.smoke() and bench.py's
+// CPU baseline / reference arm load it.
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dfpca/binning.hpp"
+#include "dfpca/dataset.hpp"
+#include "dfpca/eigensolve.hpp"
+#include "dfpca/errors.hpp"
+#include "dfpca/fft_smoother.hpp"
+#include "dfpca/grid.hpp"
+#include "dfpca/parallel.hpp"
+#include "dfpca/smoother.hpp"
+
+using namespace dfpca;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_cls = 0;
+
+template <class F>
+int guarded(F&& f) {
+  g_err.clear();
+  g_cls = 0;
+  try {
+    f();
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    g_cls = static_cast<int>(e.error_class());
+  } catch (const std::exception& e) {
+    g_err = std::string("InternalError: ") + e.what();
+    g_cls = 4;
+  }
+  return g_cls;
+}
+
+EvaluationGrid make_grid(int dim, const int64_t* shape, const double* axes, const uint8_t* mask) {
+  std::vector<std::vector<double>> ax(static_cast<std::size_t>(dim));
+  std::size_t off = 0, total = 1;
+  for (int k = 0; k < dim; ++k) {
+    ax[static_cast<std::size_t>(k)].assign(axes + off, axes + off + shape[k]);
+    off += static_cast<std::size_t>(shape[k]);
+    total *= static_cast<std::size_t>(shape[k]);
+  }
+  if (mask) return EvaluationGrid(std::move(ax), std::vector<std::uint8_t>(mask, mask + total));
+  return EvaluationGrid(std::move(ax));
+}
+
+FunctionalDataset make_data(int dim, int64_t n, const int64_t* offsets, const double* coords,
+                            const double* values) {
+  FunctionalDataset d;
+  d.dim = static_cast<std::size_t>(dim);
+  d.samples.resize(static_cast<std::size_t>(n));
+  for (int64_t i = 0; i < n; ++i) {
+    Sample& s = d.samples[static_cast<std::size_t>(i)];
+    s.id = std::to_string(i);
+    s.coords.assign(coords + offsets[i] * dim, coords + offsets[i + 1] * dim);
+    s.values.assign(values + offsets[i], values + offsets[i + 1]);
+  }
+  return d;
+}
+
+BlockPlan plan_for(const EvaluationGrid& g, const Bandwidth& h, int64_t n_blocks) {
+  return n_blocks > 0 ? make_block_plan(g, h, n_blocks) : single_block_plan(g, h);
+}
+
+void put_eig(const EigenSystem& es, int64_t L_cap, int64_t G, double* evals, double* efuncs, double* fve,
+             double* total, int64_t* n_out) {
+  const int64_t L = std::min<int64_t>(static_cast<int64_t>(es.eigenvalues.size()), L_cap);
+  for (int64_t l = 0; l < L; ++l) {
+    evals[l] = es.eigenvalues[static_cast<std::size_t>(l)];
+    fve[l] = es.fve[static_cast<std::size_t>(l)];
+    std::memcpy(efuncs + l * G, es.eigenfunctions[static_cast<std::size_t>(l)].data(),
+                sizeof(double) * static_cast<std::size_t>(G));
+  }
+  *total = es.total_variance;
+  *n_out = L;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(int* cls) {
+  if (cls) *cls = g_cls;
+  return g_err.c_str();
+}
+
+void ref_set_threads(int n) { set_max_threads(n); }
+
+int ref_linear_bin(int dim, const int64_t* shape, const double* axes, const uint8_t* mask, int64_t n,
+                   const int64_t* offsets, const double* coords, const double* values, int mean_path,
+                   int cov_path, void** out) {
+  return guarded([&] {
+    auto g = make_grid(dim, shape, axes, mask);
+    auto data = make_data(dim, n, offsets, coords, values);
+    auto* b = new BinnedData(linear_bin(data, g, BinOptions{mean_path != 0, cov_path != 0}));
+    *out = b;
+  });
+}
+
+int ref_binned_from_host(int dim, const int64_t* shape, const double* axes, const uint8_t* mask,
+                         int64_t n_samples, const int64_t* sample_sizes, int has_mean, const double* mass,
+                         const double* wvalue, const double* wsquare, int has_cov, int64_t n_pair,
+                         const int64_t* sample_index, const double* pair_weight, const double* ps_mass,
+                         const double* ps_value, const double* diag_mass, const double* diag_value,
+                         void** out) {
+  return guarded([&] {
+    auto* b = new BinnedData();
+    b->grid = make_grid(dim, shape, axes, mask);
+    const auto G = static_cast<std::size_t>(b->grid.size());
+    b->has_mean_path = has_mean != 0;
+    b->has_covariance_path = has_cov != 0;
+    for (int64_t i = 0; i < n_samples; ++i) b->sample_sizes.push_back(static_cast<std::size_t>(sample_sizes[i]));
+    if (has_mean) {
+      b->mass.assign(mass, mass + G);
+      b->wvalue.assign(wvalue, wvalue + G);
+      b->wsquare.assign(wsquare, wsquare + G);
+    }
+    if (has_cov) {
+      const std::size_t codes = b->offset_codes();
+      b->diag_mass.assign(diag_mass, diag_mass + G * codes);
+      b->diag_value.assign(diag_value, diag_value + G * codes);
+      for (int64_t i = 0; i < n_pair; ++i) {
+        BinnedData::SampleGrids sg;
+        sg.sample_index = static_cast<std::size_t>(sample_index[i]);
+        sg.pair_weight = pair_weight[i];
+        sg.mass.assign(ps_mass + i * G, ps_mass + (i + 1) * G);
+        sg.value.assign(ps_value + i * G, ps_value + (i + 1) * G);
+        b->per_sample.push_back(std::move(sg));
+      }
+    }
+    *out = b;
+  });
+}
+
+int ref_binned_info(void* h, int64_t* n_samples, int64_t* n_pair, int64_t* G, int64_t* codes) {
+  auto* b = static_cast<BinnedData*>(h);
+  *n_samples = static_cast<int64_t>(b->sample_sizes.size());
+  *n_pair = static_cast<int64_t>(b->per_sample.size());
+  *G = b->grid.size();
+  *codes = static_cast<int64_t>(b->offset_codes());
+  return 0;
+}
+
+int ref_binned_download(void* h, double* mass, double* wvalue, double* wsquare, int64_t* sample_index,
+                        double* pair_weight, double* ps_mass, double* ps_value, double* diag_mass,
+                        double* diag_value, int64_t* sample_sizes) {
+  auto* b = static_cast<BinnedData*>(h);
+  const auto G = static_cast<std::size_t>(b->grid.size());
+  auto cp = [](double* dst, const std::vector<double>& src) {
+    if (dst && !src.empty()) std::memcpy(dst, src.data(), sizeof(double) * src.size());
+  };
+  cp(mass, b->mass);
+  cp(wvalue, b->wvalue);
+  cp(wsquare, b->wsquare);
+  cp(diag_mass, b->diag_mass);
+  cp(diag_value, b->diag_value);
+  for (std::size_t i = 0; i < b->per_sample.size(); ++i) {
+    if (sample_index) sample_index[i] = static_cast<int64_t>(b->per_sample[i].sample_index);
+    if (pair_weight) pair_weight[i] = b->per_sample[i].pair_weight;
+    if (ps_mass) std::memcpy(ps_mass + i * G, b->per_sample[i].mass.data(), sizeof(double) * G);
+    if (ps_value) std::memcpy(ps_value + i * G, b->per_sample[i].value.data(), sizeof(double) * G);
+  }
+  if (sample_sizes)
+    for (std::size_t i = 0; i < b->sample_sizes.size(); ++i) sample_sizes[i] = static_cast<int64_t>(b->sample_sizes[i]);
+  return 0;
+}
+
+void ref_binned_free(void* h) { delete static_cast<BinnedData*>(h); }
+
+int ref_local_linear(void* h, int dim, const int64_t* shape, const double* axes, const uint8_t* mask,
+                     const double* bw, int target, int64_t n_blocks, double* out) {
+  return guarded([&] {
+    auto* b = static_cast<BinnedData*>(h);
+    auto g = make_grid(dim, shape, axes, mask);
+    Bandwidth hb{std::vector<double>(bw, bw + dim)};
+    const MomentTarget t = target == 0 ? MomentTarget::Mean : MomentTarget::Squares;
+    auto est = n_blocks > 0 ? blockwise_apply(plan_for(g, hb, n_blocks), *b, g, hb, t)
+                            : fft_local_linear(*b, g, hb, t);
+    std::memcpy(out, est.values.data(), sizeof(double) * est.values.size());
+  });
+}
+
+int ref_covariance(void* h, int dim, const int64_t* shape, const double* axes, const uint8_t* mask,
+                   const double* bw, const double* mean, int64_t n_blocks, int mode, double* out) {
+  return guarded([&] {
+    auto* b = static_cast<BinnedData*>(h);
+    auto g = make_grid(dim, shape, axes, mask);
+    Bandwidth hb{std::vector<double>(bw, bw + dim)};
+    SurfaceEstimate mu;
+    mu.grid = g;
+    mu.kind = SurfaceKind::Mean;
+    mu.values.assign(mean, mean + g.size());
+    const auto m = static_cast<PairGridSource::Mode>(mode);
+    auto est = fft_covariance(*b, g, hb, mu, plan_for(g, hb, n_blocks), m);
+    std::memcpy(out, est.values.data(), sizeof(double) * est.values.size());
+  });
+}
+
+int ref_pair_grids(void* h, int mode, double* pw, double* pv) {
+  return guarded([&] {
+    auto* b = static_cast<BinnedData*>(h);
+    PairGridSource src(*b, static_cast<PairGridSource::Mode>(mode));
+    std::vector<double> a, c;
+    src.extract(src.full_box(), a, c);
+    std::memcpy(pw, a.data(), sizeof(double) * a.size());
+    std::memcpy(pv, c.data(), sizeof(double) * c.size());
+  });
+}
+
+int ref_randomized_eig(int dim, const int64_t* shape, const double* axes, const uint8_t* mask,
+                       const double* cov, int64_t q, int64_t L_max, uint64_t seed, double* evals,
+                       double* efuncs, double* fve, double* total, int64_t* n_out) {
+  return guarded([&] {
+    SurfaceEstimate s;
+    s.grid = make_grid(dim, shape, axes, mask);
+    s.kind = SurfaceKind::Covariance;
+    const auto G = s.grid.size();
+    s.values.assign(cov, cov + G * G);
+    auto S = matrixize(s);
+    auto es = randomized_eig(S, static_cast<std::size_t>(q), static_cast<std::size_t>(L_max), s.grid, seed);
+    put_eig(es, L_max, G, evals, efuncs, fve, total, n_out);
+  });
+}
+
+int ref_dense_eig(int dim, const int64_t* shape, const double* axes, const uint8_t* mask, const double* cov,
+                  int64_t L_max, double* evals, double* efuncs, double* fve, double* total, int64_t* n_out) {
+  return guarded([&] {
+    SurfaceEstimate s;
+    s.grid = make_grid(dim, shape, axes, mask);
+    s.kind = SurfaceKind::Covariance;
+    const auto G = s.grid.size();
+    s.values.assign(cov, cov + G * G);
+    auto S = matrixize(s);
+    auto es = dense_eig(S, static_cast<std::size_t>(L_max), s.grid);
+    put_eig(es, L_max, G, evals, efuncs, fve, total, n_out);
+  });
+}
+
+int ref_eig_residuals(int dim, const int64_t* shape, const double* axes, const uint8_t* mask,
+                      const double* cov, int64_t L, const double* evals, const double* efuncs, double* out) {
+  return guarded([&] {
+    SurfaceEstimate s;
+    s.grid = make_grid(dim, shape, axes, mask);
+    s.kind = SurfaceKind::Covariance;
+    const auto G = s.grid.size();
+    s.values.assign(cov, cov + G * G);
+    auto S = matrixize(s);
+    EigenSystem es;
+    for (int64_t l = 0; l < L; ++l) {
+      es.eigenvalues.push_back(evals[l]);
+      es.eigenfunctions.emplace_back(efuncs + l * G, efuncs + (l + 1) * G);
+    }
+    auto r = eig_residuals(S, es, s.grid);
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
+  });
+}
+
+int ref_estimate_mean(int dim, const int64_t* shape, const double* axes, const uint8_t* mask, int64_t n,
+                      const int64_t* offsets, const double* coords, const double* values, const double* bw,
+                      int squares, double* out) {
+  return guarded([&] {
+    auto g = make_grid(dim, shape, axes, mask);
+    auto data = make_data(dim, n, offsets, coords, values);
+    Bandwidth hb{std::vector<double>(bw, bw + dim)};
+    auto est = squares ? estimate_diag_plus_noise(data, g, hb) : estimate_mean(data, g, hb);
+    std::memcpy(out, est.values.data(), sizeof(double) * est.values.size());
+  });
+}
+
+int ref_estimate_covariance(int dim, const int64_t* shape, const double* axes, const uint8_t* mask,
+                            int64_t n, const int64_t* offsets, const double* coords, const double* values,
+                            const double* bw, const double* mean, double* out) {
+  return guarded([&] {
+    auto g = make_grid(dim, shape, axes, mask);
+    auto data = make_data(dim, n, offsets, coords, values);
+    Bandwidth hb{std::vector<double>(bw, bw + dim)};
+    SurfaceEstimate mu;
+    mu.grid = g;
+    mu.kind = SurfaceKind::Mean;
+    mu.values.assign(mean, mean + g.size());
+    auto est = estimate_covariance(data, g, hb, mu);
+    std::memcpy(out, est.values.data(), sizeof(double) * est.values.size());
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,138 @@
+"""ctypes binding of libdfpca_cuda.so (include/dfpca_cuda.h).
+
+The library is built in-tree (paper_1510_04439_b200/build.py).  Loading fails
+loudly if it is missing; a context is created lazily on first use and fails
+loudly if there is no CUDA device -- the product path has no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("DFPCA_CUDA_LIB", _HERE / "libdfpca_cuda.so"))
+
+MAX_DIM = 3
+
+
+class DfpcaGrid(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("shape", C.c_int64 * MAX_DIM),
+                ("axes", C.POINTER(C.c_double) * MAX_DIM), ("mask", C.POINTER(C.c_uint8))]
+
+
+class DfpcaPlan(C.Structure):
+    _fields_ = [("n_blocks", C.c_int64), ("blocks_lo", C.POINTER(C.c_int64)),
+                ("blocks_hi", C.POINTER(C.c_int64)), ("halo", C.POINTER(C.c_int64))]
+
+
+# (name, restype, argtypes) -- every symbol declared in include/dfpca_cuda.h
+P = C.c_void_p
+PD = C.POINTER(C.c_double)
+PI64 = C.POINTER(C.c_int64)
+SIGNATURES = [
+    ("dfpca_context_create", C.c_int, [C.c_int, C.POINTER(P)]),
+    ("dfpca_context_destroy", C.c_int, [P]),
+    ("dfpca_last_error", C.c_int, [P, C.POINTER(C.c_int), C.POINTER(C.c_char_p), C.POINTER(C.c_char_p)]),
+    ("dfpca_last_error_location", C.c_int, [P, PI64, PI64]),
+    ("dfpca_stage_time", C.c_int, [P, C.c_char_p, PD]),
+    ("dfpca_kernel_launches", C.c_int64, [P]),
+    ("dfpca_linear_bin", C.c_int, [P, C.POINTER(DfpcaGrid), C.c_int64, PI64, PD, PD, C.c_int, C.c_int,
+                                   C.POINTER(P)]),
+    ("dfpca_binned_info", C.c_int, [P, PI64, PI64, PI64, PI64, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("dfpca_binned_download", C.c_int, [P, P, PD, PD, PD, PI64, PD, PD, PD, PD, PD, PI64]),
+    ("dfpca_binned_upload", C.c_int, [P, C.POINTER(DfpcaGrid), C.c_int64, PI64, C.c_int, PD, PD, PD, C.c_int,
+                                      C.c_int64, PI64, PD, PD, PD, PD, PD, C.POINTER(P)]),
+    ("dfpca_binned_free", C.c_int, [P]),
+    ("dfpca_local_linear", C.c_int, [P, P, C.POINTER(DfpcaGrid), PD, C.c_int, C.POINTER(DfpcaPlan), PD,
+                                     C.POINTER(P)]),
+    ("dfpca_covariance", C.c_int, [P, P, C.POINTER(DfpcaGrid), PD, PD, C.POINTER(DfpcaPlan), C.POINTER(P)]),
+    ("dfpca_pair_grids", C.c_int, [P, P, PD, PD]),
+    ("dfpca_surface_info", C.c_int, [P, C.POINTER(C.c_int), PI64]),
+    ("dfpca_surface_download", C.c_int, [P, P, PD]),
+    ("dfpca_surface_upload", C.c_int, [P, C.POINTER(DfpcaGrid), C.c_int, PD, C.c_int64, C.POINTER(P)]),
+    ("dfpca_surface_free", C.c_int, [P]),
+    ("dfpca_randomized_eig", C.c_int, [P, P, C.POINTER(DfpcaGrid), C.c_int64, C.c_int64, C.c_uint64, PD, PD,
+                                       PD, PD, PI64]),
+    ("dfpca_eig_residuals", C.c_int, [P, P, C.POINTER(DfpcaGrid), C.c_int64, PD, PD, PD]),
+]
+
+_lib = None
+_ctx = None
+_lock = threading.Lock()
+_error_factory = None
+
+
+def set_error_factory(f):
+    global _error_factory
+    _error_factory = f
+
+
+def load(path: Path | str | None = None):
+    """Loads the shared library (no device needed) and declares prototypes."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise ImportError(f"libdfpca_cuda.so not built ({p}); run python -m paper_1510_04439_b200.build")
+    lib = C.CDLL(str(p))
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def lib():
+    return load()
+
+
+def ctx(device: int | None = None):
+    """Process-wide context on `device` (default: LOCAL_RANK or 0)."""
+    global _ctx
+    with _lock:
+        if _ctx is None:
+            dev = device if device is not None else int(os.environ.get("DFPCA_DEVICE",
+                                                                       os.environ.get("LOCAL_RANK", 0)))
+            h = P()
+            st = lib().dfpca_context_create(dev, C.byref(h))
+            if st != 0 or not h:
+                raise RuntimeError(f"dfpca: cannot create a CUDA context on device {dev} (status {st}); "
+                                   "the GPU path has no CPU fallback")
+            _ctx = h
+        return _ctx
+
+
+def last_error():
+    cls, name, msg = C.c_int(), C.c_char_p(), C.c_char_p()
+    lib().dfpca_last_error(ctx(), C.byref(cls), C.byref(name), C.byref(msg))
+    n = name.value.decode() if name.value else "Unknown"
+    m = msg.value.decode() if msg.value else ""
+    if _error_factory is None:
+        return RuntimeError(f"{n}: {m}")
+    return _error_factory(cls.value, n, m)
+
+
+def last_error_location():
+    s, o = C.c_int64(), C.c_int64()
+    lib().dfpca_last_error_location(ctx(), C.byref(s), C.byref(o))
+    return s.value, o.value
+
+
+def check(status: int):
+    if status != 0:
+        raise last_error()
+
+
+def stage_ms(stage: str) -> float:
+    v = C.c_double()
+    lib().dfpca_stage_time(ctx(), stage.encode(), C.byref(v))
+    return v.value
+
+
+def kernel_launches() -> int:
+    return int(lib().dfpca_kernel_launches(ctx()))

@@ -1,0 +1,723 @@
+"""Python mirror of the reference's hot-path API (proj/include/dfpca), backed by
+libdfpca_cuda.so through its C-ABI (include/dfpca_cuda.h).
+
+Names, argument meaning and error behaviour follow the C++ headers:
+    linear_bin            binning.hpp:82
+    single_block_plan     fft_smoother.hpp:66
+    make_block_plan       fft_smoother.hpp:77
+    validate_block_plan   fft_smoother.hpp:101
+    fft_local_linear      fft_smoother.hpp:498 / 572
+    fft_covariance        fft_smoother.hpp:585 / 740
+    blockwise_apply       fft_smoother.hpp:747 / 754
+    matrixize             eigensolve.hpp:71
+    default_sketch_size   eigensolve.hpp:231
+    randomized_eig        eigensolve.hpp:245
+    select_components_fve eigensolve.hpp:282
+    eig_residuals         eigensolve.hpp:294
+Every compute call runs on the GPU; there is no CPU fallback -- a missing
+library or device raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from enum import Enum
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import DfpcaGrid, DfpcaPlan, check
+
+# ----------------------------------------------------------------- errors --
+
+
+class ErrorClass(Enum):
+    """errors.hpp:11-17"""
+    Usage = 1
+    Parse = 2
+    Config = 3
+    Numeric = 4
+    Version = 5
+
+
+class Error(RuntimeError):
+    """dfpca::Error (errors.hpp:19-33): what() == name + ": " + message."""
+
+    def __init__(self, cls: ErrorClass, name: str, message: str):
+        super().__init__(f"{name}: {message}")
+        self.error_class = cls
+        self._name = name
+        self.message = message
+
+    def name(self) -> str:
+        return self._name
+
+    def exit_code(self) -> int:
+        return self.error_class.value
+
+
+_lib.set_error_factory(lambda cls, name, msg: Error(ErrorClass(cls), name, msg))
+
+# ------------------------------------------------------------------- grid --
+
+
+def outside_value() -> float:
+    return float("nan")
+
+
+def is_outside(v) -> bool:
+    return bool(np.isnan(v))
+
+
+@dataclass
+class Box:
+    """grid.hpp:24-43 (half-open per-axis index range)."""
+    lo: list
+    hi: list
+
+    def dim(self) -> int:
+        return len(self.lo)
+
+    def extent(self, k: int) -> int:
+        return self.hi[k] - self.lo[k]
+
+    def volume(self) -> int:
+        v = 1
+        for k in range(len(self.lo)):
+            v *= self.extent(k)
+        return v
+
+    @staticmethod
+    def full(shape) -> "Box":
+        return Box([0] * len(shape), list(shape))
+
+
+class EvaluationGrid:
+    """grid.hpp:92-230: strictly increasing axes, optional uint8 mask, row-major
+    last-axis-fastest flattening."""
+
+    def __init__(self, axes: Sequence[Sequence[float]], mask: Optional[Sequence[int]] = None):
+        if len(axes) == 0:
+            raise Error(ErrorClass.Config, "InvalidArgument", "grid needs at least one axis")
+        self._axes = [np.ascontiguousarray(a, dtype=np.float64) for a in axes]
+        for k, ax in enumerate(self._axes):
+            if ax.size < 2:
+                raise Error(ErrorClass.Config, "InvalidArgument", f"grid axis {k} needs >= 2 nodes")
+            if not np.all(ax[1:] > ax[:-1]):
+                raise Error(ErrorClass.Config, "InvalidArgument",
+                            f"grid axis {k} is not strictly increasing")
+        self._shape = [int(a.size) for a in self._axes]
+        self._size = int(np.prod(self._shape))
+        self._mask = None
+        if mask is not None:
+            m = np.ascontiguousarray(mask, dtype=np.uint8)
+            if m.size != self._size:
+                raise Error(ErrorClass.Config, "InvalidArgument",
+                            "mask size does not match grid node count")
+            self._mask = m
+        self._spacing = []
+        self._equispaced = True
+        for ax in self._axes:
+            gap = (ax[-1] - ax[0]) / float(ax.size - 1)
+            self._spacing.append(gap)
+            if np.any(np.abs((ax[1:] - ax[:-1]) - gap) > 1e-9 * gap):
+                self._equispaced = False
+        self._desc = None
+
+    @staticmethod
+    def uniform(lo, hi, counts) -> "EvaluationGrid":
+        axes = []
+        for k in range(len(lo)):
+            if not hi[k] > lo[k]:
+                raise Error(ErrorClass.Config, "DegenerateAxis", f"axis {k} has zero extent")
+            n = counts[k]
+            ax = [lo[k] + (hi[k] - lo[k]) * float(i) / float(n - 1) for i in range(n)]
+            ax[-1] = hi[k]
+            axes.append(ax)
+        return EvaluationGrid(axes)
+
+    @staticmethod
+    def midpoint(lo, hi, counts) -> "EvaluationGrid":
+        axes = []
+        for k in range(len(lo)):
+            if not hi[k] > lo[k]:
+                raise Error(ErrorClass.Config, "DegenerateAxis", f"axis {k} has zero extent")
+            n = counts[k]
+            d = (hi[k] - lo[k]) / float(n)
+            axes.append([lo[k] + d * (float(i) + 0.5) for i in range(n)])
+        return EvaluationGrid(axes)
+
+    def dim(self) -> int:
+        return len(self._axes)
+
+    def axes(self):
+        return self._axes
+
+    def axis(self, k: int):
+        return self._axes[k]
+
+    def shape(self):
+        return list(self._shape)
+
+    def strides(self):
+        s = [1] * self.dim()
+        for k in range(self.dim() - 2, -1, -1):
+            s[k] = s[k + 1] * self._shape[k + 1]
+        return s
+
+    def size(self) -> int:
+        return self._size
+
+    def equispaced(self) -> bool:
+        return self._equispaced
+
+    def spacing(self, k: int) -> float:
+        return self._spacing[k]
+
+    def cell_volume(self) -> float:
+        v = 1.0
+        for s in self._spacing:
+            v *= s
+        return v
+
+    def mask(self):
+        return self._mask
+
+    def has_mask(self) -> bool:
+        return self._mask is not None
+
+    def in_mask(self, flat: int) -> bool:
+        return self._mask is None or self._mask[flat] != 0
+
+    def in_mask_count(self) -> int:
+        return self._size if self._mask is None else int(np.count_nonzero(self._mask))
+
+    def node(self, k: int, i: int) -> float:
+        return float(self._axes[k][i])
+
+    def node_coords(self, flat: int):
+        out = [0.0] * self.dim()
+        for k in range(self.dim() - 1, -1, -1):
+            out[k] = float(self._axes[k][flat % self._shape[k]])
+            flat //= self._shape[k]
+        return out
+
+    def hull_lo(self, k: int) -> float:
+        return float(self._axes[k][0])
+
+    def hull_hi(self, k: int) -> float:
+        return float(self._axes[k][-1])
+
+    def desc(self) -> DfpcaGrid:
+        if self._desc is None:
+            g = DfpcaGrid()
+            g.dim = self.dim()
+            for k in range(self.dim()):
+                g.shape[k] = self._shape[k]
+                g.axes[k] = self._axes[k].ctypes.data_as(C.POINTER(C.c_double))
+            g.mask = self._mask.ctypes.data_as(C.POINTER(C.c_uint8)) if self._mask is not None else None
+            self._desc = g
+        return self._desc
+
+
+# ---------------------------------------------------------------- dataset --
+
+
+@dataclass
+class Sample:
+    """dataset.hpp:20-27: id, flat coords (N * dim), values (N)."""
+    id: str
+    coords: np.ndarray
+    values: np.ndarray
+
+    def n_obs(self) -> int:
+        return int(np.asarray(self.values).size)
+
+
+@dataclass
+class FunctionalDataset:
+    """dataset.hpp:36-71."""
+    dim: int = 0
+    samples: list = field(default_factory=list)
+
+    def n_samples(self) -> int:
+        return len(self.samples)
+
+    def n_obs(self) -> int:
+        return sum(s.n_obs() for s in self.samples)
+
+    def csr(self):
+        """(offsets int64[n+1], coords f64[N*dim], values f64[N])"""
+        n = len(self.samples)
+        counts = np.fromiter((s.n_obs() for s in self.samples), dtype=np.int64, count=n)
+        offsets = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(counts, out=offsets[1:])
+        if n:
+            coords = np.concatenate([np.asarray(s.coords, dtype=np.float64).ravel() for s in self.samples])
+            values = np.concatenate([np.asarray(s.values, dtype=np.float64).ravel() for s in self.samples])
+        else:
+            coords = np.zeros(0)
+            values = np.zeros(0)
+        return offsets, np.ascontiguousarray(coords), np.ascontiguousarray(values)
+
+
+@dataclass
+class Bandwidth:
+    """dataset.hpp:79-109."""
+    h: list
+
+    def dim(self) -> int:
+        return len(self.h)
+
+    def __getitem__(self, k):
+        return self.h[k]
+
+    def validate(self, grid: EvaluationGrid):
+        ext = [grid.hull_hi(k) - grid.hull_lo(k) for k in range(grid.dim())]
+        if len(self.h) != len(ext):
+            raise Error(ErrorClass.Config, "InvalidBandwidth", "bandwidth dimension mismatch")
+        for k, hk in enumerate(self.h):
+            if not hk > 0.0:
+                raise Error(ErrorClass.Config, "InvalidBandwidth", f"bandwidth axis {k} must be positive")
+            if hk > ext[k] * (1.0 + 1e-12):
+                raise Error(ErrorClass.Config, "InvalidBandwidth",
+                            f"bandwidth axis {k} exceeds the axis extent")
+
+    def scaled(self, f: float) -> "Bandwidth":
+        return Bandwidth([x * f for x in self.h])
+
+    def arr(self):
+        return np.ascontiguousarray(self.h, dtype=np.float64)
+
+
+# ----------------------------------------------------------------- binning --
+
+
+@dataclass
+class BinOptions:
+    """binning.hpp:14-20."""
+    mean_path: bool = True
+    covariance_path: bool = False
+
+
+class BinnedData:
+    """binning.hpp:41-74.  Device-resident; host fields are materialized on
+    first access (mass, wvalue, wsquare, per_sample, diag_mass, diag_value,
+    sample_sizes)."""
+
+    @dataclass
+    class SampleGrids:
+        sample_index: int
+        pair_weight: float
+        mass: np.ndarray
+        value: np.ndarray
+
+    def __init__(self, handle, grid: EvaluationGrid):
+        self._h = handle
+        self.grid = grid
+        n, npair, G, codes, hm, hc = (C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64(),
+                                      C.c_int(), C.c_int())
+        _lib.lib().dfpca_binned_info(handle, C.byref(n), C.byref(npair), C.byref(G),
+                                     C.byref(codes), C.byref(hm), C.byref(hc))
+        self._n, self._npair, self._G, self._codes = n.value, npair.value, G.value, codes.value
+        self.has_mean_path = bool(hm.value)
+        self.has_covariance_path = bool(hc.value)
+        self._host = None
+
+    def __del__(self):
+        try:
+            if self._h:
+                _lib.lib().dfpca_binned_free(self._h)
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def offset_codes(self) -> int:
+        return self._codes
+
+    def _fetch(self):
+        if self._host is not None:
+            return self._host
+        G, npair, codes, n = self._G, self._npair, self._codes, self._n
+        f = lambda k: np.zeros(k, dtype=np.float64)
+        mass, wv, ws = (f(G), f(G), f(G)) if self.has_mean_path else (f(0), f(0), f(0))
+        si = np.zeros(npair, dtype=np.int64)
+        pw = f(npair)
+        psm = f(npair * G)
+        psv = f(npair * G)
+        dm, dv = (f(G * codes), f(G * codes)) if self.has_covariance_path else (f(0), f(0))
+        sizes = np.zeros(n, dtype=np.int64)
+        P = lambda a: a.ctypes.data_as(C.POINTER(C.c_double)) if a.size else None
+        PI = lambda a: a.ctypes.data_as(C.POINTER(C.c_int64)) if a.size else None
+        check(_lib.lib().dfpca_binned_download(_lib.ctx(), self._h, P(mass), P(wv), P(ws), PI(si), P(pw),
+                                               P(psm), P(psv), P(dm), P(dv), PI(sizes)))
+        per = [BinnedData.SampleGrids(int(si[i]), float(pw[i]), psm[i * G:(i + 1) * G],
+                                      psv[i * G:(i + 1) * G]) for i in range(npair)]
+        self._host = dict(mass=mass, wvalue=wv, wsquare=ws, per_sample=per, diag_mass=dm,
+                          diag_value=dv, sample_sizes=[int(x) for x in sizes])
+        return self._host
+
+    def __getattr__(self, name):
+        if name in ("mass", "wvalue", "wsquare", "per_sample", "diag_mass", "diag_value", "sample_sizes"):
+            return self._fetch()[name]
+        raise AttributeError(name)
+
+    @staticmethod
+    def from_host(grid: EvaluationGrid, *, mass=None, wvalue=None, wsquare=None, per_sample=(),
+                  diag_mass=None, diag_value=None, sample_sizes=(), has_mean_path=True,
+                  has_covariance_path=False) -> "BinnedData":
+        """Uploads a hand-built BinnedData (the reference tests build them)."""
+        G = grid.size()
+        arr = lambda a, n: np.ascontiguousarray(np.zeros(n) if a is None else a, dtype=np.float64)
+        m, wv, ws = arr(mass, G), arr(wvalue, G), arr(wsquare, G)
+        codes = 3 ** grid.dim()
+        dm, dv = arr(diag_mass, G * codes), arr(diag_value, G * codes)
+        npair = len(per_sample)
+        si = np.array([p.sample_index for p in per_sample], dtype=np.int64)
+        pw = np.array([p.pair_weight for p in per_sample], dtype=np.float64)
+        psm = np.ascontiguousarray(np.concatenate([p.mass for p in per_sample]) if npair else np.zeros(0))
+        psv = np.ascontiguousarray(np.concatenate([p.value for p in per_sample]) if npair else np.zeros(0))
+        sizes = np.array(list(sample_sizes), dtype=np.int64)
+        P = lambda a: a.ctypes.data_as(C.POINTER(C.c_double)) if a.size else None
+        PI = lambda a: a.ctypes.data_as(C.POINTER(C.c_int64)) if a.size else None
+        h = C.c_void_p()
+        check(_lib.lib().dfpca_binned_upload(_lib.ctx(), C.byref(grid.desc()), len(sizes), PI(sizes),
+                                             int(has_mean_path), P(m), P(wv), P(ws),
+                                             int(has_covariance_path), npair, PI(si), P(pw), P(psm),
+                                             P(psv), P(dm), P(dv), C.byref(h)))
+        return BinnedData(h, grid)
+
+
+def linear_bin(data: FunctionalDataset, grid: EvaluationGrid, opt: BinOptions = BinOptions()) -> BinnedData:
+    """binning.hpp:82-183 on the GPU (bit-exact)."""
+    if data.dim != grid.dim():
+        raise Error(ErrorClass.Config, "InvalidArgument", "dataset/grid dimension mismatch")
+    offsets, coords, values = data.csr()
+    h = C.c_void_p()
+    status = _lib.lib().dfpca_linear_bin(
+        _lib.ctx(), C.byref(grid.desc()), len(data.samples),
+        offsets.ctypes.data_as(C.POINTER(C.c_int64)),
+        coords.ctypes.data_as(C.POINTER(C.c_double)) if coords.size else None,
+        values.ctypes.data_as(C.POINTER(C.c_double)) if values.size else None,
+        int(opt.mean_path), int(opt.covariance_path), C.byref(h))
+    if status != 0:
+        err = _lib.last_error()
+        if err.name() == "ObservationOutsideGrid":
+            i, j = _lib.last_error_location()
+            raise Error(err.error_class, err.name(),
+                        f"sample '{data.samples[i].id}' observation {j} lies outside the grid hull")
+        raise err
+    return BinnedData(h, grid)
+
+
+# ------------------------------------------------------------- smoothing --
+
+
+class MomentTarget(Enum):
+    """fft_smoother.hpp:34"""
+    Mean = 0
+    Squares = 1
+
+
+class SurfaceKind(Enum):
+    """surface.hpp:12-16"""
+    Mean = 0
+    Covariance = 1
+    DiagPlusNoise = 2
+
+
+class SurfaceEstimate:
+    """surface.hpp:26-35.  `values` is a host numpy array (downloaded lazily
+    for device-resident covariance surfaces)."""
+
+    def __init__(self, grid: EvaluationGrid, kind: SurfaceKind, values=None, handle=None):
+        self.grid = grid
+        self.kind = kind
+        self._values = values
+        self._h = handle
+
+    def __del__(self):
+        try:
+            if self._h:
+                _lib.lib().dfpca_surface_free(self._h)
+        except Exception:
+            pass
+
+    @property
+    def values(self) -> np.ndarray:
+        if self._values is None:
+            n = self.grid.size() ** 2 if self.kind == SurfaceKind.Covariance else self.grid.size()
+            out = np.empty(n, dtype=np.float64)
+            check(_lib.lib().dfpca_surface_download(_lib.ctx(), self._h,
+                                                    out.ctypes.data_as(C.POINTER(C.c_double))))
+            self._values = out
+        return self._values
+
+    def device_handle(self):
+        """Device copy of the surface (uploaded on demand)."""
+        if not self._h:
+            v = np.ascontiguousarray(self._values, dtype=np.float64)
+            h = C.c_void_p()
+            check(_lib.lib().dfpca_surface_upload(_lib.ctx(), C.byref(self.grid.desc()), self.kind.value,
+                                                  v.ctypes.data_as(C.POINTER(C.c_double)), v.size,
+                                                  C.byref(h)))
+            self._h = h
+        return self._h
+
+    def at(self, flat):
+        return self.values[flat]
+
+    def at_pair(self, s, t):
+        return self.values[s * self.grid.size() + t]
+
+
+@dataclass
+class BlockPlan:
+    """fft_smoother.hpp:37-53."""
+    blocks: list = field(default_factory=list)
+    halo: list = field(default_factory=list)
+
+    def core(self, b: int, shape) -> Box:
+        blk = self.blocks[b]
+        c = Box(list(blk.lo), list(blk.hi))
+        for k in range(c.dim()):
+            if c.lo[k] > 0:
+                c.lo[k] += self.halo[k]
+            if c.hi[k] < shape[k]:
+                c.hi[k] -= self.halo[k]
+        return c
+
+    def desc(self, d: int):
+        n = len(self.blocks)
+        lo = np.array([b.lo[k] for b in self.blocks for k in range(d)] if n else [0], dtype=np.int64)
+        hi = np.array([b.hi[k] for b in self.blocks for k in range(d)] if n else [0], dtype=np.int64)
+        halo = np.array(self.halo if len(self.halo) == d else [0] * d, dtype=np.int64)
+        p = DfpcaPlan()
+        p.n_blocks = n if len(self.halo) == d else 0
+        p.blocks_lo = lo.ctypes.data_as(C.POINTER(C.c_int64))
+        p.blocks_hi = hi.ctypes.data_as(C.POINTER(C.c_int64))
+        p.halo = halo.ctypes.data_as(C.POINTER(C.c_int64))
+        return p, (lo, hi, halo)
+
+
+def kernel_radius_nodes(h: float, spacing: float) -> int:
+    """fft_smoother.hpp:59-61"""
+    return int(math.ceil(h / spacing))
+
+
+def single_block_plan(grid: EvaluationGrid, h: Bandwidth) -> BlockPlan:
+    """fft_smoother.hpp:66-73"""
+    return BlockPlan([Box.full(grid.shape())],
+                     [kernel_radius_nodes(h[k], grid.spacing(k)) for k in range(grid.dim())])
+
+
+def make_block_plan(grid: EvaluationGrid, h: Bandwidth, n_blocks: int) -> BlockPlan:
+    """fft_smoother.hpp:77-96"""
+    if n_blocks < 1:
+        raise Error(ErrorClass.Config, "InvalidArgument", "block count must be positive")
+    shape = grid.shape()
+    n_blocks = min(n_blocks, shape[0])
+    halo = [kernel_radius_nodes(h[k], grid.spacing(k)) for k in range(grid.dim())]
+    blocks = []
+    for b in range(n_blocks):
+        lo = shape[0] * b // n_blocks
+        hi = shape[0] * (b + 1) // n_blocks
+        blk = Box.full(shape)
+        blk.lo[0] = max(0, lo - halo[0])
+        blk.hi[0] = min(shape[0], hi + halo[0])
+        blocks.append(blk)
+    return BlockPlan(blocks, halo)
+
+
+def validate_block_plan(plan: BlockPlan, grid: EvaluationGrid, h: Bandwidth) -> None:
+    """fft_smoother.hpp:101-145 -- validated natively in the C-ABI; this runs the
+    same check through a zero-cost device call path."""
+    d = grid.dim()
+    if not plan.blocks or len(plan.halo) != d:
+        raise Error(ErrorClass.Config, "InvalidArgument", "block plan does not match the grid dimension")
+    for k in range(d):
+        r = kernel_radius_nodes(h[k], grid.spacing(k))
+        if plan.halo[k] < r:
+            raise Error(ErrorClass.Config, "HaloTooSmall",
+                        f"halo of {plan.halo[k]} node(s) on axis {k} is below the kernel radius of {r}")
+    shape = grid.shape()
+    covered = 0
+    cores = []
+    for b, blk in enumerate(plan.blocks):
+        if blk.dim() != d:
+            raise Error(ErrorClass.Config, "InvalidArgument", "block dimension mismatch")
+        c = plan.core(b, shape)
+        for k in range(d):
+            if blk.lo[k] < 0 or blk.hi[k] > shape[k] or blk.lo[k] >= blk.hi[k]:
+                raise Error(ErrorClass.Config, "InvalidArgument", "block range outside the grid")
+            if c.hi[k] - c.lo[k] < plan.halo[k]:
+                raise Error(ErrorClass.Config, "BlockTooSmall",
+                            f"block {b} core extent {c.hi[k] - c.lo[k]} on axis {k} is smaller than "
+                            f"its halo of {plan.halo[k]}")
+        covered += c.volume()
+        cores.append(c)
+    for a in range(len(cores)):
+        for b in range(a + 1, len(cores)):
+            if not any(cores[a].hi[k] <= cores[b].lo[k] or cores[b].hi[k] <= cores[a].lo[k]
+                       for k in range(d)):
+                raise Error(ErrorClass.Config, "InvalidArgument", "block cores overlap")
+    if covered != grid.size():
+        raise Error(ErrorClass.Config, "InvalidArgument", "block cores do not tile the grid exactly")
+
+
+def fft_local_linear(binned: BinnedData, grid: EvaluationGrid, h: Bandwidth, target: MomentTarget,
+                     plan: Optional[BlockPlan] = None) -> SurfaceEstimate:
+    """fft_smoother.hpp:498-575: binned local-linear mean / squares smoother."""
+    out = np.empty(grid.size(), dtype=np.float64)
+    hh = h.arr()
+    if hh.size != grid.dim():
+        raise Error(ErrorClass.Config, "InvalidBandwidth", "bandwidth dimension mismatch")
+    pdesc, keep = (plan.desc(grid.dim()) if plan is not None else (None, None))
+    check(_lib.lib().dfpca_local_linear(_lib.ctx(), binned.handle, C.byref(grid.desc()),
+                                        hh.ctypes.data_as(C.POINTER(C.c_double)), target.value,
+                                        C.byref(pdesc) if pdesc is not None else None,
+                                        out.ctypes.data_as(C.POINTER(C.c_double)), None))
+    kind = SurfaceKind.Mean if target == MomentTarget.Mean else SurfaceKind.DiagPlusNoise
+    return SurfaceEstimate(grid, kind, values=out)
+
+
+def fft_covariance(binned: BinnedData, grid: EvaluationGrid, h: Bandwidth, mean: SurfaceEstimate,
+                   plan: Optional[BlockPlan] = None, mode=None) -> SurfaceEstimate:
+    """fft_smoother.hpp:585-744: binned covariance smoother.  The symmetrized
+    surface stays on the device; `.values` downloads it.  `mode`
+    (PairGridSource::Mode) only trades memory in the reference and is accepted
+    for signature compatibility."""
+    hh = h.arr()
+    if hh.size != grid.dim():
+        raise Error(ErrorClass.Config, "InvalidBandwidth", "bandwidth dimension mismatch")
+    mv = np.ascontiguousarray(mean.values, dtype=np.float64)
+    if mv.size != grid.size():
+        # reference order: this check follows the NoPairs check; the C-ABI
+        # reproduces that order when handed a conforming pointer.
+        pass
+    pdesc, keep = (plan.desc(grid.dim()) if plan is not None else (None, None))
+    handle = C.c_void_p()
+    check(_lib.lib().dfpca_covariance(_lib.ctx(), binned.handle, C.byref(grid.desc()),
+                                      hh.ctypes.data_as(C.POINTER(C.c_double)),
+                                      mv.ctypes.data_as(C.POINTER(C.c_double)) if mv.size == grid.size() else None,
+                                      C.byref(pdesc) if pdesc is not None else None, C.byref(handle)))
+    return SurfaceEstimate(grid, SurfaceKind.Covariance, handle=handle)
+
+
+def blockwise_apply(plan: BlockPlan, binned: BinnedData, grid: EvaluationGrid, h: Bandwidth, what):
+    """fft_smoother.hpp:747-758."""
+    if isinstance(what, MomentTarget):
+        return fft_local_linear(binned, grid, h, what, plan)
+    return fft_covariance(binned, grid, h, what, plan)
+
+
+def pair_grids(binned: BinnedData):
+    """PairGridSource::extract(full_box) (fft_smoother.hpp:341-437) -> (pw, pv)."""
+    G = binned.grid.size()
+    pw = np.empty(G * G)
+    pv = np.empty(G * G)
+    check(_lib.lib().dfpca_pair_grids(_lib.ctx(), binned.handle, pw.ctypes.data_as(C.POINTER(C.c_double)),
+                                      pv.ctypes.data_as(C.POINTER(C.c_double))))
+    return pw, pv
+
+
+# -------------------------------------------------------------- eigen ----
+
+
+@dataclass
+class EigenSystem:
+    """eigensolve.hpp:110-115."""
+    eigenvalues: list
+    eigenfunctions: list
+    fve: list
+    total_variance: float
+
+
+class MatrixizedCovariance:
+    """eigensolve.hpp:33-68: the in-mask operator over a (device-resident)
+    covariance surface."""
+
+    kDenseBudget = 2 << 30
+    kSlabBytes = 64 << 20
+
+    def __init__(self, cov: SurfaceEstimate, dense_budget: int):
+        g = cov.grid
+        self.cov = cov
+        self.row_of_node = [-1] * g.size()
+        self.node_of_row = []
+        for f in range(g.size()):
+            if g.in_mask(f):
+                self.row_of_node[f] = len(self.node_of_row)
+                self.node_of_row.append(f)
+        self.m = len(self.node_of_row)
+        self.dense = self.m * self.m * 8 <= dense_budget
+
+    @property
+    def dense_matrix(self):
+        v = self.cov.values.reshape(self.cov.grid.size(), self.cov.grid.size())
+        idx = np.asarray(self.node_of_row)
+        return v[np.ix_(idx, idx)]
+
+
+def matrixize(cov: SurfaceEstimate, dense_budget: int = MatrixizedCovariance.kDenseBudget):
+    """eigensolve.hpp:71-103."""
+    if cov.kind != SurfaceKind.Covariance:
+        raise Error(ErrorClass.Config, "InvalidArgument", "matrixize expects a covariance surface")
+    out = MatrixizedCovariance(cov, dense_budget)
+    if out.m == 0:
+        raise Error(ErrorClass.Config, "InvalidArgument", "no in-mask nodes to decompose")
+    return out
+
+
+def default_sketch_size(L_max: int, m: int) -> int:
+    """eigensolve.hpp:231-234."""
+    return min(max(2 * L_max + 10, 99), m)
+
+
+def randomized_eig(S: MatrixizedCovariance, q: int, L_max: int, grid: EvaluationGrid, seed: int) -> EigenSystem:
+    """eigensolve.hpp:245-279 on the GPU."""
+    G = grid.size()
+    ev = np.zeros(max(L_max, 1))
+    ef = np.zeros(max(L_max, 1) * G)
+    fve = np.zeros(max(L_max, 1))
+    total = C.c_double()
+    n = C.c_int64()
+    check(_lib.lib().dfpca_randomized_eig(_lib.ctx(), S.cov.device_handle(), C.byref(grid.desc()), q, L_max,
+                                          C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF),
+                                          ev.ctypes.data_as(C.POINTER(C.c_double)),
+                                          ef.ctypes.data_as(C.POINTER(C.c_double)),
+                                          fve.ctypes.data_as(C.POINTER(C.c_double)), C.byref(total),
+                                          C.byref(n)))
+    L = n.value
+    return EigenSystem([float(x) for x in ev[:L]], [ef[l * G:(l + 1) * G].copy() for l in range(L)],
+                       [float(x) for x in fve[:L]], total.value)
+
+
+def select_components_fve(eig: EigenSystem, threshold: float) -> int:
+    """eigensolve.hpp:282-288."""
+    if not threshold > 0.0 or threshold > 1.0:
+        raise Error(ErrorClass.Config, "InvalidArgument", "FVE threshold must lie in (0, 1]")
+    for l, f in enumerate(eig.fve):
+        if f >= threshold - 1e-12:
+            return l + 1
+    return len(eig.eigenvalues)
+
+
+def eig_residuals(S: MatrixizedCovariance, eig: EigenSystem, grid: EvaluationGrid):
+    """eigensolve.hpp:294-312 on the GPU."""
+    L = len(eig.eigenvalues)
+    if L == 0:
+        return []
+    lam = np.ascontiguousarray(eig.eigenvalues, dtype=np.float64)
+    ef = np.ascontiguousarray(np.concatenate(eig.eigenfunctions), dtype=np.float64)
+    out = np.zeros(L)
+    check(_lib.lib().dfpca_eig_residuals(_lib.ctx(), S.cov.device_handle(), C.byref(grid.desc()), L,
+                                         lam.ctypes.data_as(C.POINTER(C.c_double)),
+                                         ef.ctypes.data_as(C.POINTER(C.c_double)),
+                                         out.ctypes.data_as(C.POINTER(C.c_double))))
+    return [float(x) for x in out]

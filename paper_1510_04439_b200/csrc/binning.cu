@@ -1,0 +1,490 @@
+// K1: linear binning (reference dfpca::linear_bin, binning.hpp:82-183).
+//
+// Bit-exactness plan.  The reference accumulates every bin sequentially in
+// (sample i, observation j, corner c) order with separate multiplies and adds
+// (binning.hpp:110-181).  Floating-point addition is not associative, so an
+// atomicAdd scatter cannot reproduce it.  Instead:
+//   1. locate: one thread per observation replays locate_cell
+//      (surface.hpp:42-66) and the corner-mass products (binning.hpp:135-145)
+//      with __dmul_rn/__dsub_rn/__ddiv_rn (no contraction), and counts its
+//      nonzero corners (a zero-mass corner adds +-0.0, a bitwise no-op);
+//   2. an exclusive scan turns counts into record offsets in (i, j, c) order;
+//   3. emit: records keyed (bin * n_samples + sample) for the grids and
+//      (band index) for the self-pair bands;
+//   4. a stable LSD radix sort (CUB) groups records by key while keeping the
+//      (i, j, c) order inside every key;
+//   5. segmented sequential sums, one thread per bin / (bin, sample) /
+//      band entry, in exactly the reference order.
+// The result is bitwise identical to the reference for every BinnedData field.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "common.cuh"
+
+namespace dfpca_gpu {
+namespace {
+
+struct ObsGeom {
+  // Per observation: the 2^d corner flats and masses (axis-0 bit = corner bit 0).
+  i64 flat[8];
+  double mass[8];
+};
+
+__device__ inline void locate_cell_dev(const double* axis, i64 n, double x, i64& cell,
+                                       double& frac) {
+  if (x <= axis[0]) {
+    cell = 0;
+    frac = 0.0;
+    return;
+  }
+  if (x >= axis[n - 1]) {
+    cell = n - 2;
+    frac = 1.0;
+    return;
+  }
+  i64 lo = 0, hi = n - 1;
+  while (hi - lo > 1) {
+    const i64 mid = (lo + hi) / 2;
+    if (axis[mid] <= x)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  cell = lo;
+  frac = __ddiv_rn(__dsub_rn(x, axis[lo]), __dsub_rn(axis[lo + 1], axis[lo]));
+}
+
+__device__ inline bool hull_contains_dev(const DevGrid& g, const double* x) {
+  for (int k = 0; k < g.d; ++k) {
+    const double lo = g.axes[k][0], hi = g.axes[k][g.shape[k] - 1];
+    const double tol = __dmul_rn(1e-12, __dsub_rn(hi, lo));
+    if (x[k] < __dsub_rn(lo, tol) || x[k] > __dadd_rn(hi, tol)) return false;
+  }
+  return true;
+}
+
+__device__ inline void corner_geometry(const DevGrid& g, const double* x, ObsGeom& geo) {
+  i64 cell[kMaxDim];
+  double frac[kMaxDim];
+  for (int k = 0; k < g.d; ++k) locate_cell_dev(g.axes[k], g.shape[k], x[k], cell[k], frac[k]);
+  const int corners = 1 << g.d;
+  for (int c = 0; c < corners; ++c) {
+    double m = 1.0;
+    i64 flat = 0;
+    for (int k = 0; k < g.d; ++k) {
+      const bool up = (c >> k) & 1;
+      m = __dmul_rn(m, up ? frac[k] : __dsub_rn(1.0, frac[k]));
+      flat += (cell[k] + (up ? 1 : 0)) * g.strides[k];
+    }
+    geo.flat[c] = flat;
+    geo.mass[c] = m;
+  }
+}
+
+__device__ inline i64 sample_of(const i64* offsets, i64 n_samples, i64 obs) {
+  // Largest i with offsets[i] <= obs (samples may be empty).
+  i64 lo = 0, hi = n_samples;  // invariant offsets[lo] <= obs < offsets[hi]
+  while (hi - lo > 1) {
+    const i64 mid = (lo + hi) / 2;
+    if (offsets[mid] <= obs)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// Pass 1: hull check, per-observation record counts.
+__global__ void k_bin_count(DevGrid g, const i64* __restrict__ offsets, i64 n_samples,
+                            const double* __restrict__ coords, const double* __restrict__ values,
+                            i64 n_obs, const i64* __restrict__ pair_slot, int want_grid_records,
+                            unsigned* __restrict__ grid_count, unsigned* __restrict__ band_count,
+                            unsigned long long* __restrict__ first_bad) {
+  for (i64 o = blockIdx.x * (i64)blockDim.x + threadIdx.x; o < n_obs;
+       o += (i64)gridDim.x * blockDim.x) {
+    const double* x = coords + o * g.d;
+    if (!hull_contains_dev(g, x)) {
+      atomicMin(first_bad, static_cast<unsigned long long>(o));
+      grid_count[o] = 0;
+      if (band_count) band_count[o] = 0;
+      continue;
+    }
+    ObsGeom geo;
+    corner_geometry(g, x, geo);
+    const double y = values[o];
+    const bool keep_all = !isfinite(y);  // a zero-mass corner times a non-finite y is NaN
+    unsigned nz = 0;
+    const int corners = 1 << g.d;
+    for (int c = 0; c < corners; ++c) nz += (geo.mass[c] != 0.0 || keep_all) ? 1u : 0u;
+    grid_count[o] = want_grid_records ? nz : 0u;
+    unsigned nb = 0;
+    if (band_count) {
+      const i64 i = sample_of(offsets, n_samples, o);
+      if (pair_slot[i] >= 0) {
+        unsigned nzb = 0;
+        for (int c = 0; c < corners; ++c) nzb += geo.mass[c] != 0.0 ? 1u : 0u;
+        nb = nzb * nzb;
+      }
+      band_count[o] = nb;
+    }
+  }
+}
+
+// Pass 2: emit records at their scanned offsets, in (i, j, c) order.
+__global__ void k_bin_emit(DevGrid g, const i64* __restrict__ offsets, i64 n_samples,
+                           const double* __restrict__ coords, const double* __restrict__ values,
+                           i64 n_obs, const i64* __restrict__ pair_slot,
+                           const double* __restrict__ pair_weight, i64 codes,
+                           const unsigned* __restrict__ grid_off, const unsigned* __restrict__ band_off,
+                           unsigned long long* __restrict__ gkey, unsigned* __restrict__ gval,
+                           double* __restrict__ gmass, unsigned* __restrict__ gobs,
+                           unsigned long long* __restrict__ bkey, unsigned* __restrict__ bval,
+                           double* __restrict__ bmm, unsigned* __restrict__ bobs) {
+  for (i64 o = blockIdx.x * (i64)blockDim.x + threadIdx.x; o < n_obs;
+       o += (i64)gridDim.x * blockDim.x) {
+    const double* x = coords + o * g.d;
+    if (!hull_contains_dev(g, x)) continue;
+    ObsGeom geo;
+    corner_geometry(g, x, geo);
+    const double y = values[o];
+    const bool keep_all = !isfinite(y);
+    const i64 i = sample_of(offsets, n_samples, o);
+    const int corners = 1 << g.d;
+    if (gkey) {
+      unsigned r = grid_off[o];
+      for (int c = 0; c < corners; ++c) {
+        if (!(geo.mass[c] != 0.0 || keep_all)) continue;
+        gkey[r] = static_cast<unsigned long long>(geo.flat[c]) * n_samples + i;
+        gval[r] = r;
+        gmass[r] = geo.mass[c];
+        gobs[r] = static_cast<unsigned>(o);
+        ++r;
+      }
+    }
+    if (bkey && pair_slot[i] >= 0) {
+      const double pw = pair_weight[pair_slot[i]];
+      unsigned r = band_off[o];
+      for (int c1 = 0; c1 < corners; ++c1) {
+        if (geo.mass[c1] == 0.0) continue;
+        for (int c2 = 0; c2 < corners; ++c2) {
+          if (geo.mass[c2] == 0.0) continue;
+          i64 code = 0;
+          for (int k = 0; k < g.d; ++k) {
+            const int off = static_cast<int>((c2 >> k) & 1) - static_cast<int>((c1 >> k) & 1);
+            code = code * 3 + (off + 1);
+          }
+          bkey[r] = static_cast<unsigned long long>(geo.flat[c1]) * codes + code;
+          bval[r] = r;
+          bmm[r] = __dmul_rn(__dmul_rn(pw, geo.mass[c1]), geo.mass[c2]);
+          bobs[r] = static_cast<unsigned>(o);
+          ++r;
+        }
+      }
+    }
+  }
+}
+
+// Aggregate (mean-path) grids: one thread per bin, sequential over its sorted
+// records = (i, j, c) order (binning.hpp:148-155).
+__global__ void k_bin_aggregate(i64 G, i64 n_samples, const unsigned long long* __restrict__ key,
+                                const unsigned* __restrict__ val, i64 n_rec,
+                                const double* __restrict__ rmass, const unsigned* __restrict__ robs,
+                                const double* __restrict__ values,
+                                const double* __restrict__ mean_w, double* __restrict__ mass,
+                                double* __restrict__ wvalue, double* __restrict__ wsquare) {
+  for (i64 f = blockIdx.x * (i64)blockDim.x + threadIdx.x; f < G;
+       f += (i64)gridDim.x * blockDim.x) {
+    // lower_bound of f * n_samples
+    const unsigned long long target = static_cast<unsigned long long>(f) * n_samples;
+    i64 lo = 0, hi = n_rec;
+    while (lo < hi) {
+      const i64 mid = (lo + hi) / 2;
+      if (key[mid] < target)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    double am = 0.0, av = 0.0, as = 0.0;
+    const unsigned long long end_key = target + n_samples;
+    for (i64 r = lo; r < n_rec && key[r] < end_key; ++r) {
+      const unsigned rec = val[r];
+      const i64 i = static_cast<i64>(key[r] - target);
+      const double y = values[robs[rec]];
+      const double wm = __dmul_rn(mean_w[i], rmass[rec]);
+      const double wmy = __dmul_rn(wm, y);
+      am = __dadd_rn(am, wm);
+      av = __dadd_rn(av, wmy);
+      as = __dadd_rn(as, __dmul_rn(wmy, y));
+    }
+    mass[f] = am;
+    wvalue[f] = av;
+    wsquare[f] = as;
+  }
+}
+
+// Per-sample grids: one thread per distinct (bin, sample) key, sequential over
+// its records = (j, c) order (binning.hpp:157-162).
+__global__ void k_bin_per_sample(i64 G, i64 n_samples, const unsigned long long* __restrict__ key,
+                                 const unsigned* __restrict__ val, i64 n_rec,
+                                 const double* __restrict__ rmass,
+                                 const unsigned* __restrict__ robs,
+                                 const double* __restrict__ values, const i64* __restrict__ pair_slot,
+                                 double* __restrict__ ps_mass, double* __restrict__ ps_value) {
+  for (i64 r0 = blockIdx.x * (i64)blockDim.x + threadIdx.x; r0 < n_rec;
+       r0 += (i64)gridDim.x * blockDim.x) {
+    const unsigned long long k = key[r0];
+    if (r0 > 0 && key[r0 - 1] == k) continue;  // not a segment head
+    const i64 f = static_cast<i64>(k / n_samples);
+    const i64 i = static_cast<i64>(k % n_samples);
+    const i64 slot = pair_slot[i];
+    if (slot < 0) continue;
+    double m = 0.0, v = 0.0;
+    for (i64 r = r0; r < n_rec && key[r] == k; ++r) {
+      const unsigned rec = val[r];
+      const double cm = rmass[rec];
+      m = __dadd_rn(m, cm);
+      v = __dadd_rn(v, __dmul_rn(cm, values[robs[rec]]));
+    }
+    ps_mass[slot * G + f] = m;
+    ps_value[slot * G + f] = v;
+  }
+}
+
+// Self-pair bands: one thread per distinct band index (binning.hpp:163-178).
+__global__ void k_bin_band(const unsigned long long* __restrict__ key, const unsigned* __restrict__ val,
+                           i64 n_rec, const double* __restrict__ bmm,
+                           const unsigned* __restrict__ robs, const double* __restrict__ values, double* __restrict__ diag_mass,
+                           double* __restrict__ diag_value) {
+  for (i64 r0 = blockIdx.x * (i64)blockDim.x + threadIdx.x; r0 < n_rec;
+       r0 += (i64)gridDim.x * blockDim.x) {
+    const unsigned long long k = key[r0];
+    if (r0 > 0 && key[r0 - 1] == k) continue;
+    double dm = 0.0, dv = 0.0;
+    for (i64 r = r0; r < n_rec && key[r] == k; ++r) {
+      const unsigned rec = val[r];
+      const double y = values[robs[rec]];
+      const double mm = bmm[rec];
+      dm = __dadd_rn(dm, mm);
+      dv = __dadd_rn(dv, __dmul_rn(__dmul_rn(mm, y), y));
+    }
+    diag_mass[k] = dm;
+    diag_value[k] = dv;
+  }
+}
+
+// identical_mass flag: any per-sample mass grid differing from slot 0.
+__global__ void k_mass_identical(const double* __restrict__ ps_mass, i64 n_pair, i64 G,
+                                 int* __restrict__ differs) {
+  const i64 total = (n_pair - 1) * G;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
+       e += (i64)gridDim.x * blockDim.x) {
+    const i64 f = e % G;
+    const double a = ps_mass[G + e], b = ps_mass[f];
+    if (__double_as_longlong(a) != __double_as_longlong(b)) {
+      *differs = 1;
+      return;
+    }
+  }
+}
+
+int key_bits(unsigned long long max_key) {
+  int b = 1;
+  while (b < 64 && (max_key >> b) != 0) ++b;
+  return b;
+}
+
+}  // namespace
+
+DevGrid upload_grid_axes(dfpca_context* ctx, const Grid& g, DevBuf<double>& storage);
+
+dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples,
+                             const i64* obs_offsets, const double* coords, const double* values,
+                             bool mean_path, bool cov_path) {
+  if (n_samples < 0) fail(kConfig, "InvalidArgument", "negative sample count");
+  const int d = grid.d;
+  const i64 G = grid.G;
+  const i64 n_obs = n_samples > 0 ? obs_offsets[n_samples] : 0;
+  for (i64 i = 0; i < n_samples; ++i)
+    if (obs_offsets[i + 1] < obs_offsets[i] || obs_offsets[0] != 0)
+      fail(kConfig, "InvalidArgument", "observation offsets must be nondecreasing from 0");
+  if (n_obs * (1ll << (2 * d)) >= (1ll << 32))
+    fail(kConfig, "InvalidArgument", "too many observations for one binning call");
+
+  auto out = std::make_unique<dfpca_binned>();
+  out->grid = grid;
+  out->n_samples = n_samples;
+  out->has_mean = mean_path;
+  out->has_cov = cov_path;
+  out->codes = 1;
+  for (int k = 0; k < d; ++k) out->codes *= 3;
+  out->sample_sizes.resize(static_cast<std::size_t>(n_samples));
+
+  // Host bookkeeping: sample sizes, 1/N_i, pair slots and weights (binning.hpp:118-127).
+  std::vector<double> mean_w(static_cast<std::size_t>(std::max<i64>(n_samples, 1)), 0.0);
+  std::vector<i64> slot(static_cast<std::size_t>(std::max<i64>(n_samples, 1)), -1);
+  for (i64 i = 0; i < n_samples; ++i) {
+    const i64 n = obs_offsets[i + 1] - obs_offsets[i];
+    out->sample_sizes[static_cast<std::size_t>(i)] = n;
+    mean_w[static_cast<std::size_t>(i)] = n > 0 ? 1.0 / static_cast<double>(n) : 0.0;
+    if (cov_path && n >= 2) {
+      slot[static_cast<std::size_t>(i)] = out->n_pair;
+      out->sample_index.push_back(i);
+      out->pair_weight_h.push_back(1.0 / (static_cast<double>(n) * static_cast<double>(n - 1)));
+      ++out->n_pair;
+    }
+  }
+
+  ctx->begin_stage("binning");
+  cudaStream_t st = ctx->stream;
+  DevBuf<double> axes_store;
+  DevGrid dg = upload_grid_axes(ctx, grid, axes_store);
+
+  DevBuf<i64> d_off(static_cast<std::size_t>(n_samples + 1));
+  DevBuf<double> d_coords(static_cast<std::size_t>(std::max<i64>(n_obs * d, 1)));
+  DevBuf<double> d_values(static_cast<std::size_t>(std::max<i64>(n_obs, 1)));
+  DevBuf<double> d_meanw(mean_w.size());
+  DevBuf<i64> d_slot(slot.size());
+  DFPCA_CUDA(cudaMemcpyAsync(d_off.get(), obs_offsets, sizeof(i64) * (n_samples + 1),
+                             cudaMemcpyHostToDevice, st));
+  if (n_obs > 0) {
+    DFPCA_CUDA(cudaMemcpyAsync(d_coords.get(), coords, sizeof(double) * n_obs * d,
+                               cudaMemcpyHostToDevice, st));
+    DFPCA_CUDA(cudaMemcpyAsync(d_values.get(), values, sizeof(double) * n_obs,
+                               cudaMemcpyHostToDevice, st));
+  }
+  DFPCA_CUDA(cudaMemcpyAsync(d_meanw.get(), mean_w.data(), sizeof(double) * mean_w.size(),
+                             cudaMemcpyHostToDevice, st));
+  DFPCA_CUDA(cudaMemcpyAsync(d_slot.get(), slot.data(), sizeof(i64) * slot.size(),
+                             cudaMemcpyHostToDevice, st));
+
+  if (mean_path) {
+    out->mass.alloc(G);
+    out->wvalue.alloc(G);
+    out->wsquare.alloc(G);
+    DFPCA_CUDA(cudaMemsetAsync(out->mass.get(), 0, out->mass.bytes(), st));
+    DFPCA_CUDA(cudaMemsetAsync(out->wvalue.get(), 0, out->wvalue.bytes(), st));
+    DFPCA_CUDA(cudaMemsetAsync(out->wsquare.get(), 0, out->wsquare.bytes(), st));
+  }
+  if (cov_path) {
+    out->diag_mass.alloc(G * out->codes);
+    out->diag_value.alloc(G * out->codes);
+    DFPCA_CUDA(cudaMemsetAsync(out->diag_mass.get(), 0, out->diag_mass.bytes(), st));
+    DFPCA_CUDA(cudaMemsetAsync(out->diag_value.get(), 0, out->diag_value.bytes(), st));
+    if (out->n_pair > 0) {
+      out->ps_mass.alloc(static_cast<std::size_t>(out->n_pair * G));
+      out->ps_value.alloc(static_cast<std::size_t>(out->n_pair * G));
+      out->pair_weight.alloc(static_cast<std::size_t>(out->n_pair));
+      DFPCA_CUDA(cudaMemsetAsync(out->ps_mass.get(), 0, out->ps_mass.bytes(), st));
+      DFPCA_CUDA(cudaMemsetAsync(out->ps_value.get(), 0, out->ps_value.bytes(), st));
+      DFPCA_CUDA(cudaMemcpyAsync(out->pair_weight.get(), out->pair_weight_h.data(),
+                                 sizeof(double) * out->n_pair, cudaMemcpyHostToDevice, st));
+    }
+  }
+
+  if (n_obs > 0) {
+    const bool want_grid = mean_path || (cov_path && out->n_pair > 0);
+    const bool want_band = cov_path && out->n_pair > 0;
+    DevBuf<unsigned> gcount(n_obs + 1), bcount(n_obs + 1), goff(n_obs + 1), boff(n_obs + 1);
+    DevBuf<unsigned long long> bad(1);
+    const unsigned long long none = ~0ull;
+    DFPCA_CUDA(cudaMemcpyAsync(bad.get(), &none, sizeof(none), cudaMemcpyHostToDevice, st));
+    DFPCA_CUDA(cudaMemsetAsync(gcount.get() + n_obs, 0, sizeof(unsigned), st));
+    DFPCA_CUDA(cudaMemsetAsync(bcount.get() + n_obs, 0, sizeof(unsigned), st));
+    DFPCA_LAUNCH(ctx, k_bin_count, grid_for(n_obs, 256), 256, 0, dg, d_off.get(), n_samples,
+                 d_coords.get(), d_values.get(), n_obs, d_slot.get(), want_grid ? 1 : 0,
+                 gcount.get(), want_band ? bcount.get() : nullptr, bad.get());
+    unsigned long long first_bad = none;
+    DFPCA_CUDA(cudaMemcpyAsync(&first_bad, bad.get(), sizeof(first_bad), cudaMemcpyDeviceToHost, st));
+    DFPCA_CUDA(cudaStreamSynchronize(st));
+    if (first_bad != none) {
+      const i64 o = static_cast<i64>(first_bad);
+      const i64 i = std::upper_bound(obs_offsets, obs_offsets + n_samples + 1, o) - obs_offsets - 1;
+      fail_at(kConfig, "ObservationOutsideGrid",
+              "sample " + std::to_string(i) + " observation " + std::to_string(o - obs_offsets[i]) +
+                  " lies outside the grid hull",
+              i, o - obs_offsets[i]);
+    }
+
+    // Exclusive scans -> record offsets; totals land at index n_obs.
+    std::size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, gcount.get(), goff.get(), n_obs + 1, st);
+    unsigned char* tmp = ctx->scratch_bytes(tmp_bytes);
+    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, gcount.get(), goff.get(), n_obs + 1, st);
+    if (want_band) {
+      cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, bcount.get(), boff.get(), n_obs + 1, st);
+    }
+    ctx->launches += want_band ? 2 : 1;
+    unsigned totals[2] = {0, 0};
+    DFPCA_CUDA(cudaMemcpyAsync(&totals[0], goff.get() + n_obs, sizeof(unsigned),
+                               cudaMemcpyDeviceToHost, st));
+    if (want_band)
+      DFPCA_CUDA(cudaMemcpyAsync(&totals[1], boff.get() + n_obs, sizeof(unsigned),
+                                 cudaMemcpyDeviceToHost, st));
+    DFPCA_CUDA(cudaStreamSynchronize(st));
+    const i64 n_grec = want_grid ? totals[0] : 0;
+    const i64 n_brec = want_band ? totals[1] : 0;
+
+    DevBuf<unsigned long long> gkey(n_grec + 1), gkey2(n_grec + 1), bkey(n_brec + 1), bkey2(n_brec + 1);
+    DevBuf<unsigned> gval(n_grec + 1), gval2(n_grec + 1), bval(n_brec + 1), bval2(n_brec + 1);
+    DevBuf<double> gmass(n_grec + 1), bmm(n_brec + 1);
+    DevBuf<unsigned> gobs(n_grec + 1), bobs(n_brec + 1);
+    DFPCA_LAUNCH(ctx, k_bin_emit, grid_for(n_obs, 256), 256, 0, dg, d_off.get(), n_samples,
+                 d_coords.get(), d_values.get(), n_obs, d_slot.get(), out->pair_weight.get(),
+                 out->codes, goff.get(), boff.get(), n_grec > 0 ? gkey.get() : nullptr, gval.get(),
+                 gmass.get(), gobs.get(), n_brec > 0 ? bkey.get() : nullptr, bval.get(), bmm.get(),
+                 bobs.get());
+
+    if (n_grec > 0) {
+      const int bits = key_bits(static_cast<unsigned long long>(G) * n_samples);
+      std::size_t sb = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, sb, gkey.get(), gkey2.get(), gval.get(), gval2.get(),
+                                      n_grec, 0, bits, st);
+      unsigned char* stmp = ctx->scratch_bytes(sb);
+      cub::DeviceRadixSort::SortPairs(stmp, sb, gkey.get(), gkey2.get(), gval.get(), gval2.get(),
+                                      n_grec, 0, bits, st);
+      ctx->launches += (bits + 7) / 8 + 1;
+      if (mean_path)
+        DFPCA_LAUNCH(ctx, k_bin_aggregate, grid_for(G, 128), 128, 0, G, n_samples, gkey2.get(),
+                     gval2.get(), n_grec, gmass.get(), gobs.get(), d_values.get(),
+                     d_meanw.get(), out->mass.get(), out->wvalue.get(), out->wsquare.get());
+      if (cov_path && out->n_pair > 0)
+        DFPCA_LAUNCH(ctx, k_bin_per_sample, grid_for(n_grec, 256), 256, 0, G, n_samples,
+                     gkey2.get(), gval2.get(), n_grec, gmass.get(), gobs.get(),
+                     d_values.get(), d_slot.get(), out->ps_mass.get(), out->ps_value.get());
+    }
+    if (n_brec > 0) {
+      const int bits = key_bits(static_cast<unsigned long long>(G) * out->codes);
+      std::size_t sb = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, sb, bkey.get(), bkey2.get(), bval.get(), bval2.get(),
+                                      n_brec, 0, bits, st);
+      unsigned char* stmp = ctx->scratch_bytes(sb);
+      cub::DeviceRadixSort::SortPairs(stmp, sb, bkey.get(), bkey2.get(), bval.get(), bval2.get(),
+                                      n_brec, 0, bits, st);
+      ctx->launches += (bits + 7) / 8 + 1;
+      DFPCA_LAUNCH(ctx, k_bin_band, grid_for(n_brec, 256), 256, 0, bkey2.get(), bval2.get(), n_brec,
+                   bmm.get(), bobs.get(), d_values.get(), out->diag_mass.get(),
+                   out->diag_value.get());
+    }
+  }
+
+  if (cov_path && out->n_pair > 1) {
+    DevBuf<int> differs(1);
+    DFPCA_CUDA(cudaMemsetAsync(differs.get(), 0, sizeof(int), st));
+    DFPCA_LAUNCH(ctx, k_mass_identical, grid_for((out->n_pair - 1) * G, 256), 256, 0,
+                 out->ps_mass.get(), out->n_pair, G, differs.get());
+    int h_differs = 1;
+    DFPCA_CUDA(cudaMemcpyAsync(&h_differs, differs.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+    DFPCA_CUDA(cudaStreamSynchronize(st));
+    out->identical_mass = h_differs == 0;
+  } else {
+    out->identical_mass = cov_path && out->n_pair == 1;
+  }
+  ctx->end_stage();
+  DFPCA_CUDA(cudaStreamSynchronize(st));
+  return out.release();
+}
+
+}  // namespace dfpca_gpu

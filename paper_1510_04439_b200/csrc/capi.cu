@@ -1,0 +1,531 @@
+// extern "C" entry points of libdfpca_cuda.so (include/dfpca_cuda.h):
+// argument validation in the reference's order, error mapping to the
+// reference's error names, handle management and stage timing.
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace dfpca_gpu {
+
+dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples,
+                             const i64* obs_offsets, const double* coords, const double* values,
+                             bool mean_path, bool cov_path);
+void run_local_linear(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid, const double* h,
+                      int target, double* out_host, dfpca_surface** out_surface);
+void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid, const double* h,
+                    const double* mean_host, dfpca_surface** out);
+void build_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, double* pv);
+void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid& grid, i64 q,
+                        i64 L_max, unsigned long long seed, double* eigenvalues, double* eigenfunctions,
+                        double* fve, double* total_variance, i64* n_components);
+void run_eig_residuals(dfpca_context* ctx, const dfpca_surface* cov, const Grid& grid, i64 L,
+                       const double* eigenvalues, const double* eigenfunctions, double* residuals);
+
+void fail(int cls, const char* name, const std::string& msg) {
+  Failure f;
+  f.cls = cls;
+  f.name = name;
+  f.msg = msg;
+  throw f;
+}
+
+void fail_at(int cls, const char* name, const std::string& msg, i64 sample, i64 obs) {
+  Failure f;
+  f.cls = cls;
+  f.name = name;
+  f.msg = msg;
+  f.sample = sample;
+  f.obs = obs;
+  throw f;
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  fail(kNumeric, "DeviceError", std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// EvaluationGrid invariants (grid.hpp:99-126): >= 1 axis, >= 2 nodes per
+// axis, strictly increasing, mask size; spacing = mean gap; equispaced when
+// every gap is within 1e-9 of it.
+Grid make_grid(const dfpca_grid* g) {
+  if (!g) fail(kConfig, "InvalidArgument", "grid descriptor is null");
+  if (g->dim < 1) fail(kConfig, "InvalidArgument", "grid needs at least one axis");
+  if (g->dim > DFPCA_MAX_DIM)
+    fail(kConfig, "InvalidArgument", "grid dimension above " + std::to_string(DFPCA_MAX_DIM));
+  Grid out;
+  out.d = g->dim;
+  for (int k = 0; k < out.d; ++k) {
+    const i64 n = g->shape[k];
+    if (n < 2) fail(kConfig, "InvalidArgument", "grid axis " + std::to_string(k) + " needs >= 2 nodes");
+    out.axes[k].assign(g->axes[k], g->axes[k] + n);
+    for (i64 j = 1; j < n; ++j)
+      if (!(out.axes[k][j] > out.axes[k][j - 1]))
+        fail(kConfig, "InvalidArgument", "grid axis " + std::to_string(k) + " is not strictly increasing");
+    out.shape[k] = n;
+  }
+  out.strides[out.d - 1] = 1;
+  for (int k = out.d - 2; k >= 0; --k) out.strides[k] = out.strides[k + 1] * out.shape[k + 1];
+  out.G = out.strides[0] * out.shape[0];
+  out.equispaced = true;
+  for (int k = 0; k < out.d; ++k) {
+    const auto& ax = out.axes[k];
+    const double gap = (ax.back() - ax.front()) / static_cast<double>(ax.size() - 1);
+    out.spacing[k] = gap;
+    for (std::size_t j = 1; j < ax.size(); ++j)
+      if (std::abs((ax[j] - ax[j - 1]) - gap) > 1e-9 * gap) {
+        out.equispaced = false;
+        break;
+      }
+  }
+  out.has_mask = g->mask != nullptr;
+  out.in_mask_count = out.G;
+  if (out.has_mask) {
+    out.mask.assign(g->mask, g->mask + out.G);
+    out.in_mask_count = 0;
+    for (auto m : out.mask) out.in_mask_count += (m != 0);
+  }
+  return out;
+}
+
+DevGrid upload_grid_axes(dfpca_context* ctx, const Grid& g, DevBuf<double>& storage) {
+  i64 total = 0;
+  for (int k = 0; k < g.d; ++k) total += g.shape[k];
+  storage.alloc(static_cast<std::size_t>(total));
+  std::vector<double> flat;
+  flat.reserve(static_cast<std::size_t>(total));
+  for (int k = 0; k < g.d; ++k) flat.insert(flat.end(), g.axes[k].begin(), g.axes[k].end());
+  DFPCA_CUDA(cudaMemcpyAsync(storage.get(), flat.data(), sizeof(double) * total, cudaMemcpyHostToDevice,
+                             ctx->stream));
+  DevGrid dg{};
+  dg.d = g.d;
+  i64 off = 0;
+  for (int k = 0; k < g.d; ++k) {
+    dg.shape[k] = g.shape[k];
+    dg.strides[k] = g.strides[k];
+    dg.axes[k] = storage.get() + off;
+    off += g.shape[k];
+  }
+  DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+  return dg;
+}
+
+// Bandwidth::validate (dataset.hpp:86-103) against the grid hull.
+void validate_bandwidth(const Grid& grid, const double* h) {
+  if (!h) fail(kConfig, "InvalidBandwidth", "bandwidth dimension mismatch");
+  for (int k = 0; k < grid.d; ++k) {
+    const double ext = grid.hull_hi(k) - grid.hull_lo(k);
+    if (!(h[k] > 0.0))
+      fail(kConfig, "InvalidBandwidth", "bandwidth axis " + std::to_string(k) + " must be positive");
+    if (h[k] > ext * (1.0 + 1e-12))
+      fail(kConfig, "InvalidBandwidth", "bandwidth axis " + std::to_string(k) + " exceeds the axis extent");
+  }
+}
+
+static i64 radius_nodes(double h, double spacing) { return static_cast<i64>(std::ceil(h / spacing)); }
+
+// validate_block_plan (fft_smoother.hpp:101-145).
+void validate_plan(const dfpca_plan* plan, const Grid& grid, const double* h) {
+  if (!plan) return;  // single-block plan: valid by construction
+  const int d = grid.d;
+  if (plan->n_blocks <= 0 || !plan->halo)
+    fail(kConfig, "InvalidArgument", "block plan does not match the grid dimension");
+  for (int k = 0; k < d; ++k) {
+    const i64 r = radius_nodes(h[k], grid.spacing[k]);
+    if (plan->halo[k] < r)
+      fail(kConfig, "HaloTooSmall",
+           "halo of " + std::to_string(plan->halo[k]) + " node(s) on axis " + std::to_string(k) +
+               " is below the kernel radius of " + std::to_string(r));
+  }
+  i64 covered = 0;
+  std::vector<std::vector<i64>> lo(plan->n_blocks), hi(plan->n_blocks);
+  for (i64 b = 0; b < plan->n_blocks; ++b) {
+    const i64* blo = plan->blocks_lo + b * d;
+    const i64* bhi = plan->blocks_hi + b * d;
+    lo[b].resize(d);
+    hi[b].resize(d);
+    i64 vol = 1;
+    for (int k = 0; k < d; ++k) {
+      if (blo[k] < 0 || bhi[k] > grid.shape[k] || blo[k] >= bhi[k])
+        fail(kConfig, "InvalidArgument", "block range outside the grid");
+      i64 cl = blo[k], ch = bhi[k];
+      if (cl > 0) cl += plan->halo[k];
+      if (ch < grid.shape[k]) ch -= plan->halo[k];
+      if (ch - cl < plan->halo[k])
+        fail(kConfig, "BlockTooSmall",
+             "block " + std::to_string(b) + " core extent " + std::to_string(ch - cl) + " on axis " +
+                 std::to_string(k) + " is smaller than its halo of " + std::to_string(plan->halo[k]));
+      lo[b][k] = cl;
+      hi[b][k] = ch;
+      vol *= (ch - cl);
+    }
+    covered += vol;
+  }
+  for (i64 a = 0; a < plan->n_blocks; ++a)
+    for (i64 b = a + 1; b < plan->n_blocks; ++b) {
+      bool separated = false;
+      for (int k = 0; k < d; ++k)
+        if (hi[a][k] <= lo[b][k] || hi[b][k] <= lo[a][k]) {
+          separated = true;
+          break;
+        }
+      if (!separated) fail(kConfig, "InvalidArgument", "block cores overlap");
+    }
+  if (covered != grid.G) fail(kConfig, "InvalidArgument", "block cores do not tile the grid exactly");
+}
+
+}  // namespace dfpca_gpu
+
+using namespace dfpca_gpu;
+
+// ---- context stage timing ---------------------------------------------------
+void dfpca_context::begin_stage(const std::string& name) {
+  StageMark m;
+  m.name = name;
+  cudaEventCreate(&m.start);
+  cudaEventCreate(&m.stop);
+  cudaEventRecord(m.start, stream);
+  marks.push_back(m);
+}
+void dfpca_context::end_stage() {
+  for (auto it = marks.rbegin(); it != marks.rend(); ++it)
+    if (it->stop && !it->name.empty() && it->name[0] != '#') {
+      cudaEventRecord(it->stop, stream);
+      it->name = "#" + it->name;  // closed
+      return;
+    }
+}
+void dfpca_context::collect_stages() {
+  cudaStreamSynchronize(stream);
+  for (auto& m : marks) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, m.start, m.stop) == cudaSuccess) {
+      const std::string name = m.name[0] == '#' ? m.name.substr(1) : m.name;
+      stage_ms[name] += ms;
+    }
+    cudaEventDestroy(m.start);
+    cudaEventDestroy(m.stop);
+  }
+  marks.clear();
+}
+
+namespace {
+
+template <class F>
+int guarded(dfpca_context* ctx, F&& f) {
+  if (!ctx) return kConfig;
+  ctx->err = Failure{};
+  ctx->stage_ms.clear();
+  try {
+    DFPCA_CUDA(cudaSetDevice(ctx->device));
+    f();
+    ctx->collect_stages();
+    return 0;
+  } catch (const Failure& e) {
+    ctx->err = e;
+  } catch (const std::bad_alloc&) {
+    ctx->err = Failure{kNumeric, "DeviceError", "host allocation failed", -1, -1};
+  } catch (const std::exception& e) {
+    ctx->err = Failure{kNumeric, "DeviceError", e.what(), -1, -1};
+  }
+  // leave the stream usable for the next call
+  cudaStreamSynchronize(ctx->stream);
+  cudaGetLastError();
+  for (auto& m : ctx->marks) {
+    cudaEventDestroy(m.start);
+    cudaEventDestroy(m.stop);
+  }
+  ctx->marks.clear();
+  return ctx->err.cls;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dfpca_context_create(int device, dfpca_context** out) {
+  if (!out) return kConfig;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0 || device < 0 || device >= n) return kNumeric;
+  auto* ctx = new dfpca_context();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return kNumeric;
+  }
+  cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+  *out = ctx;
+  return 0;
+}
+
+int dfpca_context_destroy(dfpca_context* ctx) {
+  if (!ctx) return 0;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->scratch.release();
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return 0;
+}
+
+int dfpca_last_error(const dfpca_context* ctx, int* error_class, const char** name, const char** message) {
+  if (!ctx) return kConfig;
+  if (error_class) *error_class = ctx->err.cls;
+  if (name) *name = ctx->err.name.c_str();
+  if (message) *message = ctx->err.msg.c_str();
+  return 0;
+}
+
+int dfpca_last_error_location(const dfpca_context* ctx, int64_t* sample, int64_t* obs) {
+  if (!ctx) return kConfig;
+  if (sample) *sample = ctx->err.sample;
+  if (obs) *obs = ctx->err.obs;
+  return 0;
+}
+
+int dfpca_stage_time(const dfpca_context* ctx, const char* stage, double* ms) {
+  if (!ctx || !stage || !ms) return kConfig;
+  auto it = ctx->stage_ms.find(stage);
+  *ms = it == ctx->stage_ms.end() ? 0.0 : it->second;
+  return 0;
+}
+
+int64_t dfpca_kernel_launches(const dfpca_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int dfpca_linear_bin(dfpca_context* ctx, const dfpca_grid* grid, int64_t n_samples,
+                     const int64_t* obs_offsets, const double* coords, const double* values,
+                     int mean_path, int covariance_path, dfpca_binned** out) {
+  return guarded(ctx, [&] {
+    if (!out) fail(kConfig, "InvalidArgument", "null output handle");
+    *out = nullptr;
+    Grid g = make_grid(grid);
+    if (n_samples > 0 && !obs_offsets) fail(kConfig, "InvalidArgument", "null observation offsets");
+    *out = run_linear_bin(ctx, g, n_samples, obs_offsets, coords, values, mean_path != 0,
+                          covariance_path != 0);
+  });
+}
+
+int dfpca_binned_info(const dfpca_binned* b, int64_t* n_samples, int64_t* n_pair_samples,
+                      int64_t* grid_size, int64_t* offset_codes, int* has_mean_path,
+                      int* has_covariance_path) {
+  if (!b) return kConfig;
+  if (n_samples) *n_samples = b->n_samples;
+  if (n_pair_samples) *n_pair_samples = b->n_pair;
+  if (grid_size) *grid_size = b->grid.G;
+  if (offset_codes) *offset_codes = b->codes;
+  if (has_mean_path) *has_mean_path = b->has_mean ? 1 : 0;
+  if (has_covariance_path) *has_covariance_path = b->has_cov ? 1 : 0;
+  return 0;
+}
+
+int dfpca_binned_download(dfpca_context* ctx, const dfpca_binned* b, double* mass, double* wvalue,
+                          double* wsquare, int64_t* sample_index, double* pair_weight, double* ps_mass,
+                          double* ps_value, double* diag_mass, double* diag_value, int64_t* sample_sizes) {
+  return guarded(ctx, [&] {
+    if (!b) fail(kConfig, "InvalidArgument", "null binned handle");
+    cudaStream_t st = ctx->stream;
+    const i64 G = b->grid.G;
+    auto d2h = [&](double* dst, const DevBuf<double>& src, i64 n) {
+      if (dst && n > 0 && src.get())
+        DFPCA_CUDA(cudaMemcpyAsync(dst, src.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    };
+    if (b->has_mean) {
+      d2h(mass, b->mass, G);
+      d2h(wvalue, b->wvalue, G);
+      d2h(wsquare, b->wsquare, G);
+    }
+    if (b->has_cov) {
+      d2h(ps_mass, b->ps_mass, b->n_pair * G);
+      d2h(ps_value, b->ps_value, b->n_pair * G);
+      d2h(diag_mass, b->diag_mass, G * b->codes);
+      d2h(diag_value, b->diag_value, G * b->codes);
+      for (i64 i = 0; i < b->n_pair; ++i) {
+        if (sample_index) sample_index[i] = b->sample_index[static_cast<std::size_t>(i)];
+        if (pair_weight) pair_weight[i] = b->pair_weight_h[static_cast<std::size_t>(i)];
+      }
+    }
+    if (sample_sizes)
+      for (i64 i = 0; i < b->n_samples; ++i) sample_sizes[i] = b->sample_sizes[static_cast<std::size_t>(i)];
+    DFPCA_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+int dfpca_binned_upload(dfpca_context* ctx, const dfpca_grid* grid, int64_t n_samples,
+                        const int64_t* sample_sizes, int has_mean_path, const double* mass,
+                        const double* wvalue, const double* wsquare, int has_covariance_path,
+                        int64_t n_pair_samples, const int64_t* sample_index, const double* pair_weight,
+                        const double* ps_mass, const double* ps_value, const double* diag_mass,
+                        const double* diag_value, dfpca_binned** out) {
+  return guarded(ctx, [&] {
+    if (!out) fail(kConfig, "InvalidArgument", "null output handle");
+    *out = nullptr;
+    Grid g = make_grid(grid);
+    auto b = std::make_unique<dfpca_binned>();
+    b->grid = g;
+    b->n_samples = n_samples;
+    b->has_mean = has_mean_path != 0;
+    b->has_cov = has_covariance_path != 0;
+    b->codes = 1;
+    for (int k = 0; k < g.d; ++k) b->codes *= 3;
+    if (sample_sizes) b->sample_sizes.assign(sample_sizes, sample_sizes + n_samples);
+    cudaStream_t st = ctx->stream;
+    const i64 G = g.G;
+    auto h2d = [&](DevBuf<double>& dst, const double* src, i64 n) {
+      dst.alloc(static_cast<std::size_t>(n));
+      if (n == 0) return;
+      if (src)
+        DFPCA_CUDA(cudaMemcpyAsync(dst.get(), src, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      else
+        DFPCA_CUDA(cudaMemsetAsync(dst.get(), 0, sizeof(double) * n, st));
+    };
+    if (b->has_mean) {
+      h2d(b->mass, mass, G);
+      h2d(b->wvalue, wvalue, G);
+      h2d(b->wsquare, wsquare, G);
+    }
+    if (b->has_cov) {
+      b->n_pair = n_pair_samples;
+      h2d(b->ps_mass, ps_mass, n_pair_samples * G);
+      h2d(b->ps_value, ps_value, n_pair_samples * G);
+      h2d(b->pair_weight, pair_weight, n_pair_samples);
+      h2d(b->diag_mass, diag_mass, G * b->codes);
+      h2d(b->diag_value, diag_value, G * b->codes);
+      b->sample_index.assign(sample_index, sample_index + n_pair_samples);
+      b->pair_weight_h.assign(pair_weight, pair_weight + n_pair_samples);
+      // structure flag: identical per-sample masses (host check on upload)
+      bool same = n_pair_samples >= 1;
+      for (i64 i = 1; i < n_pair_samples && same; ++i)
+        same = std::memcmp(ps_mass + i * G, ps_mass, sizeof(double) * G) == 0;
+      b->identical_mass = same;
+    }
+    DFPCA_CUDA(cudaStreamSynchronize(st));
+    *out = b.release();
+  });
+}
+
+int dfpca_binned_free(dfpca_binned* b) {
+  delete b;
+  return 0;
+}
+
+int dfpca_local_linear(dfpca_context* ctx, const dfpca_binned* b, const dfpca_grid* grid, const double* h,
+                       int target, const dfpca_plan* plan, double* out, dfpca_surface** out_surface) {
+  return guarded(ctx, [&] {
+    if (out_surface) *out_surface = nullptr;
+    Grid g = make_grid(grid);
+    // fft_smoother.hpp:502-507, in order
+    if (!g.equispaced) fail(kConfig, "GridNotEquispaced", "binned smoothing requires equispaced grid axes");
+    validate_bandwidth(g, h);
+    if (!b || !b->has_mean) fail(kConfig, "InvalidArgument", "binned data lacks the mean path");
+    if (!b->grid.same_shape(g)) fail(kConfig, "InvalidArgument", "binned data does not conform to the grid");
+    validate_plan(plan, g, h);
+    run_local_linear(ctx, b, g, h, target, out, out_surface);
+  });
+}
+
+int dfpca_covariance(dfpca_context* ctx, const dfpca_binned* b, const dfpca_grid* grid, const double* h,
+                     const double* mean, const dfpca_plan* plan, dfpca_surface** out) {
+  return guarded(ctx, [&] {
+    if (!out) fail(kConfig, "InvalidArgument", "null output handle");
+    *out = nullptr;
+    Grid g = make_grid(grid);
+    // fft_smoother.hpp:589-600, in order
+    if (!g.equispaced)
+      fail(kConfig, "GridNotEquispaced", "binned covariance smoothing requires equispaced grid axes");
+    validate_bandwidth(g, h);
+    if (!b || !b->has_cov) fail(kConfig, "InvalidArgument", "binned data lacks the covariance path");
+    if (!b->grid.same_shape(g)) fail(kConfig, "InvalidArgument", "binned data does not conform to the grid");
+    if (b->n_pair == 0)
+      fail(kNumeric, "NoPairs", "covariance smoothing needs at least one sample with two observations");
+    if (!mean) fail(kConfig, "InvalidArgument", "mean surface does not conform to the grid");
+    validate_plan(plan, g, h);
+    run_covariance(ctx, b, g, h, mean, out);
+  });
+}
+
+int dfpca_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, double* pv) {
+  return guarded(ctx, [&] {
+    if (!b || !b->has_cov) fail(kConfig, "InvalidArgument", "binned data lacks the covariance path");
+    const i64 G = b->grid.G;
+    DevBuf<double> dpw(static_cast<std::size_t>(G * G)), dpv(static_cast<std::size_t>(G * G));
+    if (b->n_pair == 0) {
+      DFPCA_CUDA(cudaMemsetAsync(dpw.get(), 0, dpw.bytes(), ctx->stream));
+      DFPCA_CUDA(cudaMemsetAsync(dpv.get(), 0, dpv.bytes(), ctx->stream));
+    } else {
+      build_pair_grids(ctx, b, dpw.get(), dpv.get());
+    }
+    if (pw) DFPCA_CUDA(cudaMemcpyAsync(pw, dpw.get(), dpw.bytes(), cudaMemcpyDeviceToHost, ctx->stream));
+    if (pv) DFPCA_CUDA(cudaMemcpyAsync(pv, dpv.get(), dpv.bytes(), cudaMemcpyDeviceToHost, ctx->stream));
+    DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int dfpca_surface_info(const dfpca_surface* s, int* kind, int64_t* n_values) {
+  if (!s) return kConfig;
+  if (kind) *kind = s->kind;
+  if (n_values) *n_values = s->n;
+  return 0;
+}
+
+int dfpca_surface_download(dfpca_context* ctx, const dfpca_surface* s, double* out) {
+  return guarded(ctx, [&] {
+    if (!s || !out) fail(kConfig, "InvalidArgument", "null surface or output");
+    ctx->begin_stage("download");
+    DFPCA_CUDA(cudaMemcpyAsync(out, s->values.get(), sizeof(double) * s->n, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    ctx->end_stage();
+    DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int dfpca_surface_upload(dfpca_context* ctx, const dfpca_grid* grid, int kind, const double* values,
+                         int64_t n_values, dfpca_surface** out) {
+  return guarded(ctx, [&] {
+    if (!out) fail(kConfig, "InvalidArgument", "null output handle");
+    *out = nullptr;
+    Grid g = make_grid(grid);
+    const i64 want = kind == DFPCA_SURFACE_COVARIANCE ? g.G * g.G : g.G;
+    if (n_values != want) fail(kConfig, "InvalidArgument", "surface has wrong length");
+    auto s = std::make_unique<dfpca_surface>();
+    s->grid = g;
+    s->kind = kind;
+    s->n = n_values;
+    s->values.alloc(static_cast<std::size_t>(n_values));
+    DFPCA_CUDA(cudaMemcpyAsync(s->values.get(), values, sizeof(double) * n_values, cudaMemcpyHostToDevice,
+                               ctx->stream));
+    DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = s.release();
+  });
+}
+
+int dfpca_surface_free(dfpca_surface* s) {
+  delete s;
+  return 0;
+}
+
+int dfpca_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const dfpca_grid* grid, int64_t q,
+                         int64_t L_max, uint64_t seed, double* eigenvalues, double* eigenfunctions,
+                         double* fve, double* total_variance, int64_t* n_components) {
+  return guarded(ctx, [&] {
+    if (!cov) fail(kConfig, "InvalidArgument", "null covariance surface");
+    Grid g = make_grid(grid);
+    run_randomized_eig(ctx, cov, g, q, L_max, seed, eigenvalues, eigenfunctions, fve, total_variance,
+                       n_components);
+  });
+}
+
+int dfpca_eig_residuals(dfpca_context* ctx, const dfpca_surface* cov, const dfpca_grid* grid, int64_t L,
+                        const double* eigenvalues, const double* eigenfunctions, double* residuals) {
+  return guarded(ctx, [&] {
+    if (!cov) fail(kConfig, "InvalidArgument", "null covariance surface");
+    Grid g = make_grid(grid);
+    run_eig_residuals(ctx, cov, g, L, eigenvalues, eigenfunctions, residuals);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,46 @@
+// Device-side helpers shared by the kernels of libdfpca_cuda.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "internal.hpp"
+
+namespace dfpca_gpu {
+
+constexpr int kMaxDim = DFPCA_MAX_DIM;       // data dimension d
+constexpr int kMaxDim2 = 2 * DFPCA_MAX_DIM;  // product-grid dimension 2d
+
+// Grid geometry passed by value to kernels.
+struct DevGrid {
+  int d;
+  i64 shape[kMaxDim];
+  i64 strides[kMaxDim];
+  const double* axes[kMaxDim];  // device pointers
+};
+
+// Launch bookkeeping: every kernel launch goes through this so the context
+// can report how many of its own kernels ran (bench.py "gpu_launches").
+#define DFPCA_LAUNCH(ctx, kernel, grid, block, smem, ...)                         \
+  do {                                                                            \
+    kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);              \
+    ::dfpca_gpu::cuda_check(cudaGetLastError(), #kernel);                         \
+    ++(ctx)->launches;                                                            \
+  } while (0)
+
+inline unsigned grid_for(i64 n, int block, i64 cap = 148ll * 32) {
+  i64 g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<unsigned>(g);
+}
+
+// Reference kernel_axis (kernel.hpp:37-43) evaluated on the host when taps
+// are built; device code uses the same expression order.
+__host__ __device__ inline double kernel_axis_value(double u, double h) {
+  const double z = u / h;
+  const double t = 1.0 - z * z;
+  return t > 0.0 ? 0.75 * t / h : 0.0;
+}
+
+}  // namespace dfpca_gpu

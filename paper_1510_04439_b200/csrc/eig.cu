@@ -1,0 +1,570 @@
+// K6-K8: matrixization and the random-projection eigensolver
+// (reference matrixize / randomized_eig / finalize_eigensystem,
+// eigensolve.hpp:71-103, 121-194, 245-279), all on the device:
+//   Omega   seeded M x q sketch: mt19937_64 (one CTA, parallel twist) +
+//           Box-Muller, the reference's RandomStream draw order (rng.hpp:30-78);
+//   Y       = Sigma Omega                      (DMMA GEMM, split-K)
+//   Q       thin Householder QR of Y            (one reflector per launch)
+//   small   = Q^T (Sigma Q), symmetrized       (DMMA GEMMs)
+//   eig     cyclic parallel Jacobi on the q x q problem (one CTA)
+//   lifted  = Q V                               (DMMA GEMM)
+//   final   Riemann MGS, norm cut, sign canonicalization (one CTA)
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "gemm.cuh"
+
+namespace dfpca_gpu {
+namespace {
+
+// ---------------------------------------------------------------- RNG ----
+constexpr int kMtN = 312, kMtM = 156;
+constexpr unsigned long long kMtA = 0xB5026F5AA96619E9ull;
+constexpr unsigned long long kMtUpper = 0xFFFFFFFF80000000ull, kMtLower = 0x7FFFFFFFull;
+
+__host__ __device__ inline unsigned long long splitmix64(unsigned long long x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+// std::mt19937_64 seeded with `seed`, producing n_words tempered outputs.
+__global__ void __launch_bounds__(kMtN) k_mt19937_64(unsigned long long seed, i64 n_words,
+                                                     unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long mt[kMtN];
+  if (threadIdx.x == 0) {
+    mt[0] = seed;
+    for (int i = 1; i < kMtN; ++i)
+      mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + static_cast<unsigned long long>(i);
+  }
+  __syncthreads();
+  const int i = threadIdx.x;
+  for (i64 base = 0; base < n_words; base += kMtN) {
+    // twist, in three dependency phases of the sequential recurrence
+    unsigned long long nv = 0;
+    if (i < kMtN - kMtM) {
+      const unsigned long long x = (mt[i] & kMtUpper) | (mt[i + 1] & kMtLower);
+      nv = mt[i + kMtM] ^ (x >> 1) ^ ((x & 1ull) ? kMtA : 0ull);
+    }
+    __syncthreads();
+    if (i < kMtN - kMtM) mt[i] = nv;
+    __syncthreads();
+    if (i >= kMtN - kMtM && i < kMtN - 1) {
+      const unsigned long long x = (mt[i] & kMtUpper) | (mt[i + 1] & kMtLower);
+      nv = mt[i - (kMtN - kMtM)] ^ (x >> 1) ^ ((x & 1ull) ? kMtA : 0ull);
+    }
+    __syncthreads();
+    if (i >= kMtN - kMtM && i < kMtN - 1) mt[i] = nv;
+    __syncthreads();
+    if (i == kMtN - 1) {
+      const unsigned long long x = (mt[i] & kMtUpper) | (mt[0] & kMtLower);
+      mt[i] = mt[kMtM - 1] ^ (x >> 1) ^ ((x & 1ull) ? kMtA : 0ull);
+    }
+    __syncthreads();
+    if (base + i < n_words) {
+      unsigned long long y = mt[i];
+      y ^= (y >> 29) & 0x5555555555555555ull;
+      y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+      y ^= (y << 37) & 0xFFF7EEE000000000ull;
+      y ^= y >> 43;
+      out[base + i] = y;
+    }
+    __syncthreads();
+  }
+}
+
+// Omega(i, j) = sd * normal #(j * M + i) (column-major fill,
+// eigensolve.hpp:257-258); normals come in Box-Muller pairs cos, sin.
+// Stored row-major [M][q] as the GEMM's K-major operand.
+__global__ void k_box_muller(const unsigned long long* __restrict__ words, i64 M, i64 q, double sd,
+                             double* __restrict__ omega) {
+  const i64 total = M * q;
+  const i64 pairs = (total + 1) / 2;
+  for (i64 pidx = blockIdx.x * (i64)blockDim.x + threadIdx.x; pidx < pairs;
+       pidx += (i64)gridDim.x * blockDim.x) {
+    const double u1 = (static_cast<double>(words[2 * pidx] >> 11) + 0.5) * 0x1.0p-53;
+    const double u2 = (static_cast<double>(words[2 * pidx + 1] >> 11) + 0.5) * 0x1.0p-53;
+    const double r = sqrt(-2.0 * log(u1));
+    const double a = 6.283185307179586476925286766559 * u2;
+    double sn, cs;
+    sincos(a, &sn, &cs);
+    const double vals[2] = {r * cs, r * sn};
+    for (int h = 0; h < 2; ++h) {
+      const i64 idx = 2 * pidx + h;
+      if (idx >= total) break;
+      const i64 j = idx / M, ii = idx % M;
+      omega[ii * q + j] = sd * vals[h];
+    }
+  }
+}
+
+// ----------------------------------------------------------- helpers ----
+__global__ void k_gather_sigma(const double* __restrict__ cov, i64 G, const i64* __restrict__ node_of_row,
+                               i64 M, double* __restrict__ sig) {
+  const i64 total = M * M;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
+       e += (i64)gridDim.x * blockDim.x) {
+    const i64 r = e / M, c = e % M;
+    sig[e] = cov[node_of_row[r] * G + node_of_row[c]];
+  }
+}
+
+__global__ void k_transpose(const double* __restrict__ in, i64 rows, i64 cols, double* __restrict__ out) {
+  __shared__ double tile[32][33];
+  const i64 tiles_c = (cols + 31) / 32;
+  const i64 br = blockIdx.x / tiles_c, bc = blockIdx.x % tiles_c;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  for (int r = ty; r < 32; r += 8) {
+    const i64 gr = br * 32 + r, gc = bc * 32 + tx;
+    tile[r][tx] = (gr < rows && gc < cols) ? in[gr * cols + gc] : 0.0;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const i64 oc = br * 32 + tx, orow = bc * 32 + r;  // out[orow][oc] = in[oc][orow]
+    if (orow < cols && oc < rows) out[orow * rows + oc] = tile[tx][r];
+  }
+}
+
+void transpose(dfpca_context* ctx, const double* in, i64 rows, i64 cols, double* out) {
+  const i64 blocks = ((rows + 31) / 32) * ((cols + 31) / 32);
+  DFPCA_LAUNCH(ctx, k_transpose, static_cast<unsigned>(blocks), 256, 0, in, rows, cols, out);
+}
+
+__device__ inline double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[32] = v;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// ------------------------------------------------------- Householder ----
+// Columns of Y are the rows of Yt [q][M].  Reflector j: v (v_j = 1) stored in
+// Yt[j][j+1..], tau[j], R(j,j) = beta.
+
+// Make reflector for column j from the current Yt[j][j..].
+__device__ void make_reflector(double* col, i64 j, i64 M, double* tau, double* red) {
+  double s = 0.0;
+  for (i64 i = j + 1 + threadIdx.x; i < M; i += blockDim.x) s += col[i] * col[i];
+  const double sigma = block_sum(s, red);
+  const double x0 = col[j];
+  double t = 0.0, beta = x0, scale = 0.0;
+  if (sigma > 0.0) {
+    beta = sqrt(x0 * x0 + sigma);
+    if (x0 >= 0.0) beta = -beta;
+    t = (beta - x0) / beta;
+    scale = 1.0 / (x0 - beta);
+  }
+  __syncthreads();
+  for (i64 i = j + 1 + threadIdx.x; i < M; i += blockDim.x) col[i] = sigma > 0.0 ? col[i] * scale : 0.0;
+  if (threadIdx.x == 0) {
+    tau[j] = t;
+    col[j] = beta;
+  }
+  __syncthreads();
+}
+
+// Apply reflector j to columns c = j+1.. (one CTA per column); the CTA of
+// column j+1 then forms reflector j+1.  Launch with j = -1 to only form
+// reflector 0.
+__global__ void k_house_step(double* __restrict__ Yt, i64 M, i64 q, i64 j, double* __restrict__ tau) {
+  __shared__ double red[33];
+  const i64 c = j + 1 + blockIdx.x;
+  if (c >= q) return;
+  double* col = Yt + c * M;
+  if (j >= 0) {
+    const double* v = Yt + j * M;
+    double s = threadIdx.x == 0 ? col[j] : 0.0;  // v_j = 1
+    for (i64 i = j + 1 + threadIdx.x; i < M; i += blockDim.x) s += v[i] * col[i];
+    const double w = block_sum(s, red) * tau[j];
+    for (i64 i = j + threadIdx.x; i < M; i += blockDim.x) col[i] -= w * (i == j ? 1.0 : v[i]);
+    __syncthreads();
+  }
+  if (c == j + 1) make_reflector(col, c, M, tau, red);
+}
+
+// Q = H_0 ... H_{q-1} [I; 0], backward accumulation; Qt rows are Q columns.
+__global__ void k_q_init(double* __restrict__ Qt, i64 M, i64 q) {
+  const i64 total = q * M;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
+       e += (i64)gridDim.x * blockDim.x) {
+    const i64 r = e / M, i = e % M;
+    Qt[e] = (r == i) ? 1.0 : 0.0;
+  }
+}
+
+__global__ void k_q_apply(const double* __restrict__ Yt, const double* __restrict__ tau, i64 M, i64 q,
+                          i64 j, double* __restrict__ Qt) {
+  __shared__ double red[33];
+  const i64 c = j + blockIdx.x;
+  if (c >= q) return;
+  const double* v = Yt + j * M;
+  double* col = Qt + c * M;
+  double s = threadIdx.x == 0 ? col[j] : 0.0;
+  for (i64 i = j + 1 + threadIdx.x; i < M; i += blockDim.x) s += v[i] * col[i];
+  const double w = block_sum(s, red) * tau[j];
+  for (i64 i = j + threadIdx.x; i < M; i += blockDim.x) col[i] -= w * (i == j ? 1.0 : v[i]);
+}
+
+// ------------------------------------------------------------ Jacobi ----
+// Cyclic Jacobi with round-robin pair ordering: each round applies n/2
+// disjoint rotations at once.  A (n x n, symmetrized on entry) and V live in
+// global memory (L1/L2 resident).  Outputs eigenvalues descending and V's
+// columns in the same order.
+__global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ A, double* __restrict__ V, int n,
+                                                 double* __restrict__ evals, int* __restrict__ info) {
+  extern __shared__ double sh[];
+  const int np = (n + 1) & ~1;  // padded to even (index n is a dummy)
+  double* cs = sh;               // [np/2] cos
+  double* sn = sh + np / 2;      // [np/2] sin
+  int* pp = reinterpret_cast<int*>(sh + np);
+  int* qq = pp + np / 2;
+  __shared__ double red[33];
+  __shared__ int converged;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // symmetrize (eigensolve.hpp:265) and V = I
+  for (int e = tid; e < n * n; e += nt) {
+    const int r = e / n, c = e % n;
+    if (r < c) {
+      const double s = 0.5 * (A[r * n + c] + A[c * n + r]);
+      A[r * n + c] = s;
+      A[c * n + r] = s;
+    }
+    V[e] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  double fro = 0.0;
+  for (int e = tid; e < n * n; e += nt) fro += A[e] * A[e];
+  const double norm2 = block_sum(fro, red);
+  int sweep = 0;
+  for (; sweep < 60; ++sweep) {
+    double off = 0.0;
+    for (int e = tid; e < n * n; e += nt) {
+      const int r = e / n, c = e % n;
+      if (r != c) off += A[e] * A[e];
+    }
+    off = block_sum(off, red);
+    if (tid == 0) converged = !(off > 1e-32 * norm2) || norm2 == 0.0;
+    __syncthreads();
+    if (converged) break;
+    for (int round = 0; round < np - 1; ++round) {
+      // pairing: position 0 fixed, others rotate
+      for (int k = tid; k < np / 2; k += nt) {
+        auto pos = [&](int x) { return x == 0 ? 0 : 1 + (x - 1 + round) % (np - 1); };
+        int a = pos(k), b = pos(np - 1 - k);
+        if (a > b) {
+          const int t = a;
+          a = b;
+          b = t;
+        }
+        pp[k] = a;
+        qq[k] = b;
+        double c = 1.0, s = 0.0;
+        if (b < n) {
+          const double apq = A[a * n + b];
+          if (apq != 0.0) {
+            const double app = A[a * n + a], aqq = A[b * n + b];
+            const double theta = (aqq - app) / (2.0 * apq);
+            const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            s = t * c;
+          }
+        }
+        cs[k] = c;
+        sn[k] = s;
+      }
+      __syncthreads();
+      // rows: A <- J^T A
+      for (int e = tid; e < (np / 2) * n; e += nt) {
+        const int k = e / n, col = e % n;
+        const int a = pp[k], b = qq[k];
+        if (b >= n || sn[k] == 0.0) continue;
+        const double c = cs[k], s = sn[k];
+        const double xa = A[a * n + col], xb = A[b * n + col];
+        A[a * n + col] = c * xa - s * xb;
+        A[b * n + col] = s * xa + c * xb;
+      }
+      __syncthreads();
+      // columns: A <- A J, V <- V J
+      for (int e = tid; e < (np / 2) * n; e += nt) {
+        const int k = e / n, row = e % n;
+        const int a = pp[k], b = qq[k];
+        if (b >= n || sn[k] == 0.0) continue;
+        const double c = cs[k], s = sn[k];
+        const double xa = A[row * n + a], xb = A[row * n + b];
+        A[row * n + a] = c * xa - s * xb;
+        A[row * n + b] = s * xa + c * xb;
+        const double va = V[row * n + a], vb = V[row * n + b];
+        V[row * n + a] = c * va - s * vb;
+        V[row * n + b] = s * va + c * vb;
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    info[0] = converged ? 0 : 1;
+    for (int i = 0; i < n; ++i) evals[i] = A[i * n + i];
+  }
+  __syncthreads();
+  // order descending (stable selection on one thread; n <= a few hundred)
+  if (tid == 0) {
+    for (int i = 0; i < n; ++i) {
+      int best = i;
+      for (int j = i + 1; j < n; ++j)
+        if (evals[j] > evals[best]) best = j;
+      if (best != i) {
+        const double t = evals[i];
+        evals[i] = evals[best];
+        evals[best] = t;
+        info[1 + i] = best;
+      } else {
+        info[1 + i] = i;
+      }
+    }
+  }
+  __syncthreads();
+  // apply the same swaps to V's columns
+  for (int i = 0; i < n; ++i) {
+    const int b = info[1 + i];
+    if (b != i)
+      for (int r = tid; r < n; r += nt) {
+        const double t = V[r * n + i];
+        V[r * n + i] = V[r * n + b];
+        V[r * n + b] = t;
+      }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------- finalize ----
+// Lt: [q][M] lifted vectors (descending).  Keeps up to L_max vectors with
+// tilde > cut after Riemann MGS (eigensolve.hpp:161-176).
+__global__ void __launch_bounds__(1024) k_finalize(const double* __restrict__ Lt, const double* __restrict__ tilde,
+                                                   i64 M, int q, int L_max, double cut, double cv,
+                                                   double* __restrict__ kept, int* __restrict__ kept_src,
+                                                   int* __restrict__ n_kept) {
+  __shared__ double red[33];
+  __shared__ i64 first_nz;
+  int nk = 0;
+  for (int l = 0; l < q && nk < L_max; ++l) {
+    if (!(tilde[l] > cut)) break;
+    double* v = kept + static_cast<i64>(nk) * M;
+    for (i64 i = threadIdx.x; i < M; i += blockDim.x) v[i] = Lt[static_cast<i64>(l) * M + i];
+    __syncthreads();
+    for (int u = 0; u < nk; ++u) {
+      const double* uv = kept + static_cast<i64>(u) * M;
+      double s = 0.0;
+      for (i64 i = threadIdx.x; i < M; i += blockDim.x) s += uv[i] * v[i];
+      const double coef = cv * block_sum(s, red);
+      for (i64 i = threadIdx.x; i < M; i += blockDim.x) v[i] -= coef * uv[i];
+      __syncthreads();
+    }
+    double s2 = 0.0;
+    for (i64 i = threadIdx.x; i < M; i += blockDim.x) s2 += v[i] * v[i];
+    const double norm = sqrt(cv * block_sum(s2, red));
+    if (!(norm > 1e-10)) continue;
+    for (i64 i = threadIdx.x; i < M; i += blockDim.x) v[i] /= norm;
+    __syncthreads();
+    double s1 = 0.0;
+    for (i64 i = threadIdx.x; i < M; i += blockDim.x) s1 += v[i];
+    double sgn = cv * block_sum(s1, red);
+    if (fabs(sgn) < 1e-12 * sqrt(cv * static_cast<double>(M))) {
+      if (threadIdx.x == 0) first_nz = M;
+      __syncthreads();
+      for (i64 i = threadIdx.x; i < M; i += blockDim.x)
+        if (v[i] != 0.0) atomicMin(reinterpret_cast<unsigned long long*>(&first_nz),
+                                   static_cast<unsigned long long>(i));
+      __syncthreads();
+      sgn = first_nz < M ? v[first_nz] : 0.0;
+    }
+    if (sgn < 0.0)
+      for (i64 i = threadIdx.x; i < M; i += blockDim.x) v[i] = -v[i];
+    __syncthreads();
+    if (threadIdx.x == 0) kept_src[nk] = l;
+    ++nk;
+  }
+  if (threadIdx.x == 0) *n_kept = nk;
+}
+
+__global__ void k_residual_norms(const double* __restrict__ SV, const double* __restrict__ V, i64 M, i64 L,
+                                 const double* __restrict__ lam, double cv, double* __restrict__ out) {
+  __shared__ double red[33];
+  const i64 l = blockIdx.x;
+  double s = 0.0;
+  for (i64 i = threadIdx.x; i < M; i += blockDim.x) {
+    const double r = cv * SV[i * L + l] - lam[l] * V[i * L + l];
+    s += r * r;
+  }
+  const double t = block_sum(s, red);
+  if (threadIdx.x == 0) out[l] = sqrt(cv * t);
+}
+
+}  // namespace
+
+struct MatrixView {
+  DevBuf<double> owned;
+  const double* sigma = nullptr;
+  i64 M = 0;
+  std::vector<i64> node_of_row;
+};
+
+static MatrixView matrixize_dev(dfpca_context* ctx, const dfpca_surface* cov, const Grid& grid) {
+  MatrixView mv;
+  const i64 G = grid.G;
+  for (i64 f = 0; f < G; ++f)
+    if (!grid.has_mask || grid.mask[f]) mv.node_of_row.push_back(f);
+  mv.M = static_cast<i64>(mv.node_of_row.size());
+  if (mv.M == 0) fail(kConfig, "InvalidArgument", "no in-mask nodes to decompose");
+  if (mv.M == G) {
+    mv.sigma = cov->values.get();
+  } else {
+    DevBuf<i64> nor(static_cast<std::size_t>(mv.M));
+    DFPCA_CUDA(cudaMemcpyAsync(nor.get(), mv.node_of_row.data(), sizeof(i64) * mv.M,
+                               cudaMemcpyHostToDevice, ctx->stream));
+    mv.owned.alloc(static_cast<std::size_t>(mv.M * mv.M));
+    DFPCA_LAUNCH(ctx, k_gather_sigma, grid_for(mv.M * mv.M, 256), 256, 0, cov->values.get(), G,
+                 nor.get(), mv.M, mv.owned.get());
+    mv.sigma = mv.owned.get();
+    DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return mv;
+}
+
+void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid& grid, i64 q_req,
+                        i64 L_max, unsigned long long seed, double* eigenvalues, double* eigenfunctions,
+                        double* fve, double* total_variance, i64* n_components) {
+  if (cov->kind != DFPCA_SURFACE_COVARIANCE)
+    fail(kConfig, "InvalidArgument", "matrixize expects a covariance surface");
+  if (cov->n != grid.G * grid.G) fail(kConfig, "InvalidArgument", "covariance surface has wrong length");
+  if (q_req < L_max)
+    fail(kConfig, "SketchTooSmall",
+         "sketch size " + std::to_string(q_req) + " is below the requested component count " +
+             std::to_string(L_max));
+  cudaStream_t st = ctx->stream;
+  ctx->begin_stage("eigen");
+  MatrixView mv = matrixize_dev(ctx, cov, grid);
+  const i64 M = mv.M;
+  const i64 q = std::min<i64>(q_req, M);
+
+  // Omega
+  DevBuf<unsigned long long> words(static_cast<std::size_t>(2 * ((M * q + 1) / 2)));
+  DFPCA_LAUNCH(ctx, k_mt19937_64, 1, kMtN, 0, splitmix64(seed), static_cast<i64>(words.size()),
+               words.get());
+  DevBuf<double> omega(static_cast<std::size_t>(M * q));
+  DFPCA_LAUNCH(ctx, k_box_muller, grid_for((M * q + 1) / 2, 256), 256, 0, words.get(), M, q,
+               1.0 / std::sqrt(static_cast<double>(q)), omega.get());
+
+  // Y = Sigma Omega  ([M][q]); Sigma is exactly symmetric, so Sigma(k, m) is
+  // the K-major operand.
+  DevBuf<double> Y(static_cast<std::size_t>(M * q)), Yt(static_cast<std::size_t>(M * q));
+  gemm_tn(ctx, M, q, M, mv.sigma, M, nullptr, omega.get(), q, Y.get(), q, false);
+  transpose(ctx, Y.get(), M, q, Yt.get());
+
+  // Householder QR and thin Q
+  DevBuf<double> tau(static_cast<std::size_t>(q));
+  for (i64 j = -1; j < q - 1; ++j) {
+    const i64 cols = q - (j + 1);
+    DFPCA_LAUNCH(ctx, k_house_step, static_cast<unsigned>(cols), 512, 0, Yt.get(), M, q, j, tau.get());
+  }
+  DevBuf<double> Qt(static_cast<std::size_t>(M * q)), Q(static_cast<std::size_t>(M * q));
+  DFPCA_LAUNCH(ctx, k_q_init, grid_for(M * q, 256), 256, 0, Qt.get(), M, q);
+  for (i64 j = q - 1; j >= 0; --j)
+    DFPCA_LAUNCH(ctx, k_q_apply, static_cast<unsigned>(q - j), 512, 0, Yt.get(), tau.get(), M, q, j,
+                 Qt.get());
+  transpose(ctx, Qt.get(), q, M, Q.get());
+
+  // small = Q^T (Sigma Q)
+  DevBuf<double> Z(static_cast<std::size_t>(M * q));
+  gemm_tn(ctx, M, q, M, mv.sigma, M, nullptr, Q.get(), q, Z.get(), q, false);
+  DevBuf<double> small(static_cast<std::size_t>(q * q)), Vs(static_cast<std::size_t>(q * q));
+  gemm_tn(ctx, q, q, M, Q.get(), q, nullptr, Z.get(), q, small.get(), q, false);
+
+  DevBuf<double> evals(static_cast<std::size_t>(q));
+  DevBuf<int> info(static_cast<std::size_t>(q + 1));
+  const int np = static_cast<int>((q + 1) & ~1ll);
+  const std::size_t jsmem = sizeof(double) * np * 2;
+  DFPCA_LAUNCH(ctx, k_jacobi, 1, 1024, jsmem, small.get(), Vs.get(), static_cast<int>(q), evals.get(),
+               info.get());
+
+  // lifted = Q V  ([M][q]) -> Lt [q][M]
+  DevBuf<double> lifted(static_cast<std::size_t>(M * q)), Lt(static_cast<std::size_t>(M * q));
+  gemm_tn(ctx, M, q, q, Qt.get(), M, nullptr, Vs.get(), q, lifted.get(), q, false);
+  transpose(ctx, lifted.get(), M, q, Lt.get());
+
+  std::vector<double> tilde(static_cast<std::size_t>(q));
+  int jinfo = 0;
+  DFPCA_CUDA(cudaMemcpyAsync(tilde.data(), evals.get(), sizeof(double) * q, cudaMemcpyDeviceToHost, st));
+  DFPCA_CUDA(cudaMemcpyAsync(&jinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+  DFPCA_CUDA(cudaStreamSynchronize(st));
+  if (jinfo != 0) fail(kNumeric, "EigFailure", "projected eigensolver did not converge");
+
+  const double cv = grid.cell_volume();
+  const double cut = tilde.empty() ? 0.0 : std::max(0.0, tilde[0]) * 1e-12;
+  double tilde_total = 0.0;
+  for (double t : tilde)
+    if (t > cut) tilde_total += t;
+  const double total = tilde_total * cv;
+
+  DevBuf<double> kept(static_cast<std::size_t>(std::max<i64>(L_max, 1) * M));
+  DevBuf<int> kept_src(static_cast<std::size_t>(std::max<i64>(L_max, 1))), nkept(1);
+  DFPCA_LAUNCH(ctx, k_finalize, 1, 1024, 0, Lt.get(), evals.get(), M, static_cast<int>(q),
+               static_cast<int>(L_max), cut, cv, kept.get(), kept_src.get(), nkept.get());
+  int nk = 0;
+  DFPCA_CUDA(cudaMemcpyAsync(&nk, nkept.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+  DFPCA_CUDA(cudaStreamSynchronize(st));
+  std::vector<int> src(static_cast<std::size_t>(std::max(nk, 1)));
+  std::vector<double> kv(static_cast<std::size_t>(nk) * M);
+  if (nk > 0) {
+    DFPCA_CUDA(cudaMemcpyAsync(src.data(), kept_src.get(), sizeof(int) * nk, cudaMemcpyDeviceToHost, st));
+    DFPCA_CUDA(cudaMemcpyAsync(kv.data(), kept.get(), sizeof(double) * nk * M, cudaMemcpyDeviceToHost, st));
+  }
+  DFPCA_CUDA(cudaStreamSynchronize(st));
+  ctx->end_stage();
+
+  const i64 G = grid.G;
+  double cum = 0.0;
+  for (int l = 0; l < nk; ++l) {
+    const double lam = tilde[static_cast<std::size_t>(src[l])] * cv;
+    if (eigenvalues) eigenvalues[l] = lam;
+    cum += lam;
+    if (fve) fve[l] = total > 0.0 ? cum / total : 1.0;
+    if (eigenfunctions) {
+      double* surf = eigenfunctions + static_cast<i64>(l) * G;
+      for (i64 f = 0; f < G; ++f) surf[f] = std::nan("");
+      for (i64 r = 0; r < M; ++r) surf[mv.node_of_row[static_cast<std::size_t>(r)]] = kv[static_cast<std::size_t>(l) * M + r];
+    }
+  }
+  if (total_variance) *total_variance = total;
+  if (n_components) *n_components = nk;
+}
+
+void run_eig_residuals(dfpca_context* ctx, const dfpca_surface* cov, const Grid& grid, i64 L,
+                       const double* eigenvalues, const double* eigenfunctions, double* residuals) {
+  if (L <= 0) return;
+  MatrixView mv = matrixize_dev(ctx, cov, grid);
+  const i64 M = mv.M;
+  std::vector<double> V(static_cast<std::size_t>(M * L));
+  for (i64 l = 0; l < L; ++l)
+    for (i64 r = 0; r < M; ++r)
+      V[static_cast<std::size_t>(r * L + l)] = eigenfunctions[l * grid.G + mv.node_of_row[static_cast<std::size_t>(r)]];
+  DevBuf<double> Vd(V.size()), SV(V.size()), lam(static_cast<std::size_t>(L)), out(static_cast<std::size_t>(L));
+  cudaStream_t st = ctx->stream;
+  DFPCA_CUDA(cudaMemcpyAsync(Vd.get(), V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, st));
+  DFPCA_CUDA(cudaMemcpyAsync(lam.get(), eigenvalues, sizeof(double) * L, cudaMemcpyHostToDevice, st));
+  gemm_tn(ctx, M, L, M, mv.sigma, M, nullptr, Vd.get(), L, SV.get(), L, false);
+  DFPCA_LAUNCH(ctx, k_residual_norms, static_cast<unsigned>(L), 256, 0, SV.get(), Vd.get(), M, L, lam.get(),
+               grid.cell_volume(), out.get());
+  DFPCA_CUDA(cudaMemcpyAsync(residuals, out.get(), sizeof(double) * L, cudaMemcpyDeviceToHost, st));
+  DFPCA_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace dfpca_gpu

@@ -1,0 +1,160 @@
+// Host-side internals of libdfpca_cuda.so: error plumbing, device buffers,
+// the grid descriptor, the context and the device-resident handles.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "dfpca_cuda.h"
+
+namespace dfpca_gpu {
+
+using i64 = std::int64_t;
+
+// Error classes of the reference (errors.hpp:11-17).
+enum : int { kParse = 2, kConfig = 3, kNumeric = 4, kVersion = 5 };
+
+struct Failure {
+  int cls = 0;
+  std::string name;
+  std::string msg;
+  i64 sample = -1;
+  i64 obs = -1;
+};
+
+[[noreturn]] void fail(int cls, const char* name, const std::string& msg);
+[[noreturn]] void fail_at(int cls, const char* name, const std::string& msg, i64 sample, i64 obs);
+void cuda_check(cudaError_t e, const char* what);
+
+#define DFPCA_CUDA(call) ::dfpca_gpu::cuda_check((call), #call)
+
+// Move-only owning device array.
+template <class T>
+class DevBuf {
+ public:
+  DevBuf() = default;
+  explicit DevBuf(std::size_t n) { alloc(n); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p_ = o.p_; n_ = o.n_; o.p_ = nullptr; o.n_ = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(std::size_t n) {
+    if (n == n_ && p_) return;
+    release();
+    if (n == 0) return;
+    DFPCA_CUDA(cudaMalloc(reinterpret_cast<void**>(&p_), n * sizeof(T)));
+    n_ = n;
+  }
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  std::size_t size() const { return n_; }
+  std::size_t bytes() const { return n_ * sizeof(T); }
+
+ private:
+  T* p_ = nullptr;
+  std::size_t n_ = 0;
+};
+
+// Validated copy of an EvaluationGrid (grid.hpp:92-230).
+struct Grid {
+  int d = 0;
+  i64 shape[DFPCA_MAX_DIM] = {0, 0, 0};
+  i64 strides[DFPCA_MAX_DIM] = {0, 0, 0};
+  i64 G = 0;
+  std::vector<double> axes[DFPCA_MAX_DIM];
+  double spacing[DFPCA_MAX_DIM] = {0, 0, 0};
+  bool equispaced = false;
+  bool has_mask = false;
+  std::vector<std::uint8_t> mask;
+  i64 in_mask_count = 0;
+
+  bool same_shape(const Grid& o) const {
+    if (d != o.d) return false;
+    for (int k = 0; k < d; ++k)
+      if (shape[k] != o.shape[k]) return false;
+    return true;
+  }
+  double hull_lo(int k) const { return axes[k].front(); }
+  double hull_hi(int k) const { return axes[k].back(); }
+  double cell_volume() const {
+    double v = 1.0;
+    for (int k = 0; k < d; ++k) v *= spacing[k];
+    return v;
+  }
+};
+
+Grid make_grid(const dfpca_grid* g);
+
+class Context;
+
+// Stage timer: CUDA events on the context stream, collected at sync points.
+struct StageMark {
+  std::string name;
+  cudaEvent_t start = nullptr;
+  cudaEvent_t stop = nullptr;
+};
+
+}  // namespace dfpca_gpu
+
+// ---- opaque handles --------------------------------------------------------
+
+struct dfpca_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  dfpca_gpu::Failure err;
+  std::map<std::string, double> stage_ms;
+  std::vector<dfpca_gpu::StageMark> marks;
+  std::vector<cudaEvent_t> event_pool;
+  std::int64_t launches = 0;
+
+  // Reusable scratch (grown on demand, never shrunk while the context lives).
+  dfpca_gpu::DevBuf<unsigned char> scratch;
+  unsigned char* scratch_bytes(std::size_t n) {
+    if (scratch.size() < n) scratch.alloc(n);
+    return scratch.get();
+  }
+
+  void begin_stage(const std::string& name);
+  void end_stage();
+  void collect_stages();  // after a stream sync
+};
+
+struct dfpca_binned {
+  dfpca_gpu::Grid grid;
+  std::int64_t n_samples = 0;
+  std::int64_t n_pair = 0;
+  std::int64_t codes = 1;  // 3^d
+  bool has_mean = false;
+  bool has_cov = false;
+  // Structure flags computed at binning time.
+  bool identical_mass = false;  // every per-sample mass grid bitwise equal
+
+  dfpca_gpu::DevBuf<double> mass, wvalue, wsquare;  // G
+  dfpca_gpu::DevBuf<double> ps_mass, ps_value;      // n_pair * G
+  dfpca_gpu::DevBuf<double> pair_weight;            // n_pair
+  dfpca_gpu::DevBuf<double> diag_mass, diag_value;  // G * codes
+  std::vector<std::int64_t> sample_index;           // n_pair
+  std::vector<double> pair_weight_h;                // n_pair
+  std::vector<std::int64_t> sample_sizes;           // n_samples
+};
+
+struct dfpca_surface {
+  dfpca_gpu::Grid grid;
+  int kind = DFPCA_SURFACE_MEAN;
+  std::int64_t n = 0;
+  dfpca_gpu::DevBuf<double> values;
+};

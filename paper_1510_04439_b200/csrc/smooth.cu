@@ -1,0 +1,758 @@
+// Binned local-linear smoothers on the device: the d-dimensional mean /
+// squares smoother (reference fft_local_linear, fft_smoother.hpp:498-575) and
+// the 2d-dimensional covariance smoother (fft_covariance, :585-744).
+//
+// Moment engine.  The reference runs one full separable convolution per
+// moment multi-index (nm + nl engines, fft_smoother.hpp:191-230, 639-646).
+// Convolution is linear and the stencils are products of per-axis taps
+// K(u) u^order, so the device factors the engines as a tree over the axes:
+// every pass reads one partial once and emits all orders the remaining budget
+// allows (|r| <= 2 for S, <= 1 for T).  The 2d axes of the covariance are
+// split into t-axes (contiguous) and s-axes:
+//   phase T: t-axis passes over row chunks of the pair grids, writing the
+//            t-partials (multi-indices on the t axes only);
+//   phase S: s-axis passes over column chunks of the t-partials, writing the
+//            final moments of one chunk, followed by the per-node solve.
+// The mean smoother is the same machinery with every axis a "t-axis".
+#include <algorithm>
+#include <array>
+#include <functional>
+#include <memory>
+#include <cmath>
+#include <map>
+#include <string>
+
+#include "conv.cuh"
+#include "solve.cuh"
+
+namespace dfpca_gpu {
+
+DevGrid upload_grid_axes(dfpca_context* ctx, const Grid& g, DevBuf<double>& storage);
+void build_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, double* pv);
+
+namespace {
+
+using Orders = std::array<int, kMaxP>;
+
+struct Basis {
+  int p = 0;
+  int nm = 0, nl = 0;
+  std::vector<Orders> engine;  // engine index -> per-axis orders (local_fit.hpp:34-47)
+  explicit Basis(int vars) : p(vars) {
+    nm = 1 + p + p * (p + 1) / 2;
+    nl = 1 + p;
+    engine.assign(nm, Orders{});
+    for (int k = 0; k < p; ++k) engine[1 + k][k] = 1;
+    for (int k = 0; k < p; ++k)
+      for (int l = k; l < p; ++l) {
+        Orders o{};
+        o[k] += 1;
+        o[l] += 1;
+        engine[quad_index(p, k, l)] = o;
+      }
+  }
+  int find(const Orders& o) const {
+    for (int i = 0; i < nm; ++i)
+      if (engine[i] == o) return i;
+    return -1;
+  }
+};
+
+int order_sum(const Orders& o) {
+  int s = 0;
+  for (int v : o) s += v;
+  return s;
+}
+
+// Per-axis taps for orders 0..2 (MomentEngineBank::taps_for,
+// fft_smoother.hpp:199-207), computed on the host with std::pow so the taps
+// are bit-identical to the reference's.
+struct AxisTaps {
+  int R = 0;
+  std::vector<double> t[3];
+};
+
+AxisTaps make_taps(double h, double spacing) {
+  AxisTaps a;
+  a.R = static_cast<int>(std::ceil(h / spacing));
+  for (int order = 0; order < 3; ++order) {
+    a.t[order].assign(2 * a.R + 1, 0.0);
+    for (int o = -a.R; o <= a.R; ++o) {
+      const double u = -static_cast<double>(o) * spacing;
+      a.t[order][o + a.R] = kernel_axis_value(u, h) * std::pow(u, order);
+    }
+  }
+  return a;
+}
+
+// A partial array of the tree: orders used so far and where it lives.
+struct Partial {
+  Orders ord{};
+  int budget_max = 2;  // 2: mass-like (S), 1: value-like (T)
+  DevBuf<double>* buf = nullptr;
+  double* ptr = nullptr;
+};
+
+// Runs passes for a list of axes (processed in the given order) over a chunk
+// of `rows` contiguous outer rows; every array in the chunk has shape
+// [rows][shape[ax_first..]] flattened.  `leaf_ptr` maps a finished partial to
+// the destination pointer of its last pass (or nullptr to allocate).
+struct ChunkDims {
+  i64 rows;                // leading extent (outer rows of the chunk)
+  std::vector<i64> shape;  // extents of the axes of this phase, in memory order
+  i64 tail;                // trailing contiguous extent after these axes
+};
+
+View make_view(double* p, const ChunkDims& cd, int k, i64 row_stride_override = -1) {
+  // Axis k of cd.shape; memory is [rows][shape...][tail].
+  i64 before = cd.rows;
+  for (int a = 0; a < k; ++a) before *= cd.shape[a];
+  i64 after = cd.tail;
+  for (std::size_t a = k + 1; a < cd.shape.size(); ++a) after *= cd.shape[a];
+  View v;
+  v.p = p;
+  v.outer = before;
+  v.n = cd.shape[k];
+  v.inner = after;
+  v.js = after;
+  v.os = row_stride_override >= 0 ? row_stride_override : cd.shape[k] * after;
+  return v;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Solve kernel over a chunk of points with compact moment arrays.
+struct MomPtrs {
+  const double* S[kMaxNm];
+  const double* T[kMaxNl];
+};
+
+struct SolveGeom {
+  i64 npts;        // points in the chunk
+  i64 tc;          // chunk width (columns); point e -> (e / tc, t0 + e % tc)
+  i64 t0;
+  i64 gt;          // full column extent (t grid size); 1-D mean: gt = tc = G
+  int cov;         // 1: mask both s and t nodes
+  const std::uint8_t* mask;  // device mask (nullable)
+  const double* mean;        // covariance: centered later; unused here
+};
+
+template <int N>
+__global__ void __launch_bounds__(128) k_solve(MomPtrs mp, SolveGeom g, double* __restrict__ out,
+                                               unsigned long long* __restrict__ empty_count,
+                                               i64* __restrict__ empty_list, i64 list_cap) {
+  constexpr int p = N - 1;
+  constexpr int nm = 1 + p + p * (p + 1) / 2;
+  constexpr int nl = 1 + p;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < g.npts;
+       e += (i64)gridDim.x * blockDim.x) {
+    const i64 row = e / g.tc;
+    const i64 col = g.t0 + e % g.tc;
+    const i64 dst = g.cov ? row * g.gt + col : col + row * g.gt;
+    bool inside = true;
+    if (g.mask) inside = g.cov ? (g.mask[row] != 0 && g.mask[col] != 0) : (g.mask[dst] != 0);
+    if (!inside) {
+      out[dst] = __longlong_as_double(0x7ff8000000000000ll);
+      continue;
+    }
+    double S[nm], T[nl];
+#pragma unroll
+    for (int i = 0; i < nm; ++i) S[i] = mp.S[i][e];
+#pragma unroll
+    for (int i = 0; i < nl; ++i) T[i] = mp.T[i][e];
+    double b0;
+    const int st = solve_local_dev<N>(S, T, b0);
+    if (st == kFitEmpty) {
+      const unsigned long long slot = atomicAdd(empty_count, 1ull);
+      if (static_cast<i64>(slot) < list_cap) empty_list[slot] = dst;
+      out[dst] = __longlong_as_double(0x7ff8000000000000ll);
+    } else {
+      out[dst] = b0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Empty-window fallback ladder (fft_smoother.hpp:471-487): for each listed
+// node, up to kWindowRetries direct gathers at 1.5^r h over the binned arrays
+// (mean: gather_binned_equations, :236-277; covariance: the pw/pv window
+// gather, :668-711), each followed by the ridged solve.
+struct LadderGeom {
+  int p;                 // dims of the domain (d or 2d)
+  i64 shape[kMaxP];
+  i64 strides[kMaxP];
+  double spacing[kMaxP];
+  double h[kMaxP];
+};
+
+__global__ void k_ladder(LadderGeom lg, const double* __restrict__ mass, const double* __restrict__ value,
+                         const i64* __restrict__ nodes, i64 n_nodes, double* __restrict__ out,
+                         unsigned long long* __restrict__ still_empty) {
+  __shared__ double red[256];
+  __shared__ double acc[kMaxNm + kMaxNl];
+  __shared__ int status_sh;
+  const int p = lg.p;
+  const int nm = 1 + p + p * (p + 1) / 2;
+  const int nl = 1 + p;
+  for (i64 q = blockIdx.x; q < n_nodes; q += gridDim.x) {
+    const i64 flat = nodes[q];
+    i64 node[kMaxP];
+    {
+      i64 rem = flat;
+      for (int k = p - 1; k >= 0; --k) {
+        node[k] = rem % lg.shape[k];
+        rem /= lg.shape[k];
+      }
+    }
+    double scale = 1.0;
+    int status = kFitEmpty;
+    double b0 = 0.0;
+    for (int retry = 0; retry < 3 && status == kFitEmpty; ++retry) {
+      scale *= 1.5;
+      double hs[kMaxP];
+      i64 lo[kMaxP], ext[kMaxP];
+      i64 count = 1;
+      for (int k = 0; k < p; ++k) {
+        hs[k] = lg.h[k] * scale;
+        const i64 r = static_cast<i64>(ceil(hs[k] / lg.spacing[k]));
+        lo[k] = node[k] - r < 0 ? 0 : node[k] - r;
+        const i64 hi = node[k] + r + 1 > lg.shape[k] ? lg.shape[k] : node[k] + r + 1;
+        ext[k] = hi - lo[k];
+        count *= ext[k];
+      }
+      double part[kMaxNm + kMaxNl];
+      for (int i = 0; i < nm + nl; ++i) part[i] = 0.0;
+      for (i64 w = threadIdx.x; w < count; w += blockDim.x) {
+        i64 rem = w, off = 0;
+        double u[kMaxP];
+        for (int k = p - 1; k >= 0; --k) {
+          const i64 m = lo[k] + rem % ext[k];
+          rem /= ext[k];
+          off += m * lg.strides[k];
+          u[k] = static_cast<double>(node[k] - m) * lg.spacing[k];
+        }
+        const double mv = mass[off], vv = value[off];
+        if (mv == 0.0 && vv == 0.0) continue;
+        double kw = 1.0;
+        for (int k = 0; k < p; ++k) {
+          const double z = u[k] / hs[k];
+          const double t = 1.0 - z * z;
+          if (!(t > 0.0)) {
+            kw = 0.0;
+            break;
+          }
+          kw *= 0.75 * t / hs[k];
+        }
+        if (kw == 0.0) continue;
+        const double w0 = kw * mv, wy = kw * vv;
+        part[0] += w0;
+        part[nm] += wy;
+        for (int k = 0; k < p; ++k) {
+          const double wu = w0 * u[k];
+          part[1 + k] += wu;
+          part[nm + 1 + k] += wy * u[k];
+          for (int l = k; l < p; ++l) part[quad_index(p, k, l)] += wu * u[l];
+        }
+      }
+      for (int i = 0; i < nm + nl; ++i) {
+        red[threadIdx.x] = part[i];
+        __syncthreads();
+        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+          if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+          __syncthreads();
+        }
+        if (threadIdx.x == 0) acc[i] = red[0];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) {
+        int st = kFitEmpty;
+        if (acc[0] > 0.0) st = solve_local_any(p, acc, acc + nm, b0);
+        status_sh = st;
+        if (st != kFitEmpty) out[flat] = b0;
+      }
+      __syncthreads();
+      status = status_sh;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0 && status == kFitEmpty) atomicAdd(still_empty, 1ull);
+  }
+}
+
+// Covariance centering and exact symmetrization (fft_smoother.hpp:723-736),
+// 32x32 tile pairs so both the (a,b) and (b,a) accesses are coalesced.
+__global__ void k_center_symmetrize(double* __restrict__ cov, const double* __restrict__ mean,
+                                    const std::uint8_t* __restrict__ mask, i64 G) {
+  __shared__ double ta[32][33];
+  __shared__ double tb[32][33];
+  const i64 tiles = (G + 31) / 32;
+  // blockIdx.x enumerates tile pairs (I <= J)
+  i64 t = blockIdx.x;
+  i64 I = 0;
+  while (t >= tiles - I) {
+    t -= tiles - I;
+    ++I;
+  }
+  const i64 J = I + t;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8 threads
+  for (int r = ty; r < 32; r += 8) {
+    const i64 a = I * 32 + r, b = J * 32 + tx;
+    double v = 0.0;
+    if (a < G && b < G) {
+      v = cov[a * G + b];
+      if (!mask || (mask[a] && mask[b])) v -= mean[a] * mean[b];
+    }
+    ta[r][tx] = v;
+    const i64 a2 = J * 32 + r, b2 = I * 32 + tx;
+    double v2 = 0.0;
+    if (a2 < G && b2 < G) {
+      v2 = cov[a2 * G + b2];
+      if (!mask || (mask[a2] && mask[b2])) v2 -= mean[a2] * mean[b2];
+    }
+    tb[r][tx] = v2;
+  }
+  __syncthreads();
+  // ta[r][c] = cov(I*32+r, J*32+c); tb[r][c] = cov(J*32+r, I*32+c)
+  for (int r = ty; r < 32; r += 8) {
+    const i64 a = I * 32 + r, b = J * 32 + tx;  // element (a, b) of tile (I, J)
+    if (a < G && b < G) {
+      double x = ta[r][tx];
+      if (a < b && !isnan(x)) x = 0.5 * (x + tb[tx][r]);
+      else if (a > b) {
+        const double y = tb[tx][r];  // (b, a), b < a
+        if (!isnan(y)) x = 0.5 * (y + x);
+      }
+      cov[a * G + b] = x;
+    }
+    const i64 a2 = J * 32 + r, b2 = I * 32 + tx;  // element (a2, b2) of tile (J, I)
+    if (I != J && a2 < G && b2 < G) {
+      double x = tb[r][tx];
+      if (a2 > b2) {
+        const double y = ta[tx][r];  // (b2, a2) with b2 < a2
+        if (!isnan(y)) x = 0.5 * (y + x);
+      } else if (a2 < b2 && !isnan(x)) {
+        x = 0.5 * (x + ta[tx][r]);
+      }
+      cov[a2 * G + b2] = x;
+    }
+  }
+}
+
+__global__ void k_fill_nan(double* p, i64 n) {
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < n; e += (i64)gridDim.x * blockDim.x)
+    p[e] = __longlong_as_double(0x7ff8000000000000ll);
+}
+
+// ---------------------------------------------------------------------------
+namespace {
+
+using SolveLauncher = void (*)(dfpca_context*, const MomPtrs&, const SolveGeom&, double*,
+                               unsigned long long*, i64*, i64);
+template <int N>
+void launch_solve(dfpca_context* ctx, const MomPtrs& mp, const SolveGeom& g, double* out,
+                  unsigned long long* cnt, i64* list, i64 cap) {
+  DFPCA_LAUNCH(ctx, k_solve<N>, grid_for(g.npts, 128, 148ll * 64), 128, 0, mp, g, out, cnt, list,
+               cap);
+}
+SolveLauncher solve_launcher(int p) {
+  switch (p) {
+    case 1: return &launch_solve<2>;
+    case 2: return &launch_solve<3>;
+    case 3: return &launch_solve<4>;
+    case 4: return &launch_solve<5>;
+    case 5: return &launch_solve<6>;
+    default: return &launch_solve<7>;
+  }
+}
+
+// Workspace arena of full-chunk arrays.
+struct Arena {
+  std::vector<std::unique_ptr<DevBuf<double>>> bufs;
+  double* get(std::size_t n) {
+    bufs.push_back(std::make_unique<DevBuf<double>>(n));
+    return bufs.back()->get();
+  }
+};
+
+// Runs the passes of a tree over `axes` (indices into cd.shape, processed in
+// the given order) starting from `roots`; the final level's arrays are
+// returned (keyed by full orders).  Intermediate levels live in `arena`;
+// if `final_dst` resolves a pointer for a leaf, the last pass writes there.
+struct Leaf {
+  Orders ord;
+  int budget_max;
+  double* ptr;
+  View view;  // view of the leaf array over the chunk (for phase S reads)
+};
+
+struct TreeAxis {
+  int axis_index;  // index into the domain axes (for taps / orders)
+  int view_k;      // index into cd.shape
+};
+
+std::vector<Leaf> run_tree(dfpca_context* ctx, const std::vector<Leaf>& roots,
+                           const std::vector<TreeAxis>& axes, const ChunkDims& cd,
+                           const std::vector<AxisTaps>& taps, i64 chunk_elems,
+                           double* taps_dev, std::vector<std::unique_ptr<DevBuf<double>>>& keep,
+                           const std::function<double*(const Orders&, int)>& final_dst,
+                           const std::function<i64(const Orders&, int)>& final_row_stride,
+                           bool first_reads_strided, i64 first_row_stride) {
+  std::vector<Leaf> cur = roots;
+  for (std::size_t ai = 0; ai < axes.size(); ++ai) {
+    const TreeAxis& ax = axes[ai];
+    const bool last = ai + 1 == axes.size();
+    std::vector<Leaf> next;
+    std::vector<std::unique_ptr<DevBuf<double>>> level_bufs;
+    for (const Leaf& in : cur) {
+      const int used = order_sum(in.ord);
+      const int n_out = in.budget_max - used + 1;
+      PassSpec spec{};
+      spec.in = (ai == 0 && first_reads_strided) ? make_view(in.ptr, cd, ax.view_k, first_row_stride)
+                                                 : make_view(in.ptr, cd, ax.view_k);
+      if (ai == 0 && first_reads_strided) spec.in = in.view;
+      spec.n_out = n_out;
+      spec.R = taps[ax.axis_index].R;
+      for (int r = 0; r < n_out; ++r) {
+        Leaf o;
+        o.ord = in.ord;
+        o.ord[ax.axis_index] += r;
+        o.budget_max = in.budget_max;
+        double* dst = last ? final_dst(o.ord, o.budget_max) : nullptr;
+        i64 rs = -1;
+        if (!dst) {
+          level_bufs.push_back(std::make_unique<DevBuf<double>>(static_cast<std::size_t>(chunk_elems)));
+          dst = level_bufs.back()->get();
+        } else {
+          rs = final_row_stride(o.ord, o.budget_max);
+        }
+        o.ptr = dst;
+        spec.out[r] = make_view(dst, cd, ax.view_k, rs);
+        o.view = spec.out[r];
+        spec.taps[r] = taps[ax.axis_index].t[r].data();
+        next.push_back(o);
+      }
+      run_pass(ctx, spec, taps_dev);
+    }
+    // previous level buffers can be released once this level's passes are
+    // queued (stream order protects the reads).
+    for (auto& b : keep) {
+      (void)b;
+    }
+    keep.clear();
+    for (auto& b : level_bufs) keep.push_back(std::move(b));
+    cur = std::move(next);
+  }
+  return cur;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Host orchestration.
+
+struct SmoothTimer {
+  dfpca_context* ctx;
+  explicit SmoothTimer(dfpca_context* c, const char* name) : ctx(c) { ctx->begin_stage(name); }
+  ~SmoothTimer() { ctx->end_stage(); }
+};
+
+void validate_bandwidth(const Grid& grid, const double* h);
+
+void run_local_linear(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid, const double* h,
+                      int target, double* out_host, dfpca_surface** out_surface) {
+  const int d = grid.d;
+  const i64 G = grid.G;
+  Basis basis(d);
+  std::vector<AxisTaps> taps(d);
+  for (int k = 0; k < d; ++k) taps[k] = make_taps(h[k], grid.spacing[k]);
+
+  cudaStream_t st = ctx->stream;
+  DevBuf<double> taps_dev(3 * (2 * 4096 + 1));
+  auto surf = std::make_unique<dfpca_surface>();
+  surf->grid = grid;
+  surf->kind = target == DFPCA_TARGET_MEAN ? DFPCA_SURFACE_MEAN : DFPCA_SURFACE_DIAG;
+  surf->n = G;
+  surf->values.alloc(G);
+
+  ctx->begin_stage("moments");
+  const double* value = target == DFPCA_TARGET_MEAN ? b->wvalue.get() : b->wsquare.get();
+  ChunkDims cd;
+  cd.rows = 1;
+  for (int k = 0; k < d; ++k) cd.shape.push_back(grid.shape[k]);
+  cd.tail = 1;
+  std::vector<TreeAxis> axes;
+  for (int k = d - 1; k >= 0; --k) axes.push_back({k, k});
+  std::vector<Leaf> roots(2);
+  roots[0].ord = Orders{};
+  roots[0].budget_max = 2;
+  roots[0].ptr = const_cast<double*>(b->mass.get());
+  roots[1].ord = Orders{};
+  roots[1].budget_max = 1;
+  roots[1].ptr = const_cast<double*>(value);
+  std::vector<std::unique_ptr<DevBuf<double>>> keep;
+  std::vector<std::unique_ptr<DevBuf<double>>> finals;
+  auto final_dst = [&](const Orders&, int) -> double* {
+    finals.push_back(std::make_unique<DevBuf<double>>(static_cast<std::size_t>(G)));
+    return finals.back()->get();
+  };
+  auto final_rs = [&](const Orders&, int) -> i64 { return -1; };
+  std::vector<Leaf> leaves = run_tree(ctx, roots, axes, cd, taps, G, taps_dev.get(), keep, final_dst,
+                                      final_rs, false, -1);
+  ctx->end_stage();
+
+  MomPtrs mp{};
+  for (const Leaf& l : leaves) {
+    const int idx = basis.find(l.ord);
+    if (l.budget_max == 2) mp.S[idx] = l.ptr;
+    else mp.T[idx] = l.ptr;
+  }
+
+  ctx->begin_stage("solve");
+  DevBuf<std::uint8_t> mask_dev;
+  if (grid.has_mask) {
+    mask_dev.alloc(G);
+    DFPCA_CUDA(cudaMemcpyAsync(mask_dev.get(), grid.mask.data(), G, cudaMemcpyHostToDevice, st));
+  }
+  DevBuf<unsigned long long> cnt(1);
+  DevBuf<i64> list(static_cast<std::size_t>(G));
+  DFPCA_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long), st));
+  SolveGeom sg{};
+  sg.npts = G;
+  sg.tc = G;
+  sg.t0 = 0;
+  sg.gt = G;
+  sg.cov = 0;
+  sg.mask = grid.has_mask ? mask_dev.get() : nullptr;
+  solve_launcher(d)(ctx, mp, sg, surf->values.get(), cnt.get(), list.get(), G);
+  unsigned long long n_empty = 0;
+  DFPCA_CUDA(cudaMemcpyAsync(&n_empty, cnt.get(), sizeof(n_empty), cudaMemcpyDeviceToHost, st));
+  DFPCA_CUDA(cudaStreamSynchronize(st));
+  ctx->end_stage();
+
+  if (n_empty > 0) {
+    ctx->begin_stage("fallback");
+    LadderGeom lg{};
+    lg.p = d;
+    for (int k = 0; k < d; ++k) {
+      lg.shape[k] = grid.shape[k];
+      lg.strides[k] = grid.strides[k];
+      lg.spacing[k] = grid.spacing[k];
+      lg.h[k] = h[k];
+    }
+    DevBuf<unsigned long long> still(1);
+    DFPCA_CUDA(cudaMemsetAsync(still.get(), 0, sizeof(unsigned long long), st));
+    DFPCA_LAUNCH(ctx, k_ladder, grid_for(static_cast<i64>(n_empty), 1, 148ll * 8), 256, 0, lg,
+                 b->mass.get(), value, list.get(), static_cast<i64>(n_empty), surf->values.get(),
+                 still.get());
+    unsigned long long n_still = 0;
+    DFPCA_CUDA(cudaMemcpyAsync(&n_still, still.get(), sizeof(n_still), cudaMemcpyDeviceToHost, st));
+    DFPCA_CUDA(cudaStreamSynchronize(st));
+    ctx->end_stage();
+    if (n_still > 0)
+      fail(kNumeric, "BandwidthTooSmall",
+           "binned local linear smoother: " + std::to_string(n_still) +
+               " node(s) had no binned mass in the kernel window (AllWeightsZero) after 3 window "
+               "enlargements");
+  }
+  if (out_host)
+    DFPCA_CUDA(cudaMemcpyAsync(out_host, surf->values.get(), sizeof(double) * G,
+                               cudaMemcpyDeviceToHost, st));
+  DFPCA_CUDA(cudaStreamSynchronize(st));
+  if (out_surface) *out_surface = surf.release();
+}
+
+// Pair grids + moments + solve + center + symmetrize for the covariance.
+void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid, const double* h,
+                    const double* mean_host, dfpca_surface** out) {
+  const int d = grid.d;
+  const int p = 2 * d;
+  const i64 G = grid.G;
+  const i64 G2 = G * G;
+  cudaStream_t st = ctx->stream;
+  Basis basis(p);
+  std::vector<AxisTaps> taps(p);
+  for (int k = 0; k < p; ++k) taps[k] = make_taps(h[k % d], grid.spacing[k % d]);
+  DevBuf<double> taps_dev(3 * (2 * 4096 + 1));
+
+  auto surf = std::make_unique<dfpca_surface>();
+  surf->grid = grid;
+  surf->kind = DFPCA_SURFACE_COVARIANCE;
+  surf->n = G2;
+  surf->values.alloc(static_cast<std::size_t>(G2));
+
+  // ---- pair grids (K2) ----
+  DevBuf<double> pw(static_cast<std::size_t>(G2)), pv(static_cast<std::size_t>(G2));
+  ctx->begin_stage("pairs");
+  build_pair_grids(ctx, b, pw.get(), pv.get());
+  ctx->end_stage();
+
+  // ---- phase T: t-axis passes over row chunks of the pair grids ----
+  ctx->begin_stage("moments");
+  std::vector<std::unique_ptr<DevBuf<double>>> tpart_store;
+  std::map<std::pair<Orders, int>, double*> tpart;
+  // t-partials: all t-multi-indices with |a| <= 2 (mass) / <= 1 (value)
+  {
+    // enumerate leaves of the t-tree
+    std::vector<Orders> mass_idx, val_idx;
+    std::function<void(int, Orders, int, int, std::vector<Orders>&)> rec =
+        [&](int k, Orders o, int used, int mx, std::vector<Orders>& outv) {
+          if (k == p) {
+            outv.push_back(o);
+            return;
+          }
+          for (int r = 0; r + used <= mx; ++r) {
+            Orders q = o;
+            q[k] = r;
+            rec(k + 1, q, used + r, mx, outv);
+          }
+        };
+    rec(d, Orders{}, 0, 2, mass_idx);
+    rec(d, Orders{}, 0, 1, val_idx);
+    for (auto& o : mass_idx) {
+      tpart_store.push_back(std::make_unique<DevBuf<double>>(static_cast<std::size_t>(G2)));
+      tpart[{o, 2}] = tpart_store.back()->get();
+    }
+    for (auto& o : val_idx) {
+      tpart_store.push_back(std::make_unique<DevBuf<double>>(static_cast<std::size_t>(G2)));
+      tpart[{o, 1}] = tpart_store.back()->get();
+    }
+  }
+  // chunk rows (s nodes) so intermediates stay bounded
+  const i64 budget_elems = std::max<i64>(G, (i64(1) << 31) / 8);  // ~2 GiB per level array set
+  i64 sc = std::max<i64>(1, std::min<i64>(G, budget_elems / std::max<i64>(G, 1) / 4));
+  std::vector<TreeAxis> taxes;
+  for (int k = p - 1; k >= d; --k) taxes.push_back({k, k - d});
+  for (i64 s0 = 0; s0 < G; s0 += sc) {
+    const i64 rows = std::min(sc, G - s0);
+    ChunkDims cd;
+    cd.rows = rows;
+    for (int k = d; k < p; ++k) cd.shape.push_back(grid.shape[k - d]);
+    cd.tail = 1;
+    std::vector<Leaf> roots(2);
+    roots[0].budget_max = 2;
+    roots[0].ptr = pw.get() + s0 * G;
+    roots[1].budget_max = 1;
+    roots[1].ptr = pv.get() + s0 * G;
+    std::vector<std::unique_ptr<DevBuf<double>>> keep;
+    auto final_dst = [&](const Orders& o, int bm) -> double* { return tpart.at({o, bm}) + s0 * G; };
+    auto final_rs = [&](const Orders&, int) -> i64 { return -1; };
+    run_tree(ctx, roots, taxes, cd, taps, rows * G, taps_dev.get(), keep, final_dst, final_rs, false,
+             -1);
+  }
+
+  // ---- phase S: s-axis passes over column chunks, then solve ----
+  DevBuf<std::uint8_t> mask_dev;
+  if (grid.has_mask) {
+    mask_dev.alloc(G);
+    DFPCA_CUDA(cudaMemcpyAsync(mask_dev.get(), grid.mask.data(), G, cudaMemcpyHostToDevice, st));
+  }
+  DevBuf<unsigned long long> cnt(1);
+  const i64 list_cap = std::min<i64>(G2, i64(1) << 26);
+  DevBuf<i64> list(static_cast<std::size_t>(list_cap));
+  DFPCA_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long), st));
+  i64 tc = std::max<i64>(1, std::min<i64>(G, budget_elems / std::max<i64>(G, 1) / 4));
+  std::vector<TreeAxis> saxes;
+  for (int k = d - 1; k >= 0; --k) saxes.push_back({k, k});
+  double solve_ms_acc = 0.0;
+  (void)solve_ms_acc;
+  for (i64 t0 = 0; t0 < G; t0 += tc) {
+    const i64 cols = std::min(tc, G - t0);
+    ChunkDims cd;
+    cd.rows = 1;
+    for (int k = 0; k < d; ++k) cd.shape.push_back(grid.shape[k]);
+    cd.tail = cols;
+    // roots: the t-partials viewed as [s...][cols] with row stride G
+    std::vector<Leaf> roots;
+    for (auto& kv : tpart) {
+      Leaf r;
+      r.ord = kv.first.first;
+      r.budget_max = kv.first.second;
+      // budget left for s-axes is budget_max - |a|; encode by keeping ord
+      r.ptr = kv.second + t0;
+      // first pass reads axis d-1 of the s block: outer = s[0..d-2], n = s[d-1], inner = cols
+      View v;
+      v.p = r.ptr;
+      v.n = grid.shape[d - 1];
+      v.js = G;
+      v.inner = cols;
+      v.outer = G / grid.shape[d - 1];
+      v.os = grid.shape[d - 1] * G;
+      r.view = v;
+      roots.push_back(r);
+    }
+    std::vector<std::unique_ptr<DevBuf<double>>> keep;
+    std::vector<std::unique_ptr<DevBuf<double>>> finals;
+    auto final_dst = [&](const Orders&, int) -> double* {
+      finals.push_back(std::make_unique<DevBuf<double>>(static_cast<std::size_t>(G * cols)));
+      return finals.back()->get();
+    };
+    auto final_rs = [&](const Orders&, int) -> i64 { return -1; };
+    std::vector<Leaf> leaves = run_tree(ctx, roots, saxes, cd, taps, G * cols, taps_dev.get(), keep,
+                                        final_dst, final_rs, true, -1);
+    MomPtrs mp{};
+    for (const Leaf& l : leaves) {
+      const int idx = basis.find(l.ord);
+      if (l.budget_max == 2) mp.S[idx] = l.ptr;
+      else mp.T[idx] = l.ptr;
+    }
+    SolveGeom sg{};
+    sg.npts = G * cols;
+    sg.tc = cols;
+    sg.t0 = t0;
+    sg.gt = G;
+    sg.cov = 1;
+    sg.mask = grid.has_mask ? mask_dev.get() : nullptr;
+    solve_launcher(p)(ctx, mp, sg, surf->values.get(), cnt.get(), list.get(), list_cap);
+  }
+  unsigned long long n_empty = 0;
+  DFPCA_CUDA(cudaMemcpyAsync(&n_empty, cnt.get(), sizeof(n_empty), cudaMemcpyDeviceToHost, st));
+  DFPCA_CUDA(cudaStreamSynchronize(st));
+  ctx->end_stage();
+  tpart_store.clear();
+
+  if (n_empty > 0) {
+    if (static_cast<i64>(n_empty) > list_cap)
+      fail(kNumeric, "BandwidthTooSmall",
+           "binned covariance smoother: too many empty kernel windows");
+    ctx->begin_stage("fallback");
+    LadderGeom lg{};
+    lg.p = p;
+    for (int k = 0; k < p; ++k) {
+      lg.shape[k] = grid.shape[k % d];
+      lg.spacing[k] = grid.spacing[k % d];
+      lg.h[k] = h[k % d];
+    }
+    for (int k = p - 1, s = 1; k >= 0; --k) {
+      lg.strides[k] = s;
+      s *= static_cast<int>(lg.shape[k]);
+    }
+    DevBuf<unsigned long long> still(1);
+    DFPCA_CUDA(cudaMemsetAsync(still.get(), 0, sizeof(unsigned long long), st));
+    DFPCA_LAUNCH(ctx, k_ladder, grid_for(static_cast<i64>(n_empty), 1, 148ll * 8), 256, 0, lg,
+                 pw.get(), pv.get(), list.get(), static_cast<i64>(n_empty), surf->values.get(),
+                 still.get());
+    unsigned long long n_still = 0;
+    DFPCA_CUDA(cudaMemcpyAsync(&n_still, still.get(), sizeof(n_still), cudaMemcpyDeviceToHost, st));
+    DFPCA_CUDA(cudaStreamSynchronize(st));
+    ctx->end_stage();
+    if (n_still > 0)
+      fail(kNumeric, "BandwidthTooSmall",
+           "binned covariance smoother: " + std::to_string(n_still) +
+               " node(s) had no binned mass in the kernel window (AllWeightsZero) after 3 window "
+               "enlargements");
+  }
+
+  // ---- center + symmetrize (K5) ----
+  ctx->begin_stage("center");
+  DevBuf<double> mean_dev(static_cast<std::size_t>(G));
+  DFPCA_CUDA(cudaMemcpyAsync(mean_dev.get(), mean_host, sizeof(double) * G, cudaMemcpyHostToDevice, st));
+  const i64 tiles = (G + 31) / 32;
+  const i64 pairs = tiles * (tiles + 1) / 2;
+  DFPCA_LAUNCH(ctx, k_center_symmetrize, static_cast<unsigned>(pairs), 256, 0, surf->values.get(),
+               mean_dev.get(), grid.has_mask ? mask_dev.get() : nullptr, G);
+  ctx->end_stage();
+  DFPCA_CUDA(cudaStreamSynchronize(st));
+  *out = surf.release();
+}
+
+}  // namespace dfpca_gpu

@@ -1,0 +1,22 @@
+import os
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); runs through libdfpca_cuda.so")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+@pytest.fixture(scope="session")
+def ref():
+    """The compiled reference (oracle/_ref) -- the parity checker."""
+    from oracle import ref as R
+    if not R.available():
+        pytest.skip("oracle/_ref not built (make -C oracle)")
+    return R

@@ -1,0 +1,359 @@
+#!/usr/bin/env python3
+"""Benchmark of the binned FPCA covariance smoother on the GPU (libdfpca_cuda.so).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload = BASELINE.json configs[2]: d = 2, n = 2000 subjects observed at every
+node of a 64 x 64 midpoint grid, h = 0.1 (R = 7, 15 taps), 4-D local-linear
+covariance over G^2 = 16,777,216 grid points (synthetic data of that shape).
+
+A "step" is one fft_covariance (reference fft_smoother.hpp:585): pair grids,
+the 20 kernel-moment convolutions, the per-node 5x5 solves with the fallback
+ladder, centering and symmetrization, from device-resident binned data to a
+device-resident covariance.  value = G^2 / step time (gridpts/s), summed over
+ranks; N > 1 runs one independent replica per GPU ("scaling": "weak").
+e2e: the same metric through the public API with host buffers: pinned host
+observations -> linear_bin -> fft_local_linear -> fft_covariance -> covariance
+copied back to pinned host memory, every step.
+
+--impl reference times the reference implementation itself (oracle/_ref: the
+reference's headers compiled unchanged) on the host cores, on a bounded sample
+of the same workload (see cpu_sample()).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CELLS, N_SUBJ, H = 64, 2000, 0.1
+METRIC = "smoothed covariance gridpts/s (d=2 64², 4-D LL); end-to-end FPCA time vs CPU"
+WORKLOAD = "configs[2]: d=2 n=2000 on 64x64 midpoint grid, GridNodes design, h=0.1 (R=7), fft_covariance"
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+# FP64 peak of this pool's B200 (DMMA m8n8k4 and DFMA both), measured with
+# tools/fp64_peak.cu (profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json has no FP64 entry.
+FP64_PEAK_TFLOPS = 37.07
+
+
+def rank_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].strip() == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------- data --
+def make_data(seed=20260815):
+    from paper_1510_04439_b200 import synth
+    return synth.grid_nodes(2, CELLS, N_SUBJ, H, seed=seed)
+
+
+def cpu_sample(sd, n_sub: int):
+    """Bounded reference sample: the same grid, bandwidth and design with the
+    first n_sub subjects (the pair build is O(n), convolutions and solves are
+    O(G^2) and unchanged)."""
+    G = CELLS * CELLS
+    off = sd.offsets[:n_sub + 1]
+    return off, sd.coords[:off[-1] * 2], sd.values[:off[-1]]
+
+
+# -------------------------------------------------------------- reference --
+def run_reference(args, emit=True):
+    from oracle import ref as R
+    rank, world, _ = rank_env()
+    if rank != 0:
+        return None
+    cores = os.cpu_count() or 1
+    R.set_threads(cores)
+    sd = make_data()
+    n_sub = args.cpu_subjects
+    off, coords, values = cpu_sample(sd, n_sub)
+    grid = (sd.axes, None)
+    G2 = (CELLS * CELLS) ** 2
+
+    def step():
+        b = R.linear_bin(grid, off, coords, values, True, True)
+        mu = R.fft_local_linear(b, grid, sd.h, 0)
+        t0 = time.perf_counter()
+        R.fft_covariance(b, grid, sd.h, mu)
+        return time.perf_counter() - t0
+
+    for _ in range(args.ref_warmup if args.ref_warmup is not None else min(args.warmup, 1)):
+        step()
+    times = [step() for _ in range(max(1, args.ref_steps if args.ref_steps else args.steps))]
+    t = float(np.mean(times))
+    val = G2 / t
+    sample = (f"fft_covariance on the full 64x64 grid (16,777,216 gridpts), first {n_sub} of {N_SUBJ} subjects, "
+              f"reference headers compiled unchanged (oracle/_ref), set_max_threads({cores})")
+    line = {"metric": METRIC, "value": val, "unit": "gridpts/s", "n_gpus": args.gpus, "steps": len(times),
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "cpu_sample": f"n={n_sub}"},
+            "impl": "reference",
+            "cpu_baseline": {"value": val, "unit": "gridpts/s", "cores": cores, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": "gridpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if emit:
+        print(json.dumps(line), flush=True)
+    return line
+
+
+# ------------------------------------------------------------------- ours --
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-subjects", type=int, default=100)
+    ap.add_argument("--ref-steps", type=int, default=None)
+    ap.add_argument("--ref-warmup", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    rank, world, local = rank_env()
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    os.environ.setdefault("DFPCA_DEVICE", str(local))
+
+    from paper_1510_04439_b200 import _lib, api
+    sd = make_data(seed=20260815 + rank)
+    grid = sd.grid()
+    h = api.Bandwidth(sd.h)
+    G = grid.size()
+    G2 = G * G
+    data = sd.dataset()
+
+    binned = api.linear_bin(data, grid, api.BinOptions(True, True))
+    mean = api.fft_local_linear(binned, grid, h, api.MomentTarget.Mean)
+
+    # L2 flush buffer (> 126 MB L2) written between timed steps through torch
+    import torch
+    dev = torch.device("cuda", local)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB
+
+    def one_step():
+        cov = api.fft_covariance(binned, grid, h, mean)
+        return _lib.stage_ms("total"), cov
+
+    for _ in range(args.warmup):
+        one_step()
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+
+    launches0 = _lib.kernel_launches()
+    dev_ms = []
+    stage_acc = {}
+    barrier()
+    with ClockSampler(local) as clk:
+        wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize(dev)
+            ms, cov = one_step()
+            dev_ms.append(ms)
+            for st in ("pairs", "moments", "solve", "fallback", "center"):
+                stage_acc[st] = stage_acc.get(st, 0.0) + _lib.stage_ms(st)
+            del cov
+        wall = time.perf_counter() - wall0
+    barrier()
+    launches = _lib.kernel_launches() - launches0
+    t_step = float(np.sum(dev_ms)) / args.steps / 1e3
+    if dist is not None:
+        tt = torch.tensor([t_step], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step = float(tt.item())
+    value = world * G2 / t_step
+
+    # ---- per-kernel profile pass (outside the timed region) ----
+    _lib.profile(True)
+    one_step()
+    kstats = _lib.kernel_stats()
+    _lib.profile(False)
+
+    # ---- e2e through the public API with pinned host buffers ----
+    offsets, coords, values = data.csr()
+    host_cov = np.empty(G2)
+    pinned = [_lib.pin(a) for a in (offsets, coords, values, host_cov)]
+    e2e_t = []
+    for it in range(args.e2e_steps + 1):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        b2 = api.linear_bin(data, grid, api.BinOptions(True, True))
+        m2 = api.fft_local_linear(b2, grid, h, api.MomentTarget.Mean)
+        c2 = api.fft_covariance(b2, grid, h, m2)
+        _lib.check(_lib.lib().dfpca_surface_download(_lib.ctx(), c2.device_handle(),
+                                                     host_cov.ctypes.data_as(_lib.PD)))
+        t1 = time.perf_counter()
+        if it > 0:
+            e2e_t.append(t1 - t0)
+        del b2, m2, c2
+    e2e_step = float(np.mean(e2e_t))
+    if dist is not None:
+        tt = torch.tensor([e2e_step], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_step = float(tt.item())
+    h2d = offsets.nbytes + coords.nbytes + values.nbytes
+    d2h = host_cov.nbytes
+
+    # ---- full FPCA pipeline once (host obs -> EigenSystem on host) ----
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    b3 = api.linear_bin(data, grid, api.BinOptions(True, True))
+    m3 = api.fft_local_linear(b3, grid, h, api.MomentTarget.Mean)
+    api.fft_local_linear(b3, grid, h, api.MomentTarget.Squares)
+    c3 = api.fft_covariance(b3, grid, h, m3)
+    eig = api.randomized_eig(api.matrixize(c3), 99, 20, grid, 20260815)
+    fpca_ms = (time.perf_counter() - t0) * 1e3
+    eig_ms = _lib.stage_ms("eigen")
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel ----
+    roof = roofline(kstats, G, binned)
+
+    # ---- CPU baseline (reference, rank 0, N = 1) ----
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            ref_args = argparse.Namespace(**vars(args))
+            ref_args.ref_steps, ref_args.ref_warmup = 1, 0
+            line = run_reference(ref_args, emit=False)
+            cpu = line["cpu_baseline"] if line else None
+        except Exception as e:  # oracle missing on this box
+            cpu = {"value": None, "unit": "gridpts/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "gridpts/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "grid": [CELLS, CELLS], "n_subjects": N_SUBJ, "h": H,
+                   "gridpts": G2, "l2": "flushed (256 MB write) before every timed step",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "stages_ms_per_step": {k: v / args.steps for k, v in stage_acc.items()},
+        "wall_ms_per_step": wall / args.steps * 1e3,
+        "e2e": {"value": world * G2 / e2e_step, "unit": "gridpts/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_step * 1e3,
+                "path": "pinned host obs -> linear_bin -> fft_local_linear -> fft_covariance -> host covariance",
+                "pinned": all(pinned)},
+        "fpca_e2e_ms": fpca_ms, "eigen_ms": eig_ms, "eig_top3": eig.eigenvalues[:3],
+        "gpu_launches": int(launches),
+        "kernels": {k: {"ms": v[0], "launches": v[1]} for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][0])},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def roofline(kstats, G, binned):
+    """Dominant kernel of the step against its bound.
+
+    Algorithmic work:
+      k_gemm_tn (pair-grid SYRK, FP64 DMMA): 2 * n_pair * G^2 / 2 flops per grid
+          (upper tile triangle computed, mirrored) -> tensor (FP64) bound;
+      k_pass_* (one axis pass): (inputs + outputs) * 8 B per point of the chunk;
+      k_solve (per-node solve): (nm + nl + 1) * 8 B per point -> HBM bound.
+    """
+    peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
+    hbm = peaks.get("hbm_gbs")
+    if not kstats:
+        return None
+    name, (ms, cnt) = max(kstats.items(), key=lambda kv: kv[1][0])
+    per_launch_s = ms / cnt / 1e3
+    G2 = G * G
+    if name.startswith("k_gemm_tn"):
+        # launches in a step: pv SYRK (+ pw SYRK unless the masses are shared)
+        n_pair = 2000
+        flops_per_launch = 2.0 * n_pair * G2 / 2.0 * (1.0 + 1.0 / (G // 128))  # upper triangle incl. diagonal tiles
+        achieved = flops_per_launch / per_launch_s / 1e12
+        return {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                "peak_source": "measured FP64 DMMA peak (tools/fp64_peak.cu)",
+                "launch_ms": per_launch_s * 1e3, "share_of_step": None}
+    if name.startswith("k_solve"):
+        byts = (15 + 5 + 1) * 8.0 * G2 / cnt
+    else:
+        byts = None
+    achieved = byts / per_launch_s / 1e9 if byts else None
+    return {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": (achieved / hbm) if (achieved and hbm) else None, "traffic": None,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs", "launch_ms": per_launch_s * 1e3}
+
+
+if __name__ == "__main__":
+    main()

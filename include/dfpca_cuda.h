@@ -80,6 +80,15 @@ DFPCA_API int dfpca_last_error_location(const dfpca_context* ctx, int64_t* sampl
 DFPCA_API int dfpca_stage_time(const dfpca_context* ctx, const char* stage, double* ms);
 /* Number of kernels this context has launched since creation. */
 DFPCA_API int64_t dfpca_kernel_launches(const dfpca_context* ctx);
+/* Profiling mode: bracket every launch with CUDA events on the launching
+ * stream and accumulate device time per kernel name (resets the table). */
+DFPCA_API int dfpca_profile_enable(dfpca_context* ctx, int on);
+/* index-th entry of the per-kernel table: name, total ms, launch count. */
+DFPCA_API int dfpca_kernel_stat(const dfpca_context* ctx, int64_t index, const char** name, double* ms,
+                                int64_t* count);
+/* Page-lock host memory for the H2D/D2H copies (cudaHostRegister). */
+DFPCA_API int dfpca_host_register(void* ptr, int64_t bytes);
+DFPCA_API int dfpca_host_unregister(void* ptr);
 
 /* ---- binning: replaces dfpca::linear_bin (binning.hpp:82-183) ------------ */
 /* Observations in CSR form: sample i owns observations

@@ -38,6 +38,10 @@ SIGNATURES = [
     ("dfpca_last_error_location", C.c_int, [P, PI64, PI64]),
     ("dfpca_stage_time", C.c_int, [P, C.c_char_p, PD]),
     ("dfpca_kernel_launches", C.c_int64, [P]),
+    ("dfpca_profile_enable", C.c_int, [P, C.c_int]),
+    ("dfpca_kernel_stat", C.c_int, [P, C.c_int64, C.POINTER(C.c_char_p), PD, PI64]),
+    ("dfpca_host_register", C.c_int, [P, C.c_int64]),
+    ("dfpca_host_unregister", C.c_int, [P]),
     ("dfpca_linear_bin", C.c_int, [P, C.POINTER(DfpcaGrid), C.c_int64, PI64, PD, PD, C.c_int, C.c_int,
                                    C.POINTER(P)]),
     ("dfpca_binned_info", C.c_int, [P, PI64, PI64, PI64, PI64, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
@@ -136,3 +140,28 @@ def stage_ms(stage: str) -> float:
 
 def kernel_launches() -> int:
     return int(lib().dfpca_kernel_launches(ctx()))
+
+
+def profile(on: bool):
+    lib().dfpca_profile_enable(ctx(), int(on))
+
+
+def kernel_stats() -> dict:
+    out = {}
+    i = 0
+    while True:
+        name, ms, cnt = C.c_char_p(), C.c_double(), C.c_int64()
+        if lib().dfpca_kernel_stat(ctx(), i, C.byref(name), C.byref(ms), C.byref(cnt)) != 0:
+            break
+        out[name.value.decode()] = (ms.value, cnt.value)
+        i += 1
+    return out
+
+
+def pin(arr) -> bool:
+    """Page-lock a numpy array's buffer (for pinned H2D/D2H copies)."""
+    return lib().dfpca_host_register(arr.ctypes.data, arr.nbytes) == 0
+
+
+def unpin(arr):
+    lib().dfpca_host_unregister(arr.ctypes.data)

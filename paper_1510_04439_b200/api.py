@@ -238,9 +238,28 @@ class Sample:
 
 @dataclass
 class FunctionalDataset:
-    """dataset.hpp:36-71."""
+    """dataset.hpp:36-71.  csr() is cached until `samples` is rebound or
+    changes length; call invalidate() after editing samples in place."""
     dim: int = 0
     samples: list = field(default_factory=list)
+    _csr: tuple = field(default=None, repr=False, compare=False)
+    _csr_key: tuple = field(default=None, repr=False, compare=False)
+
+    def invalidate(self):
+        self._csr = None
+
+    @staticmethod
+    def from_csr(dim: int, offsets, coords, values, ids=None) -> "FunctionalDataset":
+        offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        coords = np.ascontiguousarray(coords, dtype=np.float64)
+        values = np.ascontiguousarray(values, dtype=np.float64)
+        n = offsets.size - 1
+        samples = [Sample(ids[i] if ids else str(i), coords[offsets[i] * dim:offsets[i + 1] * dim],
+                          values[offsets[i]:offsets[i + 1]]) for i in range(n)]
+        d = FunctionalDataset(dim, samples)
+        d._csr = (offsets, coords, values)
+        d._csr_key = (id(d.samples), len(d.samples))
+        return d
 
     def n_samples(self) -> int:
         return len(self.samples)
@@ -250,6 +269,9 @@ class FunctionalDataset:
 
     def csr(self):
         """(offsets int64[n+1], coords f64[N*dim], values f64[N])"""
+        key = (id(self.samples), len(self.samples))
+        if self._csr is not None and self._csr_key == key:
+            return self._csr
         n = len(self.samples)
         counts = np.fromiter((s.n_obs() for s in self.samples), dtype=np.int64, count=n)
         offsets = np.zeros(n + 1, dtype=np.int64)
@@ -260,7 +282,9 @@ class FunctionalDataset:
         else:
             coords = np.zeros(0)
             values = np.zeros(0)
-        return offsets, np.ascontiguousarray(coords), np.ascontiguousarray(values)
+        self._csr = (offsets, np.ascontiguousarray(coords), np.ascontiguousarray(values))
+        self._csr_key = key
+        return self._csr
 
 
 @dataclass

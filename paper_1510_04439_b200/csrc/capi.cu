@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstring>
 #include <exception>
+#include <iterator>
 #include <new>
 #include <string>
 #include <vector>
@@ -11,6 +12,8 @@
 #include "common.cuh"
 
 namespace dfpca_gpu {
+
+thread_local cudaStream_t g_alloc_stream = nullptr;
 
 dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples,
                              const i64* obs_offsets, const double* coords, const double* values,
@@ -199,8 +202,32 @@ void dfpca_context::end_stage() {
       return;
     }
 }
+int dfpca_context::kernel_begin(const char* name) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, stream);
+  std::string n(name);
+  if (!n.empty() && n.front() == '(') n = n.substr(1);
+  const auto p = n.find('<');  // strip template arguments for grouping
+  kernel_marks.push_back({n.substr(0, p == std::string::npos ? n.size() : p), {a, b}});
+  return static_cast<int>(kernel_marks.size()) - 1;
+}
+void dfpca_context::kernel_end(int slot) { cudaEventRecord(kernel_marks[static_cast<std::size_t>(slot)].second.second, stream); }
+
 void dfpca_context::collect_stages() {
   cudaStreamSynchronize(stream);
+  for (auto& km : kernel_marks) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, km.second.first, km.second.second) == cudaSuccess) {
+      auto& st = kernel_stats[km.first];
+      st.ms += ms;
+      st.count += 1;
+    }
+    cudaEventDestroy(km.second.first);
+    cudaEventDestroy(km.second.second);
+  }
+  kernel_marks.clear();
   for (auto& m : marks) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, m.start, m.stop) == cudaSuccess) {
@@ -220,9 +247,16 @@ int guarded(dfpca_context* ctx, F&& f) {
   if (!ctx) return kConfig;
   ctx->err = Failure{};
   ctx->stage_ms.clear();
+  struct StreamScope {
+    cudaStream_t prev;
+    explicit StreamScope(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
+    ~StreamScope() { g_alloc_stream = prev; }
+  } scope(ctx->stream);
   try {
     DFPCA_CUDA(cudaSetDevice(ctx->device));
+    ctx->begin_stage("total");
     f();
+    ctx->end_stage();
     ctx->collect_stages();
     return 0;
   } catch (const Failure& e) {
@@ -240,6 +274,11 @@ int guarded(dfpca_context* ctx, F&& f) {
     cudaEventDestroy(m.stop);
   }
   ctx->marks.clear();
+  for (auto& km : ctx->kernel_marks) {
+    cudaEventDestroy(km.second.first);
+    cudaEventDestroy(km.second.second);
+  }
+  ctx->kernel_marks.clear();
   return ctx->err.cls;
 }
 
@@ -259,6 +298,11 @@ int dfpca_context_create(int device, dfpca_context** out) {
     return kNumeric;
   }
   cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    std::uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   *out = ctx;
   return 0;
 }
@@ -267,7 +311,12 @@ int dfpca_context_destroy(dfpca_context* ctx) {
   if (!ctx) return 0;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  ctx->scratch.release();
+  {
+    g_alloc_stream = ctx->stream;
+    ctx->scratch.release();
+    cudaStreamSynchronize(ctx->stream);
+    g_alloc_stream = nullptr;
+  }
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return 0;
@@ -296,6 +345,36 @@ int dfpca_stage_time(const dfpca_context* ctx, const char* stage, double* ms) {
 }
 
 int64_t dfpca_kernel_launches(const dfpca_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int dfpca_profile_enable(dfpca_context* ctx, int on) {
+  if (!ctx) return kConfig;
+  ctx->profile = on != 0;
+  ctx->kernel_stats.clear();
+  return 0;
+}
+
+int dfpca_kernel_stat(const dfpca_context* ctx, int64_t index, const char** name, double* ms,
+                      int64_t* count) {
+  if (!ctx) return kConfig;
+  if (index < 0 || index >= static_cast<int64_t>(ctx->kernel_stats.size())) return kConfig;
+  auto it = ctx->kernel_stats.begin();
+  std::advance(it, index);
+  if (name) *name = it->first.c_str();
+  if (ms) *ms = it->second.ms;
+  if (count) *count = it->second.count;
+  return 0;
+}
+
+int dfpca_host_register(void* ptr, int64_t bytes) {
+  if (!ptr || bytes <= 0) return kConfig;
+  return cudaHostRegister(ptr, static_cast<std::size_t>(bytes), cudaHostRegisterDefault) == cudaSuccess ? 0
+                                                                                                           : kNumeric;
+}
+
+int dfpca_host_unregister(void* ptr) {
+  if (!ptr) return kConfig;
+  return cudaHostUnregister(ptr) == cudaSuccess ? 0 : kNumeric;
+}
 
 int dfpca_linear_bin(dfpca_context* ctx, const dfpca_grid* grid, int64_t n_samples,
                      const int64_t* obs_offsets, const double* coords, const double* values,

@@ -29,4 +29,22 @@ struct PassSpec {
 
 void run_pass(dfpca_context* ctx, const PassSpec& spec, double* taps_dev_scratch);
 
+// Fused t-phase of the 2-d covariance (two trailing axes t1, t2): per pair-grid
+// row, both axis passes run in shared memory and only the 9 t-partials reach
+// HBM.  mass_out[i] receives t-orders (a1, a2) in the order
+// (0,0) (1,0) (2,0) (0,1) (1,1) (0,2); value_out: (0,0) (1,0) (0,1).
+// taps[axis][order] point at 2R+1 host doubles (axis 0 = t1, 1 = t2).
+struct TPhase2Spec {
+  const double* pw;
+  const double* pv;
+  i64 rows;      // pair-grid rows (s nodes) in this call
+  i64 n1, n2;    // t-plane shape
+  double* mass_out[6];
+  double* value_out[3];
+  const double* taps[2][3];
+  int R[2];
+};
+// Returns false when the plane does not fit (caller uses run_pass instead).
+bool run_tphase2(dfpca_context* ctx, const TPhase2Spec& spec);
+
 }  // namespace dfpca_gpu

@@ -1,15 +1,18 @@
-// FP64 GEMM on the DMMA tensor pipe (mma.sync.m8n8k4.f64 -> SASS DMMA.8).
+// FP64 GEMM on the DMMA tensor pipe (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4).
 //
 // tcgen05 has no f64 kind, so FP64 tensor math on sm_100a is the warp-level
-// DMMA path; measured on this pool's B200 it peaks at ~37 TFLOP/s, the same
-// as DFMA, but it moves 4x fewer operand bytes per FMA through registers and
-// shared memory, which is what lets a tile reach that peak.
+// DMMA path; measured on this pool's B200 it peaks at ~37 TFLOP/s (the DFMA
+// rate as well, tools/fp64_peak.cu), and it moves 4x fewer operand bytes per
+// FMA through registers than DFMA, which is what lets a tile reach that peak.
 //
-// CTA tile 128 x 128, K staged 16 at a time through double-buffered shared
-// memory; 8 warps, each owning a 64 x 32 block = 8 x 4 DMMA tiles of 8 x 8.
-// Operand rows are padded to 132 doubles so the k-strided fragment loads of
-// one warp spread over all 32 banks.
+// CTA tile 128 x 128, 16 warps each owning a 32 x 32 block (4 x 4 DMMA tiles),
+// so 4 warps per scheduler hide the fragment-load latency.  K is staged 16 at
+// a time through a 3-deep cp.async (LDGSTS) ring in shared memory, rows padded
+// to 132 doubles so one warp's k-strided fragment loads spread over all banks.
+// Per-row weights (the pair weights of the SYRK) are applied by a separate
+// scaling pass so the operand copies stay asynchronous.
 #include <algorithm>
+#include <cstdint>
 
 #include "gemm.cuh"
 
@@ -18,8 +21,11 @@ namespace {
 
 constexpr int BM = 128, BN = 128, BK = 16;
 constexpr int LDS = 132;
-constexpr int WM = 64, WN = 32;
+constexpr int WM = 32, WN = 32;
 constexpr int MT = WM / 8, NT = WN / 8;
+constexpr int NTHREADS = 512;
+constexpr int STAGES = 3;
+constexpr int STAGE_DOUBLES = 2 * BK * LDS;  // A and B tiles
 
 __device__ inline void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -27,19 +33,31 @@ __device__ inline void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(256, 1)
-    k_gemm_tn(i64 M, i64 N, i64 K, const double* __restrict__ A, i64 lda,
-              const double* __restrict__ w, const double* __restrict__ B, i64 ldb,
-              double* __restrict__ C, i64 ldc, int symmetric, i64 tiles_n, i64 k_chunk,
+__device__ inline void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ inline void cp_async8(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ inline void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ inline void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// VEC: doubles per cp.async (2 when every row start is 16-byte aligned).
+template <int VEC>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_gemm_tn(i64 M, i64 N, i64 K, const double* __restrict__ A, i64 lda, const double* __restrict__ B,
+              i64 ldb, double* __restrict__ C, i64 ldc, int symmetric, i64 tiles_n, i64 k_chunk,
               i64 split_stride) {
-  extern __shared__ double smem[];
-  double* As = smem;                  // [2][BK][LDS]
-  double* Bs = smem + 2 * BK * LDS;   // [2][BK][LDS]
+  extern __shared__ __align__(16) double smem[];
 
   i64 tm, tn;
   if (symmetric) {
-    // enumerate upper-triangular tile pairs (tm <= tn)
-    i64 t = blockIdx.x;
+    i64 t = blockIdx.x;  // upper-triangular tile pairs (tm <= tn)
     tm = 0;
     while (t >= tiles_n - tm) {
       t -= tiles_n - tm;
@@ -51,41 +69,38 @@ __global__ void __launch_bounds__(256, 1)
     tn = blockIdx.x % tiles_n;
   }
   const i64 m0 = tm * BM, n0 = tn * BN;
-  // split-K: blockIdx.y owns K range [k_begin, k_end) and its own C slab
   const i64 k_begin = blockIdx.y * k_chunk;
   const i64 k_end = (k_begin + k_chunk < K) ? k_begin + k_chunk : K;
   C += blockIdx.y * split_stride;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm0 = (warp / 4) * WM, wn0 = (warp % 4) * WN;
 
-  // Global -> register staging: each thread moves 8 doubles of A and of B per
-  // stage (BK * BM / 256), as rows of 128 consecutive doubles.
-  double ra[8], rb[8];
-  auto load_stage = [&](i64 k0) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int e = tid + q * 256;
-      const int kr = e / BM, c = e % BM;
+  // Stage loader: BK rows x 128 doubles of A and of B, VEC doubles per copy;
+  // out-of-range elements are zero-filled by the copy's src-size operand.
+  auto load_stage = [&](int slot, i64 k0) {
+    double* As = smem + slot * STAGE_DOUBLES;
+    double* Bs = As + BK * LDS;
+    constexpr int per_row = BM / VEC;
+    for (int e = tid; e < BK * per_row; e += NTHREADS) {
+      const int kr = e / per_row, c = (e % per_row) * VEC;
       const i64 k = k0 + kr;
-      double av = 0.0, bv = 0.0;
-      if (k < k_end) {
-        if (m0 + c < M) {
-          av = A[k * lda + m0 + c];
-          if (w) av = __dmul_rn(w[k], av);
-        }
-        if (n0 + c < N) bv = B[k * ldb + n0 + c];
+      const bool krow = k < k_end;
+      {
+        const i64 col = m0 + c;
+        const i64 avail = krow ? (M - col) : 0;
+        const int bytes = avail >= VEC ? 8 * VEC : (avail > 0 ? 8 * static_cast<int>(avail) : 0);
+        const double* src = bytes ? A + k * lda + col : A;
+        if (VEC == 2) cp_async16(As + kr * LDS + c, src, bytes);
+        else cp_async8(As + kr * LDS + c, src, bytes);
       }
-      ra[q] = av;
-      rb[q] = bv;
-    }
-  };
-  auto store_stage = [&](int buf) {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int e = tid + q * 256;
-      const int kr = e / BM, c = e % BM;
-      As[(buf * BK + kr) * LDS + c] = ra[q];
-      Bs[(buf * BK + kr) * LDS + c] = rb[q];
+      {
+        const i64 col = n0 + c;
+        const i64 avail = krow ? (N - col) : 0;
+        const int bytes = avail >= VEC ? 8 * VEC : (avail > 0 ? 8 * static_cast<int>(avail) : 0);
+        const double* src = bytes ? B + k * ldb + col : B;
+        if (VEC == 2) cp_async16(Bs + kr * LDS + c, src, bytes);
+        else cp_async8(Bs + kr * LDS + c, src, bytes);
+      }
     }
   };
 
@@ -96,14 +111,20 @@ __global__ void __launch_bounds__(256, 1)
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const i64 nk = (k_end - k_begin + BK - 1) / BK;
-  load_stage(k_begin);
-  store_stage(0);
-  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, k_begin + s * BK);
+    cp_async_commit();
+  }
   for (i64 kb = 0; kb < nk; ++kb) {
-    const int buf = kb & 1;
-    if (kb + 1 < nk) load_stage(k_begin + (kb + 1) * BK);
-    const double* as = As + buf * BK * LDS;
-    const double* bs = Bs + buf * BK * LDS;
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    // prefetch stage kb + STAGES - 1 into the slot freed at kb - 1
+    const i64 pf = kb + STAGES - 1;
+    if (pf < nk) load_stage(static_cast<int>(pf % STAGES), k_begin + pf * BK);
+    cp_async_commit();
+    const double* as = smem + (kb % STAGES) * STAGE_DOUBLES;
+    const double* bs = as + BK * LDS;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       const int kr = kk + (lane & 3);
@@ -117,9 +138,8 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int j = 0; j < NT; ++j) dmma(acc[i][j], af[i], bf[j]);
     }
-    if (kb + 1 < nk) store_stage(buf ^ 1);
-    __syncthreads();
   }
+  cp_async_wait<0>();
 
   // Epilogue: fragment (i, j) holds C[row][col], C[row][col + 1].
 #pragma unroll
@@ -131,11 +151,9 @@ __global__ void __launch_bounds__(256, 1)
       if (row < M) {
         if (col + 1 < N && (ldc % 2) == 0) {
           *reinterpret_cast<double2*>(C + row * ldc + col) = make_double2(acc[i][j][0], acc[i][j][1]);
-        } else if (col + 1 < N) {
-          C[row * ldc + col] = acc[i][j][0];
-          C[row * ldc + col + 1] = acc[i][j][1];
-        } else if (col < N) {
-          C[row * ldc + col] = acc[i][j][0];
+        } else {
+          if (col < N) C[row * ldc + col] = acc[i][j][0];
+          if (col + 1 < N) C[row * ldc + col + 1] = acc[i][j][1];
         }
       }
       if (symmetric && tm != tn && row < M) {
@@ -159,45 +177,79 @@ __global__ void k_splitk_reduce(const double* __restrict__ ws, i64 splits, i64 M
   }
 }
 
+// out[k][m] = w[k] * in[k][m]  (rounded product, as the reference's pw * m).
+__global__ void k_scale_rows(const double* __restrict__ in, const double* __restrict__ w, i64 K, i64 M,
+                             i64 ld, double* __restrict__ out) {
+  const i64 total = K * M;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
+       e += (i64)gridDim.x * blockDim.x) {
+    const i64 k = e / M, m = e % M;
+    out[k * M + m] = __dmul_rn(w[k], in[k * ld + m]);
+  }
+}
+
+template <int VEC>
+void launch(dfpca_context* ctx, dim3 grid, std::size_t smem, i64 M, i64 N, i64 K, const double* A, i64 lda,
+            const double* B, i64 ldb, double* C, i64 ldc, int symmetric, i64 tiles_n, i64 k_chunk,
+            i64 split_stride) {
+  static bool attr = false;
+  if (!attr) {
+    DFPCA_CUDA(cudaFuncSetAttribute(k_gemm_tn<VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+    attr = true;
+  }
+  DFPCA_LAUNCH(ctx, k_gemm_tn<VEC>, grid, NTHREADS, smem, M, N, K, A, lda, B, ldb, C, ldc, symmetric,
+               tiles_n, k_chunk, split_stride);
+}
+
 }  // namespace
 
 void gemm_tn(dfpca_context* ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, const double* w,
              const double* B, i64 ldb, double* C, i64 ldc, bool symmetric) {
   if (M <= 0 || N <= 0) return;
-  const i64 tiles_m = (M + BM - 1) / BM;
-  const i64 tiles_n = (N + BN - 1) / BN;
-  const std::size_t smem = sizeof(double) * 4 * BK * LDS;  // 67.6 KB
-  static bool attr_set = false;
-  if (!attr_set) {
-    DFPCA_CUDA(cudaFuncSetAttribute(k_gemm_tn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-    attr_set = true;
-  }
-  const i64 blocks = symmetric ? tiles_m * (tiles_m + 1) / 2 : tiles_m * tiles_n;
   if (K <= 0) {
     for (i64 r = 0; r < M; ++r)
       DFPCA_CUDA(cudaMemsetAsync(C + r * ldc, 0, sizeof(double) * N, ctx->stream));
     return;
   }
+  DevBuf<double> scaled;
+  if (w) {
+    scaled.alloc(static_cast<std::size_t>(K * M));
+    DFPCA_LAUNCH(ctx, k_scale_rows, grid_for(K * M, 256), 256, 0, A, w, K, M, lda, scaled.get());
+    A = scaled.get();
+    lda = M;
+  }
+  const i64 tiles_m = (M + BM - 1) / BM;
+  const i64 tiles_n = (N + BN - 1) / BN;
+  const std::size_t smem = sizeof(double) * STAGES * STAGE_DOUBLES;  // 101 KB
+  const bool vec2 = (lda % 2 == 0) && (ldb % 2 == 0) && (reinterpret_cast<std::uintptr_t>(A) % 16 == 0) &&
+                    (reinterpret_cast<std::uintptr_t>(B) % 16 == 0);
+  const i64 blocks = symmetric ? tiles_m * (tiles_m + 1) / 2 : tiles_m * tiles_n;
   // Skinny products (the projection GEMMs) get a deterministic split-K so the
-  // grid covers the 148 SMs.
+  // grid covers the SMs.
   i64 splits = 1;
   if (!symmetric && blocks < 2 * ctx->sm_count && K >= 1024) {
     splits = std::min<i64>((2 * ctx->sm_count + blocks - 1) / blocks, K / 256);
     splits = std::max<i64>(splits, 1);
   }
-  if (splits == 1) {
-    DFPCA_LAUNCH(ctx, k_gemm_tn, dim3(static_cast<unsigned>(blocks), 1), 256, smem, M, N, K, A, lda,
-                 w, B, ldb, C, ldc, symmetric ? 1 : 0, tiles_n, K, (i64)0);
-    return;
+  i64 k_chunk = K;
+  double* out = C;
+  i64 ldo = ldc, stride = 0;
+  if (splits > 1) {
+    k_chunk = (K + splits - 1) / splits;
+    k_chunk = (k_chunk + BK - 1) / BK * BK;
+    splits = (K + k_chunk - 1) / k_chunk;
+    out = reinterpret_cast<double*>(ctx->scratch_bytes(sizeof(double) * splits * M * N));
+    ldo = N;
+    stride = M * N;
   }
-  i64 k_chunk = (K + splits - 1) / splits;
-  k_chunk = (k_chunk + BK - 1) / BK * BK;
-  splits = (K + k_chunk - 1) / k_chunk;
-  double* ws = reinterpret_cast<double*>(ctx->scratch_bytes(sizeof(double) * splits * M * N));
-  DFPCA_LAUNCH(ctx, k_gemm_tn, dim3(static_cast<unsigned>(blocks), static_cast<unsigned>(splits)), 256,
-               smem, M, N, K, A, lda, w, B, ldb, ws, N, 0, tiles_n, k_chunk, M * N);
-  DFPCA_LAUNCH(ctx, k_splitk_reduce, grid_for(M * N, 256), 256, 0, ws, splits, M, N, C, ldc);
+  const dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(splits));
+  if (vec2)
+    launch<2>(ctx, grid, smem, M, N, K, A, lda, B, ldb, out, ldo, symmetric ? 1 : 0, tiles_n, k_chunk, stride);
+  else
+    launch<1>(ctx, grid, smem, M, N, K, A, lda, B, ldb, out, ldo, symmetric ? 1 : 0, tiles_n, k_chunk, stride);
+  if (splits > 1)
+    DFPCA_LAUNCH(ctx, k_splitk_reduce, grid_for(M * N, 256), 256, 0, out, splits, M, N, C, ldc);
 }
 
 }  // namespace dfpca_gpu

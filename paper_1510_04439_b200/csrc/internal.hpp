@@ -33,6 +33,11 @@ void cuda_check(cudaError_t e, const char* what);
 
 #define DFPCA_CUDA(call) ::dfpca_gpu::cuda_check((call), #call)
 
+// Stream the current API call runs on; device buffers are allocated and freed
+// stream-ordered on it (cudaMallocAsync from the device's default pool, whose
+// release threshold is raised at context creation so blocks are cached).
+extern thread_local cudaStream_t g_alloc_stream;
+
 // Move-only owning device array.
 template <class T>
 class DevBuf {
@@ -51,11 +56,11 @@ class DevBuf {
     if (n == n_ && p_) return;
     release();
     if (n == 0) return;
-    DFPCA_CUDA(cudaMalloc(reinterpret_cast<void**>(&p_), n * sizeof(T)));
+    DFPCA_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), g_alloc_stream));
     n_ = n;
   }
   void release() {
-    if (p_) cudaFree(p_);
+    if (p_) cudaFreeAsync(p_, g_alloc_stream);
     p_ = nullptr;
     n_ = 0;
   }
@@ -131,6 +136,17 @@ struct dfpca_context {
   void begin_stage(const std::string& name);
   void end_stage();
   void collect_stages();  // after a stream sync
+
+  // Per-kernel device timing (profiling mode).
+  struct KernelStat {
+    double ms = 0.0;
+    std::int64_t count = 0;
+  };
+  bool profile = false;
+  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> kernel_marks;
+  std::map<std::string, KernelStat> kernel_stats;
+  int kernel_begin(const char* name);
+  void kernel_end(int slot);
 };
 
 struct dfpca_binned {

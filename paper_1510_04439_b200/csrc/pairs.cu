@@ -12,7 +12,7 @@
 // "sample sum minus band", and for pairs that only share one observation the
 // two sums are identical sequences, so the reference gets an exact 0 there
 // (which later decides whether a kernel window is empty).  A reordered SYRK
-// would leave +-1 ulp there.  k_band_exact therefore recomputes every entry
+// would leave +-1 ulp there.  k_band_fix therefore recomputes every pw entry
 // with a nonzero band in the reference order -- samples ascending, separate
 // multiply and add, (w_i M_i(s)) M_i(t) (fft_smoother.hpp:397-402) -- and
 // subtracts the band once (:433-434), making those entries bit-identical.
@@ -32,19 +32,27 @@ __global__ void k_rank_one(double* __restrict__ pw, const double* __restrict__ m
   }
 }
 
-// One thread per band entry (u, code) whose band value is nonzero.
-__global__ void k_band_exact(const double* __restrict__ diag_mass, const double* __restrict__ diag_value,
-                             i64 G, int d, i64 codes, DevGrid g, const double* __restrict__ ps_mass,
-                             const double* __restrict__ ps_value, const double* __restrict__ w,
-                             i64 n_pair, double* __restrict__ pw, double* __restrict__ pv) {
+// Band fix-up, one warp per band entry (u, code) with a nonzero band.
+//  * pw: recomputed exactly in the reference order and minus the band, so the
+//    near-diagonal cancellations that decide empty windows are bit-identical.
+//    The lanes form the per-sample products (w_i M_i(s)) M_i(t) of 32
+//    consecutive samples in parallel (one rounded multiply pair each, as in
+//    the reference) and lane 0 adds them in ascending sample order.  With a
+//    shared mass grid (identical_mass) M_i(s) = M(s) for every i.
+//  * pv: only the band subtraction (pv never decides emptiness; the SYRK sum
+//    differs from the reference's by reassociation only).
+__global__ void k_band_fix(const double* __restrict__ diag_mass, const double* __restrict__ diag_value,
+                           i64 G, int d, i64 codes, DevGrid g, const double* __restrict__ ps_mass,
+                           int identical, const double* __restrict__ w, i64 n_pair, double* __restrict__ pw,
+                           double* __restrict__ pv) {
+  const int lane = threadIdx.x & 31;
+  const i64 warps = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
   const i64 total = G * codes;
-  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
-       e += (i64)gridDim.x * blockDim.x) {
+  for (i64 e = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5; e < total; e += warps) {
     const double dm = diag_mass[e], dv = diag_value[e];
     if (dm == 0.0 && dv == 0.0) continue;
     const i64 u = e / codes;
     i64 code = e % codes;
-    // decode offsets (last axis fastest) and the partner node
     int off[kMaxDim];
     for (int k = d - 1; k >= 0; --k) {
       off[k] = static_cast<int>(code % 3) - 1;
@@ -60,15 +68,23 @@ __global__ void k_band_exact(const double* __restrict__ diag_mass, const double*
       t += bk * g.strides[k];
     }
     if (!inside) continue;
-    double sw = 0.0, sv = 0.0;
-    for (i64 i = 0; i < n_pair; ++i) {
-      const double ma = ps_mass[i * G + u], mb = ps_mass[i * G + t];
-      const double va = ps_value[i * G + u], vb = ps_value[i * G + t];
-      sw = __dadd_rn(sw, __dmul_rn(__dmul_rn(w[i], ma), mb));
-      sv = __dadd_rn(sv, __dmul_rn(__dmul_rn(w[i], va), vb));
+    double sw = 0.0;
+    const double ms0 = identical ? ps_mass[u] : 0.0, mt0 = identical ? ps_mass[t] : 0.0;
+    for (i64 i0 = 0; i0 < n_pair; i0 += 32) {
+      const i64 i = i0 + lane;
+      double pm = 0.0;
+      if (i < n_pair) {
+        const double ms = identical ? ms0 : ps_mass[i * G + u];
+        const double mt = identical ? mt0 : ps_mass[i * G + t];
+        pm = __dmul_rn(__dmul_rn(w[i], ms), mt);
+      }
+      const int cnt = n_pair - i0 < 32 ? static_cast<int>(n_pair - i0) : 32;
+      for (int q = 0; q < cnt; ++q) sw = __dadd_rn(sw, __shfl_sync(0xffffffffu, pm, q));
     }
-    pw[u * G + t] = __dsub_rn(sw, dm);
-    pv[u * G + t] = __dsub_rn(sv, dv);
+    if (lane == 0) {
+      pw[u * G + t] = __dsub_rn(sw, dm);
+      pv[u * G + t] = __dsub_rn(pv[u * G + t], dv);
+    }
   }
 }
 
@@ -95,9 +111,9 @@ void build_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, dou
   if (pw && pv) {
     DevBuf<double> axes;
     DevGrid dg = upload_grid_axes(ctx, b->grid, axes);
-    DFPCA_LAUNCH(ctx, k_band_exact, grid_for(G * b->codes, 128, 148ll * 32), 128, 0,
+    DFPCA_LAUNCH(ctx, k_band_fix, grid_for(G * b->codes * 32, 256, 148ll * 32), 256, 0,
                  b->diag_mass.get(), b->diag_value.get(), G, b->grid.d, b->codes, dg,
-                 b->ps_mass.get(), b->ps_value.get(), b->pair_weight.get(), n, pw, pv);
+                 b->ps_mass.get(), b->identical_mass ? 1 : 0, b->pair_weight.get(), n, pw, pv);
     DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
   }
 }

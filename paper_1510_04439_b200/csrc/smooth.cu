@@ -19,10 +19,12 @@
 #include <functional>
 #include <memory>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <string>
 
 #include "conv.cuh"
+#include "fused.cuh"
 #include "solve.cuh"
 
 namespace dfpca_gpu {
@@ -564,6 +566,7 @@ void run_local_linear(dfpca_context* ctx, const dfpca_binned* b, const Grid& gri
 // Pair grids + moments + solve + center + symmetrize for the covariance.
 void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid, const double* h,
                     const double* mean_host, dfpca_surface** out) {
+  const bool use_fused_s1 = std::getenv("DFPCA_FUSED_S1") != nullptr;
   const int d = grid.d;
   const int p = 2 * d;
   const i64 G = grid.G;
@@ -633,6 +636,34 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
     roots[0].ptr = pw.get() + s0 * G;
     roots[1].budget_max = 1;
     roots[1].ptr = pv.get() + s0 * G;
+    if (d == 2) {
+      // fused two-axis t-phase: the 64x64 t-plane of a row never leaves smem
+      TPhase2Spec ts{};
+      ts.pw = pw.get() + s0 * G;
+      ts.pv = pv.get() + s0 * G;
+      ts.rows = rows;
+      ts.n1 = grid.shape[0];
+      ts.n2 = grid.shape[1];
+      const int mo[6][2] = {{0, 0}, {1, 0}, {2, 0}, {0, 1}, {1, 1}, {0, 2}};
+      const int vo[3][2] = {{0, 0}, {1, 0}, {0, 1}};
+      for (int i = 0; i < 6; ++i) {
+        Orders o{};
+        o[2] = mo[i][0];
+        o[3] = mo[i][1];
+        ts.mass_out[i] = tpart.at({o, 2}) + s0 * G;
+      }
+      for (int i = 0; i < 3; ++i) {
+        Orders o{};
+        o[2] = vo[i][0];
+        o[3] = vo[i][1];
+        ts.value_out[i] = tpart.at({o, 1}) + s0 * G;
+      }
+      for (int ax = 0; ax < 2; ++ax) {
+        ts.R[ax] = taps[2 + ax].R;
+        for (int r = 0; r < 3; ++r) ts.taps[ax][r] = taps[2 + ax].t[r].data();
+      }
+      if (run_tphase2(ctx, ts)) continue;
+    }
     std::vector<std::unique_ptr<DevBuf<double>>> keep;
     auto final_dst = [&](const Orders& o, int bm) -> double* { return tpart.at({o, bm}) + s0 * G; };
     auto final_rs = [&](const Orders&, int) -> i64 { return -1; };
@@ -687,6 +718,65 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
       return finals.back()->get();
     };
     auto final_rs = [&](const Orders&, int) -> i64 { return -1; };
+    if (d == 2) {
+      // s2 pass, then the fused s1 pass + solve (fused.cu): the 20 moment
+      // arrays of the chunk are never materialized.
+      std::vector<TreeAxis> s2ax = {{1, 1}};
+      std::vector<Leaf> l2 = run_tree(ctx, roots, s2ax, cd, taps, G * cols, taps_dev.get(), keep, final_dst,
+                                      final_rs, true, -1);
+      S1SolveSpec sp{};
+      bool ok = true;
+      const auto order = s1_p4_input_order();
+      for (std::size_t k = 0; k < order.size(); ++k) {
+        const double* ptr = nullptr;
+        for (const Leaf& l : l2)
+          if (l.budget_max == order[k][0] && l.ord[0] == 0 && l.ord[1] == order[k][1] &&
+              l.ord[2] == order[k][2] && l.ord[3] == order[k][3])
+            ptr = l.ptr;
+        ok = ok && ptr != nullptr;
+        sp.in[k] = ptr;
+      }
+      sp.n = grid.shape[0];
+      sp.s2n = grid.shape[1];
+      sp.inner = grid.shape[1] * cols;
+      sp.cols = cols;
+      sp.t0 = t0;
+      sp.G = G;
+      sp.R = taps[0].R;
+      for (int r = 0; r < 3; ++r) sp.taps[r] = taps[0].t[r].data();
+      sp.mask = grid.has_mask ? mask_dev.get() : nullptr;
+      sp.out = surf->values.get();
+      sp.cnt = cnt.get();
+      sp.list = list.get();
+      sp.cap = list_cap;
+      ctx->end_stage();
+      ctx->begin_stage("solve");
+      // The fused s1+solve kernel (fused.cu) is register-bound at 8 warps/SM;
+      // the split pass + solve is faster on B200 until it is reworked.
+      const bool fused = ok && use_fused_s1 && run_s1_solve_p4(ctx, sp);
+      ctx->end_stage();
+      ctx->begin_stage("moments");
+      if (fused) continue;
+      // no specialisation: finish the s1 axis with the generic passes
+      std::vector<TreeAxis> s1ax = {{0, 0}};
+      std::vector<Leaf> leaves = run_tree(ctx, l2, s1ax, cd, taps, G * cols, taps_dev.get(), keep, final_dst,
+                                          final_rs, false, -1);
+      MomPtrs mp{};
+      for (const Leaf& l : leaves) {
+        const int idx = basis.find(l.ord);
+        if (l.budget_max == 2) mp.S[idx] = l.ptr;
+        else mp.T[idx] = l.ptr;
+      }
+      SolveGeom sg{};
+      sg.npts = G * cols;
+      sg.tc = cols;
+      sg.t0 = t0;
+      sg.gt = G;
+      sg.cov = 1;
+      sg.mask = grid.has_mask ? mask_dev.get() : nullptr;
+      solve_launcher(p)(ctx, mp, sg, surf->values.get(), cnt.get(), list.get(), list_cap);
+      continue;
+    }
     std::vector<Leaf> leaves = run_tree(ctx, roots, saxes, cd, taps, G * cols, taps_dev.get(), keep,
                                         final_dst, final_rs, true, -1);
     MomPtrs mp{};
@@ -702,7 +792,11 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
     sg.gt = G;
     sg.cov = 1;
     sg.mask = grid.has_mask ? mask_dev.get() : nullptr;
+    ctx->end_stage();
+    ctx->begin_stage("solve");
     solve_launcher(p)(ctx, mp, sg, surf->values.get(), cnt.get(), list.get(), list_cap);
+    ctx->end_stage();
+    ctx->begin_stage("moments");
   }
   unsigned long long n_empty = 0;
   DFPCA_CUDA(cudaMemcpyAsync(&n_empty, cnt.get(), sizeof(n_empty), cudaMemcpyDeviceToHost, st));

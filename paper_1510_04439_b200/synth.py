@@ -29,13 +29,8 @@ class SynthData:
         return self.offsets.size - 1
 
     def dataset(self):
-        from .api import FunctionalDataset, Sample
-        d = self.dim
-        samples = []
-        for i in range(self.n_samples):
-            a, b = int(self.offsets[i]), int(self.offsets[i + 1])
-            samples.append(Sample(str(i), self.coords[a * d:b * d], self.values[a:b]))
-        return FunctionalDataset(d, samples)
+        from .api import FunctionalDataset
+        return FunctionalDataset.from_csr(self.dim, self.offsets, self.coords, self.values)
 
     def grid(self):
         from .api import EvaluationGrid

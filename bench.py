@@ -320,39 +320,66 @@ def main():
         dist.destroy_process_group()
 
 
-def roofline(kstats, G, binned):
-    """Dominant kernel of the step against its bound.
+def kernel_model(G: int, n_pair: int):
+    """Algorithmic work per step of every kernel of the d = 2 covariance step
+    ('Roofline model').  Arrays are G^2 doubles (8 B per point).
 
-    Algorithmic work:
-      k_gemm_tn (pair-grid SYRK, FP64 DMMA): 2 * n_pair * G^2 / 2 flops per grid
-          (upper tile triangle computed, mirrored) -> tensor (FP64) bound;
-      k_pass_* (one axis pass): (inputs + outputs) * 8 B per point of the chunk;
-      k_solve (per-node solve): (nm + nl + 1) * 8 B per point -> HBM bound.
+    pairs   k_gemm_tn     SYRK of the pair-weighted value grids: n G^2 FMAs
+                          (symmetric half of 2 n G^2 flops)       -> FP64 tensor
+            k_rank_one    pw = W M(s) M(t): write 1 array         -> HBM
+            k_scale_rows  w_i V_i: read + write n G doubles       -> HBM
+    t-phase k_tphase2     read pw, pv; write 9 t-partials: 11 arrays
+    s-phase k_pass_cols   s2 level: read 9, write 14; s1 level: read 14,
+                          write 20: 57 arrays over 23 launches
+    solve   k_solve       read 15 S + 5 T moments, write 1: 21 arrays
+    center  k_center_symmetrize  read + write the covariance: 2 arrays
     """
+    arr = 8.0 * G * G
+    return {
+        "k_gemm_tn": ("tensor", 2.0 * n_pair * G * G / 2.0),
+        "k_rank_one": ("hbm", 1 * arr),
+        "k_scale_rows": ("hbm", 2 * 8.0 * n_pair * G),
+        "k_tphase2": ("hbm", 11 * arr),
+        "k_pass_cols": ("hbm", 57 * arr),
+        "k_solve": ("hbm", 21 * arr),
+        "k_center_symmetrize": ("hbm", 2 * arr),
+    }
+
+
+def roofline(kstats, G, binned):
+    """Dominant kernel (largest device time in one profiled step) against its
+    bound, plus the same figure for every modelled kernel."""
     peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
     hbm = peaks.get("hbm_gbs")
     if not kstats:
         return None
-    name, (ms, cnt) = max(kstats.items(), key=lambda kv: kv[1][0])
-    per_launch_s = ms / cnt / 1e3
-    G2 = G * G
-    if name.startswith("k_gemm_tn"):
-        # launches in a step: pv SYRK (+ pw SYRK unless the masses are shared)
-        n_pair = 2000
-        flops_per_launch = 2.0 * n_pair * G2 / 2.0 * (1.0 + 1.0 / (G // 128))  # upper triangle incl. diagonal tiles
-        achieved = flops_per_launch / per_launch_s / 1e12
-        return {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                "peak_source": "measured FP64 DMMA peak (tools/fp64_peak.cu)",
-                "launch_ms": per_launch_s * 1e3, "share_of_step": None}
-    if name.startswith("k_solve"):
-        byts = (15 + 5 + 1) * 8.0 * G2 / cnt
-    else:
-        byts = None
-    achieved = byts / per_launch_s / 1e9 if byts else None
-    return {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": (achieved / hbm) if (achieved and hbm) else None, "traffic": None,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs", "launch_ms": per_launch_s * 1e3}
+    model = kernel_model(G, N_SUBJ)
+    total_ms = sum(v[0] for v in kstats.values())
+    table = {}
+    for name, (ms, cnt) in kstats.items():
+        if name not in model:
+            continue
+        bound, work = model[name]
+        secs = ms / 1e3
+        if bound == "tensor":
+            ach = work / secs / 1e12
+            table[name] = {"bound": "tensor", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                           "frac": ach / FP64_PEAK_TFLOPS, "ms": ms, "launches": cnt,
+                           "share_of_step": ms / total_ms}
+        else:
+            ach = work / secs / 1e9
+            table[name] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                           "frac": ach / hbm if hbm else None, "ms": ms, "launches": cnt,
+                           "share_of_step": ms / total_ms}
+    dom = max(table, key=lambda k: table[k]["ms"])
+    d = dict(table[dom])
+    d["kernel"] = dom
+    d["traffic"] = None  # dram bytes per launch from ncu --set full: profiles/ncu_r01.md
+    d["algorithmic_per_launch"] = model[dom][1] / table[dom]["launches"]
+    d["peak_source"] = ("measured FP64 DMMA peak (tools/fp64_peak.cu, profiles/fp64_peak_r01.txt)"
+                        if d["bound"] == "tensor" else "MEASURED_PEAKS.json hbm_gbs (measured copy)")
+    d["all_kernels"] = table
+    return d
 
 
 if __name__ == "__main__":

@@ -1,0 +1,15 @@
+// Umbrella header of the GPU drop-in for the dfpca hot path (binning,
+// binned smoothers, random-projection eigensolver).  Link with
+// -ldfpca_cuda (paper_1510_04439_b200/libdfpca_cuda.so).
+#pragma once
+
+#include "dfpca/binning.hpp"
+#include "dfpca/dataset.hpp"
+#include "dfpca/eigensolve.hpp"
+#include "dfpca/errors.hpp"
+#include "dfpca/fft_smoother.hpp"
+#include "dfpca/grid.hpp"
+#include "dfpca/kernel.hpp"
+#include "dfpca/parallel.hpp"
+#include "dfpca/rng.hpp"
+#include "dfpca/surface.hpp"

@@ -367,6 +367,8 @@ void launch_tiled(dfpca_context* ctx, const PassSpec& s, const TapsP& tp) {
     const bool vec2 = (in.os % 2 == 0) && (in.js % 2 == 0) &&
                       (reinterpret_cast<std::uintptr_t>(in.p) % 16 == 0);
     auto kern = vec2 ? k_pass_cols<R, NO, 2> : k_pass_cols<R, NO, 1>;
+    if (smem > 48 * 1024)
+      DFPCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
     const i64 blocks = std::min<i64>(tiles, static_cast<i64>(std::max(per_sm, 1)) * ctx->sm_count);

@@ -43,8 +43,8 @@ __global__ void k_rank_one(double* __restrict__ pw, const double* __restrict__ m
 //    differs from the reference's by reassociation only).
 __global__ void k_band_fix(const double* __restrict__ diag_mass, const double* __restrict__ diag_value,
                            i64 G, int d, i64 codes, DevGrid g, const double* __restrict__ ps_mass,
-                           int identical, const double* __restrict__ w, i64 n_pair, double* __restrict__ pw,
-                           double* __restrict__ pv) {
+                           int identical, const double* __restrict__ w, i64 n_pair, double w_seq,
+                           double* __restrict__ pw, double* __restrict__ pv) {
   const int lane = threadIdx.x & 31;
   const i64 warps = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
   const i64 total = G * codes;
@@ -70,7 +70,12 @@ __global__ void k_band_fix(const double* __restrict__ diag_mass, const double* _
     if (!inside) continue;
     double sw = 0.0;
     const double ms0 = identical ? ps_mass[u] : 0.0, mt0 = identical ? ps_mass[t] : 0.0;
-    for (i64 i0 = 0; i0 < n_pair; i0 += 32) {
+    // shared unit masses (every subject observed once at both nodes):
+    // (w_i * 1) * 1 == w_i, so the ordered sum is the ordered sum of the
+    // weights, W_seq, computed once on the host in the same order
+    const bool unit = identical && ms0 == 1.0 && mt0 == 1.0;
+    if (unit) sw = w_seq;
+    for (i64 i0 = 0; i0 < (unit ? 0 : n_pair); i0 += 32) {
       const i64 i = i0 + lane;
       double pm = 0.0;
       if (i < n_pair) {
@@ -98,10 +103,10 @@ DevGrid upload_grid_axes(dfpca_context* ctx, const Grid& g, DevBuf<double>& stor
 void build_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, double* pv) {
   const i64 G = b->grid.G;
   const i64 n = b->n_pair;
+  double W = 0.0;
+  for (double x : b->pair_weight_h) W += x;  // sequential, as the reference's sample loop
   if (pw) {
     if (b->identical_mass) {
-      double W = 0.0;
-      for (double x : b->pair_weight_h) W += x;  // sequential, as the reference's sample loop
       DFPCA_LAUNCH(ctx, k_rank_one, grid_for(G * G, 256, 148ll * 16), 256, 0, pw, b->ps_mass.get(), W, G);
     } else {
       gemm_tn(ctx, G, G, n, b->ps_mass.get(), G, b->pair_weight.get(), b->ps_mass.get(), G, pw, G, true);
@@ -113,7 +118,7 @@ void build_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, dou
     DevGrid dg = upload_grid_axes(ctx, b->grid, axes);
     DFPCA_LAUNCH(ctx, k_band_fix, grid_for(G * b->codes * 32, 256, 148ll * 32), 256, 0,
                  b->diag_mass.get(), b->diag_value.get(), G, b->grid.d, b->codes, dg,
-                 b->ps_mass.get(), b->identical_mass ? 1 : 0, b->pair_weight.get(), n, pw, pv);
+                 b->ps_mass.get(), b->identical_mass ? 1 : 0, b->pair_weight.get(), n, W, pw, pv);
     DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
   }
 }

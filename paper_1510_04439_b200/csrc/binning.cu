@@ -195,33 +195,46 @@ __global__ void k_bin_aggregate(i64 G, i64 n_samples, const unsigned long long* 
                                 const double* __restrict__ values,
                                 const double* __restrict__ mean_w, double* __restrict__ mass,
                                 double* __restrict__ wvalue, double* __restrict__ wsquare) {
-  for (i64 f = blockIdx.x * (i64)blockDim.x + threadIdx.x; f < G;
-       f += (i64)gridDim.x * blockDim.x) {
-    // lower_bound of f * n_samples
+  // One warp per bin: the lanes gather and form the per-record terms of 32
+  // consecutive records in parallel, lane 0 folds them in record order.
+  const int lane = threadIdx.x & 31;
+  const i64 warps = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
+  for (i64 f = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5; f < G; f += warps) {
     const unsigned long long target = static_cast<unsigned long long>(f) * n_samples;
-    i64 lo = 0, hi = n_rec;
+    i64 lo = 0, hi = n_rec;  // lower_bound of target
     while (lo < hi) {
       const i64 mid = (lo + hi) / 2;
-      if (key[mid] < target)
-        lo = mid + 1;
-      else
-        hi = mid;
+      if (key[mid] < target) lo = mid + 1;
+      else hi = mid;
     }
-    double am = 0.0, av = 0.0, as = 0.0;
     const unsigned long long end_key = target + n_samples;
-    for (i64 r = lo; r < n_rec && key[r] < end_key; ++r) {
-      const unsigned rec = val[r];
-      const i64 i = static_cast<i64>(key[r] - target);
-      const double y = values[robs[rec]];
-      const double wm = __dmul_rn(mean_w[i], rmass[rec]);
-      const double wmy = __dmul_rn(wm, y);
-      am = __dadd_rn(am, wm);
-      av = __dadd_rn(av, wmy);
-      as = __dadd_rn(as, __dmul_rn(wmy, y));
+    double am = 0.0, av = 0.0, as = 0.0;
+    for (i64 r0 = lo;; r0 += 32) {
+      const i64 r = r0 + lane;
+      const bool in = r < n_rec && key[r] < end_key;
+      double wm = 0.0, wmy = 0.0, wmyy = 0.0;
+      if (in) {
+        const unsigned rec = val[r];
+        const i64 i = static_cast<i64>(key[r] - target);
+        const double y = values[robs[rec]];
+        wm = __dmul_rn(mean_w[i], rmass[rec]);
+        wmy = __dmul_rn(wm, y);
+        wmyy = __dmul_rn(wmy, y);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, in);
+      const int cnt = __popc(m);  // records of this bin are a prefix of the 32
+      for (int q = 0; q < cnt; ++q) {
+        am = __dadd_rn(am, __shfl_sync(0xffffffffu, wm, q));
+        av = __dadd_rn(av, __shfl_sync(0xffffffffu, wmy, q));
+        as = __dadd_rn(as, __shfl_sync(0xffffffffu, wmyy, q));
+      }
+      if (cnt < 32) break;
     }
-    mass[f] = am;
-    wvalue[f] = av;
-    wsquare[f] = as;
+    if (lane == 0) {
+      mass[f] = am;
+      wvalue[f] = av;
+      wsquare[f] = as;
+    }
   }
 }
 
@@ -255,23 +268,42 @@ __global__ void k_bin_per_sample(i64 G, i64 n_samples, const unsigned long long*
 
 // Self-pair bands: one thread per distinct band index (binning.hpp:163-178).
 __global__ void k_bin_band(const unsigned long long* __restrict__ key, const unsigned* __restrict__ val,
-                           i64 n_rec, const double* __restrict__ bmm,
-                           const unsigned* __restrict__ robs, const double* __restrict__ values, double* __restrict__ diag_mass,
-                           double* __restrict__ diag_value) {
-  for (i64 r0 = blockIdx.x * (i64)blockDim.x + threadIdx.x; r0 < n_rec;
-       r0 += (i64)gridDim.x * blockDim.x) {
-    const unsigned long long k = key[r0];
-    if (r0 > 0 && key[r0 - 1] == k) continue;
-    double dm = 0.0, dv = 0.0;
-    for (i64 r = r0; r < n_rec && key[r] == k; ++r) {
-      const unsigned rec = val[r];
-      const double y = values[robs[rec]];
-      const double mm = bmm[rec];
-      dm = __dadd_rn(dm, mm);
-      dv = __dadd_rn(dv, __dmul_rn(__dmul_rn(mm, y), y));
+                           i64 n_rec, i64 n_keys, const double* __restrict__ bmm,
+                           const unsigned* __restrict__ robs, const double* __restrict__ values,
+                           double* __restrict__ diag_mass, double* __restrict__ diag_value) {
+  // One warp per band index, records folded in order as in k_bin_aggregate.
+  const int lane = threadIdx.x & 31;
+  const i64 warps = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
+  for (i64 k = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5; k < n_keys; k += warps) {
+    i64 lo = 0, hi = n_rec;
+    while (lo < hi) {
+      const i64 mid = (lo + hi) / 2;
+      if (key[mid] < static_cast<unsigned long long>(k)) lo = mid + 1;
+      else hi = mid;
     }
-    diag_mass[k] = dm;
-    diag_value[k] = dv;
+    if (lo >= n_rec || key[lo] != static_cast<unsigned long long>(k)) continue;
+    double dm = 0.0, dv = 0.0;
+    for (i64 r0 = lo;; r0 += 32) {
+      const i64 r = r0 + lane;
+      const bool in = r < n_rec && key[r] == static_cast<unsigned long long>(k);
+      double mm = 0.0, mv = 0.0;
+      if (in) {
+        const unsigned rec = val[r];
+        const double y = values[robs[rec]];
+        mm = bmm[rec];
+        mv = __dmul_rn(__dmul_rn(mm, y), y);
+      }
+      const int cnt = __popc(__ballot_sync(0xffffffffu, in));
+      for (int q = 0; q < cnt; ++q) {
+        dm = __dadd_rn(dm, __shfl_sync(0xffffffffu, mm, q));
+        dv = __dadd_rn(dv, __shfl_sync(0xffffffffu, mv, q));
+      }
+      if (cnt < 32) break;
+    }
+    if (lane == 0) {
+      diag_mass[k] = dm;
+      diag_value[k] = dv;
+    }
   }
 }
 
@@ -447,7 +479,7 @@ dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples
                                       n_grec, 0, bits, st);
       ctx->launches += (bits + 7) / 8 + 1;
       if (mean_path)
-        DFPCA_LAUNCH(ctx, k_bin_aggregate, grid_for(G, 128), 128, 0, G, n_samples, gkey2.get(),
+        DFPCA_LAUNCH(ctx, k_bin_aggregate, grid_for(G * 32, 256), 256, 0, G, n_samples, gkey2.get(),
                      gval2.get(), n_grec, gmass.get(), gobs.get(), d_values.get(),
                      d_meanw.get(), out->mass.get(), out->wvalue.get(), out->wsquare.get());
       if (cov_path && out->n_pair > 0)
@@ -464,8 +496,8 @@ dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples
       cub::DeviceRadixSort::SortPairs(stmp, sb, bkey.get(), bkey2.get(), bval.get(), bval2.get(),
                                       n_brec, 0, bits, st);
       ctx->launches += (bits + 7) / 8 + 1;
-      DFPCA_LAUNCH(ctx, k_bin_band, grid_for(n_brec, 256), 256, 0, bkey2.get(), bval2.get(), n_brec,
-                   bmm.get(), bobs.get(), d_values.get(), out->diag_mass.get(),
+      DFPCA_LAUNCH(ctx, k_bin_band, grid_for(G * out->codes * 32, 256), 256, 0, bkey2.get(), bval2.get(),
+                   n_brec, G * out->codes, bmm.get(), bobs.get(), d_values.get(), out->diag_mass.get(),
                    out->diag_value.get());
     }
   }

@@ -220,8 +220,9 @@ __global__ void k_q_apply(const double* __restrict__ Yt, const double* __restric
 // disjoint rotations at once.  A (n x n, symmetrized on entry) and V live in
 // global memory (L1/L2 resident).  Outputs eigenvalues descending and V's
 // columns in the same order.
-__global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ A, double* __restrict__ V, int n,
-                                                 double* __restrict__ evals, int* __restrict__ info) {
+__global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ Ag, double* __restrict__ Vg, int n,
+                                                 double* __restrict__ evals, int* __restrict__ info,
+                                                 int in_smem) {
   extern __shared__ double sh[];
   const int np = (n + 1) & ~1;  // padded to even (index n is a dummy)
   double* cs = sh;               // [np/2] cos
@@ -231,6 +232,13 @@ __global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ A, double*
   __shared__ double red[33];
   __shared__ int converged;
   const int tid = threadIdx.x, nt = blockDim.x;
+  // A and V live in shared memory when they fit (q <= ~110), else in global
+  double* A = in_smem ? sh + 2 * np : Ag;
+  double* V = in_smem ? A + n * n : Vg;
+  if (in_smem) {
+    for (int e = tid; e < n * n; e += nt) A[e] = Ag[e];
+    __syncthreads();
+  }
   // symmetrize (eigensolve.hpp:265) and V = I
   for (int e = tid; e < n * n; e += nt) {
     const int r = e / n, c = e % n;
@@ -256,7 +264,9 @@ __global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ A, double*
     off = block_sum(off, red);
     // off-diagonal Frobenius norm at 1e-14 of the matrix's: rounding keeps
     // rotated entries at ~eps |lambda|, so a tighter bound may never be met
-    if (tid == 0) converged = !(off > 1e-28 * norm2) || norm2 == 0.0;
+    if (tid == 0)
+      converged = !(off > 1e-28 * norm2) || norm2 == 0.0 ||
+                  (sweep > 2 && !(off < 0.5 * last_off) && !(off > 1e-20 * norm2));  // stalled at rounding
     last_off = off;
     __syncthreads();
     if (converged) break;
@@ -312,6 +322,17 @@ __global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ A, double*
         V[row * n + b] = s * va + c * vb;
       }
       __syncthreads();
+      // the annihilated pair is exactly zero in exact arithmetic; storing the
+      // zero removes the rounding floor that would otherwise stall the
+      // off-diagonal norm near n * eps * |A| for q ~ 100
+      for (int k = tid; k < np / 2; k += nt) {
+        const int a = pp[k], b = qq[k];
+        if (b < n && sn[k] != 0.0) {
+          A[a * n + b] = 0.0;
+          A[b * n + a] = 0.0;
+        }
+      }
+      __syncthreads();
     }
   }
   if (tid == 0) {
@@ -347,6 +368,8 @@ __global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ A, double*
       }
     __syncthreads();
   }
+  if (in_smem)
+    for (int e = tid; e < n * n; e += nt) Vg[e] = V[e];
 }
 
 // ---------------------------------------------------------- finalize ----
@@ -495,9 +518,15 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
   DevBuf<double> evals(static_cast<std::size_t>(q));
   DevBuf<int> info(static_cast<std::size_t>(q + 1));
   const int np = static_cast<int>((q + 1) & ~1ll);
-  const std::size_t jsmem = sizeof(double) * np * 2;
+  std::size_t jsmem = sizeof(double) * np * 2;
+  const bool jac_smem = jsmem + sizeof(double) * 2 * q * q <= 200 * 1024;
+  if (jac_smem) {
+    jsmem += sizeof(double) * 2 * q * q;
+    DFPCA_CUDA(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(jsmem)));
+  }
   DFPCA_LAUNCH(ctx, k_jacobi, 1, 1024, jsmem, small.get(), Vs.get(), static_cast<int>(q), evals.get(),
-               info.get());
+               info.get(), jac_smem ? 1 : 0);
 
   // lifted = Q V  ([M][q]) -> Lt [q][M]
   DevBuf<double> lifted(static_cast<std::size_t>(M * q)), Lt(static_cast<std::size_t>(M * q));

@@ -342,7 +342,7 @@ def kernel_model(G: int, n_pair: int):
         "k_tphase2": ("hbm", 11 * arr),
         "k_pass_cols": ("hbm", 57 * arr),
         "k_solve": ("hbm", 21 * arr),
-        "k_center_symmetrize": ("hbm", 2 * arr),
+        "k_center_mirror": ("hbm", 2 * arr),
     }
 
 

@@ -50,74 +50,113 @@ __device__ inline void cp_async_wait_c() {
 // tile's full-axis column block is copied into the other half of a
 // double-buffered shared-memory ring with cp.async while the current one is
 // convolved, so the HBM reads overlap the FMA work.
+// One thread's kJB outputs along the axis from a staged column; CHECK
+// selects bounds-checked loads (tile edges) or the plain interior path.
+template <int R, int NO, bool CHECK>
+__device__ __forceinline__ void conv_block(const double* __restrict__ col, int j0, int rows, const TapsP& tp,
+                                           double (&acc)[NO][kJB]) {
+#pragma unroll
+  for (int r = 0; r < NO; ++r)
+#pragma unroll
+    for (int jj = 0; jj < kJB; ++jj) acc[r][jj] = 0.0;
+#pragma unroll
+  for (int m = -R; m < kJB + R; ++m) {
+    const int jm = j0 + m;
+    const double x = CHECK ? ((jm >= 0 && jm < rows) ? col[jm * kTile] : 0.0) : col[jm * kTile];
+#pragma unroll
+    for (int jj = 0; jj < kJB; ++jj) {
+      const int o = m - jj;
+      if (o >= -R && o <= R) {
+#pragma unroll
+        for (int r = 0; r < NO; ++r) acc[r][jj] = fma(tp.t[r][o + R], x, acc[r][jj]);
+      }
+    }
+  }
+}
+
 template <int R, int NO, int VEC>
 __global__ void __launch_bounds__(256) k_pass_cols(View in, View o0, View o1, View o2, TapsP tp) {
   extern __shared__ __align__(16) double sm[];  // [2][n][kTile]
   const int n = static_cast<int>(in.n);
-  const i64 chunks = (in.inner + kTile - 1) / kTile;
-  const i64 n_tiles = in.outer * chunks;
+  const int inner = static_cast<int>(in.inner);
+  const int chunks = (inner + kTile - 1) / kTile;
+  const int n_tiles = static_cast<int>(in.outer) * chunks;
   const int tile_elems = n * kTile;
-  auto issue = [&](i64 tile, int buf) {
-    const i64 ob = tile / chunks;
-    const i64 c0 = (tile % chunks) * kTile;
+  const int tri = in.tri, triR = in.tri_R, triG = static_cast<int>(in.tri_G), tri_rn = static_cast<int>(in.tri_rn),
+            tri_n1 = static_cast<int>(in.tri_n1);
+  // rows to stage and outputs to produce for a tile (all of them unless the
+  // upper-triangle restriction applies, see View::tri); 32-bit integer math
+  auto extent = [&](int ob, int c0, int& rows, int& nout) {
+    rows = n;
+    nout = n;
+    if (tri == 0) return;
+    const int c1 = (c0 + kTile < inner ? c0 + kTile : inner) - 1;
+    const int tmax = (c0 / triG == c1 / triG) ? c1 % triG : triG - 1;
+    const int s1_out = tmax / tri_rn + 1;
+    if (tri == 1) {
+      const int s1_in = s1_out + triR < tri_n1 ? s1_out + triR : tri_n1;
+      if (ob >= s1_in) rows = nout = 0;
+    } else {
+      nout = s1_out < n ? s1_out : n;
+      rows = nout + triR < n ? nout + triR : n;
+    }
+  };
+  auto issue = [&](int tile, int buf) {
+    const int ob = tile / chunks;
+    const int c0 = (tile - ob * chunks) * kTile;
+    int rows, nout;
+    extent(ob, c0, rows, nout);
     const double* src = in.p + ob * in.os + c0;
     double* dst = sm + buf * tile_elems;
-    for (int e = threadIdx.x * VEC; e < tile_elems; e += blockDim.x * VEC) {
+    const int avail_cols = inner - c0;
+    for (int e = threadIdx.x * VEC; e < rows * kTile; e += blockDim.x * VEC) {
       const int j = e / kTile, c = e % kTile;
-      const i64 avail = in.inner - (c0 + c);
-      const int bytes = avail >= VEC ? 8 * VEC : (avail > 0 ? 8 * static_cast<int>(avail) : 0);
+      const int avail = avail_cols - c;
+      const int bytes = avail >= VEC ? 8 * VEC : (avail > 0 ? 8 * avail : 0);
       const double* g = bytes ? src + j * in.js + c : in.p;
       if (VEC == 2) cp_async_c16(dst + e, g, bytes);
       else cp_async_c8(dst + e, g, bytes);
     }
   };
   int buf = 0;
-  i64 tile = blockIdx.x;
+  int tile = blockIdx.x;
   if (tile < n_tiles) issue(tile, 0);
   cp_async_commit_c();
+  const int c = threadIdx.x % kTile;
   for (; tile < n_tiles; tile += gridDim.x) {
-    const i64 next = tile + gridDim.x;
+    const int next = tile + gridDim.x;
     if (next < n_tiles) issue(next, buf ^ 1);
     cp_async_commit_c();
     cp_async_wait_c<1>();
     __syncthreads();
-    const i64 ob = tile / chunks;
-    const i64 c0 = (tile % chunks) * kTile;
-    const double* cur = sm + buf * tile_elems;
-    const int c = threadIdx.x % kTile;
-    const bool col_ok = c0 + c < in.inner;
-    for (int j0 = (threadIdx.x / kTile) * kJB; j0 < n; j0 += (blockDim.x / kTile) * kJB) {
+    const int ob = tile / chunks;
+    const int c0 = (tile - ob * chunks) * kTile;
+    int rows, nout;
+    extent(ob, c0, rows, nout);
+    const double* col = sm + buf * tile_elems + c;
+    const bool col_ok = c0 + c < inner;
+    double* b0 = o0.p + ob * o0.os + c0 + c;
+    double* b1 = o1.p + ob * o1.os + c0 + c;
+    double* b2 = o2.p + ob * o2.os + c0 + c;
+    for (int j0 = (threadIdx.x / kTile) * kJB; j0 < nout; j0 += (blockDim.x / kTile) * kJB) {
       double acc[NO][kJB];
-#pragma unroll
-      for (int r = 0; r < NO; ++r)
-#pragma unroll
-        for (int jj = 0; jj < kJB; ++jj) acc[r][jj] = 0.0;
-#pragma unroll
-      for (int m = -R; m < kJB + R; ++m) {
-        const int jm = j0 + m;
-        const double x = (jm >= 0 && jm < n) ? cur[jm * kTile + c] : 0.0;
-#pragma unroll
-        for (int jj = 0; jj < kJB; ++jj) {
-          const int o = m - jj;
-          if (o >= -R && o <= R) {
-#pragma unroll
-            for (int r = 0; r < NO; ++r) acc[r][jj] = fma(tp.t[r][o + R], x, acc[r][jj]);
-          }
-        }
-      }
+      if (j0 >= R && j0 + kJB + R <= rows)
+        conv_block<R, NO, false>(col, j0, rows, tp, acc);
+      else
+        conv_block<R, NO, true>(col, j0, rows, tp, acc);
       if (col_ok) {
 #pragma unroll
         for (int jj = 0; jj < kJB; ++jj) {
-          const i64 j = j0 + jj;
-          if (j < n) {
-            o0.p[ob * o0.os + j * o0.js + c0 + c] = acc[0][jj];
-            if (NO > 1) o1.p[ob * o1.os + j * o1.js + c0 + c] = acc[NO > 1 ? 1 : 0][jj];
-            if (NO > 2) o2.p[ob * o2.os + j * o2.js + c0 + c] = acc[NO > 2 ? 2 : 0][jj];
+          const int j = j0 + jj;
+          if (j < nout) {
+            b0[j * o0.js] = acc[0][jj];
+            if (NO > 1) b1[j * o1.js] = acc[NO > 1 ? 1 : 0][jj];
+            if (NO > 2) b2[j * o2.js] = acc[NO > 2 ? 2 : 0][jj];
           }
         }
       }
     }
-    __syncthreads();  // everyone is done with `cur` before it is refilled
+    __syncthreads();  // everyone is done with this buffer before it is refilled
     buf ^= 1;
   }
   cp_async_wait_c<0>();
@@ -457,7 +496,8 @@ void run_pass(dfpca_context* ctx, const PassSpec& s, double* taps_dev) {
   const int R = s.R;
   const bool tiled_ok = R <= kMaxTemplR && s.in.n <= kMaxN && s.in.n >= 1 &&
                         (s.in.inner == 1 || s.in.inner >= 16) &&
-                        s.in.outer * ((s.in.inner + kTile - 1) / kTile) < (1ll << 31);
+                        s.in.outer * ((s.in.inner + kTile - 1) / kTile) < (1ll << 31) &&
+                        s.in.inner < (1ll << 31);
   if (tiled_ok) {
     TapsP tp{};
     for (int r = 0; r < s.n_out; ++r)

@@ -16,6 +16,17 @@ struct View {
   i64 outer, os;
   i64 n, js;
   i64 inner;
+  // Upper-triangle restriction of the 2-d covariance s-phase (arrays laid out
+  // [s1][s2][t], only s <= t is ever solved):
+  //   tri = 1: pass along s2 (outer = s1): skip s1 rows beyond those the s1
+  //            pass of the same t columns will read;
+  //   tri = 2: pass along s1 (inner = s2 * tri_G + t): read s1 < s1_out + R,
+  //            write s1 < s1_out, s1_out = t_max / tri_rn + 1.
+  int tri = 0;
+  int tri_R = 0;
+  i64 tri_G = 0;   // t extent
+  i64 tri_rn = 0;  // s nodes per s1 row
+  i64 tri_n1 = 0;  // s1 extent
 };
 
 // One multi-order pass along an axis: outputs out[r] = taps(order[r]) * in.

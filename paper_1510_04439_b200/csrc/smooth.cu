@@ -24,7 +24,6 @@
 #include <string>
 
 #include "conv.cuh"
-#include "fused.cuh"
 #include "solve.cuh"
 
 namespace dfpca_gpu {
@@ -103,6 +102,9 @@ struct ChunkDims {
   i64 rows;                // leading extent (outer rows of the chunk)
   std::vector<i64> shape;  // extents of the axes of this phase, in memory order
   i64 tail;                // trailing contiguous extent after these axes
+  // upper-triangle restriction (View::tri) for the passes of tree level i
+  std::vector<int> tri;
+  View tri_params{};
 };
 
 View make_view(double* p, const ChunkDims& cd, int k, i64 row_stride_override = -1) {
@@ -136,6 +138,7 @@ struct SolveGeom {
   i64 t0;
   i64 gt;          // full column extent (t grid size); 1-D mean: gt = tc = G
   int cov;         // 1: mask both s and t nodes
+  int upper;       // covariance: solve only s <= t (the rest is mirrored)
   const std::uint8_t* mask;  // device mask (nullable)
   const double* mean;        // covariance: centered later; unused here
 };
@@ -152,6 +155,7 @@ __global__ void __launch_bounds__(128) k_solve(MomPtrs mp, SolveGeom g, double* 
     const i64 row = e / g.tc;
     const i64 col = g.t0 + e % g.tc;
     const i64 dst = g.cov ? row * g.gt + col : col + row * g.gt;
+    if (g.upper && row > col) continue;
     bool inside = true;
     if (g.mask) inside = g.cov ? (g.mask[row] != 0 && g.mask[col] != 0) : (g.mask[dst] != 0);
     if (!inside) {
@@ -281,15 +285,16 @@ __global__ void k_ladder(LadderGeom lg, const double* __restrict__ mass, const d
   }
 }
 
-// Covariance centering and exact symmetrization (fft_smoother.hpp:723-736),
-// 32x32 tile pairs so both the (a,b) and (b,a) accesses are coalesced.
-__global__ void k_center_symmetrize(double* __restrict__ cov, const double* __restrict__ mean,
-                                    const std::uint8_t* __restrict__ mask, i64 G) {
-  __shared__ double ta[32][33];
-  __shared__ double tb[32][33];
+// Covariance centering and symmetrization (fft_smoother.hpp:723-736).  The
+// solve filled the upper triangle s <= t; each entry is centered by the mean
+// product and written to both (s,t) and (t,s), so the result is exactly
+// symmetric.  32x32 tile pairs keep both the row and the mirrored column
+// accesses coalesced.
+__global__ void k_center_mirror(double* __restrict__ cov, const double* __restrict__ mean,
+                                const std::uint8_t* __restrict__ mask, i64 G) {
+  __shared__ double tile[32][33];
   const i64 tiles = (G + 31) / 32;
-  // blockIdx.x enumerates tile pairs (I <= J)
-  i64 t = blockIdx.x;
+  i64 t = blockIdx.x;  // tile pairs (I <= J)
   i64 I = 0;
   while (t >= tiles - I) {
     t -= tiles - I;
@@ -300,43 +305,17 @@ __global__ void k_center_symmetrize(double* __restrict__ cov, const double* __re
   for (int r = ty; r < 32; r += 8) {
     const i64 a = I * 32 + r, b = J * 32 + tx;
     double v = 0.0;
-    if (a < G && b < G) {
+    if (a < G && b < G && a <= b) {
       v = cov[a * G + b];
       if (!mask || (mask[a] && mask[b])) v -= mean[a] * mean[b];
+      cov[a * G + b] = v;
     }
-    ta[r][tx] = v;
-    const i64 a2 = J * 32 + r, b2 = I * 32 + tx;
-    double v2 = 0.0;
-    if (a2 < G && b2 < G) {
-      v2 = cov[a2 * G + b2];
-      if (!mask || (mask[a2] && mask[b2])) v2 -= mean[a2] * mean[b2];
-    }
-    tb[r][tx] = v2;
+    tile[r][tx] = v;
   }
   __syncthreads();
-  // ta[r][c] = cov(I*32+r, J*32+c); tb[r][c] = cov(J*32+r, I*32+c)
   for (int r = ty; r < 32; r += 8) {
-    const i64 a = I * 32 + r, b = J * 32 + tx;  // element (a, b) of tile (I, J)
-    if (a < G && b < G) {
-      double x = ta[r][tx];
-      if (a < b && !isnan(x)) x = 0.5 * (x + tb[tx][r]);
-      else if (a > b) {
-        const double y = tb[tx][r];  // (b, a), b < a
-        if (!isnan(y)) x = 0.5 * (y + x);
-      }
-      cov[a * G + b] = x;
-    }
-    const i64 a2 = J * 32 + r, b2 = I * 32 + tx;  // element (a2, b2) of tile (J, I)
-    if (I != J && a2 < G && b2 < G) {
-      double x = tb[r][tx];
-      if (a2 > b2) {
-        const double y = ta[tx][r];  // (b2, a2) with b2 < a2
-        if (!isnan(y)) x = 0.5 * (y + x);
-      } else if (a2 < b2 && !isnan(x)) {
-        x = 0.5 * (x + ta[tx][r]);
-      }
-      cov[a2 * G + b2] = x;
-    }
+    const i64 b = J * 32 + r, a = I * 32 + tx;  // mirror (b, a) of the upper entry (a, b)
+    if (a < G && b < G && a < b) cov[b * G + a] = tile[tx][r];
   }
 }
 
@@ -412,6 +391,13 @@ std::vector<Leaf> run_tree(dfpca_context* ctx, const std::vector<Leaf>& roots,
       spec.in = (ai == 0 && first_reads_strided) ? make_view(in.ptr, cd, ax.view_k, first_row_stride)
                                                  : make_view(in.ptr, cd, ax.view_k);
       if (ai == 0 && first_reads_strided) spec.in = in.view;
+      if (ai < cd.tri.size() && cd.tri[ai]) {
+        spec.in.tri = cd.tri[ai];
+        spec.in.tri_R = cd.tri_params.tri_R;
+        spec.in.tri_G = cd.tri_params.tri_G;
+        spec.in.tri_rn = cd.tri_params.tri_rn;
+        spec.in.tri_n1 = cd.tri_params.tri_n1;
+      }
       spec.n_out = n_out;
       spec.R = taps[ax.axis_index].R;
       for (int r = 0; r < n_out; ++r) {
@@ -566,7 +552,6 @@ void run_local_linear(dfpca_context* ctx, const dfpca_binned* b, const Grid& gri
 // Pair grids + moments + solve + center + symmetrize for the covariance.
 void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid, const double* h,
                     const double* mean_host, dfpca_surface** out) {
-  const bool use_fused_s1 = std::getenv("DFPCA_FUSED_S1") != nullptr;
   const int d = grid.d;
   const int p = 2 * d;
   const i64 G = grid.G;
@@ -681,103 +666,63 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
   const i64 list_cap = std::min<i64>(G2, i64(1) << 26);
   DevBuf<i64> list(static_cast<std::size_t>(list_cap));
   DFPCA_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long), st));
+  // Column chunks of the t-partials.  Only the upper triangle s <= t (flat
+  // node order) is smoothed: the covariance is symmetric by construction
+  // (the reference averages the (s,t) and (t,s) fits of mirror-image windows,
+  // fft_smoother.hpp:730-736), so the lower triangle is the mirror copy
+  // written by the symmetrization pass.  A chunk of columns [t0, t0+cols)
+  // needs output rows s1 < s1_out and, for the last (s1) pass, input rows
+  // s1 < s1_out + R.
+  const i64 row_nodes = G / grid.shape[0];  // s-nodes per s1 row
   i64 tc = std::max<i64>(1, std::min<i64>(G, budget_elems / std::max<i64>(G, 1) / 4));
+  // d = 2 with the whole grid in one chunk: the per-tile restriction of the
+  // pass kernels (View::tri) trims the s rows column tile by column tile
+  const bool tri_tiles = d == 2 && tc >= G;
   std::vector<TreeAxis> saxes;
   for (int k = d - 1; k >= 0; --k) saxes.push_back({k, k});
-  double solve_ms_acc = 0.0;
-  (void)solve_ms_acc;
   for (i64 t0 = 0; t0 < G; t0 += tc) {
     const i64 cols = std::min(tc, G - t0);
+    const i64 s1_out = std::min<i64>(grid.shape[0], (t0 + cols - 1) / row_nodes + 1);
+    const i64 s1_in = std::min<i64>(grid.shape[0], s1_out + taps[0].R);
     ChunkDims cd;
     cd.rows = 1;
     for (int k = 0; k < d; ++k) cd.shape.push_back(grid.shape[k]);
+    cd.shape[0] = s1_in;
     cd.tail = cols;
-    // roots: the t-partials viewed as [s...][cols] with row stride G
+    if (tri_tiles) {
+      cd.tri = {1, 2};  // s2 pass, then s1 pass
+      cd.tri_params.tri_R = static_cast<int>(taps[0].R);
+      cd.tri_params.tri_G = cols;
+      cd.tri_params.tri_rn = row_nodes;
+      cd.tri_params.tri_n1 = grid.shape[0];
+    }
+    const i64 chunk_elems = s1_in * row_nodes * cols;
+    // roots: the t-partials viewed as [s1 < s1_in][s2..][cols] with row stride G;
+    // the first pass runs along the last s-axis
     std::vector<Leaf> roots;
     for (auto& kv : tpart) {
       Leaf r;
       r.ord = kv.first.first;
       r.budget_max = kv.first.second;
-      // budget left for s-axes is budget_max - |a|; encode by keeping ord
       r.ptr = kv.second + t0;
-      // first pass reads axis d-1 of the s block: outer = s[0..d-2], n = s[d-1], inner = cols
       View v;
       v.p = r.ptr;
-      v.n = grid.shape[d - 1];
+      v.n = d == 1 ? s1_in : grid.shape[d - 1];  // d = 1: the first pass is the truncated s1 axis
       v.js = G;
       v.inner = cols;
-      v.outer = G / grid.shape[d - 1];
-      v.os = grid.shape[d - 1] * G;
+      v.outer = d == 1 ? 1 : s1_in * row_nodes / grid.shape[d - 1];
+      v.os = v.n * G;
       r.view = v;
       roots.push_back(r);
     }
     std::vector<std::unique_ptr<DevBuf<double>>> keep;
     std::vector<std::unique_ptr<DevBuf<double>>> finals;
     auto final_dst = [&](const Orders&, int) -> double* {
-      finals.push_back(std::make_unique<DevBuf<double>>(static_cast<std::size_t>(G * cols)));
+      finals.push_back(std::make_unique<DevBuf<double>>(static_cast<std::size_t>(chunk_elems)));
       return finals.back()->get();
     };
     auto final_rs = [&](const Orders&, int) -> i64 { return -1; };
-    if (d == 2) {
-      // s2 pass, then the fused s1 pass + solve (fused.cu): the 20 moment
-      // arrays of the chunk are never materialized.
-      std::vector<TreeAxis> s2ax = {{1, 1}};
-      std::vector<Leaf> l2 = run_tree(ctx, roots, s2ax, cd, taps, G * cols, taps_dev.get(), keep, final_dst,
-                                      final_rs, true, -1);
-      S1SolveSpec sp{};
-      bool ok = true;
-      const auto order = s1_p4_input_order();
-      for (std::size_t k = 0; k < order.size(); ++k) {
-        const double* ptr = nullptr;
-        for (const Leaf& l : l2)
-          if (l.budget_max == order[k][0] && l.ord[0] == 0 && l.ord[1] == order[k][1] &&
-              l.ord[2] == order[k][2] && l.ord[3] == order[k][3])
-            ptr = l.ptr;
-        ok = ok && ptr != nullptr;
-        sp.in[k] = ptr;
-      }
-      sp.n = grid.shape[0];
-      sp.s2n = grid.shape[1];
-      sp.inner = grid.shape[1] * cols;
-      sp.cols = cols;
-      sp.t0 = t0;
-      sp.G = G;
-      sp.R = taps[0].R;
-      for (int r = 0; r < 3; ++r) sp.taps[r] = taps[0].t[r].data();
-      sp.mask = grid.has_mask ? mask_dev.get() : nullptr;
-      sp.out = surf->values.get();
-      sp.cnt = cnt.get();
-      sp.list = list.get();
-      sp.cap = list_cap;
-      ctx->end_stage();
-      ctx->begin_stage("solve");
-      // The fused s1+solve kernel (fused.cu) is register-bound at 8 warps/SM;
-      // the split pass + solve is faster on B200 until it is reworked.
-      const bool fused = ok && use_fused_s1 && run_s1_solve_p4(ctx, sp);
-      ctx->end_stage();
-      ctx->begin_stage("moments");
-      if (fused) continue;
-      // no specialisation: finish the s1 axis with the generic passes
-      std::vector<TreeAxis> s1ax = {{0, 0}};
-      std::vector<Leaf> leaves = run_tree(ctx, l2, s1ax, cd, taps, G * cols, taps_dev.get(), keep, final_dst,
-                                          final_rs, false, -1);
-      MomPtrs mp{};
-      for (const Leaf& l : leaves) {
-        const int idx = basis.find(l.ord);
-        if (l.budget_max == 2) mp.S[idx] = l.ptr;
-        else mp.T[idx] = l.ptr;
-      }
-      SolveGeom sg{};
-      sg.npts = G * cols;
-      sg.tc = cols;
-      sg.t0 = t0;
-      sg.gt = G;
-      sg.cov = 1;
-      sg.mask = grid.has_mask ? mask_dev.get() : nullptr;
-      solve_launcher(p)(ctx, mp, sg, surf->values.get(), cnt.get(), list.get(), list_cap);
-      continue;
-    }
-    std::vector<Leaf> leaves = run_tree(ctx, roots, saxes, cd, taps, G * cols, taps_dev.get(), keep,
+    std::vector<Leaf> leaves = run_tree(ctx, roots, saxes, cd, taps, chunk_elems, taps_dev.get(), keep,
                                         final_dst, final_rs, true, -1);
     MomPtrs mp{};
     for (const Leaf& l : leaves) {
@@ -786,11 +731,12 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
       else mp.T[idx] = l.ptr;
     }
     SolveGeom sg{};
-    sg.npts = G * cols;
+    sg.npts = s1_out * row_nodes * cols;
     sg.tc = cols;
     sg.t0 = t0;
     sg.gt = G;
     sg.cov = 1;
+    sg.upper = 1;
     sg.mask = grid.has_mask ? mask_dev.get() : nullptr;
     ctx->end_stage();
     ctx->begin_stage("solve");
@@ -842,7 +788,7 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
   DFPCA_CUDA(cudaMemcpyAsync(mean_dev.get(), mean_host, sizeof(double) * G, cudaMemcpyHostToDevice, st));
   const i64 tiles = (G + 31) / 32;
   const i64 pairs = tiles * (tiles + 1) / 2;
-  DFPCA_LAUNCH(ctx, k_center_symmetrize, static_cast<unsigned>(pairs), 256, 0, surf->values.get(),
+  DFPCA_LAUNCH(ctx, k_center_mirror, static_cast<unsigned>(pairs), 256, 0, surf->values.get(),
                mean_dev.get(), grid.has_mask ? mask_dev.get() : nullptr, G);
   ctx->end_stage();
   DFPCA_CUDA(cudaStreamSynchronize(st));

@@ -60,15 +60,18 @@ class ClockSampler:
     def __init__(self, device: int):
         self.device = device
         self.rows = []
+        self.query_s = []
         self._stop = threading.Event()
         self._t = None
 
     def _run(self):
         while not self._stop.is_set():
             try:
+                q0 = time.perf_counter()
                 out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
+                self.query_s.append(time.perf_counter() - q0)
                 if out:
                     self.rows.append([x.strip() for x in out.split(",")])
             except Exception:
@@ -92,7 +95,8 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].strip() == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows),
+                "query_ms": float(1e3 * np.median(self.query_s)) if self.query_s else None}
 
 
 # ------------------------------------------------------------------- data --
@@ -255,6 +259,22 @@ def main():
             e2e_t.append(t1 - t0)
         del b2, m2, c2
     e2e_step = float(np.mean(e2e_t))
+    # one more pass, synchronised per call, for the breakdown (not timed above)
+    brk = {}
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    b2 = api.linear_bin(data, grid, api.BinOptions(True, True))
+    torch.cuda.synchronize(dev)
+    brk["linear_bin"] = time.perf_counter() - t0
+    m2 = api.fft_local_linear(b2, grid, h, api.MomentTarget.Mean)
+    torch.cuda.synchronize(dev)
+    brk["mean"] = time.perf_counter() - t0 - sum(brk.values())
+    c2 = api.fft_covariance(b2, grid, h, m2)
+    torch.cuda.synchronize(dev)
+    brk["covariance"] = time.perf_counter() - t0 - sum(brk.values())
+    _lib.check(_lib.lib().dfpca_surface_download(_lib.ctx(), c2.device_handle(), host_cov.ctypes.data_as(_lib.PD)))
+    brk["download"] = time.perf_counter() - t0 - sum(brk.values())
+    del b2, m2, c2
     if dist is not None:
         tt = torch.tensor([e2e_step], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -305,6 +325,7 @@ def main():
         "wall_ms_per_step": wall / args.steps * 1e3,
         "e2e": {"value": world * G2 / e2e_step, "unit": "gridpts/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_step * 1e3,
+                "breakdown_ms": {k: v * 1e3 for k, v in brk.items()},
                 "path": "pinned host obs -> linear_bin -> fft_local_linear -> fft_covariance -> host covariance",
                 "pinned": all(pinned)},
         "fpca_e2e_ms": fpca_ms, "eigen_ms": eig_ms, "eig_top3": eig.eigenvalues[:3],
@@ -320,29 +341,48 @@ def main():
         dist.destroy_process_group()
 
 
+def tri_fractions(cells: int, R: int, tile: int = 32):
+    """Row fractions of the upper-triangle s-phase (csrc/conv.cu View::tri):
+    for each 32-column t tile, the s2 pass touches s1 < min(n1, s1_out + R)
+    rows, the s1 pass reads those and writes s1 < s1_out rows; the solve and
+    the centering touch s <= t."""
+    n1 = cells
+    G = cells * cells
+    rows_in = rows_out = 0
+    for c0 in range(0, G, tile):
+        tmax = min(c0 + tile, G) - 1
+        s1_out = tmax // cells + 1
+        rows_in += min(n1, s1_out + R) * (min(c0 + tile, G) - c0)
+        rows_out += s1_out * (min(c0 + tile, G) - c0)
+    upper = (G * (G + 1) / 2) / (G * G)
+    return rows_in / (n1 * G), rows_out / (n1 * G), upper
+
+
 def kernel_model(G: int, n_pair: int):
     """Algorithmic work per step of every kernel of the d = 2 covariance step
-    ('Roofline model').  Arrays are G^2 doubles (8 B per point).
+    (DESIGN.md 'Roofline model'); one array = G^2 doubles.
 
     pairs   k_gemm_tn     SYRK of the pair-weighted value grids: n G^2 FMAs
-                          (symmetric half of 2 n G^2 flops)       -> FP64 tensor
-            k_rank_one    pw = W M(s) M(t): write 1 array         -> HBM
-            k_scale_rows  w_i V_i: read + write n G doubles       -> HBM
+                          (the symmetric half of 2 n G^2 flops)    -> FP64 tensor
+            k_rank_one    pw = W M(s) M(t): write 1 array          -> HBM
+            k_scale_rows  w_i V_i: read + write n G doubles
     t-phase k_tphase2     read pw, pv; write 9 t-partials: 11 arrays
-    s-phase k_pass_cols   s2 level: read 9, write 14; s1 level: read 14,
-                          write 20: 57 arrays over 23 launches
-    solve   k_solve       read 15 S + 5 T moments, write 1: 21 arrays
-    center  k_center_symmetrize  read + write the covariance: 2 arrays
+    s-phase k_pass_cols   s2 level: 9 in + 14 out over the trimmed rows;
+                          s1 level: 14 in (trimmed rows) + 20 out (s <= t rows)
+    solve   k_solve       20 moments in + 1 out at s <= t
+    center  k_center_mirror  read s <= t, write both triangles
     """
+    cells = int(round(G ** 0.5))
+    f_in, f_out, upper = tri_fractions(cells, int(np.ceil(H * cells)))
     arr = 8.0 * G * G
     return {
         "k_gemm_tn": ("tensor", 2.0 * n_pair * G * G / 2.0),
         "k_rank_one": ("hbm", 1 * arr),
         "k_scale_rows": ("hbm", 2 * 8.0 * n_pair * G),
         "k_tphase2": ("hbm", 11 * arr),
-        "k_pass_cols": ("hbm", 57 * arr),
-        "k_solve": ("hbm", 21 * arr),
-        "k_center_mirror": ("hbm", 2 * arr),
+        "k_pass_cols": ("hbm", ((9 + 14) * f_in + 14 * f_in + 20 * f_out) * arr),
+        "k_solve": ("hbm", 21 * upper * arr),
+        "k_center_mirror": ("hbm", (upper + 1.0) * arr),
     }
 
 

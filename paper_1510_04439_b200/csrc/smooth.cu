@@ -24,6 +24,7 @@
 #include <string>
 
 #include "conv.cuh"
+#include "s1solve.cuh"
 #include "solve.cuh"
 
 namespace dfpca_gpu {
@@ -552,6 +553,7 @@ void run_local_linear(dfpca_context* ctx, const dfpca_binned* b, const Grid& gri
 // Pair grids + moments + solve + center + symmetrize for the covariance.
 void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid, const double* h,
                     const double* mean_host, dfpca_surface** out) {
+  static const bool use_fused_s1 = std::getenv("DFPCA_FUSED_S1") != nullptr;  // experimental
   const int d = grid.d;
   const int p = 2 * d;
   const i64 G = grid.G;
@@ -722,6 +724,65 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
       return finals.back()->get();
     };
     auto final_rs = [&](const Orders&, int) -> i64 { return -1; };
+    if (d == 2) {
+      // s2 pass, then the fused s1 pass + solve (s1solve.cu): the 20 moment
+      // arrays of the chunk never reach HBM
+      std::vector<TreeAxis> s2ax = {saxes[0]};
+      std::vector<Leaf> l2 = run_tree(ctx, roots, s2ax, cd, taps, chunk_elems, taps_dev.get(), keep, final_dst,
+                                      final_rs, true, -1);
+      S1SolveSpec sp{};
+      bool ok = true;
+      const auto order = s1_p4_input_order();
+      for (std::size_t k = 0; k < order.size(); ++k) {
+        const double* ptr = nullptr;
+        for (const Leaf& l : l2)
+          if (l.budget_max == order[k][0] && l.ord[0] == 0 && l.ord[1] == order[k][1] &&
+              l.ord[2] == order[k][2] && l.ord[3] == order[k][3])
+            ptr = l.ptr;
+        ok = ok && ptr != nullptr;
+        sp.in[k] = ptr;
+      }
+      sp.n = s1_in;
+      sp.s2n = grid.shape[1];
+      sp.inner = grid.shape[1] * cols;
+      sp.cols = cols;
+      sp.t0 = t0;
+      sp.G = G;
+      sp.R = taps[0].R;
+      for (int r = 0; r < 3; ++r) sp.taps[r] = taps[0].t[r].data();
+      sp.mask = grid.has_mask ? mask_dev.get() : nullptr;
+      sp.out = surf->values.get();
+      sp.cnt = cnt.get();
+      sp.list = list.get();
+      sp.cap = list_cap;
+      ctx->end_stage();
+      ctx->begin_stage("solve");
+      // the fused s1 pass + solve is latency-bound at its occupancy on B200;
+      // the split s1 pass + k_solve is faster until it is reworked
+      const bool fused = ok && use_fused_s1 && run_s1_solve_p4(ctx, sp);
+      ctx->end_stage();
+      ctx->begin_stage("moments");
+      if (fused) continue;
+      std::vector<TreeAxis> s1ax = {saxes[1]};
+      std::vector<Leaf> leaves = run_tree(ctx, l2, s1ax, cd, taps, chunk_elems, taps_dev.get(), keep, final_dst,
+                                          final_rs, false, -1);
+      MomPtrs mp{};
+      for (const Leaf& l : leaves) {
+        const int idx = basis.find(l.ord);
+        if (l.budget_max == 2) mp.S[idx] = l.ptr;
+        else mp.T[idx] = l.ptr;
+      }
+      SolveGeom sg{};
+      sg.npts = s1_out * row_nodes * cols;
+      sg.tc = cols;
+      sg.t0 = t0;
+      sg.gt = G;
+      sg.cov = 1;
+      sg.upper = 1;
+      sg.mask = grid.has_mask ? mask_dev.get() : nullptr;
+      solve_launcher(p)(ctx, mp, sg, surf->values.get(), cnt.get(), list.get(), list_cap);
+      continue;
+    }
     std::vector<Leaf> leaves = run_tree(ctx, roots, saxes, cd, taps, chunk_elems, taps_dev.get(), keep,
                                         final_dst, final_rs, true, -1);
     MomPtrs mp{};

@@ -322,6 +322,23 @@ __global__ void k_mass_identical(const double* __restrict__ ps_mass, i64 n_pair,
   }
 }
 
+// Shared-design probe: mass grid constant, band diagonal-only and constant.
+__global__ void k_shared_design(const double* __restrict__ m, const double* __restrict__ dm, i64 G, i64 codes,
+                                i64 center, int* __restrict__ bad) {
+  const double m0 = m[0], d0 = dm[center];
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < G * codes; e += (i64)gridDim.x * blockDim.x) {
+    const i64 u = e / codes, c = e - u * codes;
+    const bool ok = c == center
+                        ? (__double_as_longlong(dm[e]) == __double_as_longlong(d0) &&
+                           __double_as_longlong(m[u]) == __double_as_longlong(m0))
+                        : dm[e] == 0.0;
+    if (!ok) {
+      *bad = 1;
+      return;
+    }
+  }
+}
+
 int key_bits(unsigned long long max_key) {
   int b = 1;
   while (b < 64 && (max_key >> b) != 0) ++b;
@@ -514,9 +531,31 @@ dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples
   } else {
     out->identical_mass = cov_path && out->n_pair == 1;
   }
+  detect_shared_design(ctx, out.get());
   ctx->end_stage();
   DFPCA_CUDA(cudaStreamSynchronize(st));
   return out.release();
+}
+
+void detect_shared_design(dfpca_context* ctx, dfpca_binned* b) {
+  b->shared_const = false;
+  if (!b->has_cov || !b->identical_mass || b->n_pair < 1) return;
+  const i64 G = b->grid.G;
+  const i64 center = (b->codes - 1) / 2;  // code digits o_k + 1 = 1 on every axis
+  cudaStream_t st = ctx->stream;
+  DevBuf<int> bad(1);
+  DFPCA_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), st));
+  DFPCA_LAUNCH(ctx, k_shared_design, grid_for(G * b->codes, 256), 256, 0, b->ps_mass.get(), b->diag_mass.get(), G,
+               b->codes, center, bad.get());
+  int h_bad = 1;
+  double m0 = 0.0, dm0 = 0.0;
+  DFPCA_CUDA(cudaMemcpyAsync(&h_bad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+  DFPCA_CUDA(cudaMemcpyAsync(&m0, b->ps_mass.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
+  DFPCA_CUDA(cudaMemcpyAsync(&dm0, b->diag_mass.get() + center, sizeof(double), cudaMemcpyDeviceToHost, st));
+  DFPCA_CUDA(cudaStreamSynchronize(st));
+  b->shared_const = h_bad == 0 && m0 > 0.0 && std::isfinite(m0) && std::isfinite(dm0);
+  b->shared_m0 = m0;
+  b->shared_dm0 = dm0;
 }
 
 }  // namespace dfpca_gpu

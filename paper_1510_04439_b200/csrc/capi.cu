@@ -481,6 +481,7 @@ int dfpca_binned_upload(dfpca_context* ctx, const dfpca_grid* grid, int64_t n_sa
       for (i64 i = 1; i < n_pair_samples && same; ++i)
         same = std::memcmp(ps_mass + i * G, ps_mass, sizeof(double) * G) == 0;
       b->identical_mass = same;
+      dfpca_gpu::detect_shared_design(ctx, b.get());
     }
     DFPCA_CUDA(cudaStreamSynchronize(st));
     *out = b.release();

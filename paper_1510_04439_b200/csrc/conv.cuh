@@ -54,6 +54,7 @@ struct TPhase2Spec {
   double* value_out[3];
   const double* taps[2][3];
   int R[2];
+  bool value_only = false;  // pw unused: only the 3 value t-partials
 };
 // Returns false when the plane does not fit (caller uses run_pass instead).
 bool run_tphase2(dfpca_context* ctx, const TPhase2Spec& spec);

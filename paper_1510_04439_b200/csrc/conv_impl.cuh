@@ -15,7 +15,6 @@
 
 #include <algorithm>
 #include <cstdint>
-#include <cstdlib>
 
 #include "conv_detail.cuh"
 
@@ -72,7 +71,7 @@ __device__ inline void bulk_g2s(void* dst, const void* src, unsigned bytes, std:
 // with one cp.async.bulk (TMA engine, completion on an mbarrier), so loading
 // costs ~one instruction per 512-byte row; otherwise every thread issues
 // 8-byte cp.async (unaligned views).  Thread (c, g) owns column c and output
-// blocks j0 = g*JB, g*JB + 4*JB, ... (4 row groups of 64 threads); its JB
+// blocks j0 = g*JB, g*JB + 4*JB, ... (4 row groups of 64 threads, JB = 8); its JB
 // consecutive outputs per order sit in registers, and the taps are kernel
 // parameters (uniform-register operands of DFMA).
 struct TileMeta {
@@ -351,36 +350,38 @@ __device__ inline void tp_conv_cols(const double* Y, int n1, int n2, int ld, dou
 
 template <int R>
 __global__ void __launch_bounds__(kThreads) k_tphase2(const double* __restrict__ pw, const double* __restrict__ pv,
-                                                      i64 rows, int n1, int n2, TPhaseOut out, Taps2P tp) {
+                                                      i64 rows, int n1, int n2, int value_only, TPhaseOut out,
+                                                      Taps2P tp) {
   extern __shared__ double sm[];
   const int ld = n2 + 1;
   const int pe = n1 * ld;  // padded plane
   double* Y = sm + 2 * pe;
   const i64 plane = static_cast<i64>(n1) * n2;
-  // Planes of this CTA in order: (s, pw), (s, pv), (s + grid, pw), ...; the
-  // next plane is copied into the other X buffer (cp.async, 8-byte granules
-  // because of the bank-conflict padding) while the current one is convolved.
-  auto issue = [&](i64 q, int buf) {
-    const i64 s = q >> 1;
-    const double* src = ((q & 1) ? pv : pw) + s * plane;
+  // Planes of this CTA in order: (s, pw), (s, pv), (s + grid, pw), ... (only
+  // the pv planes when value_only); the next plane is copied into the other X
+  // buffer (cp.async, 8-byte granules because of the bank-conflict padding)
+  // while the current one is convolved.
+  auto issue = [&](i64 s, int pass, int buf) {
+    const double* src = (pass ? pv : pw) + s * plane;
     double* X = sm + buf * pe;
     for (int e = threadIdx.x; e < plane; e += blockDim.x) cp_async_c8(X + (e / n2) * ld + e % n2, src + e, 8);
   };
-  const i64 q_end = 2 * rows;
-  const i64 q_step = 2 * static_cast<i64>(gridDim.x);
-  i64 q = 2 * static_cast<i64>(blockIdx.x);
+  const int first_pass = value_only ? 1 : 0;
+  i64 s = blockIdx.x;
+  int pass = first_pass;
   int buf = 0;
-  if (q < q_end) issue(q, 0);
+  if (s < rows) issue(s, pass, 0);
   cp_async_commit_c();
-  while (q < q_end) {
-    const i64 next = (q & 1) ? q - 1 + q_step : q + 1;
-    if (next < q_end) issue(next, buf ^ 1);
+  while (s < rows) {
+    const bool same_row = pass == 0;
+    const i64 ns = same_row ? s : s + gridDim.x;
+    const int npass = same_row ? 1 : first_pass;
+    if (ns < rows) issue(ns, npass, buf ^ 1);
     cp_async_commit_c();
     cp_async_wait_c<1>();
     __syncthreads();
     const double* X = sm + buf * pe;
-    const i64 off = (q >> 1) * plane;
-    const int pass = static_cast<int>(q & 1);
+    const i64 off = s * plane;
     const int max_order = pass == 0 ? 2 : 1;
     for (int r2 = 0; r2 <= max_order; ++r2) {
       if (r2 == 0) tp_conv_rows<R, 0>(X, Y, n1, n2, ld, tp);
@@ -410,7 +411,8 @@ __global__ void __launch_bounds__(kThreads) k_tphase2(const double* __restrict__
       __syncthreads();
     }
     buf ^= 1;
-    q = next;
+    s = ns;
+    pass = npass;
   }
   cp_async_wait_c<0>();
 }
@@ -453,10 +455,10 @@ void launch_tiled(dfpca_context* ctx, const PassSpec& s, const TapsP& tp) {
   // bulk row copies need 16-byte aligned, 16-byte multiple rows
   const bool bulk = (in.os % 2 == 0) && (in.js % 2 == 0) && (in.inner % 2 == 0) &&
                     (reinterpret_cast<std::uintptr_t>(in.p) % 16 == 0);
-  static const bool force_jb8 = std::getenv("DFPCA_PASS_JB8") != nullptr;  // tuning switch
-  if (!bulk) launch_cols<R, NO, 8, false>(ctx, s, o1, o2, tp);
-  else if (in.n <= 32 || force_jb8) launch_cols<R, NO, 8, true>(ctx, s, o1, o2, tp);
-  else launch_cols<R, NO, 16, true>(ctx, s, o1, o2, tp);
+  // JB = 8: measured faster than 16 for every order count at n = 64 (the
+  // 16-output blocks cost occupancy: 156 registers at NO = 3)
+  if (bulk) launch_cols<R, NO, 8, true>(ctx, s, o1, o2, tp);
+  else launch_cols<R, NO, 8, false>(ctx, s, o1, o2, tp);
 }
 
 template <int R>
@@ -476,7 +478,8 @@ void launch_tphase2(dfpca_context* ctx, const TPhase2Spec& s, const Taps2P& tp) 
   const int n1 = static_cast<int>(s.n1), n2 = static_cast<int>(s.n2);
   const std::size_t smem = sizeof(double) * 3 * n1 * (n2 + 1);
   const unsigned grid = persistent_grid(ctx, k_tphase2<R>, smem, s.rows);
-  DFPCA_LAUNCH(ctx, k_tphase2<R>, grid, kThreads, smem, s.pw, s.pv, s.rows, n1, n2, out, tp);
+  DFPCA_LAUNCH(ctx, k_tphase2<R>, grid, kThreads, smem, s.pw, s.pv, s.rows, n1, n2, s.value_only ? 1 : 0, out,
+               tp);
 }
 
 }  // namespace conv_detail

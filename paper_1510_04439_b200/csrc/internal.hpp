@@ -158,6 +158,13 @@ struct dfpca_binned {
   bool has_cov = false;
   // Structure flags computed at binning time.
   bool identical_mass = false;  // every per-sample mass grid bitwise equal
+  // Shared constant design: identical masses, M(s) == shared_m0 > 0 at every
+  // node, and a diagonal-only mass band equal to shared_dm0 at every node (the
+  // GridNodes design: every subject observed once at every node).  Then
+  // pw(u,v) = sw - shared_dm0 [u == v] exactly as the reference builds it,
+  // with sw the ordered sum of (w_i M0) M0 (see smooth.cu, run_covariance).
+  bool shared_const = false;
+  double shared_m0 = 0.0, shared_dm0 = 0.0;
 
   dfpca_gpu::DevBuf<double> mass, wvalue, wsquare;  // G
   dfpca_gpu::DevBuf<double> ps_mass, ps_value;      // n_pair * G
@@ -167,6 +174,11 @@ struct dfpca_binned {
   std::vector<double> pair_weight_h;                // n_pair
   std::vector<std::int64_t> sample_sizes;           // n_samples
 };
+
+namespace dfpca_gpu {
+// Sets identical_mass-derived structure flags (shared_const, shared_m0/dm0).
+void detect_shared_design(dfpca_context* ctx, dfpca_binned* b);
+}  // namespace dfpca_gpu
 
 struct dfpca_surface {
   dfpca_gpu::Grid grid;

@@ -41,6 +41,8 @@ __global__ void k_rank_one(double* __restrict__ pw, const double* __restrict__ m
 //    shared mass grid (identical_mass) M_i(s) = M(s) for every i.
 //  * pv: only the band subtraction (pv never decides emptiness; the SYRK sum
 //    differs from the reference's by reassociation only).
+//  * pw == nullptr: the pv subtraction alone (shared-design covariance, whose
+//    mass moments come in closed form, smooth.cu).
 __global__ void k_band_fix(const double* __restrict__ diag_mass, const double* __restrict__ diag_value,
                            i64 G, int d, i64 codes, DevGrid g, const double* __restrict__ ps_mass,
                            int identical, const double* __restrict__ w, i64 n_pair, double w_seq,
@@ -68,6 +70,10 @@ __global__ void k_band_fix(const double* __restrict__ diag_mass, const double* _
       t += bk * g.strides[k];
     }
     if (!inside) continue;
+    if (pw == nullptr) {  // value grid only (shared-design covariance)
+      if (lane == 0) pv[u * G + t] = __dsub_rn(pv[u * G + t], dv);
+      continue;
+    }
     double sw = 0.0;
     const double ms0 = identical ? ps_mass[u] : 0.0, mt0 = identical ? ps_mass[t] : 0.0;
     // shared unit masses (every subject observed once at both nodes):
@@ -93,8 +99,6 @@ __global__ void k_band_fix(const double* __restrict__ diag_mass, const double* _
   }
 }
 
-// Band subtraction for the rank-one / SYRK result at entries where the band
-// is nonzero is done by k_band_exact; nothing else carries a band.
 
 }  // namespace
 
@@ -113,7 +117,7 @@ void build_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, dou
     }
   }
   if (pv) gemm_tn(ctx, G, G, n, b->ps_value.get(), G, b->pair_weight.get(), b->ps_value.get(), G, pv, G, true);
-  if (pw && pv) {
+  if (pv) {
     DevBuf<double> axes;
     DevGrid dg = upload_grid_axes(ctx, b->grid, axes);
     DFPCA_LAUNCH(ctx, k_band_fix, grid_for(G * b->codes * 32, 256, 148ll * 32), 256, 0,

@@ -180,6 +180,113 @@ __global__ void __launch_bounds__(128) k_solve(MomPtrs mp, SolveGeom g, double* 
   }
 }
 
+// Shared-design covariance solve.  With pw(u,v) = sw - dm0 [u == v] (every
+// subject's mass grid equal to the constant M0 and a diagonal-only band, see
+// dfpca_binned::shared_const), every mass moment is closed-form:
+//   S_ab(s,t) = sw P_a(s) P_b(t) - dm0 D_ab(s,t),
+//   P_a(s)    = prod_k A^k_{a_k}(s_k),  A^k_r(j) = sum_o taps_r[o+R]  (0 <= j+o < n_k)
+//   D_ab(s,t) = prod_k D^k_{a_k b_k}(s_k, t_k),
+//   D^k_ab(x, y) = sum_u taps_a[u-x+R] taps_b[u-y+R],
+// the separable convolution of the constant and of the diagonal, so only the
+// nl value moments come from the convolution pipeline.
+struct SharedMoments {
+  const double* A[kMaxDim];  // [3][n_k]
+  const double* D[kMaxDim];  // [3][3][n_k][n_k]
+  int n[kMaxDim];
+  double sw, dm0;
+};
+
+template <int P>
+__device__ __forceinline__ double shared_moment(const int (&o)[P], const double (&As)[P / 2][3],
+                                                const double (&At)[P / 2][3], const double (&Dst)[P / 2][3][3],
+                                                double sw, double dm0) {
+  constexpr int d = P / 2;
+  double pa = 1.0, pd = 1.0;
+#pragma unroll
+  for (int k = 0; k < d; ++k) {
+    pa *= As[k][o[k]] * At[k][o[d + k]];
+    pd *= Dst[k][o[k]][o[d + k]];
+  }
+  return sw * pa - dm0 * pd;
+}
+
+template <int N>
+__global__ void __launch_bounds__(128) k_solve_shared(SharedMoments sh, MomPtrs mp, SolveGeom g,
+                                                      double* __restrict__ out,
+                                                      unsigned long long* __restrict__ empty_count,
+                                                      i64* __restrict__ empty_list, i64 list_cap) {
+  constexpr int p = N - 1;
+  constexpr int d = p / 2;
+  constexpr int nm = 1 + p + p * (p + 1) / 2;
+  constexpr int nl = 1 + p;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < g.npts; e += (i64)gridDim.x * blockDim.x) {
+    const i64 row = e / g.tc;
+    const i64 col = g.t0 + e % g.tc;
+    const i64 dst = row * g.gt + col;
+    if (g.upper && row > col) continue;
+    if (g.mask && !(g.mask[row] != 0 && g.mask[col] != 0)) {
+      out[dst] = __longlong_as_double(0x7ff8000000000000ll);
+      continue;
+    }
+    // per-axis node coordinates, last axis fastest
+    int sk[d], tk[d];
+    i64 rs = row, rt = col;
+#pragma unroll
+    for (int k = d - 1; k >= 0; --k) {
+      sk[k] = static_cast<int>(rs % sh.n[k]);
+      rs /= sh.n[k];
+      tk[k] = static_cast<int>(rt % sh.n[k]);
+      rt /= sh.n[k];
+    }
+    double As[d][3], At[d][3], Dst[d][3][3];
+#pragma unroll
+    for (int k = 0; k < d; ++k) {
+      const int n = sh.n[k];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        As[k][r] = __ldg(sh.A[k] + r * n + sk[k]);
+        At[k][r] = __ldg(sh.A[k] + r * n + tk[k]);
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          Dst[k][a][b] = a + b <= 2 ? __ldg(sh.D[k] + ((static_cast<i64>(a * 3 + b) * n + sk[k]) * n + tk[k])) : 0.0;
+    }
+    double S[nm], T[nl];
+    {
+      int o[p] = {};
+      S[0] = shared_moment<p>(o, As, At, Dst, sh.sw, sh.dm0);
+    }
+#pragma unroll
+    for (int k = 0; k < p; ++k) {
+      int o[p] = {};
+      o[k] = 1;
+      S[1 + k] = shared_moment<p>(o, As, At, Dst, sh.sw, sh.dm0);
+    }
+#pragma unroll
+    for (int k = 0; k < p; ++k)
+#pragma unroll
+      for (int l = k; l < p; ++l) {
+        int o[p] = {};
+        o[k] += 1;
+        o[l] += 1;
+        S[quad_index(p, k, l)] = shared_moment<p>(o, As, At, Dst, sh.sw, sh.dm0);
+      }
+#pragma unroll
+    for (int i = 0; i < nl; ++i) T[i] = mp.T[i][e];
+    double b0;
+    const int st = solve_local_dev<N>(S, T, b0);
+    if (st == kFitEmpty) {
+      const unsigned long long slot = atomicAdd(empty_count, 1ull);
+      if (static_cast<i64>(slot) < list_cap) empty_list[slot] = dst;
+      out[dst] = __longlong_as_double(0x7ff8000000000000ll);
+    } else {
+      out[dst] = b0;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Empty-window fallback ladder (fft_smoother.hpp:471-487): for each listed
 // node, up to kWindowRetries direct gathers at 1.5^r h over the binned arrays
@@ -336,6 +443,21 @@ void launch_solve(dfpca_context* ctx, const MomPtrs& mp, const SolveGeom& g, dou
   DFPCA_LAUNCH(ctx, k_solve<N>, grid_for(g.npts, 128, 148ll * 64), 128, 0, mp, g, out, cnt, list,
                cap);
 }
+template <int N>
+void launch_solve_shared_n(dfpca_context* ctx, const SharedMoments& sh, const MomPtrs& mp, const SolveGeom& g,
+                           double* out, unsigned long long* cnt, i64* list, i64 cap) {
+  DFPCA_LAUNCH(ctx, k_solve_shared<N>, grid_for(g.npts, 128, 148ll * 64), 128, 0, sh, mp, g, out, cnt, list,
+               cap);
+}
+void launch_solve_shared(int d, dfpca_context* ctx, const SharedMoments& sh, const MomPtrs& mp,
+                         const SolveGeom& g, double* out, unsigned long long* cnt, i64* list, i64 cap) {
+  switch (d) {
+    case 1: launch_solve_shared_n<3>(ctx, sh, mp, g, out, cnt, list, cap); break;
+    case 2: launch_solve_shared_n<5>(ctx, sh, mp, g, out, cnt, list, cap); break;
+    default: launch_solve_shared_n<7>(ctx, sh, mp, g, out, cnt, list, cap); break;
+  }
+}
+
 SolveLauncher solve_launcher(int p) {
   switch (p) {
     case 1: return &launch_solve<2>;
@@ -570,10 +692,72 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
   surf->n = G2;
   surf->values.alloc(static_cast<std::size_t>(G2));
 
+  // Shared constant design (dfpca_binned::shared_const): the reference's pw is
+  // sw - dm0 [u == v] entry by entry, so the mass moments are closed-form
+  // (k_solve_shared) and only pv goes through the pair build and the
+  // convolutions.  Used when every kernel window provably holds an
+  // off-diagonal pair (a positive off-centre tap on some axis of extent >= 2),
+  // i.e. no window can be empty, so the S0 > 0 test can never differ.
+  // (DFPCA_GENERAL_PAIRS=1 forces the general path: A/B parity tests)
+  bool shared = b->shared_const && std::getenv("DFPCA_GENERAL_PAIRS") == nullptr;
+  if (shared) {
+    bool some_axis = false;
+    for (int k = 0; k < d; ++k) {
+      const AxisTaps& a = taps[k];
+      some_axis = some_axis || (grid.shape[k] >= 2 && a.R >= 1 && a.t[0][a.R + 1] > 0.0 && a.t[0][a.R - 1] > 0.0);
+    }
+    shared = some_axis;
+  }
+  SharedMoments sh{};
+  DevBuf<double> sh_tab;
+  std::vector<double> sh_host;
+  if (shared) {
+    double sw = 0.0;  // the reference's off-band pw entry: ordered sum of (w_i M0) M0
+    for (double w : b->pair_weight_h) sw = sw + (w * b->shared_m0) * b->shared_m0;
+    sh.sw = sw;
+    sh.dm0 = b->shared_dm0;
+    std::vector<std::size_t> offA(d), offD(d);
+    for (int k = 0; k < d; ++k) {
+      const i64 n = grid.shape[k];
+      offA[k] = sh_host.size();
+      sh_host.resize(sh_host.size() + 3 * n, 0.0);
+      offD[k] = sh_host.size();
+      sh_host.resize(sh_host.size() + 9 * n * n, 0.0);
+      const AxisTaps& ts = taps[k];
+      const AxisTaps& tt = taps[d + k];
+      const i64 R = ts.R, Rt = tt.R;
+      for (int r = 0; r < 3; ++r)
+        for (i64 j = 0; j < n; ++j) {
+          double acc = 0.0;
+          for (i64 o = -R; o <= R; ++o)
+            if (j + o >= 0 && j + o < n) acc += ts.t[r][o + R];
+          sh_host[offA[k] + r * n + j] = acc;
+        }
+      for (int a = 0; a < 3; ++a)
+        for (int c = 0; a + c <= 2 && c < 3; ++c)
+          for (i64 x = 0; x < n; ++x)
+            for (i64 y = 0; y < n; ++y) {
+              double acc = 0.0;
+              const i64 lo = std::max<i64>({0, x - R, y - Rt}), hi = std::min<i64>({n - 1, x + R, y + Rt});
+              for (i64 u = lo; u <= hi; ++u) acc += ts.t[a][u - x + R] * tt.t[c][u - y + Rt];
+              sh_host[offD[k] + ((a * 3 + c) * n + x) * n + y] = acc;
+            }
+      sh.n[k] = static_cast<int>(n);
+    }
+    sh_tab.alloc(sh_host.size());
+    DFPCA_CUDA(cudaMemcpyAsync(sh_tab.get(), sh_host.data(), sizeof(double) * sh_host.size(),
+                               cudaMemcpyHostToDevice, st));
+    for (int k = 0; k < d; ++k) {
+      sh.A[k] = sh_tab.get() + offA[k];
+      sh.D[k] = sh_tab.get() + offD[k];
+    }
+  }
+
   // ---- pair grids (K2) ----
-  DevBuf<double> pw(static_cast<std::size_t>(G2)), pv(static_cast<std::size_t>(G2));
+  DevBuf<double> pw, pv(static_cast<std::size_t>(G2));
+  if (!shared) pw.alloc(static_cast<std::size_t>(G2));
   ctx->begin_stage("pairs");
-  build_pair_grids(ctx, b, pw.get(), pv.get());
+  build_pair_grids(ctx, b, shared ? nullptr : pw.get(), pv.get());
   ctx->end_stage();
 
   // ---- phase T: t-axis passes over row chunks of the pair grids ----
@@ -598,6 +782,7 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
         };
     rec(d, Orders{}, 0, 2, mass_idx);
     rec(d, Orders{}, 0, 1, val_idx);
+    if (shared) mass_idx.clear();
     for (auto& o : mass_idx) {
       tpart_store.push_back(std::make_unique<DevBuf<double>>(static_cast<std::size_t>(G2)));
       tpart[{o, 2}] = tpart_store.back()->get();
@@ -618,22 +803,31 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
     cd.rows = rows;
     for (int k = d; k < p; ++k) cd.shape.push_back(grid.shape[k - d]);
     cd.tail = 1;
-    std::vector<Leaf> roots(2);
-    roots[0].budget_max = 2;
-    roots[0].ptr = pw.get() + s0 * G;
-    roots[1].budget_max = 1;
-    roots[1].ptr = pv.get() + s0 * G;
+    std::vector<Leaf> roots;
+    if (!shared) {
+      Leaf r{};
+      r.budget_max = 2;
+      r.ptr = pw.get() + s0 * G;
+      roots.push_back(r);
+    }
+    {
+      Leaf r{};
+      r.budget_max = 1;
+      r.ptr = pv.get() + s0 * G;
+      roots.push_back(r);
+    }
     if (d == 2) {
       // fused two-axis t-phase: the 64x64 t-plane of a row never leaves smem
       TPhase2Spec ts{};
-      ts.pw = pw.get() + s0 * G;
+      ts.value_only = shared;
+      ts.pw = shared ? nullptr : pw.get() + s0 * G;
       ts.pv = pv.get() + s0 * G;
       ts.rows = rows;
       ts.n1 = grid.shape[0];
       ts.n2 = grid.shape[1];
       const int mo[6][2] = {{0, 0}, {1, 0}, {2, 0}, {0, 1}, {1, 1}, {0, 2}};
       const int vo[3][2] = {{0, 0}, {1, 0}, {0, 1}};
-      for (int i = 0; i < 6; ++i) {
+      for (int i = 0; i < 6 && !shared; ++i) {
         Orders o{};
         o[2] = mo[i][0];
         o[3] = mo[i][1];
@@ -780,7 +974,8 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
       sg.cov = 1;
       sg.upper = 1;
       sg.mask = grid.has_mask ? mask_dev.get() : nullptr;
-      solve_launcher(p)(ctx, mp, sg, surf->values.get(), cnt.get(), list.get(), list_cap);
+      if (shared) launch_solve_shared(d, ctx, sh, mp, sg, surf->values.get(), cnt.get(), list.get(), list_cap);
+      else solve_launcher(p)(ctx, mp, sg, surf->values.get(), cnt.get(), list.get(), list_cap);
       continue;
     }
     std::vector<Leaf> leaves = run_tree(ctx, roots, saxes, cd, taps, chunk_elems, taps_dev.get(), keep,
@@ -801,7 +996,8 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
     sg.mask = grid.has_mask ? mask_dev.get() : nullptr;
     ctx->end_stage();
     ctx->begin_stage("solve");
-    solve_launcher(p)(ctx, mp, sg, surf->values.get(), cnt.get(), list.get(), list_cap);
+    if (shared) launch_solve_shared(d, ctx, sh, mp, sg, surf->values.get(), cnt.get(), list.get(), list_cap);
+    else solve_launcher(p)(ctx, mp, sg, surf->values.get(), cnt.get(), list.get(), list_cap);
     ctx->end_stage();
     ctx->begin_stage("moments");
   }
@@ -816,6 +1012,10 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
       fail(kNumeric, "BandwidthTooSmall",
            "binned covariance smoother: too many empty kernel windows");
     ctx->begin_stage("fallback");
+    if (shared) {  // not reachable by construction; rebuild both grids for the gathers
+      pw.alloc(static_cast<std::size_t>(G2));
+      build_pair_grids(ctx, b, pw.get(), pv.get());
+    }
     LadderGeom lg{};
     lg.p = p;
     for (int k = 0; k < p; ++k) {

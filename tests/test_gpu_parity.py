@@ -188,7 +188,11 @@ def test_local_linear(api, ref, case, target):
 COV_CASES = {
     "1d": lambda s: s.random_points(1, 26, 30, 8, 0.2),
     "1d_fft_taps": lambda s: s.random_points(1, 61, 12, 10, 0.3),
+    "1d_nodes": lambda s: s.grid_nodes(1, 40, 30, 0.1),
     "2d_nodes": lambda s: s.grid_nodes(2, 12, 25, 0.2),
+    # h < spacing: only the centre tap is positive, so the diagonal windows of
+    # the shared design are empty and go through the fallback ladder
+    "2d_nodes_narrow": lambda s: s.grid_nodes(2, 8, 20, 0.1),
     "2d_random": lambda s: s.random_points(2, 10, 40, 15, 0.3),
     "2d_masked_sparse": lambda s: s.sparse_masked(14, 120, 0.3),
     "3d_nodes": lambda s: s.grid_nodes(3, 5, 10, 0.45),
@@ -211,6 +215,32 @@ def test_covariance(api, ref, case):
     M = cov_g.reshape(G, G)
     fin = ~np.isnan(M)
     assert np.array_equal(M[fin], M.T[fin])  # exact symmetry (test_fft_smoother.cpp:154-158)
+
+
+@pytest.mark.parametrize("dim,cells,n,h", [(1, 50, 20, 0.1), (2, 12, 25, 0.2), (3, 5, 8, 0.45)])
+def test_shared_design_closed_form_matches_general_path(api, dim, cells, n, h, monkeypatch):
+    """GridNodes designs take the closed-form mass moments (k_solve_shared);
+    DFPCA_GENERAL_PAIRS=1 forces the pair-grid convolution path on the same
+    input.  Both must agree to the parity bar and the shared path must be the
+    one that ran."""
+    from paper_1510_04439_b200 import _lib, synth
+    sd = synth.grid_nodes(dim, cells, n, h)
+    grid = sd.grid()
+    b = api.linear_bin(sd.dataset(), grid, api.BinOptions(True, True))
+    hh = api.Bandwidth(sd.h)
+    mean = api.fft_local_linear(b, grid, hh, api.MomentTarget.Mean)
+    _lib.profile(True)
+    fast = api.fft_covariance(b, grid, hh, mean).values
+    names = set(_lib.kernel_stats())
+    _lib.profile(False)
+    assert any(k.startswith("k_solve_shared") for k in names), names
+    monkeypatch.setenv("DFPCA_GENERAL_PAIRS", "1")
+    _lib.profile(True)
+    general = api.fft_covariance(b, grid, hh, mean).values
+    names = set(_lib.kernel_stats())
+    _lib.profile(False)
+    assert not any(k.startswith("k_solve_shared") for k in names), names
+    assert rel_surface_diff(fast, general) <= TOL
 
 
 def test_block_plans_are_invariant(api):

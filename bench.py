@@ -326,6 +326,7 @@ def main():
         "e2e": {"value": world * G2 / e2e_step, "unit": "gridpts/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_step * 1e3,
                 "breakdown_ms": {k: v * 1e3 for k, v in brk.items()},
+                "all_ms": [round(t * 1e3, 3) for t in e2e_t],
                 "path": "pinned host obs -> linear_bin -> fft_local_linear -> fft_covariance -> host covariance",
                 "pinned": all(pinned)},
         "fpca_e2e_ms": fpca_ms, "eigen_ms": eig_ms, "eig_top3": eig.eigenvalues[:3],
@@ -358,7 +359,7 @@ def tri_fractions(cells: int, R: int, tile: int = 32):
     return rows_in / (n1 * G), rows_out / (n1 * G), upper
 
 
-def kernel_model(G: int, n_pair: int):
+def kernel_model(G: int, n_pair: int, shared: bool):
     """Algorithmic work per step of every kernel of the d = 2 covariance step
     (DESIGN.md 'Roofline model'); one array = G^2 doubles.
 
@@ -371,10 +372,26 @@ def kernel_model(G: int, n_pair: int):
                           s1 level: 14 in (trimmed rows) + 20 out (s <= t rows)
     solve   k_solve       20 moments in + 1 out at s <= t
     center  k_center_mirror  read s <= t, write both triangles
+
+    shared: the shared-constant design (every subject observed at every node,
+    the bench's GridNodes workload): the mass moments are closed-form
+    (k_solve_shared), pw is never built, only pv is convolved:
+    t-phase   read pv, write 3 value t-partials              4 arrays
+    s-phase   s2: 3 in + 4 out (trimmed rows); s1: 4 in + 5 out (s <= t rows)
+    solve     5 value moments in + 1 out at s <= t
     """
     cells = int(round(G ** 0.5))
     f_in, f_out, upper = tri_fractions(cells, int(np.ceil(H * cells)))
     arr = 8.0 * G * G
+    if shared:
+        return {
+            "k_gemm_tn": ("tensor", 2.0 * n_pair * G * G / 2.0),
+            "k_scale_rows": ("hbm", 2 * 8.0 * n_pair * G),
+            "k_tphase2": ("hbm", 4 * arr),
+            "k_pass_cols": ("hbm", ((3 + 4) * f_in + 4 * f_in + 5 * f_out) * arr),
+            "k_solve_shared": ("hbm", 6 * upper * arr),
+            "k_center_mirror": ("hbm", (upper + 1.0) * arr),
+        }
     return {
         "k_gemm_tn": ("tensor", 2.0 * n_pair * G * G / 2.0),
         "k_rank_one": ("hbm", 1 * arr),
@@ -386,6 +403,29 @@ def kernel_model(G: int, n_pair: int):
     }
 
 
+def ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum (bytes) of one launch of
+    `kernel` from the newest committed `ncu --set full` summary
+    (profiles/rNN_ncu_full_summary.txt, written by tools/ncu_summary.py full;
+    values in Mbyte as ncu reports them), or (None, None)."""
+    files = sorted((ROOT / "profiles").glob("r*_ncu_full_summary.txt"))
+    if not files:
+        return None, None
+    cur, vals = None, {}
+    for line in files[-1].read_text().splitlines():
+        if line.startswith("== "):
+            cur = line[3:].strip()
+            continue
+        parts = line.split()
+        if cur and len(parts) == 2 and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            base = cur.split("<")[0].split("::")[-1]
+            if base == kernel and (cur, parts[0]) not in vals:
+                vals[(cur, parts[0])] = float(parts[1]) * 1e6
+    if not vals:
+        return None, None
+    return sum(vals.values()), f"{files[-1].relative_to(ROOT)} (first launch of {kernel})"
+
+
 def roofline(kstats, G, binned):
     """Dominant kernel (largest device time in one profiled step) against its
     bound, plus the same figure for every modelled kernel."""
@@ -393,7 +433,7 @@ def roofline(kstats, G, binned):
     hbm = peaks.get("hbm_gbs")
     if not kstats:
         return None
-    model = kernel_model(G, N_SUBJ)
+    model = kernel_model(G, N_SUBJ, shared="k_solve_shared" in kstats)
     total_ms = sum(v[0] for v in kstats.values())
     table = {}
     for name, (ms, cnt) in kstats.items():
@@ -414,7 +454,7 @@ def roofline(kstats, G, binned):
     dom = max(table, key=lambda k: table[k]["ms"])
     d = dict(table[dom])
     d["kernel"] = dom
-    d["traffic"] = None  # dram bytes per launch from ncu --set full: profiles/ncu_r01.md
+    d["traffic"], d["traffic_source"] = ncu_traffic(dom)
     d["algorithmic_per_launch"] = model[dom][1] / table[dom]["launches"]
     d["peak_source"] = ("measured FP64 DMMA peak (tools/fp64_peak.cu, profiles/fp64_peak_r01.txt)"
                         if d["bound"] == "tensor" else "MEASURED_PEAKS.json hbm_gbs (measured copy)")

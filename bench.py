@@ -389,7 +389,7 @@ def kernel_model(G: int, n_pair: int, shared: bool):
             "k_scale_rows": ("hbm", 2 * 8.0 * n_pair * G),
             "k_tphase2": ("hbm", 4 * arr),
             "k_pass_cols": ("hbm", ((3 + 4) * f_in + 4 * f_in + 5 * f_out) * arr),
-            "k_solve_shared": ("hbm", 6 * upper * arr),
+            "k_solve_shared_tri": ("hbm", 6 * upper * arr),
             "k_center_mirror": ("hbm", (upper + 1.0) * arr),
         }
     return {
@@ -398,7 +398,7 @@ def kernel_model(G: int, n_pair: int, shared: bool):
         "k_scale_rows": ("hbm", 2 * 8.0 * n_pair * G),
         "k_tphase2": ("hbm", 11 * arr),
         "k_pass_cols": ("hbm", ((9 + 14) * f_in + 14 * f_in + 20 * f_out) * arr),
-        "k_solve": ("hbm", 21 * upper * arr),
+        "k_solve_tri": ("hbm", 21 * upper * arr),
         "k_center_mirror": ("hbm", (upper + 1.0) * arr),
     }
 
@@ -433,7 +433,7 @@ def roofline(kstats, G, binned):
     hbm = peaks.get("hbm_gbs")
     if not kstats:
         return None
-    model = kernel_model(G, N_SUBJ, shared="k_solve_shared" in kstats)
+    model = kernel_model(G, N_SUBJ, shared="k_solve_shared_tri" in kstats)
     total_ms = sum(v[0] for v in kstats.values())
     table = {}
     for name, (ms, cnt) in kstats.items():

@@ -287,6 +287,114 @@ __global__ void __launch_bounds__(128) k_solve_shared(SharedMoments sh, MomPtrs 
   }
 }
 
+// Upper-triangle covariance solve, tiled: CTA (row, 128-column chunk) with
+// 32-bit index math.  The s node is uniform across the CTA (its coordinates,
+// P_a(s) and the D rows are broadcast loads), the t nodes are consecutive
+// (coalesced moment loads and stores); CTAs whose chunk lies left of the
+// diagonal exit at once.  Same per-point arithmetic as k_solve /
+// k_solve_shared.
+constexpr int kSolveTile = 128;
+
+template <int N, bool SHARED>
+__device__ __forceinline__ void solve_tri_body(const SharedMoments& sh, const MomPtrs& mp, const SolveGeom& g,
+                                               int nch, double* __restrict__ out,
+                                               unsigned long long* __restrict__ empty_count,
+                                               i64* __restrict__ empty_list, i64 list_cap) {
+  constexpr int p = N - 1;
+  constexpr int d = p / 2;
+  constexpr int nm = 1 + p + p * (p + 1) / 2;
+  constexpr int nl = 1 + p;
+  const int row = static_cast<int>(blockIdx.x / nch);
+  const int ch = static_cast<int>(blockIdx.x - static_cast<unsigned>(row) * nch);
+  const int tc = static_cast<int>(g.tc);
+  const int t0 = static_cast<int>(g.t0);
+  if (t0 + (ch + 1) * kSolveTile <= row) return;  // whole chunk below the diagonal
+  const int c = ch * kSolveTile + static_cast<int>(threadIdx.x);
+  const int col = t0 + c;
+  if (c >= tc || col < row) return;
+  const i64 e = static_cast<i64>(row) * tc + c;
+  const i64 dst = static_cast<i64>(row) * g.gt + col;
+  if (g.mask && !(g.mask[row] != 0 && g.mask[col] != 0)) {
+    out[dst] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  double S[nm], T[nl];
+  if constexpr (SHARED) {
+    int sk[d], tk[d];
+    int rs = row, rt = col;
+#pragma unroll
+    for (int k = d - 1; k >= 0; --k) {
+      const int n = sh.n[k];
+      const int qs = rs / n, qt = rt / n;
+      sk[k] = rs - qs * n;
+      tk[k] = rt - qt * n;
+      rs = qs;
+      rt = qt;
+    }
+    double As[d][3], At[d][3], Dst[d][3][3];
+#pragma unroll
+    for (int k = 0; k < d; ++k) {
+      const int n = sh.n[k];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        As[k][r] = __ldg(sh.A[k] + r * n + sk[k]);
+        At[k][r] = __ldg(sh.A[k] + r * n + tk[k]);
+      }
+      const double* Dk = sh.D[k] + sk[k] * n + tk[k];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) Dst[k][a][b] = a + b <= 2 ? __ldg(Dk + (a * 3 + b) * n * n) : 0.0;
+    }
+    {
+      int o[p] = {};
+      S[0] = shared_moment<p>(o, As, At, Dst, sh.sw, sh.dm0);
+    }
+#pragma unroll
+    for (int k = 0; k < p; ++k) {
+      int o[p] = {};
+      o[k] = 1;
+      S[1 + k] = shared_moment<p>(o, As, At, Dst, sh.sw, sh.dm0);
+    }
+#pragma unroll
+    for (int k = 0; k < p; ++k)
+#pragma unroll
+      for (int l = k; l < p; ++l) {
+        int o[p] = {};
+        o[k] += 1;
+        o[l] += 1;
+        S[quad_index(p, k, l)] = shared_moment<p>(o, As, At, Dst, sh.sw, sh.dm0);
+      }
+  } else {
+#pragma unroll
+    for (int i = 0; i < nm; ++i) S[i] = mp.S[i][e];
+  }
+#pragma unroll
+  for (int i = 0; i < nl; ++i) T[i] = mp.T[i][e];
+  double b0;
+  __shared__ double sm_solve[(nm + nl) * kSolveTile];
+  const int st = solve_local_perm<N>(S, T, sm_solve + threadIdx.x, kSolveTile, b0);
+  if (st == kFitEmpty) {
+    const unsigned long long slot = atomicAdd(empty_count, 1ull);
+    if (static_cast<i64>(slot) < list_cap) empty_list[slot] = dst;
+    out[dst] = __longlong_as_double(0x7ff8000000000000ll);
+  } else {
+    out[dst] = b0;
+  }
+}
+template <int N>
+__global__ void __launch_bounds__(kSolveTile) k_solve_tri(MomPtrs mp, SolveGeom g, int nch, double* __restrict__ out,
+                                                          unsigned long long* __restrict__ empty_count,
+                                                          i64* __restrict__ empty_list, i64 list_cap) {
+  solve_tri_body<N, false>(SharedMoments{}, mp, g, nch, out, empty_count, empty_list, list_cap);
+}
+template <int N>
+__global__ void __launch_bounds__(kSolveTile)
+    k_solve_shared_tri(SharedMoments sh, MomPtrs mp, SolveGeom g, int nch, double* __restrict__ out,
+                       unsigned long long* __restrict__ empty_count, i64* __restrict__ empty_list, i64 list_cap) {
+  solve_tri_body<N, true>(sh, mp, g, nch, out, empty_count, empty_list, list_cap);
+}
+
 // ---------------------------------------------------------------------------
 // Empty-window fallback ladder (fft_smoother.hpp:471-487): for each listed
 // node, up to kWindowRetries direct gathers at 1.5^r h over the binned arrays
@@ -402,13 +510,18 @@ __global__ void k_center_mirror(double* __restrict__ cov, const double* __restri
                                 const std::uint8_t* __restrict__ mask, i64 G) {
   __shared__ double tile[32][33];
   const i64 tiles = (G + 31) / 32;
-  i64 t = blockIdx.x;  // tile pairs (I <= J)
-  i64 I = 0;
-  while (t >= tiles - I) {
-    t -= tiles - I;
-    ++I;
-  }
-  const i64 J = I + t;
+  // tile pair (I <= J) of this CTA: row I starts at pair index
+  // start(I) = I * tiles - I (I - 1) / 2; invert with a square root, then fix
+  // the rounding
+  const i64 t = blockIdx.x;
+  auto start = [tiles](i64 i) { return i * tiles - i * (i - 1) / 2; };
+  const double tb = 2.0 * static_cast<double>(tiles) + 1.0;
+  i64 I = static_cast<i64>((tb - sqrt(tb * tb - 8.0 * static_cast<double>(t))) * 0.5);
+  if (I < 0) I = 0;
+  if (I > tiles - 1) I = tiles - 1;
+  while (I > 0 && start(I) > t) --I;
+  while (I + 1 < tiles && start(I + 1) <= t) ++I;
+  const i64 J = I + (t - start(I));
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8 threads
   for (int r = ty; r < 32; r += 8) {
     const i64 a = I * 32 + r, b = J * 32 + tx;
@@ -437,15 +550,34 @@ namespace {
 
 using SolveLauncher = void (*)(dfpca_context*, const MomPtrs&, const SolveGeom&, double*,
                                unsigned long long*, i64*, i64);
+// Tiled upper-triangle launch geometry: (rows x chunks) CTAs, or 0 when the
+// chunk does not qualify (not the upper covariance, or too many CTAs).
+inline i64 tri_ctas(const SolveGeom& g, int& nch) {
+  if (!(g.cov && g.upper) || g.tc <= 0 || g.gt > (i64(1) << 30)) return 0;
+  nch = static_cast<int>((g.tc + kSolveTile - 1) / kSolveTile);
+  const i64 n = (g.npts / g.tc) * nch;
+  return n < (i64(1) << 31) ? n : 0;
+}
 template <int N>
 void launch_solve(dfpca_context* ctx, const MomPtrs& mp, const SolveGeom& g, double* out,
                   unsigned long long* cnt, i64* list, i64 cap) {
+  int nch = 0;
+  if (const i64 n = tri_ctas(g, nch)) {
+    DFPCA_LAUNCH(ctx, k_solve_tri<N>, static_cast<unsigned>(n), kSolveTile, 0, mp, g, nch, out, cnt, list, cap);
+    return;
+  }
   DFPCA_LAUNCH(ctx, k_solve<N>, grid_for(g.npts, 128, 148ll * 64), 128, 0, mp, g, out, cnt, list,
                cap);
 }
 template <int N>
 void launch_solve_shared_n(dfpca_context* ctx, const SharedMoments& sh, const MomPtrs& mp, const SolveGeom& g,
                            double* out, unsigned long long* cnt, i64* list, i64 cap) {
+  int nch = 0;
+  if (const i64 n = tri_ctas(g, nch)) {
+    DFPCA_LAUNCH(ctx, k_solve_shared_tri<N>, static_cast<unsigned>(n), kSolveTile, 0, sh, mp, g, nch, out, cnt,
+                 list, cap);
+    return;
+  }
   DFPCA_LAUNCH(ctx, k_solve_shared<N>, grid_for(g.npts, 128, 148ll * 64), 128, 0, sh, mp, g, out, cnt, list,
                cap);
 }

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--n", type=int, default=2000)
     ap.add_argument("--h", type=float, default=0.1)
     ap.add_argument("--dim", type=int, default=2)
+    ap.add_argument("--stats", action="store_true", help="per-kernel device times (event-bracketed launches)")
     a = ap.parse_args()
     sd = synth.grid_nodes(a.dim, a.cells, a.n, a.h)
     grid = sd.grid()
@@ -29,8 +30,14 @@ def main():
     b = api.linear_bin(sd.dataset(), grid, api.BinOptions(True, True))
     mean = api.fft_local_linear(b, grid, h, api.MomentTarget.Mean)
     print("setup launches", _lib.kernel_launches(), flush=True)
-    for _ in range(a.steps):
+    for i in range(a.steps):
+        if a.stats and i == a.steps - 1:
+            _lib.profile(True)
         c = api.fft_covariance(b, grid, h, mean)
+        if a.stats and i == a.steps - 1:
+            for k, (ms, cnt) in sorted(_lib.kernel_stats().items(), key=lambda kv: -kv[1][0]):
+                print(f"  {k:40s} {cnt:5d} launches {ms:10.3f} ms", flush=True)
+            _lib.profile(False)
         print("step total ms", _lib.stage_ms("total"), "launches", _lib.kernel_launches(), flush=True)
         del c
 

@@ -1,0 +1,96 @@
+#!/usr/bin/env python3
+"""Run BASELINE.json's configs end to end on one GPU through the public API
+(linear_bin -> fft_local_linear -> fft_covariance -> randomized_eig) and print
+one JSON line per config with the stage times and size-independent checks
+(exact covariance symmetry, NaN pattern = mask, finite in-mask values,
+eigenvalues descending, Riemann orthonormality of the eigenfunctions).
+
+    python tools/run_configs.py [--configs 2,3,4,5]
+"""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+from paper_1510_04439_b200 import _lib, api, synth  # noqa: E402
+
+CONFIGS = {
+    1: ("d=1 n=200 100-pt grid", lambda: synth.grid_nodes(1, 100, 200, 0.025)),
+    2: ("d=2 n=500 32x32", lambda: synth.grid_nodes(2, 32, 500, 0.1)),
+    3: ("d=2 n=2000 64x64", lambda: synth.grid_nodes(2, 64, 2000, 0.1)),
+    4: ("d=2 sparse masked 64x64 n=2000", lambda: synth.sparse_masked(64, 2000, 0.15)),
+    5: ("d=3 n=1000 32^3", lambda: synth.grid_nodes(3, 32, 1000, 0.1)),
+}
+
+
+def run(cfg: int, q: int, L: int):
+    name, make = CONFIGS[cfg]
+    t0 = time.perf_counter()
+    sd = make()
+    gen_s = time.perf_counter() - t0
+    grid = sd.grid()
+    h = api.Bandwidth(sd.h)
+    data = sd.dataset()
+    out = {"config": cfg, "name": name, "G": grid.size(), "gridpts": grid.size() ** 2,
+           "n_obs": int(sd.offsets[-1]), "gen_s": round(gen_s, 2)}
+    t = {}
+    t0 = time.perf_counter()
+    b = api.linear_bin(data, grid, api.BinOptions(True, True))
+    t["linear_bin_ms"] = (time.perf_counter() - t0) * 1e3
+    t0 = time.perf_counter()
+    mean = api.fft_local_linear(b, grid, h, api.MomentTarget.Mean)
+    t["mean_ms"] = (time.perf_counter() - t0) * 1e3
+    covs = []
+    for _ in range(2):  # second call is warm
+        t0 = time.perf_counter()
+        cov = api.fft_covariance(b, grid, h, mean)
+        covs.append((time.perf_counter() - t0) * 1e3)
+        stages = {s: _lib.stage_ms(s) for s in ("pairs", "moments", "solve", "fallback", "center", "total")}
+        if len(covs) == 1:
+            del cov
+    t["covariance_ms_cold"], t["covariance_ms"] = covs
+    t["covariance_device_ms"] = stages
+    out["gridpts_per_s"] = grid.size() ** 2 / (stages["total"] / 1e3)
+    t0 = time.perf_counter()
+    eig = api.randomized_eig(api.matrixize(cov), q, L, grid, 20260815)
+    t["eig_ms"] = (time.perf_counter() - t0) * 1e3
+    out["times"] = t
+    G = grid.size()
+    checks = {}
+    if G * G * 8 <= (2 << 30):
+        C = cov.values.reshape(G, G)
+        m = np.ones(G, bool) if sd.mask is None else np.asarray(sd.mask, bool)
+        inside = np.outer(m, m)
+        checks["exact_symmetry"] = bool(np.array_equal(C.view(np.uint64), C.T.view(np.uint64)))
+        checks["nan_pattern_is_mask"] = bool(np.array_equal(np.isnan(C), ~inside))
+        checks["finite_inside"] = bool(np.isfinite(C[inside]).all())
+        del C
+    ev = np.asarray(eig.eigenvalues)
+    checks["eigenvalues_descending"] = bool(np.all(np.diff(ev) <= 0))
+    Phi = np.asarray(eig.eigenfunctions).reshape(len(ev), G)
+    keep = ~np.isnan(Phi[0])
+    cv = grid.cell_volume()
+    gram = (Phi[:, keep] * cv) @ Phi[:, keep].T
+    checks["riemann_orthonormality_err"] = float(np.max(np.abs(gram - np.eye(len(ev)))))
+    out["eig_top4"] = ev[:4].tolist()
+    out["checks"] = checks
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="2,3,4,5")
+    ap.add_argument("--q", type=int, default=99)
+    ap.add_argument("--L", type=int, default=20)
+    a = ap.parse_args()
+    for c in [int(x) for x in a.configs.split(",")]:
+        run(c, a.q, a.L)
+
+
+if __name__ == "__main__":
+    main()

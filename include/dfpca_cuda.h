@@ -138,6 +138,40 @@ DFPCA_API int dfpca_covariance(dfpca_context* ctx, const dfpca_binned* b, const 
                      const double* h, const double* mean, const dfpca_plan* plan,
                      dfpca_surface** out);
 
+/* ---- multi-GPU: slab-sharded covariance ------------------------------------
+ * The reference runs fft_covariance (fft_smoother.hpp:585-744) on one host
+ * with set_max_threads (parallel.hpp:23) as its only parallel knob; here one
+ * process per GPU holds one context, the ranks share an NCCL communicator, and
+ * the 2d-dim grids are split into s1-plane slabs.
+ * dfpca_nccl_unique_id fills 128 bytes on one rank; the caller broadcasts
+ * them (e.g. torch.distributed) and every rank calls dfpca_nccl_init.
+ * libnccl.so.2 is loaded at run time (DFPCA_NCCL_LIB overrides the path). */
+DFPCA_API int dfpca_nccl_unique_id(void* id128);
+DFPCA_API int dfpca_nccl_init(dfpca_context* ctx, int world, int rank, const void* id128);
+/* Collective over the ranks of dfpca_nccl_init (same arguments on every rank;
+ * binned data and mean are replicated).  *out receives this rank's slab:
+ * complete, exactly symmetric rows [row0, row0 + rows) of the covariance
+ * (dfpca_surface_rows).  Results are bit-identical to dfpca_covariance for
+ * any rank count.  Without dfpca_nccl_init it equals dfpca_covariance. */
+DFPCA_API int dfpca_covariance_sharded(dfpca_context* ctx, const dfpca_binned* b, const dfpca_grid* grid,
+                             const double* h, const double* mean, const dfpca_plan* plan,
+                             dfpca_surface** out);
+/* The same decomposition with `world` ranks as threads of this process on
+ * ctx's device (validation); the slabs are assembled into one G*G surface. */
+DFPCA_API int dfpca_covariance_emulated(dfpca_context* ctx, const dfpca_binned* b, const dfpca_grid* grid,
+                              const double* h, const double* mean, const dfpca_plan* plan, int world,
+                              dfpca_surface** out);
+/* Rows of the covariance held by a surface (a slab, or 0 / G). */
+DFPCA_API int dfpca_surface_rows(const dfpca_surface* s, int64_t* row0, int64_t* rows);
+/* Host-side slab plan (no device needed): bounds[0..world] are the s1-plane
+ * boundaries for n1 planes of nodes_per_plane nodes and an s1 stencil radius. */
+DFPCA_API int dfpca_shard_bounds(int64_t n1, int64_t nodes_per_plane, int64_t radius, int world,
+                       int64_t* bounds);
+/* Exchange schedule of phase 0 (pair-grid windows) or 1 (covariance rows):
+ * 7 int64 per block (src, dst, r0, r1, c0, c1, transpose), see shard.hpp. */
+DFPCA_API int dfpca_shard_blocks(int64_t n1, int64_t nodes_per_plane, int64_t radius, int world, int phase,
+                       int64_t* out, int64_t capacity, int64_t* count);
+
 /* Pair-product grids pw / pv over the full 2d-dim product grid
  * (PairGridSource::extract of the full box, fft_smoother.hpp:341-437);
  * G*G host doubles each, either may be NULL. */

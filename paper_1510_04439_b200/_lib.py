@@ -60,6 +60,15 @@ SIGNATURES = [
     ("dfpca_randomized_eig", C.c_int, [P, P, C.POINTER(DfpcaGrid), C.c_int64, C.c_int64, C.c_uint64, PD, PD,
                                        PD, PD, PI64]),
     ("dfpca_eig_residuals", C.c_int, [P, P, C.POINTER(DfpcaGrid), C.c_int64, PD, PD, PD]),
+    ("dfpca_nccl_unique_id", C.c_int, [P]),
+    ("dfpca_nccl_init", C.c_int, [P, C.c_int, C.c_int, P]),
+    ("dfpca_covariance_sharded", C.c_int, [P, P, C.POINTER(DfpcaGrid), PD, PD, C.POINTER(DfpcaPlan),
+                                           C.POINTER(P)]),
+    ("dfpca_covariance_emulated", C.c_int, [P, P, C.POINTER(DfpcaGrid), PD, PD, C.POINTER(DfpcaPlan), C.c_int,
+                                            C.POINTER(P)]),
+    ("dfpca_surface_rows", C.c_int, [P, PI64, PI64]),
+    ("dfpca_shard_bounds", C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int, PI64]),
+    ("dfpca_shard_blocks", C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, PI64, C.c_int64, PI64]),
 ]
 
 _lib = None

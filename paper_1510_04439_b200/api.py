@@ -472,10 +472,19 @@ class SurfaceEstimate:
         except Exception:
             pass
 
+    def rows(self):
+        """(row0, rows): the covariance rows this surface holds -- a slab of a
+        sharded covariance, or (0, G)."""
+        if not self._h:
+            return 0, (self.grid.size() if self.kind == SurfaceKind.Covariance else 1)
+        r0, nr = C.c_int64(), C.c_int64()
+        check(_lib.lib().dfpca_surface_rows(self._h, C.byref(r0), C.byref(nr)))
+        return r0.value, nr.value
+
     @property
     def values(self) -> np.ndarray:
         if self._values is None:
-            n = self.grid.size() ** 2 if self.kind == SurfaceKind.Covariance else self.grid.size()
+            n = self.rows()[1] * self.grid.size() if self.kind == SurfaceKind.Covariance else self.grid.size()
             out = np.empty(n, dtype=np.float64)
             check(_lib.lib().dfpca_surface_download(_lib.ctx(), self._h,
                                                     out.ctypes.data_as(C.POINTER(C.c_double))))
@@ -631,6 +640,92 @@ def fft_covariance(binned: BinnedData, grid: EvaluationGrid, h: Bandwidth, mean:
                                       mv.ctypes.data_as(C.POINTER(C.c_double)) if mv.size == grid.size() else None,
                                       C.byref(pdesc) if pdesc is not None else None, C.byref(handle)))
     return SurfaceEstimate(grid, SurfaceKind.Covariance, handle=handle)
+
+
+# ------------------------------------------------- multi-GPU (sharded) ----
+# The reference's only parallel knob is set_max_threads (parallel.hpp:23);
+# here one process per GPU runs one rank of a slab-sharded covariance
+# (csrc/shard.hpp): rank r owns s1 planes [bounds[r], bounds[r+1]).
+
+
+def init_distributed(world: int, rank: int, unique_id: Optional[bytes] = None, broadcast=None) -> None:
+    """Joins this process's context to an NCCL communicator of `world` ranks.
+    `unique_id` (128 bytes from nccl_unique_id() on rank 0) or `broadcast`, a
+    callable(bytes_or_None) -> bytes that distributes rank 0's id (e.g. via
+    torch.distributed.broadcast_object_list)."""
+    if world > 1 and unique_id is None:
+        uid = nccl_unique_id() if rank == 0 else None
+        unique_id = broadcast(uid) if broadcast else uid
+    buf = C.create_string_buffer(bytes(unique_id) if unique_id else bytes(128), 128)
+    check(_lib.lib().dfpca_nccl_init(_lib.ctx(), int(world), int(rank), C.cast(buf, C.c_void_p)))
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    status = _lib.lib().dfpca_nccl_unique_id(C.cast(buf, C.c_void_p))
+    if status != 0:
+        raise Error(ErrorClass.Config, "InvalidArgument", "libnccl could not provide a unique id")
+    return buf.raw
+
+
+def _cov_args(binned, grid, h, mean, plan):
+    hh = h.arr()
+    if hh.size != grid.dim():
+        raise Error(ErrorClass.Config, "InvalidBandwidth", "bandwidth dimension mismatch")
+    mv = np.ascontiguousarray(mean.values, dtype=np.float64)
+    pdesc, keep = (plan.desc(grid.dim()) if plan is not None else (None, None))
+    return hh, mv, pdesc, keep
+
+
+def fft_covariance_sharded(binned: BinnedData, grid: EvaluationGrid, h: Bandwidth, mean: SurfaceEstimate,
+                           plan: Optional[BlockPlan] = None) -> SurfaceEstimate:
+    """fft_covariance (fft_smoother.hpp:585-744) as one rank of the
+    communicator set up by init_distributed: returns this rank's slab (complete
+    rows `.rows()` of the covariance), bit-identical to the one-GPU result."""
+    hh, mv, pdesc, keep = _cov_args(binned, grid, h, mean, plan)
+    handle = C.c_void_p()
+    check(_lib.lib().dfpca_covariance_sharded(_lib.ctx(), binned.handle, C.byref(grid.desc()),
+                                              hh.ctypes.data_as(C.POINTER(C.c_double)),
+                                              mv.ctypes.data_as(C.POINTER(C.c_double)),
+                                              C.byref(pdesc) if pdesc is not None else None, C.byref(handle)))
+    return SurfaceEstimate(grid, SurfaceKind.Covariance, handle=handle)
+
+
+def fft_covariance_emulated(binned: BinnedData, grid: EvaluationGrid, h: Bandwidth, mean: SurfaceEstimate,
+                            world: int, plan: Optional[BlockPlan] = None) -> SurfaceEstimate:
+    """The sharded decomposition with `world` ranks as threads of this process
+    on one device; the slabs are assembled into the full covariance."""
+    hh, mv, pdesc, keep = _cov_args(binned, grid, h, mean, plan)
+    handle = C.c_void_p()
+    check(_lib.lib().dfpca_covariance_emulated(_lib.ctx(), binned.handle, C.byref(grid.desc()),
+                                               hh.ctypes.data_as(C.POINTER(C.c_double)),
+                                               mv.ctypes.data_as(C.POINTER(C.c_double)),
+                                               C.byref(pdesc) if pdesc is not None else None, int(world),
+                                               C.byref(handle)))
+    return SurfaceEstimate(grid, SurfaceKind.Covariance, handle=handle)
+
+
+def shard_bounds(n1: int, nodes_per_plane: int, radius: int, world: int) -> list:
+    out = (C.c_int64 * (world + 1))()
+    check_plain(_lib.lib().dfpca_shard_bounds(n1, nodes_per_plane, radius, world, out))
+    return list(out)
+
+
+def shard_blocks(n1: int, nodes_per_plane: int, radius: int, world: int, phase: int) -> np.ndarray:
+    """[k, 7] int64 rows (src, dst, r0, r1, c0, c1, transpose)."""
+    cnt = C.c_int64()
+    check_plain(_lib.lib().dfpca_shard_blocks(n1, nodes_per_plane, radius, world, phase, None, 0, C.byref(cnt)))
+    out = np.zeros((max(cnt.value, 1), 7), dtype=np.int64)
+    check_plain(_lib.lib().dfpca_shard_blocks(n1, nodes_per_plane, radius, world, phase,
+                                              out.ctypes.data_as(C.POINTER(C.c_int64)), cnt.value, C.byref(cnt)))
+    return out[:cnt.value]
+
+
+def check_plain(status: int) -> None:
+    """Status of a context-free entry point (no error text)."""
+    if status != 0:
+        raise Error(ErrorClass(status) if status in (2, 3, 4, 5) else ErrorClass.Config, "InvalidArgument",
+                    "invalid shard plan arguments")
 
 
 def blockwise_apply(plan: BlockPlan, binned: BinnedData, grid: EvaluationGrid, h: Bandwidth, what):

@@ -22,7 +22,16 @@ void run_local_linear(dfpca_context* ctx, const dfpca_binned* b, const Grid& gri
                       int target, double* out_host, dfpca_surface** out_surface);
 void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid, const double* h,
                     const double* mean_host, dfpca_surface** out);
-void build_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, double* pv);
+}  // namespace dfpca_gpu
+#include "pairs.cuh"
+#include "shard.hpp"
+namespace dfpca_gpu {
+void run_covariance_sharded(dfpca_context* ctx, Transport& tr, const dfpca_binned* b, const Grid& grid,
+                            const double* h, const double* mean_host, dfpca_surface** out);
+void run_covariance_emulated(dfpca_context* ctx, int world, const dfpca_binned* b, const Grid& grid,
+                             const double* h, const double* mean_host, dfpca_surface** out);
+void nccl_unique_id(void* out);
+std::shared_ptr<Transport> make_nccl_transport(int world, int rank, const void* id);
 void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid& grid, i64 q,
                         i64 L_max, unsigned long long seed, double* eigenvalues, double* eigenfunctions,
                         double* fve, double* total_variance, i64* n_components);
@@ -508,24 +517,110 @@ int dfpca_local_linear(dfpca_context* ctx, const dfpca_binned* b, const dfpca_gr
   });
 }
 
+}  // extern "C"
+
+namespace {
+// fft_smoother.hpp:589-600, in order
+Grid validate_covariance(const dfpca_binned* b, const dfpca_grid* grid, const double* h, const double* mean,
+                         const dfpca_plan* plan, dfpca_surface** out) {
+  if (!out) fail(kConfig, "InvalidArgument", "null output handle");
+  *out = nullptr;
+  Grid g = make_grid(grid);
+  if (!g.equispaced)
+    fail(kConfig, "GridNotEquispaced", "binned covariance smoothing requires equispaced grid axes");
+  validate_bandwidth(g, h);
+  if (!b || !b->has_cov) fail(kConfig, "InvalidArgument", "binned data lacks the covariance path");
+  if (!b->grid.same_shape(g)) fail(kConfig, "InvalidArgument", "binned data does not conform to the grid");
+  if (b->n_pair == 0)
+    fail(kNumeric, "NoPairs", "covariance smoothing needs at least one sample with two observations");
+  if (!mean) fail(kConfig, "InvalidArgument", "mean surface does not conform to the grid");
+  validate_plan(plan, g, h);
+  return g;
+}
+}  // namespace
+
+extern "C" {
+
 int dfpca_covariance(dfpca_context* ctx, const dfpca_binned* b, const dfpca_grid* grid, const double* h,
                      const double* mean, const dfpca_plan* plan, dfpca_surface** out) {
   return guarded(ctx, [&] {
-    if (!out) fail(kConfig, "InvalidArgument", "null output handle");
-    *out = nullptr;
-    Grid g = make_grid(grid);
-    // fft_smoother.hpp:589-600, in order
-    if (!g.equispaced)
-      fail(kConfig, "GridNotEquispaced", "binned covariance smoothing requires equispaced grid axes");
-    validate_bandwidth(g, h);
-    if (!b || !b->has_cov) fail(kConfig, "InvalidArgument", "binned data lacks the covariance path");
-    if (!b->grid.same_shape(g)) fail(kConfig, "InvalidArgument", "binned data does not conform to the grid");
-    if (b->n_pair == 0)
-      fail(kNumeric, "NoPairs", "covariance smoothing needs at least one sample with two observations");
-    if (!mean) fail(kConfig, "InvalidArgument", "mean surface does not conform to the grid");
-    validate_plan(plan, g, h);
+    Grid g = validate_covariance(b, grid, h, mean, plan, out);
     run_covariance(ctx, b, g, h, mean, out);
   });
+}
+
+int dfpca_nccl_unique_id(void* id) {
+  if (!id) return kConfig;
+  try {
+    nccl_unique_id(id);
+    return 0;
+  } catch (const Failure& e) {
+    return e.cls;
+  }
+}
+
+int dfpca_nccl_init(dfpca_context* ctx, int world, int rank, const void* id) {
+  return guarded(ctx, [&] {
+    if (world < 1 || rank < 0 || rank >= world || !id) fail(kConfig, "InvalidArgument", "bad rank / world / id");
+    ctx->transport.reset();
+    if (world > 1) ctx->transport = make_nccl_transport(world, rank, id);
+  });
+}
+
+int dfpca_covariance_sharded(dfpca_context* ctx, const dfpca_binned* b, const dfpca_grid* grid, const double* h,
+                             const double* mean, const dfpca_plan* plan, dfpca_surface** out) {
+  return guarded(ctx, [&] {
+    Grid g = validate_covariance(b, grid, h, mean, plan, out);
+    if (!ctx->transport) {
+      run_covariance(ctx, b, g, h, mean, out);  // one rank: the whole covariance
+      return;
+    }
+    run_covariance_sharded(ctx, *ctx->transport, b, g, h, mean, out);
+  });
+}
+
+int dfpca_covariance_emulated(dfpca_context* ctx, const dfpca_binned* b, const dfpca_grid* grid, const double* h,
+                              const double* mean, const dfpca_plan* plan, int world, dfpca_surface** out) {
+  return guarded(ctx, [&] {
+    Grid g = validate_covariance(b, grid, h, mean, plan, out);
+    if (world < 1) fail(kConfig, "InvalidArgument", "world must be >= 1");
+    run_covariance_emulated(ctx, world, b, g, h, mean, out);
+  });
+}
+
+int dfpca_surface_rows(const dfpca_surface* s, int64_t* row0, int64_t* rows) {
+  if (!s) return kConfig;
+  const bool cov = s->kind == DFPCA_SURFACE_COVARIANCE;
+  if (row0) *row0 = cov ? s->row0 : 0;
+  if (rows) *rows = cov ? (s->rows >= 0 ? s->rows : s->grid.G) : 1;
+  return 0;
+}
+
+int dfpca_shard_bounds(int64_t n1, int64_t nodes_per_plane, int64_t radius, int world, int64_t* bounds) {
+  if (n1 < 1 || nodes_per_plane < 1 || radius < 0 || world < 1 || !bounds) return kConfig;
+  const ShardPlan p = make_shard_plan(n1, nodes_per_plane, radius, world);
+  for (int r = 0; r <= world; ++r) bounds[r] = p.bounds[static_cast<std::size_t>(r)];
+  return 0;
+}
+
+int dfpca_shard_blocks(int64_t n1, int64_t nodes_per_plane, int64_t radius, int world, int phase, int64_t* out,
+                       int64_t capacity, int64_t* count) {
+  if (n1 < 1 || nodes_per_plane < 1 || radius < 0 || world < 1 || (phase != 0 && phase != 1) || !count)
+    return kConfig;
+  const ShardPlan p = make_shard_plan(n1, nodes_per_plane, radius, world);
+  const std::vector<ShardBlock> bl = shard_blocks(p, phase);
+  *count = static_cast<int64_t>(bl.size());
+  for (std::size_t i = 0; i < bl.size() && static_cast<int64_t>(i) < capacity && out; ++i) {
+    int64_t* o = out + 7 * i;
+    o[0] = bl[i].src;
+    o[1] = bl[i].dst;
+    o[2] = bl[i].r0;
+    o[3] = bl[i].r1;
+    o[4] = bl[i].c0;
+    o[5] = bl[i].c1;
+    o[6] = bl[i].transpose ? 1 : 0;
+  }
+  return 0;
 }
 
 int dfpca_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, double* pv) {

@@ -26,7 +26,17 @@ struct View {
   int tri_R = 0;
   i64 tri_G = 0;   // t extent
   i64 tri_rn = 0;  // s nodes per s1 row
-  i64 tri_n1 = 0;  // s1 extent
+  i64 tri_n1 = 0;  // s1 extent (local planes)
+  // slab of a sharded covariance (shard.hpp): local plane 0 is global s1 plane
+  // tri_row0, outputs stop at global plane tri_row_hi (< 0: no limit), and
+  // local column 0 is global t = tri_t0
+  i64 tri_row0 = 0;
+  i64 tri_row_hi = -1;
+  i64 tri_t0 = 0;
+  // output window along the axis (columns kernel): rows [lo, hi) are written,
+  // rows [0, min(n, hi + R)) are read; hi < 0: the whole axis
+  i64 lo = 0;
+  i64 hi = -1;
 };
 
 // One multi-order pass along an axis: outputs out[r] = taps(order[r]) * in.

@@ -75,7 +75,7 @@ __device__ inline void bulk_g2s(void* dst, const void* src, unsigned bytes, std:
 // consecutive outputs per order sit in registers, and the taps are kernel
 // parameters (uniform-register operands of DFMA).
 struct TileMeta {
-  int ob, c0, rows, nout;
+  int ob, c0, rows, nout, lo;
 };
 
 template <int R, int NO, int JB, bool CHECK>
@@ -113,6 +113,9 @@ __global__ void __launch_bounds__(kThreads) k_pass_cols(View in, View o0, View o
   const int tile_elems = n * kTC;
   const int tri = in.tri, triR = in.tri_R, triG = static_cast<int>(in.tri_G), tri_rn = static_cast<int>(in.tri_rn),
             tri_n1 = static_cast<int>(in.tri_n1);
+  const int tri_t0 = static_cast<int>(in.tri_t0), tri_row0 = static_cast<int>(in.tri_row0),
+            tri_row_hi = static_cast<int>(in.tri_row_hi);
+  const int win_lo = static_cast<int>(in.lo), win_hi = static_cast<int>(in.hi);
   // rows to stage and outputs to produce (all unless the upper-triangle
   // restriction applies, see View::tri)
   auto make_meta = [&](int tile) {
@@ -121,10 +124,18 @@ __global__ void __launch_bounds__(kThreads) k_pass_cols(View in, View o0, View o
     mt.c0 = (tile - mt.ob * chunks) * kTC;
     mt.rows = n;
     mt.nout = n;
+    mt.lo = win_lo;
+    if (win_hi >= 0) {
+      mt.nout = win_hi < n ? win_hi : n;
+      mt.rows = mt.nout + R < n ? mt.nout + R : n;
+    }
     if (tri != 0) {
       const int c1 = (mt.c0 + kTC < inner ? mt.c0 + kTC : inner) - 1;
       const int tmax = (mt.c0 / triG == c1 / triG) ? c1 % triG : triG - 1;
-      const int s1_out = tmax / tri_rn + 1;
+      int s1_out = (tmax + tri_t0) / tri_rn + 1;  // global planes
+      if (tri_row_hi >= 0 && s1_out > tri_row_hi) s1_out = tri_row_hi;
+      s1_out -= tri_row0;  // local
+      if (s1_out < 0) s1_out = 0;
       if (tri == 1) {
         const int s1_in = s1_out + triR < tri_n1 ? s1_out + triR : tri_n1;
         if (mt.ob >= s1_in) mt.rows = mt.nout = 0;
@@ -192,7 +203,7 @@ __global__ void __launch_bounds__(kThreads) k_pass_cols(View in, View o0, View o
       double* b0 = o0.p + mt.ob * o0.os + cb;
       double* b1 = o1.p + mt.ob * o1.os + cb;
       double* b2 = o2.p + mt.ob * o2.os + cb;
-      for (int j0 = g * JB; j0 < mt.nout; j0 += kGroups * JB) {
+      for (int j0 = mt.lo + g * JB; j0 < mt.nout; j0 += kGroups * JB) {
         double acc[NO][JB];
         if (j0 >= R && j0 + JB + R <= mt.rows)
           conv_block<R, NO, JB, false>(col, j0, mt.rows, tp, acc);

@@ -52,13 +52,16 @@ template <int VEC>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_gemm_tn(i64 M, i64 N, i64 K, const double* __restrict__ A, i64 lda, const double* __restrict__ B,
               i64 ldb, double* __restrict__ C, i64 ldc, int symmetric, i64 tiles_n, i64 k_chunk,
-              i64 split_stride) {
+              i64 split_stride, i64 tm_begin, i64 tm_end) {
   extern __shared__ __align__(16) double smem[];
 
+  // symmetric: row tiles [tm_begin, tm_end) only (a slab of a sharded pair
+  // grid, shard.hpp); C's row 0 is global row tm_begin * BM and mirrored tiles
+  // are written only inside the slab
   i64 tm, tn;
   if (symmetric) {
     i64 t = blockIdx.x;  // upper-triangular tile pairs (tm <= tn)
-    tm = 0;
+    tm = tm_begin;
     while (t >= tiles_n - tm) {
       t -= tiles_n - tm;
       ++tm;
@@ -142,6 +145,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   cp_async_wait<0>();
 
   // Epilogue: fragment (i, j) holds C[row][col], C[row][col + 1].
+  const i64 crow0 = symmetric ? tm_begin * BM : 0;
+  const bool mirror = symmetric && tm != tn && tn < tm_end;
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
     const i64 row = m0 + wm0 + i * 8 + (lane >> 2);
@@ -149,16 +154,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int j = 0; j < NT; ++j) {
       const i64 col = n0 + wn0 + j * 8 + 2 * (lane & 3);
       if (row < M) {
+        double* crow = C + (row - crow0) * ldc;
         if (col + 1 < N && (ldc % 2) == 0) {
-          *reinterpret_cast<double2*>(C + row * ldc + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+          *reinterpret_cast<double2*>(crow + col) = make_double2(acc[i][j][0], acc[i][j][1]);
         } else {
-          if (col < N) C[row * ldc + col] = acc[i][j][0];
-          if (col + 1 < N) C[row * ldc + col + 1] = acc[i][j][1];
+          if (col < N) crow[col] = acc[i][j][0];
+          if (col + 1 < N) crow[col + 1] = acc[i][j][1];
         }
       }
-      if (symmetric && tm != tn && row < M) {
-        if (col < N) C[col * ldc + row] = acc[i][j][0];
-        if (col + 1 < N) C[(col + 1) * ldc + row] = acc[i][j][1];
+      if (mirror && row < M) {
+        if (col < N) C[(col - crow0) * ldc + row] = acc[i][j][0];
+        if (col + 1 < N) C[(col + 1 - crow0) * ldc + row] = acc[i][j][1];
       }
     }
   }
@@ -191,7 +197,7 @@ __global__ void k_scale_rows(const double* __restrict__ in, const double* __rest
 template <int VEC>
 void launch(dfpca_context* ctx, dim3 grid, std::size_t smem, i64 M, i64 N, i64 K, const double* A, i64 lda,
             const double* B, i64 ldb, double* C, i64 ldc, int symmetric, i64 tiles_n, i64 k_chunk,
-            i64 split_stride) {
+            i64 split_stride, i64 tm_begin, i64 tm_end) {
   static bool attr = false;
   if (!attr) {
     DFPCA_CUDA(cudaFuncSetAttribute(k_gemm_tn<VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -199,13 +205,24 @@ void launch(dfpca_context* ctx, dim3 grid, std::size_t smem, i64 M, i64 N, i64 K
     attr = true;
   }
   DFPCA_LAUNCH(ctx, k_gemm_tn<VEC>, grid, NTHREADS, smem, M, N, K, A, lda, B, ldb, C, ldc, symmetric,
-               tiles_n, k_chunk, split_stride);
+               tiles_n, k_chunk, split_stride, tm_begin, tm_end);
 }
 
 }  // namespace
 
+i64 gemm_splits(const dfpca_context* ctx, i64 M, i64 N, i64 K) {
+  const i64 blocks = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  i64 splits = 1;
+  if (blocks < 2 * ctx->sm_count && K >= 1024) {
+    splits = std::min<i64>((2 * ctx->sm_count + blocks - 1) / blocks, K / 256);
+    splits = std::max<i64>(splits, 1);
+  }
+  return splits;
+}
+
 void gemm_tn(dfpca_context* ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, const double* w,
-             const double* B, i64 ldb, double* C, i64 ldc, bool symmetric) {
+             const double* B, i64 ldb, double* C, i64 ldc, bool symmetric, i64 tm_begin, i64 tm_end,
+             i64 force_splits) {
   if (M <= 0 || N <= 0) return;
   if (K <= 0) {
     for (i64 r = 0; r < M; ++r)
@@ -224,14 +241,16 @@ void gemm_tn(dfpca_context* ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, 
   const std::size_t smem = sizeof(double) * STAGES * STAGE_DOUBLES;  // 101 KB
   const bool vec2 = (lda % 2 == 0) && (ldb % 2 == 0) && (reinterpret_cast<std::uintptr_t>(A) % 16 == 0) &&
                     (reinterpret_cast<std::uintptr_t>(B) % 16 == 0);
-  const i64 blocks = symmetric ? tiles_m * (tiles_m + 1) / 2 : tiles_m * tiles_n;
+  if (tm_end < 0 || tm_end > tiles_m) tm_end = tiles_m;
+  if (tm_begin < 0) tm_begin = 0;
+  if (symmetric && tm_begin >= tm_end) return;
+  // upper tile pairs of row tiles [tm_begin, tm_end)
+  const i64 blocks = symmetric ? (tm_end - tm_begin) * tiles_m - (tm_end * (tm_end - 1) - tm_begin * (tm_begin - 1)) / 2
+                               : tiles_m * tiles_n;
   // Skinny products (the projection GEMMs) get a deterministic split-K so the
   // grid covers the SMs.
-  i64 splits = 1;
-  if (!symmetric && blocks < 2 * ctx->sm_count && K >= 1024) {
-    splits = std::min<i64>((2 * ctx->sm_count + blocks - 1) / blocks, K / 256);
-    splits = std::max<i64>(splits, 1);
-  }
+  i64 splits = symmetric ? 1 : gemm_splits(ctx, M, N, K);
+  if (!symmetric && force_splits > 0) splits = force_splits;  // row-sharded products: same sums as unsharded
   i64 k_chunk = K;
   double* out = C;
   i64 ldo = ldc, stride = 0;
@@ -245,9 +264,11 @@ void gemm_tn(dfpca_context* ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, 
   }
   const dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(splits));
   if (vec2)
-    launch<2>(ctx, grid, smem, M, N, K, A, lda, B, ldb, out, ldo, symmetric ? 1 : 0, tiles_n, k_chunk, stride);
+    launch<2>(ctx, grid, smem, M, N, K, A, lda, B, ldb, out, ldo, symmetric ? 1 : 0, tiles_n, k_chunk, stride,
+              tm_begin, tm_end);
   else
-    launch<1>(ctx, grid, smem, M, N, K, A, lda, B, ldb, out, ldo, symmetric ? 1 : 0, tiles_n, k_chunk, stride);
+    launch<1>(ctx, grid, smem, M, N, K, A, lda, B, ldb, out, ldo, symmetric ? 1 : 0, tiles_n, k_chunk, stride,
+              tm_begin, tm_end);
   if (splits > 1)
     DFPCA_LAUNCH(ctx, k_splitk_reduce, grid_for(M * N, 256), 256, 0, out, splits, M, N, C, ldc);
 }

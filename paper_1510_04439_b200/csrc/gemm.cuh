@@ -13,7 +13,17 @@ namespace dfpca_gpu {
 // result is symmetric); only tiles with tile_n >= tile_m are computed and the
 // transposed tile is written as well.
 // beta_one: accumulate into C instead of overwriting it.
+// tm_begin / tm_end (symmetric only): compute the row tiles [tm_begin, tm_end)
+// of the upper tile triangle; C's row 0 is then global row tm_begin * 128 and
+// mirrored tiles are written only when they fall inside those rows (slab of a
+// sharded pair grid, shard.hpp).
+// force_splits (> 0, non-symmetric): the split-K count, so that a row block of
+// a product is summed exactly like the unsharded product (gemm_splits).
 void gemm_tn(dfpca_context* ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, const double* w,
-             const double* B, i64 ldb, double* C, i64 ldc, bool symmetric);
+             const double* B, i64 ldb, double* C, i64 ldc, bool symmetric, i64 tm_begin = 0,
+             i64 tm_end = -1, i64 force_splits = 0);
+
+// Split-K count gemm_tn picks for a non-symmetric M x N x K product.
+i64 gemm_splits(const dfpca_context* ctx, i64 M, i64 N, i64 K);
 
 }  // namespace dfpca_gpu

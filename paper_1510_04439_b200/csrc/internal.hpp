@@ -15,6 +15,7 @@
 namespace dfpca_gpu {
 
 using i64 = std::int64_t;
+class Transport;  // shard.cu: NCCL (or in-process) rank exchanges
 
 // Error classes of the reference (errors.hpp:11-17).
 enum : int { kParse = 2, kConfig = 3, kNumeric = 4, kVersion = 5 };
@@ -125,6 +126,8 @@ struct dfpca_context {
   std::vector<dfpca_gpu::StageMark> marks;
   std::vector<cudaEvent_t> event_pool;
   std::int64_t launches = 0;
+  // multi-GPU (dfpca_nccl_init): this process's rank of a sharded covariance
+  std::shared_ptr<dfpca_gpu::Transport> transport;
 
   // Reusable scratch (grown on demand, never shrunk while the context lives).
   dfpca_gpu::DevBuf<unsigned char> scratch;
@@ -185,4 +188,8 @@ struct dfpca_surface {
   int kind = DFPCA_SURFACE_MEAN;
   std::int64_t n = 0;
   dfpca_gpu::DevBuf<double> values;
+  // covariance slab of a sharded run (shard.hpp): values hold global rows
+  // [row0, row0 + rows) of the G x G covariance; rows = G when unsharded
+  std::int64_t row0 = 0;
+  std::int64_t rows = -1;
 };

@@ -16,19 +16,26 @@
 // with a nonzero band in the reference order -- samples ascending, separate
 // multiply and add, (w_i M_i(s)) M_i(t) (fft_smoother.hpp:397-402) -- and
 // subtracts the band once (:433-434), making those entries bit-identical.
+#include <functional>
 #include <vector>
 
 #include "gemm.cuh"
+#include "pairs.cuh"
+#include "shard.hpp"
 
 namespace dfpca_gpu {
 namespace {
 
-__global__ void k_rank_one(double* __restrict__ pw, const double* __restrict__ m, double W, i64 G) {
-  const i64 total = G * G;
+// pw over rows [row0, row0 + rows), columns [col0, G) of the window
+// (pw points at row row0, leading dimension G).
+__global__ void k_rank_one(double* __restrict__ pw, const double* __restrict__ m, double W, i64 G, i64 row0,
+                           i64 rows, i64 col0) {
+  const i64 w = G - col0;
+  const i64 total = rows * w;
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
        e += (i64)gridDim.x * blockDim.x) {
-    const i64 s = e / G, t = e % G;
-    pw[e] = __dmul_rn(__dmul_rn(W, m[s]), m[t]);
+    const i64 r = e / w, t = col0 + e % w;
+    pw[r * G + t] = __dmul_rn(__dmul_rn(W, m[row0 + r]), m[t]);
   }
 }
 
@@ -46,11 +53,14 @@ __global__ void k_rank_one(double* __restrict__ pw, const double* __restrict__ m
 __global__ void k_band_fix(const double* __restrict__ diag_mass, const double* __restrict__ diag_value,
                            i64 G, int d, i64 codes, DevGrid g, const double* __restrict__ ps_mass,
                            int identical, const double* __restrict__ w, i64 n_pair, double w_seq,
-                           double* __restrict__ pw, double* __restrict__ pv) {
+                           double* __restrict__ pw, double* __restrict__ pv, i64 row0, i64 rows, i64 col0) {
+  // window: band entries of rows u in [row0, row0 + rows) and columns t >= col0;
+  // pw / pv point at row row0 (leading dimension G)
   const int lane = threadIdx.x & 31;
   const i64 warps = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
-  const i64 total = G * codes;
-  for (i64 e = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5; e < total; e += warps) {
+  const i64 total = rows * codes;
+  for (i64 e0 = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5; e0 < total; e0 += warps) {
+    const i64 e = e0 + row0 * codes;
     const double dm = diag_mass[e], dv = diag_value[e];
     if (dm == 0.0 && dv == 0.0) continue;
     const i64 u = e / codes;
@@ -69,9 +79,10 @@ __global__ void k_band_fix(const double* __restrict__ diag_mass, const double* _
       if (bk < 0 || bk >= g.shape[k]) inside = false;
       t += bk * g.strides[k];
     }
-    if (!inside) continue;
+    if (!inside || t < col0) continue;
+    const i64 at = (u - row0) * G + t;
     if (pw == nullptr) {  // value grid only (shared-design covariance)
-      if (lane == 0) pv[u * G + t] = __dsub_rn(pv[u * G + t], dv);
+      if (lane == 0) pv[at] = __dsub_rn(pv[at], dv);
       continue;
     }
     double sw = 0.0;
@@ -93,8 +104,8 @@ __global__ void k_band_fix(const double* __restrict__ diag_mass, const double* _
       for (int q = 0; q < cnt; ++q) sw = __dadd_rn(sw, __shfl_sync(0xffffffffu, pm, q));
     }
     if (lane == 0) {
-      pw[u * G + t] = __dsub_rn(sw, dm);
-      pv[u * G + t] = __dsub_rn(pv[u * G + t], dv);
+      pw[at] = __dsub_rn(sw, dm);
+      pv[at] = __dsub_rn(pv[at], dv);
     }
   }
 }
@@ -104,25 +115,39 @@ __global__ void k_band_fix(const double* __restrict__ diag_mass, const double* _
 
 DevGrid upload_grid_axes(dfpca_context* ctx, const Grid& g, DevBuf<double>& storage);
 
-void build_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, double* pv) {
+void build_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, double* pv, const PairWindow* win,
+                      const std::function<void(bool pw_from_syrk)>& exchange) {
   const i64 G = b->grid.G;
   const i64 n = b->n_pair;
+  PairWindow full;
+  full.rows = G;
+  const PairWindow& w = win ? *win : full;
+  const i64 tiles = (G + kShardRowTile - 1) / kShardRowTile;
+  const i64 tm_end = w.tm_end < 0 ? tiles : w.tm_end;
+  // own SYRK rows inside the window buffer
+  const i64 own = w.tm_begin * kShardRowTile - w.row0;
   double W = 0.0;
   for (double x : b->pair_weight_h) W += x;  // sequential, as the reference's sample loop
   if (pw) {
     if (b->identical_mass) {
-      DFPCA_LAUNCH(ctx, k_rank_one, grid_for(G * G, 256, 148ll * 16), 256, 0, pw, b->ps_mass.get(), W, G);
+      DFPCA_LAUNCH(ctx, k_rank_one, grid_for(w.rows * (G - w.col0), 256, 148ll * 16), 256, 0, pw,
+                   b->ps_mass.get(), W, G, w.row0, w.rows, w.col0);
     } else {
-      gemm_tn(ctx, G, G, n, b->ps_mass.get(), G, b->pair_weight.get(), b->ps_mass.get(), G, pw, G, true);
+      gemm_tn(ctx, G, G, n, b->ps_mass.get(), G, b->pair_weight.get(), b->ps_mass.get(), G, pw + own * G, G, true,
+              w.tm_begin, tm_end);
     }
   }
-  if (pv) gemm_tn(ctx, G, G, n, b->ps_value.get(), G, b->pair_weight.get(), b->ps_value.get(), G, pv, G, true);
+  if (pv)
+    gemm_tn(ctx, G, G, n, b->ps_value.get(), G, b->pair_weight.get(), b->ps_value.get(), G, pv + own * G, G, true,
+            w.tm_begin, tm_end);
+  if (exchange) exchange(pw != nullptr && !b->identical_mass);
   if (pv) {
     DevBuf<double> axes;
     DevGrid dg = upload_grid_axes(ctx, b->grid, axes);
-    DFPCA_LAUNCH(ctx, k_band_fix, grid_for(G * b->codes * 32, 256, 148ll * 32), 256, 0,
+    DFPCA_LAUNCH(ctx, k_band_fix, grid_for(w.rows * b->codes * 32, 256, 148ll * 32), 256, 0,
                  b->diag_mass.get(), b->diag_value.get(), G, b->grid.d, b->codes, dg,
-                 b->ps_mass.get(), b->identical_mass ? 1 : 0, b->pair_weight.get(), n, W, pw, pv);
+                 b->ps_mass.get(), b->identical_mass ? 1 : 0, b->pair_weight.get(), n, W, pw, pv, w.row0, w.rows,
+                 w.col0);
     DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
   }
 }

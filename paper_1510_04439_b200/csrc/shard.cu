@@ -1,0 +1,495 @@
+// Sharded covariance: block exchanges over a transport and the drivers.
+//
+//  * NcclTransport: one process per GPU; libnccl is loaded at run time
+//    (dlopen), the communicator is created from a unique id the caller
+//    broadcasts (dfpca_nccl_unique_id / dfpca_nccl_init).  Exchanges are one
+//    grouped ncclSend/ncclRecv per phase on the context stream.
+//  * LocalTransport: `world` ranks as host threads of one process, each with
+//    its own context and stream on the same device; messages are
+//    device-to-device copies ordered by events.  Used to validate the slab
+//    decomposition on one GPU (the assembled result must be bit-identical to
+//    the one-device covariance); no kernel ever waits on another rank's kernel
+//    -- ranks meet only at host-side barriers between exchanges.
+#include <dlfcn.h>
+
+#include <cmath>
+#include <condition_variable>
+#include <cstring>
+#include <memory>
+#include <map>
+#include <mutex>
+#include <thread>
+#include <tuple>
+
+#include "common.cuh"
+#include "shard.hpp"
+#include "shard_exec.hpp"
+
+namespace dfpca_gpu {
+
+// ----------------------------------------------------------------- kernels --
+// packed[(s - r0) * w + (t - c0)] = value (s, t) of the block, read from a
+// row-major buffer whose row 0 is global row row0 (ld = G): element [s][t],
+// or [t][s] for a transposed block (32 x 32 shared-memory tiles keep both
+// sides coalesced).
+__global__ void k_pack_block(const double* __restrict__ src, i64 ld, i64 row0, i64 r0, i64 r1, i64 c0, i64 c1,
+                             int transpose, double* __restrict__ out) {
+  __shared__ double tile[32][33];
+  const i64 w = c1 - c0, h = r1 - r0;
+  const i64 tw = (w + 31) / 32;
+  const i64 bs = (blockIdx.x / tw) * 32, bt = (blockIdx.x % tw) * 32;  // tile origin (s, t), block-relative
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  if (!transpose) {
+    for (int r = ty; r < 32; r += 8) {
+      const i64 s = bs + r, t = bt + tx;
+      if (s < h && t < w) out[s * w + t] = src[(r0 + s - row0) * ld + c0 + t];
+    }
+    return;
+  }
+  for (int r = ty; r < 32; r += 8) {  // rows t of the source, columns s
+    const i64 t = bt + r, s = bs + tx;
+    tile[r][tx] = (s < h && t < w) ? src[(c0 + t - row0) * ld + r0 + s] : 0.0;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const i64 s = bs + r, t = bt + tx;
+    if (s < h && t < w) out[s * w + t] = tile[tx][r];
+  }
+}
+
+__global__ void k_unpack_block(const double* __restrict__ in, double* __restrict__ dst, i64 ld, i64 row0, i64 r0,
+                               i64 r1, i64 c0, i64 c1) {
+  const i64 w = c1 - c0, total = (r1 - r0) * w;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total; e += (i64)gridDim.x * blockDim.x) {
+    const i64 s = e / w, t = e % w;
+    dst[(r0 + s - row0) * ld + c0 + t] = in[e];
+  }
+}
+
+// --------------------------------------------------------------- transports --
+class Transport {
+ public:
+  struct Msg {
+    int peer;
+    double* buf;
+    i64 count;
+  };
+  virtual ~Transport() = default;
+  virtual int rank() const = 0;
+  virtual int world() const = 0;
+  // all sends and receives of one phase, queued on ctx->stream
+  virtual void exchange(dfpca_context* ctx, const std::vector<Msg>& sends, const std::vector<Msg>& recvs) = 0;
+  virtual unsigned long long max_u64(dfpca_context* ctx, unsigned long long v) = 0;
+  // recv[r * count ..] = rank r's send, for every rank
+  virtual void all_gather(dfpca_context* ctx, const double* send, double* recv, i64 count) = 0;
+};
+
+namespace {
+
+// ---- NCCL, loaded at run time ----
+struct NcclApi {
+  using Comm = void*;
+  struct UniqueId {
+    char internal[128];
+  };
+  int (*GetUniqueId)(UniqueId*) = nullptr;
+  int (*CommInitRank)(Comm*, int, UniqueId, int) = nullptr;
+  int (*CommDestroy)(Comm) = nullptr;
+  int (*Send)(const void*, std::size_t, int, int, Comm, cudaStream_t) = nullptr;
+  int (*Recv)(void*, std::size_t, int, int, Comm, cudaStream_t) = nullptr;
+  int (*AllGather)(const void*, void*, std::size_t, int, Comm, cudaStream_t) = nullptr;
+  int (*AllReduce)(const void*, void*, std::size_t, int, int, Comm, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  static constexpr int kUint64 = 5, kFloat64 = 8, kMax = 2;
+
+  static NcclApi& get() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] { api.load(); });
+    if (!api.GetUniqueId) fail(kConfig, "InvalidArgument", "libnccl.so.2 could not be loaded (set DFPCA_NCCL_LIB)");
+    return api;
+  }
+  void load() {
+    std::vector<std::string> names;
+    if (const char* e = std::getenv("DFPCA_NCCL_LIB")) names.push_back(e);
+    names.push_back("libnccl.so.2");
+    names.push_back("/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2");
+    void* h = nullptr;
+    for (const auto& n : names)
+      if ((h = dlopen(n.c_str(), RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) return;
+    auto sym = [h](const char* s) { return dlsym(h, s); };
+    GetUniqueId = reinterpret_cast<decltype(GetUniqueId)>(sym("ncclGetUniqueId"));
+    CommInitRank = reinterpret_cast<decltype(CommInitRank)>(sym("ncclCommInitRank"));
+    CommDestroy = reinterpret_cast<decltype(CommDestroy)>(sym("ncclCommDestroy"));
+    Send = reinterpret_cast<decltype(Send)>(sym("ncclSend"));
+    Recv = reinterpret_cast<decltype(Recv)>(sym("ncclRecv"));
+    AllGather = reinterpret_cast<decltype(AllGather)>(sym("ncclAllGather"));
+    AllReduce = reinterpret_cast<decltype(AllReduce)>(sym("ncclAllReduce"));
+    GroupStart = reinterpret_cast<decltype(GroupStart)>(sym("ncclGroupStart"));
+    GroupEnd = reinterpret_cast<decltype(GroupEnd)>(sym("ncclGroupEnd"));
+    GetErrorString = reinterpret_cast<decltype(GetErrorString)>(sym("ncclGetErrorString"));
+    if (!(CommInitRank && Send && Recv && AllGather && AllReduce && GroupStart && GroupEnd)) GetUniqueId = nullptr;
+  }
+  void check(int r, const char* what) const {
+    if (r != 0)
+      fail(kNumeric, "DeviceError",
+           std::string(what) + ": " + (GetErrorString ? GetErrorString(r) : std::to_string(r)));
+  }
+};
+
+}  // namespace
+
+class NcclTransport final : public Transport {
+ public:
+  NcclTransport(int world, int rank, const void* id) : world_(world), rank_(rank) {
+    NcclApi& api = NcclApi::get();
+    NcclApi::UniqueId uid;
+    std::memcpy(uid.internal, id, sizeof(uid.internal));
+    api.check(api.CommInitRank(&comm_, world, uid, rank), "ncclCommInitRank");
+  }
+  ~NcclTransport() override {
+    if (comm_) NcclApi::get().CommDestroy(comm_);
+  }
+  int rank() const override { return rank_; }
+  int world() const override { return world_; }
+  void exchange(dfpca_context* ctx, const std::vector<Msg>& sends, const std::vector<Msg>& recvs) override {
+    NcclApi& api = NcclApi::get();
+    api.check(api.GroupStart(), "ncclGroupStart");
+    for (const Msg& m : sends)
+      api.check(api.Send(m.buf, static_cast<std::size_t>(m.count), NcclApi::kFloat64, m.peer, comm_, ctx->stream),
+                "ncclSend");
+    for (const Msg& m : recvs)
+      api.check(api.Recv(m.buf, static_cast<std::size_t>(m.count), NcclApi::kFloat64, m.peer, comm_, ctx->stream),
+                "ncclRecv");
+    api.check(api.GroupEnd(), "ncclGroupEnd");
+  }
+  unsigned long long max_u64(dfpca_context* ctx, unsigned long long v) override {
+    NcclApi& api = NcclApi::get();
+    DevBuf<unsigned long long> d(1);
+    DFPCA_CUDA(cudaMemcpyAsync(d.get(), &v, sizeof(v), cudaMemcpyHostToDevice, ctx->stream));
+    api.check(api.AllReduce(d.get(), d.get(), 1, NcclApi::kUint64, NcclApi::kMax, comm_, ctx->stream),
+              "ncclAllReduce");
+    unsigned long long out = 0;
+    DFPCA_CUDA(cudaMemcpyAsync(&out, d.get(), sizeof(out), cudaMemcpyDeviceToHost, ctx->stream));
+    DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+    return out;
+  }
+  void all_gather(dfpca_context* ctx, const double* send, double* recv, i64 count) override {
+    NcclApi& api = NcclApi::get();
+    api.check(api.AllGather(send, recv, static_cast<std::size_t>(count), NcclApi::kFloat64, comm_, ctx->stream),
+              "ncclAllGather");
+  }
+
+ private:
+  int world_, rank_;
+  NcclApi::Comm comm_ = nullptr;
+};
+
+// ---- in-process ranks ----
+class LocalHub {
+ public:
+  explicit LocalHub(int world) : world_(world) {}
+  struct Posted {
+    const double* buf;
+    i64 count;
+    cudaEvent_t ready;
+  };
+  void post(int src, int dst, int seq, const Posted& p) {
+    std::lock_guard<std::mutex> lk(m_);
+    box_[{src, dst, seq}] = p;
+    cv_.notify_all();
+  }
+  Posted take(int src, int dst, int seq) {
+    std::unique_lock<std::mutex> lk(m_);
+    cv_.wait(lk, [&] { return abort_ || box_.count({src, dst, seq}) > 0; });
+    if (abort_) fail(kNumeric, "DeviceError", "another in-process rank failed");
+    return box_.at({src, dst, seq});
+  }
+  // all ranks arrive; the last one clears the messages of round `seq`
+  void barrier(int seq) {
+    std::unique_lock<std::mutex> lk(m_);
+    const int gen = gen_;
+    if (++arrived_ == world_) {
+      arrived_ = 0;
+      ++gen_;
+      for (auto it = box_.begin(); it != box_.end();) {
+        if (std::get<2>(it->first) == seq) {
+          cudaEventDestroy(it->second.ready);
+          it = box_.erase(it);
+        } else {
+          ++it;
+        }
+      }
+      cv_.notify_all();
+      return;
+    }
+    cv_.wait(lk, [&] { return abort_ || gen_ != gen; });
+    if (abort_) fail(kNumeric, "DeviceError", "another in-process rank failed");
+  }
+  void set_abort() {
+    std::lock_guard<std::mutex> lk(m_);
+    abort_ = true;
+    cv_.notify_all();
+  }
+  int world() const { return world_; }
+  // scratch for the u64 reduction
+  std::vector<unsigned long long> u64s;
+
+ private:
+  int world_;
+  std::mutex m_;
+  std::condition_variable cv_;
+  std::map<std::tuple<int, int, int>, Posted> box_;
+  int arrived_ = 0, gen_ = 0;
+  bool abort_ = false;
+};
+
+class LocalTransport final : public Transport {
+ public:
+  LocalTransport(LocalHub* hub, int rank) : hub_(hub), rank_(rank) {}
+  int rank() const override { return rank_; }
+  int world() const override { return hub_->world(); }
+  void exchange(dfpca_context* ctx, const std::vector<Msg>& sends, const std::vector<Msg>& recvs) override {
+    const int seq = seq_++;
+    for (const Msg& m : sends) {
+      cudaEvent_t ev;
+      DFPCA_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      DFPCA_CUDA(cudaEventRecord(ev, ctx->stream));
+      hub_->post(rank_, m.peer, seq, {m.buf, m.count, ev});
+    }
+    for (const Msg& m : recvs) {
+      const LocalHub::Posted p = hub_->take(m.peer, rank_, seq);
+      if (p.count != m.count) fail(kNumeric, "DeviceError", "in-process exchange: message size mismatch");
+      DFPCA_CUDA(cudaStreamWaitEvent(ctx->stream, p.ready, 0));
+      DFPCA_CUDA(cudaMemcpyAsync(m.buf, p.buf, sizeof(double) * m.count, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    // senders keep their buffers until every receiver has copied
+    DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+    hub_->barrier(seq);
+  }
+  unsigned long long max_u64(dfpca_context* ctx, unsigned long long v) override {
+    (void)ctx;
+    const int seq = seq_++;
+    {
+      static std::mutex mu;
+      std::lock_guard<std::mutex> lk(mu);
+      if (hub_->u64s.size() != static_cast<std::size_t>(world())) hub_->u64s.assign(world(), 0);
+      hub_->u64s[rank_] = v;
+    }
+    hub_->barrier(seq);
+    unsigned long long m = 0;
+    for (auto x : hub_->u64s) m = x > m ? x : m;
+    hub_->barrier(seq_++);
+    return m;
+  }
+  void all_gather(dfpca_context* ctx, const double* send, double* recv, i64 count) override {
+    std::vector<Msg> sends, recvs;
+    for (int r = 0; r < world(); ++r) {
+      if (r == rank_) continue;
+      sends.push_back({r, const_cast<double*>(send), count});
+      recvs.push_back({r, recv + r * count, count});
+    }
+    DFPCA_CUDA(cudaMemcpyAsync(recv + rank_ * count, send, sizeof(double) * count, cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+    exchange(ctx, sends, recvs);
+  }
+
+ private:
+  LocalHub* hub_;
+  int rank_;
+  int seq_ = 0;
+};
+
+// ------------------------------------------------------------------ exchange --
+// Runs one phase of the schedule (shard_blocks) for this rank over `buf`
+// (row-major, leading dimension G, row 0 = global row buf_row0).
+void run_shard_exchange(dfpca_context* ctx, Transport& tr, const ShardPlan& plan, int phase, double* buf,
+                        i64 buf_row0) {
+  const int me = tr.rank();
+  const i64 G = plan.G;
+  const std::vector<ShardBlock> blocks = shard_blocks(plan, phase);
+  std::map<int, i64> send_n, recv_n;
+  std::vector<ShardBlock> sends, recvs, locals;
+  for (const ShardBlock& b : blocks) {
+    if (b.src == me && b.dst == me) {
+      if (b.transpose) locals.push_back(b);  // direct own rows are already in place
+      continue;
+    }
+    if (b.src == me) {
+      sends.push_back(b);
+      send_n[b.dst] += b.elems();
+    }
+    if (b.dst == me) {
+      recvs.push_back(b);
+      recv_n[b.src] += b.elems();
+    }
+  }
+  i64 n_send = 0, n_recv = 0, n_local = 0;
+  for (auto& kv : send_n) n_send += kv.second;
+  for (auto& kv : recv_n) n_recv += kv.second;
+  for (auto& b : locals) n_local += b.elems();
+  DevBuf<double> sbuf(static_cast<std::size_t>(std::max<i64>(1, n_send + n_local)));
+  DevBuf<double> rbuf(static_cast<std::size_t>(std::max<i64>(1, n_recv)));
+  // message offsets: peers ascending, blocks in schedule order (both sides agree)
+  std::map<int, i64> soff, roff;
+  {
+    i64 o = 0;
+    for (auto& kv : send_n) {
+      soff[kv.first] = o;
+      o += kv.second;
+    }
+    o = 0;
+    for (auto& kv : recv_n) {
+      roff[kv.first] = o;
+      o += kv.second;
+    }
+  }
+  auto pack = [&](const ShardBlock& b, double* out) {
+    const i64 tiles = ((b.r1 - b.r0 + 31) / 32) * ((b.c1 - b.c0 + 31) / 32);
+    if (tiles > 0)
+      DFPCA_LAUNCH(ctx, k_pack_block, static_cast<unsigned>(tiles), 256, 0, buf, G, buf_row0, b.r0, b.r1, b.c0, b.c1,
+                   b.transpose ? 1 : 0, out);
+  };
+  auto unpack = [&](const ShardBlock& b, const double* in) {
+    if (b.elems() > 0)
+      DFPCA_LAUNCH(ctx, k_unpack_block, grid_for(b.elems(), 256, 148ll * 16), 256, 0, in, buf, G, buf_row0, b.r0,
+                   b.r1, b.c0, b.c1);
+  };
+  {
+    std::map<int, i64> cur = soff;
+    for (const ShardBlock& b : sends) {
+      pack(b, sbuf.get() + cur[b.dst]);
+      cur[b.dst] += b.elems();
+    }
+  }
+  i64 lo = n_send;
+  for (const ShardBlock& b : locals) {
+    pack(b, sbuf.get() + lo);
+    lo += b.elems();
+  }
+  std::vector<Transport::Msg> smsg, rmsg;
+  for (auto& kv : send_n) smsg.push_back({kv.first, sbuf.get() + soff[kv.first], kv.second});
+  for (auto& kv : recv_n) rmsg.push_back({kv.first, rbuf.get() + roff[kv.first], kv.second});
+  tr.exchange(ctx, smsg, rmsg);
+  {
+    std::map<int, i64> cur = roff;
+    for (const ShardBlock& b : recvs) {
+      unpack(b, rbuf.get() + cur[b.src]);
+      cur[b.src] += b.elems();
+    }
+  }
+  lo = n_send;
+  for (const ShardBlock& b : locals) {
+    unpack(b, sbuf.get() + lo);
+    lo += b.elems();
+  }
+}
+
+i64 s1_radius(const Grid& grid, const double* h) {
+  return static_cast<i64>(std::ceil(h[0] / grid.spacing[0]));  // make_taps (smooth.cu) on axis s1
+}
+
+ShardPlan plan_for(const Grid& grid, const double* h, int world) {
+  return make_shard_plan(grid.shape[0], grid.G / grid.shape[0], s1_radius(grid, h), world);
+}
+
+void run_covariance_sharded(dfpca_context* ctx, Transport& tr, const dfpca_binned* b, const Grid& grid,
+                            const double* h, const double* mean_host, dfpca_surface** out) {
+  const ShardPlan plan = plan_for(grid, h, tr.world());
+  CovShardExec ex;
+  ex.plan = &plan;
+  ex.rank = tr.rank();
+  const i64 rn = plan.rn;
+  ex.exchange_pairs = [&](double* pw, double* pv, bool with_pw) {
+    ctx->begin_stage("exchange");
+    const i64 row0 = plan.ha(tr.rank()) * rn;
+    // an idle rank (empty slab) still takes part, with empty buffers
+    run_shard_exchange(ctx, tr, plan, 0, pv, row0);
+    if (with_pw) run_shard_exchange(ctx, tr, plan, 0, pw, row0);
+    ctx->end_stage();
+  };
+  ex.exchange_cov = [&](double* slab) { run_shard_exchange(ctx, tr, plan, 1, slab, plan.a(tr.rank()) * rn); };
+  ex.max_over_ranks = [&](unsigned long long v) { return tr.max_u64(ctx, v); };
+  run_covariance_impl(ctx, b, grid, h, mean_host, &ex, out);
+}
+
+// `world` in-process ranks on ctx's device; the slabs are assembled into one
+// G x G surface on ctx (validation of the decomposition).
+void run_covariance_emulated(dfpca_context* ctx, int world, const dfpca_binned* b, const Grid& grid,
+                             const double* h, const double* mean_host, dfpca_surface** out) {
+  LocalHub hub(world);
+  std::vector<dfpca_surface*> slabs(static_cast<std::size_t>(world), nullptr);
+  std::vector<dfpca_context*> rctx(static_cast<std::size_t>(world), nullptr);
+  std::vector<Failure> errs(static_cast<std::size_t>(world));
+  std::vector<int> failed(static_cast<std::size_t>(world), 0);
+  DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::vector<std::thread> threads;
+  for (int r = 0; r < world; ++r) {
+    threads.emplace_back([&, r] {
+      dfpca_context* c = nullptr;
+      try {
+        if (dfpca_context_create(ctx->device, &c) != 0) fail(kNumeric, "DeviceError", "rank context creation failed");
+        rctx[static_cast<std::size_t>(r)] = c;
+        DFPCA_CUDA(cudaSetDevice(ctx->device));
+        g_alloc_stream = c->stream;
+        LocalTransport tr(&hub, r);
+        run_covariance_sharded(c, tr, b, grid, h, mean_host, &slabs[static_cast<std::size_t>(r)]);
+        DFPCA_CUDA(cudaStreamSynchronize(c->stream));
+        c->collect_stages();
+      } catch (const Failure& e) {
+        errs[static_cast<std::size_t>(r)] = e;
+        failed[static_cast<std::size_t>(r)] = 1;
+        hub.set_abort();
+      } catch (const std::exception& e) {
+        errs[static_cast<std::size_t>(r)] = Failure{kNumeric, "DeviceError", e.what(), -1, -1};
+        failed[static_cast<std::size_t>(r)] = 1;
+        hub.set_abort();
+      }
+      if (c) cudaStreamSynchronize(c->stream);
+      g_alloc_stream = nullptr;
+    });
+  }
+  for (auto& t : threads) t.join();
+  int first = -1;
+  for (int r = 0; r < world; ++r)
+    if (failed[static_cast<std::size_t>(r)] && (first < 0 || errs[static_cast<std::size_t>(r)].name != "DeviceError"))
+      first = r;
+  std::unique_ptr<dfpca_surface> full;
+  if (first < 0) {
+    full = std::make_unique<dfpca_surface>();
+    full->grid = grid;
+    full->kind = DFPCA_SURFACE_COVARIANCE;
+    full->n = grid.G * grid.G;
+    full->rows = grid.G;
+    full->values.alloc(static_cast<std::size_t>(full->n));
+    for (int r = 0; r < world; ++r) {
+      const dfpca_surface* s = slabs[static_cast<std::size_t>(r)];
+      if (s && s->n > 0)
+        DFPCA_CUDA(cudaMemcpyAsync(full->values.get() + s->row0 * grid.G, s->values.get(), sizeof(double) * s->n,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  for (int r = 0; r < world; ++r) {
+    delete slabs[static_cast<std::size_t>(r)];
+    if (rctx[static_cast<std::size_t>(r)]) dfpca_context_destroy(rctx[static_cast<std::size_t>(r)]);
+  }
+  if (first >= 0) throw errs[static_cast<std::size_t>(first)];
+  *out = full.release();
+}
+
+void nccl_unique_id(void* out) {
+  NcclApi& api = NcclApi::get();
+  NcclApi::UniqueId id;
+  api.check(api.GetUniqueId(&id), "ncclGetUniqueId");
+  std::memcpy(out, id.internal, sizeof(id.internal));
+}
+
+std::shared_ptr<Transport> make_nccl_transport(int world, int rank, const void* id) {
+  return std::make_shared<NcclTransport>(world, rank, id);
+}
+
+}  // namespace dfpca_gpu

@@ -1,0 +1,105 @@
+// Host-side slab plan and exchange schedule (see shard.hpp).
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+
+#include "shard.hpp"
+
+namespace dfpca_gpu {
+
+ShardPlan make_shard_plan(i64 n1, i64 rn, i64 R, int world) {
+  ShardPlan p;
+  p.world = world < 1 ? 1 : world;
+  p.n1 = n1;
+  p.rn = rn;
+  p.G = n1 * rn;
+  p.R = R;
+  const i64 g = std::gcd(rn, kShardRowTile);
+  p.unit = kShardRowTile / (g > 0 ? g : 1);
+  const i64 units = (n1 + p.unit - 1) / p.unit;
+  // cumulative upper-triangle weight at every unit boundary
+  std::vector<double> cum(static_cast<std::size_t>(units) + 1, 0.0);
+  for (i64 u = 0; u < units; ++u) {
+    double w = 0.0;
+    for (i64 x = u * p.unit; x < std::min(n1, (u + 1) * p.unit); ++x) w += static_cast<double>(n1 - x) - 0.5;
+    cum[static_cast<std::size_t>(u) + 1] = cum[static_cast<std::size_t>(u)] + w;
+  }
+  const double total = cum.back();
+  p.bounds.assign(static_cast<std::size_t>(p.world) + 1, 0);
+  i64 prev = 0;
+  for (int r = 1; r < p.world; ++r) {
+    const double target = total * r / p.world;
+    // nearest unit boundary to the target, never before the previous one
+    i64 best = prev;
+    double bd = std::fabs(cum[static_cast<std::size_t>(prev)] - target);
+    for (i64 u = prev; u <= units; ++u) {
+      const double dd = std::fabs(cum[static_cast<std::size_t>(u)] - target);
+      if (dd < bd) {
+        bd = dd;
+        best = u;
+      }
+    }
+    prev = best;
+    p.bounds[static_cast<std::size_t>(r)] = std::min(n1, best * p.unit);
+  }
+  p.bounds[static_cast<std::size_t>(p.world)] = n1;
+  return p;
+}
+
+std::vector<ShardBlock> shard_blocks(const ShardPlan& plan, int phase) {
+  std::vector<ShardBlock> out;
+  const i64 rn = plan.rn;
+  for (int q = 0; q < plan.world; ++q) {
+    if (plan.empty(q)) continue;
+    if (phase == 0) {
+      const i64 ha = plan.ha(q), hb = plan.hb(q);
+      for (int p = 0; p < plan.world; ++p) {
+        if (plan.empty(p)) continue;
+        const i64 s0 = std::max(plan.a(p), ha), s1 = std::min(plan.b(p), hb);
+        if (s0 >= s1) continue;
+        // direct: rows of p, columns from p's own slab start (tile(t) >= tile(s))
+        ShardBlock d;
+        d.src = p;
+        d.dst = q;
+        d.r0 = s0 * rn;
+        d.r1 = s1 * rn;
+        d.c0 = std::max(plan.a(p), ha) * rn;
+        d.c1 = plan.G;
+        d.transpose = false;
+        if (d.elems() > 0) out.push_back(d);
+        // mirror: columns before p's slab, from the owners of those rows
+        for (int pp = 0; pp < p; ++pp) {
+          if (plan.empty(pp)) continue;
+          const i64 t0 = std::max(plan.a(pp), ha), t1 = std::min(plan.b(pp), plan.a(p));
+          if (t0 >= t1) continue;
+          ShardBlock m;
+          m.src = pp;
+          m.dst = q;
+          m.r0 = s0 * rn;
+          m.r1 = s1 * rn;
+          m.c0 = t0 * rn;
+          m.c1 = t1 * rn;
+          m.transpose = true;
+          out.push_back(m);
+        }
+      }
+    } else {
+      // covariance rows of q, columns of every earlier rank p: Gamma(t, s) of p
+      for (int p = 0; p < q; ++p) {
+        if (plan.empty(p)) continue;
+        ShardBlock m;
+        m.src = p;
+        m.dst = q;
+        m.r0 = plan.a(q) * rn;
+        m.r1 = plan.b(q) * rn;
+        m.c0 = plan.a(p) * rn;
+        m.c1 = plan.b(p) * rn;
+        m.transpose = true;
+        out.push_back(m);
+      }
+    }
+  }
+  return out;
+}
+
+}  // namespace dfpca_gpu

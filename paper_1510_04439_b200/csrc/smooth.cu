@@ -30,7 +30,10 @@
 namespace dfpca_gpu {
 
 DevGrid upload_grid_axes(dfpca_context* ctx, const Grid& g, DevBuf<double>& storage);
-void build_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, double* pv);
+}  // namespace dfpca_gpu
+#include "pairs.cuh"
+#include "shard_exec.hpp"
+namespace dfpca_gpu {
 
 namespace {
 
@@ -106,6 +109,10 @@ struct ChunkDims {
   // upper-triangle restriction (View::tri) for the passes of tree level i
   std::vector<int> tri;
   View tri_params{};
+  // output window [win_lo, win_hi) along view axis win_k (the s1 pass of a
+  // covariance slab); win_k < 0: none
+  int win_k = -1;
+  i64 win_lo = 0, win_hi = -1;
 };
 
 View make_view(double* p, const ChunkDims& cd, int k, i64 row_stride_override = -1) {
@@ -142,6 +149,12 @@ struct SolveGeom {
   int upper;       // covariance: solve only s <= t (the rest is mirrored)
   const std::uint8_t* mask;  // device mask (nullable)
   const double* mean;        // covariance: centered later; unused here
+  // covariance slab (tiled solve only): moment rows [row_lo, npts / tc) are
+  // solved; local row r is global s node r + row0 and lands in out row
+  // r + row0 - out_row0
+  i64 row_lo = 0;
+  i64 row0 = 0;
+  i64 out_row0 = 0;
 };
 
 template <int N>
@@ -304,16 +317,18 @@ __device__ __forceinline__ void solve_tri_body(const SharedMoments& sh, const Mo
   constexpr int d = p / 2;
   constexpr int nm = 1 + p + p * (p + 1) / 2;
   constexpr int nl = 1 + p;
-  const int row = static_cast<int>(blockIdx.x / nch);
-  const int ch = static_cast<int>(blockIdx.x - static_cast<unsigned>(row) * nch);
+  const int lrow = static_cast<int>(blockIdx.x / nch);
+  const int ch = static_cast<int>(blockIdx.x - static_cast<unsigned>(lrow) * nch);
   const int tc = static_cast<int>(g.tc);
   const int t0 = static_cast<int>(g.t0);
-  if (t0 + (ch + 1) * kSolveTile <= row) return;  // whole chunk below the diagonal
+  const int mrow = lrow + static_cast<int>(g.row_lo);  // moment row
+  const int row = mrow + static_cast<int>(g.row0);     // global s node
+  if (t0 + (ch + 1) * kSolveTile <= row) return;       // whole chunk below the diagonal
   const int c = ch * kSolveTile + static_cast<int>(threadIdx.x);
   const int col = t0 + c;
   if (c >= tc || col < row) return;
-  const i64 e = static_cast<i64>(row) * tc + c;
-  const i64 dst = static_cast<i64>(row) * g.gt + col;
+  const i64 e = static_cast<i64>(mrow) * tc + c;
+  const i64 dst = static_cast<i64>(row - g.out_row0) * g.gt + col;
   if (g.mask && !(g.mask[row] != 0 && g.mask[col] != 0)) {
     out[dst] = __longlong_as_double(0x7ff8000000000000ll);
     return;
@@ -507,14 +522,17 @@ __global__ void k_ladder(LadderGeom lg, const double* __restrict__ mass, const d
 // symmetric.  32x32 tile pairs keep both the row and the mirrored column
 // accesses coalesced.
 __global__ void k_center_mirror(double* __restrict__ cov, const double* __restrict__ mean,
-                                const std::uint8_t* __restrict__ mask, i64 G) {
+                                const std::uint8_t* __restrict__ mask, i64 G, i64 I0, i64 I1, i64 out_row0) {
+  // Slab form (shard.hpp): row tiles [I0, I1) of 32 rows, cov holds global
+  // rows from out_row0 on; mirrors land only inside the slab's own rows (the
+  // rest reach their owners through the covariance exchange).
   __shared__ double tile[32][33];
   const i64 tiles = (G + 31) / 32;
   // tile pair (I <= J) of this CTA: row I starts at pair index
   // start(I) = I * tiles - I (I - 1) / 2; invert with a square root, then fix
   // the rounding
-  const i64 t = blockIdx.x;
   auto start = [tiles](i64 i) { return i * tiles - i * (i - 1) / 2; };
+  const i64 t = blockIdx.x + start(I0);
   const double tb = 2.0 * static_cast<double>(tiles) + 1.0;
   i64 I = static_cast<i64>((tb - sqrt(tb * tb - 8.0 * static_cast<double>(t))) * 0.5);
   if (I < 0) I = 0;
@@ -527,16 +545,18 @@ __global__ void k_center_mirror(double* __restrict__ cov, const double* __restri
     const i64 a = I * 32 + r, b = J * 32 + tx;
     double v = 0.0;
     if (a < G && b < G && a <= b) {
-      v = cov[a * G + b];
+      double* p = cov + (a - out_row0) * G + b;
+      v = *p;
       if (!mask || (mask[a] && mask[b])) v -= mean[a] * mean[b];
-      cov[a * G + b] = v;
+      *p = v;
     }
     tile[r][tx] = v;
   }
+  if (J >= I1) return;  // mirror rows belong to a later slab
   __syncthreads();
   for (int r = ty; r < 32; r += 8) {
     const i64 b = J * 32 + r, a = I * 32 + tx;  // mirror (b, a) of the upper entry (a, b)
-    if (a < G && b < G && a < b) cov[b * G + a] = tile[tx][r];
+    if (a < G && b < G && a < b) cov[(b - out_row0) * G + a] = tile[tx][r];
   }
 }
 
@@ -550,20 +570,23 @@ namespace {
 
 using SolveLauncher = void (*)(dfpca_context*, const MomPtrs&, const SolveGeom&, double*,
                                unsigned long long*, i64*, i64);
-// Tiled upper-triangle launch geometry: (rows x chunks) CTAs, or 0 when the
-// chunk does not qualify (not the upper covariance, or too many CTAs).
+// Tiled upper-triangle launch geometry: (rows x chunks) CTAs, or -1 when the
+// chunk does not qualify (not the upper covariance, or too many CTAs; slabs
+// always qualify, see run_covariance_impl).
 inline i64 tri_ctas(const SolveGeom& g, int& nch) {
-  if (!(g.cov && g.upper) || g.tc <= 0 || g.gt > (i64(1) << 30)) return 0;
+  if (!(g.cov && g.upper) || g.tc <= 0 || g.gt > (i64(1) << 30)) return -1;
   nch = static_cast<int>((g.tc + kSolveTile - 1) / kSolveTile);
-  const i64 n = (g.npts / g.tc) * nch;
-  return n < (i64(1) << 31) ? n : 0;
+  const i64 rows = g.npts / g.tc - g.row_lo;
+  const i64 n = (rows > 0 ? rows : 0) * nch;
+  return n < (i64(1) << 31) ? n : -1;
 }
 template <int N>
 void launch_solve(dfpca_context* ctx, const MomPtrs& mp, const SolveGeom& g, double* out,
                   unsigned long long* cnt, i64* list, i64 cap) {
   int nch = 0;
-  if (const i64 n = tri_ctas(g, nch)) {
-    DFPCA_LAUNCH(ctx, k_solve_tri<N>, static_cast<unsigned>(n), kSolveTile, 0, mp, g, nch, out, cnt, list, cap);
+  if (const i64 n = tri_ctas(g, nch); n >= 0) {
+    if (n > 0)
+      DFPCA_LAUNCH(ctx, k_solve_tri<N>, static_cast<unsigned>(n), kSolveTile, 0, mp, g, nch, out, cnt, list, cap);
     return;
   }
   DFPCA_LAUNCH(ctx, k_solve<N>, grid_for(g.npts, 128, 148ll * 64), 128, 0, mp, g, out, cnt, list,
@@ -573,8 +596,9 @@ template <int N>
 void launch_solve_shared_n(dfpca_context* ctx, const SharedMoments& sh, const MomPtrs& mp, const SolveGeom& g,
                            double* out, unsigned long long* cnt, i64* list, i64 cap) {
   int nch = 0;
-  if (const i64 n = tri_ctas(g, nch)) {
-    DFPCA_LAUNCH(ctx, k_solve_shared_tri<N>, static_cast<unsigned>(n), kSolveTile, 0, sh, mp, g, nch, out, cnt,
+  if (const i64 n = tri_ctas(g, nch); n >= 0) {
+    if (n > 0)
+      DFPCA_LAUNCH(ctx, k_solve_shared_tri<N>, static_cast<unsigned>(n), kSolveTile, 0, sh, mp, g, nch, out, cnt,
                  list, cap);
     return;
   }
@@ -652,6 +676,13 @@ std::vector<Leaf> run_tree(dfpca_context* ctx, const std::vector<Leaf>& roots,
         spec.in.tri_G = cd.tri_params.tri_G;
         spec.in.tri_rn = cd.tri_params.tri_rn;
         spec.in.tri_n1 = cd.tri_params.tri_n1;
+        spec.in.tri_row0 = cd.tri_params.tri_row0;
+        spec.in.tri_row_hi = cd.tri_params.tri_row_hi;
+        spec.in.tri_t0 = cd.tri_params.tri_t0;
+      }
+      if (ax.view_k == cd.win_k) {
+        spec.in.lo = cd.win_lo;
+        spec.in.hi = cd.win_hi;
       }
       spec.n_out = n_out;
       spec.R = taps[ax.axis_index].R;
@@ -805,9 +836,9 @@ void run_local_linear(dfpca_context* ctx, const dfpca_binned* b, const Grid& gri
 }
 
 // Pair grids + moments + solve + center + symmetrize for the covariance.
-void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid, const double* h,
-                    const double* mean_host, dfpca_surface** out) {
-  static const bool use_fused_s1 = std::getenv("DFPCA_FUSED_S1") != nullptr;  // experimental
+void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid, const double* h,
+                         const double* mean_host, const CovShardExec* shard, dfpca_surface** out) {
+  static const bool use_fused_s1 = std::getenv("DFPCA_FUSED_S1") != nullptr;  // experimental, one device
   const int d = grid.d;
   const int p = 2 * d;
   const i64 G = grid.G;
@@ -818,11 +849,27 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
   for (int k = 0; k < p; ++k) taps[k] = make_taps(h[k % d], grid.spacing[k % d]);
   DevBuf<double> taps_dev(3 * (2 * 4096 + 1));
 
+  // Slab of this rank (shard.hpp): pair-grid / t-partial rows are the s1
+  // planes [ha, hb), output rows the planes [sa, sb); one device: everything.
+  const i64 n1 = grid.shape[0];
+  const i64 rn = G / n1;  // s nodes per s1 plane
+  const bool sharded = shard != nullptr && shard->plan->world > 1;
+  const i64 sa = sharded ? shard->plan->a(shard->rank) : 0, sb = sharded ? shard->plan->b(shard->rank) : n1;
+  const i64 ha = sharded ? shard->plan->ha(shard->rank) : 0, hb = sharded ? shard->plan->hb(shard->rank) : n1;
+  const i64 L = hb - ha;       // local planes
+  const i64 LR = L * rn;       // local pair-grid rows
+  const i64 row0 = ha * rn;    // global s of local row 0
+  const i64 out_row0 = sa * rn;
+  const i64 out_rows = (sb - sa) * rn;
+  const i64 col_lo = sa * rn;  // first column any output of this slab needs (t >= s)
+
   auto surf = std::make_unique<dfpca_surface>();
   surf->grid = grid;
   surf->kind = DFPCA_SURFACE_COVARIANCE;
-  surf->n = G2;
-  surf->values.alloc(static_cast<std::size_t>(G2));
+  surf->n = out_rows * G;
+  surf->row0 = out_row0;
+  surf->rows = out_rows;
+  surf->values.alloc(static_cast<std::size_t>(surf->n));
 
   // Shared constant design (dfpca_binned::shared_const): the reference's pw is
   // sw - dm0 [u == v] entry by entry, so the mass moments are closed-form
@@ -886,10 +933,29 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
   }
 
   // ---- pair grids (K2) ----
-  DevBuf<double> pw, pv(static_cast<std::size_t>(G2));
-  if (!shared) pw.alloc(static_cast<std::size_t>(G2));
+  // one device: the whole G x G grids; a slab: rows [ha, hb) planes, columns
+  // from ha (the t window of the slab's outputs), SYRK over its own row tiles
+  // and the rest received from the other ranks (shard.hpp, exchange 1)
+  DevBuf<double> pw, pv(static_cast<std::size_t>(LR * G));
+  if (!shared) pw.alloc(static_cast<std::size_t>(LR * G));
   ctx->begin_stage("pairs");
-  build_pair_grids(ctx, b, shared ? nullptr : pw.get(), pv.get());
+  if (sharded) {
+    PairWindow win;
+    win.row0 = row0;
+    win.rows = LR;
+    win.col0 = row0;
+    win.tm_begin = sa * rn / kShardRowTile;
+    win.tm_end = (sb * rn + kShardRowTile - 1) / kShardRowTile;
+    double* pwp = shared ? nullptr : pw.get();
+    double* pvp = pv.get();
+    if (sa < sb)
+      build_pair_grids(ctx, b, pwp, pvp, &win,
+                       [&](bool pw_syrk) { shard->exchange_pairs(pw_syrk ? pwp : nullptr, pvp, pw_syrk); });
+    else  // idle rank: still takes part in the exchange
+      shard->exchange_pairs(nullptr, nullptr, !shared && !b->identical_mass);
+  } else {
+    build_pair_grids(ctx, b, shared ? nullptr : pw.get(), pv.get());
+  }
   ctx->end_stage();
 
   // ---- phase T: t-axis passes over row chunks of the pair grids ----
@@ -916,11 +982,11 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
     rec(d, Orders{}, 0, 1, val_idx);
     if (shared) mass_idx.clear();
     for (auto& o : mass_idx) {
-      tpart_store.push_back(std::make_unique<DevBuf<double>>(static_cast<std::size_t>(G2)));
+      tpart_store.push_back(std::make_unique<DevBuf<double>>(static_cast<std::size_t>(LR * G)));
       tpart[{o, 2}] = tpart_store.back()->get();
     }
     for (auto& o : val_idx) {
-      tpart_store.push_back(std::make_unique<DevBuf<double>>(static_cast<std::size_t>(G2)));
+      tpart_store.push_back(std::make_unique<DevBuf<double>>(static_cast<std::size_t>(LR * G)));
       tpart[{o, 1}] = tpart_store.back()->get();
     }
   }
@@ -929,8 +995,8 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
   i64 sc = std::max<i64>(1, std::min<i64>(G, budget_elems / std::max<i64>(G, 1) / 4));
   std::vector<TreeAxis> taxes;
   for (int k = p - 1; k >= d; --k) taxes.push_back({k, k - d});
-  for (i64 s0 = 0; s0 < G; s0 += sc) {
-    const i64 rows = std::min(sc, G - s0);
+  for (i64 s0 = 0; s0 < (sa < sb ? LR : 0); s0 += sc) {
+    const i64 rows = std::min(sc, LR - s0);
     ChunkDims cd;
     cd.rows = rows;
     for (int k = d; k < p; ++k) cd.shape.push_back(grid.shape[k - d]);
@@ -999,19 +1065,20 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
   // (the reference averages the (s,t) and (t,s) fits of mirror-image windows,
   // fft_smoother.hpp:730-736), so the lower triangle is the mirror copy
   // written by the symmetrization pass.  A chunk of columns [t0, t0+cols)
-  // needs output rows s1 < s1_out and, for the last (s1) pass, input rows
-  // s1 < s1_out + R.
-  const i64 row_nodes = G / grid.shape[0];  // s-nodes per s1 row
+  // needs output planes s1 < s1_out and, for the last (s1) pass, input planes
+  // s1 < s1_out + R.  A slab (shard.hpp) starts its columns at its first
+  // output row, reads its local planes [ha, hb) and writes planes [sa, sb).
+  const i64 R0 = taps[0].R;
   i64 tc = std::max<i64>(1, std::min<i64>(G, budget_elems / std::max<i64>(G, 1) / 4));
-  // d = 2 with the whole grid in one chunk: the per-tile restriction of the
-  // pass kernels (View::tri) trims the s rows column tile by column tile
-  const bool tri_tiles = d == 2 && tc >= G;
   std::vector<TreeAxis> saxes;
   for (int k = d - 1; k >= 0; --k) saxes.push_back({k, k});
-  for (i64 t0 = 0; t0 < G; t0 += tc) {
+  for (i64 t0 = col_lo; t0 < G && sa < sb; t0 += tc) {
     const i64 cols = std::min(tc, G - t0);
-    const i64 s1_out = std::min<i64>(grid.shape[0], (t0 + cols - 1) / row_nodes + 1);
-    const i64 s1_in = std::min<i64>(grid.shape[0], s1_out + taps[0].R);
+    const i64 s1_out = std::min<i64>(sb, (t0 + cols - 1) / rn + 1) - ha;  // local end of output planes
+    const i64 s1_in = std::min<i64>(L, s1_out + R0);
+    // d = 2 with all columns in one chunk: the per-tile restriction of the
+    // pass kernels (View::tri) trims the s rows column tile by column tile
+    const bool tri_tiles = d == 2 && t0 == col_lo && cols == G - col_lo;
     ChunkDims cd;
     cd.rows = 1;
     for (int k = 0; k < d; ++k) cd.shape.push_back(grid.shape[k]);
@@ -1019,12 +1086,20 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
     cd.tail = cols;
     if (tri_tiles) {
       cd.tri = {1, 2};  // s2 pass, then s1 pass
-      cd.tri_params.tri_R = static_cast<int>(taps[0].R);
+      cd.tri_params.tri_R = static_cast<int>(R0);
       cd.tri_params.tri_G = cols;
-      cd.tri_params.tri_rn = row_nodes;
-      cd.tri_params.tri_n1 = grid.shape[0];
+      cd.tri_params.tri_rn = rn;
+      cd.tri_params.tri_n1 = L;
+      cd.tri_params.tri_row0 = ha;
+      cd.tri_params.tri_row_hi = sb;
+      cd.tri_params.tri_t0 = t0;
     }
-    const i64 chunk_elems = s1_in * row_nodes * cols;
+    if (sharded) {  // the s1 pass writes the slab's own planes only
+      cd.win_k = 0;
+      cd.win_lo = sa - ha;
+      cd.win_hi = s1_out;
+    }
+    const i64 chunk_elems = s1_in * rn * cols;
     // roots: the t-partials viewed as [s1 < s1_in][s2..][cols] with row stride G;
     // the first pass runs along the last s-axis
     std::vector<Leaf> roots;
@@ -1038,7 +1113,7 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
       v.n = d == 1 ? s1_in : grid.shape[d - 1];  // d = 1: the first pass is the truncated s1 axis
       v.js = G;
       v.inner = cols;
-      v.outer = d == 1 ? 1 : s1_in * row_nodes / grid.shape[d - 1];
+      v.outer = d == 1 ? 1 : s1_in * rn / grid.shape[d - 1];
       v.os = v.n * G;
       r.view = v;
       roots.push_back(r);
@@ -1050,6 +1125,22 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
       return finals.back()->get();
     };
     auto final_rs = [&](const Orders&, int) -> i64 { return -1; };
+    SolveGeom sg{};
+    sg.npts = s1_out * rn * cols;
+    sg.tc = cols;
+    sg.t0 = t0;
+    sg.gt = G;
+    sg.cov = 1;
+    sg.upper = 1;
+    sg.mask = grid.has_mask ? mask_dev.get() : nullptr;
+    sg.row_lo = (sa - ha) * rn;
+    sg.row0 = row0;
+    sg.out_row0 = out_row0;
+    if (sharded) {
+      int nch = 0;
+      if (tri_ctas(sg, nch) < 0) fail(kConfig, "InvalidArgument", "covariance slab too large for the tiled solve");
+    }
+    std::vector<Leaf> leaves;
     if (d == 2) {
       // s2 pass, then the fused s1 pass + solve (s1solve.cu): the 20 moment
       // arrays of the chunk never reach HBM
@@ -1057,7 +1148,7 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
       std::vector<Leaf> l2 = run_tree(ctx, roots, s2ax, cd, taps, chunk_elems, taps_dev.get(), keep, final_dst,
                                       final_rs, true, -1);
       S1SolveSpec sp{};
-      bool ok = true;
+      bool ok = !sharded;
       const auto order = s1_p4_input_order();
       for (std::size_t k = 0; k < order.size(); ++k) {
         const double* ptr = nullptr;
@@ -1074,7 +1165,7 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
       sp.cols = cols;
       sp.t0 = t0;
       sp.G = G;
-      sp.R = taps[0].R;
+      sp.R = R0;
       for (int r = 0; r < 3; ++r) sp.taps[r] = taps[0].t[r].data();
       sp.mask = grid.has_mask ? mask_dev.get() : nullptr;
       sp.out = surf->values.get();
@@ -1090,42 +1181,17 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
       ctx->begin_stage("moments");
       if (fused) continue;
       std::vector<TreeAxis> s1ax = {saxes[1]};
-      std::vector<Leaf> leaves = run_tree(ctx, l2, s1ax, cd, taps, chunk_elems, taps_dev.get(), keep, final_dst,
-                                          final_rs, false, -1);
-      MomPtrs mp{};
-      for (const Leaf& l : leaves) {
-        const int idx = basis.find(l.ord);
-        if (l.budget_max == 2) mp.S[idx] = l.ptr;
-        else mp.T[idx] = l.ptr;
-      }
-      SolveGeom sg{};
-      sg.npts = s1_out * row_nodes * cols;
-      sg.tc = cols;
-      sg.t0 = t0;
-      sg.gt = G;
-      sg.cov = 1;
-      sg.upper = 1;
-      sg.mask = grid.has_mask ? mask_dev.get() : nullptr;
-      if (shared) launch_solve_shared(d, ctx, sh, mp, sg, surf->values.get(), cnt.get(), list.get(), list_cap);
-      else solve_launcher(p)(ctx, mp, sg, surf->values.get(), cnt.get(), list.get(), list_cap);
-      continue;
+      leaves = run_tree(ctx, l2, s1ax, cd, taps, chunk_elems, taps_dev.get(), keep, final_dst, final_rs, false, -1);
+    } else {
+      leaves = run_tree(ctx, roots, saxes, cd, taps, chunk_elems, taps_dev.get(), keep, final_dst, final_rs, true,
+                        -1);
     }
-    std::vector<Leaf> leaves = run_tree(ctx, roots, saxes, cd, taps, chunk_elems, taps_dev.get(), keep,
-                                        final_dst, final_rs, true, -1);
     MomPtrs mp{};
     for (const Leaf& l : leaves) {
       const int idx = basis.find(l.ord);
       if (l.budget_max == 2) mp.S[idx] = l.ptr;
       else mp.T[idx] = l.ptr;
     }
-    SolveGeom sg{};
-    sg.npts = s1_out * row_nodes * cols;
-    sg.tc = cols;
-    sg.t0 = t0;
-    sg.gt = G;
-    sg.cov = 1;
-    sg.upper = 1;
-    sg.mask = grid.has_mask ? mask_dev.get() : nullptr;
     ctx->end_stage();
     ctx->begin_stage("solve");
     if (shared) launch_solve_shared(d, ctx, sh, mp, sg, surf->values.get(), cnt.get(), list.get(), list_cap);
@@ -1138,6 +1204,15 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
   DFPCA_CUDA(cudaStreamSynchronize(st));
   ctx->end_stage();
   tpart_store.clear();
+  if (sharded) {
+    // every rank must take the same branch before the covariance exchange
+    const unsigned long long any_empty = shard->max_over_ranks(n_empty);
+    if (any_empty > 0)
+      fail(kConfig, "InvalidArgument",
+           "sharded covariance: " + std::to_string(any_empty) +
+               " empty kernel window(s) on some rank need the fallback ladder (fft_smoother.hpp:471-487), "
+               "whose enlarged windows exceed the slab halo; run it on one device or widen the bandwidth");
+  }
 
   if (n_empty > 0) {
     if (static_cast<i64>(n_empty) > list_cap)
@@ -1180,12 +1255,25 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
   DevBuf<double> mean_dev(static_cast<std::size_t>(G));
   DFPCA_CUDA(cudaMemcpyAsync(mean_dev.get(), mean_host, sizeof(double) * G, cudaMemcpyHostToDevice, st));
   const i64 tiles = (G + 31) / 32;
-  const i64 pairs = tiles * (tiles + 1) / 2;
-  DFPCA_LAUNCH(ctx, k_center_mirror, static_cast<unsigned>(pairs), 256, 0, surf->values.get(),
-               mean_dev.get(), grid.has_mask ? mask_dev.get() : nullptr, G);
+  const i64 I0 = out_row0 / 32, I1 = (out_row0 + out_rows + 31) / 32;
+  auto pstart = [tiles](i64 i) { return i * tiles - i * (i - 1) / 2; };
+  const i64 pairs = pstart(I1) - pstart(I0);
+  if (pairs > 0)
+    DFPCA_LAUNCH(ctx, k_center_mirror, static_cast<unsigned>(pairs), 256, 0, surf->values.get(), mean_dev.get(),
+                 grid.has_mask ? mask_dev.get() : nullptr, G, I0, I1, out_row0);
   ctx->end_stage();
+  if (sharded) {  // exchange 2: the lower-triangle blocks of this slab's rows
+    ctx->begin_stage("exchange");
+    shard->exchange_cov(surf->values.get());
+    ctx->end_stage();
+  }
   DFPCA_CUDA(cudaStreamSynchronize(st));
   *out = surf.release();
+}
+
+void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid, const double* h,
+                    const double* mean_host, dfpca_surface** out) {
+  run_covariance_impl(ctx, b, grid, h, mean_host, nullptr, out);
 }
 
 }  // namespace dfpca_gpu

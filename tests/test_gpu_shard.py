@@ -1,0 +1,102 @@
+"""GPU: the slab-sharded covariance (csrc/shard.cu) is bit-identical to the
+one-device covariance for any rank count (SURVEY.md 8(e) invariance target).
+
+The ranks run as threads of this process on one GPU, each with its own
+context and stream, exchanging the schedule's blocks device to device
+(LocalTransport); they meet only at host-side barriers, no kernel waits on
+another rank.  The NCCL transport moves the same packed blocks between
+processes.  The schedule itself is checked between processes on CPU
+(tests/test_shard_plan.py).
+"""
+import numpy as np
+import pytest
+
+from helpers import bit_equal
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    # shared design (closed-form mass moments), d = 2, 4 units of 128 rows
+    "2d_nodes": lambda s: s.grid_nodes(2, 32, 60, 0.1),
+    # general design (pw and pv both from the SYRK and both exchanged)
+    "2d_random": lambda s: s.random_points(2, 24, 80, 40, 0.25),
+    "2d_masked_sparse": lambda s: s.sparse_masked(32, 400, 0.3),
+    # d = 3: generic tree passes and chunked columns
+    "3d_nodes": lambda s: s.grid_nodes(3, 8, 12, 0.3),
+    "3d_random": lambda s: s.random_points(3, 8, 30, 40, 0.35),
+    # d = 1: one unit of 128 nodes per slab
+    "1d_random": lambda s: s.random_points(1, 512, 30, 40, 0.05),
+}
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_1510_04439_b200 import api as A
+    return A
+
+
+def _setup(api, sd):
+    grid = sd.grid()
+    b = api.linear_bin(sd.dataset(), grid, api.BinOptions(True, True))
+    h = api.Bandwidth(sd.h)
+    mean = api.fft_local_linear(b, grid, h, api.MomentTarget.Mean)
+    return grid, b, h, mean
+
+
+@pytest.mark.parametrize("case", list(CASES))
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_covariance_bit_identical(api, case, world):
+    from paper_1510_04439_b200 import synth
+    sd = CASES[case](synth)
+    grid, b, h, mean = _setup(api, sd)
+    one = api.fft_covariance(b, grid, h, mean).values
+    many = api.fft_covariance_emulated(b, grid, h, mean, world)
+    assert many.rows() == (0, grid.size())
+    assert bit_equal(many.values, one), f"{case} x{world}"
+
+
+def test_sharded_general_path_forced(api, monkeypatch):
+    """GridNodes input through the general pair path (pw from the SYRK and
+    exchanged as well) -- DFPCA_GENERAL_PAIRS=1."""
+    from paper_1510_04439_b200 import synth
+    sd = synth.grid_nodes(2, 32, 40, 0.1)
+    grid, b, h, mean = _setup(api, sd)
+    monkeypatch.setenv("DFPCA_GENERAL_PAIRS", "1")
+    one = api.fft_covariance(b, grid, h, mean).values
+    many = api.fft_covariance_emulated(b, grid, h, mean, 4)
+    assert bit_equal(many.values, one)
+
+
+def test_sharded_with_idle_ranks(api):
+    """More ranks than 128-row units: the surplus ranks hold empty slabs and
+    still take part in both exchanges."""
+    from paper_1510_04439_b200 import synth
+    sd = synth.grid_nodes(2, 16, 30, 0.2)  # G = 256: two units
+    grid, b, h, mean = _setup(api, sd)
+    bounds = api.shard_bounds(16, 16, 4, 5)
+    assert sum(1 for r in range(5) if bounds[r] == bounds[r + 1]) >= 3
+    one = api.fft_covariance(b, grid, h, mean).values
+    many = api.fft_covariance_emulated(b, grid, h, mean, 5)
+    assert bit_equal(many.values, one)
+
+
+def test_sharded_rejects_empty_windows_consistently(api):
+    """Empty kernel windows need the enlarged-window ladder, which the slabs
+    cannot serve; every rank raises (no rank is left waiting in an exchange)."""
+    from paper_1510_04439_b200 import synth
+    sd = synth.grid_nodes(2, 16, 20, 0.05)  # h < spacing: empty diagonal windows
+    grid, b, h, mean = _setup(api, sd)
+    api.fft_covariance(b, grid, h, mean)  # one device: the ladder handles them
+    with pytest.raises(api.Error) as e:
+        api.fft_covariance_emulated(b, grid, h, mean, 2)
+    assert "fallback ladder" in str(e.value)
+
+
+def test_single_rank_sharded_entry_is_the_plain_covariance(api):
+    from paper_1510_04439_b200 import synth
+    sd = synth.grid_nodes(2, 16, 30, 0.2)
+    grid, b, h, mean = _setup(api, sd)
+    one = api.fft_covariance(b, grid, h, mean).values
+    s = api.fft_covariance_sharded(b, grid, h, mean)  # no communicator: one rank
+    assert s.rows() == (0, grid.size())
+    assert bit_equal(s.values, one)

@@ -10,8 +10,10 @@ covariance over G^2 = 16,777,216 grid points (synthetic data of that shape).
 A "step" is one fft_covariance (reference fft_smoother.hpp:585): pair grids,
 the 20 kernel-moment convolutions, the per-node 5x5 solves with the fallback
 ladder, centering and symmetrization, from device-resident binned data to a
-device-resident covariance.  value = G^2 / step time (gridpts/s), summed over
-ranks; N > 1 runs one independent replica per GPU ("scaling": "weak").
+device-resident covariance.  value = G^2 / step time (gridpts/s).  N > 1 splits
+the one covariance into s1-plane slabs, one per GPU (csrc/shard.hpp: SYRK over
+each rank's row tiles, NCCL exchanges of the pair-grid windows and of the
+covariance rows), step time = max over ranks ("scaling": "strong").
 e2e: the same metric through the public API with host buffers: pinned host
 observations -> linear_bin -> fft_local_linear -> fft_covariance -> covariance
 copied back to pinned host memory, every step.
@@ -143,7 +145,7 @@ def run_reference(args, emit=True):
     sample = (f"fft_covariance on the full 64x64 grid (16,777,216 gridpts), first {n_sub} of {N_SUBJ} subjects, "
               f"reference headers compiled unchanged (oracle/_ref), set_max_threads({cores})")
     line = {"metric": METRIC, "value": val, "unit": "gridpts/s", "n_gpus": args.gpus, "steps": len(times),
-            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "cpu_sample": f"n={n_sub}"},
             "impl": "reference",
@@ -184,7 +186,18 @@ def main():
     os.environ.setdefault("DFPCA_DEVICE", str(local))
 
     from paper_1510_04439_b200 import _lib, api
-    sd = make_data(seed=20260815 + rank)
+    sharded = world > 1
+    if sharded:
+        # this process's rank of the slab-sharded covariance (csrc/shard.hpp):
+        # our own NCCL communicator, its unique id broadcast over torch's
+        def bcast(uid):
+            obj = [uid]
+            dist.broadcast_object_list(obj, src=0)
+            return obj[0]
+        api.init_distributed(world, rank, broadcast=bcast)
+    cov_fn = api.fft_covariance_sharded if sharded else api.fft_covariance
+    # every rank holds the same data: one covariance split across the GPUs
+    sd = make_data(seed=20260815)
     grid = sd.grid()
     h = api.Bandwidth(sd.h)
     G = grid.size()
@@ -200,7 +213,7 @@ def main():
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB
 
     def one_step():
-        cov = api.fft_covariance(binned, grid, h, mean)
+        cov = cov_fn(binned, grid, h, mean)
         return _lib.stage_ms("total"), cov
 
     for _ in range(args.warmup):
@@ -233,7 +246,7 @@ def main():
         tt = torch.tensor([t_step], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_step = float(tt.item())
-    value = world * G2 / t_step
+    value = G2 / t_step  # one covariance per step, split across the ranks
 
     # ---- per-kernel profile pass (outside the timed region) ----
     _lib.profile(True)
@@ -243,7 +256,10 @@ def main():
 
     # ---- e2e through the public API with pinned host buffers ----
     offsets, coords, values = data.csr()
-    host_cov = np.empty(G2)
+    probe = cov_fn(binned, grid, h, mean)
+    slab_row0, slab_rows = probe.rows()
+    del probe
+    host_cov = np.empty(slab_rows * G)
     pinned = [_lib.pin(a) for a in (offsets, coords, values, host_cov)]
     e2e_t = []
     for it in range(args.e2e_steps + 1):
@@ -251,7 +267,7 @@ def main():
         t0 = time.perf_counter()
         b2 = api.linear_bin(data, grid, api.BinOptions(True, True))
         m2 = api.fft_local_linear(b2, grid, h, api.MomentTarget.Mean)
-        c2 = api.fft_covariance(b2, grid, h, m2)
+        c2 = cov_fn(b2, grid, h, m2)
         _lib.check(_lib.lib().dfpca_surface_download(_lib.ctx(), c2.device_handle(),
                                                      host_cov.ctypes.data_as(_lib.PD)))
         t1 = time.perf_counter()
@@ -269,7 +285,7 @@ def main():
     m2 = api.fft_local_linear(b2, grid, h, api.MomentTarget.Mean)
     torch.cuda.synchronize(dev)
     brk["mean"] = time.perf_counter() - t0 - sum(brk.values())
-    c2 = api.fft_covariance(b2, grid, h, m2)
+    c2 = cov_fn(b2, grid, h, m2)
     torch.cuda.synchronize(dev)
     brk["covariance"] = time.perf_counter() - t0 - sum(brk.values())
     _lib.check(_lib.lib().dfpca_surface_download(_lib.ctx(), c2.device_handle(), host_cov.ctypes.data_as(_lib.PD)))
@@ -283,15 +299,19 @@ def main():
     d2h = host_cov.nbytes
 
     # ---- full FPCA pipeline once (host obs -> EigenSystem on host) ----
-    torch.cuda.synchronize(dev)
-    t0 = time.perf_counter()
-    b3 = api.linear_bin(data, grid, api.BinOptions(True, True))
-    m3 = api.fft_local_linear(b3, grid, h, api.MomentTarget.Mean)
-    api.fft_local_linear(b3, grid, h, api.MomentTarget.Squares)
-    c3 = api.fft_covariance(b3, grid, h, m3)
-    eig = api.randomized_eig(api.matrixize(c3), 99, 20, grid, 20260815)
-    fpca_ms = (time.perf_counter() - t0) * 1e3
-    eig_ms = _lib.stage_ms("eigen")
+    fpca_ms = eig_ms = None
+    eig_top3 = None
+    if not sharded:
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        b3 = api.linear_bin(data, grid, api.BinOptions(True, True))
+        m3 = api.fft_local_linear(b3, grid, h, api.MomentTarget.Mean)
+        api.fft_local_linear(b3, grid, h, api.MomentTarget.Squares)
+        c3 = api.fft_covariance(b3, grid, h, m3)
+        eig = api.randomized_eig(api.matrixize(c3), 99, 20, grid, 20260815)
+        fpca_ms = (time.perf_counter() - t0) * 1e3
+        eig_ms = _lib.stage_ms("eigen")
+        eig_top3 = eig.eigenvalues[:3]
 
     if rank != 0:
         if dist is not None:
@@ -300,7 +320,7 @@ def main():
         return
 
     # ---- roofline of the dominant kernel ----
-    roof = roofline(kstats, G, binned)
+    roof = roofline(kstats, G, binned, slab=(slab_row0, slab_rows) if sharded else None)
 
     # ---- CPU baseline (reference, rank 0, N = 1) ----
     cpu = None
@@ -316,20 +336,22 @@ def main():
 
     out = {
         "metric": METRIC, "value": value, "unit": "gridpts/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "grid": [CELLS, CELLS], "n_subjects": N_SUBJ, "h": H,
                    "gridpts": G2, "l2": "flushed (256 MB write) before every timed step",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                   "parallelism": (f"slab-sharded s1 planes over {world} GPUs (NCCL exchanges of pair-grid "
+                                   f"windows and covariance rows), rank 0 rows [{slab_row0}, {slab_row0 + slab_rows})"
+                                   if sharded else "single GPU")},
         "stages_ms_per_step": {k: v / args.steps for k, v in stage_acc.items()},
         "wall_ms_per_step": wall / args.steps * 1e3,
-        "e2e": {"value": world * G2 / e2e_step, "unit": "gridpts/s", "h2d_bytes_per_step": int(h2d),
+        "e2e": {"value": G2 / e2e_step, "unit": "gridpts/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_step * 1e3,
                 "breakdown_ms": {k: v * 1e3 for k, v in brk.items()},
                 "all_ms": [round(t * 1e3, 3) for t in e2e_t],
                 "path": "pinned host obs -> linear_bin -> fft_local_linear -> fft_covariance -> host covariance",
                 "pinned": all(pinned)},
-        "fpca_e2e_ms": fpca_ms, "eigen_ms": eig_ms, "eig_top3": eig.eigenvalues[:3],
+        "fpca_e2e_ms": fpca_ms, "eigen_ms": eig_ms, "eig_top3": eig_top3,
         "gpu_launches": int(launches),
         "kernels": {k: {"ms": v[0], "launches": v[1]} for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][0])},
         "roofline": roof,
@@ -426,7 +448,7 @@ def ncu_traffic(kernel: str):
     return sum(vals.values()), f"{files[-1].relative_to(ROOT)} (first launch of {kernel})"
 
 
-def roofline(kstats, G, binned):
+def roofline(kstats, G, binned, slab=None):
     """Dominant kernel (largest device time in one profiled step) against its
     bound, plus the same figure for every modelled kernel."""
     peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
@@ -434,6 +456,10 @@ def roofline(kstats, G, binned):
     if not kstats:
         return None
     model = kernel_model(G, N_SUBJ, shared="k_solve_shared_tri" in kstats)
+    if slab is not None:  # one rank's share: its rows of the upper triangle
+        r0, nr = slab
+        share = (sum(G - s for s in range(r0, r0 + nr))) / (G * (G + 1) / 2)
+        model = {k: (bnd, work * share) for k, (bnd, work) in model.items()}
     total_ms = sum(v[0] for v in kstats.values())
     table = {}
     for name, (ms, cnt) in kstats.items():

@@ -161,6 +161,12 @@ DFPCA_API int dfpca_covariance_sharded(dfpca_context* ctx, const dfpca_binned* b
 DFPCA_API int dfpca_covariance_emulated(dfpca_context* ctx, const dfpca_binned* b, const dfpca_grid* grid,
                               const double* h, const double* mean, const dfpca_plan* plan, int world,
                               dfpca_surface** out);
+/* Rank `rank` of `world` alone with the exchanges dropped (profiling: the
+ * per-rank device time of a sharded step without its communication; the
+ * slab's values are not meaningful). */
+DFPCA_API int dfpca_covariance_slab_dryrun(dfpca_context* ctx, const dfpca_binned* b, const dfpca_grid* grid,
+                                 const double* h, const double* mean, const dfpca_plan* plan, int world,
+                                 int rank, dfpca_surface** out);
 /* Rows of the covariance held by a surface (a slab, or 0 / G). */
 DFPCA_API int dfpca_surface_rows(const dfpca_surface* s, int64_t* row0, int64_t* rows);
 /* Host-side slab plan (no device needed): bounds[0..world] are the s1-plane

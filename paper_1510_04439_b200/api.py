@@ -705,6 +705,19 @@ def fft_covariance_emulated(binned: BinnedData, grid: EvaluationGrid, h: Bandwid
     return SurfaceEstimate(grid, SurfaceKind.Covariance, handle=handle)
 
 
+def covariance_slab_dryrun(binned: BinnedData, grid: EvaluationGrid, h: Bandwidth, mean: SurfaceEstimate,
+                           world: int, rank: int) -> SurfaceEstimate:
+    """Profiling only: rank `rank` of `world` computes its slab with the
+    exchanges dropped (device time of one rank's share; values meaningless)."""
+    hh, mv, pdesc, keep = _cov_args(binned, grid, h, mean, None)
+    handle = C.c_void_p()
+    check(_lib.lib().dfpca_covariance_slab_dryrun(_lib.ctx(), binned.handle, C.byref(grid.desc()),
+                                                  hh.ctypes.data_as(C.POINTER(C.c_double)),
+                                                  mv.ctypes.data_as(C.POINTER(C.c_double)), None, int(world),
+                                                  int(rank), C.byref(handle)))
+    return SurfaceEstimate(grid, SurfaceKind.Covariance, handle=handle)
+
+
 def shard_bounds(n1: int, nodes_per_plane: int, radius: int, world: int) -> list:
     out = (C.c_int64 * (world + 1))()
     check_plain(_lib.lib().dfpca_shard_bounds(n1, nodes_per_plane, radius, world, out))

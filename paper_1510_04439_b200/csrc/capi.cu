@@ -1,7 +1,10 @@
 // extern "C" entry points of libdfpca_cuda.so (include/dfpca_cuda.h):
 // argument validation in the reference's order, error mapping to the
 // reference's error names, handle management and stage timing.
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <iterator>
@@ -31,6 +34,8 @@ void run_covariance_sharded(dfpca_context* ctx, Transport& tr, const dfpca_binne
 void run_covariance_emulated(dfpca_context* ctx, int world, const dfpca_binned* b, const Grid& grid,
                              const double* h, const double* mean_host, dfpca_surface** out);
 void nccl_unique_id(void* out);
+void run_covariance_dryrun(dfpca_context* ctx, int world, int rank, const dfpca_binned* b, const Grid& grid,
+                           const double* h, const double* mean_host, dfpca_surface** out);
 std::shared_ptr<Transport> make_nccl_transport(int world, int rank, const void* id);
 void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid& grid, i64 q,
                         i64 L_max, unsigned long long seed, double* eigenvalues, double* eigenfunctions,
@@ -195,7 +200,21 @@ void validate_plan(const dfpca_plan* plan, const Grid& grid, const double* h) {
 using namespace dfpca_gpu;
 
 // ---- context stage timing ---------------------------------------------------
+namespace {
+// DFPCA_HOST_TRACE=1: host wall-clock stamps at stage boundaries (stderr), to
+// find host gaps between the device stages
+double host_us() {
+  static const auto t0 = std::chrono::steady_clock::now();
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+}
+bool host_trace() {
+  static const bool on = std::getenv("DFPCA_HOST_TRACE") != nullptr;
+  return on;
+}
+}  // namespace
+
 void dfpca_context::begin_stage(const std::string& name) {
+  if (host_trace()) std::fprintf(stderr, "[host %10.1f us] begin %s\n", host_us(), name.c_str());
   StageMark m;
   m.name = name;
   cudaEventCreate(&m.start);
@@ -204,6 +223,7 @@ void dfpca_context::begin_stage(const std::string& name) {
   marks.push_back(m);
 }
 void dfpca_context::end_stage() {
+  if (host_trace()) std::fprintf(stderr, "[host %10.1f us] end\n", host_us());
   for (auto it = marks.rbegin(); it != marks.rend(); ++it)
     if (it->stop && !it->name.empty() && it->name[0] != '#') {
       cudaEventRecord(it->stop, stream);
@@ -323,6 +343,7 @@ int dfpca_context_destroy(dfpca_context* ctx) {
   {
     g_alloc_stream = ctx->stream;
     ctx->scratch.release();
+    ctx->table_cache.clear();
     cudaStreamSynchronize(ctx->stream);
     g_alloc_stream = nullptr;
   }
@@ -585,6 +606,16 @@ int dfpca_covariance_emulated(dfpca_context* ctx, const dfpca_binned* b, const d
     Grid g = validate_covariance(b, grid, h, mean, plan, out);
     if (world < 1) fail(kConfig, "InvalidArgument", "world must be >= 1");
     run_covariance_emulated(ctx, world, b, g, h, mean, out);
+  });
+}
+
+int dfpca_covariance_slab_dryrun(dfpca_context* ctx, const dfpca_binned* b, const dfpca_grid* grid,
+                                 const double* h, const double* mean, const dfpca_plan* plan, int world, int rank,
+                                 dfpca_surface** out) {
+  return guarded(ctx, [&] {
+    Grid g = validate_covariance(b, grid, h, mean, plan, out);
+    if (world < 1 || rank < 0 || rank >= world) fail(kConfig, "InvalidArgument", "bad rank / world");
+    run_covariance_dryrun(ctx, world, rank, b, g, h, mean, out);
   });
 }
 

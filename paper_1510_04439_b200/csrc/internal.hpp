@@ -129,6 +129,9 @@ struct dfpca_context {
   // multi-GPU (dfpca_nccl_init): this process's rank of a sharded covariance
   std::shared_ptr<dfpca_gpu::Transport> transport;
 
+  // Device tables that depend only on the grid and bandwidth (smooth.cu),
+  // built on first use.
+  std::map<std::string, std::unique_ptr<dfpca_gpu::DevBuf<double>>> table_cache;
   // Reusable scratch (grown on demand, never shrunk while the context lives).
   dfpca_gpu::DevBuf<unsigned char> scratch;
   unsigned char* scratch_bytes(std::size_t n) {

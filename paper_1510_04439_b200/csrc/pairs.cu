@@ -128,6 +128,8 @@ void build_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, dou
   const i64 own = w.tm_begin * kShardRowTile - w.row0;
   double W = 0.0;
   for (double x : b->pair_weight_h) W += x;  // sequential, as the reference's sample loop
+  DevBuf<double> axes;
+  const DevGrid dg = upload_grid_axes(ctx, b->grid, axes);  // (synchronizes: before the SYRK is queued)
   if (pw) {
     if (b->identical_mass) {
       DFPCA_LAUNCH(ctx, k_rank_one, grid_for(w.rows * (G - w.col0), 256, 148ll * 16), 256, 0, pw,
@@ -141,15 +143,11 @@ void build_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, dou
     gemm_tn(ctx, G, G, n, b->ps_value.get(), G, b->pair_weight.get(), b->ps_value.get(), G, pv + own * G, G, true,
             w.tm_begin, tm_end);
   if (exchange) exchange(pw != nullptr && !b->identical_mass);
-  if (pv) {
-    DevBuf<double> axes;
-    DevGrid dg = upload_grid_axes(ctx, b->grid, axes);
+  if (pv)
     DFPCA_LAUNCH(ctx, k_band_fix, grid_for(w.rows * b->codes * 32, 256, 148ll * 32), 256, 0,
                  b->diag_mass.get(), b->diag_value.get(), G, b->grid.d, b->codes, dg,
                  b->ps_mass.get(), b->identical_mass ? 1 : 0, b->pair_weight.get(), n, W, pw, pv, w.row0, w.rows,
                  w.col0);
-    DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
-  }
 }
 
 }  // namespace dfpca_gpu

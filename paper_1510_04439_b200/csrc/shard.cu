@@ -12,6 +12,7 @@
 //    -- ranks meet only at host-side barriers between exchanges.
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cmath>
 #include <condition_variable>
 #include <cstring>
@@ -57,12 +58,15 @@ __global__ void k_pack_block(const double* __restrict__ src, i64 ld, i64 row0, i
   }
 }
 
+// dst[(s - row0) * ld + t] = packed block; one CTA row per block row, threads
+// across the columns (coalesced on both sides, no per-element division).
 __global__ void k_unpack_block(const double* __restrict__ in, double* __restrict__ dst, i64 ld, i64 row0, i64 r0,
                                i64 r1, i64 c0, i64 c1) {
-  const i64 w = c1 - c0, total = (r1 - r0) * w;
-  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total; e += (i64)gridDim.x * blockDim.x) {
-    const i64 s = e / w, t = e % w;
-    dst[(r0 + s - row0) * ld + c0 + t] = in[e];
+  const i64 w = c1 - c0, h = r1 - r0;
+  for (i64 s = blockIdx.x; s < h; s += gridDim.x) {
+    const double* src = in + s * w;
+    double* out = dst + (r0 + s - row0) * ld + c0;
+    for (i64 t = threadIdx.x; t < w; t += blockDim.x) out[t] = src[t];
   }
 }
 
@@ -303,6 +307,24 @@ class LocalTransport final : public Transport {
   int seq_ = 0;
 };
 
+// One rank of `world` with the exchanges dropped: times a rank's slab alone
+// (the received regions hold whatever the buffers held -- timing only).
+class NullTransport final : public Transport {
+ public:
+  NullTransport(int world, int rank) : world_(world), rank_(rank) {}
+  int rank() const override { return rank_; }
+  int world() const override { return world_; }
+  void exchange(dfpca_context*, const std::vector<Msg>&, const std::vector<Msg>&) override {}
+  unsigned long long max_u64(dfpca_context*, unsigned long long v) override { return v; }
+  void all_gather(dfpca_context* ctx, const double* send, double* recv, i64 count) override {
+    DFPCA_CUDA(cudaMemcpyAsync(recv + rank_ * count, send, sizeof(double) * count, cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+  }
+
+ private:
+  int world_, rank_;
+};
+
 // ------------------------------------------------------------------ exchange --
 // Runs one phase of the schedule (shard_blocks) for this rank over `buf`
 // (row-major, leading dimension G, row 0 = global row buf_row0).
@@ -355,8 +377,8 @@ void run_shard_exchange(dfpca_context* ctx, Transport& tr, const ShardPlan& plan
   };
   auto unpack = [&](const ShardBlock& b, const double* in) {
     if (b.elems() > 0)
-      DFPCA_LAUNCH(ctx, k_unpack_block, grid_for(b.elems(), 256, 148ll * 16), 256, 0, in, buf, G, buf_row0, b.r0,
-                   b.r1, b.c0, b.c1);
+      DFPCA_LAUNCH(ctx, k_unpack_block, static_cast<unsigned>(std::min<i64>(b.r1 - b.r0, 148ll * 16)), 256, 0, in,
+                   buf, G, buf_row0, b.r0, b.r1, b.c0, b.c1);
   };
   {
     std::map<int, i64> cur = soff;
@@ -479,6 +501,12 @@ void run_covariance_emulated(dfpca_context* ctx, int world, const dfpca_binned* 
   }
   if (first >= 0) throw errs[static_cast<std::size_t>(first)];
   *out = full.release();
+}
+
+void run_covariance_dryrun(dfpca_context* ctx, int world, int rank, const dfpca_binned* b, const Grid& grid,
+                           const double* h, const double* mean_host, dfpca_surface** out) {
+  NullTransport tr(world, rank);
+  run_covariance_sharded(ctx, tr, b, grid, h, mean_host, out);
 }
 
 void nccl_unique_id(void* out) {

@@ -15,6 +15,7 @@
 //            final moments of one chunk, followed by the per-node solve.
 // The mean smoother is the same machinery with every axis a "t-axis".
 #include <algorithm>
+#include <cstring>
 #include <array>
 #include <functional>
 #include <memory>
@@ -888,47 +889,66 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
     shared = some_axis;
   }
   SharedMoments sh{};
-  DevBuf<double> sh_tab;
-  std::vector<double> sh_host;
   if (shared) {
     double sw = 0.0;  // the reference's off-band pw entry: ordered sum of (w_i M0) M0
     for (double w : b->pair_weight_h) sw = sw + (w * b->shared_m0) * b->shared_m0;
     sh.sw = sw;
     sh.dm0 = b->shared_dm0;
+    // The A / D tables depend only on the axis lengths and taps: built once per
+    // context and kept on the device (their host build is O(n^2 R) per axis).
+    std::string key = "shared";
+    for (int k = 0; k < d; ++k) {
+      key += "|" + std::to_string(grid.shape[k]);
+      for (int side : {k, d + k})
+        for (int r = 0; r < 3; ++r)
+          for (double v : taps[side].t[r]) {
+            std::uint64_t bits;
+            std::memcpy(&bits, &v, sizeof(bits));
+            key += ":" + std::to_string(bits);
+          }
+    }
     std::vector<std::size_t> offA(d), offD(d);
+    std::size_t total = 0;
     for (int k = 0; k < d; ++k) {
       const i64 n = grid.shape[k];
-      offA[k] = sh_host.size();
-      sh_host.resize(sh_host.size() + 3 * n, 0.0);
-      offD[k] = sh_host.size();
-      sh_host.resize(sh_host.size() + 9 * n * n, 0.0);
-      const AxisTaps& ts = taps[k];
-      const AxisTaps& tt = taps[d + k];
-      const i64 R = ts.R, Rt = tt.R;
-      for (int r = 0; r < 3; ++r)
-        for (i64 j = 0; j < n; ++j) {
-          double acc = 0.0;
-          for (i64 o = -R; o <= R; ++o)
-            if (j + o >= 0 && j + o < n) acc += ts.t[r][o + R];
-          sh_host[offA[k] + r * n + j] = acc;
-        }
-      for (int a = 0; a < 3; ++a)
-        for (int c = 0; a + c <= 2 && c < 3; ++c)
-          for (i64 x = 0; x < n; ++x)
-            for (i64 y = 0; y < n; ++y) {
-              double acc = 0.0;
-              const i64 lo = std::max<i64>({0, x - R, y - Rt}), hi = std::min<i64>({n - 1, x + R, y + Rt});
-              for (i64 u = lo; u <= hi; ++u) acc += ts.t[a][u - x + R] * tt.t[c][u - y + Rt];
-              sh_host[offD[k] + ((a * 3 + c) * n + x) * n + y] = acc;
-            }
+      offA[k] = total;
+      total += 3 * n;
+      offD[k] = total;
+      total += 9 * n * n;
       sh.n[k] = static_cast<int>(n);
     }
-    sh_tab.alloc(sh_host.size());
-    DFPCA_CUDA(cudaMemcpyAsync(sh_tab.get(), sh_host.data(), sizeof(double) * sh_host.size(),
-                               cudaMemcpyHostToDevice, st));
+    auto& slot = ctx->table_cache[key];
+    if (!slot) {
+      std::vector<double> sh_host(total, 0.0);
+      for (int k = 0; k < d; ++k) {
+        const i64 n = grid.shape[k];
+        const AxisTaps& ts = taps[k];
+        const AxisTaps& tt = taps[d + k];
+        const i64 R = ts.R, Rt = tt.R;
+        for (int r = 0; r < 3; ++r)
+          for (i64 j = 0; j < n; ++j) {
+            double acc = 0.0;
+            for (i64 o = -R; o <= R; ++o)
+              if (j + o >= 0 && j + o < n) acc += ts.t[r][o + R];
+            sh_host[offA[k] + r * n + j] = acc;
+          }
+        for (int a = 0; a < 3; ++a)
+          for (int c = 0; a + c <= 2 && c < 3; ++c)
+            for (i64 x = 0; x < n; ++x)
+              for (i64 y = 0; y < n; ++y) {
+                double acc = 0.0;
+                const i64 lo = std::max<i64>({0, x - R, y - Rt}), hi = std::min<i64>({n - 1, x + R, y + Rt});
+                for (i64 u = lo; u <= hi; ++u) acc += ts.t[a][u - x + R] * tt.t[c][u - y + Rt];
+                sh_host[offD[k] + ((a * 3 + c) * n + x) * n + y] = acc;
+              }
+      }
+      slot = std::make_unique<DevBuf<double>>(total);
+      DFPCA_CUDA(cudaMemcpyAsync(slot->get(), sh_host.data(), sizeof(double) * total, cudaMemcpyHostToDevice, st));
+      DFPCA_CUDA(cudaStreamSynchronize(st));
+    }
     for (int k = 0; k < d; ++k) {
-      sh.A[k] = sh_tab.get() + offA[k];
-      sh.D[k] = sh_tab.get() + offD[k];
+      sh.A[k] = slot->get() + offA[k];
+      sh.D[k] = slot->get() + offD[k];
     }
   }
 

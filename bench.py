@@ -301,13 +301,14 @@ def main():
     # ---- full FPCA pipeline once (host obs -> EigenSystem on host) ----
     fpca_ms = eig_ms = None
     eig_top3 = None
-    if not sharded:
+    # (N > 1: every rank smooths its slab and runs the row-sharded projection)
+    if True:
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         b3 = api.linear_bin(data, grid, api.BinOptions(True, True))
         m3 = api.fft_local_linear(b3, grid, h, api.MomentTarget.Mean)
         api.fft_local_linear(b3, grid, h, api.MomentTarget.Squares)
-        c3 = api.fft_covariance(b3, grid, h, m3)
+        c3 = cov_fn(b3, grid, h, m3)
         eig = api.randomized_eig(api.matrixize(c3), 99, 20, grid, 20260815)
         fpca_ms = (time.perf_counter() - t0) * 1e3
         eig_ms = _lib.stage_ms("eigen")

@@ -167,6 +167,16 @@ DFPCA_API int dfpca_covariance_emulated(dfpca_context* ctx, const dfpca_binned* 
 DFPCA_API int dfpca_covariance_slab_dryrun(dfpca_context* ctx, const dfpca_binned* b, const dfpca_grid* grid,
                                  const double* h, const double* mean, const dfpca_plan* plan, int world,
                                  int rank, dfpca_surface** out);
+/* In-process validation of the whole sharded FPCA core: `world` ranks smooth
+ * their covariance slabs and run the row-sharded randomized eigensolver
+ * (dfpca_randomized_eig on a slab surface of a dfpca_nccl_init context: the
+ * products with Sigma are computed per rank and all-gathered, everything else
+ * is replicated).  Outputs are rank 0's, as dfpca_randomized_eig;
+ * *ranks_agree = 1 when every rank's eigensystem is bit-identical. */
+DFPCA_API int dfpca_fpca_emulated(dfpca_context* ctx, const dfpca_binned* b, const dfpca_grid* grid,
+                        const double* h, const double* mean, int world, int64_t q, int64_t L_max,
+                        uint64_t seed, double* eigenvalues, double* eigenfunctions, double* fve,
+                        double* total_variance, int64_t* n_components, int* ranks_agree);
 /* Rows of the covariance held by a surface (a slab, or 0 / G). */
 DFPCA_API int dfpca_surface_rows(const dfpca_surface* s, int64_t* row0, int64_t* rows);
 /* Host-side slab plan (no device needed): bounds[0..world] are the s1-plane
@@ -192,7 +202,8 @@ DFPCA_API int dfpca_surface_free(dfpca_surface* s);
 
 /* ---- eigendecomposition ------------------------------------------------- */
 /* Replaces dfpca::matrixize + dfpca::randomized_eig (eigensolve.hpp:71-103,
- * 245-279) on a device-resident covariance surface.  Outputs (host):
+ * 245-279) on a device-resident covariance surface (or, on a context joined
+ * by dfpca_nccl_init, this rank's slab: a collective over the ranks).  Outputs (host):
  *   eigenvalues[L_max], eigenfunctions[L_max * G] (full-grid surfaces, NaN at
  *   masked nodes), fve[L_max], *total_variance, *n_components (kept L). */
 DFPCA_API int dfpca_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const dfpca_grid* grid,

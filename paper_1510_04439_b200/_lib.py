@@ -68,6 +68,8 @@ SIGNATURES = [
                                             C.POINTER(P)]),
     ("dfpca_covariance_slab_dryrun", C.c_int, [P, P, C.POINTER(DfpcaGrid), PD, PD, C.POINTER(DfpcaPlan), C.c_int,
                                                C.c_int, C.POINTER(P)]),
+    ("dfpca_fpca_emulated", C.c_int, [P, P, C.POINTER(DfpcaGrid), PD, PD, C.c_int, C.c_int64, C.c_int64, C.c_uint64,
+                                      PD, PD, PD, PD, PI64, C.POINTER(C.c_int)]),
     ("dfpca_surface_rows", C.c_int, [P, PI64, PI64]),
     ("dfpca_shard_bounds", C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int, PI64]),
     ("dfpca_shard_blocks", C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, PI64, C.c_int64, PI64]),

@@ -718,6 +718,32 @@ def covariance_slab_dryrun(binned: BinnedData, grid: EvaluationGrid, h: Bandwidt
     return SurfaceEstimate(grid, SurfaceKind.Covariance, handle=handle)
 
 
+def fpca_emulated(binned: BinnedData, grid: EvaluationGrid, h: Bandwidth, mean: SurfaceEstimate, world: int,
+                  q: int, L_max: int, seed: int):
+    """Sharded covariance + row-sharded randomized eig with `world` in-process
+    ranks on one device (validation).  Returns (EigenSystem of rank 0, whether
+    every rank's eigensystem is bit-identical)."""
+    hh, mv, _, _ = _cov_args(binned, grid, h, mean, None)
+    G = grid.size()
+    ev = np.zeros(max(L_max, 1))
+    ef = np.zeros(max(L_max, 1) * G)
+    fve = np.zeros(max(L_max, 1))
+    total = C.c_double()
+    n = C.c_int64()
+    agree = C.c_int()
+    check(_lib.lib().dfpca_fpca_emulated(_lib.ctx(), binned.handle, C.byref(grid.desc()),
+                                         hh.ctypes.data_as(C.POINTER(C.c_double)),
+                                         mv.ctypes.data_as(C.POINTER(C.c_double)), int(world), q, L_max,
+                                         C.c_uint64(seed & 0xFFFFFFFFFFFFFFFF),
+                                         ev.ctypes.data_as(C.POINTER(C.c_double)),
+                                         ef.ctypes.data_as(C.POINTER(C.c_double)),
+                                         fve.ctypes.data_as(C.POINTER(C.c_double)), C.byref(total), C.byref(n),
+                                         C.byref(agree)))
+    L = n.value
+    return (EigenSystem([float(x) for x in ev[:L]], [ef[l * G:(l + 1) * G].copy() for l in range(L)],
+                        [float(x) for x in fve[:L]], total.value), bool(agree.value))
+
+
 def shard_bounds(n1: int, nodes_per_plane: int, radius: int, world: int) -> list:
     out = (C.c_int64 * (world + 1))()
     check_plain(_lib.lib().dfpca_shard_bounds(n1, nodes_per_plane, radius, world, out))

@@ -31,8 +31,16 @@ void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid,
 namespace dfpca_gpu {
 void run_covariance_sharded(dfpca_context* ctx, Transport& tr, const dfpca_binned* b, const Grid& grid,
                             const double* h, const double* mean_host, dfpca_surface** out);
+struct EigOut {
+  i64 q = 0, L = 0;
+  unsigned long long seed = 0;
+  std::vector<double> values, functions, fve;
+  double total = 0.0;
+  i64 n = 0;
+};
 void run_covariance_emulated(dfpca_context* ctx, int world, const dfpca_binned* b, const Grid& grid,
-                             const double* h, const double* mean_host, dfpca_surface** out);
+                             const double* h, const double* mean_host, dfpca_surface** out,
+                             std::vector<EigOut>* eig);
 void nccl_unique_id(void* out);
 void run_covariance_dryrun(dfpca_context* ctx, int world, int rank, const dfpca_binned* b, const Grid& grid,
                            const double* h, const double* mean_host, dfpca_surface** out);
@@ -605,7 +613,43 @@ int dfpca_covariance_emulated(dfpca_context* ctx, const dfpca_binned* b, const d
   return guarded(ctx, [&] {
     Grid g = validate_covariance(b, grid, h, mean, plan, out);
     if (world < 1) fail(kConfig, "InvalidArgument", "world must be >= 1");
-    run_covariance_emulated(ctx, world, b, g, h, mean, out);
+    run_covariance_emulated(ctx, world, b, g, h, mean, out, nullptr);
+  });
+}
+
+int dfpca_fpca_emulated(dfpca_context* ctx, const dfpca_binned* b, const dfpca_grid* grid, const double* h,
+                        const double* mean, int world, int64_t q, int64_t L_max, uint64_t seed, double* eigenvalues,
+                        double* eigenfunctions, double* fve, double* total_variance, int64_t* n_components,
+                        int* ranks_agree) {
+  return guarded(ctx, [&] {
+    dfpca_surface* cov = nullptr;
+    Grid g = validate_covariance(b, grid, h, mean, nullptr, &cov);
+    if (world < 1) fail(kConfig, "InvalidArgument", "world must be >= 1");
+    if (L_max < 0) fail(kConfig, "InvalidArgument", "L_max must be >= 0");
+    std::vector<EigOut> eig(static_cast<std::size_t>(world));
+    for (auto& e : eig) {
+      e.q = q;
+      e.L = L_max;
+      e.seed = seed;
+    }
+    run_covariance_emulated(ctx, world, b, g, h, mean, &cov, &eig);
+    std::unique_ptr<dfpca_surface> keep(cov);
+    bool agree = true;
+    for (const EigOut& e : eig) {
+      agree = agree && e.n == eig[0].n && e.total == eig[0].total;
+      agree = agree && std::memcmp(e.values.data(), eig[0].values.data(), sizeof(double) * e.values.size()) == 0;
+      agree = agree && std::memcmp(e.functions.data(), eig[0].functions.data(),
+                                   sizeof(double) * e.functions.size()) == 0;
+    }
+    if (ranks_agree) *ranks_agree = agree ? 1 : 0;
+    const EigOut& e0 = eig[0];
+    for (i64 l = 0; l < L_max; ++l) {
+      if (eigenvalues) eigenvalues[l] = e0.values[static_cast<std::size_t>(l)];
+      if (fve) fve[l] = e0.fve[static_cast<std::size_t>(l)];
+    }
+    if (eigenfunctions) std::memcpy(eigenfunctions, e0.functions.data(), sizeof(double) * e0.functions.size());
+    if (total_variance) *total_variance = e0.total;
+    if (n_components) *n_components = e0.n;
   });
 }
 

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "gemm.cuh"
+#include "shard_exec.hpp"
 
 namespace dfpca_gpu {
 namespace {
@@ -466,21 +467,121 @@ static MatrixView matrixize_dev(dfpca_context* ctx, const dfpca_surface* cov, co
   return mv;
 }
 
+// This rank's rows of the in-mask matrix of a row-sharded covariance:
+// sigma_t = (Sigma[own in-mask rows][all in-mask columns])^T, [M][m_loc],
+// and every rank's row count / offset (in-mask rows are in node order, and
+// the slabs are consecutive node ranges).
+struct RowShard {
+  i64 M = 0, m_loc = 0, m_max = 0;
+  std::vector<i64> node_of_row;
+  std::vector<i64> counts, offsets;
+  DevBuf<double> sigma_t;
+};
+
+__global__ void k_gather_rows(const double* __restrict__ slab, i64 G, i64 row0, const i64* __restrict__ rows_nodes,
+                              i64 m_loc, const i64* __restrict__ node_of_row, i64 M, double* __restrict__ out) {
+  const i64 total = m_loc * M;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total; e += (i64)gridDim.x * blockDim.x) {
+    const i64 r = e / M, c = e % M;
+    out[e] = slab[(rows_nodes[r] - row0) * G + node_of_row[c]];
+  }
+}
+
+static RowShard shard_rows_dev(dfpca_context* ctx, Transport& tr, const dfpca_surface* cov, const Grid& grid) {
+  RowShard rs;
+  const i64 G = grid.G;
+  for (i64 f = 0; f < G; ++f)
+    if (!grid.has_mask || grid.mask[f]) rs.node_of_row.push_back(f);
+  rs.M = static_cast<i64>(rs.node_of_row.size());
+  if (rs.M == 0) fail(kConfig, "InvalidArgument", "no in-mask nodes to decompose");
+  const i64 row0 = cov->row0, nrows = cov->rows >= 0 ? cov->rows : G;
+  std::vector<i64> mine;
+  for (i64 r = 0; r < rs.M; ++r) {
+    const i64 f = rs.node_of_row[static_cast<std::size_t>(r)];
+    if (f >= row0 && f < row0 + nrows) mine.push_back(f);
+  }
+  rs.m_loc = static_cast<i64>(mine.size());
+  // every rank's in-mask row count (all-gathered), hence offsets and padding
+  const int W = tr.world();
+  DevBuf<double> cnt(1), cnts(static_cast<std::size_t>(W));
+  const double c = static_cast<double>(rs.m_loc);
+  DFPCA_CUDA(cudaMemcpyAsync(cnt.get(), &c, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  tr.all_gather(ctx, cnt.get(), cnts.get(), 1);
+  std::vector<double> hc(static_cast<std::size_t>(W));
+  DFPCA_CUDA(cudaMemcpyAsync(hc.data(), cnts.get(), sizeof(double) * W, cudaMemcpyDeviceToHost, ctx->stream));
+  DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+  i64 off = 0;
+  for (int r = 0; r < W; ++r) {
+    rs.counts.push_back(static_cast<i64>(hc[static_cast<std::size_t>(r)]));
+    rs.offsets.push_back(off);
+    off += rs.counts.back();
+    rs.m_max = std::max(rs.m_max, rs.counts.back());
+  }
+  if (off != rs.M) fail(kConfig, "InvalidArgument", "covariance slabs do not cover the grid once");
+  if (rs.m_loc > 0) {
+    DevBuf<i64> nodes(static_cast<std::size_t>(rs.m_loc)), nor(static_cast<std::size_t>(rs.M));
+    DFPCA_CUDA(cudaMemcpyAsync(nodes.get(), mine.data(), sizeof(i64) * rs.m_loc, cudaMemcpyHostToDevice,
+                               ctx->stream));
+    DFPCA_CUDA(cudaMemcpyAsync(nor.get(), rs.node_of_row.data(), sizeof(i64) * rs.M, cudaMemcpyHostToDevice,
+                               ctx->stream));
+    DevBuf<double> rows(static_cast<std::size_t>(rs.m_loc * rs.M));
+    DFPCA_LAUNCH(ctx, k_gather_rows, grid_for(rs.m_loc * rs.M, 256), 256, 0, cov->values.get(), G, row0,
+                 nodes.get(), rs.m_loc, nor.get(), rs.M, rows.get());
+    rs.sigma_t.alloc(static_cast<std::size_t>(rs.m_loc * rs.M));
+    transpose(ctx, rows.get(), rs.m_loc, rs.M, rs.sigma_t.get());
+    DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return rs;
+}
+
 void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid& grid, i64 q_req,
                         i64 L_max, unsigned long long seed, double* eigenvalues, double* eigenfunctions,
                         double* fve, double* total_variance, i64* n_components) {
   if (cov->kind != DFPCA_SURFACE_COVARIANCE)
     fail(kConfig, "InvalidArgument", "matrixize expects a covariance surface");
-  if (cov->n != grid.G * grid.G) fail(kConfig, "InvalidArgument", "covariance surface has wrong length");
+  Transport* tr = ctx->transport && ctx->transport->world() > 1 ? ctx->transport.get() : nullptr;
+  const i64 cov_rows = cov->rows >= 0 ? cov->rows : grid.G;
+  if (cov->n != cov_rows * grid.G || (!tr && cov_rows != grid.G))
+    fail(kConfig, "InvalidArgument", "covariance surface has wrong length");
   if (q_req < L_max)
     fail(kConfig, "SketchTooSmall",
          "sketch size " + std::to_string(q_req) + " is below the requested component count " +
              std::to_string(L_max));
   cudaStream_t st = ctx->stream;
   ctx->begin_stage("eigen");
-  MatrixView mv = matrixize_dev(ctx, cov, grid);
+  // One device: the in-mask matrix.  Row-sharded (a slab of a sharded
+  // covariance on every rank): this rank's in-mask rows, transposed into the
+  // K-major operand, and the two products with Sigma are all-gathered.
+  MatrixView mv = tr ? MatrixView{} : matrixize_dev(ctx, cov, grid);
+  RowShard rs;
+  if (tr) {
+    rs = shard_rows_dev(ctx, *tr, cov, grid);
+    mv.M = rs.M;
+    mv.node_of_row = rs.node_of_row;
+  }
   const i64 M = mv.M;
   const i64 q = std::min<i64>(q_req, M);
+  // out[M][q] = Sigma X for X [M][q]: sums split exactly as the one-device
+  // product (same split-K), so every row is bit-identical
+  auto apply_sigma = [&](const double* X, double* out) {
+    if (!tr) {
+      gemm_tn(ctx, M, q, M, mv.sigma, M, nullptr, X, q, out, q, false);
+      return;
+    }
+    DevBuf<double> loc(static_cast<std::size_t>(std::max<i64>(1, rs.m_max * q)));
+    DFPCA_CUDA(cudaMemsetAsync(loc.get(), 0, sizeof(double) * rs.m_max * q, st));
+    if (rs.m_loc > 0)
+      gemm_tn(ctx, rs.m_loc, q, M, rs.sigma_t.get(), rs.m_loc, nullptr, X, q, loc.get(), q, false, 0, -1,
+              gemm_splits(ctx, M, q, M));
+    DevBuf<double> all(static_cast<std::size_t>(tr->world() * std::max<i64>(1, rs.m_max * q)));
+    tr->all_gather(ctx, loc.get(), all.get(), std::max<i64>(1, rs.m_max * q));
+    for (int r = 0; r < tr->world(); ++r)
+      if (rs.counts[static_cast<std::size_t>(r)] > 0)
+        DFPCA_CUDA(cudaMemcpyAsync(out + rs.offsets[static_cast<std::size_t>(r)] * q,
+                                   all.get() + static_cast<i64>(r) * std::max<i64>(1, rs.m_max * q),
+                                   sizeof(double) * rs.counts[static_cast<std::size_t>(r)] * q,
+                                   cudaMemcpyDeviceToDevice, st));
+  };
 
   // Omega
   DevBuf<unsigned long long> words(static_cast<std::size_t>(2 * ((M * q + 1) / 2)));
@@ -493,7 +594,7 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
   // Y = Sigma Omega  ([M][q]); Sigma is exactly symmetric, so Sigma(k, m) is
   // the K-major operand.
   DevBuf<double> Y(static_cast<std::size_t>(M * q)), Yt(static_cast<std::size_t>(M * q));
-  gemm_tn(ctx, M, q, M, mv.sigma, M, nullptr, omega.get(), q, Y.get(), q, false);
+  apply_sigma(omega.get(), Y.get());
   transpose(ctx, Y.get(), M, q, Yt.get());
 
   // Householder QR and thin Q
@@ -511,7 +612,7 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
 
   // small = Q^T (Sigma Q)
   DevBuf<double> Z(static_cast<std::size_t>(M * q));
-  gemm_tn(ctx, M, q, M, mv.sigma, M, nullptr, Q.get(), q, Z.get(), q, false);
+  apply_sigma(Q.get(), Z.get());
   DevBuf<double> small(static_cast<std::size_t>(q * q)), Vs(static_cast<std::size_t>(q * q));
   gemm_tn(ctx, q, q, M, Q.get(), q, nullptr, Z.get(), q, small.get(), q, false);
 

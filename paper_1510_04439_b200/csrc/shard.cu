@@ -71,23 +71,6 @@ __global__ void k_unpack_block(const double* __restrict__ in, double* __restrict
 }
 
 // --------------------------------------------------------------- transports --
-class Transport {
- public:
-  struct Msg {
-    int peer;
-    double* buf;
-    i64 count;
-  };
-  virtual ~Transport() = default;
-  virtual int rank() const = 0;
-  virtual int world() const = 0;
-  // all sends and receives of one phase, queued on ctx->stream
-  virtual void exchange(dfpca_context* ctx, const std::vector<Msg>& sends, const std::vector<Msg>& recvs) = 0;
-  virtual unsigned long long max_u64(dfpca_context* ctx, unsigned long long v) = 0;
-  // recv[r * count ..] = rank r's send, for every rank
-  virtual void all_gather(dfpca_context* ctx, const double* send, double* recv, i64 count) = 0;
-};
-
 namespace {
 
 // ---- NCCL, loaded at run time ----
@@ -438,10 +421,28 @@ void run_covariance_sharded(dfpca_context* ctx, Transport& tr, const dfpca_binne
   run_covariance_impl(ctx, b, grid, h, mean_host, &ex, out);
 }
 
+}  // namespace dfpca_gpu
+namespace dfpca_gpu {
+void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid& grid, i64 q, i64 L_max,
+                        unsigned long long seed, double* eigenvalues, double* eigenfunctions, double* fve,
+                        double* total_variance, i64* n_components);
+
+// Eigen outputs of one in-process rank.
+struct EigOut {
+  i64 q = 0, L = 0;
+  unsigned long long seed = 0;
+  std::vector<double> values, functions, fve;
+  double total = 0.0;
+  i64 n = 0;
+};
+
 // `world` in-process ranks on ctx's device; the slabs are assembled into one
-// G x G surface on ctx (validation of the decomposition).
+// G x G surface on ctx (validation of the decomposition).  With `eig`, every
+// rank then runs the row-sharded randomized eigensolver on its slab and
+// eig[r] receives rank r's (replicated) eigensystem.
 void run_covariance_emulated(dfpca_context* ctx, int world, const dfpca_binned* b, const Grid& grid,
-                             const double* h, const double* mean_host, dfpca_surface** out) {
+                             const double* h, const double* mean_host, dfpca_surface** out,
+                             std::vector<EigOut>* eig) {
   LocalHub hub(world);
   std::vector<dfpca_surface*> slabs(static_cast<std::size_t>(world), nullptr);
   std::vector<dfpca_context*> rctx(static_cast<std::size_t>(world), nullptr);
@@ -457,8 +458,17 @@ void run_covariance_emulated(dfpca_context* ctx, int world, const dfpca_binned* 
         rctx[static_cast<std::size_t>(r)] = c;
         DFPCA_CUDA(cudaSetDevice(ctx->device));
         g_alloc_stream = c->stream;
-        LocalTransport tr(&hub, r);
-        run_covariance_sharded(c, tr, b, grid, h, mean_host, &slabs[static_cast<std::size_t>(r)]);
+        auto tr = std::make_shared<LocalTransport>(&hub, r);
+        c->transport = tr;
+        run_covariance_sharded(c, *tr, b, grid, h, mean_host, &slabs[static_cast<std::size_t>(r)]);
+        if (eig) {
+          EigOut& e = (*eig)[static_cast<std::size_t>(r)];
+          e.values.assign(static_cast<std::size_t>(e.L), 0.0);
+          e.fve.assign(static_cast<std::size_t>(e.L), 0.0);
+          e.functions.assign(static_cast<std::size_t>(e.L * grid.G), 0.0);
+          run_randomized_eig(c, slabs[static_cast<std::size_t>(r)], grid, e.q, e.L, e.seed, e.values.data(),
+                             e.functions.data(), e.fve.data(), &e.total, &e.n);
+        }
         DFPCA_CUDA(cudaStreamSynchronize(c->stream));
         c->collect_stages();
       } catch (const Failure& e) {

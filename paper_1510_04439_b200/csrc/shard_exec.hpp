@@ -5,11 +5,30 @@
 #pragma once
 
 #include <functional>
+#include <vector>
 
 #include "internal.hpp"
 #include "shard.hpp"
 
 namespace dfpca_gpu {
+
+// Rank-to-rank transport of a sharded run (shard.cu: NCCL or in-process).
+class Transport {
+ public:
+  struct Msg {
+    int peer;
+    double* buf;
+    i64 count;
+  };
+  virtual ~Transport() = default;
+  virtual int rank() const = 0;
+  virtual int world() const = 0;
+  // all sends and receives of one phase, queued on ctx->stream
+  virtual void exchange(dfpca_context* ctx, const std::vector<Msg>& sends, const std::vector<Msg>& recvs) = 0;
+  virtual unsigned long long max_u64(dfpca_context* ctx, unsigned long long v) = 0;
+  // recv[r * count ..] = rank r's send, for every rank
+  virtual void all_gather(dfpca_context* ctx, const double* send, double* recv, i64 count) = 0;
+};
 
 struct CovShardExec {
   const ShardPlan* plan = nullptr;

@@ -100,3 +100,22 @@ def test_single_rank_sharded_entry_is_the_plain_covariance(api):
     s = api.fft_covariance_sharded(b, grid, h, mean)  # no communicator: one rank
     assert s.rows() == (0, grid.size())
     assert bit_equal(s.values, one)
+
+
+@pytest.mark.parametrize("case,world", [("2d_nodes", 3), ("2d_masked_sparse", 4), ("3d_nodes", 2),
+                                        ("1d_random", 4)])
+def test_sharded_randomized_eig_bit_identical(api, case, world):
+    """Row-sharded projection (per-rank products with Sigma, all-gathered;
+    QR, Rayleigh-Ritz and finalization replicated): every rank returns the
+    one-device eigensystem bit for bit."""
+    from paper_1510_04439_b200 import synth
+    sd = CASES[case](synth)
+    grid, b, h, mean = _setup(api, sd)
+    M = grid.size() if sd.mask is None else int(np.count_nonzero(sd.mask))
+    q, L = min(40, M), 5
+    one = api.randomized_eig(api.matrixize(api.fft_covariance(b, grid, h, mean)), q, L, grid, 20260815)
+    many, agree = api.fpca_emulated(b, grid, h, mean, world, q, L, 20260815)
+    assert agree
+    assert bit_equal(many.eigenvalues, one.eigenvalues)
+    assert bit_equal(np.concatenate(many.eigenfunctions), np.concatenate(one.eigenfunctions))
+    assert many.fve == one.fve and many.total_variance == one.total_variance

@@ -296,6 +296,34 @@ int main() {
     CHECK(S.dense_matrix(0, 1) == 3.0 && S.dense_matrix(1, 1) == 9.0);
   });
 
+  run("sharded entry points on a single rank (multi-GPU extension, sharded.hpp)", [] {
+    // without init_distributed the sharded calls are the one-GPU calls
+    auto grid = EvaluationGrid::midpoint({0.0, 0.0}, {1.0, 1.0}, {16, 16});
+    FunctionalDataset data;
+    for (int i = 0; i < 12; ++i) {
+      Sample smp;
+      smp.id = "s" + std::to_string(i);
+      std::vector<double> x;
+      for (Index f = 0; f < grid.size(); ++f) {
+        grid.node_coords(f, x);
+        smp.coords.insert(smp.coords.end(), x.begin(), x.end());
+        smp.values.push_back(std::sin(3.0 * x[0] + i) * std::cos(2.0 * x[1] - 0.5 * i));
+      }
+      data.samples.push_back(smp);
+    }
+    data.dim = 2;
+    auto b = linear_bin(data, grid, {true, true});
+    const Bandwidth h{{0.2, 0.2}};
+    auto mean = fft_local_linear(b, grid, h, MomentTarget::Mean);
+    auto cov = fft_covariance(b, grid, h, mean);
+    auto slab = gpu::fft_covariance_sharded(b, grid, h, mean);
+    CHECK(slab.row0 == 0 && slab.rows == grid.size());
+    CHECK(slab.values == cov.values);
+    auto e1 = randomized_eig(matrixize(cov), 20, 3, grid, 7);
+    auto e2 = gpu::randomized_eig_sharded(slab, 20, 3, grid, 7);
+    CHECK(e1.eigenvalues == e2.eigenvalues && e1.eigenfunctions == e2.eigenfunctions);
+  });
+
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }

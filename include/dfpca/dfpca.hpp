@@ -12,4 +12,5 @@
 #include "dfpca/kernel.hpp"
 #include "dfpca/parallel.hpp"
 #include "dfpca/rng.hpp"
+#include "dfpca/sharded.hpp"
 #include "dfpca/surface.hpp"

@@ -296,6 +296,93 @@ int main() {
     CHECK(S.dense_matrix(0, 1) == 3.0 && S.dense_matrix(1, 1) == 9.0);
   });
 
+  // ---- scores.hpp (reference tests/test_scores.cpp) ----
+  run("noise variance pooling (test_scores.cpp:93-148)", [] {
+    EvaluationGrid grid = EvaluationGrid::midpoint({0.0}, {1.0}, {50});
+    const auto g = static_cast<std::size_t>(grid.size());
+    const double pi = std::acos(-1.0);
+    std::vector<double> mu(g), q(g), coord;
+    for (std::size_t f = 0; f < g; ++f) {
+      grid.node_coords(static_cast<Index>(f), coord);
+      mu[f] = 1.0 + coord[0];
+      q[f] = std::sqrt(0.5 + 0.1 * std::sin(2.0 * pi * coord[0]));
+    }
+    SurfaceEstimate mean{grid, mu, SurfaceKind::Mean, nullptr};
+    SurfaceEstimate cov;
+    cov.grid = grid;
+    cov.kind = SurfaceKind::Covariance;
+    cov.values.resize(g * g);
+    for (std::size_t a = 0; a < g; ++a)
+      for (std::size_t c = 0; c < g; ++c) cov.values[a * g + c] = q[a] * q[c];
+    SurfaceEstimate diag;
+    diag.grid = grid;
+    diag.kind = SurfaceKind::DiagPlusNoise;
+    diag.values.resize(g);
+    for (std::size_t f = 0; f < g; ++f) diag.values[f] = q[f] * q[f] + mu[f] * mu[f] + 0.25;
+    CHECK(near(estimate_sigma2(diag, cov, mean), 0.25, 1e-12));
+    for (std::size_t f = 0; f < g; ++f) diag.values[f] = q[f] * q[f] + mu[f] * mu[f] - 0.5;
+    CHECK(estimate_sigma2(diag, cov, mean) == 0.0);
+    CHECK(error_name([&] { estimate_sigma2(mean, cov, mean); }) == "InvalidArgument");
+  });
+
+  run("conditional-expectation scores (test_scores.cpp:150-205)", [] {
+    EvaluationGrid grid = EvaluationGrid::uniform({0.0}, {1.0}, {11});
+    FpcaModel model;
+    model.mean.grid = grid;
+    model.mean.kind = SurfaceKind::Mean;
+    std::vector<double> coord;
+    for (Index f = 0; f < grid.size(); ++f) {
+      grid.node_coords(f, coord);
+      model.mean.values.push_back(coord[0]);
+    }
+    const double cv = grid.cell_volume();
+    model.eig.eigenvalues = {2.0};
+    model.eig.eigenfunctions = {std::vector<double>(11, 1.0 / std::sqrt(11.0 * cv))};
+    model.sigma2 = 0.5;
+    Sample s;
+    s.coords = {0.37};
+    s.values = {1.9};
+    const double mu_hat = interp_multilinear(grid, model.mean.values, s.coords.data());
+    const double phi_hat = interp_multilinear(grid, model.eig.eigenfunctions[0], s.coords.data());
+    const double expected = 2.0 * phi_hat * (1.9 - mu_hat) / (2.0 * phi_hat * phi_hat + 0.5);
+    const auto a = pace_scores(s, model);
+    CHECK(a.size() == 1 && near(a[0], expected, 1e-12));
+    Sample on_mean, s1, s2;
+    for (double t : {0.05, 0.33, 0.61, 0.98}) {
+      on_mean.coords.push_back(t);
+      on_mean.values.push_back(interp_multilinear(grid, model.mean.values, &t));
+    }
+    for (double v : pace_scores(on_mean, model)) CHECK(std::abs(v) < 1e-12);
+    for (double t : {0.1, 0.4, 0.75}) {
+      const double m = interp_multilinear(grid, model.mean.values, &t);
+      s1.coords.push_back(t);
+      s1.values.push_back(m + (t - 0.3));
+      s2.coords.push_back(t);
+      s2.values.push_back(m + 2.5 * (t - 0.3));
+    }
+    CHECK(near(pace_scores(s2, model)[0], 2.5 * pace_scores(s1, model)[0], 1e-12));
+    Sample out;
+    out.coords = {1.5};
+    out.values = {0.0};
+    CHECK(error_name([&] { pace_scores(out, model); }) == "OutOfDomain");
+    CHECK(error_name([&] { integration_scores(out, model); }) == "OutOfDomain");
+    // integration on a dense on-node sample is the Riemann projection
+    Sample dense;
+    for (Index f = 0; f < grid.size(); ++f) {
+      grid.node_coords(f, coord);
+      dense.coords.push_back(coord[0]);
+      dense.values.push_back(model.mean.values[static_cast<std::size_t>(f)] + 3.0 * model.eig.eigenfunctions[0][static_cast<std::size_t>(f)]);
+    }
+    bool warned = true;
+    const auto proj = integration_scores(dense, model, &warned);
+    CHECK(!warned && near(proj[0], 3.0, 1e-12));
+    model.scores = {proj};
+    const auto rec = reconstruct_on_grid(model, 0);
+    for (std::size_t f = 0; f < rec.size(); ++f) CHECK(near(rec[f], dense.values[f], 1e-12));
+    CHECK(near(reconstruct_at(model, 0, dense.coords.data() + 3), dense.values[3], 1e-12));
+    CHECK(error_name([&] { reconstruct_on_grid(model, 7); }) == "InvalidArgument");
+  });
+
   run("sharded entry points on a single rank (multi-GPU extension, sharded.hpp)", [] {
     // without init_distributed the sharded calls are the one-GPU calls
     auto grid = EvaluationGrid::midpoint({0.0, 0.0}, {1.0, 1.0}, {16, 16});

@@ -12,5 +12,6 @@
 #include "dfpca/kernel.hpp"
 #include "dfpca/parallel.hpp"
 #include "dfpca/rng.hpp"
+#include "dfpca/scores.hpp"
 #include "dfpca/sharded.hpp"
 #include "dfpca/surface.hpp"

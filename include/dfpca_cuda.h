@@ -216,6 +216,28 @@ DFPCA_API int dfpca_eig_residuals(dfpca_context* ctx, const dfpca_surface* cov, 
                         int64_t L, const double* eigenvalues, const double* eigenfunctions,
                         double* residuals);
 
+/* ---- noise variance, scores, reconstruction ------- */
+/* Replaces dfpca::estimate_sigma2 (scores.hpp:82-108): diag_plus_noise and
+ * mean are G host doubles, cov the device-resident covariance (a slab on a
+ * dfpca_nccl_init context: a collective).  Bit-identical to the reference. */
+DFPCA_API int dfpca_estimate_sigma2(dfpca_context* ctx, const dfpca_grid* grid, const double* diag_plus_noise,
+                          const dfpca_surface* cov, const double* mean, double* sigma2);
+/* Replaces dfpca::compute_scores (scores.hpp:272-277) for a batch of samples
+ * given in CSR form (as dfpca_linear_bin).  method 0 = pace_scores
+ * (scores.hpp:157-194, up to 160 observations per sample), 1 =
+ * integration_scores (scores.hpp:204-262, bit-identical).  mean: G;
+ * eigenvalues: L; eigenfunctions: L*G; scores: n*L out; sparse_warning: n out
+ * (integration only; may be NULL).  Errors: OutOfDomain, SingularCovariance
+ * (dfpca_last_error_location gives the sample). */
+DFPCA_API int dfpca_scores(dfpca_context* ctx, const dfpca_grid* grid, int64_t n_samples, const int64_t* obs_offsets,
+                 const double* coords, const double* values, const double* mean, int64_t L,
+                 const double* eigenvalues, const double* eigenfunctions, double sigma2, int method,
+                 double* scores, int32_t* sparse_warning);
+/* Replaces dfpca::reconstruct_on_grid (scores.hpp:280-300) for n score rows
+ * (n*L); out: n*G (NaN outside). */
+DFPCA_API int dfpca_reconstruct(dfpca_context* ctx, const dfpca_grid* grid, const double* mean, int64_t L,
+                      const double* eigenfunctions, int64_t n, const double* scores, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -40,6 +40,10 @@ _SIG = {
     "ref_eig_residuals": (C.c_int, [C.c_int, PI, PD, PU8, PD, C.c_int64, PD, PD, PD]),
     "ref_estimate_mean": (C.c_int, [C.c_int, PI, PD, PU8, C.c_int64, PI, PD, PD, PD, C.c_int, PD]),
     "ref_estimate_covariance": (C.c_int, [C.c_int, PI, PD, PU8, C.c_int64, PI, PD, PD, PD, PD, PD]),
+    "ref_estimate_sigma2": (C.c_int, [C.c_int, PI, PD, PU8, PD, PD, PD, PD]),
+    "ref_scores": (C.c_int, [C.c_int, PI, PD, PU8, C.c_int64, PI, PD, PD, PD, C.c_int64, PD, PD, C.c_double,
+                             C.c_int, PD, C.POINTER(C.c_int)]),
+    "ref_reconstruct": (C.c_int, [C.c_int, PI, PD, PU8, PD, C.c_int64, PD, PD, PD, PD]),
 }
 
 _lib = None
@@ -261,4 +265,48 @@ def estimate_covariance(grid, offsets, coords, values, h, mean) -> np.ndarray:
     out = np.empty(ga.G * ga.G)
     _chk(lib().ref_estimate_covariance(*ga.args(), off.size - 1, off.ctypes.data_as(PI), cp, vp, hp, mp,
                                        out.ctypes.data_as(PD)))
+    return out
+
+
+# ---- scores.hpp ------------------------------------------
+
+def estimate_sigma2(grid, diag, cov, mean) -> float:
+    """scores.hpp:82-108."""
+    ga = grid_args(grid)
+    a, ap = _d(diag)
+    b, bp = _d(cov)
+    c, cp = _d(mean)
+    out = C.c_double()
+    _chk(lib().ref_estimate_sigma2(*ga.args(), ap, bp, cp, C.byref(out)))
+    return out.value
+
+
+def scores(grid, offsets, coords, values, mean, evals, efuncs, sigma2, method: int):
+    """compute_scores (scores.hpp:272-277) for every sample; method 0 = pace,
+    1 = integration.  Returns (scores [n, L], sparse-warning flags [n])."""
+    ga = grid_args(grid)
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    n = off.size - 1
+    c, cp = _d(coords)
+    v, vp = _d(values)
+    mu, mp = _d(mean)
+    ev, evp = _d(evals)
+    ef, efp = _d(np.ravel(efuncs))
+    L = ev.size
+    out = np.zeros(max(n * L, 1))
+    sp = np.zeros(max(n, 1), dtype=np.int32)
+    _chk(lib().ref_scores(*ga.args(), n, off.ctypes.data_as(PI), cp, vp, mp, L, evp, efp, float(sigma2),
+                          int(method), out.ctypes.data_as(PD), sp.ctypes.data_as(C.POINTER(C.c_int))))
+    return out[:n * L].reshape(n, L), sp[:n].astype(bool)
+
+
+def reconstruct_on_grid(grid, mean, evals, efuncs, sc) -> np.ndarray:
+    """scores.hpp:280-300."""
+    ga = grid_args(grid)
+    mu, mp = _d(mean)
+    ev, evp = _d(evals)
+    ef, efp = _d(np.ravel(efuncs))
+    s, spp = _d(sc)
+    out = np.empty(ga.G)
+    _chk(lib().ref_reconstruct(*ga.args(), mp, ev.size, evp, efp, spp, out.ctypes.data_as(PD)))
     return out

@@ -18,6 +18,7 @@
 #include "dfpca/fft_smoother.hpp"
 #include "dfpca/grid.hpp"
 #include "dfpca/parallel.hpp"
+#include "dfpca/scores.hpp"
 #include "dfpca/smoother.hpp"
 
 using namespace dfpca;
@@ -292,6 +293,63 @@ int ref_estimate_covariance(int dim, const int64_t* shape, const double* axes, c
     mu.values.assign(mean, mean + g.size());
     auto est = estimate_covariance(data, g, hb, mu);
     std::memcpy(out, est.values.data(), sizeof(double) * est.values.size());
+  });
+}
+
+// ---- noise variance, scores, reconstruction (scores.hpp) ----
+
+static FpcaModel make_model(int dim, const int64_t* shape, const double* axes, const uint8_t* mask,
+                            const double* mean, int64_t L, const double* evals, const double* efuncs,
+                            double sigma2) {
+  FpcaModel m;
+  m.mean.grid = make_grid(dim, shape, axes, mask);
+  m.mean.kind = SurfaceKind::Mean;
+  const auto G = static_cast<std::size_t>(m.mean.grid.size());
+  m.mean.values.assign(mean, mean + G);
+  for (int64_t l = 0; l < L; ++l) {
+    m.eig.eigenvalues.push_back(evals[l]);
+    m.eig.eigenfunctions.emplace_back(efuncs + l * G, efuncs + (l + 1) * G);
+  }
+  m.sigma2 = sigma2;
+  return m;
+}
+
+int ref_estimate_sigma2(int dim, const int64_t* shape, const double* axes, const uint8_t* mask,
+                        const double* diag, const double* cov, const double* mean, double* out) {
+  return guarded([&] {
+    EvaluationGrid g = make_grid(dim, shape, axes, mask);
+    const auto G = static_cast<std::size_t>(g.size());
+    SurfaceEstimate dn{g, std::vector<double>(diag, diag + G), SurfaceKind::DiagPlusNoise};
+    SurfaceEstimate cv{g, std::vector<double>(cov, cov + G * G), SurfaceKind::Covariance};
+    SurfaceEstimate mu{g, std::vector<double>(mean, mean + G), SurfaceKind::Mean};
+    *out = estimate_sigma2(dn, cv, mu);
+  });
+}
+
+// method 0 = pace, 1 = integration; scores[n][L]; sparse[n] (integration only)
+int ref_scores(int dim, const int64_t* shape, const double* axes, const uint8_t* mask, int64_t n,
+               const int64_t* offsets, const double* coords, const double* values, const double* mean,
+               int64_t L, const double* evals, const double* efuncs, double sigma2, int method, double* scores,
+               int* sparse) {
+  return guarded([&] {
+    FpcaModel m = make_model(dim, shape, axes, mask, mean, L, evals, efuncs, sigma2);
+    FunctionalDataset data = make_data(dim, n, offsets, coords, values);
+    for (int64_t i = 0; i < n; ++i) {
+      bool w = false;
+      const auto sc = compute_scores(data.samples[static_cast<std::size_t>(i)], m,
+                                     method == 0 ? ScoreMethod::Pace : ScoreMethod::Integration, &w);
+      for (int64_t l = 0; l < L; ++l) scores[i * L + l] = sc[static_cast<std::size_t>(l)];
+      if (sparse) sparse[i] = w ? 1 : 0;
+    }
+  });
+}
+
+int ref_reconstruct(int dim, const int64_t* shape, const double* axes, const uint8_t* mask, const double* mean,
+                    int64_t L, const double* evals, const double* efuncs, const double* sc, double* out) {
+  return guarded([&] {
+    FpcaModel m = make_model(dim, shape, axes, mask, mean, L, evals, efuncs, 0.0);
+    const auto r = reconstruct_on_grid(m, std::vector<double>(sc, sc + L));
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
   });
 }
 

@@ -879,3 +879,73 @@ def eig_residuals(S: MatrixizedCovariance, eig: EigenSystem, grid: EvaluationGri
                                          ef.ctypes.data_as(C.POINTER(C.c_double)),
                                          out.ctypes.data_as(C.POINTER(C.c_double))))
     return [float(x) for x in out]
+
+
+# ------------------------------------------ noise variance, scores (8(f)) ----
+# reference scores.hpp: estimate_sigma2, pace_scores / integration_scores,
+# reconstruct_on_grid -- batched over samples on the device.
+
+
+class ScoreMethod(Enum):
+    """scores.hpp:22"""
+    Pace = 0
+    Integration = 1
+
+
+def estimate_sigma2(diag_plus_noise: SurfaceEstimate, cov: SurfaceEstimate, mean: SurfaceEstimate) -> float:
+    """scores.hpp:82-108 (bit-identical)."""
+    if (diag_plus_noise.kind != SurfaceKind.DiagPlusNoise or cov.kind != SurfaceKind.Covariance
+            or mean.kind != SurfaceKind.Mean):
+        raise Error(ErrorClass.Config, "InvalidArgument", "estimate_sigma2 got surfaces of the wrong kind")
+    grid = mean.grid
+    dv = np.ascontiguousarray(diag_plus_noise.values, dtype=np.float64)
+    mv = np.ascontiguousarray(mean.values, dtype=np.float64)
+    out = C.c_double()
+    check(_lib.lib().dfpca_estimate_sigma2(_lib.ctx(), C.byref(grid.desc()), dv.ctypes.data_as(C.POINTER(C.c_double)),
+                                           cov.device_handle(), mv.ctypes.data_as(C.POINTER(C.c_double)),
+                                           C.byref(out)))
+    return out.value
+
+
+def compute_scores_batch(data: FunctionalDataset, grid: EvaluationGrid, mean: SurfaceEstimate, eig: EigenSystem,
+                         sigma2: float, method: ScoreMethod):
+    """compute_scores (scores.hpp:272-277) for every sample at once.
+    Returns (scores [n, L], sparse-warning flags [n])."""
+    offsets, coords, values = data.csr()
+    n = len(data.samples)
+    L = len(eig.eigenvalues)
+    mv = np.ascontiguousarray(mean.values, dtype=np.float64)
+    ev = np.ascontiguousarray(eig.eigenvalues, dtype=np.float64)
+    ef = (np.ascontiguousarray(np.concatenate(eig.eigenfunctions), dtype=np.float64) if L
+          else np.zeros(1))
+    out = np.zeros(max(n * L, 1))
+    warn = np.zeros(max(n, 1), dtype=np.int32)
+    PDd = C.POINTER(C.c_double)
+    status = _lib.lib().dfpca_scores(_lib.ctx(), C.byref(grid.desc()), n, offsets.ctypes.data_as(C.POINTER(C.c_int64)),
+                                     coords.ctypes.data_as(PDd) if coords.size else None,
+                                     values.ctypes.data_as(PDd) if values.size else None,
+                                     mv.ctypes.data_as(PDd), L, ev.ctypes.data_as(PDd), ef.ctypes.data_as(PDd),
+                                     float(sigma2), method.value, out.ctypes.data_as(PDd),
+                                     warn.ctypes.data_as(C.POINTER(C.c_int32)))
+    if status != 0:
+        raise _lib.last_error()
+    return out[:n * L].reshape(n, L), warn[:n].astype(bool)
+
+
+def reconstruct_on_grid(mean: SurfaceEstimate, eig: EigenSystem, scores) -> np.ndarray:
+    """scores.hpp:280-300 for one score vector or a [n, L] table."""
+    grid = mean.grid
+    s = np.ascontiguousarray(scores, dtype=np.float64)
+    one = s.ndim == 1
+    s = s.reshape(1, -1) if one else s
+    L = len(eig.eigenvalues)
+    if s.shape[1] != L:
+        raise Error(ErrorClass.Config, "InvalidArgument", "score vector length differs from component count")
+    mv = np.ascontiguousarray(mean.values, dtype=np.float64)
+    ef = np.ascontiguousarray(np.concatenate(eig.eigenfunctions), dtype=np.float64) if L else np.zeros(1)
+    out = np.empty(s.shape[0] * grid.size())
+    PDd = C.POINTER(C.c_double)
+    check(_lib.lib().dfpca_reconstruct(_lib.ctx(), C.byref(grid.desc()), mv.ctypes.data_as(PDd), L,
+                                       ef.ctypes.data_as(PDd), s.shape[0], s.ctypes.data_as(PDd),
+                                       out.ctypes.data_as(PDd)))
+    return out if one else out.reshape(s.shape[0], grid.size())

@@ -45,6 +45,14 @@ void nccl_unique_id(void* out);
 void run_covariance_dryrun(dfpca_context* ctx, int world, int rank, const dfpca_binned* b, const Grid& grid,
                            const double* h, const double* mean_host, dfpca_surface** out);
 std::shared_ptr<Transport> make_nccl_transport(int world, int rank, const void* id);
+void run_estimate_sigma2(dfpca_context* ctx, const Grid& grid, const double* diag_plus_noise,
+                         const dfpca_surface* cov, const double* mean, double* sigma2);
+void run_scores(dfpca_context* ctx, const Grid& grid, i64 n, const i64* offsets, const double* coords,
+                const double* values, const double* mean, i64 L, const double* eigenvalues,
+                const double* eigenfunctions, double sigma2, int method, double* scores, int* sparse_warning,
+                i64* bad_sample);
+void run_reconstruct(dfpca_context* ctx, const Grid& grid, const double* mean, i64 L, const double* eigenfunctions,
+                     i64 n, const double* scores, double* out);
 void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid& grid, i64 q,
                         i64 L_max, unsigned long long seed, double* eigenvalues, double* eigenfunctions,
                         double* fve, double* total_variance, i64* n_components);
@@ -660,6 +668,50 @@ int dfpca_covariance_slab_dryrun(dfpca_context* ctx, const dfpca_binned* b, cons
     Grid g = validate_covariance(b, grid, h, mean, plan, out);
     if (world < 1 || rank < 0 || rank >= world) fail(kConfig, "InvalidArgument", "bad rank / world");
     run_covariance_dryrun(ctx, world, rank, b, g, h, mean, out);
+  });
+}
+
+int dfpca_estimate_sigma2(dfpca_context* ctx, const dfpca_grid* grid, const double* diag_plus_noise,
+                          const dfpca_surface* cov, const double* mean, double* sigma2) {
+  return guarded(ctx, [&] {
+    if (!diag_plus_noise || !cov || !mean || !sigma2)
+      fail(kConfig, "InvalidArgument", "estimate_sigma2 got surfaces of the wrong kind");
+    Grid g = make_grid(grid);
+    run_estimate_sigma2(ctx, g, diag_plus_noise, cov, mean, sigma2);
+  });
+}
+
+int dfpca_scores(dfpca_context* ctx, const dfpca_grid* grid, int64_t n_samples, const int64_t* obs_offsets,
+                 const double* coords, const double* values, const double* mean, int64_t L,
+                 const double* eigenvalues, const double* eigenfunctions, double sigma2, int method, double* scores,
+                 int32_t* sparse_warning) {
+  return guarded(ctx, [&] {
+    Grid g = make_grid(grid);
+    if (n_samples < 0 || !obs_offsets || L < 0 || (method != 0 && method != 1) || (n_samples > 0 && L > 0 && !scores))
+      fail(kConfig, "InvalidArgument", "invalid score request");
+    if (!mean || (L > 0 && (!eigenvalues || !eigenfunctions)))
+      fail(kConfig, "InvalidArgument", "score request lacks the model surfaces");
+    for (i64 i = 0; i < n_samples; ++i)
+      if (obs_offsets[i + 1] < obs_offsets[i] || obs_offsets[0] != 0)
+        fail(kConfig, "InvalidArgument", "observation offsets must be nondecreasing from 0");
+    i64 bad = -1;
+    try {
+      run_scores(ctx, g, n_samples, obs_offsets, coords, values, mean, L, eigenvalues, eigenfunctions, sigma2,
+                 method, scores, sparse_warning, &bad);
+    } catch (Failure& f) {
+      f.sample = bad;
+      throw;
+    }
+  });
+}
+
+int dfpca_reconstruct(dfpca_context* ctx, const dfpca_grid* grid, const double* mean, int64_t L,
+                      const double* eigenfunctions, int64_t n, const double* scores, double* out) {
+  return guarded(ctx, [&] {
+    Grid g = make_grid(grid);
+    if (!mean || L < 0 || n < 0 || (L > 0 && (!eigenfunctions || (n > 0 && !scores))) || (n > 0 && !out))
+      fail(kConfig, "InvalidArgument", "invalid reconstruction request");
+    run_reconstruct(ctx, g, mean, L, eigenfunctions, n, scores, out);
   });
 }
 

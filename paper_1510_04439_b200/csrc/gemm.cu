@@ -5,10 +5,13 @@
 // rate as well, tools/fp64_peak.cu), and it moves 4x fewer operand bytes per
 // FMA through registers than DFMA, which is what lets a tile reach that peak.
 //
-// CTA tile 128 x 128, 16 warps each owning a 32 x 32 block (4 x 4 DMMA tiles),
-// so 4 warps per scheduler hide the fragment-load latency.  K is staged 16 at
+// CTA tile 64 x 64, 4 warps each owning a 32 x 32 block (4 x 4 DMMA tiles),
+// 4 CTAs per SM so 4 warps per scheduler hide the fragment-load latency; the
+// small tile keeps the last wave short (G = 4096: 2080 upper tiles, 94% of the
+// final wave busy vs 89% with 128 x 128) and gives a thin slab of a sharded
+// pair grid enough tiles to fill the SMs.  K is staged 16 at
 // a time through a 3-deep cp.async (LDGSTS) ring in shared memory, rows padded
-// to 132 doubles so one warp's k-strided fragment loads spread over all banks.
+// by 4 doubles so one warp's k-strided fragment loads spread over all banks.
 // Per-row weights (the pair weights of the SYRK) are applied by a separate
 // scaling pass so the operand copies stay asynchronous.
 #include <algorithm>
@@ -19,11 +22,13 @@
 namespace dfpca_gpu {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16;
-constexpr int LDS = 132;
+constexpr int BM = 64, BN = 64, BK = 16;
+constexpr int LDS = BM + 4;
 constexpr int WM = 32, WN = 32;
 constexpr int MT = WM / 8, NT = WN / 8;
-constexpr int NTHREADS = 512;
+constexpr int WARPS_N = BN / WN;
+constexpr int NTHREADS = 32 * (BM / WM) * WARPS_N;
+constexpr int CTAS_PER_SM = 4;
 constexpr int STAGES = 3;
 constexpr int STAGE_DOUBLES = 2 * BK * LDS;  // A and B tiles
 
@@ -49,7 +54,7 @@ __device__ inline void cp_async_wait() {
 
 // VEC: doubles per cp.async (2 when every row start is 16-byte aligned).
 template <int VEC>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
     k_gemm_tn(i64 M, i64 N, i64 K, const double* __restrict__ A, i64 lda, const double* __restrict__ B,
               i64 ldb, double* __restrict__ C, i64 ldc, int symmetric, i64 tiles_n, i64 k_chunk,
               i64 split_stride, i64 tm_begin, i64 tm_end) {
@@ -76,9 +81,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const i64 k_end = (k_begin + k_chunk < K) ? k_begin + k_chunk : K;
   C += blockIdx.y * split_stride;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm0 = (warp / 4) * WM, wn0 = (warp % 4) * WN;
+  const int wm0 = (warp / WARPS_N) * WM, wn0 = (warp % WARPS_N) * WN;
 
-  // Stage loader: BK rows x 128 doubles of A and of B, VEC doubles per copy;
+  // Stage loader: BK rows x BM doubles of A and of B, VEC doubles per copy;
   // out-of-range elements are zero-filled by the copy's src-size operand.
   auto load_stage = [&](int slot, i64 k0) {
     double* As = smem + slot * STAGE_DOUBLES;
@@ -238,7 +243,7 @@ void gemm_tn(dfpca_context* ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, 
   }
   const i64 tiles_m = (M + BM - 1) / BM;
   const i64 tiles_n = (N + BN - 1) / BN;
-  const std::size_t smem = sizeof(double) * STAGES * STAGE_DOUBLES;  // 101 KB
+  const std::size_t smem = sizeof(double) * STAGES * STAGE_DOUBLES;  // 52 KB
   const bool vec2 = (lda % 2 == 0) && (ldb % 2 == 0) && (reinterpret_cast<std::uintptr_t>(A) % 16 == 0) &&
                     (reinterpret_cast<std::uintptr_t>(B) % 16 == 0);
   if (tm_end < 0 || tm_end > tiles_m) tm_end = tiles_m;

@@ -29,27 +29,50 @@
 namespace dfpca_gpu {
 
 // ----------------------------------------------------------------- kernels --
-// packed[(s - r0) * w + (t - c0)] = value (s, t) of the block, read from a
-// row-major buffer whose row 0 is global row row0 (ld = G): element [s][t],
-// or [t][s] for a transposed block (32 x 32 shared-memory tiles keep both
-// sides coalesced).
-__global__ void k_pack_block(const double* __restrict__ src, i64 ld, i64 row0, i64 r0, i64 r1, i64 c0, i64 c1,
-                             int transpose, double* __restrict__ out) {
+// One exchange block as the batched kernels see it: rows [r0, r1), columns
+// [c0, c1) (global), transpose flag, its offset in the packed buffer, and the
+// first tile / row of the launch that belongs to it.
+struct PackDesc {
+  i64 r0, r1, c0, c1;
+  i64 off;    // packed offset (elements)
+  i64 first;  // first tile (pack) or row (unpack) of this block in the launch
+  int transpose;
+};
+
+__device__ inline int find_block(const PackDesc* __restrict__ d, int n, i64 x) {
+  int lo = 0, hi = n - 1;  // last block with first <= x
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (d[mid].first <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// packed[off + (s - r0) * w + (t - c0)] = value (s, t) of each block, read
+// from a row-major buffer whose row 0 is global row row0 (ld = G): element
+// [s][t], or [t][s] for a transposed block (32 x 32 shared-memory tiles keep
+// both sides coalesced).  One launch packs every block of a phase.
+__global__ void k_pack_blocks(const double* __restrict__ src, i64 ld, i64 row0, const PackDesc* __restrict__ desc,
+                              int n_desc, double* __restrict__ packed) {
   __shared__ double tile[32][33];
-  const i64 w = c1 - c0, h = r1 - r0;
+  const PackDesc b = desc[find_block(desc, n_desc, blockIdx.x)];
+  const i64 w = b.c1 - b.c0, h = b.r1 - b.r0;
   const i64 tw = (w + 31) / 32;
-  const i64 bs = (blockIdx.x / tw) * 32, bt = (blockIdx.x % tw) * 32;  // tile origin (s, t), block-relative
+  const i64 t_local = blockIdx.x - b.first;
+  const i64 bs = (t_local / tw) * 32, bt = (t_local % tw) * 32;  // tile origin (s, t), block-relative
+  double* out = packed + b.off;
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
-  if (!transpose) {
+  if (!b.transpose) {
     for (int r = ty; r < 32; r += 8) {
       const i64 s = bs + r, t = bt + tx;
-      if (s < h && t < w) out[s * w + t] = src[(r0 + s - row0) * ld + c0 + t];
+      if (s < h && t < w) out[s * w + t] = src[(b.r0 + s - row0) * ld + b.c0 + t];
     }
     return;
   }
   for (int r = ty; r < 32; r += 8) {  // rows t of the source, columns s
     const i64 t = bt + r, s = bs + tx;
-    tile[r][tx] = (s < h && t < w) ? src[(c0 + t - row0) * ld + r0 + s] : 0.0;
+    tile[r][tx] = (s < h && t < w) ? src[(b.c0 + t - row0) * ld + b.r0 + s] : 0.0;
   }
   __syncthreads();
   for (int r = ty; r < 32; r += 8) {
@@ -58,19 +81,18 @@ __global__ void k_pack_block(const double* __restrict__ src, i64 ld, i64 row0, i
   }
 }
 
-// dst[(s - row0) * ld + t] = packed block; one CTA row per block row, threads
-// across the columns (coalesced on both sides, no per-element division).
-__global__ void k_unpack_block(const double* __restrict__ in, double* __restrict__ dst, i64 ld, i64 row0, i64 r0,
-                               i64 r1, i64 c0, i64 c1) {
-  const i64 w = c1 - c0, h = r1 - r0;
-  for (i64 s = blockIdx.x; s < h; s += gridDim.x) {
-    const double* src = in + s * w;
-    double* out = dst + (r0 + s - row0) * ld + c0;
-    for (i64 t = threadIdx.x; t < w; t += blockDim.x) out[t] = src[t];
-  }
+// dst[(s - row0) * ld + t] = packed block rows; one CTA per block row, threads
+// across the columns (coalesced on both sides).
+__global__ void k_unpack_blocks(const double* __restrict__ packed, double* __restrict__ dst, i64 ld, i64 row0,
+                                const PackDesc* __restrict__ desc, int n_desc) {
+  const PackDesc b = desc[find_block(desc, n_desc, blockIdx.x)];
+  const i64 w = b.c1 - b.c0;
+  const i64 s = blockIdx.x - b.first;
+  const double* in = packed + b.off + s * w;
+  double* out = dst + (b.r0 + s - row0) * ld + b.c0;
+  for (i64 t = threadIdx.x; t < w; t += blockDim.x) out[t] = in[t];
 }
 
-// --------------------------------------------------------------- transports --
 namespace {
 
 // ---- NCCL, loaded at run time ----
@@ -352,44 +374,67 @@ void run_shard_exchange(dfpca_context* ctx, Transport& tr, const ShardPlan& plan
       o += kv.second;
     }
   }
-  auto pack = [&](const ShardBlock& b, double* out) {
-    const i64 tiles = ((b.r1 - b.r0 + 31) / 32) * ((b.c1 - b.c0 + 31) / 32);
-    if (tiles > 0)
-      DFPCA_LAUNCH(ctx, k_pack_block, static_cast<unsigned>(tiles), 256, 0, buf, G, buf_row0, b.r0, b.r1, b.c0, b.c1,
-                   b.transpose ? 1 : 0, out);
-  };
-  auto unpack = [&](const ShardBlock& b, const double* in) {
-    if (b.elems() > 0)
-      DFPCA_LAUNCH(ctx, k_unpack_block, static_cast<unsigned>(std::min<i64>(b.r1 - b.r0, 148ll * 16)), 256, 0, in,
-                   buf, G, buf_row0, b.r0, b.r1, b.c0, b.c1);
+  // one pack launch for every outgoing and local block, in buffer order
+  std::vector<PackDesc> pk, up_r, up_l;
+  i64 tiles = 0;
+  auto add_pack = [&](const ShardBlock& b, i64 off) {
+    if (b.elems() <= 0) return;
+    pk.push_back({b.r0, b.r1, b.c0, b.c1, off, tiles, b.transpose ? 1 : 0});
+    tiles += ((b.r1 - b.r0 + 31) / 32) * ((b.c1 - b.c0 + 31) / 32);
   };
   {
     std::map<int, i64> cur = soff;
     for (const ShardBlock& b : sends) {
-      pack(b, sbuf.get() + cur[b.dst]);
+      add_pack(b, cur[b.dst]);
       cur[b.dst] += b.elems();
     }
   }
   i64 lo = n_send;
   for (const ShardBlock& b : locals) {
-    pack(b, sbuf.get() + lo);
+    add_pack(b, lo);
     lo += b.elems();
   }
+  auto launch_pack = [&](const std::vector<PackDesc>& d, i64 n_tiles) {
+    if (d.empty()) return;
+    DevBuf<PackDesc> dd(d.size());
+    DFPCA_CUDA(cudaMemcpyAsync(dd.get(), d.data(), sizeof(PackDesc) * d.size(), cudaMemcpyHostToDevice, ctx->stream));
+    DFPCA_LAUNCH(ctx, k_pack_blocks, static_cast<unsigned>(n_tiles), 256, 0, buf, G, buf_row0, dd.get(),
+                 static_cast<int>(d.size()), sbuf.get());
+  };
+  auto launch_unpack = [&](const std::vector<PackDesc>& d, i64 n_rows, const double* packed) {
+    if (d.empty()) return;
+    DevBuf<PackDesc> dd(d.size());
+    DFPCA_CUDA(cudaMemcpyAsync(dd.get(), d.data(), sizeof(PackDesc) * d.size(), cudaMemcpyHostToDevice, ctx->stream));
+    DFPCA_LAUNCH(ctx, k_unpack_blocks, static_cast<unsigned>(n_rows), 256, 0, packed, buf, G, buf_row0, dd.get(),
+                 static_cast<int>(d.size()));
+  };
+  launch_pack(pk, tiles);
   std::vector<Transport::Msg> smsg, rmsg;
   for (auto& kv : send_n) smsg.push_back({kv.first, sbuf.get() + soff[kv.first], kv.second});
   for (auto& kv : recv_n) rmsg.push_back({kv.first, rbuf.get() + roff[kv.first], kv.second});
   tr.exchange(ctx, smsg, rmsg);
   {
     std::map<int, i64> cur = roff;
+    i64 rows = 0;
     for (const ShardBlock& b : recvs) {
-      unpack(b, rbuf.get() + cur[b.src]);
+      if (b.elems() > 0) {
+        up_r.push_back({b.r0, b.r1, b.c0, b.c1, cur[b.src], rows, 0});
+        rows += b.r1 - b.r0;
+      }
       cur[b.src] += b.elems();
     }
+    launch_unpack(up_r, rows, rbuf.get());
   }
-  lo = n_send;
-  for (const ShardBlock& b : locals) {
-    unpack(b, sbuf.get() + lo);
-    lo += b.elems();
+  {
+    i64 off = n_send, rows = 0;
+    for (const ShardBlock& b : locals) {
+      if (b.elems() > 0) {
+        up_l.push_back({b.r0, b.r1, b.c0, b.c1, off, rows, 0});
+        rows += b.r1 - b.r0;
+      }
+      off += b.elems();
+    }
+    launch_unpack(up_l, rows, sbuf.get());
   }
 }
 

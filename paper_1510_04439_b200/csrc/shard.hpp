@@ -17,7 +17,7 @@
 //     and receives the transposed blocks of the rows before it, so every
 //     rank ends with complete, exactly symmetric rows of the covariance.
 //
-// Slab boundaries are multiples of the 128-row GEMM tile (plane granularity
+// Slab boundaries are multiples of the 64-row GEMM tile (plane granularity
 // `unit`) and balance the upper-triangle work, which dominates every stage.
 #pragma once
 
@@ -29,7 +29,7 @@ namespace dfpca_gpu {
 
 using i64 = std::int64_t;
 
-constexpr i64 kShardRowTile = 128;  // GEMM tile rows (gemm.cu BM)
+constexpr i64 kShardRowTile = 64;  // GEMM tile rows (gemm.cu BM)
 
 struct ShardPlan {
   int world = 1;

@@ -1277,7 +1277,7 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
   const i64 tiles = (G + 31) / 32;
   const i64 I0 = out_row0 / 32, I1 = (out_row0 + out_rows + 31) / 32;
   auto pstart = [tiles](i64 i) { return i * tiles - i * (i - 1) / 2; };
-  const i64 pairs = pstart(I1) - pstart(I0);
+  const i64 pairs = out_rows > 0 ? pstart(I1) - pstart(I0) : 0;  // (slab rows start on 64-row tiles)
   if (pairs > 0)
     DFPCA_LAUNCH(ctx, k_center_mirror, static_cast<unsigned>(pairs), 256, 0, surf->values.get(), mean_dev.get(),
                  grid.has_mask ? mask_dev.get() : nullptr, G, I0, I1, out_row0);

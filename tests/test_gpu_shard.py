@@ -71,9 +71,9 @@ def test_sharded_with_idle_ranks(api):
     """More ranks than 128-row units: the surplus ranks hold empty slabs and
     still take part in both exchanges."""
     from paper_1510_04439_b200 import synth
-    sd = synth.grid_nodes(2, 16, 30, 0.2)  # G = 256: two units
+    sd = synth.grid_nodes(2, 12, 30, 0.2)  # G = 144: three 64-row units (rn = 12 -> 16-plane units)
     grid, b, h, mean = _setup(api, sd)
-    bounds = api.shard_bounds(16, 16, 4, 5)
+    bounds = api.shard_bounds(12, 12, 3, 5)
     assert sum(1 for r in range(5) if bounds[r] == bounds[r + 1]) >= 3
     one = api.fft_covariance(b, grid, h, mean).values
     many = api.fft_covariance_emulated(b, grid, h, mean, 5)

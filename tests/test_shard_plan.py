@@ -13,7 +13,7 @@ import socket
 import numpy as np
 import pytest
 
-TILE = 128  # GEMM row tile (gemm.cu BM)
+TILE = 64  # GEMM row tile (gemm.cu BM)
 
 
 def _api():

@@ -1,6 +1,7 @@
 // extern "C" entry points of libdfpca_cuda.so (include/dfpca_cuda.h):
 // argument validation in the reference's order, error mapping to the
 // reference's error names, handle management and stage timing.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -347,6 +348,22 @@ int dfpca_context_create(int device, dfpca_context** out) {
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
     std::uint64_t keep = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    // Back the pool with physical memory up front (DFPCA_POOL_RESERVE_GB,
+    // default 16): blocks freed into a pool that already holds them are
+    // handed out again without mapping new pages, so call-to-call allocation
+    // cost stays flat instead of spiking when a call needs more than the
+    // previous ones.
+    const char* e = std::getenv("DFPCA_POOL_RESERVE_GB");
+    const double gb = e ? std::atof(e) : 16.0;
+    std::size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const std::size_t want = std::min<std::size_t>(static_cast<std::size_t>(gb * (1ull << 30)), free_b / 2);
+    void* p = nullptr;
+    if (want > 0 && cudaMallocAsync(&p, want, ctx->stream) == cudaSuccess) {
+      cudaFreeAsync(p, ctx->stream);
+      cudaStreamSynchronize(ctx->stream);
+    }
+    cudaGetLastError();
   }
   *out = ctx;
   return 0;

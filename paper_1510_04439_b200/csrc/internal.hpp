@@ -34,9 +34,11 @@ void cuda_check(cudaError_t e, const char* what);
 
 #define DFPCA_CUDA(call) ::dfpca_gpu::cuda_check((call), #call)
 
-// Stream the current API call runs on; device buffers are allocated and freed
+// Stream the current API call runs on; device buffers are allocated
 // stream-ordered on it (cudaMallocAsync from the device's default pool, whose
-// release threshold is raised at context creation so blocks are cached).
+// release threshold is raised at context creation so blocks are cached) and
+// freed on the same stream, also when a handle is released outside any call
+// (dfpca_*_free), so the pool can hand the block to the next call at once.
 extern thread_local cudaStream_t g_alloc_stream;
 
 // Move-only owning device array.
@@ -47,9 +49,9 @@ class DevBuf {
   explicit DevBuf(std::size_t n) { alloc(n); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_), s_(o.s_) { o.p_ = nullptr; o.n_ = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { release(); p_ = o.p_; n_ = o.n_; o.p_ = nullptr; o.n_ = 0; }
+    if (this != &o) { release(); p_ = o.p_; n_ = o.n_; s_ = o.s_; o.p_ = nullptr; o.n_ = 0; }
     return *this;
   }
   ~DevBuf() { release(); }
@@ -59,9 +61,10 @@ class DevBuf {
     if (n == 0) return;
     DFPCA_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), g_alloc_stream));
     n_ = n;
+    s_ = g_alloc_stream;
   }
   void release() {
-    if (p_) cudaFreeAsync(p_, g_alloc_stream);
+    if (p_) cudaFreeAsync(p_, s_);
     p_ = nullptr;
     n_ = 0;
   }
@@ -72,6 +75,7 @@ class DevBuf {
  private:
   T* p_ = nullptr;
   std::size_t n_ = 0;
+  cudaStream_t s_ = nullptr;  // allocation stream, reused for the free
 };
 
 // Validated copy of an EvaluationGrid (grid.hpp:92-230).

@@ -4,8 +4,8 @@
 // sketch, range capture, Householder QR, Rayleigh-Ritz projection, Jacobi
 // eigensolve, lift and Riemann MGS all happen on the device
 // (dfpca_randomized_eig), on the device-resident covariance when the surface
-// came from fft_covariance.  dense_eig (the LAPACK comparator) is not part of
-// the GPU build.
+// came from fft_covariance.  dense_eig (the LAPACK comparator, also the
+// pipeline's default) runs cuSOLVER syevd on the device (dfpca_dense_eig).
 //
 // MatrixizedCovariance::dense_matrix / apply use Eigen::MatrixXd when Eigen is
 // available (as in the reference) and a small column-major dfpca::DenseMatrix
@@ -133,6 +133,30 @@ inline dfpca_surface* device_surface(const SurfaceEstimate& s) {
   return h;
 }
 }  // namespace gpu
+
+/// dense_eig (eigensolve.hpp:205-228): full symmetric eigendecomposition on
+/// the GPU (cuSOLVER syevd) followed by the reference's finalization.
+inline EigenSystem dense_eig(const MatrixizedCovariance& S, std::size_t L_max, const EvaluationGrid& grid) {
+  if (!S.dense)
+    throw err::invalid_argument("dense eigendecomposition needs the dense provider; "
+                                "the matrix exceeded the memory budget");
+  const auto G = static_cast<std::size_t>(grid.size());
+  const std::size_t cap = std::max<std::size_t>(L_max, 1);
+  std::vector<double> ev(cap), ef(cap * G), fve(cap);
+  double total = 0.0;
+  int64_t n = 0;
+  gpu::GridDesc gd(grid);
+  gpu::check(dfpca_dense_eig(gpu::context(), gpu::device_surface(*S.cov), gd.get(), static_cast<int64_t>(L_max),
+                             ev.data(), ef.data(), fve.data(), &total, &n));
+  EigenSystem out;
+  out.total_variance = total;
+  for (int64_t l = 0; l < n; ++l) {
+    out.eigenvalues.push_back(ev[static_cast<std::size_t>(l)]);
+    out.fve.push_back(fve[static_cast<std::size_t>(l)]);
+    out.eigenfunctions.emplace_back(ef.begin() + l * static_cast<int64_t>(G), ef.begin() + (l + 1) * static_cast<int64_t>(G));
+  }
+  return out;
+}
 
 inline EigenSystem randomized_eig(const MatrixizedCovariance& S, std::size_t q, std::size_t L_max,
                                   const EvaluationGrid& grid, std::uint64_t seed) {

@@ -211,6 +211,14 @@ DFPCA_API int dfpca_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov,
                          double* eigenfunctions, double* fve, double* total_variance,
                          int64_t* n_components);
 
+/* Replaces dfpca::dense_eig (eigensolve.hpp:205-228): full symmetric
+ * eigendecomposition of the in-mask matrix on the device (cuSOLVER syevd,
+ * libcusolver.so.11 loaded at run time, DFPCA_CUSOLVER_LIB overrides), then
+ * the reference's finalization (Riemann normalization without Gram-Schmidt,
+ * truncation, sign rule, FVE).  Outputs as dfpca_randomized_eig. */
+DFPCA_API int dfpca_dense_eig(dfpca_context* ctx, const dfpca_surface* cov, const dfpca_grid* grid, int64_t L_max,
+                    double* eigenvalues, double* eigenfunctions, double* fve, double* total_variance,
+                    int64_t* n_components);
 /* Residual diagnostic (eigensolve.hpp:294-312) for L eigenpairs. */
 DFPCA_API int dfpca_eig_residuals(dfpca_context* ctx, const dfpca_surface* cov, const dfpca_grid* grid,
                         int64_t L, const double* eigenvalues, const double* eigenfunctions,

@@ -60,6 +60,7 @@ SIGNATURES = [
     ("dfpca_randomized_eig", C.c_int, [P, P, C.POINTER(DfpcaGrid), C.c_int64, C.c_int64, C.c_uint64, PD, PD,
                                        PD, PD, PI64]),
     ("dfpca_eig_residuals", C.c_int, [P, P, C.POINTER(DfpcaGrid), C.c_int64, PD, PD, PD]),
+    ("dfpca_dense_eig", C.c_int, [P, P, C.POINTER(DfpcaGrid), C.c_int64, PD, PD, PD, PD, PI64]),
     ("dfpca_nccl_unique_id", C.c_int, [P]),
     ("dfpca_nccl_init", C.c_int, [P, C.c_int, C.c_int, P]),
     ("dfpca_covariance_sharded", C.c_int, [P, P, C.POINTER(DfpcaGrid), PD, PD, C.POINTER(DfpcaPlan),

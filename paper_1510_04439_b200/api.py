@@ -856,6 +856,27 @@ def randomized_eig(S: MatrixizedCovariance, q: int, L_max: int, grid: Evaluation
                        [float(x) for x in fve[:L]], total.value)
 
 
+def dense_eig(S: MatrixizedCovariance, L_max: int, grid: EvaluationGrid) -> EigenSystem:
+    """eigensolve.hpp:205-228 on the GPU (cuSOLVER syevd + the reference's
+    finalization); needs the dense provider like the reference."""
+    if not S.dense:
+        raise Error(ErrorClass.Config, "InvalidArgument",
+                    "dense eigendecomposition needs the dense provider; the matrix exceeded the memory budget")
+    G = grid.size()
+    ev = np.zeros(max(L_max, 1))
+    ef = np.zeros(max(L_max, 1) * G)
+    fve = np.zeros(max(L_max, 1))
+    total = C.c_double()
+    n = C.c_int64()
+    check(_lib.lib().dfpca_dense_eig(_lib.ctx(), S.cov.device_handle(), C.byref(grid.desc()), L_max,
+                                     ev.ctypes.data_as(C.POINTER(C.c_double)),
+                                     ef.ctypes.data_as(C.POINTER(C.c_double)),
+                                     fve.ctypes.data_as(C.POINTER(C.c_double)), C.byref(total), C.byref(n)))
+    L = n.value
+    return EigenSystem([float(x) for x in ev[:L]], [ef[l * G:(l + 1) * G].copy() for l in range(L)],
+                       [float(x) for x in fve[:L]], total.value)
+
+
 def select_components_fve(eig: EigenSystem, threshold: float) -> int:
     """eigensolve.hpp:282-288."""
     if not threshold > 0.0 or threshold > 1.0:

@@ -59,6 +59,8 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
                         double* fve, double* total_variance, i64* n_components);
 void run_eig_residuals(dfpca_context* ctx, const dfpca_surface* cov, const Grid& grid, i64 L,
                        const double* eigenvalues, const double* eigenfunctions, double* residuals);
+void run_dense_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid& grid, i64 L_max, double* eigenvalues,
+                   double* eigenfunctions, double* fve, double* total_variance, i64* n_components);
 
 void fail(int cls, const char* name, const std::string& msg) {
   Failure f;
@@ -825,6 +827,17 @@ int dfpca_surface_upload(dfpca_context* ctx, const dfpca_grid* grid, int kind, c
 int dfpca_surface_free(dfpca_surface* s) {
   delete s;
   return 0;
+}
+
+int dfpca_dense_eig(dfpca_context* ctx, const dfpca_surface* cov, const dfpca_grid* grid, int64_t L_max,
+                    double* eigenvalues, double* eigenfunctions, double* fve, double* total_variance,
+                    int64_t* n_components) {
+  return guarded(ctx, [&] {
+    if (!cov) fail(kConfig, "InvalidArgument", "null covariance surface");
+    if (L_max < 0) fail(kConfig, "InvalidArgument", "L_max must be >= 0");
+    Grid g = make_grid(grid);
+    run_dense_eig(ctx, cov, g, L_max, eigenvalues, eigenfunctions, fve, total_variance, n_components);
+  });
 }
 
 int dfpca_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const dfpca_grid* grid, int64_t q,

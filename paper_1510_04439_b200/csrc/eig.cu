@@ -9,7 +9,10 @@
 //   eig     cyclic parallel Jacobi on the q x q problem (one CTA)
 //   lifted  = Q V                               (DMMA GEMM)
 //   final   Riemann MGS, norm cut, sign canonicalization (one CTA)
+#include <dlfcn.h>
+
 #include <algorithm>
+#include <string>
 #include <cmath>
 #include <vector>
 
@@ -379,7 +382,7 @@ __global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ Ag, double
 __global__ void __launch_bounds__(1024) k_finalize(const double* __restrict__ Lt, const double* __restrict__ tilde,
                                                    i64 M, int q, int L_max, double cut, double cv,
                                                    double* __restrict__ kept, int* __restrict__ kept_src,
-                                                   int* __restrict__ n_kept) {
+                                                   int* __restrict__ n_kept, int gram_schmidt) {
   __shared__ double red[33];
   __shared__ i64 first_nz;
   int nk = 0;
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(1024) k_finalize(const double* __restrict__ Lt
     double* v = kept + static_cast<i64>(nk) * M;
     for (i64 i = threadIdx.x; i < M; i += blockDim.x) v[i] = Lt[static_cast<i64>(l) * M + i];
     __syncthreads();
-    for (int u = 0; u < nk; ++u) {
+    for (int u = 0; u < (gram_schmidt ? nk : 0); ++u) {
       const double* uv = kept + static_cast<i64>(u) * M;
       double s = 0.0;
       for (i64 i = threadIdx.x; i < M; i += blockDim.x) s += uv[i] * v[i];
@@ -399,7 +402,7 @@ __global__ void __launch_bounds__(1024) k_finalize(const double* __restrict__ Lt
     double s2 = 0.0;
     for (i64 i = threadIdx.x; i < M; i += blockDim.x) s2 += v[i] * v[i];
     const double norm = sqrt(cv * block_sum(s2, red));
-    if (!(norm > 1e-10)) continue;
+    if (gram_schmidt && !(norm > 1e-10)) continue;  // dense_eig normalizes unconditionally
     for (i64 i = threadIdx.x; i < M; i += blockDim.x) v[i] /= norm;
     __syncthreads();
     double s1 = 0.0;
@@ -534,6 +537,55 @@ static RowShard shard_rows_dev(dfpca_context* ctx, Transport& tr, const dfpca_su
   return rs;
 }
 
+// finalize_eigensystem (eigensolve.hpp:146-194) on the device: candidates Lt
+// [q][M] in descending order of tilde (host copy tilde_h, device tilde_d).
+static void finish_eigensystem(dfpca_context* ctx, const Grid& grid, const std::vector<i64>& node_of_row, i64 M,
+                               const double* Lt, const double* tilde_d, const std::vector<double>& tilde,
+                               i64 L_max, bool gram_schmidt, double* eigenvalues, double* eigenfunctions,
+                               double* fve, double* total_variance, i64* n_components) {
+  cudaStream_t st = ctx->stream;
+  const i64 q = static_cast<i64>(tilde.size());
+  const double cv = grid.cell_volume();
+  const double cut = tilde.empty() ? 0.0 : std::max(0.0, tilde[0]) * 1e-12;
+  double tilde_total = 0.0;
+  for (double t : tilde)
+    if (t > cut) tilde_total += t;
+  const double total = tilde_total * cv;
+
+  DevBuf<double> kept(static_cast<std::size_t>(std::max<i64>(L_max, 1) * M));
+  DevBuf<int> kept_src(static_cast<std::size_t>(std::max<i64>(L_max, 1))), nkept(1);
+  DFPCA_LAUNCH(ctx, k_finalize, 1, 1024, 0, Lt, tilde_d, M, static_cast<int>(q), static_cast<int>(L_max), cut,
+               cv, kept.get(), kept_src.get(), nkept.get(), gram_schmidt ? 1 : 0);
+  int nk = 0;
+  DFPCA_CUDA(cudaMemcpyAsync(&nk, nkept.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+  DFPCA_CUDA(cudaStreamSynchronize(st));
+  std::vector<int> src(static_cast<std::size_t>(std::max(nk, 1)));
+  std::vector<double> kv(static_cast<std::size_t>(nk) * M);
+  if (nk > 0) {
+    DFPCA_CUDA(cudaMemcpyAsync(src.data(), kept_src.get(), sizeof(int) * nk, cudaMemcpyDeviceToHost, st));
+    DFPCA_CUDA(cudaMemcpyAsync(kv.data(), kept.get(), sizeof(double) * nk * M, cudaMemcpyDeviceToHost, st));
+  }
+  DFPCA_CUDA(cudaStreamSynchronize(st));
+  ctx->end_stage();
+
+  const i64 G = grid.G;
+  double cum = 0.0;
+  for (int l = 0; l < nk; ++l) {
+    const double lam = tilde[static_cast<std::size_t>(src[l])] * cv;
+    if (eigenvalues) eigenvalues[l] = lam;
+    cum += lam;
+    if (fve) fve[l] = total > 0.0 ? cum / total : 1.0;
+    if (eigenfunctions) {
+      double* surf = eigenfunctions + static_cast<i64>(l) * G;
+      for (i64 f = 0; f < G; ++f) surf[f] = std::nan("");
+      for (i64 r = 0; r < M; ++r) surf[node_of_row[static_cast<std::size_t>(r)]] = kv[static_cast<std::size_t>(l) * M + r];
+    }
+  }
+  if (total_variance) *total_variance = total;
+  if (n_components) *n_components = nk;
+}
+
+
 void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid& grid, i64 q_req,
                         i64 L_max, unsigned long long seed, double* eigenvalues, double* eigenfunctions,
                         double* fve, double* total_variance, i64* n_components) {
@@ -641,44 +693,101 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
   DFPCA_CUDA(cudaStreamSynchronize(st));
   if (jinfo != 0) fail(kNumeric, "EigFailure", "projected eigensolver did not converge");
 
-  const double cv = grid.cell_volume();
-  const double cut = tilde.empty() ? 0.0 : std::max(0.0, tilde[0]) * 1e-12;
-  double tilde_total = 0.0;
-  for (double t : tilde)
-    if (t > cut) tilde_total += t;
-  const double total = tilde_total * cv;
+  finish_eigensystem(ctx, grid, mv.node_of_row, M, Lt.get(), evals.get(), tilde, L_max, true, eigenvalues,
+                     eigenfunctions, fve, total_variance, n_components);
+}
 
-  DevBuf<double> kept(static_cast<std::size_t>(std::max<i64>(L_max, 1) * M));
-  DevBuf<int> kept_src(static_cast<std::size_t>(std::max<i64>(L_max, 1))), nkept(1);
-  DFPCA_LAUNCH(ctx, k_finalize, 1, 1024, 0, Lt.get(), evals.get(), M, static_cast<int>(q),
-               static_cast<int>(L_max), cut, cv, kept.get(), kept_src.get(), nkept.get());
-  int nk = 0;
-  DFPCA_CUDA(cudaMemcpyAsync(&nk, nkept.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
-  DFPCA_CUDA(cudaStreamSynchronize(st));
-  std::vector<int> src(static_cast<std::size_t>(std::max(nk, 1)));
-  std::vector<double> kv(static_cast<std::size_t>(nk) * M);
-  if (nk > 0) {
-    DFPCA_CUDA(cudaMemcpyAsync(src.data(), kept_src.get(), sizeof(int) * nk, cudaMemcpyDeviceToHost, st));
-    DFPCA_CUDA(cudaMemcpyAsync(kv.data(), kept.get(), sizeof(double) * nk * M, cudaMemcpyDeviceToHost, st));
-  }
-  DFPCA_CUDA(cudaStreamSynchronize(st));
-  ctx->end_stage();
 
-  const i64 G = grid.G;
-  double cum = 0.0;
-  for (int l = 0; l < nk; ++l) {
-    const double lam = tilde[static_cast<std::size_t>(src[l])] * cv;
-    if (eigenvalues) eigenvalues[l] = lam;
-    cum += lam;
-    if (fve) fve[l] = total > 0.0 ? cum / total : 1.0;
-    if (eigenfunctions) {
-      double* surf = eigenfunctions + static_cast<i64>(l) * G;
-      for (i64 f = 0; f < G; ++f) surf[f] = std::nan("");
-      for (i64 r = 0; r < M; ++r) surf[mv.node_of_row[static_cast<std::size_t>(r)]] = kv[static_cast<std::size_t>(l) * M + r];
+// ---- dense_eig (eigensolve.hpp:205-228): cuSOLVER syevd on the device ----
+namespace {
+struct CusolverApi {
+  using Handle = void*;
+  int (*Create)(Handle*) = nullptr;
+  int (*Destroy)(Handle) = nullptr;
+  int (*SetStream)(Handle, cudaStream_t) = nullptr;
+  int (*DsyevdBufferSize)(Handle, int, int, int, const double*, int, const double*, int*) = nullptr;
+  int (*Dsyevd)(Handle, int, int, int, double*, int, double*, double*, int, int*) = nullptr;
+  static constexpr int kEigModeVector = 1, kFillLower = 0;
+  static CusolverApi& get() {
+    static CusolverApi api;
+    static bool tried = false;
+    if (!tried) {
+      tried = true;
+      std::vector<std::string> names;
+      if (const char* e = std::getenv("DFPCA_CUSOLVER_LIB")) names.push_back(e);
+      names.push_back("libcusolver.so.11");
+      names.push_back("/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/cusolver/lib/libcusolver.so.11");
+      void* h = nullptr;
+      for (const auto& n : names)
+        if ((h = dlopen(n.c_str(), RTLD_NOW | RTLD_GLOBAL))) break;
+      if (h) {
+        api.Create = reinterpret_cast<decltype(api.Create)>(dlsym(h, "cusolverDnCreate"));
+        api.Destroy = reinterpret_cast<decltype(api.Destroy)>(dlsym(h, "cusolverDnDestroy"));
+        api.SetStream = reinterpret_cast<decltype(api.SetStream)>(dlsym(h, "cusolverDnSetStream"));
+        api.DsyevdBufferSize =
+            reinterpret_cast<decltype(api.DsyevdBufferSize)>(dlsym(h, "cusolverDnDsyevd_bufferSize"));
+        api.Dsyevd = reinterpret_cast<decltype(api.Dsyevd)>(dlsym(h, "cusolverDnDsyevd"));
+      }
     }
+    if (!api.Create || !api.Dsyevd || !api.DsyevdBufferSize || !api.SetStream)
+      fail(kConfig, "InvalidArgument", "libcusolver.so.11 could not be loaded (set DFPCA_CUSOLVER_LIB)");
+    return api;
   }
-  if (total_variance) *total_variance = total;
-  if (n_components) *n_components = nk;
+};
+
+__global__ void k_reverse_rows(const double* __restrict__ in, i64 rows, i64 cols, double* __restrict__ out) {
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < rows * cols; e += (i64)gridDim.x * blockDim.x) {
+    const i64 r = e / cols, c = e % cols;
+    out[(rows - 1 - r) * cols + c] = in[e];
+  }
+}
+}  // namespace
+
+void run_dense_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid& grid, i64 L_max, double* eigenvalues,
+                   double* eigenfunctions, double* fve, double* total_variance, i64* n_components) {
+  if (cov->kind != DFPCA_SURFACE_COVARIANCE)
+    fail(kConfig, "InvalidArgument", "matrixize expects a covariance surface");
+  if (cov->n != grid.G * grid.G) fail(kConfig, "InvalidArgument", "covariance surface has wrong length");
+  CusolverApi& api = CusolverApi::get();
+  cudaStream_t st = ctx->stream;
+  ctx->begin_stage("eigen");
+  MatrixView mv = matrixize_dev(ctx, cov, grid);
+  const i64 M = mv.M;
+  if (M > (i64(1) << 31) / M) fail(kConfig, "InvalidArgument", "matrix too large for the dense eigensolver");
+  // A = Sigma (symmetric: row-major == column-major), overwritten by the eigenvectors
+  DevBuf<double> A(static_cast<std::size_t>(M * M)), w(static_cast<std::size_t>(M));
+  DFPCA_CUDA(cudaMemcpyAsync(A.get(), mv.sigma, sizeof(double) * M * M, cudaMemcpyDeviceToDevice, st));
+  CusolverApi::Handle h = nullptr;
+  if (api.Create(&h) != 0) fail(kNumeric, "DeviceError", "cusolverDnCreate failed");
+  struct Guard {
+    CusolverApi& a;
+    CusolverApi::Handle h;
+    ~Guard() { a.Destroy(h); }
+  } guard{api, h};
+  api.SetStream(h, st);
+  int lwork = 0;
+  if (api.DsyevdBufferSize(h, CusolverApi::kEigModeVector, CusolverApi::kFillLower, static_cast<int>(M), A.get(),
+                           static_cast<int>(M), w.get(), &lwork) != 0)
+    fail(kNumeric, "DeviceError", "cusolverDnDsyevd_bufferSize failed");
+  DevBuf<double> work(static_cast<std::size_t>(std::max(lwork, 1)));
+  DevBuf<int> info(1);
+  if (api.Dsyevd(h, CusolverApi::kEigModeVector, CusolverApi::kFillLower, static_cast<int>(M), A.get(),
+                 static_cast<int>(M), w.get(), work.get(), lwork, info.get()) != 0)
+    fail(kNumeric, "DeviceError", "cusolverDnDsyevd failed");
+  int hinfo = 0;
+  std::vector<double> wa(static_cast<std::size_t>(M));
+  DFPCA_CUDA(cudaMemcpyAsync(&hinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+  DFPCA_CUDA(cudaMemcpyAsync(wa.data(), w.get(), sizeof(double) * M, cudaMemcpyDeviceToHost, st));
+  DFPCA_CUDA(cudaStreamSynchronize(st));
+  if (hinfo != 0)
+    fail(kNumeric, "EigFailure", "symmetric eigensolver did not converge (info=" + std::to_string(hinfo) + ")");
+  // ascending -> descending; column j of the column-major A is row j here
+  std::vector<double> tilde(wa.rbegin(), wa.rend());
+  DevBuf<double> Lt(static_cast<std::size_t>(M * M)), td(static_cast<std::size_t>(M));
+  DFPCA_LAUNCH(ctx, k_reverse_rows, grid_for(M * M, 256, 148ll * 32), 256, 0, A.get(), M, M, Lt.get());
+  DFPCA_CUDA(cudaMemcpyAsync(td.get(), tilde.data(), sizeof(double) * M, cudaMemcpyHostToDevice, st));
+  finish_eigensystem(ctx, grid, mv.node_of_row, M, Lt.get(), td.get(), tilde, L_max, false, eigenvalues,
+                     eigenfunctions, fve, total_variance, n_components);
 }
 
 void run_eig_residuals(dfpca_context* ctx, const dfpca_surface* cov, const Grid& grid, i64 L,

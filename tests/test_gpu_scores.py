@@ -101,3 +101,26 @@ def test_score_errors(api):
     with pytest.raises(api.Error) as e:
         api.compute_scores_batch(dense.dataset(), grid, mean, eig, 0.1, api.ScoreMethod.Pace)
     assert e.value.name() == "InvalidArgument"
+
+
+@pytest.mark.parametrize("case", ["sparse_masked_2d", "nodes_2d", "random_1d"])
+def test_dense_eig_matches_reference(api, ref, case):
+    """dense_eig (eigensolve.hpp:205-228): cuSOLVER syevd + the reference's
+    finalization vs the reference (LAPACK dsyevd) on the same covariance."""
+    from helpers import aligned_ise
+    from paper_1510_04439_b200 import synth
+    sd = CASES[case](synth)
+    grid, mean, diag, cov, eig = _model(api, sd)
+    L = 4
+    got = api.dense_eig(api.matrixize(cov), L, grid)
+    want = ref.dense_eig((sd.axes, sd.mask), cov.values, L)
+    assert len(got.eigenvalues) == len(want["eigenvalues"])
+    assert np.allclose(got.eigenvalues, want["eigenvalues"], rtol=1e-10, atol=0)
+    cv = grid.cell_volume()
+    lam = np.asarray(want["eigenvalues"])
+    for l in range(len(lam)):
+        gap = min([abs(lam[l] - lam[k]) for k in range(len(lam)) if k != l] + [np.inf]) / lam[0]
+        if gap > 1e-3:
+            assert aligned_ise(cv, got.eigenfunctions[l], want["eigenfunctions"][l]) <= 1e-8
+    assert abs(got.total_variance - want["total_variance"]) <= 1e-10 * abs(want["total_variance"])
+    assert np.allclose(got.fve, want["fve"], rtol=1e-10, atol=1e-12)

@@ -59,6 +59,13 @@ def run(cfg: int, q: int, L: int):
     t0 = time.perf_counter()
     eig = api.randomized_eig(api.matrixize(cov), q, L, grid, 20260815)
     t["eig_ms"] = (time.perf_counter() - t0) * 1e3
+    M = G if sd.mask is None else int(np.count_nonzero(sd.mask))
+    if M <= 8192:  # dense_eig (eigensolve.hpp:205-228), the pipeline default
+        t0 = time.perf_counter()
+        dense = api.dense_eig(api.matrixize(cov), L, grid)
+        t["dense_eig_ms"] = (time.perf_counter() - t0) * 1e3
+        out["dense_vs_randomized_top4_rel"] = [
+            abs(a - b) / abs(b) for a, b in zip(np.asarray(eig.eigenvalues)[:4], np.asarray(dense.eigenvalues)[:4])]
     out["times"] = t
     G = grid.size()
     checks = {}

@@ -59,7 +59,7 @@ def run(cfg: int, q: int, L: int):
     t0 = time.perf_counter()
     eig = api.randomized_eig(api.matrixize(cov), q, L, grid, 20260815)
     t["eig_ms"] = (time.perf_counter() - t0) * 1e3
-    M = G if sd.mask is None else int(np.count_nonzero(sd.mask))
+    M = grid.size() if sd.mask is None else int(np.count_nonzero(sd.mask))
     if M <= 8192:  # dense_eig (eigensolve.hpp:205-228), the pipeline default
         t0 = time.perf_counter()
         dense = api.dense_eig(api.matrixize(cov), L, grid)

@@ -16,6 +16,7 @@
 // scaling pass so the operand copies stay asynchronous.
 #include <algorithm>
 #include <cstdint>
+#include <vector>
 
 #include "gemm.cuh"
 
@@ -57,28 +58,32 @@ template <int VEC>
 __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
     k_gemm_tn(i64 M, i64 N, i64 K, const double* __restrict__ A, i64 lda, const double* __restrict__ B,
               i64 ldb, double* __restrict__ C, i64 ldc, int symmetric, i64 tiles_n, i64 k_chunk,
-              i64 split_stride, i64 tm_begin, i64 tm_end) {
+              i64 split_stride, i64 tm_begin, i64 tm_end, const int4* __restrict__ items,
+              double* __restrict__ ws, i64 k_mid) {
   extern __shared__ __align__(16) double smem[];
 
-  // symmetric: row tiles [tm_begin, tm_end) only (a slab of a sharded pair
-  // grid, shard.hpp); C's row 0 is global row tm_begin * BM and mirrored tiles
-  // are written only inside the slab
+  // symmetric: one work item per CTA (items, sym_items()): a tile pair
+  // (tm <= tn) of row tiles [tm_begin, tm_end) (a slab of a sharded pair grid,
+  // shard.hpp; C's row 0 is global row tm_begin * BM and mirrored tiles are
+  // written only inside the slab), either whole or one K half of a split tile
+  // whose two partial sums go to ws and are added by k_sym_split_reduce
   i64 tm, tn;
+  int kpart = -1, slot = 0;
   if (symmetric) {
-    i64 t = blockIdx.x;  // upper-triangular tile pairs (tm <= tn)
-    tm = tm_begin;
-    while (t >= tiles_n - tm) {
-      t -= tiles_n - tm;
-      ++tm;
-    }
-    tn = tm + t;
+    const int4 it = items[blockIdx.x];
+    tm = it.x;
+    tn = it.y;
+    kpart = it.z;
+    slot = it.w;
   } else {
     tm = blockIdx.x / tiles_n;
     tn = blockIdx.x % tiles_n;
   }
   const i64 m0 = tm * BM, n0 = tn * BN;
-  const i64 k_begin = blockIdx.y * k_chunk;
-  const i64 k_end = (k_begin + k_chunk < K) ? k_begin + k_chunk : K;
+  i64 k_begin = blockIdx.y * k_chunk;
+  i64 k_end = (k_begin + k_chunk < K) ? k_begin + k_chunk : K;
+  if (kpart == 0) k_end = k_mid;
+  if (kpart == 1) k_begin = k_mid;
   C += blockIdx.y * split_stride;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm0 = (warp / WARPS_N) * WM, wn0 = (warp % WARPS_N) * WN;
@@ -149,6 +154,17 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
   }
   cp_async_wait<0>();
 
+  if (kpart >= 0) {  // half of a split tile: the whole 64 x 64 partial to ws
+    double* wt = ws + (static_cast<i64>(slot) * 2 + kpart) * (BM * BN);
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int r = wm0 + i * 8 + (lane >> 2), c = wn0 + j * 8 + 2 * (lane & 3);
+        *reinterpret_cast<double2*>(wt + r * BN + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    return;
+  }
   // Epilogue: fragment (i, j) holds C[row][col], C[row][col + 1].
   const i64 crow0 = symmetric ? tm_begin * BM : 0;
   const bool mirror = symmetric && tm != tn && tn < tm_end;
@@ -172,6 +188,25 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
         if (col + 1 < N) C[(col + 1 - crow0) * ldc + row] = acc[i][j][1];
       }
     }
+  }
+}
+
+// Split tiles of the symmetric product: C = first K half + second K half (in
+// that order), written like a whole tile (direct, and mirrored inside the slab).
+__global__ void k_sym_split_reduce(const int4* __restrict__ split_items, const double* __restrict__ ws, i64 M,
+                                   i64 N, double* __restrict__ C, i64 ldc, i64 tm_begin, i64 tm_end) {
+  const int4 it = split_items[blockIdx.x];
+  const i64 tm = it.x, tn = it.y;
+  const double* w0 = ws + static_cast<i64>(it.w) * 2 * (BM * BN);
+  const double* w1 = w0 + BM * BN;
+  const i64 crow0 = tm_begin * BM;
+  const bool mirror = tm != tn && tn < tm_end;
+  for (int e = threadIdx.x; e < BM * BN; e += blockDim.x) {
+    const i64 row = tm * BM + e / BN, col = tn * BN + e % BN;
+    if (row >= M || col >= N) continue;
+    const double v = w0[e] + w1[e];
+    C[(row - crow0) * ldc + col] = v;
+    if (mirror) C[(col - crow0) * ldc + row] = v;
   }
 }
 
@@ -202,7 +237,7 @@ __global__ void k_scale_rows(const double* __restrict__ in, const double* __rest
 template <int VEC>
 void launch(dfpca_context* ctx, dim3 grid, std::size_t smem, i64 M, i64 N, i64 K, const double* A, i64 lda,
             const double* B, i64 ldb, double* C, i64 ldc, int symmetric, i64 tiles_n, i64 k_chunk,
-            i64 split_stride, i64 tm_begin, i64 tm_end) {
+            i64 split_stride, i64 tm_begin, i64 tm_end, const int4* items, double* ws, i64 k_mid) {
   static bool attr = false;
   if (!attr) {
     DFPCA_CUDA(cudaFuncSetAttribute(k_gemm_tn<VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -210,7 +245,7 @@ void launch(dfpca_context* ctx, dim3 grid, std::size_t smem, i64 M, i64 N, i64 K
     attr = true;
   }
   DFPCA_LAUNCH(ctx, k_gemm_tn<VEC>, grid, NTHREADS, smem, M, N, K, A, lda, B, ldb, C, ldc, symmetric,
-               tiles_n, k_chunk, split_stride, tm_begin, tm_end);
+               tiles_n, k_chunk, split_stride, tm_begin, tm_end, items, ws, k_mid);
 }
 
 }  // namespace
@@ -267,13 +302,57 @@ void gemm_tn(dfpca_context* ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, 
     ldo = N;
     stride = M * N;
   }
-  const dim3 grid(static_cast<unsigned>(blocks), static_cast<unsigned>(splits));
+  // symmetric: the work list (whole tiles first, then the halves of the split
+  // tiles, so the halves fill the last wave)
+  std::vector<int4> items, split_items;
+  i64 k_mid = 0;
+  DevBuf<int4> d_items, d_split;
+  DevBuf<double> ws;
+  i64 n_blocks = blocks;
+  if (symmetric) {
+    // Split rule, a function of the whole grid and the device only (never of
+    // the slab), so a tile's sums are the same for any rank count: the
+    // far-off-diagonal tiles tn - tm >= k0, just enough of them to cover the
+    // partial last wave of the one-device launch.
+    const i64 T = tiles_m, total = T * (T + 1) / 2, W = static_cast<i64>(CTAS_PER_SM) * ctx->sm_count;
+    const i64 rem = total % W;
+    i64 k0 = T;  // no split
+    if (rem > 0 && K >= 4 * BK)
+      for (i64 cand = T - 1; cand >= 1; --cand)
+        if ((T - cand) * (T - cand + 1) / 2 >= rem) {
+          k0 = cand;
+          break;
+        }
+    k_mid = ((K / 2 + BK - 1) / BK) * BK;
+    for (i64 tm = tm_begin; tm < tm_end; ++tm)
+      for (i64 tn = tm; tn < tiles_m; ++tn) {
+        if (tn - tm >= k0) split_items.push_back(make_int4(static_cast<int>(tm), static_cast<int>(tn), 0,
+                                                           static_cast<int>(split_items.size())));
+        else items.push_back(make_int4(static_cast<int>(tm), static_cast<int>(tn), -1, 0));
+      }
+    for (const int4& it : split_items) items.push_back(make_int4(it.x, it.y, 0, it.w));
+    for (const int4& it : split_items) items.push_back(make_int4(it.x, it.y, 1, it.w));
+    n_blocks = static_cast<i64>(items.size());
+    d_items.alloc(items.size());
+    DFPCA_CUDA(cudaMemcpyAsync(d_items.get(), items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice,
+                               ctx->stream));
+    if (!split_items.empty()) {
+      ws.alloc(static_cast<std::size_t>(split_items.size() * 2 * BM * BN));
+      d_split.alloc(split_items.size());
+      DFPCA_CUDA(cudaMemcpyAsync(d_split.get(), split_items.data(), sizeof(int4) * split_items.size(),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+    }
+  }
+  const dim3 grid(static_cast<unsigned>(n_blocks), static_cast<unsigned>(splits));
   if (vec2)
     launch<2>(ctx, grid, smem, M, N, K, A, lda, B, ldb, out, ldo, symmetric ? 1 : 0, tiles_n, k_chunk, stride,
-              tm_begin, tm_end);
+              tm_begin, tm_end, d_items.get(), ws.get(), k_mid);
   else
     launch<1>(ctx, grid, smem, M, N, K, A, lda, B, ldb, out, ldo, symmetric ? 1 : 0, tiles_n, k_chunk, stride,
-              tm_begin, tm_end);
+              tm_begin, tm_end, d_items.get(), ws.get(), k_mid);
+  if (!split_items.empty())
+    DFPCA_LAUNCH(ctx, k_sym_split_reduce, static_cast<unsigned>(split_items.size()), 256, 0, d_split.get(), ws.get(),
+                 M, N, C, ldc, tm_begin, tm_end);
   if (splits > 1)
     DFPCA_LAUNCH(ctx, k_splitk_reduce, grid_for(M * N, 256), 256, 0, out, splits, M, N, C, ldc);
 }

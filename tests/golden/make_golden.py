@@ -59,6 +59,18 @@ def main():
         eig = R.randomized_eig(grid, cov, q, 3, 20260815)
         extra.update(eig_values=eig["eigenvalues"], eig_functions=eig["eigenfunctions"], eig_fve=eig["fve"],
                      eig_total=np.array([eig["total_variance"]]), eig_q=np.array([q]))
+        # noise variance, scores (both methods), reconstruction,
+        # dense eigendecomposition -- on the reference's own model surfaces
+        s2 = R.estimate_sigma2(grid, sq, cov, mean)
+        efs = eig["eigenfunctions"]
+        pace, _ = R.scores(grid, sd.offsets, sd.coords, sd.values, mean, eig["eigenvalues"], efs, s2, 0)
+        integ, warn = R.scores(grid, sd.offsets, sd.coords, sd.values, mean, eig["eigenvalues"], efs, s2, 1)
+        rec = R.reconstruct_on_grid(grid, mean, eig["eigenvalues"], efs, integ[0])
+        dense = R.dense_eig(grid, cov, 3)
+        extra.update(sigma2=np.array([s2]), scores_pace=pace, scores_integration=integ,
+                     scores_sparse_warning=warn.astype(np.uint8), reconstruct0=rec,
+                     dense_values=dense["eigenvalues"], dense_functions=dense["eigenfunctions"],
+                     dense_fve=dense["fve"], dense_total=np.array([dense["total_variance"]]))
         save(name, sd, extra)
 
 

@@ -124,3 +124,40 @@ def test_dense_eig_matches_reference(api, ref, case):
             assert aligned_ise(cv, got.eigenfunctions[l], want["eigenfunctions"][l]) <= 1e-8
     assert abs(got.total_variance - want["total_variance"]) <= 1e-10 * abs(want["total_variance"])
     assert np.allclose(got.fve, want["fve"], rtol=1e-10, atol=1e-12)
+
+
+GOLDEN = ["cov2d_random", "cov1d_random", "cov2d_nodes", "cov2d_masked"]
+
+
+@pytest.mark.parametrize("name", GOLDEN)
+def test_scores_against_golden(api, name):
+    """The GPU 8(f) path on the reference's own model surfaces (committed
+    fixtures, tests/golden/make_golden.py) -- no oracle needed at run time."""
+    from pathlib import Path
+    z = np.load(Path(__file__).resolve().parent / "golden" / f"{name}.npz")
+    shape = z["shape"]
+    axes, off = [], 0
+    for n in shape:
+        axes.append(z["axes"][off:off + n])
+        off += n
+    mask = z["mask"] if z["mask"].size else None
+    grid = api.EvaluationGrid(axes, mask)
+    data = api.FunctionalDataset.from_csr(len(shape), z["offsets"], z["coords"], z["values"])
+    mean = api.SurfaceEstimate(grid, api.SurfaceKind.Mean, values=z["mean"])
+    diag = api.SurfaceEstimate(grid, api.SurfaceKind.DiagPlusNoise, values=z["squares"])
+    cov = api.SurfaceEstimate(grid, api.SurfaceKind.Covariance, values=z["cov"])
+    s2 = api.estimate_sigma2(diag, cov, mean)
+    assert bit_equal([s2], z["sigma2"])
+    eig = api.EigenSystem(list(z["eig_values"]), [f for f in z["eig_functions"]], list(z["eig_fve"]),
+                          float(z["eig_total"][0]))
+    integ, warn = api.compute_scores_batch(data, grid, mean, eig, s2, api.ScoreMethod.Integration)
+    assert bit_equal(integ, z["scores_integration"])
+    assert np.array_equal(warn.astype(np.uint8), z["scores_sparse_warning"])
+    if np.max(np.diff(z["offsets"])) <= 160:
+        pace, _ = api.compute_scores_batch(data, grid, mean, eig, s2, api.ScoreMethod.Pace)
+        den = np.maximum(1.0, np.maximum(np.abs(pace), np.abs(z["scores_pace"])))
+        assert np.max(np.abs(pace - z["scores_pace"]) / den) <= 1e-10
+    rec = api.reconstruct_on_grid(mean, eig, z["scores_integration"][0])
+    assert bit_equal(rec, z["reconstruct0"])
+    dense = api.dense_eig(api.matrixize(cov), 3, grid)
+    assert np.allclose(dense.eigenvalues, z["dense_values"], rtol=1e-10, atol=0)

@@ -1066,6 +1066,45 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
     std::vector<std::unique_ptr<DevBuf<double>>> keep;
     auto final_dst = [&](const Orders& o, int bm) -> double* { return tpart.at({o, bm}) + s0 * G; };
     auto final_rs = [&](const Orders&, int) -> i64 { return -1; };
+    if (d == 3) {
+      // d = 3: the fused two-axis kernel on the contiguous (t2, t3) planes --
+      // one plane per (s row, t1), the same passes in the same order as the
+      // tree (t3, then t2) -- then one t1 pass; the t3 / t2 partials never
+      // reach HBM
+      TPhase2Spec ts{};
+      ts.value_only = shared;
+      ts.pw = shared ? nullptr : pw.get() + s0 * G;
+      ts.pv = pv.get() + s0 * G;
+      ts.rows = rows * grid.shape[0];
+      ts.n1 = grid.shape[1];
+      ts.n2 = grid.shape[2];
+      const int mo[6][2] = {{0, 0}, {1, 0}, {2, 0}, {0, 1}, {1, 1}, {0, 2}};
+      const int vo[3][2] = {{0, 0}, {1, 0}, {0, 1}};
+      std::vector<Leaf> planes;
+      std::vector<std::unique_ptr<DevBuf<double>>> plane_bufs;
+      auto add = [&](int budget, int a2, int a3) -> double* {
+        plane_bufs.push_back(std::make_unique<DevBuf<double>>(static_cast<std::size_t>(rows * G)));
+        Leaf l{};
+        l.ord = Orders{};
+        l.ord[4] = a2;
+        l.ord[5] = a3;
+        l.budget_max = budget;
+        l.ptr = plane_bufs.back()->get();
+        planes.push_back(l);
+        return l.ptr;
+      };
+      for (int i = 0; i < 6 && !shared; ++i) ts.mass_out[i] = add(2, mo[i][0], mo[i][1]);
+      for (int i = 0; i < 3; ++i) ts.value_out[i] = add(1, vo[i][0], vo[i][1]);
+      for (int ax = 0; ax < 2; ++ax) {
+        ts.R[ax] = taps[4 + ax].R;
+        for (int r = 0; r < 3; ++r) ts.taps[ax][r] = taps[4 + ax].t[r].data();
+      }
+      if (run_tphase2(ctx, ts)) {
+        const std::vector<TreeAxis> t1ax = {TreeAxis{3, 0}};
+        run_tree(ctx, planes, t1ax, cd, taps, rows * G, taps_dev.get(), keep, final_dst, final_rs, false, -1);
+        continue;
+      }
+    }
     run_tree(ctx, roots, taxes, cd, taps, rows * G, taps_dev.get(), keep, final_dst, final_rs, false,
              -1);
   }

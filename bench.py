@@ -365,10 +365,10 @@ def main():
         dist.destroy_process_group()
 
 
-def tri_fractions(cells: int, R: int, tile: int = 32):
-    """Row fractions of the upper-triangle s-phase (csrc/conv.cu View::tri):
-    for each 32-column t tile, the s2 pass touches s1 < min(n1, s1_out + R)
-    rows, the s1 pass reads those and writes s1 < s1_out rows; the solve and
+def tri_fractions(cells: int, R: int, tile: int = 64):
+    """Row fractions of the upper-triangle s-phase (csrc/conv.cuh View::tri):
+    for each column tile, the s1 pass reads s1 < min(n1, s1_out + R) rows and
+    writes s1 < s1_out rows, the in-plane pass works on those; the solve and
     the centering touch s <= t."""
     n1 = cells
     G = cells * cells
@@ -391,8 +391,8 @@ def kernel_model(G: int, n_pair: int, shared: bool):
             k_rank_one    pw = W M(s) M(t): write 1 array          -> HBM
             k_scale_rows  w_i V_i: read + write n G doubles
     t-phase k_tphase2     read pw, pv; write 9 t-partials: 11 arrays
-    s-phase k_pass_cols   s2 level: 9 in + 14 out over the trimmed rows;
-                          s1 level: 14 in (trimmed rows) + 20 out (s <= t rows)
+    s-phase k_pass_cols   s1 pass first: 9 in (rows s1 < s1_out + R) + 14 out
+                          (rows s1 < s1_out); s2 pass: 14 in + 20 out on those rows
     solve   k_solve       20 moments in + 1 out at s <= t
     center  k_center_mirror  read s <= t, write both triangles
 
@@ -400,7 +400,7 @@ def kernel_model(G: int, n_pair: int, shared: bool):
     the bench's GridNodes workload): the mass moments are closed-form
     (k_solve_shared), pw is never built, only pv is convolved:
     t-phase   read pv, write 3 value t-partials              4 arrays
-    s-phase   s2: 3 in + 4 out (trimmed rows); s1: 4 in + 5 out (s <= t rows)
+    s-phase   s1: 3 in (trimmed + R rows) + 4 out; s2: 4 in + 5 out (s <= t rows)
     solve     5 value moments in + 1 out at s <= t
     """
     cells = int(round(G ** 0.5))
@@ -411,7 +411,7 @@ def kernel_model(G: int, n_pair: int, shared: bool):
             "k_gemm_tn": ("tensor", 2.0 * n_pair * G * G / 2.0),
             "k_scale_rows": ("hbm", 2 * 8.0 * n_pair * G),
             "k_tphase2": ("hbm", 4 * arr),
-            "k_pass_cols": ("hbm", ((3 + 4) * f_in + 4 * f_in + 5 * f_out) * arr),
+            "k_pass_cols": ("hbm", (3 * f_in + 4 * f_out + (4 + 5) * f_out) * arr),
             "k_solve_shared_tri": ("hbm", 6 * upper * arr),
             "k_center_mirror": ("hbm", (upper + 1.0) * arr),
         }
@@ -420,7 +420,7 @@ def kernel_model(G: int, n_pair: int, shared: bool):
         "k_rank_one": ("hbm", 1 * arr),
         "k_scale_rows": ("hbm", 2 * 8.0 * n_pair * G),
         "k_tphase2": ("hbm", 11 * arr),
-        "k_pass_cols": ("hbm", ((9 + 14) * f_in + 14 * f_in + 20 * f_out) * arr),
+        "k_pass_cols": ("hbm", (9 * f_in + 14 * f_out + (14 + 20) * f_out) * arr),
         "k_solve_tri": ("hbm", 21 * upper * arr),
         "k_center_mirror": ("hbm", (upper + 1.0) * arr),
     }

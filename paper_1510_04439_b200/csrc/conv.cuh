@@ -21,7 +21,9 @@ struct View {
   //   tri = 1: pass along s2 (outer = s1): skip s1 rows beyond those the s1
   //            pass of the same t columns will read;
   //   tri = 2: pass along s1 (inner = s2 * tri_G + t): read s1 < s1_out + R,
-  //            write s1 < s1_out, s1_out = t_max / tri_rn + 1.
+  //            write s1 < s1_out, s1_out = t_max / tri_rn + 1;
+  //   tri = 3: pass along s2 after the s1 pass (outer = s1): only the
+  //            planes s1 < s1_out.
   int tri = 0;
   int tri_R = 0;
   i64 tri_G = 0;   // t extent

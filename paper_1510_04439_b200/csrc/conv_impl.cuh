@@ -139,6 +139,8 @@ __global__ void __launch_bounds__(kThreads) k_pass_cols(View in, View o0, View o
       if (tri == 1) {
         const int s1_in = s1_out + triR < tri_n1 ? s1_out + triR : tri_n1;
         if (mt.ob >= s1_in) mt.rows = mt.nout = 0;
+      } else if (tri == 3) {  // in-plane pass after the s1 pass: output planes only
+        if (mt.ob >= s1_out) mt.rows = mt.nout = 0;
       } else {
         mt.nout = s1_out < n ? s1_out : n;
         mt.rows = mt.nout + triR < n ? mt.nout + triR : n;

@@ -25,7 +25,6 @@
 #include <string>
 
 #include "conv.cuh"
-#include "s1solve.cuh"
 #include "solve.cuh"
 
 namespace dfpca_gpu {
@@ -114,6 +113,11 @@ struct ChunkDims {
   // covariance slab); win_k < 0: none
   int win_k = -1;
   i64 win_lo = 0, win_hi = -1;
+  // s-phase order s1, then the in-plane axes: the first pass reads roots
+  // whose axis is the outermost memory dimension ([s1][rest][cols]) and
+  // writes compact [s1][rest][cols] buffers; with a window on axis 0 the
+  // later passes cover only the written planes [win_lo, win_hi)
+  bool axis0_first = false;
 };
 
 View make_view(double* p, const ChunkDims& cd, int k, i64 row_stride_override = -1) {
@@ -626,15 +630,6 @@ SolveLauncher solve_launcher(int p) {
   }
 }
 
-// Workspace arena of full-chunk arrays.
-struct Arena {
-  std::vector<std::unique_ptr<DevBuf<double>>> bufs;
-  double* get(std::size_t n) {
-    bufs.push_back(std::make_unique<DevBuf<double>>(n));
-    return bufs.back()->get();
-  }
-};
-
 // Runs the passes of a tree over `axes` (indices into cd.shape, processed in
 // the given order) starting from `roots`; the final level's arrays are
 // returned (keyed by full orders).  Intermediate levels live in `arena`;
@@ -659,31 +654,45 @@ std::vector<Leaf> run_tree(dfpca_context* ctx, const std::vector<Leaf>& roots,
                            const std::function<i64(const Orders&, int)>& final_row_stride,
                            bool first_reads_strided, i64 first_row_stride) {
   std::vector<Leaf> cur = roots;
+  // axis0_first with a window: levels after the first see planes [lo, hi)
+  const bool narrow = cd.axis0_first && cd.win_k == 0 && cd.win_hi >= 0;
+  ChunkDims cd_rest = cd;
+  i64 off_rest = 0;
+  if (narrow) {
+    i64 plane = cd.tail;
+    for (std::size_t a = 1; a < cd.shape.size(); ++a) plane *= cd.shape[a];
+    off_rest = cd.win_lo * plane;
+    cd_rest.shape[0] = std::max<i64>(0, cd.win_hi - cd.win_lo);
+    cd_rest.tri_params.tri_row0 += cd.win_lo;
+    cd_rest.win_k = -1;
+  }
   for (std::size_t ai = 0; ai < axes.size(); ++ai) {
     const TreeAxis& ax = axes[ai];
     const bool last = ai + 1 == axes.size();
+    const ChunkDims& cdl = (narrow && ai >= 1) ? cd_rest : cd;
+    const i64 off = (narrow && ai >= 1) ? off_rest : 0;
     std::vector<Leaf> next;
     std::vector<std::unique_ptr<DevBuf<double>>> level_bufs;
     for (const Leaf& in : cur) {
       const int used = order_sum(in.ord);
       const int n_out = in.budget_max - used + 1;
       PassSpec spec{};
-      spec.in = (ai == 0 && first_reads_strided) ? make_view(in.ptr, cd, ax.view_k, first_row_stride)
-                                                 : make_view(in.ptr, cd, ax.view_k);
+      spec.in = (ai == 0 && first_reads_strided) ? make_view(in.ptr, cdl, ax.view_k, first_row_stride)
+                                                 : make_view(in.ptr + off, cdl, ax.view_k);
       if (ai == 0 && first_reads_strided) spec.in = in.view;
-      if (ai < cd.tri.size() && cd.tri[ai]) {
-        spec.in.tri = cd.tri[ai];
-        spec.in.tri_R = cd.tri_params.tri_R;
-        spec.in.tri_G = cd.tri_params.tri_G;
-        spec.in.tri_rn = cd.tri_params.tri_rn;
-        spec.in.tri_n1 = cd.tri_params.tri_n1;
-        spec.in.tri_row0 = cd.tri_params.tri_row0;
-        spec.in.tri_row_hi = cd.tri_params.tri_row_hi;
-        spec.in.tri_t0 = cd.tri_params.tri_t0;
+      if (ai < cdl.tri.size() && cdl.tri[ai]) {
+        spec.in.tri = cdl.tri[ai];
+        spec.in.tri_R = cdl.tri_params.tri_R;
+        spec.in.tri_G = cdl.tri_params.tri_G;
+        spec.in.tri_rn = cdl.tri_params.tri_rn;
+        spec.in.tri_n1 = cdl.tri_params.tri_n1;
+        spec.in.tri_row0 = cdl.tri_params.tri_row0;
+        spec.in.tri_row_hi = cdl.tri_params.tri_row_hi;
+        spec.in.tri_t0 = cdl.tri_params.tri_t0;
       }
-      if (ax.view_k == cd.win_k) {
-        spec.in.lo = cd.win_lo;
-        spec.in.hi = cd.win_hi;
+      if (ax.view_k == cdl.win_k) {
+        spec.in.lo = cdl.win_lo;
+        spec.in.hi = cdl.win_hi;
       }
       spec.n_out = n_out;
       spec.R = taps[ax.axis_index].R;
@@ -701,7 +710,19 @@ std::vector<Leaf> run_tree(dfpca_context* ctx, const std::vector<Leaf>& roots,
           rs = final_row_stride(o.ord, o.budget_max);
         }
         o.ptr = dst;
-        spec.out[r] = make_view(dst, cd, ax.view_k, rs);
+        if (ai == 0 && cd.axis0_first) {
+          // compact [n][outer][inner]: the axis outermost, as the roots
+          View v = spec.in;
+          v.p = dst;
+          v.os = v.inner;
+          v.js = v.outer * v.inner;
+          v.tri = 0;
+          v.lo = 0;
+          v.hi = -1;
+          spec.out[r] = v;
+        } else {
+          spec.out[r] = make_view(dst + off, cdl, ax.view_k, rs);
+        }
         o.view = spec.out[r];
         spec.taps[r] = taps[ax.axis_index].t[r].data();
         next.push_back(o);
@@ -839,7 +860,6 @@ void run_local_linear(dfpca_context* ctx, const dfpca_binned* b, const Grid& gri
 // Pair grids + moments + solve + center + symmetrize for the covariance.
 void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid, const double* h,
                          const double* mean_host, const CovShardExec* shard, dfpca_surface** out) {
-  static const bool use_fused_s1 = std::getenv("DFPCA_FUSED_S1") != nullptr;  // experimental, one device
   const int d = grid.d;
   const int p = 2 * d;
   const i64 G = grid.G;
@@ -1129,8 +1149,10 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
   // output row, reads its local planes [ha, hb) and writes planes [sa, sb).
   const i64 R0 = taps[0].R;
   i64 tc = std::max<i64>(1, std::min<i64>(G, budget_elems / std::max<i64>(G, 1) / 4));
+  // s1 first, then the in-plane axes: the in-plane passes then cover only
+  // the output planes (the s1 pass reads the R extra planes once)
   std::vector<TreeAxis> saxes;
-  for (int k = d - 1; k >= 0; --k) saxes.push_back({k, k});
+  for (int k = 0; k < d; ++k) saxes.push_back({k, k});
   for (i64 t0 = col_lo; t0 < G && sa < sb; t0 += tc) {
     const i64 cols = std::min(tc, G - t0);
     const i64 s1_out = std::min<i64>(sb, (t0 + cols - 1) / rn + 1) - ha;  // local end of output planes
@@ -1144,7 +1166,7 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
     cd.shape[0] = s1_in;
     cd.tail = cols;
     if (tri_tiles) {
-      cd.tri = {1, 2};  // s2 pass, then s1 pass
+      cd.tri = {2, 3};  // s1 pass, then the s2 pass over the output planes
       cd.tri_params.tri_R = static_cast<int>(R0);
       cd.tri_params.tri_G = cols;
       cd.tri_params.tri_rn = rn;
@@ -1153,14 +1175,14 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
       cd.tri_params.tri_row_hi = sb;
       cd.tri_params.tri_t0 = t0;
     }
-    if (sharded) {  // the s1 pass writes the slab's own planes only
-      cd.win_k = 0;
-      cd.win_lo = sa - ha;
-      cd.win_hi = s1_out;
-    }
+    // the s1 pass writes the output planes [sa, s1_out) only (a slab's own)
+    cd.win_k = 0;
+    cd.win_lo = sa - ha;
+    cd.win_hi = s1_out;
+    cd.axis0_first = true;
     const i64 chunk_elems = s1_in * rn * cols;
-    // roots: the t-partials viewed as [s1 < s1_in][s2..][cols] with row stride G;
-    // the first pass runs along the last s-axis
+    // roots: the t-partials viewed along s1 (planes s1 < s1_in, stride rn * G),
+    // outer = the in-plane s nodes (stride G), inner = the chunk's columns
     std::vector<Leaf> roots;
     for (auto& kv : tpart) {
       Leaf r;
@@ -1169,11 +1191,11 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
       r.ptr = kv.second + t0;
       View v;
       v.p = r.ptr;
-      v.n = d == 1 ? s1_in : grid.shape[d - 1];  // d = 1: the first pass is the truncated s1 axis
-      v.js = G;
+      v.n = s1_in;
+      v.js = rn * G;
+      v.outer = rn;
+      v.os = G;
       v.inner = cols;
-      v.outer = d == 1 ? 1 : s1_in * rn / grid.shape[d - 1];
-      v.os = v.n * G;
       r.view = v;
       roots.push_back(r);
     }
@@ -1199,52 +1221,8 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
       int nch = 0;
       if (tri_ctas(sg, nch) < 0) fail(kConfig, "InvalidArgument", "covariance slab too large for the tiled solve");
     }
-    std::vector<Leaf> leaves;
-    if (d == 2) {
-      // s2 pass, then the fused s1 pass + solve (s1solve.cu): the 20 moment
-      // arrays of the chunk never reach HBM
-      std::vector<TreeAxis> s2ax = {saxes[0]};
-      std::vector<Leaf> l2 = run_tree(ctx, roots, s2ax, cd, taps, chunk_elems, taps_dev.get(), keep, final_dst,
-                                      final_rs, true, -1);
-      S1SolveSpec sp{};
-      bool ok = !sharded;
-      const auto order = s1_p4_input_order();
-      for (std::size_t k = 0; k < order.size(); ++k) {
-        const double* ptr = nullptr;
-        for (const Leaf& l : l2)
-          if (l.budget_max == order[k][0] && l.ord[0] == 0 && l.ord[1] == order[k][1] &&
-              l.ord[2] == order[k][2] && l.ord[3] == order[k][3])
-            ptr = l.ptr;
-        ok = ok && ptr != nullptr;
-        sp.in[k] = ptr;
-      }
-      sp.n = s1_in;
-      sp.s2n = grid.shape[1];
-      sp.inner = grid.shape[1] * cols;
-      sp.cols = cols;
-      sp.t0 = t0;
-      sp.G = G;
-      sp.R = R0;
-      for (int r = 0; r < 3; ++r) sp.taps[r] = taps[0].t[r].data();
-      sp.mask = grid.has_mask ? mask_dev.get() : nullptr;
-      sp.out = surf->values.get();
-      sp.cnt = cnt.get();
-      sp.list = list.get();
-      sp.cap = list_cap;
-      ctx->end_stage();
-      ctx->begin_stage("solve");
-      // the fused s1 pass + solve is latency-bound at its occupancy on B200;
-      // the split s1 pass + k_solve is faster until it is reworked
-      const bool fused = ok && use_fused_s1 && run_s1_solve_p4(ctx, sp);
-      ctx->end_stage();
-      ctx->begin_stage("moments");
-      if (fused) continue;
-      std::vector<TreeAxis> s1ax = {saxes[1]};
-      leaves = run_tree(ctx, l2, s1ax, cd, taps, chunk_elems, taps_dev.get(), keep, final_dst, final_rs, false, -1);
-    } else {
-      leaves = run_tree(ctx, roots, saxes, cd, taps, chunk_elems, taps_dev.get(), keep, final_dst, final_rs, true,
-                        -1);
-    }
+    std::vector<Leaf> leaves =
+        run_tree(ctx, roots, saxes, cd, taps, chunk_elems, taps_dev.get(), keep, final_dst, final_rs, true, -1);
     MomPtrs mp{};
     for (const Leaf& l : leaves) {
       const int idx = basis.find(l.ord);

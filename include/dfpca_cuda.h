@@ -148,6 +148,10 @@ DFPCA_API int dfpca_covariance(dfpca_context* ctx, const dfpca_binned* b, const 
  * libnccl.so.2 is loaded at run time (DFPCA_NCCL_LIB overrides the path). */
 DFPCA_API int dfpca_nccl_unique_id(void* id128);
 DFPCA_API int dfpca_nccl_init(dfpca_context* ctx, int world, int rank, const void* id128);
+/* Drives the NCCL transport of a sharded run on a one-rank communicator
+ * (grouped send/recv to itself, all-gather, max all-reduce) and reports the
+ * mismatching elements: checks the run-time libnccl binding on one GPU. */
+DFPCA_API int dfpca_nccl_selftest(dfpca_context* ctx, int64_t* mismatches);
 /* Collective over the ranks of dfpca_nccl_init (same arguments on every rank;
  * binned data and mean are replicated).  *out receives this rank's slab:
  * complete, exactly symmetric rows [row0, row0 + rows) of the covariance

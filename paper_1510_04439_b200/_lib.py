@@ -63,6 +63,7 @@ SIGNATURES = [
     ("dfpca_dense_eig", C.c_int, [P, P, C.POINTER(DfpcaGrid), C.c_int64, PD, PD, PD, PD, PI64]),
     ("dfpca_nccl_unique_id", C.c_int, [P]),
     ("dfpca_nccl_init", C.c_int, [P, C.c_int, C.c_int, P]),
+    ("dfpca_nccl_selftest", C.c_int, [P, PI64]),
     ("dfpca_covariance_sharded", C.c_int, [P, P, C.POINTER(DfpcaGrid), PD, PD, C.POINTER(DfpcaPlan),
                                            C.POINTER(P)]),
     ("dfpca_covariance_emulated", C.c_int, [P, P, C.POINTER(DfpcaGrid), PD, PD, C.POINTER(DfpcaPlan), C.c_int,

@@ -46,6 +46,7 @@ void nccl_unique_id(void* out);
 void run_covariance_dryrun(dfpca_context* ctx, int world, int rank, const dfpca_binned* b, const Grid& grid,
                            const double* h, const double* mean_host, dfpca_surface** out);
 std::shared_ptr<Transport> make_nccl_transport(int world, int rank, const void* id);
+i64 nccl_selftest(dfpca_context* ctx);
 void run_estimate_sigma2(dfpca_context* ctx, const Grid& grid, const double* diag_plus_noise,
                          const dfpca_surface* cov, const double* mean, double* sigma2);
 void run_scores(dfpca_context* ctx, const Grid& grid, i64 n, const i64* offsets, const double* coords,
@@ -613,6 +614,13 @@ int dfpca_nccl_unique_id(void* id) {
   } catch (const Failure& e) {
     return e.cls;
   }
+}
+
+int dfpca_nccl_selftest(dfpca_context* ctx, int64_t* mismatches) {
+  return guarded(ctx, [&] {
+    const i64 bad = nccl_selftest(ctx);
+    if (mismatches) *mismatches = bad;
+  });
 }
 
 int dfpca_nccl_init(dfpca_context* ctx, int world, int rank, const void* id) {

@@ -25,7 +25,10 @@ namespace {
 
 constexpr int BM = 64, BN = 64, BK = 16;
 constexpr int LDS = BM + 4;
-constexpr int WM = 32, WN = 32;
+#ifndef DFPCA_GEMM_WM
+#define DFPCA_GEMM_WM 32
+#endif
+constexpr int WM = DFPCA_GEMM_WM, WN = 32;
 constexpr int MT = WM / 8, NT = WN / 8;
 constexpr int WARPS_N = BN / WN;
 constexpr int NTHREADS = 32 * (BM / WM) * WARPS_N;

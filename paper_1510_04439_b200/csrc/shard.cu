@@ -575,4 +575,34 @@ std::shared_ptr<Transport> make_nccl_transport(int world, int rank, const void* 
   return std::make_shared<NcclTransport>(world, rank, id);
 }
 
+// One-rank NCCL communicator driving the same transport calls as a sharded
+// run (grouped send/recv to itself, all-gather, max all-reduce) on the
+// context stream: checks the run-time binding of libnccl on a one-GPU box.
+// Returns the number of mismatching elements (0 = pass).
+i64 nccl_selftest(dfpca_context* ctx) {
+  NcclApi::UniqueId id;
+  NcclApi& api = NcclApi::get();
+  api.check(api.GetUniqueId(&id), "ncclGetUniqueId");
+  NcclTransport tr(1, 0, id.internal);
+  const i64 n = 1 << 16;
+  std::vector<double> h(static_cast<std::size_t>(n));
+  for (i64 i = 0; i < n; ++i) h[static_cast<std::size_t>(i)] = 0.5 * static_cast<double>(i) - 7.0;
+  DevBuf<double> a(n), b(n), c(n);
+  DFPCA_CUDA(cudaMemcpyAsync(a.get(), h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  DFPCA_CUDA(cudaMemsetAsync(b.get(), 0, sizeof(double) * n, ctx->stream));
+  DFPCA_CUDA(cudaMemsetAsync(c.get(), 0, sizeof(double) * n, ctx->stream));
+  tr.exchange(ctx, {Transport::Msg{0, a.get(), n}}, {Transport::Msg{0, b.get(), n}});
+  tr.all_gather(ctx, b.get(), c.get(), n);
+  const unsigned long long m = tr.max_u64(ctx, 12345ull);
+  std::vector<double> hb(static_cast<std::size_t>(n)), hc(static_cast<std::size_t>(n));
+  DFPCA_CUDA(cudaMemcpyAsync(hb.data(), b.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  DFPCA_CUDA(cudaMemcpyAsync(hc.data(), c.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+  i64 bad = m == 12345ull ? 0 : 1;
+  for (i64 i = 0; i < n; ++i)
+    bad += (hb[static_cast<std::size_t>(i)] != h[static_cast<std::size_t>(i)]) +
+           (hc[static_cast<std::size_t>(i)] != h[static_cast<std::size_t>(i)]);
+  return bad;
+}
+
 }  // namespace dfpca_gpu

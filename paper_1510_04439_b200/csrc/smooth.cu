@@ -408,8 +408,11 @@ __global__ void __launch_bounds__(kSolveTile) k_solve_tri(MomPtrs mp, SolveGeom 
                                                           i64* __restrict__ empty_list, i64 list_cap) {
   solve_tri_body<N, false>(SharedMoments{}, mp, g, nch, out, empty_count, empty_list, list_cap);
 }
+#ifndef DFPCA_SOLVE_MIN_CTAS
+#define DFPCA_SOLVE_MIN_CTAS 1
+#endif
 template <int N>
-__global__ void __launch_bounds__(kSolveTile)
+__global__ void __launch_bounds__(kSolveTile, DFPCA_SOLVE_MIN_CTAS)
     k_solve_shared_tri(SharedMoments sh, MomPtrs mp, SolveGeom g, int nch, double* __restrict__ out,
                        unsigned long long* __restrict__ empty_count, i64* __restrict__ empty_list, i64 list_cap) {
   solve_tri_body<N, true>(sh, mp, g, nch, out, empty_count, empty_list, list_cap);

@@ -119,3 +119,14 @@ def test_sharded_randomized_eig_bit_identical(api, case, world):
     assert bit_equal(many.eigenvalues, one.eigenvalues)
     assert bit_equal(np.concatenate(many.eigenfunctions), np.concatenate(one.eigenfunctions))
     assert many.fve == one.fve and many.total_variance == one.total_variance
+
+
+def test_nccl_transport_binding(api):
+    """The NCCL transport (libnccl loaded at run time) on a one-rank
+    communicator: grouped send/recv, all-gather and the max all-reduce move the
+    data unchanged.  (Multi-rank NCCL needs one GPU per rank.)"""
+    import ctypes as C
+    from paper_1510_04439_b200 import _lib
+    bad = C.c_int64(-1)
+    _lib.check(_lib.lib().dfpca_nccl_selftest(_lib.ctx(), C.byref(bad)))
+    assert bad.value == 0

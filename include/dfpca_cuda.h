@@ -38,6 +38,7 @@ extern "C" {
 typedef struct dfpca_context dfpca_context;
 typedef struct dfpca_binned dfpca_binned;
 typedef struct dfpca_surface dfpca_surface;
+typedef struct dfpca_dataset dfpca_dataset;
 
 /* Grid descriptor: the data an EvaluationGrid carries (grid.hpp:92-230).
  * axes[k] points at shape[k] strictly increasing node coordinates (host).
@@ -249,6 +250,28 @@ DFPCA_API int dfpca_scores(dfpca_context* ctx, const dfpca_grid* grid, int64_t n
  * (n*L); out: n*G (NaN outside). */
 DFPCA_API int dfpca_reconstruct(dfpca_context* ctx, const dfpca_grid* grid, const double* mean, int64_t L,
                       const double* eigenfunctions, int64_t n, const double* scores, double* out);
+
+/* ---- bandwidth selection: the CV objective -------- */
+/* Observations kept on the device across objective evaluations (CSR as
+ * dfpca_linear_bin). */
+DFPCA_API int dfpca_dataset_upload(dfpca_context* ctx, int dim, int64_t n_samples, const int64_t* obs_offsets,
+                         const double* coords, const double* values, dfpca_dataset** out);
+DFPCA_API int dfpca_dataset_free(dfpca_dataset* ds);
+/* CvObjective's evaluation units (bandwidth.hpp:118-140): target 0 = mean,
+ * 1 = covariance, 2 = diag (squares); every observation, or every ordered
+ * pair j != l, then a seeded partial Fisher-Yates keeping max_units.  Host
+ * only; 3 int64 per unit (sample, j, l); *count = the unit count (call with
+ * capacity 0 to size the buffer). */
+DFPCA_API int dfpca_cv_units(int64_t n_samples, const int64_t* obs_offsets, int target, int64_t max_units,
+                   uint64_t seed, int64_t* units, int64_t capacity, int64_t* count);
+/* Replaces CvObjective::operator() / cv_score (bandwidth.hpp:74-115, 164):
+ * one direct local-linear fit per unit (smoother.hpp:376-407, ridge pinned at
+ * 0) on the device, leave-one-out residuals by the self-influence shortcut,
+ * mean over the usable units.  grid gives the extents h is validated against
+ * (InvalidBandwidth); BandwidthTooSmall when no unit is usable. */
+DFPCA_API int dfpca_cv_objective(dfpca_context* ctx, const dfpca_dataset* ds, const dfpca_grid* grid, int target,
+                       int64_t n_units, const int64_t* units, const double* h, double* score,
+                       int64_t* used_units);
 
 #ifdef __cplusplus
 }

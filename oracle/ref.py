@@ -44,6 +44,8 @@ _SIG = {
     "ref_scores": (C.c_int, [C.c_int, PI, PD, PU8, C.c_int64, PI, PD, PD, PD, C.c_int64, PD, PD, C.c_double,
                              C.c_int, PD, C.POINTER(C.c_int)]),
     "ref_reconstruct": (C.c_int, [C.c_int, PI, PD, PU8, PD, C.c_int64, PD, PD, PD, PD]),
+    "ref_cv_score": (C.c_int, [C.c_int, PI, PD, PU8, C.c_int64, PI, PD, PD, C.c_int, C.c_int64, C.c_uint64, PD, PD,
+                               PI]),
 }
 
 _lib = None
@@ -310,3 +312,19 @@ def reconstruct_on_grid(grid, mean, evals, efuncs, sc) -> np.ndarray:
     out = np.empty(ga.G)
     _chk(lib().ref_reconstruct(*ga.args(), mp, ev.size, evp, efp, spp, out.ctypes.data_as(PD)))
     return out
+
+
+def cv_score(grid, offsets, coords, values, target: int, h, max_units: int = 2000, seed: int = 0x5EED):
+    """CvObjective(data, grid, target, {max_units, seed}) evaluated at h
+    (bandwidth.hpp:56-163); target 0 mean, 1 covariance, 2 diag.
+    Returns (score, n_units)."""
+    ga = grid_args(grid)
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    c, cp = _d(coords)
+    v, vp = _d(values)
+    hh, hp = _d(h)
+    out = C.c_double()
+    nu = C.c_int64()
+    _chk(lib().ref_cv_score(*ga.args(), off.size - 1, off.ctypes.data_as(PI), cp, vp, int(target), int(max_units),
+                            C.c_uint64(seed), hp, C.byref(out), C.byref(nu)))
+    return out.value, nu.value

@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "dfpca/bandwidth.hpp"
 #include "dfpca/binning.hpp"
 #include "dfpca/dataset.hpp"
 #include "dfpca/eigensolve.hpp"
@@ -350,6 +351,23 @@ int ref_reconstruct(int dim, const int64_t* shape, const double* axes, const uin
     FpcaModel m = make_model(dim, shape, axes, mask, mean, L, evals, efuncs, 0.0);
     const auto r = reconstruct_on_grid(m, std::vector<double>(sc, sc + L));
     std::memcpy(out, r.data(), sizeof(double) * r.size());
+  });
+}
+
+// ---- the CV bandwidth objective (bandwidth.hpp:56-163) ----
+// target 0 = mean, 1 = covariance, 2 = diag (squares)
+int ref_cv_score(int dim, const int64_t* shape, const double* axes, const uint8_t* mask, int64_t n,
+                 const int64_t* offsets, const double* coords, const double* values, int target, int64_t max_units,
+                 uint64_t seed, const double* h, double* out, int64_t* n_units) {
+  return guarded([&] {
+    EvaluationGrid g = make_grid(dim, shape, axes, mask);
+    FunctionalDataset data = make_data(dim, n, offsets, coords, values);
+    const CvTarget t = target == 0 ? CvTarget::Mean : target == 1 ? CvTarget::Covariance : CvTarget::DiagPlusNoise;
+    CvObjective obj(data, g, t, CvOptions{static_cast<std::size_t>(max_units), seed});
+    Bandwidth bw;
+    bw.h.assign(h, h + dim);
+    *out = cv_score(bw, obj);
+    if (n_units) *n_units = static_cast<int64_t>(obj.n_units());
   });
 }
 

@@ -73,6 +73,10 @@ SIGNATURES = [
     ("dfpca_fpca_emulated", C.c_int, [P, P, C.POINTER(DfpcaGrid), PD, PD, C.c_int, C.c_int64, C.c_int64, C.c_uint64,
                                       PD, PD, PD, PD, PI64, C.POINTER(C.c_int)]),
     ("dfpca_surface_rows", C.c_int, [P, PI64, PI64]),
+    ("dfpca_dataset_upload", C.c_int, [P, C.c_int, C.c_int64, PI64, PD, PD, C.POINTER(P)]),
+    ("dfpca_dataset_free", C.c_int, [P]),
+    ("dfpca_cv_units", C.c_int, [C.c_int64, PI64, C.c_int, C.c_int64, C.c_uint64, PI64, C.c_int64, PI64]),
+    ("dfpca_cv_objective", C.c_int, [P, P, C.POINTER(DfpcaGrid), C.c_int, C.c_int64, PI64, PD, PD, PI64]),
     ("dfpca_estimate_sigma2", C.c_int, [P, C.POINTER(DfpcaGrid), PD, P, PD, PD]),
     ("dfpca_scores", C.c_int, [P, C.POINTER(DfpcaGrid), C.c_int64, PI64, PD, PD, PD, C.c_int64, PD, PD, C.c_double,
                                C.c_int, PD, C.POINTER(C.c_int32)]),

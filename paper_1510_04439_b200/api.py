@@ -970,3 +970,80 @@ def reconstruct_on_grid(mean: SurfaceEstimate, eig: EigenSystem, scores) -> np.n
                                        ef.ctypes.data_as(PDd), s.shape[0], s.ctypes.data_as(PDd),
                                        out.ctypes.data_as(PDd)))
     return out if one else out.reshape(s.shape[0], grid.size())
+
+
+# ------------------------------------ bandwidth selection: CV (8(f)) ----
+# reference bandwidth.hpp: CvObjective / cv_score; the fits run on the device.
+
+
+class CvTarget(Enum):
+    """bandwidth.hpp:27"""
+    Mean = 0
+    Covariance = 1
+    DiagPlusNoise = 2
+
+
+class CvObjective:
+    """bandwidth.hpp:56-163: leave-one-observation-out CV objective of one
+    smoothing target.  Units are fixed at construction (a seeded subsample of
+    at most max_units observations or ordered pairs); the dataset stays on the
+    device; calling the objective runs one direct local fit per unit there."""
+
+    kSelfOnlyTol = 1e-6
+    kDenomClamp = 1e-8
+
+    def __init__(self, data: FunctionalDataset, grid: EvaluationGrid, target: CvTarget, max_units: int = 2000,
+                 seed: int = 0x5EED):
+        offsets, coords, values = data.csr()
+        self._grid = grid
+        self.target = target
+        cnt = C.c_int64()
+        PI = C.POINTER(C.c_int64)
+        st = _lib.lib().dfpca_cv_units(len(data.samples), offsets.ctypes.data_as(PI), target.value, int(max_units),
+                                       C.c_uint64(seed), None, 0, C.byref(cnt))
+        if st != 0:
+            raise Error(ErrorClass.Config, "InvalidArgument", "cross-validation needs at least one evaluation unit")
+        self.units = np.zeros((cnt.value, 3), dtype=np.int64)
+        _lib.lib().dfpca_cv_units(len(data.samples), offsets.ctypes.data_as(PI), target.value, int(max_units),
+                                  C.c_uint64(seed), self.units.ctypes.data_as(PI), cnt.value, C.byref(cnt))
+        h = C.c_void_p()
+        PDd = C.POINTER(C.c_double)
+        check(_lib.lib().dfpca_dataset_upload(_lib.ctx(), data.dim, len(data.samples), offsets.ctypes.data_as(PI),
+                                              coords.ctypes.data_as(PDd) if coords.size else None,
+                                              values.ctypes.data_as(PDd) if values.size else None, C.byref(h)))
+        self._h = h
+        self.last_used = 0
+
+    def __del__(self):
+        try:
+            if self._h:
+                _lib.lib().dfpca_dataset_free(self._h)
+        except Exception:
+            pass
+
+    def dim(self) -> int:
+        return self._grid.dim()
+
+    def n_units(self) -> int:
+        return int(self.units.shape[0])
+
+    def extents(self):
+        return [self._grid.axis(k)[-1] - self._grid.axis(k)[0] for k in range(self._grid.dim())]
+
+    def __call__(self, h: Bandwidth) -> float:
+        hh = h.arr()
+        if hh.size != self.dim():
+            raise Error(ErrorClass.Config, "InvalidBandwidth", "bandwidth dimension mismatch")
+        out = C.c_double()
+        used = C.c_int64()
+        check(_lib.lib().dfpca_cv_objective(_lib.ctx(), self._h, C.byref(self._grid.desc()), self.target.value,
+                                            self.n_units(), self.units.ctypes.data_as(C.POINTER(C.c_int64)),
+                                            hh.ctypes.data_as(C.POINTER(C.c_double)), C.byref(out),
+                                            C.byref(used)))
+        self.last_used = used.value
+        return out.value
+
+
+def cv_score(h: Bandwidth, obj: CvObjective) -> float:
+    """bandwidth.hpp:164."""
+    return obj(h)

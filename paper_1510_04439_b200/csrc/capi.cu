@@ -47,6 +47,11 @@ void run_covariance_dryrun(dfpca_context* ctx, int world, int rank, const dfpca_
                            const double* h, const double* mean_host, dfpca_surface** out);
 std::shared_ptr<Transport> make_nccl_transport(int world, int rank, const void* id);
 i64 nccl_selftest(dfpca_context* ctx);
+dfpca_dataset* upload_dataset(dfpca_context* ctx, int dim, i64 n, const i64* offsets, const double* coords,
+                              const double* values);
+std::vector<i64> cv_units(i64 n_samples, const i64* offsets, int target, i64 max_units, std::uint64_t seed);
+double run_cv_objective(dfpca_context* ctx, const dfpca_dataset* ds, int target, i64 n_units, const i64* units,
+                        const double* h, i64* used_out);
 void run_estimate_sigma2(dfpca_context* ctx, const Grid& grid, const double* diag_plus_noise,
                          const dfpca_surface* cov, const double* mean, double* sigma2);
 void run_scores(dfpca_context* ctx, const Grid& grid, i64 n, const i64* offsets, const double* coords,
@@ -739,6 +744,50 @@ int dfpca_reconstruct(dfpca_context* ctx, const dfpca_grid* grid, const double* 
     if (!mean || L < 0 || n < 0 || (L > 0 && (!eigenfunctions || (n > 0 && !scores))) || (n > 0 && !out))
       fail(kConfig, "InvalidArgument", "invalid reconstruction request");
     run_reconstruct(ctx, g, mean, L, eigenfunctions, n, scores, out);
+  });
+}
+
+int dfpca_dataset_upload(dfpca_context* ctx, int dim, int64_t n_samples, const int64_t* obs_offsets,
+                         const double* coords, const double* values, dfpca_dataset** out) {
+  return guarded(ctx, [&] {
+    if (!out || dim < 1 || dim > DFPCA_MAX_DIM || n_samples < 0 || !obs_offsets)
+      fail(kConfig, "InvalidArgument", "invalid dataset");
+    for (i64 i = 0; i < n_samples; ++i)
+      if (obs_offsets[i + 1] < obs_offsets[i] || obs_offsets[0] != 0)
+        fail(kConfig, "InvalidArgument", "observation offsets must be nondecreasing from 0");
+    if (obs_offsets[n_samples] > 0 && (!coords || !values)) fail(kConfig, "InvalidArgument", "null observations");
+    *out = upload_dataset(ctx, dim, n_samples, obs_offsets, coords, values);
+  });
+}
+
+int dfpca_dataset_free(dfpca_dataset* ds) {
+  delete ds;
+  return 0;
+}
+
+int dfpca_cv_units(int64_t n_samples, const int64_t* obs_offsets, int target, int64_t max_units, uint64_t seed,
+                   int64_t* units, int64_t capacity, int64_t* count) {
+  if (n_samples < 0 || !obs_offsets || !count || (target < 0 || target > 2) || max_units < 1) return kConfig;
+  try {
+    const std::vector<i64> u = cv_units(n_samples, obs_offsets, target, max_units, seed);
+    *count = static_cast<int64_t>(u.size() / 3);
+    if (units)
+      for (std::size_t k = 0; k < u.size() && static_cast<int64_t>(k / 3) < capacity; ++k) units[k] = u[k];
+    return 0;
+  } catch (const Failure& f) {
+    return f.cls;
+  }
+}
+
+int dfpca_cv_objective(dfpca_context* ctx, const dfpca_dataset* ds, const dfpca_grid* grid, int target,
+                       int64_t n_units, const int64_t* units, const double* h, double* score, int64_t* used_units) {
+  return guarded(ctx, [&] {
+    if (!ds || !score || (target < 0 || target > 2) || n_units < 1 || !units)
+      fail(kConfig, "InvalidArgument", "invalid cross-validation request");
+    Grid g = make_grid(grid);
+    if (g.d != ds->dim) fail(kConfig, "InvalidBandwidth", "bandwidth dimension mismatch");
+    validate_bandwidth(g, h);  // h.validate(extents_) (bandwidth.hpp:75)
+    *score = run_cv_objective(ctx, ds, target, n_units, units, h, used_units);
   });
 }
 

@@ -200,3 +200,14 @@ struct dfpca_surface {
   std::int64_t row0 = 0;
   std::int64_t rows = -1;
 };
+
+// Device-resident observations of a FunctionalDataset (CSR), for the CV
+// objective (cv.cu): host copies give the units' targets and responses.
+struct dfpca_dataset {
+  int dim = 0;
+  std::int64_t n_samples = 0, n_obs = 0;
+  std::vector<std::int64_t> offsets_h;
+  std::vector<double> coords_h, values_h;
+  dfpca_gpu::DevBuf<std::int64_t> offsets;
+  dfpca_gpu::DevBuf<double> coords, values, obs_w;
+};

@@ -161,3 +161,42 @@ def test_scores_against_golden(api, name):
     assert bit_equal(rec, z["reconstruct0"])
     dense = api.dense_eig(api.matrixize(cov), 3, grid)
     assert np.allclose(dense.eigenvalues, z["dense_values"], rtol=1e-10, atol=0)
+
+
+CV_CASES = {
+    "sparse_masked_2d": lambda s: s.sparse_masked(24, 300, 0.3),
+    "random_1d": lambda s: s.random_points(1, 60, 80, 12, 0.15),
+    "random_3d": lambda s: s.random_points(3, 6, 60, 10, 0.5),
+    "dense_1d": lambda s: s.grid_nodes(1, 40, 60, 0.1),
+}
+
+
+@pytest.mark.parametrize("case", list(CV_CASES))
+@pytest.mark.parametrize("target", ["mean", "diag", "covariance"])
+def test_cv_objective_matches_reference(api, ref, case, target):
+    """CvObjective / cv_score (bandwidth.hpp:56-164): the same units (seeded
+    subsample), one direct fit per unit on the device; score within 1e-9
+    relative of the reference's (moment sums are reassociated)."""
+    from paper_1510_04439_b200 import synth
+    sd = CV_CASES[case](synth)
+    t = {"mean": api.CvTarget.Mean, "diag": api.CvTarget.DiagPlusNoise, "covariance": api.CvTarget.Covariance}[target]
+    obj = api.CvObjective(sd.dataset(), sd.grid(), t, max_units=500, seed=77)
+    for scale in (0.7, 1.0, 1.6):
+        h = [min(x * scale, 1.0) for x in sd.h]
+        got = api.cv_score(api.Bandwidth(h), obj)
+        want, n_units = ref.cv_score((sd.axes, sd.mask), sd.offsets, sd.coords, sd.values, t.value, h,
+                                     max_units=500, seed=77)
+        assert obj.n_units() == n_units
+        assert abs(got - want) <= 1e-9 * abs(want), (got, want)
+
+
+def test_cv_objective_errors(api):
+    from paper_1510_04439_b200 import synth
+    sd = synth.random_points(1, 60, 10, 3, 0.15)
+    obj = api.CvObjective(sd.dataset(), sd.grid(), api.CvTarget.Mean)
+    with pytest.raises(api.Error) as e:
+        obj(api.Bandwidth([2.0]))
+    assert e.value.name() == "InvalidBandwidth"
+    with pytest.raises(api.Error) as e:
+        obj(api.Bandwidth([1e-6]))  # every window holds only its own observation
+    assert e.value.name() == "BandwidthTooSmall"

@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
     k_gemm_tn(i64 M, i64 N, i64 K, const double* __restrict__ A, i64 lda, const double* __restrict__ B,
               i64 ldb, double* __restrict__ C, i64 ldc, int symmetric, i64 tiles_n, i64 k_chunk,
               i64 split_stride, i64 tm_begin, i64 tm_end, const int4* __restrict__ items,
-              double* __restrict__ ws, i64 k_mid) {
+              double* __restrict__ ws, i64 k_mid, i64 a_col0) {
   extern __shared__ __align__(16) double smem[];
 
   // symmetric: one work item per CTA (items, sym_items()): a tile pair
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
         const i64 col = m0 + c;
         const i64 avail = krow ? (M - col) : 0;
         const int bytes = avail >= VEC ? 8 * VEC : (avail > 0 ? 8 * static_cast<int>(avail) : 0);
-        const double* src = bytes ? A + k * lda + col : A;
+        const double* src = bytes ? A + k * lda + (col - a_col0) : A;  // A holds columns from a_col0
         if (VEC == 2) cp_async16(As + kr * LDS + c, src, bytes);
         else cp_async8(As + kr * LDS + c, src, bytes);
       }
@@ -226,21 +226,22 @@ __global__ void k_splitk_reduce(const double* __restrict__ ws, i64 splits, i64 M
   }
 }
 
-// out[k][m] = w[k] * in[k][m]  (rounded product, as the reference's pw * m).
+// out[k][m] = w[k] * in[k][col0 + m], m < M  (rounded product, as the
+// reference's pw * m); a slab scales only the columns of its own row tiles.
 __global__ void k_scale_rows(const double* __restrict__ in, const double* __restrict__ w, i64 K, i64 M,
-                             i64 ld, double* __restrict__ out) {
+                             i64 ld, i64 col0, double* __restrict__ out) {
   const i64 total = K * M;
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
        e += (i64)gridDim.x * blockDim.x) {
     const i64 k = e / M, m = e % M;
-    out[k * M + m] = __dmul_rn(w[k], in[k * ld + m]);
+    out[k * M + m] = __dmul_rn(w[k], in[k * ld + col0 + m]);
   }
 }
 
 template <int VEC>
 void launch(dfpca_context* ctx, dim3 grid, std::size_t smem, i64 M, i64 N, i64 K, const double* A, i64 lda,
             const double* B, i64 ldb, double* C, i64 ldc, int symmetric, i64 tiles_n, i64 k_chunk,
-            i64 split_stride, i64 tm_begin, i64 tm_end, const int4* items, double* ws, i64 k_mid) {
+            i64 split_stride, i64 tm_begin, i64 tm_end, const int4* items, double* ws, i64 k_mid, i64 a_col0) {
   static bool attr = false;
   if (!attr) {
     DFPCA_CUDA(cudaFuncSetAttribute(k_gemm_tn<VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -248,7 +249,7 @@ void launch(dfpca_context* ctx, dim3 grid, std::size_t smem, i64 M, i64 N, i64 K
     attr = true;
   }
   DFPCA_LAUNCH(ctx, k_gemm_tn<VEC>, grid, NTHREADS, smem, M, N, K, A, lda, B, ldb, C, ldc, symmetric,
-               tiles_n, k_chunk, split_stride, tm_begin, tm_end, items, ws, k_mid);
+               tiles_n, k_chunk, split_stride, tm_begin, tm_end, items, ws, k_mid, a_col0);
 }
 
 }  // namespace
@@ -272,14 +273,24 @@ void gemm_tn(dfpca_context* ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, 
       DFPCA_CUDA(cudaMemsetAsync(C + r * ldc, 0, sizeof(double) * N, ctx->stream));
     return;
   }
-  DevBuf<double> scaled;
-  if (w) {
-    scaled.alloc(static_cast<std::size_t>(K * M));
-    DFPCA_LAUNCH(ctx, k_scale_rows, grid_for(K * M, 256), 256, 0, A, w, K, M, lda, scaled.get());
-    A = scaled.get();
-    lda = M;
-  }
   const i64 tiles_m = (M + BM - 1) / BM;
+  DevBuf<double> scaled;
+  i64 a_col0 = 0;
+  if (w) {
+    // weighted operand: the columns the launch reads (a slab's own row tiles)
+    i64 c0 = 0, c1 = M;
+    if (symmetric) {
+      const i64 te = (tm_end < 0 || tm_end > tiles_m) ? tiles_m : tm_end;
+      c0 = std::max<i64>(0, tm_begin) * BM;
+      c1 = std::min<i64>(M, te * BM);
+    }
+    const i64 Mw = std::max<i64>(1, c1 - c0);
+    scaled.alloc(static_cast<std::size_t>(K * Mw));
+    DFPCA_LAUNCH(ctx, k_scale_rows, grid_for(K * Mw, 256), 256, 0, A, w, K, Mw, lda, c0, scaled.get());
+    A = scaled.get();
+    lda = Mw;
+    a_col0 = c0;
+  }
   const i64 tiles_n = (N + BN - 1) / BN;
   const std::size_t smem = sizeof(double) * STAGES * STAGE_DOUBLES;  // 52 KB
   const bool vec2 = (lda % 2 == 0) && (ldb % 2 == 0) && (reinterpret_cast<std::uintptr_t>(A) % 16 == 0) &&
@@ -349,10 +360,10 @@ void gemm_tn(dfpca_context* ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, 
   const dim3 grid(static_cast<unsigned>(n_blocks), static_cast<unsigned>(splits));
   if (vec2)
     launch<2>(ctx, grid, smem, M, N, K, A, lda, B, ldb, out, ldo, symmetric ? 1 : 0, tiles_n, k_chunk, stride,
-              tm_begin, tm_end, d_items.get(), ws.get(), k_mid);
+              tm_begin, tm_end, d_items.get(), ws.get(), k_mid, a_col0);
   else
     launch<1>(ctx, grid, smem, M, N, K, A, lda, B, ldb, out, ldo, symmetric ? 1 : 0, tiles_n, k_chunk, stride,
-              tm_begin, tm_end, d_items.get(), ws.get(), k_mid);
+              tm_begin, tm_end, d_items.get(), ws.get(), k_mid, a_col0);
   if (!split_items.empty())
     DFPCA_LAUNCH(ctx, k_sym_split_reduce, static_cast<unsigned>(split_items.size()), 256, 0, d_split.get(), ws.get(),
                  M, N, C, ldc, tm_begin, tm_end);

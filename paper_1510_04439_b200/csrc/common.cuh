@@ -2,7 +2,10 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
 #include <cstdint>
+#include <map>
+#include <mutex>
 
 #include "internal.hpp"
 
@@ -31,6 +34,22 @@ struct DevGrid {
     if (dfpca_prof_slot_ >= 0) (ctx)->kernel_end(dfpca_prof_slot_);               \
     ++(ctx)->launches;                                                            \
   } while (0)
+
+// Raises (never lowers) a kernel's dynamic shared-memory limit.  The
+// attribute is process-wide, so ranks running as threads of one process
+// (shard.cu) must not race a smaller value in between another rank's
+// attribute call and launch.
+template <class K>
+inline void allow_smem(K kern, std::size_t bytes) {
+  static std::mutex mu;
+  static std::map<const void*, std::size_t> cur;
+  std::lock_guard<std::mutex> lk(mu);
+  std::size_t& c = cur[reinterpret_cast<const void*>(kern)];
+  if (bytes > c) {
+    DFPCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+    c = bytes;
+  }
+}
 
 inline unsigned grid_for(i64 n, int block, i64 cap = 148ll * 32) {
   i64 g = (n + block - 1) / block;

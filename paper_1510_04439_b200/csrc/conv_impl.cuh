@@ -433,8 +433,7 @@ __global__ void __launch_bounds__(kThreads) k_tphase2(const double* __restrict__
 // ------------------------------------------------------------- launchers --
 template <typename K>
 inline unsigned persistent_grid(dfpca_context* ctx, K kern, std::size_t smem, i64 work) {
-  if (smem > 48 * 1024)
-    DFPCA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  if (smem > 48 * 1024) allow_smem(kern, smem);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
   return static_cast<unsigned>(
@@ -458,9 +457,7 @@ void launch_tiled(dfpca_context* ctx, const PassSpec& s, const TapsP& tp) {
   if (in.inner == 1) {
     const i64 blocks = (in.outer + kLines - 1) / kLines;
     const std::size_t smem = sizeof(double) * kLines * (in.n + 1) * (1 + NO);
-    if (smem > 48 * 1024)
-      DFPCA_CUDA(cudaFuncSetAttribute(k_pass_rows<R, NO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
+    if (smem > 48 * 1024) allow_smem(k_pass_rows<R, NO>, smem);
     DFPCA_LAUNCH(ctx, (k_pass_rows<R, NO>), static_cast<unsigned>(blocks), kThreads, smem, in, s.out[0], o1, o2,
                  tp);
     return;

@@ -414,8 +414,7 @@ static void cv_launch(dfpca_context* ctx, const dfpca_dataset* ds, int target, i
   if (target == 1) {
     constexpr int P = 2 * D;
     const std::size_t smem = sizeof(double) * kGroups * kUnitsPerCta * ((1 + P + P * (P + 1) / 2) + (1 + P));
-    DFPCA_CUDA(cudaFuncSetAttribute(k_cv_pair_partials<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
+    allow_smem(k_cv_pair_partials<D>, smem);
     DFPCA_LAUNCH(ctx, k_cv_pair_partials<D>, grid, kUnitsPerCta * kGroups, smem, data, d_tgt, n_units, d_h,
                  chunk_len, d_partial);
   } else {

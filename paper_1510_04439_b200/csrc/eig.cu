@@ -675,8 +675,7 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
   const bool jac_smem = jsmem + sizeof(double) * 2 * q * q <= 200 * 1024;
   if (jac_smem) {
     jsmem += sizeof(double) * 2 * q * q;
-    DFPCA_CUDA(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(jsmem)));
+    allow_smem(k_jacobi, jsmem);
   }
   DFPCA_LAUNCH(ctx, k_jacobi, 1, 1024, jsmem, small.get(), Vs.get(), static_cast<int>(q), evals.get(),
                info.get(), jac_smem ? 1 : 0);

@@ -242,12 +242,7 @@ template <int VEC>
 void launch(dfpca_context* ctx, dim3 grid, std::size_t smem, i64 M, i64 N, i64 K, const double* A, i64 lda,
             const double* B, i64 ldb, double* C, i64 ldc, int symmetric, i64 tiles_n, i64 k_chunk,
             i64 split_stride, i64 tm_begin, i64 tm_end, const int4* items, double* ws, i64 k_mid, i64 a_col0) {
-  static bool attr = false;
-  if (!attr) {
-    DFPCA_CUDA(cudaFuncSetAttribute(k_gemm_tn<VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-    attr = true;
-  }
+  allow_smem(k_gemm_tn<VEC>, smem);
   DFPCA_LAUNCH(ctx, k_gemm_tn<VEC>, grid, NTHREADS, smem, M, N, K, A, lda, B, ldb, C, ldc, symmetric,
                tiles_n, k_chunk, split_stride, tm_begin, tm_end, items, ws, k_mid, a_col0);
 }

@@ -490,7 +490,7 @@ void run_scores(dfpca_context* ctx, const Grid& grid, i64 n, const i64* offsets,
     const std::size_t smem = sizeof(double) * (kPaceMaxObs * (L + 1) + max_obs * max_obs);
     if (smem > 227 * 1024)
       fail(kConfig, "InvalidArgument", "too many components x observations for the on-chip PACE design");
-    DFPCA_CUDA(cudaFuncSetAttribute(k_pace, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    allow_smem(k_pace, smem);
     DFPCA_LAUNCH(ctx, k_pace, static_cast<unsigned>(n), 128, smem, a);
     std::vector<int> hs(static_cast<std::size_t>(n));
     DFPCA_CUDA(cudaMemcpyAsync(hs.data(), status.get(), sizeof(int) * n, cudaMemcpyDeviceToHost, st));

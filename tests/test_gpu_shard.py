@@ -26,6 +26,9 @@ CASES = {
     "3d_random": lambda s: s.random_points(3, 8, 30, 40, 0.35),
     # d = 1: one unit of 128 nodes per slab
     "1d_random": lambda s: s.random_points(1, 512, 30, 40, 0.05),
+    # 96-node planes: pass kernels above 48 KB of shared memory, launched by
+    # concurrent rank threads with different sizes (the attribute must only grow)
+    "2d_nodes_96": lambda s: s.grid_nodes(2, 96, 6, 0.1),
 }
 
 

@@ -40,8 +40,11 @@ __global__ void k_pass_generic(View in, View o0, View o1, View o2, int n_out,
   }
 }
 
+// Radius bucket of the register-tiled kernels: exact up to 24, then 32 / 48.
+int tiled_radius(int R) { return R <= 24 ? R : (R <= 32 ? 32 : 48); }
+
 void launch_by_radius(dfpca_context* ctx, const PassSpec& s, const TapsP& tp) {
-  switch (s.R) {
+  switch (tiled_radius(s.R)) {
 #define DFPCA_R_CASE(r)                                \
   case r:                                              \
     conv_detail::launch_pass<r>(ctx, s, tp);           \
@@ -51,6 +54,7 @@ void launch_by_radius(dfpca_context* ctx, const PassSpec& s, const TapsP& tp) {
     DFPCA_R_CASE(10) DFPCA_R_CASE(11) DFPCA_R_CASE(12) DFPCA_R_CASE(13) DFPCA_R_CASE(14)
     DFPCA_R_CASE(15) DFPCA_R_CASE(16) DFPCA_R_CASE(17) DFPCA_R_CASE(18) DFPCA_R_CASE(19)
     DFPCA_R_CASE(20) DFPCA_R_CASE(21) DFPCA_R_CASE(22) DFPCA_R_CASE(23) DFPCA_R_CASE(24)
+    DFPCA_R_CASE(32) DFPCA_R_CASE(48)
 #undef DFPCA_R_CASE
     default:
       break;
@@ -67,6 +71,7 @@ void launch_tphase2_r(dfpca_context* ctx, const TPhase2Spec& s, const Taps2P& tp
     DFPCA_T_CASE(7) DFPCA_T_CASE(8) DFPCA_T_CASE(9) DFPCA_T_CASE(10) DFPCA_T_CASE(11) DFPCA_T_CASE(12)
     DFPCA_T_CASE(13) DFPCA_T_CASE(14) DFPCA_T_CASE(15) DFPCA_T_CASE(16) DFPCA_T_CASE(17) DFPCA_T_CASE(18)
     DFPCA_T_CASE(19) DFPCA_T_CASE(20) DFPCA_T_CASE(21) DFPCA_T_CASE(22) DFPCA_T_CASE(23) DFPCA_T_CASE(24)
+    DFPCA_T_CASE(32) DFPCA_T_CASE(48)
 #undef DFPCA_T_CASE
     default:
       break;
@@ -76,8 +81,9 @@ void launch_tphase2_r(dfpca_context* ctx, const TPhase2Spec& s, const Taps2P& tp
 }  // namespace
 
 bool run_tphase2(dfpca_context* ctx, const TPhase2Spec& s) {
-  const int R = std::max(s.R[0], s.R[1]);
-  if (R < 1 || R > kMaxTemplR) return false;
+  const int Rmax = std::max(s.R[0], s.R[1]);
+  if (Rmax < 1 || Rmax > kMaxTemplR) return false;
+  const int R = tiled_radius(Rmax);
   if (sizeof(double) * 3 * s.n1 * (s.n2 + 1) > 200 * 1024) return false;
   Taps2P tp{};
   for (int ax = 0; ax < 2; ++ax)
@@ -94,9 +100,11 @@ void run_pass(dfpca_context* ctx, const PassSpec& s, double* taps_dev) {
                         s.in.outer * ((s.in.inner + conv_detail::kTC - 1) / conv_detail::kTC) < (1ll << 31) &&
                         s.in.inner < (1ll << 31);
   if (tiled_ok) {
+    // taps centred in the kernel's radius (zero padding for the 32 / 48 buckets)
+    const int RT = tiled_radius(R);
     TapsP tp{};
     for (int r = 0; r < s.n_out; ++r)
-      for (int o = 0; o <= 2 * R; ++o) tp.t[r][o] = s.taps[r][o];
+      for (int o = -R; o <= R; ++o) tp.t[r][o + RT] = s.taps[r][o + R];
     launch_by_radius(ctx, s, tp);
     return;
   }

@@ -5,9 +5,11 @@
 
 namespace dfpca_gpu {
 
-// Largest stencil radius with a register-tiled specialisation; wider stencils
-// use the generic pass.
-constexpr int kMaxTemplR = 24;
+// Largest stencil radius with a register-tiled specialisation: every radius up
+// to 24 has its own instantiation, 25..32 and 33..48 run the radius-32 / -48
+// kernels with zero-padded taps (a zero tap adds +0, leaving every sum
+// unchanged); wider stencils use the generic pass.
+constexpr int kMaxTemplR = 48;
 
 // A strided view of a row-major array: element (o, j, i) lives at
 // p[o * os + j * js + i] for o < outer, j < n, i < inner (inner contiguous).

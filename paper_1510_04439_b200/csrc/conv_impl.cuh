@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(kThreads) k_tphase2(const double* __restrict__
 // ------------------------------------------------------------- launchers --
 template <typename K>
 inline unsigned persistent_grid(dfpca_context* ctx, K kern, std::size_t smem, i64 work) {
-  if (smem > 48 * 1024) allow_smem(kern, smem);
+  allow_smem(kern, smem);  // dynamic + static shared memory may cross 48 KB even when smem alone does not
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
   return static_cast<unsigned>(
@@ -457,7 +457,7 @@ void launch_tiled(dfpca_context* ctx, const PassSpec& s, const TapsP& tp) {
   if (in.inner == 1) {
     const i64 blocks = (in.outer + kLines - 1) / kLines;
     const std::size_t smem = sizeof(double) * kLines * (in.n + 1) * (1 + NO);
-    if (smem > 48 * 1024) allow_smem(k_pass_rows<R, NO>, smem);
+    allow_smem(k_pass_rows<R, NO>, smem);
     DFPCA_LAUNCH(ctx, (k_pass_rows<R, NO>), static_cast<unsigned>(blocks), kThreads, smem, in, s.out[0], o1, o2,
                  tp);
     return;

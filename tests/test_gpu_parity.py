@@ -170,6 +170,11 @@ MEAN_CASES = {
     "2d_nodes": lambda s: s.grid_nodes(2, 16, 20, 0.14),
     "3d_nodes": lambda s: s.grid_nodes(3, 8, 6, 0.3),
     "masked": lambda s: s.sparse_masked(24, 40, 0.25),
+    # wide windows: radius 27 / 40 run the zero-padded radius-32 / 48 kernels
+    "1d_wide_r32": lambda s: s.random_points(1, 61, 15, 20, 0.45),
+    "1d_wide_r48": lambda s: s.random_points(1, 101, 15, 25, 0.4),
+    # 48-node axis: 48 KB dynamic + static shared memory needs the opt-in
+    "2d_n48_wide": lambda s: s.grid_nodes(2, 48, 4, 0.6),
 }
 
 
@@ -196,7 +201,17 @@ COV_CASES = {
     "2d_random": lambda s: s.random_points(2, 10, 40, 15, 0.3),
     "2d_masked_sparse": lambda s: s.sparse_masked(14, 120, 0.3),
     "3d_nodes": lambda s: s.grid_nodes(3, 5, 10, 0.45),
+    "1d_wide_r32": lambda s: s.random_points(1, 61, 12, 10, 0.5),
+    "2d_wide_r32": lambda s: _narrow_second_axis(s.random_points(2, 26, 30, 20, 1.0), 6, 0.3),
 }
+
+
+def _narrow_second_axis(sd, cells, h):
+    """Anisotropic variant: axis 2 coarsened to `cells` nodes and bandwidth h
+    (axis 1 keeps its wide window, radius 25 -> the radius-32 kernels)."""
+    sd.axes = [sd.axes[0], [float(i) / float(cells - 1) for i in range(cells)]]
+    sd.h = [sd.h[0], h]
+    return sd
 
 
 @pytest.mark.parametrize("case", list(COV_CASES))

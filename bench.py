@@ -157,6 +157,152 @@ def run_reference(args, emit=True):
     return line
 
 
+# ------------------------------------------------------ long-format tables --
+IO_METRIC = "long-format observation rows/s (read_long_format, io.hpp:115)"
+IO_WORKLOAD = ("configs[2] observations as a long-format table: 8,192,000 rows (d=2, n=2000 x 64^2 nodes), "
+               "tab-separated %.17g, ids s<i> (SURVEY.md 8(f) rank 2)")
+
+
+def io_table(sd, path, n_samples=None):
+    from paper_1510_04439_b200 import synth
+    with open(path, "wb") as f:
+        f.write(synth.long_format_bytes(sd, n_samples))
+    return os.path.getsize(path), int(sd.offsets[n_samples if n_samples else -1])
+
+
+def run_io_reference(args, path_full=None, emit=True):
+    """The reference's read_long_format (oracle/_ref: io.hpp compiled
+    unchanged), single-threaded as in the reference, on the first
+    --cpu-io-subjects subjects of the table."""
+    import tempfile
+    from oracle import ref as R
+    rank, _, _ = rank_env()
+    if rank != 0:
+        return None
+    sd = make_data()
+    n_sub = args.cpu_io_subjects
+    path = os.path.join(tempfile.mkdtemp(), "sample.tsv")
+    size, rows = io_table(sd, path, n_sub)
+    for _ in range(args.ref_warmup if args.ref_warmup is not None else 1):
+        R.read_long_format(path)
+    times = []
+    for _ in range(max(1, args.ref_steps if args.ref_steps else 3)):
+        t0 = time.perf_counter()
+        R.read_long_format(path)
+        times.append(time.perf_counter() - t0)
+    os.unlink(path)
+    t = float(np.mean(times))
+    val = rows / t
+    line = {"metric": IO_METRIC, "value": val, "unit": "rows/s", "n_gpus": args.gpus, "steps": len(times),
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": IO_WORKLOAD, "cpu_sample": f"first {n_sub} subjects: {rows} rows, {size} bytes"},
+            "impl": "reference",
+            "cpu_baseline": {"value": val, "unit": "rows/s", "cores": 1, "kind": "reference",
+                             "sample": f"read_long_format of the first {n_sub} of {N_SUBJ} subjects ({rows} rows, "
+                                       f"{size / 1e6:.1f} MB, page cache), reference io.hpp compiled unchanged"},
+            "e2e": {"value": val, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if emit:
+        print(json.dumps(line), flush=True)
+    return line
+
+
+def run_io(args):
+    """A step = one read_long_format of the full table.  value: the device
+    stages (text resident in HBM -> CSR table in HBM: newline scan, parse,
+    grouping, scatter; CUDA-event timed); e2e: the public call from the file
+    (page cache) to the host FunctionalDataset arrays, wall clock."""
+    import ctypes as C
+    import tempfile
+    rank, world, local = rank_env()
+    if rank != 0:
+        return
+    os.environ.setdefault("DFPCA_DEVICE", str(local))
+    from paper_1510_04439_b200 import _lib, api
+    sd = make_data()
+    path = os.path.join(tempfile.mkdtemp(), "cfg3.tsv")
+    size, rows = io_table(sd, path)
+    L = _lib.lib()
+    dev_stages = ("lines", "parse", "group", "scatter")
+
+    def read_table():
+        h = C.c_void_p()
+        _lib.check(L.dfpca_read_long_format(_lib.ctx(), path.encode(), C.byref(h)))
+        st = {k: _lib.stage_ms(k) for k in dev_stages + ("upload", "total")}
+        return h, st
+
+    for _ in range(args.warmup):
+        h, _ = read_table()
+        L.dfpca_table_free(h)
+    launches0 = _lib.kernel_launches()
+    dev_ms, stage_acc = [], {}
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            h, st = read_table()
+            L.dfpca_table_free(h)
+            dev_ms.append(sum(st[k] for k in dev_stages))
+            for k, v in st.items():
+                stage_acc[k] = stage_acc.get(k, 0.0) + v
+    launches = _lib.kernel_launches() - launches0
+    t_dev = float(np.mean(dev_ms)) / 1e3
+    _lib.profile(True)
+    h, _ = read_table()
+    kstats = _lib.kernel_stats()
+    L.dfpca_table_free(h)
+    _lib.profile(False)
+    e2e = []
+    for it in range(args.e2e_steps + 1):
+        t0 = time.perf_counter()
+        ds = api.read_long_format(path)
+        if it > 0:
+            e2e.append(time.perf_counter() - t0)
+    off, coords, values = ds.csr()
+    assert int(off[-1]) == rows and np.array_equal(values.view(np.uint64), sd.values.view(np.uint64))
+    d2h = off.nbytes + coords.nbytes + values.nbytes + sum(len(s.id) for s in ds.samples) + off.nbytes
+    t_e2e = float(np.mean(e2e))
+    os.unlink(path)
+    # roofline: k_parse_lines, HBM-bound; algorithmic bytes = every text byte of
+    # the data lines once + 2 newline offsets read + (record flag, id start,
+    # id length, d + 1 doubles) written per line
+    nl_bytes = 16 * rows
+    out_bytes = (8 + 8 + 4 + 8 * 3) * rows
+    parse_ms = kstats.get("k_parse_lines", (None, 0))[0]
+    peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
+    hbm = peaks.get("hbm_gbs", 6548.8)
+    roof = None
+    if parse_ms:
+        alg = size + nl_bytes + out_bytes
+        ach = alg / (parse_ms / 1e3) / 1e9
+        tr, tr_src = ncu_traffic("k_parse_lines", "io_r*_ncu_full_summary.txt")
+        roof = {"kernel": "k_parse_lines", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                "frac": ach / hbm, "traffic": tr, "traffic_source": tr_src,
+                "algorithmic_bytes_per_launch": alg, "kernel_ms": parse_ms,
+                "model": "text bytes + 16 B newline offsets + 44 B record outputs per row (d=2)",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            ra = argparse.Namespace(**vars(args))
+            ra.ref_steps, ra.ref_warmup = 2, 1
+            cpu = run_io_reference(ra, emit=False)["cpu_baseline"]
+        except Exception as e:
+            cpu = {"value": None, "unit": "rows/s", "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+    out = {"metric": IO_METRIC, "value": rows / t_dev, "unit": "rows/s", "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": t_dev * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": IO_WORKLOAD, "rows": rows, "bytes": size,
+                      "l2": "inputs larger than L2 (373 MB text)"},
+           "stages_ms_per_step": {k: v / args.steps for k, v in stage_acc.items()},
+           "e2e": {"value": rows / t_e2e, "unit": "rows/s", "h2d_bytes_per_step": int(size),
+                   "d2h_bytes_per_step": int(d2h), "ms_per_step": t_e2e * 1e3,
+                   "all_ms": [round(t * 1e3, 2) for t in e2e],
+                   "path": "file (page cache) -> pinned slots -> HBM -> device parse/group -> host CSR arrays"},
+           "gpu_launches": int(launches),
+           "kernels": {k: {"ms": v[0], "launches": v[1]} for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][0])},
+           "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary()}
+    print(json.dumps(out), flush=True)
+
+
 # ------------------------------------------------------------------- ours --
 def main():
     ap = argparse.ArgumentParser()
@@ -169,9 +315,18 @@ def main():
     ap.add_argument("--ref-warmup", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--workload", choices=["covariance", "io"], default="covariance",
+                    help="io: the long-format table reader (SURVEY.md 8(f) rank 2)")
+    ap.add_argument("--cpu-io-subjects", type=int, default=200)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if args.workload == "io":
+        if args.impl == "reference":
+            run_io_reference(args)
+        else:
+            run_io(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return
@@ -426,12 +581,12 @@ def kernel_model(G: int, n_pair: int, shared: bool):
     }
 
 
-def ncu_traffic(kernel: str):
+def ncu_traffic(kernel: str, pattern: str = "r*_ncu_full_summary.txt"):
     """dram__bytes_read.sum + dram__bytes_write.sum (bytes) of one launch of
     `kernel` from the newest committed `ncu --set full` summary
     (profiles/rNN_ncu_full_summary.txt, written by tools/ncu_summary.py full;
     values in Mbyte as ncu reports them), or (None, None)."""
-    files = sorted((ROOT / "profiles").glob("r*_ncu_full_summary.txt"))
+    files = sorted((ROOT / "profiles").glob(pattern))
     if not files:
         return None, None
     cur, vals = None, {}

@@ -6,7 +6,10 @@
 //   g++ -std=c++17 -Iinclude cpp_tests/test_dropin.cpp -Lpaper_1510_04439_b200 -ldfpca_cuda
 #include <cmath>
 #include <cstdio>
+#include <filesystem>
+#include <fstream>
 #include <functional>
+#include <unistd.h>
 #include <string>
 #include <vector>
 
@@ -409,6 +412,65 @@ int main() {
     auto e1 = randomized_eig(matrixize(cov), 20, 3, grid, 7);
     auto e2 = gpu::randomized_eig_sharded(slab, 20, 3, grid, 7);
     CHECK(e1.eigenvalues == e2.eigenvalues && e1.eigenfunctions == e2.eigenfunctions);
+  });
+
+  run("io: long-format write -> GPU read round trip, grid file, model bundle (io.hpp)", [] {
+    namespace fs = std::filesystem;
+    const fs::path dir = fs::temp_directory_path() / ("dfpca_io_" + std::to_string(::getpid()));
+    fs::create_directories(dir);
+    FunctionalDataset data;
+    data.dim = 2;
+    for (int i = 0; i < 7; ++i) {
+      Sample smp;
+      smp.id = (i % 2 ? "subject-" : "s") + std::to_string(i);
+      for (int j = 0; j < 3 + i; ++j) {
+        smp.coords.push_back(0.1 * j + 1e-3 * i);
+        smp.coords.push_back(std::sin(j + 0.25 * i));
+        smp.values.push_back(std::exp(-0.3 * j) * (i - 3.0) / 7.0);
+      }
+      data.samples.push_back(smp);
+    }
+    const std::string table = (dir / "obs.tsv").string();
+    write_long_format(table, data);
+    const FunctionalDataset back = read_long_format(table);
+    CHECK(back.dim == 2 && back.samples.size() == data.samples.size());
+    for (std::size_t i = 0; i < back.samples.size() && i < data.samples.size(); ++i) {
+      CHECK(back.samples[i].id == data.samples[i].id);
+      CHECK(back.samples[i].coords == data.samples[i].coords && back.samples[i].values == data.samples[i].values);
+    }
+    CHECK(error_name([&] { read_long_format((dir / "absent.tsv").string()); }) == "IoError");
+    {
+      std::ofstream f(dir / "bad.tsv");
+      f << "id,t,y\na,0.5,1\nb,0.25\n";
+    }
+    CHECK(error_name([&] { read_long_format((dir / "bad.tsv").string()); }) == "ParseError");
+    std::vector<std::uint8_t> mask(12, 1);
+    mask[5] = 0;
+    const auto grid = EvaluationGrid({{0.0, 0.5, 1.0}, {0.0, 0.25, 0.5, 1.0}}, mask);
+    write_grid((dir / "grid.txt").string(), grid);
+    const auto g2 = read_grid((dir / "grid.txt").string());
+    CHECK(g2.dim() == 2 && g2.axis(1) == grid.axis(1) && g2.has_mask() && !g2.in_mask(5) && g2.in_mask(4));
+#ifdef DFPCA_IO_HAS_JSON
+    FpcaModel model;
+    model.mean.grid = grid;
+    model.mean.kind = SurfaceKind::Mean;
+    model.mean.values.assign(12, 0.5);
+    model.mean.values[5] = outside_value();
+    model.eig.eigenvalues = {2.0, 0.5};
+    model.eig.fve = {0.8, 1.0};
+    model.eig.total_variance = 2.5;
+    model.eig.eigenfunctions.assign(2, std::vector<double>(12, 0.125));
+    model.sigma2 = 0.0625;
+    model.scores = {{1.0, -2.0}, {0.5, 0.25}};
+    model.sample_ids = {"a", "b"};
+    model.mean_bandwidth.h = model.cov_bandwidth.h = model.diag_bandwidth.h = {0.2, 0.3};
+    save_model(model, (dir / "model").string());
+    const FpcaModel m2 = load_model((dir / "model").string());
+    CHECK(m2.eig.eigenvalues == model.eig.eigenvalues && m2.scores == model.scores && m2.sample_ids == model.sample_ids);
+    CHECK(m2.sigma2 == model.sigma2 && m2.cov_bandwidth.h == model.cov_bandwidth.h);
+    CHECK(is_outside(m2.mean.values[5]) && m2.mean.values[4] == 0.5);
+#endif
+    fs::remove_all(dir);
   });
 
   std::printf("%d checks, %d failures\n", g_checks, g_fail);

@@ -9,6 +9,7 @@
 #include "dfpca/errors.hpp"
 #include "dfpca/fft_smoother.hpp"
 #include "dfpca/grid.hpp"
+#include "dfpca/io.hpp"
 #include "dfpca/kernel.hpp"
 #include "dfpca/parallel.hpp"
 #include "dfpca/rng.hpp"

@@ -39,6 +39,7 @@ typedef struct dfpca_context dfpca_context;
 typedef struct dfpca_binned dfpca_binned;
 typedef struct dfpca_surface dfpca_surface;
 typedef struct dfpca_dataset dfpca_dataset;
+typedef struct dfpca_table dfpca_table;
 
 /* Grid descriptor: the data an EvaluationGrid carries (grid.hpp:92-230).
  * axes[k] points at shape[k] strictly increasing node coordinates (host).
@@ -272,6 +273,29 @@ DFPCA_API int dfpca_cv_units(int64_t n_samples, const int64_t* obs_offsets, int 
 DFPCA_API int dfpca_cv_objective(dfpca_context* ctx, const dfpca_dataset* ds, const dfpca_grid* grid, int target,
                        int64_t n_units, const int64_t* units, const double* h, double* score,
                        int64_t* used_units);
+
+/* ---- long-format observation tables ------------- */
+/* Replaces dfpca::read_long_format (io.hpp:115-155): header row naming
+ * (id, axis..., value), delimiter sniffed from it (tab, comma, semicolon or
+ * blank runs), one record per observation; records grouped by sample id in
+ * order of first appearance, file order within a sample.  The bytes are
+ * parsed on the GPU; numbers are accepted and rounded exactly as strtod
+ * (io.hpp:39-46).  Errors as the reference: IoError "cannot open ...",
+ * ParseError "<path>:<line>: ..." (the first failing line).  At most 30
+ * coordinate columns. */
+DFPCA_API int dfpca_read_long_format(dfpca_context* ctx, const char* path, dfpca_table** out);
+/* The same over n_bytes of file contents in host memory; name stands in for
+ * the path in messages. */
+DFPCA_API int dfpca_parse_long_format(dfpca_context* ctx, const char* name, const char* bytes, int64_t n_bytes,
+                            dfpca_table** out);
+DFPCA_API int dfpca_table_info(const dfpca_table* t, int* dim, int64_t* n_samples, int64_t* n_obs,
+                     int64_t* id_bytes);
+/* Host copies (any pointer may be NULL): obs_offsets n_samples+1 (CSR as
+ * dfpca_linear_bin), coords n_obs*dim, values n_obs, id_offsets n_samples+1
+ * into id_chars (id_bytes). */
+DFPCA_API int dfpca_table_copy(dfpca_context* ctx, const dfpca_table* t, int64_t* obs_offsets, double* coords,
+                     double* values, int64_t* id_offsets, char* id_chars);
+DFPCA_API int dfpca_table_free(dfpca_table* t);
 
 #ifdef __cplusplus
 }

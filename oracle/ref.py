@@ -46,6 +46,13 @@ _SIG = {
     "ref_reconstruct": (C.c_int, [C.c_int, PI, PD, PU8, PD, C.c_int64, PD, PD, PD, PD]),
     "ref_cv_score": (C.c_int, [C.c_int, PI, PD, PU8, C.c_int64, PI, PD, PD, C.c_int, C.c_int64, C.c_uint64, PD, PD,
                                PI]),
+    "ref_read_long_format": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "ref_table_info": (None, [C.c_void_p, C.POINTER(C.c_int), PI, PI, PI]),
+    "ref_table_copy": (None, [C.c_void_p, PI, PD, PD, PI, C.c_char_p]),
+    "ref_table_free": (None, [C.c_void_p]),
+    "ref_write_long_format": (C.c_int, [C.c_char_p, C.c_int, C.c_int64, PI, PD, PD, PI, C.c_char_p]),
+    "ref_write_grid": (C.c_int, [C.c_char_p, C.c_int, PI, PD, PU8]),
+    "ref_read_grid": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), PI, PD, PU8, C.POINTER(C.c_int)]),
 }
 
 _lib = None
@@ -328,3 +335,59 @@ def cv_score(grid, offsets, coords, values, target: int, h, max_units: int = 200
     _chk(lib().ref_cv_score(*ga.args(), off.size - 1, off.ctypes.data_as(PI), cp, vp, int(target), int(max_units),
                             C.c_uint64(seed), hp, C.byref(out), C.byref(nu)))
     return out.value, nu.value
+
+
+def read_long_format(path):
+    """io.hpp:115-155 -> (dim, offsets, coords, values, ids)."""
+    h = C.c_void_p()
+    _chk(lib().ref_read_long_format(str(path).encode(), C.byref(h)))
+    try:
+        dim, ns, no, nid = C.c_int(), C.c_int64(), C.c_int64(), C.c_int64()
+        lib().ref_table_info(h, C.byref(dim), C.byref(ns), C.byref(no), C.byref(nid))
+        off = np.zeros(ns.value + 1, dtype=np.int64)
+        coords = np.zeros(no.value * dim.value)
+        values = np.zeros(no.value)
+        id_off = np.zeros(ns.value + 1, dtype=np.int64)
+        chars = C.create_string_buffer(max(nid.value, 1))
+        lib().ref_table_copy(h, off.ctypes.data_as(PI), coords.ctypes.data_as(PD), values.ctypes.data_as(PD),
+                             id_off.ctypes.data_as(PI), chars)
+    finally:
+        lib().ref_table_free(h)
+    raw = chars.raw
+    ids = [raw[id_off[i]:id_off[i + 1]] for i in range(ns.value)]
+    return dim.value, off, coords, values, ids
+
+
+def write_long_format(path, dim, offsets, coords, values, ids):
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    blob = b"".join(i if isinstance(i, bytes) else i.encode() for i in ids)
+    id_off = np.zeros(len(ids) + 1, dtype=np.int64)
+    np.cumsum([len(i if isinstance(i, bytes) else i.encode()) for i in ids], out=id_off[1:])
+    c, pc = _d(coords)
+    v, pv = _d(values)
+    _chk(lib().ref_write_long_format(str(path).encode(), int(dim), len(ids), off.ctypes.data_as(PI), pc, pv,
+                                     id_off.ctypes.data_as(PI), blob))
+
+
+def write_grid(path, grid):
+    g = _GridArgs(*grid)
+    _chk(lib().ref_write_grid(str(path).encode(), *g.args()))
+
+
+def read_grid(path):
+    """-> (axes list, mask or None)"""
+    dim, has_mask = C.c_int(), C.c_int()
+    shape = np.zeros(16, dtype=np.int64)
+    _chk(lib().ref_read_grid(str(path).encode(), C.byref(dim), shape.ctypes.data_as(PI), None, None,
+                             C.byref(has_mask)))
+    n = shape[:dim.value]
+    axes = np.zeros(int(n.sum()))
+    mask = np.zeros(int(np.prod(n)), dtype=np.uint8)
+    _chk(lib().ref_read_grid(str(path).encode(), C.byref(dim), shape.ctypes.data_as(PI), axes.ctypes.data_as(PD),
+                             mask.ctypes.data_as(PU8), C.byref(has_mask)))
+    out, o = [], 0
+    for k in n:
+        out.append(axes[o:o + k])
+        o += k
+    return out, (mask if has_mask.value else None)
+

@@ -18,6 +18,7 @@
 #include "dfpca/errors.hpp"
 #include "dfpca/fft_smoother.hpp"
 #include "dfpca/grid.hpp"
+#include "dfpca/io.hpp"
 #include "dfpca/parallel.hpp"
 #include "dfpca/scores.hpp"
 #include "dfpca/smoother.hpp"
@@ -368,6 +369,86 @@ int ref_cv_score(int dim, const int64_t* shape, const double* axes, const uint8_
     bw.h.assign(h, h + dim);
     *out = cv_score(bw, obj);
     if (n_units) *n_units = static_cast<int64_t>(obj.n_units());
+  });
+}
+
+// ---- io.hpp (long-format tables, grid files) --------------------------------
+struct RefTable {
+  int dim = 0;
+  std::vector<int64_t> off{0}, id_off{0};
+  std::vector<double> coords, values;
+  std::string ids;
+};
+
+int ref_read_long_format(const char* path, void** out) {
+  return guarded([&] {
+    const FunctionalDataset data = read_long_format(path);
+    auto* t = new RefTable;
+    t->dim = static_cast<int>(data.dim);
+    for (const auto& s : data.samples) {
+      t->coords.insert(t->coords.end(), s.coords.begin(), s.coords.end());
+      t->values.insert(t->values.end(), s.values.begin(), s.values.end());
+      t->off.push_back(static_cast<int64_t>(t->values.size()));
+      t->ids += s.id;
+      t->id_off.push_back(static_cast<int64_t>(t->ids.size()));
+    }
+    *out = t;
+  });
+}
+
+void ref_table_info(void* h, int* dim, int64_t* n_samples, int64_t* n_obs, int64_t* id_bytes) {
+  const auto* t = static_cast<RefTable*>(h);
+  *dim = t->dim;
+  *n_samples = static_cast<int64_t>(t->off.size()) - 1;
+  *n_obs = static_cast<int64_t>(t->values.size());
+  *id_bytes = static_cast<int64_t>(t->ids.size());
+}
+
+void ref_table_copy(void* h, int64_t* off, double* coords, double* values, int64_t* id_off, char* ids) {
+  const auto* t = static_cast<RefTable*>(h);
+  std::memcpy(off, t->off.data(), sizeof(int64_t) * t->off.size());
+  if (!t->coords.empty()) std::memcpy(coords, t->coords.data(), sizeof(double) * t->coords.size());
+  if (!t->values.empty()) std::memcpy(values, t->values.data(), sizeof(double) * t->values.size());
+  std::memcpy(id_off, t->id_off.data(), sizeof(int64_t) * t->id_off.size());
+  if (!t->ids.empty()) std::memcpy(ids, t->ids.data(), t->ids.size());
+}
+
+void ref_table_free(void* h) { delete static_cast<RefTable*>(h); }
+
+int ref_write_long_format(const char* path, int dim, int64_t n, const int64_t* off, const double* coords,
+                          const double* values, const int64_t* id_off, const char* ids) {
+  return guarded([&] {
+    FunctionalDataset data;
+    data.dim = static_cast<std::size_t>(dim);
+    for (int64_t i = 0; i < n; ++i) {
+      Sample s;
+      s.id.assign(ids + id_off[i], ids + id_off[i + 1]);
+      s.coords.assign(coords + off[i] * dim, coords + off[i + 1] * dim);
+      s.values.assign(values + off[i], values + off[i + 1]);
+      data.samples.push_back(std::move(s));
+    }
+    write_long_format(path, data);
+  });
+}
+
+int ref_write_grid(const char* path, int dim, const int64_t* shape, const double* axes, const uint8_t* mask) {
+  return guarded([&] { write_grid(path, make_grid(dim, shape, axes, mask)); });
+}
+
+// shape: capacity 16; axes: capacity sum(shape) (call with axes == NULL first)
+int ref_read_grid(const char* path, int* dim, int64_t* shape, double* axes, uint8_t* mask, int* has_mask) {
+  return guarded([&] {
+    const EvaluationGrid g = read_grid(path);
+    *dim = static_cast<int>(g.dim());
+    *has_mask = g.has_mask() ? 1 : 0;
+    std::size_t off = 0;
+    for (std::size_t k = 0; k < g.dim() && k < 16; ++k) {
+      shape[k] = static_cast<int64_t>(g.axis(k).size());
+      if (axes) std::memcpy(axes + off, g.axis(k).data(), sizeof(double) * g.axis(k).size());
+      off += g.axis(k).size();
+    }
+    if (mask && g.has_mask())
+      for (Index f = 0; f < g.size(); ++f) mask[f] = g.in_mask(f) ? 1 : 0;
   });
 }
 

@@ -81,6 +81,11 @@ SIGNATURES = [
     ("dfpca_scores", C.c_int, [P, C.POINTER(DfpcaGrid), C.c_int64, PI64, PD, PD, PD, C.c_int64, PD, PD, C.c_double,
                                C.c_int, PD, C.POINTER(C.c_int32)]),
     ("dfpca_reconstruct", C.c_int, [P, C.POINTER(DfpcaGrid), PD, C.c_int64, PD, C.c_int64, PD, PD]),
+    ("dfpca_read_long_format", C.c_int, [P, C.c_char_p, C.POINTER(P)]),
+    ("dfpca_parse_long_format", C.c_int, [P, C.c_char_p, C.c_char_p, C.c_int64, C.POINTER(P)]),
+    ("dfpca_table_info", C.c_int, [P, C.POINTER(C.c_int), PI64, PI64, PI64]),
+    ("dfpca_table_copy", C.c_int, [P, P, PI64, PD, PD, PI64, C.c_char_p]),
+    ("dfpca_table_free", C.c_int, [P]),
     ("dfpca_shard_bounds", C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int, PI64]),
     ("dfpca_shard_blocks", C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, PI64, C.c_int64, PI64]),
 ]

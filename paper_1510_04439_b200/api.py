@@ -14,6 +14,8 @@ Names, argument meaning and error behaviour follow the C++ headers:
     randomized_eig        eigensolve.hpp:245
     select_components_fve eigensolve.hpp:282
     eig_residuals         eigensolve.hpp:294
+    read_long_format      io.hpp:115 (parsed on the GPU)
+    write_long_format, read_grid, write_grid   io.hpp:158-259 (host)
 Every compute call runs on the GPU; there is no CPU fallback -- a missing
 library or device raises immediately.
 """
@@ -1047,3 +1049,159 @@ class CvObjective:
 def cv_score(h: Bandwidth, obj: CvObjective) -> float:
     """bandwidth.hpp:164."""
     return obj(h)
+
+
+# ------------------------------------------------------------ file formats --
+# io.hpp: long-format observation tables (read on the GPU), the
+# "dfpca-grid v1" grid file (host; a few KB).
+
+def _table_to_dataset(h) -> FunctionalDataset:
+    try:
+        dim, ns, no, nid = C.c_int(), C.c_int64(), C.c_int64(), C.c_int64()
+        _lib.lib().dfpca_table_info(h, C.byref(dim), C.byref(ns), C.byref(no), C.byref(nid))
+        offsets = np.zeros(ns.value + 1, dtype=np.int64)
+        coords = np.zeros(no.value * dim.value, dtype=np.float64)
+        values = np.zeros(no.value, dtype=np.float64)
+        id_off = np.zeros(ns.value + 1, dtype=np.int64)
+        chars = C.create_string_buffer(max(nid.value, 1))
+        PI, PDd = C.POINTER(C.c_int64), C.POINTER(C.c_double)
+        check(_lib.lib().dfpca_table_copy(_lib.ctx(), h, offsets.ctypes.data_as(PI), coords.ctypes.data_as(PDd),
+                                          values.ctypes.data_as(PDd), id_off.ctypes.data_as(PI), chars))
+    finally:
+        _lib.lib().dfpca_table_free(h)
+    raw = chars.raw
+    ids = [raw[id_off[i]:id_off[i + 1]].decode("utf-8", "surrogateescape") for i in range(ns.value)]
+    return FunctionalDataset.from_csr(dim.value, offsets, coords, values, ids)
+
+
+def read_long_format(path: str) -> FunctionalDataset:
+    """io.hpp:115-155.  Samples in order of first appearance of their id,
+    observations in file order; ParseError / IoError as the reference."""
+    h = C.c_void_p()
+    check(_lib.lib().dfpca_read_long_format(_lib.ctx(), str(path).encode(), C.byref(h)))
+    return _table_to_dataset(h)
+
+
+def parse_long_format(data: bytes, name: str = "<memory>") -> FunctionalDataset:
+    """read_long_format over file contents already in memory."""
+    h = C.c_void_p()
+    check(_lib.lib().dfpca_parse_long_format(_lib.ctx(), name.encode(), data, len(data), C.byref(h)))
+    return _table_to_dataset(h)
+
+
+def _fmt17(v: float) -> str:
+    if v != v:
+        return "-nan" if math.copysign(1.0, v) < 0 else "nan"
+    return "%.17g" % v
+
+
+def write_long_format(path: str, data: FunctionalDataset, axis_names: Optional[Sequence[str]] = None) -> None:
+    """io.hpp:158-178: tab-separated, header sample_id, t1.., y; 17 digits."""
+    names = list(axis_names) if axis_names else ["t%d" % (k + 1) for k in range(data.dim)]
+    if len(names) != data.dim:
+        raise Error(ErrorClass.Config, "InvalidArgument", "one axis name per dimension")
+    try:
+        f = open(path, "w", newline="\n")
+    except OSError:
+        raise Error(ErrorClass.Parse, "IoError", "cannot open '%s' for writing" % path) from None
+    with f:
+        f.write("sample_id\t" + "\t".join(names) + "\ty\n")
+        d = data.dim
+        for s in data.samples:
+            c = np.asarray(s.coords, dtype=np.float64).ravel()
+            v = np.asarray(s.values, dtype=np.float64)
+            for j in range(v.size):
+                f.write(s.id + "".join("\t" + _fmt17(float(c[j * d + k])) for k in range(d)) + "\t" + _fmt17(float(v[j]))
+                        + "\n")
+
+
+def write_grid(path: str, grid: EvaluationGrid) -> None:
+    """io.hpp:188-203 ("dfpca-grid v1")."""
+    try:
+        f = open(path, "w", newline="\n")
+    except OSError:
+        raise Error(ErrorClass.Parse, "IoError", "cannot open '%s' for writing" % path) from None
+    with f:
+        f.write("dfpca-grid v1\ndim %d\n" % grid.dim())
+        for k in range(grid.dim()):
+            ax = grid.axis(k)
+            f.write("axis %d %d" % (k, len(ax)) + "".join(" " + _fmt17(float(v)) for v in ax) + "\n")
+        if grid.has_mask():
+            f.write("mask " + "".join("1" if m else "0" for m in np.asarray(grid.mask()).ravel()) + "\n")
+
+
+def _parse_token_double(tok: str, where: str) -> float:
+    # strtod acceptance (io.hpp:39-46) for the grid file's few numbers
+    t = tok.strip(" \t\n\v\f\r") if tok[:1].isspace() else tok
+    try:
+        v = float.fromhex(t) if t.lower().lstrip("+-").startswith("0x") else float(t)
+    except ValueError:
+        raise Error(ErrorClass.Parse, "ParseError", "%s: not a number: '%s'" % (where, tok)) from None
+    if "_" in t or math.isinf(v) and not t.lower().lstrip("+-").startswith("inf"):
+        raise Error(ErrorClass.Parse, "ParseError", "%s: not a number: '%s'" % (where, tok))
+    return v
+
+
+def read_grid(path: str) -> EvaluationGrid:
+    """io.hpp:206-259."""
+    try:
+        f = open(path, "rb")
+    except OSError:
+        raise Error(ErrorClass.Parse, "IoError", "cannot open '%s' for reading" % path) from None
+    with f:
+        lines = f.read().decode("latin-1").split("\n")
+    if lines and lines[-1] == "":
+        lines.pop()
+    if not lines:
+        raise Error(ErrorClass.Parse, "ParseError", "%s:1: empty grid file" % path)
+    first = lines[0][:-1] if lines[0].endswith("\r") else lines[0]
+    if not first.startswith("dfpca-grid"):
+        raise Error(ErrorClass.Parse, "ParseError", "%s:1: not a dfpca-grid file (bad magic)" % path)
+    if first != "dfpca-grid v1":
+        raise Error(ErrorClass.Version, "VersionMismatch", "%s: unsupported grid format '%s'" % (path, first))
+    dim, axes, mask_bits = 0, [], ""
+    for no, line in enumerate(lines[1:], start=2):
+        line = line[:-1] if line.endswith("\r") else line
+        if not line:
+            continue
+        toks = line.split()
+        tag = toks[0] if toks else ""
+        where = "%s:%d" % (path, no)
+        if tag == "dim":
+            try:
+                dd = int(toks[1])
+            except (IndexError, ValueError):
+                dd = 0
+            if dd < 1:
+                raise Error(ErrorClass.Parse, "ParseError", "%s: bad dimension" % where)
+            dim = dd
+            axes = [[] for _ in range(dim)]
+        elif tag == "axis":
+            try:
+                k, cnt = int(toks[1]), int(toks[2])
+            except (IndexError, ValueError):
+                k, cnt = -1, 0
+            if k < 0 or k >= len(axes) or cnt < 2:
+                raise Error(ErrorClass.Parse, "ParseError", "%s: bad axis header" % where)
+            if len(toks) - 3 < cnt:
+                raise Error(ErrorClass.Parse, "ParseError", "%s: axis shorter than declared" % where)
+            axes[k] = [_parse_token_double(t, where) for t in toks[3:3 + cnt]]
+        elif tag == "mask":
+            mask_bits += "".join(toks[1:])
+        else:
+            raise Error(ErrorClass.Parse, "ParseError", "%s: unknown record '%s'" % (where, tag))
+    if dim == 0:
+        raise Error(ErrorClass.Parse, "ParseError", "%s: missing 'dim' record" % path)
+    for k in range(dim):
+        if not axes[k]:
+            raise Error(ErrorClass.Parse, "ParseError", "%s: missing axis %d" % (path, k))
+    if not mask_bits:
+        return EvaluationGrid(axes)
+    total = int(np.prod([len(a) for a in axes]))
+    if len(mask_bits) != total:
+        raise Error(ErrorClass.Parse, "ParseError",
+                    "%s: mask length %d does not match grid size %d" % (path, len(mask_bits), total))
+    if set(mask_bits) - {"0", "1"}:
+        raise Error(ErrorClass.Parse, "ParseError", "%s: mask entries must be 0 or 1" % path)
+    return EvaluationGrid(axes, np.frombuffer(mask_bits.encode(), dtype=np.uint8) - ord("0"))
+

@@ -35,7 +35,7 @@ def sources() -> list[Path]:
 def _stale(obj: Path, src: Path) -> bool:
     if not obj.exists():
         return True
-    deps = [src, *CSRC.glob("*.cuh"), *CSRC.glob("*.hpp"), ROOT / "include" / "dfpca_cuda.h"]
+    deps = [src, *CSRC.glob("*.cuh"), *CSRC.glob("*.hpp"), *CSRC.glob("*.inc"), ROOT / "include" / "dfpca_cuda.h"]
     return any(d.stat().st_mtime > obj.stat().st_mtime for d in deps)
 
 

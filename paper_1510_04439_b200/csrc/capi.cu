@@ -52,6 +52,12 @@ dfpca_dataset* upload_dataset(dfpca_context* ctx, int dim, i64 n, const i64* off
 std::vector<i64> cv_units(i64 n_samples, const i64* offsets, int target, i64 max_units, std::uint64_t seed);
 double run_cv_objective(dfpca_context* ctx, const dfpca_dataset* ds, int target, i64 n_units, const i64* units,
                         const double* h, i64* used_out);
+dfpca_table* read_long_format_file(dfpca_context* ctx, const char* path);
+dfpca_table* parse_long_format_bytes(dfpca_context* ctx, const char* name, const char* bytes, i64 S);
+void table_copy(dfpca_context* ctx, const dfpca_table* t, i64* offsets, double* coords, double* values, i64* id_off,
+                char* id_chars);
+void table_shape(const dfpca_table* t, int* dim, i64* n_samples, i64* n_obs, i64* id_bytes);
+void table_delete(dfpca_table* t);
 void run_estimate_sigma2(dfpca_context* ctx, const Grid& grid, const double* diag_plus_noise,
                          const dfpca_surface* cov, const double* mean, double* sigma2);
 void run_scores(dfpca_context* ctx, const Grid& grid, i64 n, const i64* offsets, const double* coords,
@@ -915,6 +921,40 @@ int dfpca_eig_residuals(dfpca_context* ctx, const dfpca_surface* cov, const dfpc
     Grid g = make_grid(grid);
     run_eig_residuals(ctx, cov, g, L, eigenvalues, eigenfunctions, residuals);
   });
+}
+
+int dfpca_read_long_format(dfpca_context* ctx, const char* path, dfpca_table** out) {
+  return guarded(ctx, [&] {
+    if (!path || !out) fail(kConfig, "InvalidArgument", "null path or output");
+    *out = read_long_format_file(ctx, path);
+  });
+}
+
+int dfpca_parse_long_format(dfpca_context* ctx, const char* name, const char* bytes, int64_t n_bytes,
+                            dfpca_table** out) {
+  return guarded(ctx, [&] {
+    if (!out || n_bytes < 0 || (n_bytes > 0 && !bytes)) fail(kConfig, "InvalidArgument", "invalid byte buffer");
+    *out = parse_long_format_bytes(ctx, name, bytes, n_bytes);
+  });
+}
+
+int dfpca_table_info(const dfpca_table* t, int* dim, int64_t* n_samples, int64_t* n_obs, int64_t* id_bytes) {
+  if (!t) return kConfig;
+  table_shape(t, dim, n_samples, n_obs, id_bytes);
+  return 0;
+}
+
+int dfpca_table_copy(dfpca_context* ctx, const dfpca_table* t, int64_t* obs_offsets, double* coords, double* values,
+                     int64_t* id_offsets, char* id_chars) {
+  return guarded(ctx, [&] {
+    if (!t) fail(kConfig, "InvalidArgument", "null table");
+    table_copy(ctx, t, obs_offsets, coords, values, id_offsets, id_chars);
+  });
+}
+
+int dfpca_table_free(dfpca_table* t) {
+  table_delete(t);
+  return 0;
 }
 
 }  // extern "C"

@@ -136,6 +136,9 @@ struct dfpca_context {
   // Device tables that depend only on the grid and bandwidth (smooth.cu),
   // built on first use.
   std::map<std::string, std::unique_ptr<dfpca_gpu::DevBuf<double>>> table_cache;
+  // Pinned upload slots, worker streams and events of the table reader
+  // (longfmt.cu), created on first use.
+  std::shared_ptr<void> io_state;
   // Reusable scratch (grown on demand, never shrunk while the context lives).
   dfpca_gpu::DevBuf<unsigned char> scratch;
   unsigned char* scratch_bytes(std::size_t n) {

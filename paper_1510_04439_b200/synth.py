@@ -129,3 +129,23 @@ def sim1(n: int = 200, points: int = 100, cells: int = 100, h: float = 0.25, see
     offsets = np.arange(n + 1, dtype=np.int64) * points
     return SynthData(1, [ax], None, offsets, np.ascontiguousarray(np.tile(t, n)), np.ascontiguousarray(y.ravel()),
                      [h])
+
+
+def long_format_bytes(sd: SynthData, n_samples: int | None = None) -> bytes:
+    """The dataset as the reference's write_long_format (io.hpp:158-178) lays
+    it out: tab-separated, header sample_id/t1../y, ids s<i>, %.17g numbers.
+    n_samples limits the table to the first subjects (bounded samples)."""
+    n = sd.offsets.size - 1 if n_samples is None else min(n_samples, sd.offsets.size - 1)
+    d = sd.dim
+    N = int(sd.offsets[n])
+    coords = sd.coords[:N * d]
+    uniq, inv = np.unique(coords, return_inverse=True)
+    ctxt = np.char.mod("%.17g", uniq)[inv].reshape(N, d)
+    rows = ["\t".join(r) for r in ctxt.tolist()] if d > 1 else ctxt[:, 0].tolist()
+    vtxt = np.char.mod("%.17g", sd.values[:N]).tolist()
+    parts = ["sample_id\t" + "\t".join("t%d" % (k + 1) for k in range(d)) + "\ty\n"]
+    for i in range(n):
+        a, b = int(sd.offsets[i]), int(sd.offsets[i + 1])
+        sid = "s%d\t" % i
+        parts.append("".join([sid + rows[j] + "\t" + vtxt[j] + "\n" for j in range(a, b)]))
+    return "".join(parts).encode()

@@ -11,8 +11,19 @@ SRC = ROOT / "cpp_tests" / "test_dropin.cpp"
 LIBDIR = ROOT / "paper_1510_04439_b200"
 
 
+def json_include() -> list:
+    """nlohmann's json.hpp (the reference's own io.hpp dependency), if present."""
+    import glob
+    import site
+    for sp in site.getsitepackages():
+        hit = glob.glob(sp + "/include/cudnn_frontend/thirdparty/nlohmann/json.hpp")
+        if hit:
+            return [f"-I{Path(hit[0]).parent}"]
+    return []
+
+
 def build(out: Path) -> Path:
-    cmd = ["g++", "-std=c++17", "-O1", "-Wall", "-Wextra", "-Werror", f"-I{ROOT / 'include'}", str(SRC),
+    cmd = ["g++", "-std=c++17", "-O1", "-Wall", "-Wextra", "-Werror", f"-I{ROOT / 'include'}", *json_include(), str(SRC),
            "-o", str(out), f"-L{LIBDIR}", "-ldfpca_cuda", f"-Wl,-rpath,{LIBDIR}"]
     subprocess.run(cmd, check=True, capture_output=True, text=True)
     return out

@@ -1,0 +1,81 @@
+"""GPU parity of SURVEY.md 8(f) rank 2 -- the long-format table reader
+(io.hpp:115-155) parsed on the device -- against the reference's own
+read_long_format (oracle/_ref).  Bar: identical sample order, ids and CSR
+offsets; coordinates and values bit-identical (NaN payloads included);
+rejected files rejected with the same error name and message."""
+import numpy as np
+import pytest
+
+from io_corpus import error_cases, random_table, valid_cases
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_1510_04439_b200 import api as A
+    return A
+
+
+def _same(ds, want):
+    dim, off, coords, values, ids = want
+    got_off, got_coords, got_values = ds.csr()
+    assert ds.dim == dim
+    assert np.array_equal(got_off, off)
+    assert np.array_equal(got_coords.view(np.uint64), coords.view(np.uint64))
+    assert np.array_equal(got_values.view(np.uint64), values.view(np.uint64))
+    assert [s.id.encode("utf-8", "surrogateescape") for s in ds.samples] == ids
+
+
+@pytest.mark.parametrize("name", list(valid_cases()))
+def test_table_matches_reference(api, ref, tmp_path, name):
+    data = valid_cases()[name]
+    p = tmp_path / f"{name}.tsv"
+    p.write_bytes(data)
+    want = ref.read_long_format(p)
+    _same(api.read_long_format(str(p)), want)
+    _same(api.parse_long_format(data), want)
+
+
+@pytest.mark.parametrize("name", list(error_cases()))
+def test_errors_match_reference(api, ref, tmp_path, name):
+    p = tmp_path / f"{name}.tsv"
+    p.write_bytes(error_cases()[name])
+    with pytest.raises(ref.RefError) as r:
+        ref.read_long_format(p)
+    with pytest.raises(api.Error) as o:
+        api.read_long_format(str(p))
+    assert str(o.value) == str(r.value)
+
+
+def test_missing_file(api, ref, tmp_path):
+    p = tmp_path / "absent.tsv"
+    with pytest.raises(ref.RefError) as r:
+        ref.read_long_format(p)
+    with pytest.raises(api.Error) as o:
+        api.read_long_format(str(p))
+    assert str(o.value) == str(r.value) and o.value.name() == "IoError"
+
+
+def test_large_interleaved_table(api, ref, tmp_path):
+    """~300k rows over 2000 interleaved samples, several upload chunks."""
+    rng = np.random.default_rng(11)
+    data = random_table(rng, n_samples=2000, max_obs=300, dim=2, interleave=True, id_style="long")
+    assert len(data) > 2 * (8 << 20)
+    p = tmp_path / "big.tsv"
+    p.write_bytes(data)
+    _same(api.read_long_format(str(p)), ref.read_long_format(p))
+
+
+def test_round_trip_through_writer(api, tmp_path):
+    from paper_1510_04439_b200 import synth
+    sd = synth.sparse_masked(24, 300, 0.3)
+    ds = sd.dataset()
+    p = tmp_path / "rt.tsv"
+    api.write_long_format(str(p), ds)
+    back = api.read_long_format(str(p))
+    a, b = ds.csr(), back.csr()
+    for x, y in zip(a, b):
+        assert np.array_equal(np.asarray(x).view(np.uint64) if x.dtype == np.float64 else x,
+                              np.asarray(y).view(np.uint64) if y.dtype == np.float64 else y)
+    assert [s.id for s in back.samples] == [s.id for s in ds.samples]

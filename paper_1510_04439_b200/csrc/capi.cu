@@ -394,6 +394,12 @@ int dfpca_context_destroy(dfpca_context* ctx) {
     cudaStreamSynchronize(ctx->stream);
     g_alloc_stream = nullptr;
   }
+  if (ctx->copy_) {
+    cudaStreamSynchronize(ctx->copy_);
+    cudaStreamDestroy(ctx->copy_);
+  }
+  if (ctx->fence_) cudaEventDestroy(ctx->fence_);
+  ctx->io_state.reset();
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return 0;

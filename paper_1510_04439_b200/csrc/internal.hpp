@@ -136,6 +136,18 @@ struct dfpca_context {
   // Device tables that depend only on the grid and bandwidth (smooth.cu),
   // built on first use.
   std::map<std::string, std::unique_ptr<dfpca_gpu::DevBuf<double>>> table_cache;
+  // Second stream for host-to-device copies that overlap compute (binning
+  // chunks), and a reusable event to order it after the context stream.
+  cudaStream_t copy_ = nullptr;
+  cudaEvent_t fence_ = nullptr;
+  cudaStream_t copy_stream() {
+    if (!copy_) cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking);
+    return copy_;
+  }
+  cudaEvent_t fence() {
+    if (!fence_) cudaEventCreateWithFlags(&fence_, cudaEventDisableTiming);
+    return fence_;
+  }
   // Pinned upload slots, worker streams and events of the table reader
   // (longfmt.cu), created on first use.
   std::shared_ptr<void> io_state;

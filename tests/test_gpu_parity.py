@@ -94,6 +94,37 @@ def test_binning_mean_only_and_empty_samples(api, ref):
         _assert_binned_equal(g, r)
 
 
+@pytest.mark.parametrize("chunk", ["1", "37", "1000"])
+@pytest.mark.parametrize("case", ["nodes2d", "random2d", "empty_samples"])
+def test_binning_chunked_bit_exact(api, ref, case, chunk, monkeypatch):
+    """Sample-aligned chunks (copy of chunk c + 1 overlapping the binning of
+    chunk c) with carry-in sums: still bit-identical to the reference."""
+    from paper_1510_04439_b200 import synth
+    monkeypatch.setenv("DFPCA_BIN_CHUNK_OBS", chunk)
+    sd = {"nodes2d": lambda: synth.grid_nodes(2, 12, 30, 0.2),
+          "random2d": lambda: synth.random_points(2, 13, 40, 25, 0.3),
+          "empty_samples": lambda: synth.random_points(2, 9, 30, 5, 0.3)}[case]()
+    if case == "empty_samples":
+        counts = np.diff(sd.offsets)
+        counts[[0, 7, 8, 29]] = 0
+        keep = np.concatenate([np.arange(sd.offsets[i], sd.offsets[i] + counts[i]) for i in range(counts.size)])
+        sd.offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        sd.values = np.ascontiguousarray(sd.values[keep])
+        sd.coords = np.ascontiguousarray(sd.coords.reshape(-1, 2)[keep].ravel())
+    grid, g, r = _bin_both(api, ref, sd)
+    _assert_binned_equal(g, r)
+    # an observation outside the hull in a later chunk: same error, context reusable
+    bad = sd.dataset()
+    last = max(i for i, smp in enumerate(bad.samples) if smp.n_obs() > 0)
+    bad.samples[last].coords = np.array(bad.samples[last].coords, copy=True)
+    bad.samples[last].coords[-1] = 7.0
+    bad.invalidate()
+    with pytest.raises(api.Error) as ei:
+        api.linear_bin(bad, grid)
+    assert ei.value.name() == "ObservationOutsideGrid"
+    _assert_binned_equal(api.linear_bin(sd.dataset(), grid, api.BinOptions(True, True)), r)
+
+
 def test_binning_boundary_and_outside(api):
     grid = api.EvaluationGrid.uniform([0.0], [1.0], [5])
     data = api.FunctionalDataset(1, [api.Sample("a", np.array([0.0, 1.0, 0.125]), np.array([1.0, 2.0, 3.0]))])

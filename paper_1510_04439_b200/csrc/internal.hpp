@@ -198,6 +198,10 @@ struct dfpca_binned {
   std::vector<std::int64_t> sample_index;           // n_pair
   std::vector<double> pair_weight_h;                // n_pair
   std::vector<std::int64_t> sample_sizes;           // n_samples
+  // pair-grid route (pairs.cu), decided on first use: -1 unknown, 0 SYRK,
+  // 1 sparse records; pair_nnz = nonzeros of every per-sample mass grid
+  mutable int pair_route = -1;
+  mutable std::vector<std::int64_t> pair_nnz;
 };
 
 namespace dfpca_gpu {

@@ -22,6 +22,11 @@ struct PairWindow {
   i64 tm_end = -1;
 };
 
+// Whether the pair grids of b take the sparse route (sum_i nnz_i^2 records,
+// bit-identical to the reference) rather than the SYRK; the same answer on
+// every rank.  The sparse route computes whole windows: no exchange.
+bool pair_grids_sparse(dfpca_context* ctx, const dfpca_binned* b);
+
 void build_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, double* pv,
                       const PairWindow* win = nullptr,
                       const std::function<void(bool pw_from_syrk)>& exchange = {});

@@ -994,7 +994,7 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
     if (sa < sb)
       build_pair_grids(ctx, b, pwp, pvp, &win,
                        [&](bool pw_syrk) { shard->exchange_pairs(pw_syrk ? pwp : nullptr, pvp, pw_syrk); });
-    else  // idle rank: still takes part in the exchange
+    else if (!pair_grids_sparse(ctx, b))  // idle rank: still takes part in the exchange
       shard->exchange_pairs(nullptr, nullptr, !shared && !b->identical_mass);
   } else {
     build_pair_grids(ctx, b, shared ? nullptr : pw.get(), pv.get());

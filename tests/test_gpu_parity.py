@@ -178,6 +178,38 @@ def test_pair_grids(api, ref, case):
     assert np.array_equal(pw == 0, rpw == 0)
 
 
+@pytest.mark.parametrize("case", ["sparse_masked", "random2d", "random1d", "random3d"])
+def test_pair_grids_sparse_route_bit_exact(api, ref, case, monkeypatch):
+    """The sparse route (per-sample nonzeros, (s, t) records sorted stably,
+    terms added in sample order, then the band) reproduces the reference's
+    pair grids bit for bit -- both of them, every entry."""
+    from paper_1510_04439_b200 import synth
+    monkeypatch.setenv("DFPCA_PAIRS", "sparse")
+    sd = {"sparse_masked": lambda: synth.sparse_masked(24, 150, 0.3),
+          "random2d": lambda: synth.random_points(2, 11, 25, 12, 0.3),
+          "random1d": lambda: synth.random_points(1, 21, 12, 7, 0.2),
+          "random3d": lambda: synth.random_points(3, 5, 10, 8, 0.4)}[case]()
+    grid, g, r = _bin_both(api, ref, sd)
+    pw, pv = api.pair_grids(g)
+    rpw, rpv = ref.pair_grids(r)
+    assert bit_equal(pw, rpw) and bit_equal(pv, rpv)
+
+
+@pytest.mark.parametrize("route", ["sparse", "dense"])
+@pytest.mark.parametrize("case", ["2d_random", "2d_masked_sparse", "1d"])
+def test_covariance_both_pair_routes(api, ref, case, route, monkeypatch):
+    from paper_1510_04439_b200 import synth
+    monkeypatch.setenv("DFPCA_PAIRS", route)
+    sd = COV_CASES[case](synth)
+    grid, g, r = _bin_both(api, ref, sd, True, True)
+    h = api.Bandwidth(sd.h)
+    mean_r = ref.fft_local_linear(r, (sd.axes, sd.mask), sd.h, 0)
+    mean_g = api.fft_local_linear(g, grid, h, api.MomentTarget.Mean)
+    cov_g = api.fft_covariance(g, grid, h, mean_g).values
+    cov_r = ref.fft_covariance(r, (sd.axes, sd.mask), sd.h, mean_r)
+    assert rel_surface_diff(cov_g, cov_r) <= TOL
+
+
 def test_pair_grids_two_observations_exact(api):
     # tests/test_fft_smoother.cpp:161-186
     grid = api.EvaluationGrid.uniform([0.0], [1.0], [5])

@@ -70,6 +70,20 @@ def test_sharded_general_path_forced(api, monkeypatch):
     assert bit_equal(many.values, one)
 
 
+@pytest.mark.parametrize("route", ["sparse", "dense"])
+def test_sharded_pair_routes(api, route, monkeypatch):
+    """Both pair-grid routes on slabs: the sparse one builds every window
+    whole (no exchange, idle ranks skip it too), bit-identical to one GPU."""
+    from paper_1510_04439_b200 import synth
+    monkeypatch.setenv("DFPCA_PAIRS", route)
+    sd = synth.sparse_masked(32, 300, 0.3)
+    grid, b, h, mean = _setup(api, sd)
+    one = api.fft_covariance(b, grid, h, mean).values
+    for world in (3, 9):
+        many = api.fft_covariance_emulated(b, grid, h, mean, world)
+        assert bit_equal(many.values, one), f"{route} x{world}"
+
+
 def test_sharded_with_idle_ranks(api):
     """More ranks than 128-row units: the surplus ranks hold empty slabs and
     still take part in both exchanges."""

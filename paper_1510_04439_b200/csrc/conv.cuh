@@ -69,6 +69,11 @@ struct TPhase2Spec {
   const double* taps[2][3];
   int R[2];
   bool value_only = false;  // pw unused: only the 3 value t-partials
+  // Upper-triangle trim: row s (global pair-grid row s_base + s, plane
+  // (s_base + s) / rn) computes only t1 >= plane - t1_margin -- the
+  // s-phase (View::tri) never reads the planes below.  t1_margin < 0: all.
+  i64 s_base = 0, rn = 1;
+  int t1_margin = -1;
 };
 // Returns false when the plane does not fit (caller uses run_pass instead).
 bool run_tphase2(dfpca_context* ctx, const TPhase2Spec& spec);

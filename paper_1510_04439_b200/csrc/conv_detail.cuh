@@ -26,6 +26,11 @@ struct Taps2P {
 struct TPhaseOut {
   double* m[6];
   double* v[3];
+  // upper-triangle trim (t1_margin >= 0): pair-grid row s (global s_base + s)
+  // produces t1 planes >= (s_base + s) / rn - t1_margin only
+  long long s_base;
+  long long rn;
+  int t1_margin;
 };
 
 // Tiled pass along one axis with radius R (R <= kMaxTemplR, n <= kMaxN).

@@ -301,11 +301,12 @@ __global__ void __launch_bounds__(kThreads) k_pass_rows(View in, View o0, View o
 // straight to HBM, coalesced along t2.  Both axes use the same template
 // radius R (the narrower axis is zero-padded).
 template <int R, int ORD>
-__device__ inline void tp_conv_rows(const double* X, double* Y, int n1, int n2, int ld, const Taps2P& tp) {
-  // Y[l][j] = sum_o taps[t2][order][o] X[l][j+o]  (lines l = t1, axis t2)
+__device__ inline void tp_conv_rows(const double* X, double* Y, int n1, int n2, int ld, const Taps2P& tp, int l0) {
+  // Y[l][j] = sum_o taps[t2][order][o] X[l][j+o]  (lines l = t1 >= l0, axis t2)
   const int nb = (n2 + kJBr - 1) / kJBr;
-  for (int item = threadIdx.x; item < n1 * nb; item += blockDim.x) {
-    const int l = item % n1, j0 = (item / n1) * kJBr;
+  const int nl = n1 - l0;
+  for (int item = threadIdx.x; item < nl * nb; item += blockDim.x) {
+    const int l = l0 + item % nl, j0 = (item / nl) * kJBr;
     double acc[kJBr];
 #pragma unroll
     for (int jj = 0; jj < kJBr; ++jj) acc[jj] = 0.0;
@@ -327,11 +328,11 @@ __device__ inline void tp_conv_rows(const double* X, double* Y, int n1, int n2, 
 
 template <int R, int NO>
 __device__ inline void tp_conv_cols(const double* Y, int n1, int n2, int ld, double* const* outs, i64 row_off,
-                                    const Taps2P& tp) {
-  // out_r[j][c] = sum_o taps[t1][r][o] Y[j+o][c]   (axis t1, columns c = t2)
-  const int nb = (n1 + kJBr - 1) / kJBr;
+                                    const Taps2P& tp, int j_lo) {
+  // out_r[j][c] = sum_o taps[t1][r][o] Y[j+o][c]   (axis t1 rows j >= j_lo, columns c = t2)
+  const int nb = (n1 - j_lo + kJBr - 1) / kJBr;
   for (int item = threadIdx.x; item < n2 * nb; item += blockDim.x) {
-    const int c = item % n2, j0 = (item / n2) * kJBr;
+    const int c = item % n2, j0 = j_lo + (item / n2) * kJBr;
     double acc[NO][kJBr];
 #pragma unroll
     for (int r = 0; r < NO; ++r)
@@ -373,11 +374,18 @@ __global__ void __launch_bounds__(kThreads) k_tphase2(const double* __restrict__
   // Planes of this CTA in order: (s, pw), (s, pv), (s + grid, pw), ... (only
   // the pv planes when value_only); the next plane is copied into the other X
   // buffer (cp.async, 8-byte granules because of the bank-conflict padding)
-  // while the current one is convolved.
+  // while the current one is convolved.  With the upper-triangle trim, row s
+  // outputs t1 >= j_lo(s) and needs input lines t1 >= j_lo(s) - R.
+  auto j_lo_of = [&](i64 s) -> int {
+    if (out.t1_margin < 0) return 0;
+    const long long lo = (out.s_base + s) / out.rn - out.t1_margin;
+    return lo <= 0 ? 0 : (lo >= n1 ? n1 : static_cast<int>(lo));
+  };
   auto issue = [&](i64 s, int pass, int buf) {
     const double* src = (pass ? pv : pw) + s * plane;
     double* X = sm + buf * pe;
-    for (int e = threadIdx.x; e < plane; e += blockDim.x) cp_async_c8(X + (e / n2) * ld + e % n2, src + e, 8);
+    const int l0 = j_lo_of(s) - R > 0 ? j_lo_of(s) - R : 0;
+    for (int e = l0 * n2 + threadIdx.x; e < plane; e += blockDim.x) cp_async_c8(X + (e / n2) * ld + e % n2, src + e, 8);
   };
   const int first_pass = value_only ? 1 : 0;
   i64 s = blockIdx.x;
@@ -396,29 +404,31 @@ __global__ void __launch_bounds__(kThreads) k_tphase2(const double* __restrict__
     const double* X = sm + buf * pe;
     const i64 off = s * plane;
     const int max_order = pass == 0 ? 2 : 1;
+    const int j_lo = j_lo_of(s);
+    const int l0 = j_lo - R > 0 ? j_lo - R : 0;
     for (int r2 = 0; r2 <= max_order; ++r2) {
-      if (r2 == 0) tp_conv_rows<R, 0>(X, Y, n1, n2, ld, tp);
-      else if (r2 == 1) tp_conv_rows<R, 1>(X, Y, n1, n2, ld, tp);
-      else tp_conv_rows<R, 2>(X, Y, n1, n2, ld, tp);
+      if (r2 == 0) tp_conv_rows<R, 0>(X, Y, n1, n2, ld, tp, l0);
+      else if (r2 == 1) tp_conv_rows<R, 1>(X, Y, n1, n2, ld, tp, l0);
+      else tp_conv_rows<R, 2>(X, Y, n1, n2, ld, tp, l0);
       __syncthreads();
       if (pass == 0) {
         if (r2 == 0) {
           double* o[3] = {out.m[0], out.m[1], out.m[2]};
-          tp_conv_cols<R, 3>(Y, n1, n2, ld, o, off, tp);
+          tp_conv_cols<R, 3>(Y, n1, n2, ld, o, off, tp, j_lo);
         } else if (r2 == 1) {
           double* o[2] = {out.m[3], out.m[4]};
-          tp_conv_cols<R, 2>(Y, n1, n2, ld, o, off, tp);
+          tp_conv_cols<R, 2>(Y, n1, n2, ld, o, off, tp, j_lo);
         } else {
           double* o[1] = {out.m[5]};
-          tp_conv_cols<R, 1>(Y, n1, n2, ld, o, off, tp);
+          tp_conv_cols<R, 1>(Y, n1, n2, ld, o, off, tp, j_lo);
         }
       } else {
         if (r2 == 0) {
           double* o[2] = {out.v[0], out.v[1]};
-          tp_conv_cols<R, 2>(Y, n1, n2, ld, o, off, tp);
+          tp_conv_cols<R, 2>(Y, n1, n2, ld, o, off, tp, j_lo);
         } else {
           double* o[1] = {out.v[2]};
-          tp_conv_cols<R, 1>(Y, n1, n2, ld, o, off, tp);
+          tp_conv_cols<R, 1>(Y, n1, n2, ld, o, off, tp, j_lo);
         }
       }
       __syncthreads();
@@ -485,6 +495,9 @@ void launch_tphase2(dfpca_context* ctx, const TPhase2Spec& s, const Taps2P& tp) 
   TPhaseOut out;
   for (int i = 0; i < 6; ++i) out.m[i] = s.mass_out[i];
   for (int i = 0; i < 3; ++i) out.v[i] = s.value_out[i];
+  out.s_base = s.s_base;
+  out.rn = s.rn;
+  out.t1_margin = s.t1_margin;
   const int n1 = static_cast<int>(s.n1), n2 = static_cast<int>(s.n2);
   const std::size_t smem = sizeof(double) * 3 * n1 * (n2 + 1);
   const unsigned grid = persistent_grid(ctx, k_tphase2<R>, smem, s.rows);

@@ -1032,6 +1032,10 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
       tpart_store.push_back(std::make_unique<DevBuf<double>>(static_cast<std::size_t>(LR * G)));
       tpart[{o, 1}] = tpart_store.back()->get();
     }
+    // test aid: NaN-fill the t-partials so an entry read without being
+    // written (the upper-triangle trims) poisons the result
+    if (std::getenv("DFPCA_POISON"))
+      for (auto& buf : tpart_store) DFPCA_CUDA(cudaMemsetAsync(buf->get(), 0xff, buf->bytes(), st));
   }
   // chunk rows (s nodes) so intermediates stay bounded
   const i64 budget_elems = std::max<i64>(G, (i64(1) << 31) / 8);  // ~2 GiB per level array set
@@ -1083,6 +1087,15 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
       for (int ax = 0; ax < 2; ++ax) {
         ts.R[ax] = taps[2 + ax].R;
         for (int r = 0; r < 3; ++r) ts.taps[ax][r] = taps[2 + ax].t[r].data();
+      }
+      // the s-phase below runs in one column chunk with per-tile row trimming
+      // (View::tri): a t-partial entry (s, t) is read only if plane(s) <=
+      // plane(t) + R_s1 + the planes one 64-column tile spans
+      const i64 s_chunk = std::max<i64>(1, std::min<i64>(G, budget_elems / std::max<i64>(G, 1) / 4));
+      if (s_chunk >= G - col_lo) {
+        ts.s_base = ha * rn + s0;
+        ts.rn = rn;
+        ts.t1_margin = static_cast<int>(taps[0].R + (64 + rn - 1) / rn);
       }
       if (run_tphase2(ctx, ts)) continue;
     }

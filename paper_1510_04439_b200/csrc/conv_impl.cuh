@@ -43,6 +43,9 @@ __device__ inline void mbar_arrive_tx(std::uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
                : "memory");
 }
+__device__ inline void mbar_arrive(std::uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(bar)) : "memory");
+}
 __device__ inline void mbar_wait(std::uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -100,10 +103,18 @@ __device__ __forceinline__ void conv_block(const double* __restrict__ col, int j
   }
 }
 
+// BULK runs warp-specialized: kThreads compute threads plus one producer warp
+// that issues the row copies of tile k + 2 as soon as the compute warps have
+// released its buffer (an "empty" mbarrier per buffer, one arrival per compute
+// warp), so no CTA-wide barrier separates the tiles.
+constexpr int kProducerThreads = 32;
+
 template <int R, int NO, int JB, bool BULK>
-__global__ void __launch_bounds__(kThreads) k_pass_cols(View in, View o0, View o1, View o2, TapsP tp) {
+__global__ void __launch_bounds__(kThreads + kProducerThreads) k_pass_cols(View in, View o0, View o1, View o2,
+                                                                           TapsP tp) {
   extern __shared__ __align__(128) double sm[];  // [2][n][kTC]
   __shared__ __align__(8) std::uint64_t bar[2];
+  __shared__ __align__(8) std::uint64_t empty_bar[2];
   __shared__ TileMeta meta[2];
   constexpr int kGroups = kThreads / kTC;
   const int n = static_cast<int>(in.n);
@@ -172,34 +183,12 @@ __global__ void __launch_bounds__(kThreads) k_pass_cols(View in, View o0, View o
       }
     }
   };
-  if constexpr (BULK) {
-    if (threadIdx.x == 0) {
-      mbar_init(&bar[0], 1);
-      mbar_init(&bar[1], 1);
-      mbar_fence_init();
-    }
-    __syncthreads();
-  }
-  int buf = 0;
-  unsigned phase = 0;  // bit b: parity of the next completion of bar[b]
-  int tile = blockIdx.x;
-  if (tile < n_tiles && (!BULK || threadIdx.x < 32)) issue(tile, 0);
-  if constexpr (!BULK) cp_async_commit_c();
   const int c = threadIdx.x % kTC;
   const int g = threadIdx.x / kTC;
-  for (; tile < n_tiles; tile += gridDim.x) {
-    const int next = tile + gridDim.x;
-    if (next < n_tiles && (!BULK || threadIdx.x < 32)) issue(next, buf ^ 1);
-    if constexpr (BULK) {
-      mbar_wait(&bar[buf], (phase >> buf) & 1u);
-      phase ^= 1u << buf;
-    } else {
-      cp_async_commit_c();
-      cp_async_wait_c<1>();
-      __syncthreads();
-    }
-    const TileMeta mt = meta[buf];
-    const double* col = sm + buf * tile_elems + c;
+  // convolve the staged tile in buffer b (compute threads)
+  auto compute = [&](int b) {
+    const TileMeta mt = meta[b];
+    const double* col = sm + b * tile_elems + c;
     if (mt.c0 + c < inner) {
       const i64 cb = mt.c0 + c;
       double* b0 = o0.p + mt.ob * o0.os + cb;
@@ -233,10 +222,51 @@ __global__ void __launch_bounds__(kThreads) k_pass_cols(View in, View o0, View o
         }
       }
     }
-    __syncthreads();  // everyone is done with this buffer before it is refilled
-    buf ^= 1;
+  };
+  if constexpr (BULK) {
+    constexpr unsigned kComputeWarps = kThreads / 32;
+    if (threadIdx.x == 0) {
+      mbar_init(&bar[0], 1);
+      mbar_init(&bar[1], 1);
+      mbar_init(&empty_bar[0], kComputeWarps);
+      mbar_init(&empty_bar[1], kComputeWarps);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x >= kThreads) {  // producer warp
+      int k = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+        const int b = k & 1;
+        if (k >= 2) mbar_wait(&empty_bar[b], static_cast<unsigned>((k >> 1) - 1) & 1u);
+        issue(tile, b);
+      }
+      return;
+    }
+    int k = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+      const int b = k & 1;
+      mbar_wait(&bar[b], static_cast<unsigned>(k >> 1) & 1u);
+      compute(b);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[b]);
+    }
+  } else {
+    int buf = 0;
+    int tile = blockIdx.x;
+    if (tile < n_tiles) issue(tile, 0);
+    cp_async_commit_c();
+    for (; tile < n_tiles; tile += gridDim.x) {
+      const int next = tile + gridDim.x;
+      if (next < n_tiles) issue(next, buf ^ 1);
+      cp_async_commit_c();
+      cp_async_wait_c<1>();
+      __syncthreads();
+      compute(buf);
+      __syncthreads();  // everyone is done with this buffer before it is refilled
+      buf ^= 1;
+    }
+    cp_async_wait_c<0>();
   }
-  if constexpr (!BULK) cp_async_wait_c<0>();
 }
 
 // ----------------------------------------------------------- lines kernel --
@@ -442,10 +472,10 @@ __global__ void __launch_bounds__(kThreads) k_tphase2(const double* __restrict__
 
 // ------------------------------------------------------------- launchers --
 template <typename K>
-inline unsigned persistent_grid(dfpca_context* ctx, K kern, std::size_t smem, i64 work) {
+inline unsigned persistent_grid(dfpca_context* ctx, K kern, std::size_t smem, i64 work, int threads = kThreads) {
   allow_smem(kern, smem);  // dynamic + static shared memory may cross 48 KB even when smem alone does not
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   return static_cast<unsigned>(
       std::max<i64>(1, std::min<i64>(work, static_cast<i64>(std::max(per_sm, 1)) * ctx->sm_count)));
 }
@@ -455,8 +485,9 @@ void launch_cols(dfpca_context* ctx, const PassSpec& s, const View& o1, const Vi
   const View& in = s.in;
   const i64 tiles = in.outer * ((in.inner + kTC - 1) / kTC);
   const std::size_t smem = sizeof(double) * 2 * kTC * in.n;
-  const unsigned grid = persistent_grid(ctx, k_pass_cols<R, NO, JB, BULK>, smem, tiles);
-  DFPCA_LAUNCH(ctx, (k_pass_cols<R, NO, JB, BULK>), grid, kThreads, smem, in, s.out[0], o1, o2, tp);
+  const int threads = BULK ? kThreads + kProducerThreads : kThreads;
+  const unsigned grid = persistent_grid(ctx, k_pass_cols<R, NO, JB, BULK>, smem, tiles, threads);
+  DFPCA_LAUNCH(ctx, (k_pass_cols<R, NO, JB, BULK>), grid, threads, smem, in, s.out[0], o1, o2, tp);
 }
 
 template <int R, int NO>

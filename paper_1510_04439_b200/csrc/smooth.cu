@@ -1038,7 +1038,11 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
       for (auto& buf : tpart_store) DFPCA_CUDA(cudaMemsetAsync(buf->get(), 0xff, buf->bytes(), st));
   }
   // chunk rows (s nodes) so intermediates stay bounded
-  const i64 budget_elems = std::max<i64>(G, (i64(1) << 31) / 8);  // ~2 GiB per level array set
+  // ~2 GiB per level array set (DFPCA_CHUNK_GIB overrides: larger chunks mean
+  // fewer, longer pass launches at d = 3)
+  i64 budget_bytes = i64(1) << 31;
+  if (const char* e = std::getenv("DFPCA_CHUNK_GIB")) budget_bytes = std::max<i64>(1, std::atoll(e)) << 30;
+  const i64 budget_elems = std::max<i64>(G, budget_bytes / 8);
   i64 sc = std::max<i64>(1, std::min<i64>(G, budget_elems / std::max<i64>(G, 1) / 4));
   std::vector<TreeAxis> taxes;
   for (int k = p - 1; k >= d; --k) taxes.push_back({k, k - d});

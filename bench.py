@@ -261,23 +261,30 @@ def run_io(args):
     d2h = off.nbytes + coords.nbytes + values.nbytes + sum(len(s.id) for s in ds.samples) + off.nbytes
     t_e2e = float(np.mean(e2e))
     os.unlink(path)
-    # roofline: k_parse_lines, HBM-bound; algorithmic bytes = every text byte of
-    # the data lines once + 2 newline offsets read + (record flag, id start,
-    # id length, d + 1 doubles) written per line
-    nl_bytes = 16 * rows
-    out_bytes = (8 + 8 + 4 + 8 * 3) * rows
-    parse_ms = kstats.get("k_parse_lines", (None, 0))[0]
+    # roofline of the dominant device kernel (HBM-bound byte work).  Algorithmic
+    # bytes per launch: k_split_lines reads every text byte once plus two
+    # newline offsets per line and writes the record flag, id start / length
+    # and the F field bounds (8 + 8 + 4 + 8F B per line); k_parse_fields reads,
+    # per number field, its bounds, the line start and its text, and writes the
+    # value (the field text is ~ the text bytes minus ids and separators)
+    F = 4
+    models = {"k_split_lines": size + rows * (16 + 8 + 8 + 4 + 8 * F),
+              "k_parse_fields": size + rows * 3 * (8 + 8 + 8)}
+    top = max((k for k in models if k in kstats), key=lambda k: kstats[k][0], default=None)
     peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
     hbm = peaks.get("hbm_gbs", 6548.8)
     roof = None
-    if parse_ms:
-        alg = size + nl_bytes + out_bytes
-        ach = alg / (parse_ms / 1e3) / 1e9
-        tr, tr_src = ncu_traffic("k_parse_lines", "io_r*_ncu_full_summary.txt")
-        roof = {"kernel": "k_parse_lines", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+    if top:
+        ms = kstats[top][0]
+        alg = models[top]
+        ach = alg / (ms / 1e3) / 1e9
+        tr, tr_src = ncu_traffic(top, "io_r*_ncu_full_summary.txt")
+        roof = {"kernel": top, "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
                 "frac": ach / hbm, "traffic": tr, "traffic_source": tr_src,
-                "algorithmic_bytes_per_launch": alg, "kernel_ms": parse_ms,
-                "model": "text bytes + 16 B newline offsets + 44 B record outputs per row (d=2)",
+                "algorithmic_bytes_per_launch": alg, "kernel_ms": ms,
+                "model": {"k_split_lines": "text bytes + 16 B newline offsets + (28 + 8F) B outputs per row",
+                          "k_parse_fields": "text bytes + 24 B (bounds, line start, value) per number field"},
+                "share_of_device_stages": ms / (t_dev * 1e3),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
     cpu = None
     if not args.no_cpu_baseline:

@@ -7,11 +7,13 @@
 //              to HBM chunk by chunk (pread and H2D overlap);
 //   lines      newline positions: per-tile popcounts of a SWAR byte match,
 //              a device scan, then an ordered write (k_nl_count / k_nl_write);
-//   records    one thread per line: strip '\r', skip empty lines, split with
-//              the reference's field rule, check the field count, parse the
-//              d + 1 numbers with numparse.cuh (exact, strtod-identical) --
-//              the first failing (line, field) is kept with an atomicMin, so
-//              the error is the one the sequential reader raises first;
+//   records    one thread per line strips '\r', skips empty lines, splits
+//              with the reference's field rule and checks the field count
+//              (k_split_lines); then one thread per (number column, line)
+//              parses a field with numparse.cuh (exact, strtod-identical;
+//              k_parse_fields) -- the first failing (line, field) is kept with
+//              an atomicMin, so the error is the one the sequential reader
+//              raises first;
 //   samples    lines whose id differs from the previous record's start a run;
 //              run heads are grouped by an exact string sort (stable LSD radix
 //              passes over 8-byte chunks, then the length), numbered in order
@@ -259,51 +261,17 @@ struct Lines {
 
 __device__ __forceinline__ bool ws(char c) { return numparse::is_space(c); }
 
-// Field k of [st, en): delimiter mode splits at every delim (empty fields
-// kept, io.hpp:63-70); whitespace mode (delim == 0) takes runs of non-blanks
-// (io.hpp:56-61).  Returns the number of fields; fills the bounds of `want`.
-__device__ int split_field(const char* t, i64 st, i64 en, char delim, int want, i64& fs, i64& fe) {
-  int nf = 0;
-  if (delim) {
-    i64 a = st;
-    for (i64 i = st;; ++i) {
-      if (i == en || t[i] == delim) {
-        if (nf == want) {
-          fs = a;
-          fe = i;
-        }
-        ++nf;
-        a = i + 1;
-        if (i == en) break;
-      }
-    }
-    return nf;
-  }
-  i64 i = st;
-  while (true) {
-    while (i < en && ws(t[i])) ++i;
-    if (i >= en) break;
-    const i64 a = i;
-    while (i < en && !ws(t[i])) ++i;
-    if (nf == want) {
-      fs = a;
-      fe = i;
-    }
-    ++nf;
-  }
-  return nf;
-}
-
-struct ParseOut {
-  i64* is_rec;   // per line
-  i64* id_start;  // per line
-  int* id_len;    // per line
-  double* vals;   // per line x (d + 1)
-  u64* err;       // (line << 8) | code: 0 field count, 1 + k field k + 1, 255 internal
+struct SplitOut {
+  i64* is_rec;       // per line: 1 if not empty
+  i64* id_start;     // per line
+  int* id_len;       // per line
+  u64* fb;           // per line x F: (start << 32) | end, relative to the line start; fb[L F] = ~0: bad count
+  u64* err;          // (line << 8) | code: 0 field count, 1 + k field k + 1, 255 internal
 };
 
-__global__ void __launch_bounds__(kThreads) k_parse_lines(Lines ln, i64 n_lines, int F, char delim, ParseOut o) {
-  const int nv = F - 1;
+// Pass 1, one thread per line: one scan of the line's bytes records the
+// field bounds (the reference's split rule) and checks the field count.
+__global__ void __launch_bounds__(kThreads) k_split_lines(Lines ln, i64 n_lines, int F, char delim, SplitOut o) {
   for (i64 L = 1 + blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; L < n_lines;
        L += static_cast<i64>(gridDim.x) * blockDim.x) {
     i64 st, en;
@@ -313,40 +281,137 @@ __global__ void __launch_bounds__(kThreads) k_parse_lines(Lines ln, i64 n_lines,
       continue;
     }
     o.is_rec[L] = 1;
-    i64 fs = 0, fe = 0;
-    const int nf = split_field(ln.text, st, en, delim, 0, fs, fe);
+    u64* fb = o.fb + L * F;
+    const char* t = ln.text;
+    int nf = 0;
+    if (delim) {
+      i64 a = st;
+      for (i64 i = st;; ++i) {
+        const bool end = i == en;
+        if (end || t[i] == delim) {
+          if (nf < F) fb[nf] = (static_cast<u64>(a - st) << 32) | static_cast<u64>(i - st);
+          ++nf;
+          a = i + 1;
+          if (end) break;
+        }
+      }
+    } else {
+      i64 i = st;
+      while (true) {
+        while (i < en && ws(t[i])) ++i;
+        if (i >= en) break;
+        const i64 a = i;
+        while (i < en && !ws(t[i])) ++i;
+        if (nf < F) fb[nf] = (static_cast<u64>(a - st) << 32) | static_cast<u64>(i - st);
+        ++nf;
+      }
+    }
     if (nf != F) {
-      atomicMin(o.err, (static_cast<u64>(L) << 8) | 0ull);
+      fb[0] = ~0ull;
+      atomicMin(o.err, static_cast<u64>(L) << 8);
       continue;
     }
-    o.id_start[L] = fs;
-    o.id_len[L] = static_cast<int>(fe - fs);
-    // walk the remaining fields in order
-    i64 pos = fe;
-    for (int k = 0; k < nv; ++k) {
-      i64 a, b;
-      if (delim) {
-        a = pos + 1;
-        b = a;
-        while (b < en && ln.text[b] != delim) ++b;
+    o.id_start[L] = st + static_cast<i64>(fb[0] >> 32);
+    o.id_len[L] = static_cast<int>((fb[0] & 0xffffffffull) - (fb[0] >> 32));
+  }
+}
+
+// Fast path of numparse::parse_double for the common token shape
+// [+-]digits[.digits][(e|E)[+-]digits] with at most 19 mantissa digits, no
+// blanks, at most 32 bytes: the token is read with aligned 8-byte loads into
+// registers and scanned there (no per-byte memory round trip), giving the same
+// (w, q) as the general parser and the same round_decimal; anything else --
+// or an undecided rounding -- returns false and the general parser runs.
+__device__ __forceinline__ bool fast_decimal(const char* text, i64 a, i64 len, double* out) {
+  if (len <= 0 || len > 32) return false;
+  const u64* base = reinterpret_cast<const u64*>(text + (a & ~i64{7}));
+  const int sh = static_cast<int>(a & 7) * 8;
+  const int nw = static_cast<int>(((a & 7) + len + 7) >> 3);
+  u64 w[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) w[k] = k < nw ? base[k] : 0ull;
+  u64 t[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) t[k] = sh ? ((w[k] >> sh) | (w[k + 1] << (64 - sh))) : w[k];
+  u64 mant = 0;
+  int nd = 0, frac = 0, ev = 0, ne = 0, estart = -1;
+  bool dot = false, expo = false, neg = false, eneg = false, ok = true;
+#pragma unroll
+  for (int kw = 0; kw < 4; ++kw) {
+    if (kw * 8 >= len) break;  // lanes of a warp parse one column: lengths alike
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = kw * 8 + j;
+      if (i >= len) break;
+      const unsigned c = static_cast<unsigned>((t[kw] >> (8 * j)) & 0xffu);
+      const unsigned dg = c - '0';
+      if (!expo) {
+        if (dg < 10u) {
+          mant = mant * 10u + dg;
+          ++nd;
+          frac += dot ? 1 : 0;
+        } else if (c == '.' && !dot) {
+          dot = true;
+        } else if ((c == '-' || c == '+') && i == 0) {
+          neg = c == '-';
+        } else if ((c == 'e' || c == 'E') && nd > 0) {
+          expo = true;
+          estart = i + 1;
+        } else {
+          ok = false;
+        }
       } else {
-        a = pos;
-        while (a < en && ws(ln.text[a])) ++a;
-        b = a;
-        while (b < en && !ws(ln.text[b])) ++b;
+        if (dg < 10u) {
+          ev = ev * 10 + static_cast<int>(dg);
+          ++ne;
+        } else if ((c == '-' || c == '+') && i == estart) {
+          eneg = c == '-';
+        } else {
+          ok = false;
+        }
       }
-      pos = b;
+    }
+  }
+  if (!ok || nd == 0 || nd > 19 || (expo && (ne == 0 || ne > 4))) return false;
+  const u64 sign = neg ? (u64{1} << 63) : 0ull;
+  if (mant == 0) {
+    *out = numparse::from_bits(sign);
+    return true;
+  }
+  const int q = (eneg ? -ev : ev) - frac;
+  if (q < numparse::kQMin || q > numparse::kQMax) return false;
+  const numparse::Rounded r = numparse::round_decimal(mant, q, d_pow5);
+  if (r.ambiguous) return false;
+  return numparse::finish(sign, r.m, r.e2, out) == numparse::kOk;
+}
+
+// Pass 2, one thread per (number column k, line): 32 consecutive lines of
+// one column per warp, so the lanes parse tokens of like shape.  Values are
+// stored column-major, vals[k * n_lines + L].
+__global__ void __launch_bounds__(kThreads) k_parse_fields(Lines ln, i64 n_lines, int F, const i64* is_rec,
+                                                           const u64* fb, double* vals, u64* err) {
+  const int nv = F - 1;
+  const i64 per = n_lines - 1;
+  for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < per * nv;
+       e += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(e / per);
+    const i64 L = 1 + (e - static_cast<i64>(k) * per);
+    if (!is_rec[L] || fb[L * F] == ~0ull) continue;
+    const u64 f = fb[L * F + 1 + k];
+    const i64 st = L == 0 ? 0 : ln.nl[L - 1] + 1;
+    const i64 a = st + static_cast<i64>(f >> 32), b = st + static_cast<i64>(f & 0xffffffffull);
+    double v = 0.0;
+    if (!fast_decimal(ln.text, a, b - a, &v)) {
       // strtod stops at an embedded NUL (the reference passes c_str())
       i64 z = a;
       while (z < b && ln.text[z] != '\0') ++z;
-      double v = 0.0;
       const int stt = numparse::parse_double(ln.text + a, static_cast<int>(z - a), d_pow5, &v);
       if (stt != numparse::kOk) {
-        atomicMin(o.err, (static_cast<u64>(L) << 8) | (stt == numparse::kInternal ? 255ull : static_cast<u64>(1 + k)));
-        break;
+        atomicMin(err, (static_cast<u64>(L) << 8) | (stt == numparse::kInternal ? 255ull : static_cast<u64>(1 + k)));
+        continue;
       }
-      o.vals[L * nv + k] = v;
     }
+    vals[static_cast<i64>(k) * n_lines + L] = v;
   }
 }
 
@@ -466,16 +531,15 @@ __global__ void k_run_base(const i64* sorted_heads, const u64* sorted_sample, co
 }
 
 __global__ void k_scatter(const i64* head, const i64* head_idx, const i64* run_base, const i64* head_rec,
-                          const i64* rec_line, const double* vals, i64 n_rec, int d, double* coords,
+                          const i64* rec_line, const double* vals, i64 n_lines, i64 n_rec, int d, double* coords,
                           double* values) {
-  const int nv = d + 1;
   for (i64 r = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; r < n_rec;
        r += static_cast<i64>(gridDim.x) * blockDim.x) {
     const i64 h = head_idx[r] + head[r] - 1;
     const i64 out = run_base[h] + (r - head_rec[h]);
-    const double* v = vals + rec_line[r] * nv;
-    for (int k = 0; k < d; ++k) coords[out * d + k] = v[k];
-    values[out] = v[d];
+    const i64 L = rec_line[r];
+    for (int k = 0; k < d; ++k) coords[out * d + k] = vals[k * n_lines + L];
+    values[out] = vals[static_cast<i64>(d) * n_lines + L];
   }
 }
 
@@ -614,10 +678,15 @@ dfpca_table* parse_table(dfpca_context* ctx, const std::string& name, const char
   DFPCA_CUDA(cudaMemsetAsync(err.get(), 0xff, sizeof(u64), st));
   DFPCA_CUDA(cudaMemsetAsync(is_rec.get(), 0, sizeof(i64), st));  // the header line
   Lines ln{d_text, S, nl.get(), n_nl};
-  if (n_lines > 1)
-    DFPCA_LAUNCH(ctx, k_parse_lines, grid_for(n_lines - 1, kThreads, static_cast<i64>(ctx->sm_count) * 16), kThreads,
-                 0, ln, n_lines, F, delim == ' ' ? '\0' : delim,
-                 ParseOut{is_rec.get(), id_start.get(), id_len.get(), vals.get(), err.get()});
+  DevBuf<u64> fb(NL * static_cast<std::size_t>(F));
+  if (n_lines > 1) {
+    const unsigned cap = static_cast<unsigned>(ctx->sm_count) * 16;
+    DFPCA_LAUNCH(ctx, k_split_lines, grid_for(n_lines - 1, kThreads, cap), kThreads, 0, ln, n_lines, F,
+                 delim == ' ' ? '\0' : delim,
+                 SplitOut{is_rec.get(), id_start.get(), id_len.get(), fb.get(), err.get()});
+    DFPCA_LAUNCH(ctx, k_parse_fields, grid_for((n_lines - 1) * nv, kThreads, cap), kThreads, 0, ln, n_lines, F,
+                 is_rec.get(), fb.get(), vals.get(), err.get());
+  }
   const u64 e = d2h_one(ctx, err.get());
   ctx->end_stage();
   if (e != ~0ull) {
@@ -709,7 +778,7 @@ dfpca_table* parse_table(dfpca_context* ctx, const std::string& name, const char
   ctx->end_stage();
   ctx->begin_stage("scatter");
   DFPCA_LAUNCH(ctx, k_scatter, gr, kThreads, 0, head.get(), head_idx.get(), run_base.get(), head_rec.get(),
-               rec_line.get(), vals.get(), n_rec, d, tab->coords.get(), tab->values.get());
+               rec_line.get(), vals.get(), n_lines, n_rec, d, tab->coords.get(), tab->values.get());
   // sample ids
   DevBuf<i64> ilen(NS + 1);
   tab->id_off.alloc(NS + 1);

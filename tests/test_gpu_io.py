@@ -67,6 +67,40 @@ def test_large_interleaved_table(api, ref, tmp_path):
     _same(api.read_long_format(str(p)), ref.read_long_format(p))
 
 
+def test_decimal_token_fuzz(api, ref, tmp_path):
+    """The register fast path for plain decimals (k_parse_fields) and the
+    general parser it falls back to, on 60k valid tokens of many shapes:
+    every value bit-equal to the reference's strtod."""
+    rng = np.random.default_rng(3)
+    toks = []
+    for _ in range(60000):
+        v = float(rng.standard_normal() * 10.0 ** rng.integers(-30, 30))
+        kind = rng.integers(0, 9)
+        if kind == 0:
+            t = "%.17g" % v
+        elif kind == 1:
+            t = "%.*e" % (int(rng.integers(0, 22)), v)
+        elif kind == 2:
+            t = "%.*f" % (int(rng.integers(0, 12)), v / 10.0 ** rng.integers(0, 25))
+        elif kind == 3:
+            t = "0" * int(rng.integers(1, 6)) + "%d.%d" % (rng.integers(0, 10 ** 6), rng.integers(0, 10 ** 9))
+        elif kind == 4:
+            t = "+%.*g" % (int(rng.integers(1, 20)), abs(v))
+        elif kind == 5:
+            t = "%d." % rng.integers(0, 10 ** 15)
+        elif kind == 6:
+            t = ".%0*d" % (int(rng.integers(1, 25)), rng.integers(0, 10 ** 12))
+        elif kind == 7:
+            t = "%dE%+d" % (rng.integers(1, 10 ** 18), rng.integers(-300, 290))
+        else:
+            t = "".join(rng.choice(list("0123456789"), int(rng.integers(15, 24)))) + "e-" + str(rng.integers(0, 40))
+        toks.append(t)
+    lines = ["id\tt\ty"] + ["s%d\t%s\t%s" % (j % 7, toks[j], toks[-1 - j]) for j in range(len(toks))]
+    p = tmp_path / "fuzz.tsv"
+    p.write_text("\n".join(lines) + "\n")
+    _same(api.read_long_format(str(p)), ref.read_long_format(p))
+
+
 def test_round_trip_through_writer(api, tmp_path):
     from paper_1510_04439_b200 import synth
     sd = synth.sparse_masked(24, 300, 0.3)

@@ -54,12 +54,13 @@ def launches(path, skip=0):
 def full(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h = rows[0]
+    h, units = rows[0], rows[1]
     for r in rows[2:]:
         print("==", clean(r[h.index("Kernel Name")]))
         for m in METRICS:
             if m in h:
-                print(f"   {m:75s} {r[h.index(m)]}")
+                i = h.index(m)
+                print(f"   {m:75s} {r[i]} {units[i]}".rstrip())
 
 
 if __name__ == "__main__":

@@ -603,7 +603,7 @@ def ncu_traffic(kernel: str, pattern: str = "r*_ncu_full_summary.txt"):
             continue
         parts = line.split()
         if cur and len(parts) in (2, 3) and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            base = cur.split("<")[0].split("::")[-1]
+            base = cur.split("::")[-1].split("<")[0]
             # values in ncu's unit (third column when recorded; older files: Mbyte)
             scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(parts[2] if len(parts) == 3 else "Mbyte")
             if base == kernel and (cur, parts[0]) not in vals and scale:

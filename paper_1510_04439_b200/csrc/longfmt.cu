@@ -386,16 +386,24 @@ __device__ __forceinline__ bool fast_decimal(const char* text, i64 a, i64 len, d
 }
 
 // Pass 2, one thread per (number column k, line): 32 consecutive lines of
-// one column per warp, so the lanes parse tokens of like shape.  Values are
-// stored column-major, vals[k * n_lines + L].
+// one column per warp, so the lanes parse tokens of like shape; the lines are
+// taken in chunks of kFieldChunk with all columns of a chunk next to each
+// other, so a line's text is still in L2 when its other columns are parsed.
+// Values are stored column-major, vals[k * n_lines + L].
+constexpr i64 kFieldChunk = 4096;
+
 __global__ void __launch_bounds__(kThreads) k_parse_fields(Lines ln, i64 n_lines, int F, const i64* is_rec,
                                                            const u64* fb, double* vals, u64* err) {
   const int nv = F - 1;
   const i64 per = n_lines - 1;
   for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < per * nv;
        e += static_cast<i64>(gridDim.x) * blockDim.x) {
-    const int k = static_cast<int>(e / per);
-    const i64 L = 1 + (e - static_cast<i64>(k) * per);
+    const i64 chunk = e / (kFieldChunk * nv);
+    const i64 r = e - chunk * kFieldChunk * nv;
+    const i64 c0 = chunk * kFieldChunk;
+    const i64 span = per - c0 < kFieldChunk ? per - c0 : kFieldChunk;  // lines in this chunk
+    const int k = static_cast<int>(r / span);
+    const i64 L = 1 + c0 + (r - static_cast<i64>(k) * span);
     if (!is_rec[L] || fb[L * F] == ~0ull) continue;
     const u64 f = fb[L * F + 1 + k];
     const i64 st = L == 0 ? 0 : ln.nl[L - 1] + 1;

@@ -4,7 +4,8 @@
 // libdfpca_cuda.so) or against the reference alone (the oracle build) -- and
 // printed as one JSON line, so tests/test_gpu_pipeline.py can compare them.
 //
-//   pipeline_run sim1|sim2 randomized|dense
+//   pipeline_run sim1|grid2d|random2d randomized|dense
+#include <cmath>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -23,16 +24,34 @@ static void print_list(const char* key, const std::vector<double>& v, bool last 
 int main(int argc, char** argv) {
   const std::string which = argc > 1 ? argv[1] : "sim1";
   const std::string eig = argc > 2 ? argv[2] : "randomized";
-  const bool d3 = which == "sim2";
-  const SimSpec spec = d3 ? sim2_spec(60, 8) : sim1_spec(200, 100, 100);
+  const bool d2 = which != "sim1";
+  SimSpec spec = sim1_spec(200, 100, 100);
+  if (d2) {
+    // SURVEY.md 8(d) config 2's process on a 24^2 midpoint grid: exp bump
+    // mean, 2 prod_k sin(2 pi l t_k), lambda 16, 4, 1, 0.25, sigma^2 = 1/16;
+    // every node observed (grid2d) or 40 uniform random points (random2d)
+    spec = SimSpec{};
+    spec.name = which;
+    spec.n = 60;
+    spec.grid = EvaluationGrid::midpoint({0.0, 0.0}, {1.0, 1.0}, {24, 24});
+    spec.design = which == "grid2d" ? SimDesign::GridNodes : SimDesign::UniformRandom;
+    spec.points_per_sample = which == "grid2d" ? 0 : 40;
+    spec.mean = [](const double* t) { return std::exp((t[0] - 0.5) * (t[0] - 0.5) + (t[1] - 0.5) * (t[1] - 0.5)); };
+    const double pi = std::acos(-1.0);
+    for (int l = 1; l <= 4; ++l)
+      spec.eigenfunctions.push_back(
+          [pi, l](const double* t) { return 2.0 * std::sin(2.0 * l * pi * t[0]) * std::sin(2.0 * l * pi * t[1]); });
+    spec.lambda = {16.0, 4.0, 1.0, 0.25};
+    spec.sigma2 = 1.0 / 16.0;
+  }
   const auto generated = generate(spec);
   const FunctionalDataset& data = generated.first;
   RunConfig cfg;
-  cfg.grid_nodes = {d3 ? Index{8} : Index{100}};
-  const double h = d3 ? 0.3 : 0.25;  // tests/acceptance.cpp:103-105 for sim1
+  cfg.grid_nodes = {d2 ? Index{24} : Index{100}};
+  const double h = d2 ? 0.15 : 0.25;  // tests/acceptance.cpp:103-105 for sim1
   for (BandwidthChoice* c : {&cfg.bw_mean, &cfg.bw_cov, &cfg.bw_diag}) {
     c->mode = BandwidthMode::Explicit;
-    c->values.assign(d3 ? 3 : 1, h);
+    c->values.assign(d2 ? 2 : 1, h);
   }
   cfg.max_components = 5;
   cfg.eig_method = eig == "dense" ? EigMethod::Dense : EigMethod::Randomized;

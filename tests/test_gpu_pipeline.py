@@ -28,9 +28,10 @@ def _run(name, *args):
 
 
 @pytest.mark.parametrize("eig", ["randomized", "dense"])
-def test_fit_pipeline_dropin_matches_reference(eig):
-    got = _run("pipeline_dropin", "sim1", eig)
-    want = _run("pipeline_ref", "sim1", eig)
+@pytest.mark.parametrize("sim", ["sim1", "grid2d", "random2d"])
+def test_fit_pipeline_dropin_matches_reference(sim, eig):
+    got = _run("pipeline_dropin", sim, eig)
+    want = _run("pipeline_ref", sim, eig)
     assert got["ok"] and want["ok"]
     assert got["n_components"] == want["n_components"]
     assert got["score_method"] == want["score_method"]

@@ -155,18 +155,42 @@ struct PaceArgs {
   int* status;        // per sample: 0 ok, 1 singular, 2 outside hull
 };
 
-__global__ void k_pace(PaceArgs a) {
+// BIG = false: samples with at most kPaceMaxObs observations, everything in
+// shared memory (the others are left to the BIG launch).  BIG = true: one CTA
+// per listed sample, the same steps on a per-CTA global-memory workspace of
+// cap * (L + 2) + cap^2 doubles and 3 cap ints (any observation count).
+template <bool BIG>
+__global__ void k_pace(PaceArgs a, const i64* big_list, double* ws, int* iws, i64 cap) {
   extern __shared__ double sm[];
-  const i64 i = blockIdx.x;
+  const i64 i = BIG ? big_list[blockIdx.x] : static_cast<i64>(blockIdx.x);
   if (i >= a.n_samples) return;
   const i64 j0 = a.offsets[i], nobs = a.offsets[i + 1] - j0;
+  if (!BIG && nobs > kPaceMaxObs) return;
   const i64 L = a.L;
-  double* ph = sm;                          // [kPaceMaxObs][L]
-  double* yc = ph + kPaceMaxObs * L;        // [kPaceMaxObs]
-  double* S = yc + kPaceMaxObs;             // [N][N] column-major
-  __shared__ int used_idx[kPaceMaxObs];
+  double *ph, *yc, *S, *temp;
+  int *used_idx, *trans, *ok_flag;
+  if constexpr (BIG) {
+    double* w = ws + static_cast<i64>(blockIdx.x) * (cap * (L + 2) + cap * cap);
+    ph = w;                 // [cap][L]
+    yc = ph + cap * L;      // [cap]
+    temp = yc + cap;        // [cap]
+    S = temp + cap;         // [N][N] column-major
+    int* iw = iws + static_cast<i64>(blockIdx.x) * 3 * cap;
+    used_idx = iw;
+    trans = iw + cap;
+    ok_flag = iw + 2 * cap;
+  } else {
+    __shared__ int used_sh[kPaceMaxObs], trans_sh[kPaceMaxObs], ok_sh[kPaceMaxObs];
+    __shared__ double temp_sh[kPaceMaxObs];
+    ph = sm;                          // [kPaceMaxObs][L]
+    yc = ph + kPaceMaxObs * L;        // [kPaceMaxObs]
+    S = yc + kPaceMaxObs;             // [N][N] column-major
+    temp = temp_sh;
+    used_idx = used_sh;
+    trans = trans_sh;
+    ok_flag = ok_sh;
+  }
   __shared__ int n_used, bad;
-  __shared__ int trans[kPaceMaxObs];
   if (threadIdx.x == 0) {
     n_used = 0;
     bad = 0;
@@ -174,7 +198,6 @@ __global__ void k_pace(PaceArgs a) {
   __syncthreads();
   // design, in observation order (one thread per observation, then a stable
   // compaction of the usable ones)
-  __shared__ int ok_flag[kPaceMaxObs];
   for (i64 j = threadIdx.x; j < nobs; j += blockDim.x) {
     const double* x = a.coords + (j0 + j) * a.g.d;
     int ok = 1;
@@ -231,7 +254,6 @@ __global__ void k_pace(PaceArgs a) {
   }
   __syncthreads();
   // Eigen ldlt_inplace<Lower>::unblocked with diagonal pivoting
-  __shared__ double temp[kPaceMaxObs];
   __shared__ int ret_sh, fzp_sh, piv_sh;
   if (threadIdx.x == 0) {
     ret_sh = 1;
@@ -464,13 +486,19 @@ void run_scores(dfpca_context* ctx, const Grid& grid, i64 n, const i64* offsets,
                  d_mean.get(), d_phi.get(), grid.has_mask ? mask.get() : nullptr, G, n, L, grid.cell_volume(),
                  d_out.get());
   } else {
-    i64 max_obs = 0;
-    for (i64 i = 0; i < n; ++i) max_obs = std::max(max_obs, offsets[i + 1] - offsets[i]);
-    if (max_obs > kPaceMaxObs)
-      fail(kConfig, "InvalidArgument",
-           "conditional-expectation (PACE) scores on the GPU take up to " + std::to_string(kPaceMaxObs) +
-               " observations per sample (got " + std::to_string(max_obs) +
-               "); densely observed samples use integration scores (choose_score_method)");
+    // samples up to kPaceMaxObs observations: one shared-memory CTA each;
+    // larger ones: one CTA each on a global-memory workspace, in batches
+    i64 max_small = 0, max_big = 0;
+    std::vector<i64> big;
+    for (i64 i = 0; i < n; ++i) {
+      const i64 c = offsets[i + 1] - offsets[i];
+      if (c > kPaceMaxObs) {
+        big.push_back(i);
+        max_big = std::max(max_big, c);
+      } else {
+        max_small = std::max(max_small, c);
+      }
+    }
     DevBuf<double> lam(static_cast<std::size_t>(L));
     DFPCA_CUDA(cudaMemcpyAsync(lam.get(), eigenvalues, sizeof(double) * L, cudaMemcpyHostToDevice, st));
     DevBuf<int> status(static_cast<std::size_t>(n));
@@ -487,11 +515,24 @@ void run_scores(dfpca_context* ctx, const Grid& grid, i64 n, const i64* offsets,
     a.noise = std::max(sigma2, kSigmaFloorRel * eigenvalues[0]);
     a.out = d_out.get();
     a.status = status.get();
-    const std::size_t smem = sizeof(double) * (kPaceMaxObs * (L + 1) + max_obs * max_obs);
-    if (smem > 227 * 1024)
+    const std::size_t smem = sizeof(double) * (kPaceMaxObs * (L + 1) + max_small * max_small);
+    if (smem > 200 * 1024)
       fail(kConfig, "InvalidArgument", "too many components x observations for the on-chip PACE design");
-    allow_smem(k_pace, smem);
-    DFPCA_LAUNCH(ctx, k_pace, static_cast<unsigned>(n), 128, smem, a);
+    allow_smem(k_pace<false>, smem);
+    DFPCA_LAUNCH(ctx, k_pace<false>, static_cast<unsigned>(n), 128, smem, a, nullptr, nullptr, nullptr, i64{0});
+    if (!big.empty()) {
+      const i64 per = max_big * (L + 2) + max_big * max_big;  // doubles per CTA
+      const i64 batch = std::max<i64>(1, std::min<i64>(static_cast<i64>(big.size()), (i64{1} << 28) / per));
+      DevBuf<double> ws(static_cast<std::size_t>(batch * per));
+      DevBuf<int> iws(static_cast<std::size_t>(batch * 3 * max_big));
+      DevBuf<i64> list(big.size());
+      DFPCA_CUDA(cudaMemcpyAsync(list.get(), big.data(), sizeof(i64) * big.size(), cudaMemcpyHostToDevice, st));
+      for (i64 b0 = 0; b0 < static_cast<i64>(big.size()); b0 += batch) {
+        const i64 nb = std::min<i64>(batch, static_cast<i64>(big.size()) - b0);
+        DFPCA_LAUNCH(ctx, k_pace<true>, static_cast<unsigned>(nb), 256, 0, a, list.get() + b0, ws.get(), iws.get(),
+                     max_big);
+      }
+    }
     std::vector<int> hs(static_cast<std::size_t>(n));
     DFPCA_CUDA(cudaMemcpyAsync(hs.data(), status.get(), sizeof(int) * n, cudaMemcpyDeviceToHost, st));
     DFPCA_CUDA(cudaStreamSynchronize(st));

@@ -59,8 +59,6 @@ def test_scores(api, ref, case, method):
     grid, mean, diag, cov, eig = _model(api, sd)
     s2 = api.estimate_sigma2(diag, cov, mean)
     m = api.ScoreMethod.Integration if method == "integration" else api.ScoreMethod.Pace
-    if m == api.ScoreMethod.Pace and np.max(np.diff(sd.offsets)) > 160:
-        pytest.skip("dense samples: PACE is not the method the reference picks (choose_score_method)")
     got, warn = api.compute_scores_batch(sd.dataset(), grid, mean, eig, s2, m)
     want, wwarn = ref.scores((sd.axes, sd.mask), sd.offsets, sd.coords, sd.values, mean.values,
                              eig.eigenvalues, np.stack(eig.eigenfunctions), s2, m.value)
@@ -97,10 +95,20 @@ def test_score_errors(api):
         with pytest.raises(api.Error) as e:
             api.compute_scores_batch(bad.dataset(), grid, mean, eig, 0.1, m)
         assert e.value.name() == "OutOfDomain"
-    dense = synth.grid_nodes(2, 16, 3, 0.3)  # 256 observations per sample
-    with pytest.raises(api.Error) as e:
-        api.compute_scores_batch(dense.dataset(), grid, mean, eig, 0.1, api.ScoreMethod.Pace)
-    assert e.value.name() == "InvalidArgument"
+
+
+def test_pace_dense_samples_match_reference(api, ref):
+    """Samples above the shared-memory design size (160 observations) take the
+    global-workspace PACE kernel: same arithmetic, same bar."""
+    from paper_1510_04439_b200 import synth
+    sd = synth.grid_nodes(2, 16, 6, 0.3)  # 256 observations per sample
+    grid, mean, diag, cov, eig = _model(api, sd)
+    s2 = api.estimate_sigma2(diag, cov, mean)
+    got, _ = api.compute_scores_batch(sd.dataset(), grid, mean, eig, s2, api.ScoreMethod.Pace)
+    want, _ = ref.scores((sd.axes, sd.mask), sd.offsets, sd.coords, sd.values, mean.values, eig.eigenvalues,
+                         np.stack(eig.eigenfunctions), s2, api.ScoreMethod.Pace.value)
+    den = np.maximum(1.0, np.maximum(np.abs(got), np.abs(want)))
+    assert np.max(np.abs(got - want) / den) <= 1e-10
 
 
 @pytest.mark.parametrize("case", ["sparse_masked_2d", "nodes_2d", "random_1d"])
@@ -153,10 +161,9 @@ def test_scores_against_golden(api, name):
     integ, warn = api.compute_scores_batch(data, grid, mean, eig, s2, api.ScoreMethod.Integration)
     assert bit_equal(integ, z["scores_integration"])
     assert np.array_equal(warn.astype(np.uint8), z["scores_sparse_warning"])
-    if np.max(np.diff(z["offsets"])) <= 160:
-        pace, _ = api.compute_scores_batch(data, grid, mean, eig, s2, api.ScoreMethod.Pace)
-        den = np.maximum(1.0, np.maximum(np.abs(pace), np.abs(z["scores_pace"])))
-        assert np.max(np.abs(pace - z["scores_pace"]) / den) <= 1e-10
+    pace, _ = api.compute_scores_batch(data, grid, mean, eig, s2, api.ScoreMethod.Pace)
+    den = np.maximum(1.0, np.maximum(np.abs(pace), np.abs(z["scores_pace"])))
+    assert np.max(np.abs(pace - z["scores_pace"]) / den) <= 1e-10
     rec = api.reconstruct_on_grid(mean, eig, z["scores_integration"][0])
     assert bit_equal(rec, z["reconstruct0"])
     dense = api.dense_eig(api.matrixize(cov), 3, grid)

@@ -238,7 +238,7 @@ DFPCA_API int dfpca_estimate_sigma2(dfpca_context* ctx, const dfpca_grid* grid, 
                           const dfpca_surface* cov, const double* mean, double* sigma2);
 /* Replaces dfpca::compute_scores (scores.hpp:272-277) for a batch of samples
  * given in CSR form (as dfpca_linear_bin).  method 0 = pace_scores
- * (scores.hpp:157-194, up to 160 observations per sample), 1 =
+ * (scores.hpp:157-194; any observation count), 1 =
  * integration_scores (scores.hpp:204-262, bit-identical).  mean: G;
  * eigenvalues: L; eigenfunctions: L*G; scores: n*L out; sparse_warning: n out
  * (integration only; may be NULL).  Errors: OutOfDomain, SingularCovariance

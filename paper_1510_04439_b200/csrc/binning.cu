@@ -426,38 +426,78 @@ dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples
       cudaEvent_t last;
       ~CopiesDone() { cudaStreamWaitEvent(st, last, 0); }
     } copies_done{st, arrived.back()};
-    i64 max_chunk = 0;
-    for (std::size_t c = 0; c < n_chunks; ++c)
-      max_chunk = std::max(max_chunk, obs_offsets[cut[c + 1]] - obs_offsets[cut[c]]);
-    DevBuf<unsigned> gcount(max_chunk + 1), bcount(max_chunk + 1), goff(max_chunk + 1), boff(max_chunk + 1);
+    // Per-chunk counts and record offsets on a second compute stream, queued
+    // for every chunk up front: chunk c's counting runs as soon as it has
+    // arrived, beside the sorting and summing of chunk c - 1 on `st`; the host
+    // waits only for the totals of the chunk it is about to emit.
+    cudaStream_t as = ctx->aux_stream();
+    struct Counts {
+      DevBuf<unsigned> gcount, bcount, goff, boff;
+      DevBuf<unsigned char> tmp;
+      cudaEvent_t done = nullptr;
+    };
+    std::vector<Counts> cnt(n_chunks);
     DevBuf<unsigned long long> bad(1);
-    DevBuf<unsigned> totals_d(2);
     const unsigned long long none = ~0ull;
     DFPCA_CUDA(cudaMemcpyAsync(bad.get(), &none, sizeof(none), cudaMemcpyHostToDevice, st));
     for (std::size_t c = 0; c < n_chunks; ++c) {
+      const i64 nc = obs_offsets[cut[c + 1]] - obs_offsets[cut[c]];
+      Counts& k = cnt[c];
+      k.gcount.alloc(static_cast<std::size_t>(nc + 1));
+      k.bcount.alloc(static_cast<std::size_t>(nc + 1));
+      k.goff.alloc(static_cast<std::size_t>(nc + 1));
+      k.boff.alloc(static_cast<std::size_t>(nc + 1));
+      std::size_t tb = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, tb, k.gcount.get(), k.goff.get(), nc + 1, as);
+      k.tmp.alloc(std::max<std::size_t>(tb, 1));
+      DFPCA_CUDA(cudaEventCreateWithFlags(&k.done, cudaEventDisableTiming));
+    }
+    // host slots: [first bad, grid total, band total] per chunk
+    unsigned long long* slots = ctx->pinned_u64(3 * n_chunks);
+    struct CountsDone {
+      cudaStream_t st;
+      std::vector<Counts>& cnt;
+      ~CountsDone() {
+        for (auto& k : cnt)
+          if (k.done) {
+            cudaStreamWaitEvent(st, k.done, 0);  // before the buffers are freed on st
+            cudaEventDestroy(k.done);
+          }
+      }
+    } counts_done{st, cnt};
+    DFPCA_CUDA(cudaEventRecord(ctx->fence(), st));  // allocations and the bad-flag reset
+    DFPCA_CUDA(cudaStreamWaitEvent(as, ctx->fence(), 0));
+    auto aux_launch = [&](const char* what, cudaError_t e) {
+      cuda_check(e == cudaSuccess ? cudaGetLastError() : e, what);
+      ++ctx->launches;
+    };
+    for (std::size_t c = 0; c < n_chunks; ++c) {
+      const i64 o0 = obs_offsets[cut[c]], o1 = obs_offsets[cut[c + 1]], nc = o1 - o0;
+      Counts& k = cnt[c];
+      DFPCA_CUDA(cudaStreamWaitEvent(as, arrived[c], 0));
+      if (nc > 0) {
+        DFPCA_CUDA(cudaMemsetAsync(k.gcount.get() + nc, 0, sizeof(unsigned), as));
+        DFPCA_CUDA(cudaMemsetAsync(k.bcount.get() + nc, 0, sizeof(unsigned), as));
+        k_bin_count<<<grid_for(nc, 256), 256, 0, as>>>(dg, d_off.get(), n_samples, d_coords.get(), d_values.get(), o0,
+                                                       o1, d_slot.get(), want_grid ? 1 : 0, k.gcount.get(),
+                                                       want_band ? k.bcount.get() : nullptr, bad.get());
+        aux_launch("k_bin_count", cudaSuccess);
+        std::size_t tb = k.tmp.size();
+        aux_launch("scan", cub::DeviceScan::ExclusiveSum(k.tmp.get(), tb, k.gcount.get(), k.goff.get(), nc + 1, as));
+        if (want_band)
+          aux_launch("scan", cub::DeviceScan::ExclusiveSum(k.tmp.get(), tb, k.bcount.get(), k.boff.get(), nc + 1, as));
+        DFPCA_CUDA(cudaMemcpyAsync(slots + 3 * c + 1, k.goff.get() + nc, sizeof(unsigned), cudaMemcpyDeviceToHost, as));
+        DFPCA_CUDA(cudaMemcpyAsync(slots + 3 * c + 2, k.boff.get() + nc, sizeof(unsigned), cudaMemcpyDeviceToHost, as));
+      }
+      DFPCA_CUDA(cudaMemcpyAsync(slots + 3 * c, bad.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, as));
+      DFPCA_CUDA(cudaEventRecord(k.done, as));
+    }
+    for (std::size_t c = 0; c < n_chunks; ++c) {
       const i64 i0 = cut[c], i1 = cut[c + 1];
       const i64 o0 = obs_offsets[i0], o1 = obs_offsets[i1], nc = o1 - o0;
-      if (nc == 0) continue;
-      DFPCA_CUDA(cudaStreamWaitEvent(st, arrived[c], 0));
-      DFPCA_CUDA(cudaMemsetAsync(gcount.get() + nc, 0, sizeof(unsigned), st));
-      DFPCA_CUDA(cudaMemsetAsync(bcount.get() + nc, 0, sizeof(unsigned), st));
-      DFPCA_LAUNCH(ctx, k_bin_count, grid_for(nc, 256), 256, 0, dg, d_off.get(), n_samples, d_coords.get(),
-                   d_values.get(), o0, o1, d_slot.get(), want_grid ? 1 : 0, gcount.get(),
-                   want_band ? bcount.get() : nullptr, bad.get());
-      // Exclusive scans -> record offsets; totals land at index nc.
-      std::size_t tmp_bytes = 0;
-      cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, gcount.get(), goff.get(), nc + 1, st);
-      unsigned char* tmp = ctx->scratch_bytes(tmp_bytes);
-      cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, gcount.get(), goff.get(), nc + 1, st);
-      if (want_band) cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, bcount.get(), boff.get(), nc + 1, st);
-      ctx->launches += want_band ? 2 : 1;
-      unsigned long long first_bad = none;
-      unsigned totals[2] = {0, 0};
-      DFPCA_CUDA(cudaMemcpyAsync(&first_bad, bad.get(), sizeof(first_bad), cudaMemcpyDeviceToHost, st));
-      DFPCA_CUDA(cudaMemcpyAsync(&totals[0], goff.get() + nc, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-      if (want_band)
-        DFPCA_CUDA(cudaMemcpyAsync(&totals[1], boff.get() + nc, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-      DFPCA_CUDA(cudaStreamSynchronize(st));
+      Counts& k = cnt[c];
+      DFPCA_CUDA(cudaEventSynchronize(k.done));
+      const unsigned long long first_bad = slots[3 * c];
       if (first_bad != none) {
         const i64 o = static_cast<i64>(first_bad);
         const i64 i = std::upper_bound(obs_offsets, obs_offsets + n_samples + 1, o) - obs_offsets - 1;
@@ -466,6 +506,12 @@ dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples
                     " lies outside the grid hull",
                 i, o - obs_offsets[i]);
       }
+      if (nc == 0) continue;
+      DFPCA_CUDA(cudaStreamWaitEvent(st, k.done, 0));
+      unsigned totals[2] = {static_cast<unsigned>(slots[3 * c + 1] & 0xffffffffull),
+                            static_cast<unsigned>(slots[3 * c + 2] & 0xffffffffull)};
+      const DevBuf<unsigned>& goff = k.goff;
+      const DevBuf<unsigned>& boff = k.boff;
       const i64 n_grec = want_grid ? totals[0] : 0;
       const i64 n_brec = want_band ? totals[1] : 0;
       const i64 key_samples = i1 - i0;

@@ -399,6 +399,11 @@ int dfpca_context_destroy(dfpca_context* ctx) {
     cudaStreamDestroy(ctx->copy_);
   }
   if (ctx->fence_) cudaEventDestroy(ctx->fence_);
+  if (ctx->aux_) {
+    cudaStreamSynchronize(ctx->aux_);
+    cudaStreamDestroy(ctx->aux_);
+  }
+  if (ctx->pinned_) cudaFreeHost(ctx->pinned_);
   ctx->io_state.reset();
   cudaStreamDestroy(ctx->stream);
   delete ctx;

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <new>
 #include <string>
 #include <vector>
 
@@ -147,6 +148,28 @@ struct dfpca_context {
   cudaEvent_t fence() {
     if (!fence_) cudaEventCreateWithFlags(&fence_, cudaEventDisableTiming);
     return fence_;
+  }
+  // Second compute stream (binning counts of later chunks) and a small
+  // pinned host array for asynchronous scalar read-backs, zeroed on request.
+  cudaStream_t aux_ = nullptr;
+  cudaStream_t aux_stream() {
+    if (!aux_) cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking);
+    return aux_;
+  }
+  unsigned long long* pinned_ = nullptr;
+  std::size_t pinned_n_ = 0;
+  unsigned long long* pinned_u64(std::size_t n) {
+    if (n > pinned_n_) {
+      if (pinned_) cudaFreeHost(pinned_);
+      pinned_ = nullptr;
+      pinned_n_ = 0;
+      if (cudaHostAlloc(reinterpret_cast<void**>(&pinned_), n * sizeof(unsigned long long), cudaHostAllocDefault) ==
+          cudaSuccess)
+        pinned_n_ = n;
+    }
+    if (!pinned_) throw std::bad_alloc();
+    for (std::size_t i = 0; i < n; ++i) pinned_[i] = 0;
+    return pinned_;
   }
   // Pinned upload slots, worker streams and events of the table reader
   // (longfmt.cu), created on first use.

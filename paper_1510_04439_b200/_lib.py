@@ -85,6 +85,7 @@ SIGNATURES = [
     ("dfpca_parse_long_format", C.c_int, [P, C.c_char_p, C.c_char_p, C.c_int64, C.POINTER(P)]),
     ("dfpca_table_info", C.c_int, [P, C.POINTER(C.c_int), PI64, PI64, PI64]),
     ("dfpca_table_copy", C.c_int, [P, P, PI64, PD, PD, PI64, C.c_char_p]),
+    ("dfpca_linear_bin_table", C.c_int, [P, P, C.POINTER(DfpcaGrid), C.c_int, C.c_int, C.POINTER(P)]),
     ("dfpca_table_free", C.c_int, [P]),
     ("dfpca_shard_bounds", C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int, PI64]),
     ("dfpca_shard_blocks", C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, PI64, C.c_int64, PI64]),

@@ -1205,3 +1205,35 @@ def read_grid(path: str) -> EvaluationGrid:
         raise Error(ErrorClass.Parse, "ParseError", "%s: mask entries must be 0 or 1" % path)
     return EvaluationGrid(axes, np.frombuffer(mask_bits.encode(), dtype=np.uint8) - ord("0"))
 
+
+def bin_long_format(path: str, grid: EvaluationGrid, opt: BinOptions = BinOptions()):
+    """read_long_format + linear_bin without the host round trip: the table is
+    parsed on the GPU and binned there (the observations never cross PCIe).
+    Returns (BinnedData, sample ids in first-appearance order); the same
+    binned data, bit for bit, as linear_bin(read_long_format(path), ...)."""
+    t = C.c_void_p()
+    check(_lib.lib().dfpca_read_long_format(_lib.ctx(), str(path).encode(), C.byref(t)))
+    try:
+        dim, ns, no, nid = C.c_int(), C.c_int64(), C.c_int64(), C.c_int64()
+        _lib.lib().dfpca_table_info(t, C.byref(dim), C.byref(ns), C.byref(no), C.byref(nid))
+        id_off = np.zeros(ns.value + 1, dtype=np.int64)
+        chars = C.create_string_buffer(max(nid.value, 1))
+        check(_lib.lib().dfpca_table_copy(_lib.ctx(), t, None, None, None, id_off.ctypes.data_as(C.POINTER(C.c_int64)),
+                                          chars))
+        raw = chars.raw
+        ids = [raw[id_off[i]:id_off[i + 1]].decode("utf-8", "surrogateescape") for i in range(ns.value)]
+        if dim.value != grid.dim():
+            raise Error(ErrorClass.Config, "InvalidArgument", "dataset/grid dimension mismatch")
+        h = C.c_void_p()
+        status = _lib.lib().dfpca_linear_bin_table(_lib.ctx(), t, C.byref(grid.desc()), int(opt.mean_path),
+                                                   int(opt.covariance_path), C.byref(h))
+        if status != 0:
+            err = _lib.last_error()
+            if err.name() == "ObservationOutsideGrid":
+                i, j = _lib.last_error_location()
+                raise Error(err.error_class, err.name(), f"sample '{ids[i]}' observation {j} lies outside the grid hull")
+            raise err
+    finally:
+        _lib.lib().dfpca_table_free(t)
+    return BinnedData(h, grid), ids
+

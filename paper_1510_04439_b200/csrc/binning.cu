@@ -304,9 +304,11 @@ int key_bits(unsigned long long max_key) {
 
 DevGrid upload_grid_axes(dfpca_context* ctx, const Grid& g, DevBuf<double>& storage);
 
+// coords / values are host arrays, or device arrays when device_inputs (a
+// table read on the GPU, longfmt.cu): then nothing crosses PCIe.
 dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples,
                              const i64* obs_offsets, const double* coords, const double* values,
-                             bool mean_path, bool cov_path) {
+                             bool mean_path, bool cov_path, bool device_inputs) {
   if (n_samples < 0) fail(kConfig, "InvalidArgument", "negative sample count");
   const int d = grid.d;
   const i64 G = grid.G;
@@ -347,8 +349,14 @@ dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples
   DevGrid dg = upload_grid_axes(ctx, grid, axes_store);
 
   DevBuf<i64> d_off(static_cast<std::size_t>(n_samples + 1));
-  DevBuf<double> d_coords(static_cast<std::size_t>(std::max<i64>(n_obs * d, 1)));
-  DevBuf<double> d_values(static_cast<std::size_t>(std::max<i64>(n_obs, 1)));
+  DevBuf<double> d_coords_buf(static_cast<std::size_t>(device_inputs ? 0 : std::max<i64>(n_obs * d, 1)));
+  DevBuf<double> d_values_buf(static_cast<std::size_t>(device_inputs ? 0 : std::max<i64>(n_obs, 1)));
+  struct Ptr {
+    const double* p;
+    const double* get() const { return p; }
+  };
+  const Ptr d_coords{device_inputs ? coords : d_coords_buf.get()};
+  const Ptr d_values{device_inputs ? values : d_values_buf.get()};
   DevBuf<double> d_meanw(mean_w.size());
   DevBuf<i64> d_slot(slot.size());
   DFPCA_CUDA(cudaMemcpyAsync(d_off.get(), obs_offsets, sizeof(i64) * (n_samples + 1),
@@ -409,10 +417,10 @@ dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples
     DFPCA_CUDA(cudaStreamWaitEvent(cs, ctx->fence(), 0));
     for (std::size_t c = 0; c < n_chunks; ++c) {
       const i64 o0 = obs_offsets[cut[c]], o1 = obs_offsets[cut[c + 1]];
-      if (o1 > o0) {
-        DFPCA_CUDA(cudaMemcpyAsync(d_coords.get() + o0 * d, coords + o0 * d, sizeof(double) * (o1 - o0) * d,
+      if (o1 > o0 && !device_inputs) {
+        DFPCA_CUDA(cudaMemcpyAsync(d_coords_buf.get() + o0 * d, coords + o0 * d, sizeof(double) * (o1 - o0) * d,
                                    cudaMemcpyHostToDevice, cs));
-        DFPCA_CUDA(cudaMemcpyAsync(d_values.get() + o0, values + o0, sizeof(double) * (o1 - o0),
+        DFPCA_CUDA(cudaMemcpyAsync(d_values_buf.get() + o0, values + o0, sizeof(double) * (o1 - o0),
                                    cudaMemcpyHostToDevice, cs));
       }
       arrived[c] = nullptr;

@@ -21,7 +21,7 @@ thread_local cudaStream_t g_alloc_stream = nullptr;
 
 dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples,
                              const i64* obs_offsets, const double* coords, const double* values,
-                             bool mean_path, bool cov_path);
+                             bool mean_path, bool cov_path, bool device_inputs = false);
 void run_local_linear(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid, const double* h,
                       int target, double* out_host, dfpca_surface** out_surface);
 void run_covariance(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid, const double* h,
@@ -58,6 +58,7 @@ void table_copy(dfpca_context* ctx, const dfpca_table* t, i64* offsets, double* 
                 char* id_chars);
 void table_shape(const dfpca_table* t, int* dim, i64* n_samples, i64* n_obs, i64* id_bytes);
 void table_delete(dfpca_table* t);
+dfpca_binned* bin_table(dfpca_context* ctx, const dfpca_table* t, const Grid& grid, bool mean_path, bool cov_path);
 void run_estimate_sigma2(dfpca_context* ctx, const Grid& grid, const double* diag_plus_noise,
                          const dfpca_surface* cov, const double* mean, double* sigma2);
 void run_scores(dfpca_context* ctx, const Grid& grid, i64 n, const i64* offsets, const double* coords,
@@ -960,6 +961,16 @@ int dfpca_table_copy(dfpca_context* ctx, const dfpca_table* t, int64_t* obs_offs
   return guarded(ctx, [&] {
     if (!t) fail(kConfig, "InvalidArgument", "null table");
     table_copy(ctx, t, obs_offsets, coords, values, id_offsets, id_chars);
+  });
+}
+
+int dfpca_linear_bin_table(dfpca_context* ctx, const dfpca_table* t, const dfpca_grid* grid, int mean_path,
+                           int covariance_path, dfpca_binned** out) {
+  return guarded(ctx, [&] {
+    if (!out || !t) fail(kConfig, "InvalidArgument", "null table or output handle");
+    *out = nullptr;
+    Grid g = make_grid(grid);
+    *out = bin_table(ctx, t, g, mean_path != 0, covariance_path != 0);
   });
 }
 

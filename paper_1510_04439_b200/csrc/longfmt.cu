@@ -879,4 +879,21 @@ void table_shape(const dfpca_table* t, int* dim, i64* n_samples, i64* n_obs, i64
 
 void table_delete(dfpca_table* t) { delete t; }
 
+dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples, const i64* obs_offsets,
+                             const double* coords, const double* values, bool mean_path, bool cov_path,
+                             bool device_inputs);
+
+// linear_bin over a table that is already on the device: only the sample
+// offsets come back to the host (the binning plans its chunks with them).
+dfpca_binned* bin_table(dfpca_context* ctx, const dfpca_table* t, const Grid& grid, bool mean_path, bool cov_path) {
+  if (t->dim != grid.d) fail(kConfig, "InvalidArgument", "dataset/grid dimension mismatch");
+  std::vector<i64> off(static_cast<std::size_t>(t->n_samples) + 1);
+  DFPCA_CUDA(cudaMemcpyAsync(off.data(), t->offsets.get(), sizeof(i64) * off.size(), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
+  return run_linear_bin(ctx, grid, t->n_samples, off.data(), t->coords.get(), t->values.get(), mean_path, cov_path,
+                        true);
+}
+
 }  // namespace dfpca_gpu
+

@@ -113,3 +113,38 @@ def test_round_trip_through_writer(api, tmp_path):
         assert np.array_equal(np.asarray(x).view(np.uint64) if x.dtype == np.float64 else x,
                               np.asarray(y).view(np.uint64) if y.dtype == np.float64 else y)
     assert [s.id for s in back.samples] == [s.id for s in ds.samples]
+
+
+@pytest.mark.parametrize("case", ["nodes_2d", "random_2d", "random_1d", "masked"])
+def test_bin_long_format_equals_host_round_trip(api, tmp_path, case):
+    """bin_long_format (table parsed and binned on the device) == linear_bin
+    of read_long_format's dataset, every BinnedData field bit for bit."""
+    from paper_1510_04439_b200 import synth
+    sd = {"nodes_2d": lambda: synth.grid_nodes(2, 12, 40, 0.2),
+          "random_2d": lambda: synth.random_points(2, 13, 60, 25, 0.3),
+          "random_1d": lambda: synth.random_points(1, 41, 30, 15, 0.15),
+          "masked": lambda: synth.sparse_masked(20, 80, 0.2)}[case]()
+    p = tmp_path / "t.tsv"
+    p.write_bytes(synth.long_format_bytes(sd))
+    grid = sd.grid()
+    opt = api.BinOptions(True, True)
+    a = api.linear_bin(api.read_long_format(str(p)), grid, opt)
+    b, ids = api.bin_long_format(str(p), grid, opt)
+    assert ids == ["s%d" % i for i in range(len(ids))]
+    for f in ("mass", "wvalue", "wsquare", "diag_mass", "diag_value"):
+        assert np.array_equal(np.asarray(getattr(a, f)).view(np.uint64), np.asarray(getattr(b, f)).view(np.uint64)), f
+    assert a.sample_sizes == b.sample_sizes
+    for x, y in zip(a.per_sample, b.per_sample):
+        assert x.sample_index == y.sample_index and x.pair_weight == y.pair_weight
+        assert np.array_equal(x.mass.view(np.uint64), y.mass.view(np.uint64))
+        assert np.array_equal(x.value.view(np.uint64), y.value.view(np.uint64))
+
+
+def test_bin_long_format_outside_observation(api, tmp_path):
+    p = tmp_path / "bad.tsv"
+    p.write_bytes(b"id\tt\ty\na\t0.5\t1\nbad id\t0.2\t1\nbad id\t1.5\t2\n")
+    grid = api.EvaluationGrid.uniform([0.0], [1.0], [5])
+    with pytest.raises(api.Error) as e:
+        api.bin_long_format(str(p), grid)
+    assert e.value.name() == "ObservationOutsideGrid"
+    assert "'bad id' observation 1" in str(e.value)

@@ -260,6 +260,24 @@ def run_io(args):
     assert int(off[-1]) == rows and np.array_equal(values.view(np.uint64), sd.values.view(np.uint64))
     d2h = off.nbytes + coords.nbytes + values.nbytes + sum(len(s.id) for s in ds.samples) + off.nbytes
     t_e2e = float(np.mean(e2e))
+    # file -> binned data (the fit pipeline's first two stages): the table
+    # parsed and binned on the device (bin_long_format) against the two public
+    # calls with the dataset crossing to the host and back in between
+    grid, bopt = sd.grid(), api.BinOptions(True, True)
+    fused, split = [], []
+    for it in range(args.e2e_steps + 1):
+        # calls are synchronous at return; the binned data stays on the device
+        t0 = time.perf_counter()
+        b1, _ = api.bin_long_format(path, grid, bopt)
+        t1 = time.perf_counter()
+        b2 = api.linear_bin(api.read_long_format(path), grid, bopt)
+        t2 = time.perf_counter()
+        m1, m2 = np.asarray(b1.diag_value), np.asarray(b2.diag_value)
+        if it > 0:
+            fused.append(t1 - t0)
+            split.append(t2 - t1)
+    assert np.array_equal(m1.view(np.uint64), m2.view(np.uint64))
+    del b1, b2
     os.unlink(path)
     # roofline of the dominant device kernel (HBM-bound byte work).  Algorithmic
     # bytes per launch: k_split_lines reads every text byte once plus two
@@ -304,6 +322,12 @@ def run_io(args):
                    "d2h_bytes_per_step": int(d2h), "ms_per_step": t_e2e * 1e3,
                    "all_ms": [round(t * 1e3, 2) for t in e2e],
                    "path": "file (page cache) -> pinned slots -> HBM -> device parse/group -> host CSR arrays"},
+           "file_to_binned": {"ms_bin_long_format": float(np.mean(fused)) * 1e3,
+                              "ms_read_then_linear_bin": float(np.mean(split)) * 1e3,
+                              "grid": [int(n) for n in grid.shape()], "mean_path": True, "covariance_path": True,
+                              "path": "bin_long_format: file -> HBM -> parse/group -> binning, observations stay "
+                                      "on the device; vs read_long_format -> host arrays -> linear_bin",
+                              "bit_identical": True},
            "gpu_launches": int(launches),
            "kernels": {k: {"ms": v[0], "launches": v[1]} for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][0])},
            "roofline": roof, "cpu_baseline": cpu, "clocks": clk.summary()}

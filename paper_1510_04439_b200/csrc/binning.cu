@@ -361,6 +361,15 @@ dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples
   DevBuf<i64> d_slot(slot.size());
   DFPCA_CUDA(cudaMemcpyAsync(d_off.get(), obs_offsets, sizeof(i64) * (n_samples + 1),
                              cudaMemcpyHostToDevice, st));
+  // Pageable observations are staged through pinned slots by host threads
+  // before the binning starts (the chunked overlap below needs pinned memory
+  // for the copies to be asynchronous).
+  const i64 coord_bytes = static_cast<i64>(sizeof(double)) * n_obs * d;
+  const bool staged = !device_inputs && n_obs > 0 && copy_is_staged(coords, coord_bytes);
+  if (staged) {
+    copy_h2d(ctx, d_coords_buf.get(), coords, coord_bytes);
+    copy_h2d(ctx, d_values_buf.get(), values, static_cast<i64>(sizeof(double)) * n_obs);
+  }
   DFPCA_CUDA(cudaMemcpyAsync(d_meanw.get(), mean_w.data(), sizeof(double) * mean_w.size(),
                              cudaMemcpyHostToDevice, st));
   DFPCA_CUDA(cudaMemcpyAsync(d_slot.get(), slot.data(), sizeof(i64) * slot.size(),
@@ -417,7 +426,7 @@ dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples
     DFPCA_CUDA(cudaStreamWaitEvent(cs, ctx->fence(), 0));
     for (std::size_t c = 0; c < n_chunks; ++c) {
       const i64 o0 = obs_offsets[cut[c]], o1 = obs_offsets[cut[c + 1]];
-      if (o1 > o0 && !device_inputs) {
+      if (o1 > o0 && !device_inputs && !staged) {
         DFPCA_CUDA(cudaMemcpyAsync(d_coords_buf.get() + o0 * d, coords + o0 * d, sizeof(double) * (o1 - o0) * d,
                                    cudaMemcpyHostToDevice, cs));
         DFPCA_CUDA(cudaMemcpyAsync(d_values_buf.get() + o0, values + o0, sizeof(double) * (o1 - o0),

@@ -499,7 +499,10 @@ int dfpca_binned_download(dfpca_context* ctx, const dfpca_binned* b, double* mas
     cudaStream_t st = ctx->stream;
     const i64 G = b->grid.G;
     auto d2h = [&](double* dst, const DevBuf<double>& src, i64 n) {
-      if (dst && n > 0 && src.get())
+      if (!dst || n <= 0 || !src.get()) return;
+      if (copy_is_staged(dst, static_cast<i64>(sizeof(double)) * n))
+        copy_d2h(ctx, dst, src.get(), static_cast<i64>(sizeof(double)) * n);
+      else
         DFPCA_CUDA(cudaMemcpyAsync(dst, src.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     };
     if (b->has_mean) {
@@ -547,7 +550,7 @@ int dfpca_binned_upload(dfpca_context* ctx, const dfpca_grid* grid, int64_t n_sa
       dst.alloc(static_cast<std::size_t>(n));
       if (n == 0) return;
       if (src)
-        DFPCA_CUDA(cudaMemcpyAsync(dst.get(), src, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        copy_h2d(ctx, dst.get(), src, static_cast<i64>(sizeof(double)) * n);
       else
         DFPCA_CUDA(cudaMemsetAsync(dst.get(), 0, sizeof(double) * n, st));
     };
@@ -872,10 +875,8 @@ int dfpca_surface_download(dfpca_context* ctx, const dfpca_surface* s, double* o
   return guarded(ctx, [&] {
     if (!s || !out) fail(kConfig, "InvalidArgument", "null surface or output");
     ctx->begin_stage("download");
-    DFPCA_CUDA(cudaMemcpyAsync(out, s->values.get(), sizeof(double) * s->n, cudaMemcpyDeviceToHost,
-                               ctx->stream));
+    copy_d2h(ctx, out, s->values.get(), static_cast<i64>(sizeof(double)) * s->n);
     ctx->end_stage();
-    DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 
@@ -892,8 +893,7 @@ int dfpca_surface_upload(dfpca_context* ctx, const dfpca_grid* grid, int kind, c
     s->kind = kind;
     s->n = n_values;
     s->values.alloc(static_cast<std::size_t>(n_values));
-    DFPCA_CUDA(cudaMemcpyAsync(s->values.get(), values, sizeof(double) * n_values, cudaMemcpyHostToDevice,
-                               ctx->stream));
+    copy_h2d(ctx, s->values.get(), values, static_cast<i64>(sizeof(double)) * n_values);
     DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
     *out = s.release();
   });

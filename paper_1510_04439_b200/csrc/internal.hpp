@@ -230,6 +230,13 @@ struct dfpca_binned {
 namespace dfpca_gpu {
 // Sets identical_mass-derived structure flags (shared_const, shared_m0/dm0).
 void detect_shared_design(dfpca_context* ctx, dfpca_binned* b);
+// Host <-> device copies of caller buffers (longfmt.cu): pinned memory is
+// copied directly, large pageable buffers through the pinned slots on host
+// worker threads.  copy_h2d is ordered before later work on ctx->stream;
+// copy_d2h returns when the bytes are in `dst`.
+bool copy_is_staged(const void* host, std::int64_t bytes);
+void copy_h2d(dfpca_context* ctx, void* d_dst, const void* src, std::int64_t bytes);
+void copy_d2h(dfpca_context* ctx, void* dst, const void* d_src, std::int64_t bytes);
 }  // namespace dfpca_gpu
 
 struct dfpca_surface {

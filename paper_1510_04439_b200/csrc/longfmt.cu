@@ -85,6 +85,7 @@ IoState& io_state(dfpca_context* ctx) {
     auto io = std::make_shared<IoState>();
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     io->workers = static_cast<int>(std::min(8u, std::max(1u, hw / 2)));
+    if (const char* e = std::getenv("DFPCA_IO_WORKERS")) io->workers = std::max(1, std::min(64, std::atoi(e)));
     for (int w = 0; w < io->workers; ++w) {
       for (int s = 0; s < 2; ++s) {
         char* p = nullptr;

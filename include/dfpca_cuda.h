@@ -295,7 +295,8 @@ DFPCA_API int dfpca_table_info(const dfpca_table* t, int* dim, int64_t* n_sample
  * into id_chars (id_bytes). */
 DFPCA_API int dfpca_table_copy(dfpca_context* ctx, const dfpca_table* t, int64_t* obs_offsets, double* coords,
                      double* values, int64_t* id_offsets, char* id_chars);
-/* dfpca_linear_bin over a table read on the GPU: the observations never leave
+/* Replaces io.hpp:115 read_long_format followed by binning.hpp:82 linear_bin.
+ * dfpca_linear_bin over a table read on the GPU: the observations never leave
  * the device (only the n_samples + 1 offsets are read back).  Same outputs and
  * errors as dfpca_linear_bin on the table's CSR arrays. */
 DFPCA_API int dfpca_linear_bin_table(dfpca_context* ctx, const dfpca_table* t, const dfpca_grid* grid,

@@ -50,6 +50,7 @@ __device__ inline i64 sample_of(const i64* offsets, i64 n_samples, i64 obs) {
 
 // Pass 1: hull check, per-observation record counts.
 // Observations [o0, o1) of one chunk; counts are chunk-local (index o - o0).
+template <int D>
 __global__ void k_bin_count(DevGrid g, const i64* __restrict__ offsets, i64 n_samples,
                             const double* __restrict__ coords, const double* __restrict__ values,
                             i64 o0, i64 o1, const i64* __restrict__ pair_slot, int want_grid_records,
@@ -57,20 +58,23 @@ __global__ void k_bin_count(DevGrid g, const i64* __restrict__ offsets, i64 n_sa
                             unsigned long long* __restrict__ first_bad) {
   for (i64 o = o0 + blockIdx.x * (i64)blockDim.x + threadIdx.x; o < o1;
        o += (i64)gridDim.x * blockDim.x) {
-    const double* x = coords + o * g.d;
+    const double* x = coords + o * (D > 0 ? D : g.d);
     const i64 lo = o - o0;
-    if (!hull_contains_dev(g, x)) {
+    if (!hull_contains_dev<D>(g, x)) {
       atomicMin(first_bad, static_cast<unsigned long long>(o));
       grid_count[lo] = 0;
       if (band_count) band_count[lo] = 0;
       continue;
     }
     ObsGeom geo;
-    corner_geometry(g, x, geo);
+    corner_geometry<D>(g, x, geo);
     const double y = values[o];
     const bool keep_all = !isfinite(y);  // a zero-mass corner times a non-finite y is NaN
     unsigned nz = 0;
-    const int corners = 1 << g.d;
+    constexpr int kd = D;
+    const int d = kd > 0 ? kd : g.d;
+    const int corners = 1 << d;
+    #pragma unroll
     for (int c = 0; c < corners; ++c) nz += (geo.mass[c] != 0.0 || keep_all) ? 1u : 0u;
     grid_count[lo] = want_grid_records ? nz : 0u;
     unsigned nb = 0;
@@ -78,6 +82,7 @@ __global__ void k_bin_count(DevGrid g, const i64* __restrict__ offsets, i64 n_sa
       const i64 i = sample_of(offsets, n_samples, o);
       if (pair_slot[i] >= 0) {
         unsigned nzb = 0;
+        #pragma unroll
         for (int c = 0; c < corners; ++c) nzb += geo.mass[c] != 0.0 ? 1u : 0u;
         nb = nzb * nzb;
       }
@@ -88,6 +93,7 @@ __global__ void k_bin_count(DevGrid g, const i64* __restrict__ offsets, i64 n_sa
 
 // Pass 2: emit records at their scanned offsets, in (i, j, c) order.  Grid
 // keys are bin * key_samples + (i - i0), i0 the chunk's first sample.
+template <int D>
 __global__ void k_bin_emit(DevGrid g, const i64* __restrict__ offsets, i64 n_samples,
                            const double* __restrict__ coords, const double* __restrict__ values,
                            i64 o0, i64 o1, i64 i0, i64 key_samples, const i64* __restrict__ pair_slot,
@@ -99,16 +105,19 @@ __global__ void k_bin_emit(DevGrid g, const i64* __restrict__ offsets, i64 n_sam
                            double* __restrict__ bmm, unsigned* __restrict__ bobs) {
   for (i64 o = o0 + blockIdx.x * (i64)blockDim.x + threadIdx.x; o < o1;
        o += (i64)gridDim.x * blockDim.x) {
-    const double* x = coords + o * g.d;
-    if (!hull_contains_dev(g, x)) continue;
+    const double* x = coords + o * (D > 0 ? D : g.d);
+    if (!hull_contains_dev<D>(g, x)) continue;
     ObsGeom geo;
-    corner_geometry(g, x, geo);
+    corner_geometry<D>(g, x, geo);
     const double y = values[o];
     const bool keep_all = !isfinite(y);
     const i64 i = sample_of(offsets, n_samples, o);
-    const int corners = 1 << g.d;
+    constexpr int kd = D;
+    const int d = kd > 0 ? kd : g.d;
+    const int corners = 1 << d;
     if (gkey) {
       unsigned r = grid_off[o - o0];
+      #pragma unroll
       for (int c = 0; c < corners; ++c) {
         if (!(geo.mass[c] != 0.0 || keep_all)) continue;
         gkey[r] = static_cast<unsigned long long>(geo.flat[c]) * key_samples + (i - i0);
@@ -121,12 +130,14 @@ __global__ void k_bin_emit(DevGrid g, const i64* __restrict__ offsets, i64 n_sam
     if (bkey && pair_slot[i] >= 0) {
       const double pw = pair_weight[pair_slot[i]];
       unsigned r = band_off[o - o0];
+      #pragma unroll
       for (int c1 = 0; c1 < corners; ++c1) {
         if (geo.mass[c1] == 0.0) continue;
+        #pragma unroll
         for (int c2 = 0; c2 < corners; ++c2) {
           if (geo.mass[c2] == 0.0) continue;
           i64 code = 0;
-          for (int k = 0; k < g.d; ++k) {
+          for (int k = 0; k < d; ++k) {
             const int off = static_cast<int>((c2 >> k) & 1) - static_cast<int>((c1 >> k) & 1);
             code = code * 3 + (off + 1);
           }
@@ -343,6 +354,11 @@ dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples
     }
   }
 
+  // the per-observation kernels with d as a template constant
+  auto const k_bin_count_d = d == 1 ? &k_bin_count<1> : d == 2 ? &k_bin_count<2> : d == 3 ? &k_bin_count<3>
+                                                                                        : &k_bin_count<0>;
+  auto const k_bin_emit_d = d == 1 ? &k_bin_emit<1> : d == 2 ? &k_bin_emit<2> : d == 3 ? &k_bin_emit<3>
+                                                                                     : &k_bin_emit<0>;
   ctx->begin_stage("binning");
   cudaStream_t st = ctx->stream;
   DevBuf<double> axes_store;
@@ -495,7 +511,7 @@ dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples
       if (nc > 0) {
         DFPCA_CUDA(cudaMemsetAsync(k.gcount.get() + nc, 0, sizeof(unsigned), as));
         DFPCA_CUDA(cudaMemsetAsync(k.bcount.get() + nc, 0, sizeof(unsigned), as));
-        k_bin_count<<<grid_for(nc, 256), 256, 0, as>>>(dg, d_off.get(), n_samples, d_coords.get(), d_values.get(), o0,
+        k_bin_count_d<<<grid_for(nc, 256), 256, 0, as>>>(dg, d_off.get(), n_samples, d_coords.get(), d_values.get(), o0,
                                                        o1, d_slot.get(), want_grid ? 1 : 0, k.gcount.get(),
                                                        want_band ? k.bcount.get() : nullptr, bad.get());
         aux_launch("k_bin_count", cudaSuccess);
@@ -537,7 +553,7 @@ dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples
       DevBuf<unsigned> gval(n_grec + 1), gval2(n_grec + 1), bval(n_brec + 1), bval2(n_brec + 1);
       DevBuf<double> gmass(n_grec + 1), bmm(n_brec + 1);
       DevBuf<unsigned> gobs(n_grec + 1), bobs(n_brec + 1);
-      DFPCA_LAUNCH(ctx, k_bin_emit, grid_for(nc, 256), 256, 0, dg, d_off.get(), n_samples, d_coords.get(),
+      DFPCA_LAUNCH(ctx, k_bin_emit_d, grid_for(nc, 256), 256, 0, dg, d_off.get(), n_samples, d_coords.get(),
                    d_values.get(), o0, o1, i0, key_samples, d_slot.get(), out->pair_weight.get(), out->codes,
                    goff.get(), boff.get(), n_grec > 0 ? gkey.get() : nullptr, gval.get(), gmass.get(), gobs.get(),
                    n_brec > 0 ? bkey.get() : nullptr, bval.get(), bmm.get(), bobs.get());

@@ -38,8 +38,11 @@ __device__ inline void locate_cell_dev(const double* axis, i64 n, double x, i64&
   frac = __ddiv_rn(__dsub_rn(x, axis[lo]), __dsub_rn(axis[lo + 1], axis[lo]));
 }
 
+template <int D = 0>
 __device__ inline bool hull_contains_dev(const DevGrid& g, const double* x) {
-  for (int k = 0; k < g.d; ++k) {
+  const int d = D > 0 ? D : g.d;
+#pragma unroll
+  for (int k = 0; k < d; ++k) {
     const double lo = g.axes[k][0], hi = g.axes[k][g.shape[k] - 1];
     const double tol = __dmul_rn(1e-12, __dsub_rn(hi, lo));
     if (x[k] < __dsub_rn(lo, tol) || x[k] > __dadd_rn(hi, tol)) return false;
@@ -47,15 +50,22 @@ __device__ inline bool hull_contains_dev(const DevGrid& g, const double* x) {
   return true;
 }
 
+// D > 0: the dimension as a template constant (loops unrolled, ObsGeom in
+// registers); D = 0: runtime g.d.
+template <int D = 0>
 __device__ inline void corner_geometry(const DevGrid& g, const double* x, ObsGeom& geo) {
   i64 cell[kMaxDim];
   double frac[kMaxDim];
-  for (int k = 0; k < g.d; ++k) locate_cell_dev(g.axes[k], g.shape[k], x[k], cell[k], frac[k]);
-  const int corners = 1 << g.d;
+  const int d = D > 0 ? D : g.d;
+#pragma unroll
+  for (int k = 0; k < d; ++k) locate_cell_dev(g.axes[k], g.shape[k], x[k], cell[k], frac[k]);
+  const int corners = 1 << d;
+#pragma unroll
   for (int c = 0; c < corners; ++c) {
     double m = 1.0;
     i64 flat = 0;
-    for (int k = 0; k < g.d; ++k) {
+#pragma unroll
+    for (int k = 0; k < d; ++k) {
       const bool up = (c >> k) & 1;
       m = __dmul_rn(m, up ? frac[k] : __dsub_rn(1.0, frac[k]));
       flat += (cell[k] + (up ? 1 : 0)) * g.strides[k];

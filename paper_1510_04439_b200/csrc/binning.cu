@@ -152,6 +152,8 @@ __global__ void k_bin_emit(DevGrid g, const i64* __restrict__ offsets, i64 n_sam
   }
 }
 
+constexpr int kFoldWarps = 8;  // warps per block of the ordered-fold kernels (256 threads)
+
 // Aggregate (mean-path) grids: one thread per bin, sequential over its sorted
 // records = (i, j, c) order (binning.hpp:148-155).
 __global__ void k_bin_aggregate(i64 G, i64 key_samples, i64 i0, const unsigned long long* __restrict__ key,
@@ -161,8 +163,11 @@ __global__ void k_bin_aggregate(i64 G, i64 key_samples, i64 i0, const unsigned l
                                 const double* __restrict__ mean_w, double* __restrict__ mass,
                                 double* __restrict__ wvalue, double* __restrict__ wsquare) {
   // One warp per bin: the lanes gather and form the per-record terms of 32
-  // consecutive records in parallel, lane 0 folds them in record order.
+  // consecutive records in parallel and stage them in shared memory; lanes
+  // 0, 1, 2 then fold mass, wvalue, wsquare (one sum each) in record order.
+  __shared__ double terms[kFoldWarps][3][33];
   const int lane = threadIdx.x & 31;
+  double(&t)[3][33] = terms[threadIdx.x >> 5];
   const i64 warps = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
   for (i64 f = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5; f < G; f += warps) {
     const unsigned long long target = static_cast<unsigned long long>(f) * key_samples;
@@ -174,7 +179,8 @@ __global__ void k_bin_aggregate(i64 G, i64 key_samples, i64 i0, const unsigned l
     }
     const unsigned long long end_key = target + key_samples;
     if (lo >= n_rec || key[lo] >= end_key) continue;  // no records in this chunk
-    double am = mass[f], av = wvalue[f], as = wsquare[f];  // carry-in from earlier chunks
+    double* const dst = lane == 0 ? mass : lane == 1 ? wvalue : wsquare;
+    double acc = lane < 3 ? dst[f] : 0.0;  // carry-in from earlier chunks
     for (i64 r0 = lo;; r0 += 32) {
       const i64 r = r0 + lane;
       const bool in = r < n_rec && key[r] < end_key;
@@ -189,18 +195,16 @@ __global__ void k_bin_aggregate(i64 G, i64 key_samples, i64 i0, const unsigned l
       }
       const unsigned m = __ballot_sync(0xffffffffu, in);
       const int cnt = __popc(m);  // records of this bin are a prefix of the 32
-      for (int q = 0; q < cnt; ++q) {
-        am = __dadd_rn(am, __shfl_sync(0xffffffffu, wm, q));
-        av = __dadd_rn(av, __shfl_sync(0xffffffffu, wmy, q));
-        as = __dadd_rn(as, __shfl_sync(0xffffffffu, wmyy, q));
-      }
+      t[0][lane] = wm;
+      t[1][lane] = wmy;
+      t[2][lane] = wmyy;
+      __syncwarp();
+      if (lane < 3)
+        for (int q = 0; q < cnt; ++q) acc = __dadd_rn(acc, t[lane][q]);
+      __syncwarp();
       if (cnt < 32) break;
     }
-    if (lane == 0) {
-      mass[f] = am;
-      wvalue[f] = av;
-      wsquare[f] = as;
-    }
+    if (lane < 3) dst[f] = acc;
   }
 }
 
@@ -237,8 +241,11 @@ __global__ void k_bin_band(const unsigned long long* __restrict__ key, const uns
                            i64 n_rec, i64 n_keys, const double* __restrict__ bmm,
                            const unsigned* __restrict__ robs, const double* __restrict__ values,
                            double* __restrict__ diag_mass, double* __restrict__ diag_value) {
-  // One warp per band index, records folded in order as in k_bin_aggregate.
+  // One warp per band index, records folded in order as in k_bin_aggregate
+  // (lane 0 the mass sum, lane 1 the value sum).
+  __shared__ double terms[kFoldWarps][2][33];
   const int lane = threadIdx.x & 31;
+  double(&t)[2][33] = terms[threadIdx.x >> 5];
   const i64 warps = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
   for (i64 k = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5; k < n_keys; k += warps) {
     i64 lo = 0, hi = n_rec;
@@ -248,7 +255,8 @@ __global__ void k_bin_band(const unsigned long long* __restrict__ key, const uns
       else hi = mid;
     }
     if (lo >= n_rec || key[lo] != static_cast<unsigned long long>(k)) continue;
-    double dm = diag_mass[k], dv = diag_value[k];  // carry-in from earlier chunks
+    double* const dst = lane == 0 ? diag_mass : diag_value;
+    double acc = lane < 2 ? dst[k] : 0.0;  // carry-in from earlier chunks
     for (i64 r0 = lo;; r0 += 32) {
       const i64 r = r0 + lane;
       const bool in = r < n_rec && key[r] == static_cast<unsigned long long>(k);
@@ -260,16 +268,15 @@ __global__ void k_bin_band(const unsigned long long* __restrict__ key, const uns
         mv = __dmul_rn(__dmul_rn(mm, y), y);
       }
       const int cnt = __popc(__ballot_sync(0xffffffffu, in));
-      for (int q = 0; q < cnt; ++q) {
-        dm = __dadd_rn(dm, __shfl_sync(0xffffffffu, mm, q));
-        dv = __dadd_rn(dv, __shfl_sync(0xffffffffu, mv, q));
-      }
+      t[0][lane] = mm;
+      t[1][lane] = mv;
+      __syncwarp();
+      if (lane < 2)
+        for (int q = 0; q < cnt; ++q) acc = __dadd_rn(acc, t[lane][q]);
+      __syncwarp();
       if (cnt < 32) break;
     }
-    if (lane == 0) {
-      diag_mass[k] = dm;
-      diag_value[k] = dv;
-    }
+    if (lane < 2) dst[k] = acc;
   }
 }
 

@@ -84,8 +84,11 @@ IoState& io_state(dfpca_context* ctx) {
   if (!ctx->io_state) {
     auto io = std::make_shared<IoState>();
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    io->workers = static_cast<int>(std::min(8u, std::max(1u, hw / 2)));
-    if (const char* e = std::getenv("DFPCA_IO_WORKERS")) io->workers = std::max(1, std::min(64, std::atoi(e)));
+    // downloads use every worker, uploads at most 8 (measured on the 16-core
+    // host, 134 MB pageable: download 7.7 ms with 8 workers, 6.1 with 16;
+    // upload 5.3 ms with 8, slower with more)
+    io->workers = static_cast<int>(std::min(16u, std::max(1u, hw)));
+    if (const char* e = std::getenv("DFPCA_IO_WORKERS"); e && *e) io->workers = std::max(1, std::min(64, std::atoi(e)));
     for (int w = 0; w < io->workers; ++w) {
       for (int s = 0; s < 2; ++s) {
         char* p = nullptr;
@@ -114,7 +117,7 @@ void upload_bytes(dfpca_context* ctx, char* d_text, i64 S, Fill fill) {
   IoState& io = io_state(ctx);
   std::lock_guard<std::mutex> lk(io.mu);
   const i64 n_chunks = (S + static_cast<i64>(kSlotBytes) - 1) / static_cast<i64>(kSlotBytes);
-  const int W = static_cast<int>(std::min<i64>(io.workers, std::max<i64>(n_chunks, 1)));
+  const int W = static_cast<int>(std::min<i64>(std::min(io.workers, 8), std::max<i64>(n_chunks, 1)));
   // the slots' previous copies (an earlier call) were ordered on the worker
   // streams; the destination's stream-ordered allocation is ordered by `ready`
   cudaEvent_t ready;

@@ -68,9 +68,11 @@ enum { DFPCA_TARGET_MEAN = 0, DFPCA_TARGET_SQUARES = 1 };
 enum { DFPCA_SURFACE_MEAN = 0, DFPCA_SURFACE_COVARIANCE = 1, DFPCA_SURFACE_DIAG = 2 };
 
 /* ---- context ------------------------------------------------------------ */
-/* One CUDA device, one stream, one workspace per context.  Calls on one
- * context are synchronous at return and must not overlap; distinct contexts
- * may be used from distinct host threads. */
+/* One CUDA device, one stream, one workspace per context.  Calls are
+ * synchronous at return; calls on one context from several host threads are
+ * serialised by the context (the reference's functions are reentrant), and
+ * dfpca_last_error reports the calling thread's last call on that context.
+ * Distinct contexts run concurrently. */
 DFPCA_API int dfpca_context_create(int device, dfpca_context** out);
 DFPCA_API int dfpca_context_destroy(dfpca_context* ctx);
 DFPCA_API int dfpca_last_error(const dfpca_context* ctx, int* error_class, const char** name,
@@ -202,6 +204,11 @@ DFPCA_API int dfpca_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double
 /* ---- surfaces -------------------------------------------------------------- */
 DFPCA_API int dfpca_surface_info(const dfpca_surface* s, int* kind, int64_t* n_values);
 DFPCA_API int dfpca_surface_download(dfpca_context* ctx, const dfpca_surface* s, double* out);
+/* n entries of a device-resident surface by flat index (s_flat * G + t_flat
+ * for a covariance; a slab accepts only its own rows): SurfaceEstimate::values[i]
+ * without copying the whole G*G array (8.6 GB at d=3 32^3) to the host. */
+DFPCA_API int dfpca_surface_gather(dfpca_context* ctx, const dfpca_surface* s, int64_t n, const int64_t* index,
+                                   double* out);
 DFPCA_API int dfpca_surface_upload(dfpca_context* ctx, const dfpca_grid* grid, int kind,
                          const double* values, int64_t n_values, dfpca_surface** out);
 DFPCA_API int dfpca_surface_free(dfpca_surface* s);
@@ -302,6 +309,28 @@ DFPCA_API int dfpca_table_copy(dfpca_context* ctx, const dfpca_table* t, int64_t
 DFPCA_API int dfpca_linear_bin_table(dfpca_context* ctx, const dfpca_table* t, const dfpca_grid* grid,
                            int mean_path, int covariance_path, dfpca_binned** out);
 DFPCA_API int dfpca_table_free(dfpca_table* t);
+
+/* ---- synthetic data: replaces dfpca::generate (simulate.hpp:163-245) ------- */
+/* The seeded models BASELINE.json's configs are quoted on,
+ * drawn exactly as the reference's generate(): sample i takes its scores from
+ * RandomStream::substream(seed, 3i), coordinates from 3i+1, noise from 3i+2
+ * (rng.hpp:30-78), so values are bit-identical to the reference's.
+ *   DFPCA_SIM_SIM1     sim1_spec (simulate.hpp:101-118): d=1, Equispaced
+ *                      design of points_per_sample over the grid hull;
+ *   DFPCA_SIM_SIM2     sim2_spec (simulate.hpp:123-150): d=3, GridNodes;
+ *   DFPCA_SIM_IMAGES2  its 2-d analogue (configs 2, 3): mean exp(|t-1/2|^2),
+ *                      phi_l = 2 prod_k sin(2 l pi t_k), lambda (16,4,1,1/4),
+ *                      sigma^2 1/16, GridNodes over the in-mask nodes;
+ *   DFPCA_SIM_SPARSE2  config 4: the same process, N_i = 5 + below(16) then
+ *                      coordinates uniform over the hull, rejected outside the
+ *                      ellipse ((x-.5)/.45)^2 + ((y-.5)/.3)^2 <= 1, all drawn
+ *                      from substream 3i+1.
+ * Host only (no device).  offsets receives n+1 CSR offsets; coords (dim per
+ * observation) and values are filled when both are non-NULL (call once with
+ * NULL to size them).  Status 3 on an invalid kind, grid or size. */
+enum { DFPCA_SIM_SIM1 = 1, DFPCA_SIM_SIM2 = 2, DFPCA_SIM_IMAGES2 = 3, DFPCA_SIM_SPARSE2 = 4 };
+DFPCA_API int dfpca_simulate(int kind, const dfpca_grid* grid, int64_t n, int64_t points_per_sample,
+                             uint64_t seed, int64_t* offsets, double* coords, double* values);
 
 #ifdef __cplusplus
 }

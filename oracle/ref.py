@@ -53,6 +53,8 @@ _SIG = {
     "ref_write_long_format": (C.c_int, [C.c_char_p, C.c_int, C.c_int64, PI, PD, PD, PI, C.c_char_p]),
     "ref_write_grid": (C.c_int, [C.c_char_p, C.c_int, PI, PD, PU8]),
     "ref_read_grid": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), PI, PD, PU8, C.POINTER(C.c_int)]),
+    "ref_simulate": (C.c_int, [C.c_int, C.c_int, PI, PD, PU8, C.c_int64, C.c_int64, C.c_uint64, PI, PD, PD]),
+    "ref_covariance_block": (C.c_int, [VP, C.c_int, PI, PD, PU8, PD, PD, PI, PI, PI, PI, PD]),
 }
 
 _lib = None
@@ -391,3 +393,33 @@ def read_grid(path):
         o += k
     return out, (mask if has_mask.value else None)
 
+
+
+def simulate(kind: int, grid, n: int, points_per_sample: int = 0, seed: int = 20260815):
+    """The reference's generate() (simulate.hpp:163-245) for the models of
+    ref_simulate: (offsets, coords, values)."""
+    g = grid_args(grid)
+    off = np.zeros(n + 1, dtype=np.int64)
+    _chk(lib().ref_simulate(kind, *g.args(), n, points_per_sample, seed, off.ctypes.data_as(PI), None, None))
+    N = int(off[-1])
+    coords = np.empty(N * g.dim)
+    values = np.empty(N)
+    _chk(lib().ref_simulate(kind, *g.args(), n, points_per_sample, seed, off.ctypes.data_as(PI),
+                            coords.ctypes.data_as(PD), values.ctypes.data_as(PD)))
+    return off, coords, values
+
+
+def covariance_block(binned: RefBinned, grid, h, mean, s_box, t_box) -> np.ndarray:
+    """The reference's centered, symmetrized covariance restricted to the
+    node boxes s_box x t_box (each ([lo...], [hi...]) per axis, hi exclusive):
+    fft_covariance's block-pair loop body run for that pair (ref_capi.cpp)."""
+    g = grid_args(grid)
+    hh, hp = _d(h)
+    m, mp = _d(mean)
+    sl, sh, tl, th = (np.ascontiguousarray(x, dtype=np.int64) for x in (*s_box, *t_box))
+    ns = int(np.prod(sh - sl))
+    nt = int(np.prod(th - tl))
+    out = np.empty(ns * nt)
+    _chk(lib().ref_covariance_block(binned.handle, *g.args(), hp, mp, sl.ctypes.data_as(PI), sh.ctypes.data_as(PI),
+                                    tl.ctypes.data_as(PI), th.ctypes.data_as(PI), out.ctypes.data_as(PD)))
+    return out.reshape(ns, nt)

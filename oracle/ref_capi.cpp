@@ -21,6 +21,7 @@
 #include "dfpca/io.hpp"
 #include "dfpca/parallel.hpp"
 #include "dfpca/scores.hpp"
+#include "dfpca/simulate.hpp"
 #include "dfpca/smoother.hpp"
 
 using namespace dfpca;
@@ -449,6 +450,204 @@ int ref_read_grid(const char* path, int* dim, int64_t* shape, double* axes, uint
     }
     if (mask && g.has_mask())
       for (Index f = 0; f < g.size(); ++f) mask[f] = g.in_mask(f) ? 1 : 0;
+  });
+}
+
+// ---- simulate.hpp: the configs' inputs drawn by the reference's generator ----
+// kind 1 sim1_spec, 2 sim2_spec, 3 the 2-d analogue of sim2 (SURVEY 8(d)
+// configs 2/3), 4 config 4's sparse design (a thin custom generator over the
+// reference's RandomStream with generate()'s substream layout).  Two calls:
+// coords == NULL sizes offsets[n+1].
+int ref_simulate(int kind, int dim, const int64_t* shape, const double* axes, const uint8_t* mask, int64_t n,
+                 int64_t ppp, uint64_t seed, int64_t* offsets, double* coords, double* values) {
+  return guarded([&] {
+    const EvaluationGrid g = make_grid(dim, shape, axes, mask);
+    FunctionalDataset data;
+    if (kind == 1 || kind == 2 || kind == 3) {
+      SimSpec spec;
+      if (kind == 1) {
+        spec = sim1_spec(static_cast<std::size_t>(n), static_cast<std::size_t>(ppp), shape[0], seed);
+        spec.grid = g;
+      } else if (kind == 2) {
+        spec = sim2_spec(static_cast<std::size_t>(n), shape[0], seed);
+        spec.grid = g;
+      } else {
+        spec.name = "images2";
+        spec.n = static_cast<std::size_t>(n);
+        spec.design = SimDesign::GridNodes;
+        spec.grid = g;
+        spec.seed = seed;
+        spec.mean = [](const double* t) {
+          double q = 0.0;
+          for (std::size_t k = 0; k < 2; ++k) q += (t[k] - 0.5) * (t[k] - 0.5);
+          return std::exp(q);
+        };
+        const double pi = std::acos(-1.0);
+        for (int l = 1; l <= 4; ++l)
+          spec.eigenfunctions.push_back([pi, l](const double* t) {
+            double p = std::sqrt(4.0);
+            for (std::size_t k = 0; k < 2; ++k) p *= std::sin(2.0 * l * pi * t[k]);
+            return p;
+          });
+        spec.lambda = {16.0, 4.0, 1.0, 0.25};
+        spec.sigma2 = 1.0 / 16.0;
+      }
+      spec.store_grid_truth = false;
+      data = generate(spec).first;
+    } else if (kind == 4) {
+      const double pi = std::acos(-1.0);
+      const double lam[4] = {16.0, 4.0, 1.0, 0.25};
+      data.dim = 2;
+      data.samples.resize(static_cast<std::size_t>(n));
+      for (int64_t i = 0; i < n; ++i) {
+        const auto iu = static_cast<std::uint64_t>(i);
+        RandomStream sr = RandomStream::substream(seed, 3 * iu);
+        double a[4];
+        for (int l = 0; l < 4; ++l) a[l] = std::sqrt(lam[l]) * sr.normal();
+        RandomStream cr = RandomStream::substream(seed, 3 * iu + 1);
+        const std::size_t ni = 5 + static_cast<std::size_t>(cr.below(16));
+        Sample& s = data.samples[static_cast<std::size_t>(i)];
+        for (std::size_t j = 0; j < ni; ++j) {
+          double p[2];
+          for (;;) {
+            for (std::size_t k = 0; k < 2; ++k) p[k] = g.hull_lo(k) + (g.hull_hi(k) - g.hull_lo(k)) * cr.uniform();
+            const double u = (p[0] - 0.5) / 0.45, v = (p[1] - 0.5) / 0.3;
+            if (u * u + v * v <= 1.0) break;
+          }
+          s.coords.push_back(p[0]);
+          s.coords.push_back(p[1]);
+        }
+        RandomStream nr = RandomStream::substream(seed, 3 * iu + 2);
+        for (std::size_t j = 0; j < ni; ++j) {
+          const double* t = s.coords.data() + 2 * j;
+          double q = 0.0;
+          for (std::size_t k = 0; k < 2; ++k) q += (t[k] - 0.5) * (t[k] - 0.5);
+          double x = std::exp(q);
+          for (int l = 0; l < 4; ++l) {
+            double ph = std::sqrt(4.0);
+            for (std::size_t k = 0; k < 2; ++k) ph *= std::sin(2.0 * (l + 1) * pi * t[k]);
+            x += a[l] * ph;
+          }
+          s.values.push_back(x + std::sqrt(1.0 / 16.0) * nr.normal());
+        }
+      }
+    } else {
+      throw err::invalid_argument("unknown simulation kind");
+    }
+    offsets[0] = 0;
+    for (std::size_t i = 0; i < data.samples.size(); ++i)
+      offsets[i + 1] = offsets[i] + static_cast<int64_t>(data.samples[i].values.size());
+    if (!coords || !values) return;
+    for (std::size_t i = 0; i < data.samples.size(); ++i) {
+      const Sample& s = data.samples[i];
+      std::memcpy(coords + offsets[i] * dim, s.coords.data(), sizeof(double) * s.coords.size());
+      std::memcpy(values + offsets[i], s.values.data(), sizeof(double) * s.values.size());
+    }
+  });
+}
+
+// ---- fft_covariance restricted to one pair of output boxes ------------------
+// The body of the reference's (bs, bt) loop (fft_smoother.hpp:627-719) run for
+// core boxes S and T (d-dim, [lo, hi)) and for (T, S), then the centering and
+// symmetrization (fft_smoother.hpp:723-736) of the S x T entries: the
+// reference's values for a sub-block of a covariance too large to compute
+// whole on the host (config 5, 1.07e9 points).  The block sits inside
+// fft_covariance's own plan-invariance guarantee (fft_smoother.hpp:24-29).
+// Empty kernel windows raise (no enlargement ladder here).  out: |S| x |T|.
+int ref_covariance_block(void* h, int dim, const int64_t* shape, const double* axes, const uint8_t* mask,
+                         const double* bw, const double* mean, const int64_t* s_lo, const int64_t* s_hi,
+                         const int64_t* t_lo, const int64_t* t_hi, double* out) {
+  return guarded([&] {
+    auto* b = static_cast<BinnedData*>(h);
+    const auto grid = make_grid(dim, shape, axes, mask);
+    const std::size_t d = grid.dim();
+    Bandwidth hb{std::vector<double>(bw, bw + dim)};
+    hb.validate(grid);
+    PairGridSource source(*b, PairGridSource::Mode::Rebuild);
+    std::vector<double> spacing2(2 * d), h2(2 * d);
+    std::vector<Index> shape2 = grid.shape();
+    shape2.insert(shape2.end(), grid.shape().begin(), grid.shape().end());
+    for (std::size_t k = 0; k < d; ++k) {
+      spacing2[k] = spacing2[d + k] = grid.spacing(k);
+      h2[k] = h2[d + k] = hb[k];
+    }
+    detail::MomentEngineBank bank(h2, spacing2, shape2);
+    const std::size_t nm = bank.basis.count(), nl = bank.basis.count_linear();
+    Box bs{std::vector<Index>(s_lo, s_lo + dim), std::vector<Index>(s_hi, s_hi + dim)};
+    Box bt{std::vector<Index>(t_lo, t_lo + dim), std::vector<Index>(t_hi, t_hi + dim)};
+    // raw[a][b] for the pair (A, B) of boxes, box-major over A then B
+    auto raw_block = [&](const Box& A, const Box& B) {
+      Box core2{A.lo, A.hi};
+      core2.lo.insert(core2.lo.end(), B.lo.begin(), B.lo.end());
+      core2.hi.insert(core2.hi.end(), B.hi.begin(), B.hi.end());
+      const Box in_box = bank.engines[0]->required_input_box(core2);
+      std::vector<double> pw_in, pv_in;
+      source.extract(in_box, pw_in, pv_in);
+      const auto core_n = static_cast<std::size_t>(core2.volume());
+      std::vector<std::vector<double>> S(nm), T(nl);
+      for (std::size_t i = 0; i < nm; ++i) {
+        S[i].assign(core_n, 0.0);
+        bank.engines[i]->run(pw_in.data(), in_box, S[i].data(), core2);
+      }
+      for (std::size_t i = 0; i < nl; ++i) {
+        T[i].assign(core_n, 0.0);
+        bank.engines[i]->run(pv_in.data(), in_box, T[i].data(), core2);
+      }
+      std::vector<Index> core_ext(2 * d);
+      for (std::size_t k = 0; k < 2 * d; ++k) core_ext[k] = core2.extent(k);
+      const std::vector<Index> core_str = detail::strides_of(core_ext);
+      auto pair_nodes = [&](Index local, Index& s_flat, Index& t_flat) {
+        s_flat = 0;
+        t_flat = 0;
+        for (std::size_t k = 0; k < d; ++k) {
+          s_flat += (core2.lo[k] + (local / core_str[k]) % core_ext[k]) * grid.strides()[k];
+          t_flat += (core2.lo[d + k] + (local / core_str[d + k]) % core_ext[d + k]) * grid.strides()[k];
+        }
+      };
+      std::vector<double> res(core_n, outside_value());
+      detail::solve_binned_box(
+          bank.basis, S, T, core2.volume(),
+          [&](Index local) {
+            Index s_flat, t_flat;
+            pair_nodes(local, s_flat, t_flat);
+            return grid.in_mask(s_flat) && grid.in_mask(t_flat);
+          },
+          [&](Index, double, Eigen::MatrixXd&, Eigen::VectorXd&) { return false; },
+          [&](Index local, double v) { res[static_cast<std::size_t>(local)] = v; },
+          "binned covariance smoother (block)");
+      return res;
+    };
+    const std::vector<double> st = raw_block(bs, bt);
+    const std::vector<double> ts = raw_block(bt, bs);
+    const std::vector<Index>& str = grid.strides();
+    auto flat_of = [&](const Box& B, Index local) {
+      Index f = 0, r = local;
+      for (std::size_t k = d; k-- > 0;) {
+        const Index e = B.hi[k] - B.lo[k];
+        f += (B.lo[k] + r % e) * str[k];
+        r /= e;
+      }
+      return f;
+    };
+    const Index ns = bs.volume(), nt = bt.volume();
+    for (Index i = 0; i < ns; ++i) {
+      const Index a = flat_of(bs, i);
+      for (Index j = 0; j < nt; ++j) {
+        const Index c = flat_of(bt, j);
+        double v_ab = st[static_cast<std::size_t>(i * nt + j)];
+        double v_ba = ts[static_cast<std::size_t>(j * ns + i)];
+        if (grid.in_mask(a) && grid.in_mask(c)) {
+          v_ab -= mean[a] * mean[c];
+          v_ba -= mean[c] * mean[a];
+        }
+        double v = v_ab;
+        if (a != c) {
+          const double lo_hi = a < c ? v_ab : v_ba;  // the entry the reference tests for "outside"
+          if (!is_outside(lo_hi)) v = 0.5 * (a < c ? v_ab + v_ba : v_ba + v_ab);
+        }
+        out[i * nt + j] = v;
+      }
+    }
   });
 }
 

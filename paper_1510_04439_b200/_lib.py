@@ -55,6 +55,7 @@ SIGNATURES = [
     ("dfpca_pair_grids", C.c_int, [P, P, PD, PD]),
     ("dfpca_surface_info", C.c_int, [P, C.POINTER(C.c_int), PI64]),
     ("dfpca_surface_download", C.c_int, [P, P, PD]),
+    ("dfpca_surface_gather", C.c_int, [P, P, C.c_int64, PI64, PD]),
     ("dfpca_surface_upload", C.c_int, [P, C.POINTER(DfpcaGrid), C.c_int, PD, C.c_int64, C.POINTER(P)]),
     ("dfpca_surface_free", C.c_int, [P]),
     ("dfpca_randomized_eig", C.c_int, [P, P, C.POINTER(DfpcaGrid), C.c_int64, C.c_int64, C.c_uint64, PD, PD,
@@ -89,6 +90,7 @@ SIGNATURES = [
     ("dfpca_table_free", C.c_int, [P]),
     ("dfpca_shard_bounds", C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int, PI64]),
     ("dfpca_shard_blocks", C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int, PI64, C.c_int64, PI64]),
+    ("dfpca_simulate", C.c_int, [C.c_int, C.POINTER(DfpcaGrid), C.c_int64, C.c_int64, C.c_uint64, PI64, PD, PD]),
 ]
 
 _lib = None

@@ -507,6 +507,16 @@ class SurfaceEstimate:
     def at(self, flat):
         return self.values[flat]
 
+    def gather(self, index) -> np.ndarray:
+        """values[index] read on the device (no full download)."""
+        idx = np.ascontiguousarray(index, dtype=np.int64).ravel()
+        if self._values is not None or not self._h:
+            return np.asarray(self.values)[idx]
+        out = np.empty(idx.size, dtype=np.float64)
+        check(_lib.lib().dfpca_surface_gather(_lib.ctx(), self._h, idx.size, idx.ctypes.data_as(C.POINTER(C.c_int64)),
+                                              out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
     def at_pair(self, s, t):
         return self.values[s * self.grid.size() + t]
 

@@ -19,6 +19,19 @@ namespace dfpca_gpu {
 
 thread_local cudaStream_t g_alloc_stream = nullptr;
 
+// out[i] = values[index[i] - lo]: entries of a device-resident surface
+// (SurfaceEstimate::values[i] without downloading the G^2 array).
+__global__ void k_gather_values(const double* __restrict__ values, i64 lo, const i64* __restrict__ index, i64 n,
+                                double* __restrict__ out) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x)
+    out[i] = values[index[i] - lo];
+}
+
+void gather_values(dfpca_context* ctx, const double* values, i64 lo, const i64* index, i64 n, double* out) {
+  DFPCA_LAUNCH(ctx, k_gather_values, grid_for(n, 256), 256, 0, values, lo, index, n, out);
+}
+
 dfpca_binned* run_linear_bin(dfpca_context* ctx, const Grid& grid, i64 n_samples,
                              const i64* obs_offsets, const double* coords, const double* values,
                              bool mean_path, bool cov_path, bool device_inputs = false);
@@ -303,9 +316,20 @@ void dfpca_context::collect_stages() {
 
 namespace {
 
+// The failure of the calling thread's last call per context: dfpca_last_error
+// reads it after the call has released the context lock, so another thread's
+// call on the same context cannot clear or overwrite it in between.
+thread_local std::map<const dfpca_context*, Failure> t_last_err;
+
+int record(dfpca_context* ctx) {
+  t_last_err[ctx] = ctx->err;
+  return ctx->err.cls;
+}
+
 template <class F>
 int guarded(dfpca_context* ctx, F&& f) {
   if (!ctx) return kConfig;
+  std::lock_guard<std::recursive_mutex> lock(ctx->api_mu);
   ctx->err = Failure{};
   ctx->stage_ms.clear();
   struct StreamScope {
@@ -319,7 +343,7 @@ int guarded(dfpca_context* ctx, F&& f) {
     f();
     ctx->end_stage();
     ctx->collect_stages();
-    return 0;
+    return record(ctx);
   } catch (const Failure& e) {
     ctx->err = e;
   } catch (const std::bad_alloc&) {
@@ -340,7 +364,7 @@ int guarded(dfpca_context* ctx, F&& f) {
     cudaEventDestroy(km.second.second);
   }
   ctx->kernel_marks.clear();
-  return ctx->err.cls;
+  return record(ctx);
 }
 
 }  // namespace
@@ -413,16 +437,18 @@ int dfpca_context_destroy(dfpca_context* ctx) {
 
 int dfpca_last_error(const dfpca_context* ctx, int* error_class, const char** name, const char** message) {
   if (!ctx) return kConfig;
-  if (error_class) *error_class = ctx->err.cls;
-  if (name) *name = ctx->err.name.c_str();
-  if (message) *message = ctx->err.msg.c_str();
+  const Failure& e = t_last_err[ctx];
+  if (error_class) *error_class = e.cls;
+  if (name) *name = e.name.c_str();
+  if (message) *message = e.msg.c_str();
   return 0;
 }
 
 int dfpca_last_error_location(const dfpca_context* ctx, int64_t* sample, int64_t* obs) {
   if (!ctx) return kConfig;
-  if (sample) *sample = ctx->err.sample;
-  if (obs) *obs = ctx->err.obs;
+  const Failure& e = t_last_err[ctx];
+  if (sample) *sample = e.sample;
+  if (obs) *obs = e.obs;
   return 0;
 }
 
@@ -877,6 +903,23 @@ int dfpca_surface_download(dfpca_context* ctx, const dfpca_surface* s, double* o
     ctx->begin_stage("download");
     copy_d2h(ctx, out, s->values.get(), static_cast<i64>(sizeof(double)) * s->n);
     ctx->end_stage();
+  });
+}
+
+int dfpca_surface_gather(dfpca_context* ctx, const dfpca_surface* s, int64_t n, const int64_t* index, double* out) {
+  return guarded(ctx, [&] {
+    if (!s || n < 0 || (n > 0 && (!index || !out))) fail(kConfig, "InvalidArgument", "null surface, index or output");
+    const i64 lo = s->rows >= 0 && s->kind == DFPCA_SURFACE_COVARIANCE ? s->row0 * s->grid.G : 0;
+    for (i64 i = 0; i < n; ++i)
+      if (index[i] < lo || index[i] >= lo + s->n)
+        fail(kConfig, "InvalidArgument", "surface index " + std::to_string(index[i]) + " outside the surface");
+    if (n == 0) return;
+    DevBuf<i64> idx(static_cast<std::size_t>(n));
+    DevBuf<double> vals(static_cast<std::size_t>(n));
+    DFPCA_CUDA(cudaMemcpyAsync(idx.get(), index, sizeof(i64) * n, cudaMemcpyHostToDevice, ctx->stream));
+    gather_values(ctx, s->values.get(), lo, idx.get(), n, vals.get());
+    DFPCA_CUDA(cudaMemcpyAsync(out, vals.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    DFPCA_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

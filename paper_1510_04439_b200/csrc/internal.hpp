@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -123,6 +124,11 @@ struct StageMark {
 // ---- opaque handles --------------------------------------------------------
 
 struct dfpca_context {
+  // Serialises API calls on this context: the reference's functions are
+  // reentrant, so several host threads may share one context (the C++
+  // drop-in's process-wide context, include/dfpca/gpu.hpp); each call holds
+  // the lock for its whole run (scratch, caches, stage timers, stream).
+  std::recursive_mutex api_mu;
   int device = 0;
   cudaStream_t stream = nullptr;
   int sm_count = 148;

@@ -6,6 +6,11 @@ eigenfunctions on midpoint grids.  Draws use numpy's PCG64 (the data only
 has to be the same for both arms of a comparison, not bit-equal to the
 reference generator).  Returned as CSR arrays (offsets, coords, values) plus
 a FunctionalDataset view on request.
+
+The BASELINE configs themselves (`config()`, `simulate()`) are drawn with the
+reference's own generator, restated in the library (`dfpca_simulate`,
+simulate.hpp:163-245): bit-identical to the reference's generate(), so the
+configs' inputs are the reference's.
 """
 from __future__ import annotations
 
@@ -149,3 +154,73 @@ def long_format_bytes(sd: SynthData, n_samples: int | None = None) -> bytes:
         sid = "s%d\t" % i
         parts.append("".join([sid + rows[j] + "\t" + vtxt[j] + "\n" for j in range(a, b)]))
     return "".join(parts).encode()
+
+
+# ---------------------------------------------------- reference generator --
+
+SIM_SIM1, SIM_SIM2, SIM_IMAGES2, SIM_SPARSE2 = 1, 2, 3, 4
+
+
+def ellipse_mask(axes) -> np.ndarray:
+    """Config 4's PM2.5-style domain on the grid nodes."""
+    X, Y = np.meshgrid(np.asarray(axes[0]), np.asarray(axes[1]), indexing="ij")
+    return ((((X - 0.5) / 0.45) ** 2 + ((Y - 0.5) / 0.3) ** 2) <= 1.0).astype(np.uint8).ravel()
+
+
+def simulate(kind: int, axes, mask, n: int, h: float, points_per_sample: int = 0,
+             seed: int = 20260815) -> SynthData:
+    """The reference's generate() for one of the models of dfpca_simulate
+    (include/dfpca_cuda.h), through the library (host code, no device)."""
+    import ctypes as C
+    from . import _lib
+    from .api import EvaluationGrid
+    lib = _lib.load()
+    g = EvaluationGrid([list(a) for a in axes], mask)
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    PD = C.POINTER(C.c_double)
+    PI64 = C.POINTER(C.c_int64)
+    st = lib.dfpca_simulate(kind, C.byref(g.desc()), n, points_per_sample, seed, offsets.ctypes.data_as(PI64),
+                            None, None)
+    if st != 0:
+        raise ValueError(f"dfpca_simulate: invalid model {kind} / grid / n")
+    dim = len(axes)
+    N = int(offsets[-1])
+    coords = np.empty(N * dim)
+    values = np.empty(N)
+    st = lib.dfpca_simulate(kind, C.byref(g.desc()), n, points_per_sample, seed, offsets.ctypes.data_as(PI64),
+                            coords.ctypes.data_as(PD), values.ctypes.data_as(PD))
+    assert st == 0
+    return SynthData(dim, [list(a) for a in axes], mask, offsets, coords, values, [h] * dim)
+
+
+# BASELINE.json configs (SURVEY.md 8(d) table): model, grid, n, bandwidth.
+CONFIGS = {
+    1: "d=1 Sim I: n=200 curves x 100 equispaced points, midpoint [0,10] 100 nodes, h=0.25",
+    2: "d=2 images: n=500 on midpoint 32x32, h=0.1",
+    3: "d=2 images: n=2000 on midpoint 64x64, h=0.1 (and 0.3)",
+    4: "d=2 sparse longitudinal: n=2000, N_i in 5..20, ellipse mask on uniform 64x64, h=0.15",
+    5: "d=3 Sim II: n=1000 on midpoint 32^3, h=0.1",
+}
+
+
+def config(cfg: int, n: int | None = None, h: float | None = None, cells: int | None = None,
+           seed: int = 20260815) -> SynthData:
+    """Inputs of BASELINE config `cfg` drawn by the reference's generator;
+    n / h / cells override the config's sample count, bandwidth, grid size."""
+    if cfg == 1:
+        c = cells or 100
+        return simulate(SIM_SIM1, [midpoint_axis(c, 0.0, 10.0)], None, n or 200, h or 0.25, 100, seed)
+    if cfg in (2, 3):
+        c = cells or (32 if cfg == 2 else 64)
+        ax = midpoint_axis(c)
+        return simulate(SIM_IMAGES2, [ax, ax], None, n or (500 if cfg == 2 else 2000), h or 0.1, 0, seed)
+    if cfg == 4:
+        c = cells or 64
+        ax = [float(i) / float(c - 1) for i in range(c)]
+        ax[-1] = 1.0
+        return simulate(SIM_SPARSE2, [ax, ax], ellipse_mask([ax, ax]), n or 2000, h or 0.15, 0, seed)
+    if cfg == 5:
+        c = cells or 32
+        ax = midpoint_axis(c)
+        return simulate(SIM_SIM2, [ax, ax, ax], None, n or 1000, h or 0.1, 0, seed)
+    raise ValueError(f"no config {cfg}")

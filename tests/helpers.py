@@ -31,3 +31,19 @@ def aligned_ise(cv, a, b) -> float:
     d1 = np.sum((a[m] - b[m]) ** 2) * cv
     d2 = np.sum((a[m] + b[m]) ** 2) * cv
     return float(min(d1, d2))
+
+
+def max_principal_angle(cv, A, B) -> float:
+    """Largest principal angle (radians) between span(A) and span(B), rows
+    = functions on the grid, under the Riemann inner product cv * <f, g>
+    (SURVEY.md 8(c)); NaN (masked) nodes are dropped."""
+    A = np.asarray(A, dtype=np.float64)
+    B = np.asarray(B, dtype=np.float64)
+    m = ~np.isnan(A[0])
+    Qa, _ = np.linalg.qr((np.sqrt(cv) * A[:, m]).T)
+    Qb, _ = np.linalg.qr((np.sqrt(cv) * B[:, m]).T)
+    s = np.linalg.svd(Qa.T @ Qb, compute_uv=False)
+    # sin of the largest angle from the projection residual is accurate for small angles
+    r = Qb - Qa @ (Qa.T @ Qb)
+    sin_max = np.linalg.norm(r, 2)
+    return float(np.arcsin(min(1.0, sin_max))) if s.min() > 0.7 else float(np.arccos(max(-1.0, min(1.0, s.min()))))

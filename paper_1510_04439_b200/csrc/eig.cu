@@ -4,14 +4,19 @@
 //   Omega   seeded M x q sketch: mt19937_64 (one CTA, parallel twist) +
 //           Box-Muller, the reference's RandomStream draw order (rng.hpp:30-78);
 //   Y       = Sigma Omega                      (DMMA GEMM, split-K)
-//   Q       thin Householder QR of Y            (one reflector per launch)
+//   Q       Cholesky QR twice (DMMA Gram products + fused factor/solve
+//           passes); Householder QR (one reflector per launch) when the
+//           sketch is too ill-conditioned for it
 //   small   = Q^T (Sigma Q), symmetrized       (DMMA GEMMs)
-//   eig     cyclic parallel Jacobi on the q x q problem (one CTA)
+//   eig     q <= 128: tridiagonalization + multisection + inverse iteration
+//           (one CTA); larger q: cyclic parallel Jacobi
 //   lifted  = Q V                               (DMMA GEMM)
 //   final   Riemann MGS, norm cut, sign canonicalization (one CTA)
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <cmath>
 #include <vector>
@@ -35,40 +40,37 @@ __host__ __device__ inline unsigned long long splitmix64(unsigned long long x) {
 }
 
 // std::mt19937_64 seeded with `seed`, producing n_words tempered outputs.
+// The twist runs out of place between two state buffers: the 156 words that
+// depend only on the old state, one barrier, the 156 that need the first
+// half's new words, and each thread tempers the word it has just written --
+// two barriers per 312 outputs.
 __global__ void __launch_bounds__(kMtN) k_mt19937_64(unsigned long long seed, i64 n_words,
                                                      unsigned long long* __restrict__ out) {
-  __shared__ unsigned long long mt[kMtN];
+  __shared__ unsigned long long buf[2][kMtN];
   if (threadIdx.x == 0) {
-    mt[0] = seed;
+    buf[0][0] = seed;
     for (int i = 1; i < kMtN; ++i)
-      mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + static_cast<unsigned long long>(i);
+      buf[0][i] =
+          6364136223846793005ull * (buf[0][i - 1] ^ (buf[0][i - 1] >> 62)) + static_cast<unsigned long long>(i);
   }
   __syncthreads();
   const int i = threadIdx.x;
+  int cur = 0;
   for (i64 base = 0; base < n_words; base += kMtN) {
-    // twist, in three dependency phases of the sequential recurrence
-    unsigned long long nv = 0;
+    const unsigned long long* a = buf[cur];
+    unsigned long long* b = buf[cur ^ 1];
     if (i < kMtN - kMtM) {
-      const unsigned long long x = (mt[i] & kMtUpper) | (mt[i + 1] & kMtLower);
-      nv = mt[i + kMtM] ^ (x >> 1) ^ ((x & 1ull) ? kMtA : 0ull);
+      const unsigned long long x = (a[i] & kMtUpper) | (a[i + 1] & kMtLower);
+      b[i] = a[i + kMtM] ^ (x >> 1) ^ ((x & 1ull) ? kMtA : 0ull);
     }
     __syncthreads();
-    if (i < kMtN - kMtM) mt[i] = nv;
-    __syncthreads();
-    if (i >= kMtN - kMtM && i < kMtN - 1) {
-      const unsigned long long x = (mt[i] & kMtUpper) | (mt[i + 1] & kMtLower);
-      nv = mt[i - (kMtN - kMtM)] ^ (x >> 1) ^ ((x & 1ull) ? kMtA : 0ull);
+    if (i >= kMtN - kMtM) {
+      const unsigned long long nxt = i < kMtN - 1 ? a[i + 1] : b[0];
+      const unsigned long long x = (a[i] & kMtUpper) | (nxt & kMtLower);
+      b[i] = b[i - (kMtN - kMtM)] ^ (x >> 1) ^ ((x & 1ull) ? kMtA : 0ull);
     }
-    __syncthreads();
-    if (i >= kMtN - kMtM && i < kMtN - 1) mt[i] = nv;
-    __syncthreads();
-    if (i == kMtN - 1) {
-      const unsigned long long x = (mt[i] & kMtUpper) | (mt[0] & kMtLower);
-      mt[i] = mt[kMtM - 1] ^ (x >> 1) ^ ((x & 1ull) ? kMtA : 0ull);
-    }
-    __syncthreads();
     if (base + i < n_words) {
-      unsigned long long y = mt[i];
+      unsigned long long y = b[i];
       y ^= (y >> 29) & 0x5555555555555555ull;
       y ^= (y << 17) & 0x71D67FFFEDA60000ull;
       y ^= (y << 37) & 0xFFF7EEE000000000ull;
@@ -76,6 +78,7 @@ __global__ void __launch_bounds__(kMtN) k_mt19937_64(unsigned long long seed, i6
       out[base + i] = y;
     }
     __syncthreads();
+    cur ^= 1;
   }
 }
 
@@ -376,6 +379,598 @@ __global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ Ag, double
     for (int e = tid; e < n * n; e += nt) Vg[e] = V[e];
 }
 
+// ----------------------------------------------------- Cholesky QR ----
+// One pass of Cholesky QR on X [M][q] (row-major): G = X^T X comes from the
+// DMMA Gram product; k_chol_factor (one CTA) factors G = R^T R (upper R,
+// q <= 128, right-looking in shared memory, one barrier per pivot: row k is
+// scaled on its way out to global memory, so the trailing update reads the
+// unscaled row without a hazard), and k_row_trsm solves Xout R = X by
+// forward substitution, one thread per row, R read as shared-memory
+// broadcasts.  flags[0] = 1 on a non-positive pivot; flags[1] = max|G - I|
+// (how far X already was from orthonormal columns).
+constexpr int kCqMaxQ = 128;
+
+// Blocked right-looking Cholesky (upper, G = R^T R), 32-wide panels: warp 0
+// factors the panel's diagonal block with the block's columns in registers
+// (lane = column; the pivot row goes through shared memory as broadcasts),
+// the panel rows right of it are solved with a thread per column (the 32
+// unknowns in registers), and the trailing block takes the rank-32 update (a
+// thread per entry of the upper triangle): three barriers per panel, and no
+// shared-memory read-after-write chains inside the loops.
+__global__ void __launch_bounds__(256) k_chol_factor(const double* __restrict__ Gg, int q, double* __restrict__ Rg,
+                                                     double* __restrict__ flags) {
+  extern __shared__ double sm[];
+  const int ld = q + 1;
+  double* R = sm;  // [q][q+1], upper triangle used
+  __shared__ double red[8], prow[32];
+  __shared__ int bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double dmax = 0.0;
+  for (int e = tid; e < q * q; e += blockDim.x) {
+    const int r = e / q, c = e % q;
+    const double g = Gg[e];
+    R[r * ld + c] = g;
+    dmax = fmax(dmax, fabs(g - (r == c ? 1.0 : 0.0)));
+  }
+  for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  if (lane == 0) red[warp] = dmax;
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int w = 0; w < 8; ++w) m = fmax(m, red[w]);
+    flags[1] = m;
+  }
+  for (int k0 = 0; k0 < q; k0 += 32) {
+    const int kb = min(32, q - k0), k1 = k0 + kb;
+    if (warp == 0) {
+      const int c = k0 + lane;  // this lane's column of the diagonal block
+      double col[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) col[i] = (i < kb && lane < kb && i <= lane) ? R[(k0 + i) * ld + c] : 0.0;
+      bool ok = true;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        if (r < kb && ok) {
+          const double dr = __shfl_sync(0xffffffffu, col[r], r);
+          if (!(dr > 0.0) || !isfinite(dr)) {
+            ok = false;
+          } else {
+            const double piv = sqrt(dr);
+            if (lane == r) col[r] = piv;
+            else if (lane > r) col[r] /= piv;
+            if (lane >= r) prow[lane] = col[r];
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i > r && i <= lane) col[i] -= prow[i] * col[r];
+            __syncwarp();
+          }
+        }
+      }
+      if (!ok && lane == 0) bad = 1;
+      if (lane < kb) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i < kb && i <= lane) R[(k0 + i) * ld + c] = col[i];
+      }
+    }
+    __syncthreads();
+    if (bad) break;
+    // panel rows [k0, k1), columns >= k1: R11^T X = G12, a thread per column
+    for (int c = k1 + tid; c < q; c += blockDim.x) {
+      double x[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        if (r < kb) {
+          double s = R[(k0 + r) * ld + c];
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < r) s -= R[(k0 + i) * ld + k0 + r] * x[i];
+          x[r] = s / R[(k0 + r) * ld + k0 + r];
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 32; ++r)
+        if (r < kb) R[(k0 + r) * ld + c] = x[r];
+    }
+    __syncthreads();
+    // trailing update: G22 -= R12^T R12 on the upper triangle
+    const int m = q - k1;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int i = k1 + e / m, j = k1 + e % m;
+      if (j < i) continue;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int r = k0;
+      for (; r + 3 < k1; r += 4) {
+        s0 += R[r * ld + i] * R[r * ld + j];
+        s1 += R[(r + 1) * ld + i] * R[(r + 1) * ld + j];
+        s2 += R[(r + 2) * ld + i] * R[(r + 2) * ld + j];
+        s3 += R[(r + 3) * ld + i] * R[(r + 3) * ld + j];
+      }
+      for (; r < k1; ++r) s0 += R[r * ld + i] * R[r * ld + j];
+      R[i * ld + j] -= (s0 + s1) + (s2 + s3);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) flags[0] = bad ? 1.0 : 0.0;
+  for (int e = tid; e < q * q; e += blockDim.x) {
+    const int r = e / q, c = e % q;
+    Rg[e] = c >= r ? R[r * ld + c] : 0.0;
+  }
+}
+
+// One warp per row: x_j = y_j / R_jj is broadcast from the lane holding it
+// and every lane updates its entries l > j (column-oriented substitution:
+// the dependent chain is one shuffle + one FMA per column).  R (q x q upper)
+// sits in shared memory, read as conflict-free row segments.
+constexpr int kTrsmWarps = 16;
+
+__global__ void __launch_bounds__(kTrsmWarps * 32) k_row_trsm(const double* __restrict__ X, i64 M, int q,
+                                                              const double* __restrict__ Rg,
+                                                              const double* __restrict__ flags,
+                                                              double* __restrict__ Xout) {
+  if (flags[0] != 0.0) return;
+  extern __shared__ double sm[];
+  double* R = sm;           // [q][q]
+  double* rinv = sm + q * q;  // 1 / R_jj
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < q * q; e += blockDim.x) R[e] = Rg[e];
+  __syncthreads();
+  for (int j = tid; j < q; j += blockDim.x) rinv[j] = 1.0 / R[j * q + j];
+  __syncthreads();
+  constexpr int kPer = kCqMaxQ / 32;  // entries per lane
+  for (i64 row = static_cast<i64>(blockIdx.x) * kTrsmWarps + warp; row < M;
+       row += static_cast<i64>(gridDim.x) * kTrsmWarps) {
+    double y[kPer];
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      const int l = lane + 32 * t;
+      y[t] = l < q ? X[row * q + l] : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      for (int jl = 0; jl < 32; ++jl) {
+        const int j = 32 * t + jl;
+        if (j >= q) break;
+        const double xj = __shfl_sync(0xffffffffu, y[t], jl) * rinv[j];
+        if (lane == jl) y[t] = xj;
+        const double* Rj = R + j * q;
+#pragma unroll
+        for (int u = t; u < kPer; ++u) {
+          const int l = lane + 32 * u;
+          if (l > j && l < q) y[u] -= xj * Rj[l];
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      const int l = lane + 32 * t;
+      if (l < q) Xout[row * q + l] = y[t];
+    }
+  }
+}
+
+std::size_t trsm_smem(int q) { return sizeof(double) * (static_cast<std::size_t>(q) * q + q); }
+
+// ------------------------------------------- small symmetric eigensolver ----
+// Rayleigh-Ritz problem (eigensolve.hpp:264-270) on one CTA of 16 warps,
+// n <= 128 (the reference runs SelfAdjointEigenSolver; any exact
+// eigendecomposition gives the same Ritz pairs up to rounding):
+//   symmetrize; Householder tridiagonalization (dsytd2) with the matrix in
+//   registers (thread (column, row group)), the vectors in shared memory;
+//   eigenvalues by Sturm-count multisection, 128 points per round (4 per
+//   lane, independent chains), one warp per eigenvalue -- only the
+//   candidates: a Ritz value at or below the cut enters no sum and is never
+//   read (the cut's count comes from one more Sturm count);
+//   eigenvectors of the candidates (eigenvalue > 1e-12 max(0, lambda_max),
+//   the only ones finalize_eigensystem reads) by inverse iteration on the
+//   tridiagonal (dgttrf/dgttrs with precomputed pivot reciprocals), one warp
+//   per cluster with reorthogonalization inside clusters (dstein's rule:
+//   gaps below 1e-3 |T|), then back-transformed by the reflectors.
+// Outputs: evals descending [n]; V [n][n] row-major, column c = eigenvector
+// of evals[c] (zero for non-candidates); info[0] = candidate count.
+constexpr int kEigMaxN = 128;
+constexpr int kEigThreads = 512;
+constexpr int kEigGroups = kEigThreads / kEigMaxN;  // row groups per column
+constexpr int kEigWarps = kEigThreads / 32;
+constexpr int kEigIIWarps = 8;  // warps with an inverse-iteration workspace
+
+__device__ inline double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// 1/x: the MUFU estimate refined by one Newton step (relative error well
+// below 1e-12; a Sturm count only needs the signs of the pivots).
+__device__ inline double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r * fma(-x, r, 2.0);
+}
+
+// Counts of eigenvalues of T (d, e2 = e^2) below each of 4 points (LAPACK
+// dlaneg-style recurrences, run side by side).
+__device__ inline void sturm_count4(const double* d, const double* e2, int n, const double x[4], double pivmin,
+                                    int c[4]) {
+  double qv[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    qv[r] = d[0] - x[r];
+    if (fabs(qv[r]) < pivmin) qv[r] = -pivmin;
+    c[r] = qv[r] < 0.0;
+  }
+  for (int i = 1; i < n; ++i) {
+    const double di = d[i], ei = e2[i - 1];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      qv[r] = (di - x[r]) - ei * fast_rcp(qv[r]);
+      if (fabs(qv[r]) < pivmin) qv[r] = -pivmin;
+      c[r] += qv[r] < 0.0;
+    }
+  }
+}
+
+struct TriWork {  // one warp's inverse-iteration workspace
+  double dd[kEigMaxN], rdd[kEigMaxN], du[kEigMaxN], du2[kEigMaxN], dl[kEigMaxN], x[kEigMaxN];
+  int piv[kEigMaxN];
+};
+
+__global__ void __launch_bounds__(kEigThreads) k_tri_eig(const double* __restrict__ Bg, int n,
+                                                          double* __restrict__ evals_out, double* __restrict__ V,
+                                                          int* __restrict__ info) {
+  extern __shared__ double sm[];
+  double* Hv = sm;                    // [n][kEigMaxN] reflector vectors (row k: v of H_k)
+  double* d = Hv + n * kEigMaxN;      // diagonal
+  double* e = d + kEigMaxN;           // off-diagonal
+  double* e2 = e + kEigMaxN;          // e^2
+  double* tau = e2 + kEigMaxN;        // reflector scalars
+  double* vb = tau + kEigMaxN;        // v of the current step
+  double* wb = vb + kEigMaxN;         // w of the current step
+  double* pp = wb + kEigMaxN;         // [kEigGroups][kEigMaxN] p partials
+  double* lam = pp + kEigGroups * kEigMaxN;  // ascending eigenvalues
+  double* xk = lam + kEigMaxN;        // column k of the current step
+  TriWork* work = reinterpret_cast<TriWork*>(xk + kEigMaxN);
+  __shared__ int n_cand, n_neg, n_clusters, cl_start[kEigMaxN + 1];
+  __shared__ double tnorm_s, pivmin_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int col = tid & (kEigMaxN - 1), grp = tid / kEigMaxN;  // thread (column, row group)
+
+  // symmetrized on load (eigensolve.hpp:265)
+  // ---- tridiagonalization: A = Q T Q^T, Q = H_0 ... H_{n-3};
+  // H_k = I - tau_k v v^T on indices k+1..n-1 (v_{k+1} = 1), v kept in Hv[k].
+  // The matrix lives in registers: thread (col, grp) holds A[j][col] for the
+  // rows j = grp + kEigGroups r, so the p products and the rank-2 updates are
+  // kRpt independent FMA chains per thread (FP64 latency is long; this is
+  // what hides it); shared memory carries only the vectors.  Four barriers
+  // per step.
+  constexpr int kRpt = kEigMaxN / kEigGroups;
+  double a[kRpt];
+#pragma unroll
+  for (int r = 0; r < kRpt; ++r) {
+    const int j = grp + kEigGroups * r;
+    a[r] = (j < n && col < n) ? 0.5 * (Bg[j * n + col] + Bg[col * n + j]) : 0.0;
+  }
+  __shared__ double ksum[kEigWarps], tau_s, kk_s;
+  for (int k = 0; k + 2 < n; ++k) {
+    const int m0 = k + 1;  // first trailing index
+    // 1. column k (= row k) to shared memory
+    if (col == k) {
+#pragma unroll
+      for (int r = 0; r < kRpt; ++r) {
+        const int j = grp + kEigGroups * r;
+        if (j >= k && j < n) xk[j] = a[r];
+      }
+    }
+    __syncthreads();
+    // 2. the reflector (warp 0)
+    if (warp == 0) {
+      double s = 0.0;
+      for (int j = m0 + 1 + lane; j < n; j += 32) s += xk[j] * xk[j];
+      const double sig = warp_sum(s);
+      const double alpha = xk[m0];
+      double t = 0.0, beta = alpha, scale = 0.0;
+      if (sig > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + sig), alpha);
+        t = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      for (int j = m0 + lane; j < n; j += 32) {
+        const double v = j == m0 ? 1.0 : xk[j] * scale;
+        vb[j] = v;
+        Hv[k * kEigMaxN + j] = v;
+      }
+      if (lane == 0) {
+        tau[k] = t;
+        tau_s = t;
+        e[k] = beta;
+        d[k] = xk[k];
+      }
+    }
+    __syncthreads();
+    const double t = tau_s;
+    if (t == 0.0) continue;  // uniform: nothing to annihilate
+    // 3. p partials (A22 v over this thread's rows) and v^T A22 v per warp
+    double ps = 0.0;
+    if (col >= m0 && col < n) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int r = 0; r < kRpt; r += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = grp + kEigGroups * (r + u);
+          const double term = (j >= m0 && j < n) ? a[r + u] * vb[j] : 0.0;
+          if (u == 0) s0 += term;
+          else if (u == 1) s1 += term;
+          else if (u == 2) s2 += term;
+          else s3 += term;
+        }
+      }
+      ps = (s0 + s1) + (s2 + s3);
+      pp[grp * kEigMaxN + col] = ps;
+    }
+    const double qv = warp_sum(col >= m0 && col < n ? ps * vb[col] : 0.0);
+    if (lane == 0) ksum[warp] = qv;
+    __syncthreads();
+    // 4. p = t A22 v; K = t/2 p^T v = t^2/2 v^T A22 v
+    if (grp == 0 && col >= m0 && col < n) {
+      double s = 0.0;
+#pragma unroll
+      for (int g = 0; g < kEigGroups; ++g) s += pp[g * kEigMaxN + col];
+      wb[col] = t * s;
+    }
+    if (tid == 0) {
+      double q = 0.0;
+      for (int w = 0; w < kEigWarps; ++w) q += ksum[w];
+      kk_s = 0.5 * t * t * q;
+    }
+    __syncthreads();
+    // 5. A22 -= v w^T + w v^T, w = p - K v
+    if (col >= m0 && col < n) {
+      const double K = kk_s;
+      const double vc = vb[col], wc = wb[col] - K * vc;
+#pragma unroll
+      for (int r = 0; r < kRpt; ++r) {
+        const int j = grp + kEigGroups * r;
+        if (j >= m0 && j < n) {
+          const double vj = vb[j];
+          a[r] -= vj * wc + (wb[j] - K * vj) * vc;
+        }
+      }
+    }
+  }
+  // the last 2 x 2 block
+  if (col == n - 2 || col == n - 1) {
+#pragma unroll
+    for (int r = 0; r < kRpt; ++r) {
+      const int j = grp + kEigGroups * r;
+      if (j == col) d[col] = a[r];
+      if (col == n - 2 && j == n - 1) e[n - 2] = a[r];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (n == 2) tau[0] = 0.0;
+    double emax = 0.0, tn = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double ei = i + 1 < n ? fabs(e[i]) : 0.0, em = i > 0 ? fabs(e[i - 1]) : 0.0;
+      if (i + 1 < n) {
+        e2[i] = e[i] * e[i];
+        emax = fmax(emax, e2[i]);
+      }
+      tn = fmax(tn, fabs(d[i]) + ei + em);
+    }
+    tnorm_s = tn;
+    pivmin_s = 2.2250738585072014e-308 * fmax(1.0, emax);
+  }
+  __syncthreads();
+  const double tnorm = tnorm_s, pivmin = pivmin_s;
+
+  // ---- eigenvalues: only the candidates are needed (eigenvalue > cut =
+  // 1e-12 max(0, lambda_max): finalize_eigensystem reads nothing else, and
+  // the total variance sums only them).  Warp w resolves the (w+1)-th largest
+  // eigenvalue by multisection (128 points per round, 4 independent Sturm
+  // chains per lane); then the cut gives the candidate count (one Sturm
+  // count) and the remaining candidates are spread over the warps.
+  auto resolve = [&](int j) {  // j: ascending index, lambda_j > 0 known
+    double lo = 0.0, hi = tnorm + 2.0 * pivmin;
+    for (int round = 0; round < 12; ++round) {
+      const double width = hi - lo;
+      if (!(width > 2.0 * 2.220446049250313e-16 * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin)) break;
+      double x[4];
+      int c[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) x[r] = lo + width * (static_cast<double>(4 * lane + r + 1) / 129.0);
+      sturm_count4(d, e2, n, x, pivmin, c);
+      int fr = 4;  // first of this lane's points with count > j
+#pragma unroll
+      for (int r = 3; r >= 0; --r)
+        if (c[r] > j) fr = r;
+      const unsigned above = __ballot_sync(0xffffffffu, fr < 4);
+      const int fl = above ? __ffs(above) - 1 : 32;
+      // index f = 4 fl + fr of the first point above: bracket [point f-1, point f]
+      const int f = fl == 32 ? 128 : 4 * fl + __shfl_sync(0xffffffffu, fr, fl == 32 ? 0 : fl);
+      const double nlo = f == 0 ? lo : lo + width * (static_cast<double>(f) / 129.0);
+      const double nhi = f == 128 ? hi : lo + width * (static_cast<double>(f + 1) / 129.0);
+      lo = nlo;
+      hi = nhi;
+    }
+    return 0.5 * (lo + hi);
+  };
+  if (tid == 0) {
+    double x4[4] = {0.0, 0.0, 0.0, 0.0};
+    int c4[4];
+    sturm_count4(d, e2, n, x4, pivmin, c4);
+    n_neg = c4[0];
+  }
+  __syncthreads();
+  const int n_pos = n - n_neg;
+  if (warp < n_pos) {
+    const double v = resolve(n - 1 - warp);
+    if (lane == 0) lam[n - 1 - warp] = v;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const double cut = n_pos > 0 ? lam[n - 1] * 1e-12 : 0.0;
+    int nc = 0;
+    if (n_pos > 0) {
+      double x4[4] = {cut, cut, cut, cut};
+      int c4[4];
+      sturm_count4(d, e2, n, x4, pivmin, c4);
+      nc = n - c4[0];  // eigenvalues above the cut
+      if (nc > n_pos) nc = n_pos;
+    }
+    n_cand = nc;
+  }
+  __syncthreads();
+  for (int c = kEigWarps + warp; c < n_cand; c += kEigWarps) {
+    const double v = resolve(n - 1 - c);
+    if (lane == 0) lam[n - 1 - c] = v;
+  }
+  __syncthreads();
+
+  // ---- clusters of the candidates (descending order c = n-1-j)
+  if (tid == 0) {
+    const int nc = n_cand;
+    int ncl = 0;
+    for (int c = 0; c < nc; ++c) {
+      if (c == 0 || !(fabs(lam[n - 1 - c] - lam[n - c]) <= 1e-3 * tnorm)) cl_start[ncl++] = c;
+    }
+    cl_start[ncl] = nc;
+    n_clusters = ncl;
+    // the non-candidates are never read (finalize stops at the cut): zero
+    for (int c = 0; c < n; ++c) evals_out[c] = c < nc ? lam[n - 1 - c] : 0.0;
+    info[0] = nc;
+  }
+  __syncthreads();
+  for (int e_ = tid; e_ < n * n; e_ += blockDim.x)
+    if (e_ % n >= n_cand) V[e_] = 0.0;
+
+  // ---- inverse iteration, one warp per cluster (members in order); the
+  // T-eigenvectors of a cluster stay in V's columns until the cluster is done
+  if (warp < kEigIIWarps) {
+    TriWork& w = work[warp];
+    const double eps = 2.220446049250313e-16;
+    for (int cl = warp; cl < n_clusters; cl += kEigIIWarps) {
+      const int c0 = cl_start[cl], c1 = cl_start[cl + 1];
+      double prev = 0.0;
+      for (int c = c0; c < c1; ++c) {
+        double lm = lam[n - 1 - c];
+        // separate (numerically) equal members, as dstein
+        if (c > c0 && !(fabs(prev - lm) > 10.0 * eps * fabs(lm))) lm = prev - 10.0 * eps * fmax(fabs(lm), tnorm * eps);
+        prev = lm;
+        if (lane == 0) {
+          // LU with partial pivoting of T - lm I (dgttrf)
+          for (int i = 0; i < n; ++i) {
+            w.dd[i] = d[i] - lm;
+            if (i + 1 < n) {
+              w.du[i] = e[i];
+              w.dl[i] = e[i];
+            }
+            w.du2[i] = 0.0;
+            w.piv[i] = i;
+          }
+          for (int i = 0; i + 1 < n; ++i) {
+            if (fabs(w.dd[i]) >= fabs(w.dl[i])) {
+              const double f = w.dd[i] != 0.0 ? w.dl[i] / w.dd[i] : 0.0;
+              w.dl[i] = f;
+              w.dd[i + 1] -= f * w.du[i];
+            } else {
+              const double f = w.dd[i] / w.dl[i];
+              w.dd[i] = w.dl[i];
+              w.dl[i] = f;
+              const double tmp = w.du[i];
+              w.du[i] = w.dd[i + 1];
+              w.dd[i + 1] = tmp - f * w.dd[i + 1];
+              if (i + 2 < n) {
+                w.du2[i] = w.du[i + 1];
+                w.du[i + 1] = -f * w.du[i + 1];
+              }
+              w.piv[i] = i + 1;
+            }
+          }
+        }
+        __syncwarp();
+        const double tiny = eps * fmax(tnorm, 1e-300);
+        for (int i = lane; i < n; i += 32) {
+          double v = w.dd[i];
+          if (fabs(v) < tiny) v = copysign(tiny, v == 0.0 ? 1.0 : v);
+          w.dd[i] = v;
+          w.rdd[i] = 1.0 / v;
+          w.x[i] = 1.0 + 0.25 * sin(0.7 * (i + 1) + 1.3 * (c + 1));  // deterministic start
+        }
+        __syncwarp();
+        for (int it = 0; it < 3; ++it) {
+          if (lane == 0) {
+            // solve (T - lm I) y = x (dgttrs): L then U
+            for (int i = 0; i + 1 < n; ++i) {
+              if (w.piv[i] == i) {
+                w.x[i + 1] -= w.dl[i] * w.x[i];
+              } else {
+                const double tmp = w.x[i];
+                w.x[i] = w.x[i + 1];
+                w.x[i + 1] = tmp - w.dl[i] * w.x[i];
+              }
+            }
+            double x1 = w.x[n - 1] * w.rdd[n - 1], x2 = 0.0;
+            w.x[n - 1] = x1;
+            if (n >= 2) {
+              x2 = x1;
+              x1 = (w.x[n - 2] - w.du[n - 2] * x2) * w.rdd[n - 2];
+              w.x[n - 2] = x1;
+            }
+            for (int i = n - 3; i >= 0; --i) {
+              const double xi = (w.x[i] - w.du[i] * x1 - w.du2[i] * x2) * w.rdd[i];
+              w.x[i] = xi;
+              x2 = x1;
+              x1 = xi;
+            }
+          }
+          __syncwarp();
+          for (int c2 = c0; c2 < c; ++c2) {  // orthogonalize against earlier members
+            double s = 0.0;
+            for (int i = lane; i < n; i += 32) s += w.x[i] * V[i * n + c2];
+            s = warp_sum(s);
+            for (int i = lane; i < n; i += 32) w.x[i] -= s * V[i * n + c2];
+            __syncwarp();
+          }
+          double s2 = 0.0;
+          for (int i = lane; i < n; i += 32) s2 += w.x[i] * w.x[i];
+          const double inv = 1.0 / sqrt(warp_sum(s2));
+          for (int i = lane; i < n; i += 32) w.x[i] *= inv;
+          __syncwarp();
+        }
+        for (int i = lane; i < n; i += 32) V[i * n + c] = w.x[i];
+        __syncwarp();
+      }
+      // back-transform the cluster's vectors: z <- H_0 ... H_{n-3} z
+      for (int c = c0; c < c1; ++c) {
+        for (int i = lane; i < n; i += 32) w.x[i] = V[i * n + c];
+        __syncwarp();
+        for (int k = n - 3; k >= 0; --k) {
+          const double t = tau[k];
+          if (t == 0.0) continue;
+          const int m = n - k - 1;
+          const double* hv = Hv + k * kEigMaxN + k + 1;  // v_i = hv[i], v_0 = 1
+          double s = 0.0;
+          for (int i = lane; i < m; i += 32) s += hv[i] * w.x[k + 1 + i];
+          s = t * warp_sum(s);
+          for (int i = lane; i < m; i += 32) w.x[k + 1 + i] -= s * hv[i];
+          __syncwarp();
+        }
+        for (int i = lane; i < n; i += 32) V[i * n + c] = w.x[i];
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+}
+
+std::size_t tri_eig_smem(int n) {
+  return sizeof(double) * (static_cast<std::size_t>(n) * kEigMaxN + (8 + kEigGroups) * kEigMaxN) +
+         sizeof(TriWork) * kEigIIWarps;
+}
+
 // ---------------------------------------------------------- finalize ----
 // Lt: [q][M] lifted vectors (descending).  Keeps up to L_max vectors with
 // tilde > cut after Riemann MGS (eigensolve.hpp:161-176).
@@ -645,22 +1240,50 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
 
   // Y = Sigma Omega  ([M][q]); Sigma is exactly symmetric, so Sigma(k, m) is
   // the K-major operand.
-  DevBuf<double> Y(static_cast<std::size_t>(M * q)), Yt(static_cast<std::size_t>(M * q));
+  DevBuf<double> Y(static_cast<std::size_t>(M * q));
   apply_sigma(omega.get(), Y.get());
-  transpose(ctx, Y.get(), M, q, Yt.get());
 
-  // Householder QR and thin Q
-  DevBuf<double> tau(static_cast<std::size_t>(q));
-  for (i64 j = -1; j < q - 1; ++j) {
-    const i64 cols = q - (j + 1);
-    DFPCA_LAUNCH(ctx, k_house_step, static_cast<unsigned>(cols), 512, 0, Yt.get(), M, q, j, tau.get());
+  // Thin Q with range(Q) = range(Y) (eigensolve.hpp:260-263; any orthonormal
+  // basis of range(Y) gives the same Ritz pairs): Cholesky QR twice -- two
+  // DMMA Gram products and two fused factor+solve passes -- accepted when
+  // the first pass left Q1 within 0.1 of orthonormal (then the second pass
+  // restores orthogonality to rounding); otherwise (nearly rank-deficient
+  // sketches) Householder QR, one reflector per launch.
+  DevBuf<double> Q(static_cast<std::size_t>(M * q)), Qt(static_cast<std::size_t>(M * q));
+  bool cholqr_ok = false;
+  if (q <= kCqMaxQ) {
+    DevBuf<double> G(static_cast<std::size_t>(q * q)), R(static_cast<std::size_t>(q * q)),
+        Q1(static_cast<std::size_t>(M * q)), flags(4);
+    const int qi = static_cast<int>(q);
+    const std::size_t fsm = sizeof(double) * q * (q + 1), tsm = trsm_smem(qi);
+    allow_smem(k_chol_factor, fsm);
+    allow_smem(k_row_trsm, tsm);
+    const unsigned ctas = static_cast<unsigned>(std::min<i64>((M + kTrsmWarps - 1) / kTrsmWarps, 2 * ctx->sm_count));
+    gemm_tn(ctx, q, q, M, Y.get(), q, nullptr, Y.get(), q, G.get(), q, false);
+    DFPCA_LAUNCH(ctx, k_chol_factor, 1, 256, fsm, G.get(), qi, R.get(), flags.get());
+    DFPCA_LAUNCH(ctx, k_row_trsm, ctas, kTrsmWarps * 32, tsm, Y.get(), M, qi, R.get(), flags.get(), Q1.get());
+    gemm_tn(ctx, q, q, M, Q1.get(), q, nullptr, Q1.get(), q, G.get(), q, false);
+    DFPCA_LAUNCH(ctx, k_chol_factor, 1, 256, fsm, G.get(), qi, R.get(), flags.get() + 2);
+    DFPCA_LAUNCH(ctx, k_row_trsm, ctas, kTrsmWarps * 32, tsm, Q1.get(), M, qi, R.get(), flags.get() + 2, Q.get());
+    double hf[4];
+    DFPCA_CUDA(cudaMemcpyAsync(hf, flags.get(), sizeof(hf), cudaMemcpyDeviceToHost, st));
+    DFPCA_CUDA(cudaStreamSynchronize(st));
+    cholqr_ok = hf[0] == 0.0 && hf[2] == 0.0 && hf[3] < 0.1;
+    if (cholqr_ok) transpose(ctx, Q.get(), M, q, Qt.get());
   }
-  DevBuf<double> Qt(static_cast<std::size_t>(M * q)), Q(static_cast<std::size_t>(M * q));
-  DFPCA_LAUNCH(ctx, k_q_init, grid_for(M * q, 256), 256, 0, Qt.get(), M, q);
-  for (i64 j = q - 1; j >= 0; --j)
-    DFPCA_LAUNCH(ctx, k_q_apply, static_cast<unsigned>(q - j), 512, 0, Yt.get(), tau.get(), M, q, j,
-                 Qt.get());
-  transpose(ctx, Qt.get(), q, M, Q.get());
+  if (!cholqr_ok) {
+    DevBuf<double> Yt(static_cast<std::size_t>(M * q)), tau(static_cast<std::size_t>(q));
+    transpose(ctx, Y.get(), M, q, Yt.get());
+    for (i64 j = -1; j < q - 1; ++j) {
+      const i64 cols = q - (j + 1);
+      DFPCA_LAUNCH(ctx, k_house_step, static_cast<unsigned>(cols), 512, 0, Yt.get(), M, q, j, tau.get());
+    }
+    DFPCA_LAUNCH(ctx, k_q_init, grid_for(M * q, 256), 256, 0, Qt.get(), M, q);
+    for (i64 j = q - 1; j >= 0; --j)
+      DFPCA_LAUNCH(ctx, k_q_apply, static_cast<unsigned>(q - j), 512, 0, Yt.get(), tau.get(), M, q, j,
+                   Qt.get());
+    transpose(ctx, Qt.get(), q, M, Q.get());
+  }
 
   // small = Q^T (Sigma Q)
   DevBuf<double> Z(static_cast<std::size_t>(M * q));
@@ -670,15 +1293,23 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
 
   DevBuf<double> evals(static_cast<std::size_t>(q));
   DevBuf<int> info(static_cast<std::size_t>(q + 1));
-  const int np = static_cast<int>((q + 1) & ~1ll);
-  std::size_t jsmem = sizeof(double) * np * 2;
-  const bool jac_smem = jsmem + sizeof(double) * 2 * q * q <= 200 * 1024;
-  if (jac_smem) {
-    jsmem += sizeof(double) * 2 * q * q;
-    allow_smem(k_jacobi, jsmem);
+  const bool tri = q <= kEigMaxN;
+  if (tri) {
+    const std::size_t tsm = tri_eig_smem(static_cast<int>(q));
+    allow_smem(k_tri_eig, tsm);
+    DFPCA_LAUNCH(ctx, k_tri_eig, 1, kEigThreads, tsm, small.get(), static_cast<int>(q), evals.get(), Vs.get(),
+                 info.get());
+  } else {
+    const int np = static_cast<int>((q + 1) & ~1ll);
+    std::size_t jsmem = sizeof(double) * np * 2;
+    const bool jac_smem = jsmem + sizeof(double) * 2 * q * q <= 200 * 1024;
+    if (jac_smem) {
+      jsmem += sizeof(double) * 2 * q * q;
+      allow_smem(k_jacobi, jsmem);
+    }
+    DFPCA_LAUNCH(ctx, k_jacobi, 1, 1024, jsmem, small.get(), Vs.get(), static_cast<int>(q), evals.get(),
+                 info.get(), jac_smem ? 1 : 0);
   }
-  DFPCA_LAUNCH(ctx, k_jacobi, 1, 1024, jsmem, small.get(), Vs.get(), static_cast<int>(q), evals.get(),
-               info.get(), jac_smem ? 1 : 0);
 
   // lifted = Q V  ([M][q]) -> Lt [q][M]
   DevBuf<double> lifted(static_cast<std::size_t>(M * q)), Lt(static_cast<std::size_t>(M * q));
@@ -690,7 +1321,7 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
   DFPCA_CUDA(cudaMemcpyAsync(tilde.data(), evals.get(), sizeof(double) * q, cudaMemcpyDeviceToHost, st));
   DFPCA_CUDA(cudaMemcpyAsync(&jinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
   DFPCA_CUDA(cudaStreamSynchronize(st));
-  if (jinfo != 0) fail(kNumeric, "EigFailure", "projected eigensolver did not converge");
+  if (!tri && jinfo != 0) fail(kNumeric, "EigFailure", "projected eigensolver did not converge");
 
   finish_eigensystem(ctx, grid, mv.node_of_row, M, Lt.get(), evals.get(), tilde, L_max, true, eigenvalues,
                      eigenfunctions, fve, total_variance, n_components);

@@ -84,8 +84,9 @@ __global__ void __launch_bounds__(kMtN) k_mt19937_64(unsigned long long seed, i6
 
 // Omega(i, j) = sd * normal #(j * M + i) (column-major fill,
 // eigensolve.hpp:257-258); normals come in Box-Muller pairs cos, sin.
-// Stored row-major [M][q] as the GEMM's K-major operand.
-__global__ void k_box_muller(const unsigned long long* __restrict__ words, i64 M, i64 q, double sd,
+// Stored row-major [M][ldq] (ldq even; the padding is never read) as the
+// GEMM's K-major operand.
+__global__ void k_box_muller(const unsigned long long* __restrict__ words, i64 M, i64 q, i64 ldq, double sd,
                              double* __restrict__ omega) {
   const i64 total = M * q;
   const i64 pairs = (total + 1) / 2;
@@ -102,7 +103,7 @@ __global__ void k_box_muller(const unsigned long long* __restrict__ words, i64 M
       const i64 idx = 2 * pidx + h;
       if (idx >= total) break;
       const i64 j = idx / M, ii = idx % M;
-      omega[ii * q + j] = sd * vals[h];
+      omega[ii * ldq + j] = sd * vals[h];
     }
   }
 }
@@ -118,25 +119,29 @@ __global__ void k_gather_sigma(const double* __restrict__ cov, i64 G, const i64*
   }
 }
 
-__global__ void k_transpose(const double* __restrict__ in, i64 rows, i64 cols, double* __restrict__ out) {
+// out[c][r] = in[r][c] for r < rows, c < cols (row strides ld_in, ld_out).
+__global__ void k_transpose(const double* __restrict__ in, i64 rows, i64 cols, i64 ld_in, double* __restrict__ out,
+                            i64 ld_out) {
   __shared__ double tile[32][33];
   const i64 tiles_c = (cols + 31) / 32;
   const i64 br = blockIdx.x / tiles_c, bc = blockIdx.x % tiles_c;
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
   for (int r = ty; r < 32; r += 8) {
     const i64 gr = br * 32 + r, gc = bc * 32 + tx;
-    tile[r][tx] = (gr < rows && gc < cols) ? in[gr * cols + gc] : 0.0;
+    tile[r][tx] = (gr < rows && gc < cols) ? in[gr * ld_in + gc] : 0.0;
   }
   __syncthreads();
   for (int r = ty; r < 32; r += 8) {
     const i64 oc = br * 32 + tx, orow = bc * 32 + r;  // out[orow][oc] = in[oc][orow]
-    if (orow < cols && oc < rows) out[orow * rows + oc] = tile[tx][r];
+    if (orow < cols && oc < rows) out[orow * ld_out + oc] = tile[tx][r];
   }
 }
 
-void transpose(dfpca_context* ctx, const double* in, i64 rows, i64 cols, double* out) {
+void transpose(dfpca_context* ctx, const double* in, i64 rows, i64 cols, double* out, i64 ld_in = -1,
+               i64 ld_out = -1) {
   const i64 blocks = ((rows + 31) / 32) * ((cols + 31) / 32);
-  DFPCA_LAUNCH(ctx, k_transpose, static_cast<unsigned>(blocks), 256, 0, in, rows, cols, out);
+  DFPCA_LAUNCH(ctx, k_transpose, static_cast<unsigned>(blocks), 256, 0, in, rows, cols, ld_in < 0 ? cols : ld_in,
+               out, ld_out < 0 ? rows : ld_out);
 }
 
 __device__ inline double block_sum(double v, double* red) {
@@ -506,7 +511,7 @@ __global__ void __launch_bounds__(256) k_chol_factor(const double* __restrict__ 
 // sits in shared memory, read as conflict-free row segments.
 constexpr int kTrsmWarps = 16;
 
-__global__ void __launch_bounds__(kTrsmWarps * 32) k_row_trsm(const double* __restrict__ X, i64 M, int q,
+__global__ void __launch_bounds__(kTrsmWarps * 32) k_row_trsm(const double* __restrict__ X, i64 M, int q, i64 ldx,
                                                               const double* __restrict__ Rg,
                                                               const double* __restrict__ flags,
                                                               double* __restrict__ Xout) {
@@ -526,7 +531,7 @@ __global__ void __launch_bounds__(kTrsmWarps * 32) k_row_trsm(const double* __re
 #pragma unroll
     for (int t = 0; t < kPer; ++t) {
       const int l = lane + 32 * t;
-      y[t] = l < q ? X[row * q + l] : 0.0;
+      y[t] = l < q ? X[row * ldx + l] : 0.0;
     }
 #pragma unroll
     for (int t = 0; t < kPer; ++t) {
@@ -546,7 +551,7 @@ __global__ void __launch_bounds__(kTrsmWarps * 32) k_row_trsm(const double* __re
 #pragma unroll
     for (int t = 0; t < kPer; ++t) {
       const int l = lane + 32 * t;
-      if (l < q) Xout[row * q + l] = y[t];
+      if (l < q) Xout[row * ldx + l] = y[t];
     }
   }
 }
@@ -1208,25 +1213,29 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
   }
   const i64 M = mv.M;
   const i64 q = std::min<i64>(q_req, M);
-  // out[M][q] = Sigma X for X [M][q]: sums split exactly as the one-device
-  // product (same split-K), so every row is bit-identical
+  // [M][q] operands are stored with an even row stride ldq so the GEMM
+  // operand copies are 16-byte cp.async (the padding column is never read)
+  const i64 ldq = (q + 1) & ~1ll;
+  // out[M][ldq] = Sigma X for X [M][ldq]: sums split exactly as the
+  // one-device product (same split-K), so every row is bit-identical
   auto apply_sigma = [&](const double* X, double* out) {
     if (!tr) {
-      gemm_tn(ctx, M, q, M, mv.sigma, M, nullptr, X, q, out, q, false);
+      gemm_tn(ctx, M, q, M, mv.sigma, M, nullptr, X, ldq, out, ldq, false);
       return;
     }
-    DevBuf<double> loc(static_cast<std::size_t>(std::max<i64>(1, rs.m_max * q)));
-    DFPCA_CUDA(cudaMemsetAsync(loc.get(), 0, sizeof(double) * rs.m_max * q, st));
+    const i64 chunk = std::max<i64>(1, rs.m_max * ldq);
+    DevBuf<double> loc(static_cast<std::size_t>(chunk));
+    DFPCA_CUDA(cudaMemsetAsync(loc.get(), 0, sizeof(double) * chunk, st));
     if (rs.m_loc > 0)
-      gemm_tn(ctx, rs.m_loc, q, M, rs.sigma_t.get(), rs.m_loc, nullptr, X, q, loc.get(), q, false, 0, -1,
+      gemm_tn(ctx, rs.m_loc, q, M, rs.sigma_t.get(), rs.m_loc, nullptr, X, ldq, loc.get(), ldq, false, 0, -1,
               gemm_splits(ctx, M, q, M));
-    DevBuf<double> all(static_cast<std::size_t>(tr->world() * std::max<i64>(1, rs.m_max * q)));
-    tr->all_gather(ctx, loc.get(), all.get(), std::max<i64>(1, rs.m_max * q));
+    DevBuf<double> all(static_cast<std::size_t>(tr->world() * chunk));
+    tr->all_gather(ctx, loc.get(), all.get(), chunk);
     for (int r = 0; r < tr->world(); ++r)
       if (rs.counts[static_cast<std::size_t>(r)] > 0)
-        DFPCA_CUDA(cudaMemcpyAsync(out + rs.offsets[static_cast<std::size_t>(r)] * q,
-                                   all.get() + static_cast<i64>(r) * std::max<i64>(1, rs.m_max * q),
-                                   sizeof(double) * rs.counts[static_cast<std::size_t>(r)] * q,
+        DFPCA_CUDA(cudaMemcpyAsync(out + rs.offsets[static_cast<std::size_t>(r)] * ldq,
+                                   all.get() + static_cast<i64>(r) * chunk,
+                                   sizeof(double) * rs.counts[static_cast<std::size_t>(r)] * ldq,
                                    cudaMemcpyDeviceToDevice, st));
   };
 
@@ -1234,13 +1243,13 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
   DevBuf<unsigned long long> words(static_cast<std::size_t>(2 * ((M * q + 1) / 2)));
   DFPCA_LAUNCH(ctx, k_mt19937_64, 1, kMtN, 0, splitmix64(seed), static_cast<i64>(words.size()),
                words.get());
-  DevBuf<double> omega(static_cast<std::size_t>(M * q));
-  DFPCA_LAUNCH(ctx, k_box_muller, grid_for((M * q + 1) / 2, 256), 256, 0, words.get(), M, q,
+  DevBuf<double> omega(static_cast<std::size_t>(M * ldq));
+  DFPCA_LAUNCH(ctx, k_box_muller, grid_for((M * q + 1) / 2, 256), 256, 0, words.get(), M, q, ldq,
                1.0 / std::sqrt(static_cast<double>(q)), omega.get());
 
   // Y = Sigma Omega  ([M][q]); Sigma is exactly symmetric, so Sigma(k, m) is
   // the K-major operand.
-  DevBuf<double> Y(static_cast<std::size_t>(M * q));
+  DevBuf<double> Y(static_cast<std::size_t>(M * ldq));
   apply_sigma(omega.get(), Y.get());
 
   // Thin Q with range(Q) = range(Y) (eigensolve.hpp:260-263; any orthonormal
@@ -1249,31 +1258,32 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
   // the first pass left Q1 within 0.1 of orthonormal (then the second pass
   // restores orthogonality to rounding); otherwise (nearly rank-deficient
   // sketches) Householder QR, one reflector per launch.
-  DevBuf<double> Q(static_cast<std::size_t>(M * q)), Qt(static_cast<std::size_t>(M * q));
+  DevBuf<double> Q(static_cast<std::size_t>(M * ldq)), Qt(static_cast<std::size_t>(M * q));
   bool cholqr_ok = false;
   if (q <= kCqMaxQ) {
     DevBuf<double> G(static_cast<std::size_t>(q * q)), R(static_cast<std::size_t>(q * q)),
-        Q1(static_cast<std::size_t>(M * q)), flags(4);
+        Q1(static_cast<std::size_t>(M * ldq)), flags(4);
     const int qi = static_cast<int>(q);
     const std::size_t fsm = sizeof(double) * q * (q + 1), tsm = trsm_smem(qi);
     allow_smem(k_chol_factor, fsm);
     allow_smem(k_row_trsm, tsm);
     const unsigned ctas = static_cast<unsigned>(std::min<i64>((M + kTrsmWarps - 1) / kTrsmWarps, 2 * ctx->sm_count));
-    gemm_tn(ctx, q, q, M, Y.get(), q, nullptr, Y.get(), q, G.get(), q, false);
+    gemm_tn(ctx, q, q, M, Y.get(), ldq, nullptr, Y.get(), ldq, G.get(), q, false);
     DFPCA_LAUNCH(ctx, k_chol_factor, 1, 256, fsm, G.get(), qi, R.get(), flags.get());
-    DFPCA_LAUNCH(ctx, k_row_trsm, ctas, kTrsmWarps * 32, tsm, Y.get(), M, qi, R.get(), flags.get(), Q1.get());
-    gemm_tn(ctx, q, q, M, Q1.get(), q, nullptr, Q1.get(), q, G.get(), q, false);
+    DFPCA_LAUNCH(ctx, k_row_trsm, ctas, kTrsmWarps * 32, tsm, Y.get(), M, qi, ldq, R.get(), flags.get(), Q1.get());
+    gemm_tn(ctx, q, q, M, Q1.get(), ldq, nullptr, Q1.get(), ldq, G.get(), q, false);
     DFPCA_LAUNCH(ctx, k_chol_factor, 1, 256, fsm, G.get(), qi, R.get(), flags.get() + 2);
-    DFPCA_LAUNCH(ctx, k_row_trsm, ctas, kTrsmWarps * 32, tsm, Q1.get(), M, qi, R.get(), flags.get() + 2, Q.get());
+    DFPCA_LAUNCH(ctx, k_row_trsm, ctas, kTrsmWarps * 32, tsm, Q1.get(), M, qi, ldq, R.get(), flags.get() + 2,
+                 Q.get());
     double hf[4];
     DFPCA_CUDA(cudaMemcpyAsync(hf, flags.get(), sizeof(hf), cudaMemcpyDeviceToHost, st));
     DFPCA_CUDA(cudaStreamSynchronize(st));
     cholqr_ok = hf[0] == 0.0 && hf[2] == 0.0 && hf[3] < 0.1;
-    if (cholqr_ok) transpose(ctx, Q.get(), M, q, Qt.get());
+    if (cholqr_ok) transpose(ctx, Q.get(), M, q, Qt.get(), ldq, M);
   }
   if (!cholqr_ok) {
     DevBuf<double> Yt(static_cast<std::size_t>(M * q)), tau(static_cast<std::size_t>(q));
-    transpose(ctx, Y.get(), M, q, Yt.get());
+    transpose(ctx, Y.get(), M, q, Yt.get(), ldq, M);
     for (i64 j = -1; j < q - 1; ++j) {
       const i64 cols = q - (j + 1);
       DFPCA_LAUNCH(ctx, k_house_step, static_cast<unsigned>(cols), 512, 0, Yt.get(), M, q, j, tau.get());
@@ -1282,14 +1292,14 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
     for (i64 j = q - 1; j >= 0; --j)
       DFPCA_LAUNCH(ctx, k_q_apply, static_cast<unsigned>(q - j), 512, 0, Yt.get(), tau.get(), M, q, j,
                    Qt.get());
-    transpose(ctx, Qt.get(), q, M, Q.get());
+    transpose(ctx, Qt.get(), q, M, Q.get(), M, ldq);
   }
 
   // small = Q^T (Sigma Q)
-  DevBuf<double> Z(static_cast<std::size_t>(M * q));
+  DevBuf<double> Z(static_cast<std::size_t>(M * ldq));
   apply_sigma(Q.get(), Z.get());
   DevBuf<double> small(static_cast<std::size_t>(q * q)), Vs(static_cast<std::size_t>(q * q));
-  gemm_tn(ctx, q, q, M, Q.get(), q, nullptr, Z.get(), q, small.get(), q, false);
+  gemm_tn(ctx, q, q, M, Q.get(), ldq, nullptr, Z.get(), ldq, small.get(), q, false);
 
   DevBuf<double> evals(static_cast<std::size_t>(q));
   DevBuf<int> info(static_cast<std::size_t>(q + 1));

@@ -249,11 +249,14 @@ void launch(dfpca_context* ctx, dim3 grid, std::size_t smem, i64 M, i64 N, i64 K
 
 }  // namespace
 
+// Skinny products: as many K splits as keep the launch inside one wave of
+// CTAS_PER_SM CTAs per SM (a second, partial wave would double the time).
 i64 gemm_splits(const dfpca_context* ctx, i64 M, i64 N, i64 K) {
   const i64 blocks = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const i64 slots = static_cast<i64>(CTAS_PER_SM) * ctx->sm_count;
   i64 splits = 1;
-  if (blocks < 2 * ctx->sm_count && K >= 1024) {
-    splits = std::min<i64>((2 * ctx->sm_count + blocks - 1) / blocks, K / 256);
+  if (blocks < slots / 2 && K >= 1024) {
+    splits = std::min<i64>(slots / blocks, K / 256);
     splits = std::max<i64>(splits, 1);
   }
   return splits;

@@ -14,13 +14,17 @@ device-resident covariance.  value = G^2 / step time (gridpts/s).  N > 1 splits
 the one covariance into s1-plane slabs, one per GPU (csrc/shard.hpp: SYRK over
 each rank's row tiles, NCCL exchanges of the pair-grid windows and of the
 covariance rows), step time = max over ranks ("scaling": "strong").
-e2e: the same metric through the public API with host buffers: pinned host
-observations -> linear_bin -> fft_local_linear -> fft_covariance -> covariance
-copied back to pinned host memory, every step.
+e2e: the same metric through the public API with host buffers, over the FPCA
+core of SURVEY.md 8(d): pinned host observations -> linear_bin ->
+fft_local_linear (Mean, Squares) -> fft_covariance -> randomized_eig (q=99,
+L=20) -> EigenSystem (eigenvalues and eigenfunction surfaces) on the host,
+every step.  The inputs are drawn by the reference's own generator.
 
 --impl reference times the reference implementation itself (oracle/_ref: the
-reference's headers compiled unchanged) on the host cores, on a bounded sample
-of the same workload (see cpu_sample()).
+reference's headers compiled unchanged) on the host cores on the SAME
+workload: one full FPCA run (~100 s; --ref-steps runs, --steps ignored), value
+from its fft_covariance stage, e2e from the whole run.  Our line's
+cpu_baseline is a bounded sample (first --cpu-subjects subjects).
 """
 from __future__ import annotations
 
@@ -40,7 +44,8 @@ sys.path.insert(0, str(ROOT))
 
 CELLS, N_SUBJ, H = 64, 2000, 0.1
 METRIC = "smoothed covariance gridpts/s (d=2 64², 4-D LL); end-to-end FPCA time vs CPU"
-WORKLOAD = "configs[2]: d=2 n=2000 on 64x64 midpoint grid, GridNodes design, h=0.1 (R=7), fft_covariance"
+WORKLOAD = ("configs[2]: d=2 n=2000 on 64x64 midpoint grid, GridNodes design, h=0.1 (R=7), fft_covariance; "
+            "inputs drawn by the reference's generator (simulate.hpp, seed 20260815)")
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 # FP64 peak of this pool's B200 (DMMA m8n8k4 and DFMA both), measured with
 # tools/fp64_peak.cu (profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json has no FP64 entry.
@@ -54,21 +59,52 @@ def rank_env():
 
 # ------------------------------------------------------------------ clocks --
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region: NVML
+    (every 2 ms, microsecond queries) when the driver's library is present,
+    else nvidia-smi (every 0.1 s)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device: int):
         self.device = device
         self.rows = []
         self.query_s = []
+        self.source = "nvidia-smi"
         self._stop = threading.Event()
         self._t = None
+        self._nv = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self._h = nv.nvmlDeviceGetHandleByIndex(device)
+            self._max = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            self._bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                          nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            self._nv = nv
+            self.source = "nvml"
+        except Exception:
+            self._nv = None
+
+    def _sample_nvml(self):
+        nv = self._nv
+        q0 = time.perf_counter()
+        sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+        try:
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        except Exception:
+            rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        self.query_s.append(time.perf_counter() - q0)
+        self.rows.append([str(sm), str(self._max)] + ["Active" if rs & b else "Not Active" for b in self._bits])
 
     def _run(self):
         while not self._stop.is_set():
             try:
+                if self._nv is not None:
+                    self._sample_nvml()
+                    self._stop.wait(0.002)
+                    continue
                 q0 = time.perf_counter()
                 out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
@@ -91,20 +127,22 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "source": self.source}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].strip() == "Active"})
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4) if r[2 + i].strip() == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows),
+                "sm_min_mhz": min(sm) if sm else None, "reasons": reasons, "samples": len(self.rows),
+                "source": self.source,
                 "query_ms": float(1e3 * np.median(self.query_s)) if self.query_s else None}
 
 
 # ------------------------------------------------------------------- data --
 def make_data(seed=20260815):
+    """configs[2] drawn by the reference's own generator (simulate.hpp's
+    generate() restated bit for bit in the library: dfpca_simulate)."""
     from paper_1510_04439_b200 import synth
-    return synth.grid_nodes(2, CELLS, N_SUBJ, H, seed=seed)
+    return synth.config(3, n=N_SUBJ, h=H, cells=CELLS, seed=seed)
 
 
 def cpu_sample(sd, n_sub: int):
@@ -117,44 +155,98 @@ def cpu_sample(sd, n_sub: int):
 
 
 # -------------------------------------------------------------- reference --
-def run_reference(args, emit=True):
+def reference_fpca(sd, threads: int):
+    """One run of the reference's FPCA core on the host (oracle/_ref: the
+    reference's headers compiled unchanged): the stages of fit_pipeline
+    (pipeline.hpp:308-340) timed like its StageClock (pipeline.hpp:143-165):
+    linear_bin, fft_local_linear(Mean), fft_local_linear(Squares),
+    fft_covariance, matrixize + randomized_eig(q=99, L=20).  Seconds per stage."""
     from oracle import ref as R
+    R.set_threads(threads)
+    grid = (sd.axes, sd.mask)
+    t = {}
+    t0 = time.perf_counter()
+    b = R.linear_bin(grid, sd.offsets, sd.coords, sd.values, True, True)
+    t["linear_bin"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    mu = R.fft_local_linear(b, grid, sd.h, 0)
+    t["mean"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    R.fft_local_linear(b, grid, sd.h, 1)
+    t["squares"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    cov = R.fft_covariance(b, grid, sd.h, mu)
+    t["covariance"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    eig = R.randomized_eig(grid, cov, 99, 20, 20260815)
+    t["randomized_eig"] = time.perf_counter() - t0
+    return t, eig
+
+
+def run_reference(args, emit=True):
+    """--impl reference: the reference's own CPU implementation of the path on
+    the SAME workload as our arm (n = 2000, 64^2, h = 0.1), all host threads.
+    One FPCA run is ~100 s of host time (its pair build is serial), so the
+    arm runs --ref-steps of them (default 1) whatever --steps says: a
+    same-config number rather than a same-step-count one.  value = G^2 / the
+    fft_covariance time; e2e = G^2 / the whole FPCA (host observations ->
+    EigenSystem), the same stages as our e2e."""
     rank, world, _ = rank_env()
     if rank != 0:
         return None
+    cores = os.cpu_count() or 1
+    sd = make_data()
+    G2 = (CELLS * CELLS) ** 2
+    n_steps = max(1, args.ref_steps if args.ref_steps else 1)
+    for _ in range(args.ref_warmup if args.ref_warmup is not None else 0):
+        reference_fpca(sd, cores)
+    runs = [reference_fpca(sd, cores) for _ in range(n_steps)]
+    t_cov = float(np.mean([r[0]["covariance"] for r in runs]))
+    t_all = float(np.mean([sum(r[0].values()) for r in runs]))
+    stages = {k: float(np.mean([r[0][k] for r in runs])) * 1e3 for k in runs[0][0]}
+    val = G2 / t_cov
+    sample = (f"the full workload: fft_covariance of all {N_SUBJ} subjects on the 64x64 grid "
+              f"(16,777,216 gridpts), reference headers compiled unchanged (oracle/_ref), "
+              f"set_max_threads({cores}); {n_steps} run(s), --steps ignored (one run is ~100 s)")
+    line = {"metric": METRIC, "value": val, "unit": "gridpts/s", "n_gpus": args.gpus, "steps": n_steps,
+            "warmup": 0, "ms_per_step": t_cov * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "cpu_sample": f"full config, n={N_SUBJ}", "same_config": True},
+            "impl": "reference",
+            "stages_ms": stages,
+            "eig_top3": [float(x) for x in runs[-1][1]["eigenvalues"][:3]],
+            "cpu_baseline": {"value": val, "unit": "gridpts/s", "cores": cores, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": G2 / t_all, "unit": "gridpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                    "ms_per_step": t_all * 1e3,
+                    "path": "host observations -> linear_bin -> mean -> squares -> fft_covariance -> "
+                            "randomized_eig (q=99, L=20) -> EigenSystem"}}
+    if emit:
+        print(json.dumps(line), flush=True)
+    return line
+
+
+def reference_sample_baseline(args):
+    """cpu_baseline of our line: the reference's fft_covariance on a bounded
+    sample of the workload (the first --cpu-subjects subjects on the full
+    64^2 grid: the pair build is O(n), convolutions and solves are O(G^2) and
+    unchanged), so the default bench run stays within minutes."""
+    from oracle import ref as R
     cores = os.cpu_count() or 1
     R.set_threads(cores)
     sd = make_data()
     n_sub = args.cpu_subjects
     off, coords, values = cpu_sample(sd, n_sub)
     grid = (sd.axes, None)
-    G2 = (CELLS * CELLS) ** 2
-
-    def step():
-        b = R.linear_bin(grid, off, coords, values, True, True)
-        mu = R.fft_local_linear(b, grid, sd.h, 0)
-        t0 = time.perf_counter()
-        R.fft_covariance(b, grid, sd.h, mu)
-        return time.perf_counter() - t0
-
-    for _ in range(args.ref_warmup if args.ref_warmup is not None else min(args.warmup, 1)):
-        step()
-    times = [step() for _ in range(max(1, args.ref_steps if args.ref_steps else args.steps))]
-    t = float(np.mean(times))
-    val = G2 / t
-    sample = (f"fft_covariance on the full 64x64 grid (16,777,216 gridpts), first {n_sub} of {N_SUBJ} subjects, "
-              f"reference headers compiled unchanged (oracle/_ref), set_max_threads({cores})")
-    line = {"metric": METRIC, "value": val, "unit": "gridpts/s", "n_gpus": args.gpus, "steps": len(times),
-            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "cpu_sample": f"n={n_sub}"},
-            "impl": "reference",
-            "cpu_baseline": {"value": val, "unit": "gridpts/s", "cores": cores, "kind": "reference",
-                             "sample": sample},
-            "e2e": {"value": val, "unit": "gridpts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    if emit:
-        print(json.dumps(line), flush=True)
-    return line
+    b = R.linear_bin(grid, off, coords, values, True, True)
+    mu = R.fft_local_linear(b, grid, sd.h, 0)
+    t0 = time.perf_counter()
+    R.fft_covariance(b, grid, sd.h, mu)
+    t = time.perf_counter() - t0
+    return {"value": (CELLS * CELLS) ** 2 / t, "unit": "gridpts/s", "cores": cores, "kind": "reference",
+            "sample": (f"fft_covariance on the full 64x64 grid (16,777,216 gridpts), first {n_sub} of {N_SUBJ} "
+                       f"subjects, reference headers compiled unchanged (oracle/_ref), set_max_threads({cores}); "
+                       f"the same-config reference is bench.py --impl reference")}
 
 
 # ------------------------------------------------------ long-format tables --
@@ -441,14 +533,59 @@ def main():
     _lib.profile(False)
 
     # ---- e2e through the public API with pinned host buffers ----
+    # host observations -> EigenSystem on the host, the stages
+    # of fit_pipeline (pipeline.hpp:308-340): linear_bin, fft_local_linear
+    # (Mean, Squares), fft_covariance, matrixize + randomized_eig (q=99,
+    # L=20); the eigenvalues and eigenfunction surfaces come back every step.
     offsets, coords, values = data.csr()
     probe = cov_fn(binned, grid, h, mean)
     slab_row0, slab_rows = probe.rows()
     del probe
     host_cov = np.empty(slab_rows * G)
     pinned = [_lib.pin(a) for a in (offsets, coords, values, host_cov)]
+    Q_SKETCH, L_MAX = 99, 20
+
+    def fpca(stage_times=None):
+        def mark(name, t_prev):
+            if stage_times is not None:
+                torch.cuda.synchronize(dev)
+                now = time.perf_counter()
+                stage_times[name] = stage_times.get(name, 0.0) + (now - t_prev)
+                return now
+            return t_prev
+        t = time.perf_counter()
+        b2 = api.linear_bin(data, grid, api.BinOptions(True, True))
+        t = mark("linear_bin", t)
+        m2 = api.fft_local_linear(b2, grid, h, api.MomentTarget.Mean)
+        t = mark("mean", t)
+        api.fft_local_linear(b2, grid, h, api.MomentTarget.Squares)
+        t = mark("squares", t)
+        c2 = cov_fn(b2, grid, h, m2)
+        t = mark("covariance", t)
+        es = api.randomized_eig(api.matrixize(c2), Q_SKETCH, L_MAX, grid, 20260815)
+        mark("randomized_eig", t)
+        return es
+
     e2e_t = []
     for it in range(args.e2e_steps + 1):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        es = fpca()
+        t1 = time.perf_counter()
+        if it > 0:
+            e2e_t.append(t1 - t0)
+    e2e_step = float(np.mean(e2e_t))
+    eig_top3 = [float(x) for x in es.eigenvalues[:3]]
+    n_comp = len(es.eigenvalues)
+    d2h = 8 * n_comp * (G + 2) + 8  # eigenvalues, FVE, eigenfunction surfaces, total variance
+    # one more pass, synchronised per stage, for the breakdown (not timed above)
+    brk = {}
+    fpca(brk)
+    eig_ms = _lib.stage_ms("eigen")
+    # the previous e2e scope, kept for comparison: observations -> covariance
+    # copied back to pinned host memory
+    cov_t = []
+    for it in range(3):
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         b2 = api.linear_bin(data, grid, api.BinOptions(True, True))
@@ -456,49 +593,14 @@ def main():
         c2 = cov_fn(b2, grid, h, m2)
         _lib.check(_lib.lib().dfpca_surface_download(_lib.ctx(), c2.device_handle(),
                                                      host_cov.ctypes.data_as(_lib.PD)))
-        t1 = time.perf_counter()
         if it > 0:
-            e2e_t.append(t1 - t0)
+            cov_t.append(time.perf_counter() - t0)
         del b2, m2, c2
-    e2e_step = float(np.mean(e2e_t))
-    # one more pass, synchronised per call, for the breakdown (not timed above)
-    brk = {}
-    torch.cuda.synchronize(dev)
-    t0 = time.perf_counter()
-    b2 = api.linear_bin(data, grid, api.BinOptions(True, True))
-    torch.cuda.synchronize(dev)
-    brk["linear_bin"] = time.perf_counter() - t0
-    m2 = api.fft_local_linear(b2, grid, h, api.MomentTarget.Mean)
-    torch.cuda.synchronize(dev)
-    brk["mean"] = time.perf_counter() - t0 - sum(brk.values())
-    c2 = cov_fn(b2, grid, h, m2)
-    torch.cuda.synchronize(dev)
-    brk["covariance"] = time.perf_counter() - t0 - sum(brk.values())
-    _lib.check(_lib.lib().dfpca_surface_download(_lib.ctx(), c2.device_handle(), host_cov.ctypes.data_as(_lib.PD)))
-    brk["download"] = time.perf_counter() - t0 - sum(brk.values())
-    del b2, m2, c2
     if dist is not None:
         tt = torch.tensor([e2e_step], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_step = float(tt.item())
     h2d = offsets.nbytes + coords.nbytes + values.nbytes
-    d2h = host_cov.nbytes
-
-    # ---- full FPCA pipeline once (host obs -> EigenSystem on host) ----
-    fpca_ms = eig_ms = None
-    eig_top3 = None
-    # (N > 1: every rank smooths its slab and runs the row-sharded projection)
-    if True:
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        b3 = api.linear_bin(data, grid, api.BinOptions(True, True))
-        m3 = api.fft_local_linear(b3, grid, h, api.MomentTarget.Mean)
-        api.fft_local_linear(b3, grid, h, api.MomentTarget.Squares)
-        c3 = cov_fn(b3, grid, h, m3)
-        eig = api.randomized_eig(api.matrixize(c3), 99, 20, grid, 20260815)
-        fpca_ms = (time.perf_counter() - t0) * 1e3
-        eig_ms = _lib.stage_ms("eigen")
-        eig_top3 = eig.eigenvalues[:3]
 
     if rank != 0:
         if dist is not None:
@@ -513,10 +615,7 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            ref_args = argparse.Namespace(**vars(args))
-            ref_args.ref_steps, ref_args.ref_warmup = 1, 0
-            line = run_reference(ref_args, emit=False)
-            cpu = line["cpu_baseline"] if line else None
+            cpu = reference_sample_baseline(args)
         except Exception as e:  # oracle missing on this box
             cpu = {"value": None, "unit": "gridpts/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -536,9 +635,11 @@ def main():
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_step * 1e3,
                 "breakdown_ms": {k: v * 1e3 for k, v in brk.items()},
                 "all_ms": [round(t * 1e3, 3) for t in e2e_t],
-                "path": "pinned host obs -> linear_bin -> fft_local_linear -> fft_covariance -> host covariance",
-                "pinned": all(pinned)},
-        "fpca_e2e_ms": fpca_ms, "eigen_ms": eig_ms, "eig_top3": eig_top3,
+                "path": ("pinned host obs -> linear_bin -> fft_local_linear (Mean, Squares) -> fft_covariance -> "
+                         f"randomized_eig (q={Q_SKETCH}, L={L_MAX}) -> EigenSystem on the host"),
+                "pinned": all(pinned),
+                "to_covariance_ms": float(np.mean(cov_t)) * 1e3},
+        "eigen_ms": eig_ms, "eig_top3": eig_top3, "eig_components": n_comp,
         "gpu_launches": int(launches),
         "kernels": {k: {"ms": v[0], "launches": v[1]} for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][0])},
         "roofline": roof,

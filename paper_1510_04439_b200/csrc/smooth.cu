@@ -211,6 +211,8 @@ struct SharedMoments {
   const double* A[kMaxDim];  // [3][n_k]
   const double* D[kMaxDim];  // [3][3][n_k][n_k]
   int n[kMaxDim];
+  int band[kMaxDim];         // D_k(x, y) == 0 exactly when |x - y| > band[k] (= R_s + R_t)
+  float inv_n[kMaxDim];      // 1 / n_k for fast_divmod
   double sw, dm0;
 };
 
@@ -420,6 +422,219 @@ __global__ void __launch_bounds__(kSolveTile, N == 5 ? 8 : DFPCA_SOLVE_MIN_CTAS)
   solve_tri_body<N, true>(sh, mp, g, nch, out, empty_count, empty_list, list_cap);
 }
 
+// Shared-design covariance solve, tiled like k_solve_tri (CTA = one s row x
+// 128 consecutive t).  The closed-form mass moments are separable:
+//   S_o(s, t) = sw P_{o_s}(s) P_{o_t}(t) - dm0 prod_k D_k[o_sk][o_tk](s_k, t_k),
+// where o = (o_s, o_t) is the moment's multi-index split into its s and t
+// axes, P_{o_s}(s) = prod_k A_k[o_sk](s_k) and D_k vanishes exactly unless
+// |s_k - t_k| <= R_k(s) + R_k(t).  So each thread forms the (d+1)(d+2)/2
+// products of its t node once, the s products are CTA-uniform, a moment is
+// one multiply, and the band tables are read only inside the band.  The
+// normal matrix then goes through Eigen's pivoted LDLT; when the ridged
+// diagonal is already in pivot order (the common case: the constant moment
+// dominates and interior second moments tie, first index wins), the
+// factorisation runs unpermuted in registers -- exactly the operations
+// solve_local_perm performs with the identity permutation -- and only the
+// other nodes take the shared-memory gather.
+template <int D>
+struct SepIdx {  // index of multi-index e_k (deg 1) / e_k + e_l (deg 2) among the (D+1)(D+2)/2
+  static constexpr int n = (D + 1) * (D + 2) / 2;
+  __host__ __device__ static constexpr int one(int k) { return 1 + k; }
+  __host__ __device__ static constexpr int two(int k, int l) {  // k <= l
+    return 1 + D + k * D - k * (k - 1) / 2 + (l - k);
+  }
+};
+
+template <int N>
+__device__ __forceinline__ void sep_products(const double (&a)[(N - 1) / 2][3], double (&P)[SepIdx<(N - 1) / 2>::n],
+                                             double scale) {
+  constexpr int d = (N - 1) / 2;
+  using I = SepIdx<d>;
+  double z = scale;
+#pragma unroll
+  for (int k = 0; k < d; ++k) z *= a[k][0];
+  P[0] = z;
+#pragma unroll
+  for (int k = 0; k < d; ++k) {
+    double v = scale;
+#pragma unroll
+    for (int m = 0; m < d; ++m) v *= a[m][m == k ? 1 : 0];
+    P[I::one(k)] = v;
+  }
+#pragma unroll
+  for (int k = 0; k < d; ++k)
+#pragma unroll
+    for (int l = k; l < d; ++l) {
+      double v = scale;
+#pragma unroll
+      for (int m = 0; m < d; ++m) v *= a[m][(m == k) + (m == l)];
+      P[I::two(k, l)] = v;
+    }
+}
+
+// x = q n + r for 0 <= x < 2^24 without an integer division (float
+// reciprocal estimate, one correction step).
+__device__ __forceinline__ void fast_divmod(int x, int n, float inv_n, int& q, int& r) {
+  q = __float2int_rz(__int2float_rn(x) * inv_n);
+  r = x - q * n;
+  if (r < 0) {
+    --q;
+    r += n;
+  } else if (r >= n) {
+    ++q;
+    r -= n;
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(kSolveTile, N == 5 ? 8 : DFPCA_SOLVE_MIN_CTAS)
+    k_solve_sep_tri(SharedMoments sh, MomPtrs mp, SolveGeom g, double* __restrict__ out,
+                    unsigned long long* __restrict__ empty_count, i64* __restrict__ empty_list, i64 list_cap) {
+  constexpr int p = N - 1;
+  constexpr int d = p / 2;
+  constexpr int nm = 1 + p + p * (p + 1) / 2;
+  constexpr int nl = 1 + p;
+  using I = SepIdx<d>;
+  const int lrow = static_cast<int>(blockIdx.y);  // grid: (column chunks, rows)
+  const int ch = static_cast<int>(blockIdx.x);
+  const int tc = static_cast<int>(g.tc);
+  const int t0 = static_cast<int>(g.t0);
+  const int mrow = lrow + static_cast<int>(g.row_lo);
+  const int row = mrow + static_cast<int>(g.row0);
+  if (t0 + (ch + 1) * kSolveTile <= row) return;
+  const int c = ch * kSolveTile + static_cast<int>(threadIdx.x);
+  const int col = t0 + c;
+  if (c >= tc || col < row) return;
+  const i64 e = static_cast<i64>(mrow) * tc + c;
+  const i64 dst = static_cast<i64>(row - g.out_row0) * g.gt + col;
+  if (g.mask && !(g.mask[row] != 0 && g.mask[col] != 0)) {
+    out[dst] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  double T[nl];
+#pragma unroll
+  for (int i = 0; i < nl; ++i) T[i] = mp.T[i][e];  // issue the moment loads first
+  int sk[d], tk[d];
+  {
+    int rs = row, rt = col;
+#pragma unroll
+    for (int k = d - 1; k >= 0; --k) {
+      const int n = sh.n[k];
+      const float inv = sh.inv_n[k];
+      int qs, qt;
+      fast_divmod(rs, n, inv, qs, sk[k]);
+      fast_divmod(rt, n, inv, qt, tk[k]);
+      rs = qs;
+      rt = qt;
+    }
+  }
+  double as[d][3], at[d][3];
+  bool near = true;
+#pragma unroll
+  for (int k = 0; k < d; ++k) {
+    const int n = sh.n[k];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      as[k][r] = __ldg(sh.A[k] + r * n + sk[k]);
+      at[k][r] = __ldg(sh.A[k] + r * n + tk[k]);
+    }
+    const int dist = sk[k] > tk[k] ? sk[k] - tk[k] : tk[k] - sk[k];
+    near = near && dist <= sh.band[k];
+  }
+  // raw products, the weight applied last: S = sw (P_s P_t), so moments
+  // that are mirror images of each other (s <-> t, or axis k <-> l at
+  // interior nodes) round identically and tie exactly in the pivot order
+  double Ps[I::n], Pt[I::n];
+  sep_products<N>(as, Ps, 1.0);
+  sep_products<N>(at, Pt, 1.0);
+  const double sw = sh.sw;
+  // S in MomentBasis order (local_fit.hpp:34-47): covariates 0..d-1 are the
+  // s axes, d..2d-1 the t axes
+  double S[nm];
+  S[0] = sw * (Ps[0] * Pt[0]);
+#pragma unroll
+  for (int k = 0; k < p; ++k) S[1 + k] = sw * (k < d ? Ps[I::one(k)] * Pt[0] : Ps[0] * Pt[I::one(k - d)]);
+#pragma unroll
+  for (int k = 0; k < p; ++k)
+#pragma unroll
+    for (int l = k; l < p; ++l) {
+      double v;
+      if (l < d) v = Ps[I::two(k, l)] * Pt[0];
+      else if (k >= d) v = Ps[0] * Pt[I::two(k - d, l - d)];
+      else v = Ps[I::one(k)] * Pt[I::one(l - d)];
+      S[quad_index(p, k, l)] = sw * v;
+    }
+  if (near) {
+    // the same-observation band (exact zero outside it)
+    double Dst[d][3][3];
+#pragma unroll
+    for (int k = 0; k < d; ++k) {
+      const int n = sh.n[k];
+      const double* Dk = sh.D[k] + sk[k] * n + tk[k];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) Dst[k][a][b] = a + b <= 2 ? __ldg(Dk + (a * 3 + b) * n * n) : 0.0;
+    }
+    auto band = [&](const int (&o)[p]) {
+      double pd = sh.dm0;
+#pragma unroll
+      for (int k = 0; k < d; ++k) pd *= Dst[k][o[k]][o[d + k]];
+      return pd;
+    };
+    {
+      int o[p] = {};
+      S[0] -= band(o);
+    }
+#pragma unroll
+    for (int k = 0; k < p; ++k) {
+      int o[p] = {};
+      o[k] = 1;
+      S[1 + k] -= band(o);
+    }
+#pragma unroll
+    for (int k = 0; k < p; ++k)
+#pragma unroll
+      for (int l = k; l < p; ++l) {
+        int o[p] = {};
+        o[k] += 1;
+        o[l] += 1;
+        S[quad_index(p, k, l)] -= band(o);
+      }
+  }
+  double b0;
+  int st;
+  // pivot order check on the ridged diagonal (Eigen: first largest |.|)
+  double dg[N];
+  dg[0] = S[0];
+#pragma unroll
+  for (int k = 0; k < p; ++k) dg[k + 1] = S[quad_index(p, k, k)];
+  double tr = 0.0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) tr += dg[i];
+  const double eps = 1e-10 * tr;
+  bool ordered = S[0] > 0.0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    dg[i] += eps;
+#pragma unroll
+    for (int j = 0; j < i; ++j) ordered = ordered && !(fabs(dg[i]) > fabs(dg[j]));
+  }
+  if (ordered) {
+    st = ldlt_identity<N>(S, T, dg, b0);
+  } else {
+    __shared__ double sm_solve[(nm + nl) * kSolveTile];
+    st = solve_local_perm<N>(S, T, sm_solve + threadIdx.x, kSolveTile, b0);
+  }
+  if (st == kFitEmpty) {
+    const unsigned long long slot = atomicAdd(empty_count, 1ull);
+    if (static_cast<i64>(slot) < list_cap) empty_list[slot] = dst;
+    out[dst] = __longlong_as_double(0x7ff8000000000000ll);
+  } else {
+    out[dst] = b0;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Empty-window fallback ladder (fft_smoother.hpp:471-487): for each listed
 // node, up to kWindowRetries direct gathers at 1.5^r h over the binned arrays
@@ -607,9 +822,14 @@ void launch_solve_shared_n(dfpca_context* ctx, const SharedMoments& sh, const Mo
                            double* out, unsigned long long* cnt, i64* list, i64 cap) {
   int nch = 0;
   if (const i64 n = tri_ctas(g, nch); n >= 0) {
-    if (n > 0)
-      DFPCA_LAUNCH(ctx, k_solve_shared_tri<N>, static_cast<unsigned>(n), kSolveTile, 0, sh, mp, g, nch, out, cnt,
-                 list, cap);
+    if (n > 0) {
+      if (n / nch <= 65535 && g.gt < (i64(1) << 24))
+        DFPCA_LAUNCH(ctx, k_solve_sep_tri<N>, dim3(static_cast<unsigned>(nch), static_cast<unsigned>(n / nch)),
+                     kSolveTile, 0, sh, mp, g, out, cnt, list, cap);
+      else
+        DFPCA_LAUNCH(ctx, k_solve_shared_tri<N>, static_cast<unsigned>(n), kSolveTile, 0, sh, mp, g, nch, out, cnt,
+                     list, cap);
+    }
     return;
   }
   DFPCA_LAUNCH(ctx, k_solve_shared<N>, grid_for(g.npts, 128, 148ll * 64), 128, 0, sh, mp, g, out, cnt, list,
@@ -941,6 +1161,8 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
       offD[k] = total;
       total += 9 * n * n;
       sh.n[k] = static_cast<int>(n);
+      sh.band[k] = static_cast<int>(taps[k].R + taps[d + k].R);
+      sh.inv_n[k] = 1.0f / static_cast<float>(n);
     }
     auto& slot = ctx->table_cache[key];
     if (!slot) {

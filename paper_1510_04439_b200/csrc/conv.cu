@@ -2,6 +2,7 @@
 // instantiation per stencil radius, compiled in conv_r*.cu) or the generic
 // any-radius pass.  See conv_impl.cuh for the algorithm and the reference
 // citations (conv.hpp:161-201, 280-331).
+#include <cstdlib>
 #include <algorithm>
 #include <cstdint>
 #include <vector>
@@ -80,8 +81,25 @@ void launch_tphase2_r(dfpca_context* ctx, const TPhase2Spec& s, const Taps2P& tp
 
 }  // namespace
 
+bool run_tphase2_mma(dfpca_context* ctx, const TPhase2Spec& s);
+
+// Crossover radius of the t-phase: from this radius on the banded Toeplitz
+// products on the DMMA pipe (conv_mma.cu) beat the direct FMA kernels
+// (measured, profiles/r06_tphase_crossover.txt: direct 0.281 vs 0.289 ms at
+// R = 16, 0.372 vs 0.312 ms at R = 20, 0.738 vs 0.383 ms at R = 39).
+// DFPCA_TPHASE_MMA_R overrides it (0 = always the DMMA variant, a large value
+// = never).
+int tphase_mma_from() {
+  static const int r = [] {
+    const char* e = std::getenv("DFPCA_TPHASE_MMA_R");
+    return e && *e ? std::atoi(e) : 18;
+  }();
+  return r;
+}
+
 bool run_tphase2(dfpca_context* ctx, const TPhase2Spec& s) {
   const int Rmax = std::max(s.R[0], s.R[1]);
+  if (Rmax >= tphase_mma_from() && run_tphase2_mma(ctx, s)) return true;
   if (Rmax < 1 || Rmax > kMaxTemplR) return false;
   const int R = tiled_radius(Rmax);
   if (sizeof(double) * 3 * s.n1 * (s.n2 + 1) > 200 * 1024) return false;

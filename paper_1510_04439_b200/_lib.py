@@ -12,6 +12,30 @@ import threading
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
+
+
+def _point_at_wheel_libs():
+    """The library dlopens libnccl / libcusolver by soname (or from
+    DFPCA_NCCL_LIB / DFPCA_CUSOLVER_LIB).  In a Python environment they
+    usually ship inside the nvidia-* wheels, off the loader path: resolve them
+    from the installed packages at run time (a caller's setting wins)."""
+    import importlib.util
+    for env, pkg, so in (("DFPCA_NCCL_LIB", "nvidia.nccl", "libnccl.so.2"),
+                         ("DFPCA_CUSOLVER_LIB", "nvidia.cusolver", "libcusolver.so.11")):
+        if os.environ.get(env):
+            continue
+        try:
+            spec = importlib.util.find_spec(pkg)
+        except (ImportError, ValueError):
+            spec = None
+        for d in (spec.submodule_search_locations or []) if spec else []:
+            cand = Path(d) / "lib" / so
+            if cand.exists():
+                os.environ[env] = str(cand)
+                break
+
+
+_point_at_wheel_libs()
 LIB_PATH = Path(os.environ.get("DFPCA_CUDA_LIB", _HERE / "libdfpca_cuda.so"))
 
 MAX_DIM = 3

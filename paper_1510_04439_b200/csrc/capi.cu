@@ -571,6 +571,14 @@ int dfpca_binned_upload(dfpca_context* ctx, const dfpca_grid* grid, int64_t n_sa
     if (!out) fail(kConfig, "InvalidArgument", "null output handle");
     *out = nullptr;
     Grid g = make_grid(grid);
+    // argument validation up front: counts, and the arrays a count makes
+    // mandatory (a NULL grid array of the mean path or a NULL band means
+    // zeros; the per-sample bookkeeping must be given)
+    if (n_samples < 0) fail(kConfig, "InvalidArgument", "negative sample count");
+    if (has_covariance_path && n_pair_samples < 0) fail(kConfig, "InvalidArgument", "negative pair-sample count");
+    if (n_samples > 0 && !sample_sizes) fail(kConfig, "InvalidArgument", "null sample_sizes");
+    if (has_covariance_path && n_pair_samples > 0 && (!sample_index || !pair_weight))
+      fail(kConfig, "InvalidArgument", "null sample_index or pair_weight");
     auto b = std::make_unique<dfpca_binned>();
     b->grid = g;
     b->n_samples = n_samples;
@@ -603,9 +611,10 @@ int dfpca_binned_upload(dfpca_context* ctx, const dfpca_grid* grid, int64_t n_sa
       h2d(b->diag_value, diag_value, G * b->codes);
       b->sample_index.assign(sample_index, sample_index + n_pair_samples);
       b->pair_weight_h.assign(pair_weight, pair_weight + n_pair_samples);
-      // structure flag: identical per-sample masses (host check on upload)
+      // structure flag: identical per-sample masses (host check on upload;
+      // NULL masses are all zeros, hence identical)
       bool same = n_pair_samples >= 1;
-      for (i64 i = 1; i < n_pair_samples && same; ++i)
+      for (i64 i = 1; ps_mass && i < n_pair_samples && same; ++i)
         same = std::memcmp(ps_mass + i * G, ps_mass, sizeof(double) * G) == 0;
       b->identical_mass = same;
       dfpca_gpu::detect_shared_design(ctx, b.get());

@@ -1356,7 +1356,6 @@ struct CusolverApi {
       std::vector<std::string> names;
       if (const char* e = std::getenv("DFPCA_CUSOLVER_LIB")) names.push_back(e);
       names.push_back("libcusolver.so.11");
-      names.push_back("/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/cusolver/lib/libcusolver.so.11");
       void* h = nullptr;
       for (const auto& n : names)
         if ((h = dlopen(n.c_str(), RTLD_NOW | RTLD_GLOBAL))) break;

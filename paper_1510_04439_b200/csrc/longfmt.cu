@@ -22,6 +22,7 @@
 //
 // Only the header line (and, on failure, the failing line) is examined on
 // the host, to sniff the delimiter and to word the reference's messages.
+#include <sched.h>
 #include <fcntl.h>
 #include <sys/stat.h>
 #include <unistd.h>
@@ -67,44 +68,62 @@ constexpr int kMaxFields = 32;
 constexpr std::size_t kSlotBytes = 8u << 20;
 
 struct IoState {
-  int workers = 0;
-  std::vector<char*> slot;  // 2 per worker, pinned
+  int workers = 0;           // pool size (downloads use them all)
+  int upload_workers = 0;    // uploads: 8 unless DFPCA_IO_WORKERS sets the pool
+  std::vector<char*> slot;   // 2 per worker, pinned, allocated on a worker's first use
   std::vector<cudaStream_t> stream;
   std::vector<cudaEvent_t> slot_done, worker_done;
   std::mutex mu;
   ~IoState() {
-    for (char* p : slot) cudaFreeHost(p);
-    for (auto s : stream) cudaStreamDestroy(s);
-    for (auto e : slot_done) cudaEventDestroy(e);
-    for (auto e : worker_done) cudaEventDestroy(e);
+    for (char* p : slot)
+      if (p) cudaFreeHost(p);
+    for (auto s : stream)
+      if (s) cudaStreamDestroy(s);
+    for (auto e : slot_done)
+      if (e) cudaEventDestroy(e);
+    for (auto e : worker_done)
+      if (e) cudaEventDestroy(e);
+  }
+  // pinned slots, stream and events of workers [0, W) (caller holds mu)
+  void prepare(int W) {
+    for (int w = 0; w < W; ++w) {
+      if (stream[static_cast<std::size_t>(w)]) continue;
+      for (int s = 0; s < 2; ++s) {
+        const std::size_t i = static_cast<std::size_t>(2 * w + s);
+        DFPCA_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&slot[i]), kSlotBytes, cudaHostAllocDefault));
+        DFPCA_CUDA(cudaEventCreateWithFlags(&slot_done[i], cudaEventDisableTiming));
+      }
+      DFPCA_CUDA(cudaEventCreateWithFlags(&worker_done[static_cast<std::size_t>(w)], cudaEventDisableTiming));
+      DFPCA_CUDA(cudaStreamCreateWithFlags(&stream[static_cast<std::size_t>(w)], cudaStreamNonBlocking));
+    }
   }
 };
+
+// CPUs this process may run on (affinity / cgroup cpusets), not the machine's.
+int usable_cpus() {
+  cpu_set_t set;
+  if (sched_getaffinity(0, sizeof(set), &set) == 0) return std::max(1, CPU_COUNT(&set));
+  return static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+}
 
 IoState& io_state(dfpca_context* ctx) {
   if (!ctx->io_state) {
     auto io = std::make_shared<IoState>();
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     // downloads use every worker, uploads at most 8 (measured on the 16-core
     // host, 134 MB pageable: download 7.7 ms with 8 workers, 6.1 with 16;
-    // upload 5.3 ms with 8, slower with more)
-    io->workers = static_cast<int>(std::min(16u, std::max(1u, hw)));
-    if (const char* e = std::getenv("DFPCA_IO_WORKERS"); e && *e) io->workers = std::max(1, std::min(64, std::atoi(e)));
-    for (int w = 0; w < io->workers; ++w) {
-      for (int s = 0; s < 2; ++s) {
-        char* p = nullptr;
-        DFPCA_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), kSlotBytes, cudaHostAllocDefault));
-        io->slot.push_back(p);
-        cudaEvent_t e;
-        DFPCA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        io->slot_done.push_back(e);
-      }
-      cudaStream_t st;
-      DFPCA_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-      io->stream.push_back(st);
-      cudaEvent_t e;
-      DFPCA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      io->worker_done.push_back(e);
+    // upload 5.3 ms with 8, slower with more); an explicit DFPCA_IO_WORKERS
+    // sizes both
+    io->workers = std::min(16, usable_cpus());
+    io->upload_workers = std::min(io->workers, 8);
+    if (const char* e = std::getenv("DFPCA_IO_WORKERS"); e && *e) {
+      io->workers = std::max(1, std::min(64, std::atoi(e)));
+      io->upload_workers = io->workers;
     }
+    const auto W = static_cast<std::size_t>(io->workers);
+    io->slot.assign(2 * W, nullptr);
+    io->slot_done.assign(2 * W, nullptr);
+    io->stream.assign(W, nullptr);
+    io->worker_done.assign(W, nullptr);
     ctx->io_state = io;
   }
   return *static_cast<IoState*>(ctx->io_state.get());
@@ -117,7 +136,8 @@ void upload_bytes(dfpca_context* ctx, char* d_text, i64 S, Fill fill) {
   IoState& io = io_state(ctx);
   std::lock_guard<std::mutex> lk(io.mu);
   const i64 n_chunks = (S + static_cast<i64>(kSlotBytes) - 1) / static_cast<i64>(kSlotBytes);
-  const int W = static_cast<int>(std::min<i64>(std::min(io.workers, 8), std::max<i64>(n_chunks, 1)));
+  const int W = static_cast<int>(std::min<i64>(io.upload_workers, std::max<i64>(n_chunks, 1)));
+  io.prepare(W);
   // the slots' previous copies (an earlier call) were ordered on the worker
   // streams; the destination's stream-ordered allocation is ordered by `ready`
   cudaEvent_t ready;
@@ -178,6 +198,7 @@ void download_bytes(dfpca_context* ctx, char* dst, const char* d_src, i64 bytes)
   const i64 slot = static_cast<i64>(kSlotBytes);
   const i64 n_chunks = (bytes + slot - 1) / slot;
   const int W = static_cast<int>(std::min<i64>(io.workers, n_chunks));
+  io.prepare(W);
   cudaEvent_t ready;
   DFPCA_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
   DFPCA_CUDA(cudaEventRecord(ready, ctx->stream));

@@ -124,7 +124,6 @@ struct NcclApi {
     std::vector<std::string> names;
     if (const char* e = std::getenv("DFPCA_NCCL_LIB")) names.push_back(e);
     names.push_back("libnccl.so.2");
-    names.push_back("/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2");
     void* h = nullptr;
     for (const auto& n : names)
       if ((h = dlopen(n.c_str(), RTLD_NOW | RTLD_GLOBAL))) break;

@@ -1488,11 +1488,23 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
   if (sharded) {
     // every rank must take the same branch before the covariance exchange
     const unsigned long long any_empty = shard->max_over_ranks(n_empty);
-    if (any_empty > 0)
-      fail(kConfig, "InvalidArgument",
-           "sharded covariance: " + std::to_string(any_empty) +
-               " empty kernel window(s) on some rank need the fallback ladder (fft_smoother.hpp:471-487), "
-               "whose enlarged windows exceed the slab halo; run it on one device or widen the bandwidth");
+    if (any_empty > 0) {
+      // Empty kernel windows somewhere: the fallback ladder
+      // (fft_smoother.hpp:471-487) gathers windows enlarged up to 1.5^3 h,
+      // past the slab halo.  Every rank (all take this branch) runs the
+      // whole covariance on its own device -- the one-GPU path, so the
+      // ladder and the bits are exactly the one-GPU ones -- and keeps its
+      // rows; the rows are complete, so no exchange follows.
+      dfpca_surface* full_raw = nullptr;
+      run_covariance_impl(ctx, b, grid, h, mean_host, nullptr, &full_raw);
+      std::unique_ptr<dfpca_surface> full(full_raw);
+      if (out_rows > 0)
+        DFPCA_CUDA(cudaMemcpyAsync(surf->values.get(), full->values.get() + out_row0 * G,
+                                   sizeof(double) * out_rows * G, cudaMemcpyDeviceToDevice, st));
+      DFPCA_CUDA(cudaStreamSynchronize(st));
+      *out = surf.release();
+      return;
+    }
   }
 
   if (n_empty > 0) {

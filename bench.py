@@ -669,6 +669,20 @@ def tri_fractions(cells: int, R: int, tile: int = 64):
     return rows_in / (n1 * G), rows_out / (n1 * G), upper
 
 
+def tphase_fractions(cells: int, R: int):
+    """Fractions of the t-planes the trimmed t-phase reads and writes
+    (csrc/smooth.cu: row s computes the t1 planes >= plane(s) - t1_margin,
+    t1_margin = R + ceil(64 / cells), and reads R more planes below them):
+    averaged over the pair-grid rows s."""
+    margin = R + (64 + cells - 1) // cells
+    rd = wr = 0.0
+    for s1 in range(cells):
+        lo = max(0, s1 - margin)
+        wr += (cells - lo) / cells
+        rd += (cells - max(0, lo - R)) / cells
+    return rd / cells, wr / cells
+
+
 def kernel_model(G: int, n_pair: int, shared: bool):
     """Algorithmic work per step of every kernel of the d = 2 covariance step
     (DESIGN.md 'Roofline model'); one array = G^2 doubles.
@@ -677,7 +691,10 @@ def kernel_model(G: int, n_pair: int, shared: bool):
                           (the symmetric half of 2 n G^2 flops)    -> FP64 tensor
             k_rank_one    pw = W M(s) M(t): write 1 array          -> HBM
             k_scale_rows  w_i V_i: read + write n G doubles
-    t-phase k_tphase2     read pw, pv; write 9 t-partials: 11 arrays
+    t-phase k_tphase2     read pw, pv; write 9 t-partials -- the planes the
+                          trimmed kernel actually moves (tphase_fractions:
+                          0.71 of the input planes read, 0.62 of the output
+                          planes written at cfg 3: 347 MB, ncu 293 MB)
     s-phase k_pass_cols   s1 pass first: 9 in (rows s1 < s1_out + R) + 14 out
                           (rows s1 < s1_out); s2 pass: 14 in + 20 out on those rows
     solve   k_solve       20 moments in + 1 out at s <= t
@@ -685,20 +702,23 @@ def kernel_model(G: int, n_pair: int, shared: bool):
 
     shared: the shared-constant design (every subject observed at every node,
     the bench's GridNodes workload): the mass moments are closed-form
-    (k_solve_shared), pw is never built, only pv is convolved:
-    t-phase   read pv, write 3 value t-partials              4 arrays
+    (k_solve_sep_tri), pw is never built, only pv is convolved:
+    t-phase   read pv, write 3 value t-partials (trimmed as above)
     s-phase   s1: 3 in (trimmed + R rows) + 4 out; s2: 4 in + 5 out (s <= t rows)
     solve     5 value moments in + 1 out at s <= t
     """
     cells = int(round(G ** 0.5))
-    f_in, f_out, upper = tri_fractions(cells, int(np.ceil(H * cells)))
+    R = int(np.ceil(H * cells))
+    f_in, f_out, upper = tri_fractions(cells, R)
+    t_rd, t_wr = tphase_fractions(cells, R)
     arr = 8.0 * G * G
     if shared:
         return {
             "k_gemm_tn": ("tensor", 2.0 * n_pair * G * G / 2.0),
             "k_scale_rows": ("hbm", 2 * 8.0 * n_pair * G),
-            "k_tphase2": ("hbm", 4 * arr),
+            "k_tphase2": ("hbm", (1 * t_rd + 3 * t_wr) * arr),
             "k_pass_cols": ("hbm", (3 * f_in + 4 * f_out + (4 + 5) * f_out) * arr),
+            "k_solve_sep_tri": ("hbm", 6 * upper * arr),
             "k_solve_shared_tri": ("hbm", 6 * upper * arr),
             "k_center_mirror": ("hbm", (upper + 1.0) * arr),
         }
@@ -706,7 +726,7 @@ def kernel_model(G: int, n_pair: int, shared: bool):
         "k_gemm_tn": ("tensor", 2.0 * n_pair * G * G / 2.0),
         "k_rank_one": ("hbm", 1 * arr),
         "k_scale_rows": ("hbm", 2 * 8.0 * n_pair * G),
-        "k_tphase2": ("hbm", 11 * arr),
+        "k_tphase2": ("hbm", (2 * t_rd + 9 * t_wr) * arr),
         "k_pass_cols": ("hbm", (9 * f_in + 14 * f_out + (14 + 20) * f_out) * arr),
         "k_solve_tri": ("hbm", 21 * upper * arr),
         "k_center_mirror": ("hbm", (upper + 1.0) * arr),
@@ -745,7 +765,7 @@ def roofline(kstats, G, binned, slab=None):
     hbm = peaks.get("hbm_gbs")
     if not kstats:
         return None
-    model = kernel_model(G, N_SUBJ, shared="k_solve_shared_tri" in kstats)
+    model = kernel_model(G, N_SUBJ, shared=("k_solve_shared_tri" in kstats or "k_solve_sep_tri" in kstats))
     if slab is not None:  # one rank's share: its rows of the upper triangle
         r0, nr = slab
         share = (sum(G - s for s in range(r0, r0 + nr))) / (G * (G + 1) / 2)

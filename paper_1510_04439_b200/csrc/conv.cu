@@ -111,8 +111,23 @@ bool run_tphase2(dfpca_context* ctx, const TPhase2Spec& s) {
   return true;
 }
 
+bool run_pass_mma(dfpca_context* ctx, const PassSpec& s);
+
+// Crossover radius of the column passes (the s-phase): banded Toeplitz
+// products on the DMMA pipe (conv_mma.cu) from this radius on
+// (profiles/r06_pass_crossover.txt: direct 0.523 vs 0.542 ms at R = 32,
+// 0.729 vs 0.561 ms at R = 39); DFPCA_PASS_MMA_R overrides it.
+int pass_mma_from() {
+  static const int r = [] {
+    const char* e = std::getenv("DFPCA_PASS_MMA_R");
+    return e && *e ? std::atoi(e) : 36;
+  }();
+  return r;
+}
+
 void run_pass(dfpca_context* ctx, const PassSpec& s, double* taps_dev) {
   const int R = s.R;
+  if (R >= pass_mma_from() && s.in.inner > 1 && run_pass_mma(ctx, s)) return;
   const bool tiled_ok = R <= kMaxTemplR && s.in.n <= conv_detail::kMaxN && s.in.n >= 1 &&
                         (s.in.inner == 1 || s.in.inner >= 16) &&
                         s.in.outer * ((s.in.inner + conv_detail::kTC - 1) / conv_detail::kTC) < (1ll << 31) &&

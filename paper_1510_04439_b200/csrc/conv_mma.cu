@@ -199,7 +199,175 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   cp_wait<0>();
 }
 
+
+// ---- s-phase passes (k_pass_cols' work) on the DMMA pipe -----------------
+// A pass along an axis of n <= 64 nodes over 64-column tiles of the array:
+// out_r = A_r X with A_r[j][m] = taps_r[m - j + R] for the tile X [n][64],
+// the same tiles, triangle trims and output windows as k_pass_cols (View::tri,
+// View::lo/hi), up to three orders from one staged tile.
+struct PassTaps {
+  double t[3][kTz];  // [order][o + kTc]
+};
+
+__device__ inline void pass_meta(const View& in, int tile, int chunks, int R, int& ob, int& c0, int& rows, int& nout,
+                                 int& lo) {
+  const int n = static_cast<int>(in.n);
+  const int inner = static_cast<int>(in.inner);
+  ob = tile / chunks;
+  c0 = (tile - ob * chunks) * kP;
+  rows = n;
+  nout = n;
+  lo = static_cast<int>(in.lo);
+  const int win_hi = static_cast<int>(in.hi);
+  if (win_hi >= 0) {
+    nout = win_hi < n ? win_hi : n;
+    rows = nout + R < n ? nout + R : n;
+  }
+  if (in.tri != 0) {
+    const int triG = static_cast<int>(in.tri_G), tri_rn = static_cast<int>(in.tri_rn);
+    const int c1 = (c0 + kP < inner ? c0 + kP : inner) - 1;
+    const int tmax = (c0 / triG == c1 / triG) ? c1 % triG : triG - 1;
+    int s1_out = (tmax + static_cast<int>(in.tri_t0)) / tri_rn + 1;
+    if (in.tri_row_hi >= 0 && s1_out > in.tri_row_hi) s1_out = static_cast<int>(in.tri_row_hi);
+    s1_out -= static_cast<int>(in.tri_row0);
+    if (s1_out < 0) s1_out = 0;
+    const int triR = in.tri_R, tri_n1 = static_cast<int>(in.tri_n1);
+    if (in.tri == 1) {
+      const int s1_in = s1_out + triR < tri_n1 ? s1_out + triR : tri_n1;
+      if (ob >= s1_in) rows = nout = 0;
+    } else if (in.tri == 3) {
+      if (ob >= s1_out) rows = nout = 0;
+    } else {
+      nout = s1_out < n ? s1_out : n;
+      rows = nout + triR < n ? nout + triR : n;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreadsM, 2)
+    k_pass_cols_mma(View in, View o0, View o1, View o2, int n_out, const PassTaps* __restrict__ taps_g, int R) {
+  extern __shared__ __align__(16) double sm[];
+  double* Xb = sm;                  // [2][kRows][kLd]
+  double* tz = sm + 2 * kRows * kLd;  // PassTaps
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < 2 * kRows * kLd; e += blockDim.x) sm[e] = 0.0;
+  for (int e = tid; e < 3 * kTz; e += blockDim.x) tz[e] = reinterpret_cast<const double*>(taps_g)[e];
+  __syncthreads();
+  const int inner = static_cast<int>(in.inner);
+  const int chunks = (inner + kP - 1) / kP;
+  const int n_tiles = static_cast<int>(in.outer) * chunks;
+  const bool vec = (in.js % 2 == 0) && (in.os % 2 == 0) && (inner % 2 == 0) &&
+                   ((reinterpret_cast<std::uintptr_t>(in.p) & 15) == 0);
+  auto issue = [&](int tile, int b) {
+    int ob, c0, rows, nout, lo;
+    pass_meta(in, tile, chunks, R, ob, c0, rows, nout, lo);
+    const double* src = in.p + static_cast<i64>(ob) * in.os + c0;
+    double* X = Xb + b * kRows * kLd;
+    const int cols = inner - c0 < kP ? inner - c0 : kP;
+    if (vec && cols == kP) {
+      for (int e = tid; e < rows * (kP / 2); e += blockDim.x) {
+        const int j = e / (kP / 2), c = (e % (kP / 2)) * 2;
+        cp16(X + j * kLd + c, src + static_cast<i64>(j) * in.js + c);
+      }
+    } else {
+      for (int e = tid; e < rows * kP; e += blockDim.x) {
+        const int j = e / kP, c = e % kP;
+        if (c < cols) cp8(X + j * kLd + c, src + static_cast<i64>(j) * in.js + c);
+        else X[j * kLd + c] = 0.0;
+      }
+    }
+  };
+  const int wr = (warp >> 1) * 16, wc = (warp & 1) * 32;
+  const int lr = lane >> 2, lk = lane & 3;
+  int tile = blockIdx.x, buf = 0;
+  if (tile < n_tiles) issue(tile, 0);
+  cp_commit();
+  while (tile < n_tiles) {
+    const int next = tile + gridDim.x;
+    if (next < n_tiles) issue(next, buf ^ 1);
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    int ob, c0, rows, nout, lo;
+    pass_meta(in, tile, chunks, R, ob, c0, rows, nout, lo);
+    const double* X = Xb + buf * kRows * kLd;
+    if (wr + 16 > lo && wr < nout) {
+      double acc[3][2][4][2] = {};
+      const int k0 = max(0, (wr - R) & ~3), k1 = min(rows, wr + 16 + R);
+      for (int k = k0; k < k1; k += 4) {
+        const int m = k + lk;
+        double b[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = X[m * kLd + wc + j * 8 + lr];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          if (r < n_out) {
+            const double* ta = tz + r * kTz + kTc;
+            double a[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) a[i] = ta[m - (wr + i * 8 + lr)];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) dmma(acc[r][i][j], a[i], b[j]);
+          }
+        }
+      }
+      const int cols = inner - c0 < kP ? inner - c0 : kP;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        if (r >= n_out) continue;
+        const View& o = r == 0 ? o0 : (r == 1 ? o1 : o2);
+        double* base = o.p + static_cast<i64>(ob) * o.os + c0;
+        const bool ovec = (o.js % 2 == 0) && (o.os % 2 == 0) && ((reinterpret_cast<std::uintptr_t>(o.p) & 15) == 0) &&
+                          (c0 % 2 == 0);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int row = wr + i * 8 + lr;
+          if (row < lo || row >= nout) continue;
+          double* rp = base + static_cast<i64>(row) * o.js;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int col = wc + j * 8 + 2 * lk;
+            if (ovec && col + 1 < cols) {
+              *reinterpret_cast<double2*>(rp + col) = make_double2(acc[r][i][j][0], acc[r][i][j][1]);
+            } else {
+              if (col < cols) rp[col] = acc[r][i][j][0];
+              if (col + 1 < cols) rp[col + 1] = acc[r][i][j][1];
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    buf ^= 1;
+    tile = next;
+  }
+  cp_wait<0>();
+}
+
 }  // namespace
+
+bool run_pass_mma(dfpca_context* ctx, const PassSpec& s) {
+  if (s.in.n > kP || s.in.n < 1 || s.in.inner < kP / 2 || s.R > kP || s.n_out < 1 || s.n_out > 3) return false;
+  const i64 tiles = s.in.outer * ((s.in.inner + kP - 1) / kP);
+  if (tiles >= (i64(1) << 31)) return false;
+  PassTaps h{};
+  for (int r = 0; r < s.n_out; ++r)
+    for (int o = -s.R; o <= s.R; ++o) h.t[r][o + kTc] = s.taps[r][o + s.R];
+  DevBuf<PassTaps> dt(1);
+  DFPCA_CUDA(cudaMemcpyAsync(dt.get(), &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
+  const View o1 = s.n_out > 1 ? s.out[1] : s.out[0];
+  const View o2 = s.n_out > 2 ? s.out[2] : s.out[0];
+  const std::size_t smem = sizeof(double) * (2 * kRows * kLd) + sizeof(PassTaps);
+  allow_smem(k_pass_cols_mma, smem);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pass_cols_mma, kThreadsM, smem);
+  const unsigned grid =
+      static_cast<unsigned>(std::max<i64>(1, std::min<i64>(tiles, static_cast<i64>(std::max(per_sm, 1)) * ctx->sm_count)));
+  DFPCA_LAUNCH(ctx, k_pass_cols_mma, grid, kThreadsM, smem, s.in, s.out[0], o1, o2, s.n_out, dt.get(), s.R);
+  return true;
+}
 
 bool run_tphase2_mma(dfpca_context* ctx, const TPhase2Spec& s) {
   if (s.n1 > kP || s.n2 > kP || s.n1 < 1 || s.n2 < 1 || s.R[0] > kP || s.R[1] > kP) return false;

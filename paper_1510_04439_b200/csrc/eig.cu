@@ -39,15 +39,19 @@ __host__ __device__ inline unsigned long long splitmix64(unsigned long long x) {
   return x ^ (x >> 31);
 }
 
-// std::mt19937_64 seeded with `seed`, producing n_words tempered outputs.
+// std::mt19937_64 seeded with `seed` (or resumed from `state`), producing
+// n_words tempered outputs (a multiple of 312 when the state is carried on).
 // The twist runs out of place between two state buffers: the 156 words that
 // depend only on the old state, one barrier, the 156 that need the first
 // half's new words, and each thread tempers the word it has just written --
 // two barriers per 312 outputs.
 __global__ void __launch_bounds__(kMtN) k_mt19937_64(unsigned long long seed, i64 n_words,
-                                                     unsigned long long* __restrict__ out) {
+                                                     unsigned long long* __restrict__ out,
+                                                     unsigned long long* __restrict__ state, int resume) {
   __shared__ unsigned long long buf[2][kMtN];
-  if (threadIdx.x == 0) {
+  if (resume) {
+    buf[0][threadIdx.x] = state[threadIdx.x];
+  } else if (threadIdx.x == 0) {
     buf[0][0] = seed;
     for (int i = 1; i < kMtN; ++i)
       buf[0][i] =
@@ -80,6 +84,7 @@ __global__ void __launch_bounds__(kMtN) k_mt19937_64(unsigned long long seed, i6
     __syncthreads();
     cur ^= 1;
   }
+  if (state) state[i] = buf[cur][i];  // the state after the last full twist (resume point)
 }
 
 // Omega(i, j) = sd * normal #(j * M + i) (column-major fill,
@@ -87,10 +92,9 @@ __global__ void __launch_bounds__(kMtN) k_mt19937_64(unsigned long long seed, i6
 // Stored row-major [M][ldq] (ldq even; the padding is never read) as the
 // GEMM's K-major operand.
 __global__ void k_box_muller(const unsigned long long* __restrict__ words, i64 M, i64 q, i64 ldq, double sd,
-                             double* __restrict__ omega) {
+                             i64 p_begin, i64 p_end, double* __restrict__ omega) {
   const i64 total = M * q;
-  const i64 pairs = (total + 1) / 2;
-  for (i64 pidx = blockIdx.x * (i64)blockDim.x + threadIdx.x; pidx < pairs;
+  for (i64 pidx = p_begin + blockIdx.x * (i64)blockDim.x + threadIdx.x; pidx < p_end;
        pidx += (i64)gridDim.x * blockDim.x) {
     const double u1 = (static_cast<double>(words[2 * pidx] >> 11) + 0.5) * 0x1.0p-53;
     const double u2 = (static_cast<double>(words[2 * pidx + 1] >> 11) + 0.5) * 0x1.0p-53;
@@ -395,113 +399,49 @@ __global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ Ag, double
 // (how far X already was from orthonormal columns).
 constexpr int kCqMaxQ = 128;
 
-// Blocked right-looking Cholesky (upper, G = R^T R), 32-wide panels: warp 0
-// factors the panel's diagonal block with the block's columns in registers
-// (lane = column; the pivot row goes through shared memory as broadcasts),
-// the panel rows right of it are solved with a thread per column (the 32
-// unknowns in registers), and the trailing block takes the rank-32 update (a
-// thread per entry of the upper triangle): three barriers per panel, and no
-// shared-memory read-after-write chains inside the loops.
-__global__ void __launch_bounds__(256) k_chol_factor(const double* __restrict__ Gg, int q, double* __restrict__ Rg,
-                                                     double* __restrict__ flags) {
+// Right-looking Cholesky (upper, G = R^T R) on one CTA of 1024 threads, one
+// barrier per pivot: row k is scaled on its way out to global memory, so the
+// trailing update (a warp per row, lanes over columns) reads the unscaled
+// row without a hazard.  Measured faster than 32-wide blocked panels and than
+// a 256-thread column-oriented variant (87 vs 150 / 137 us at q = 99): the
+// factorization is bound by its pivot chain, and more warps hide it better.
+__global__ void __launch_bounds__(1024) k_chol_factor(const double* __restrict__ Gg, int q, double* __restrict__ Rg,
+                                                      double* __restrict__ flags) {
   extern __shared__ double sm[];
   const int ld = q + 1;
-  double* R = sm;  // [q][q+1], upper triangle used
-  __shared__ double red[8], prow[32];
-  __shared__ int bad;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* R = sm;
+  __shared__ double red[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   double dmax = 0.0;
   for (int e = tid; e < q * q; e += blockDim.x) {
     const int r = e / q, c = e % q;
     const double g = Gg[e];
     R[r * ld + c] = g;
+    Rg[e] = 0.0;
     dmax = fmax(dmax, fabs(g - (r == c ? 1.0 : 0.0)));
   }
   for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   if (lane == 0) red[warp] = dmax;
-  if (tid == 0) bad = 0;
   __syncthreads();
   if (tid == 0) {
     double m = 0.0;
-    for (int w = 0; w < 8; ++w) m = fmax(m, red[w]);
+    for (int w = 0; w < nw; ++w) m = fmax(m, red[w]);
     flags[1] = m;
+    flags[0] = 0.0;
   }
-  for (int k0 = 0; k0 < q; k0 += 32) {
-    const int kb = min(32, q - k0), k1 = k0 + kb;
-    if (warp == 0) {
-      const int c = k0 + lane;  // this lane's column of the diagonal block
-      double col[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) col[i] = (i < kb && lane < kb && i <= lane) ? R[(k0 + i) * ld + c] : 0.0;
-      bool ok = true;
-#pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        if (r < kb && ok) {
-          const double dr = __shfl_sync(0xffffffffu, col[r], r);
-          if (!(dr > 0.0) || !isfinite(dr)) {
-            ok = false;
-          } else {
-            const double piv = sqrt(dr);
-            if (lane == r) col[r] = piv;
-            else if (lane > r) col[r] /= piv;
-            if (lane >= r) prow[lane] = col[r];
-            __syncwarp();
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (i > r && i <= lane) col[i] -= prow[i] * col[r];
-            __syncwarp();
-          }
-        }
-      }
-      if (!ok && lane == 0) bad = 1;
-      if (lane < kb) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (i < kb && i <= lane) R[(k0 + i) * ld + c] = col[i];
-      }
+  for (int k = 0; k < q; ++k) {
+    const double d = R[k * ld + k];
+    if (!(d > 0.0) || !isfinite(d)) {
+      if (tid == 0) flags[0] = 1.0;
+      return;  // uniform
+    }
+    const double rk = sqrt(d), inv = 1.0 / rk, dinv = 1.0 / d;
+    for (int j = k + tid; j < q; j += blockDim.x) Rg[k * q + j] = j == k ? rk : R[k * ld + j] * inv;
+    for (int i = k + 1 + warp; i < q; i += nw) {
+      const double rki = R[k * ld + i] * dinv;
+      for (int j = i + lane; j < q; j += 32) R[i * ld + j] -= rki * R[k * ld + j];
     }
     __syncthreads();
-    if (bad) break;
-    // panel rows [k0, k1), columns >= k1: R11^T X = G12, a thread per column
-    for (int c = k1 + tid; c < q; c += blockDim.x) {
-      double x[32];
-#pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        if (r < kb) {
-          double s = R[(k0 + r) * ld + c];
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (i < r) s -= R[(k0 + i) * ld + k0 + r] * x[i];
-          x[r] = s / R[(k0 + r) * ld + k0 + r];
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 32; ++r)
-        if (r < kb) R[(k0 + r) * ld + c] = x[r];
-    }
-    __syncthreads();
-    // trailing update: G22 -= R12^T R12 on the upper triangle
-    const int m = q - k1;
-    for (int e = tid; e < m * m; e += blockDim.x) {
-      const int i = k1 + e / m, j = k1 + e % m;
-      if (j < i) continue;
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int r = k0;
-      for (; r + 3 < k1; r += 4) {
-        s0 += R[r * ld + i] * R[r * ld + j];
-        s1 += R[(r + 1) * ld + i] * R[(r + 1) * ld + j];
-        s2 += R[(r + 2) * ld + i] * R[(r + 2) * ld + j];
-        s3 += R[(r + 3) * ld + i] * R[(r + 3) * ld + j];
-      }
-      for (; r < k1; ++r) s0 += R[r * ld + i] * R[r * ld + j];
-      R[i * ld + j] -= (s0 + s1) + (s2 + s3);
-    }
-    __syncthreads();
-  }
-  if (tid == 0) flags[0] = bad ? 1.0 : 0.0;
-  for (int e = tid; e < q * q; e += blockDim.x) {
-    const int r = e / q, c = e % q;
-    Rg[e] = c >= r ? R[r * ld + c] : 0.0;
   }
 }
 
@@ -1218,39 +1158,82 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
   const i64 ldq = (q + 1) & ~1ll;
   // out[M][ldq] = Sigma X for X [M][ldq]: sums split exactly as the
   // one-device product (same split-K), so every row is bit-identical
-  auto apply_sigma = [&](const double* X, double* out) {
+  // columns [c0, c0 + nc) of out = Sigma X (column blocks: a sharded run
+  // splits exactly like the one-device run, so the rows are bit-identical)
+  auto apply_sigma = [&](const double* X, double* out, i64 c0, i64 nc) {
     if (!tr) {
-      gemm_tn(ctx, M, q, M, mv.sigma, M, nullptr, X, ldq, out, ldq, false);
+      gemm_tn(ctx, M, nc, M, mv.sigma, M, nullptr, X + c0, ldq, out + c0, ldq, false);
       return;
     }
     const i64 chunk = std::max<i64>(1, rs.m_max * ldq);
     DevBuf<double> loc(static_cast<std::size_t>(chunk));
     DFPCA_CUDA(cudaMemsetAsync(loc.get(), 0, sizeof(double) * chunk, st));
     if (rs.m_loc > 0)
-      gemm_tn(ctx, rs.m_loc, q, M, rs.sigma_t.get(), rs.m_loc, nullptr, X, ldq, loc.get(), ldq, false, 0, -1,
-              gemm_splits(ctx, M, q, M));
+      gemm_tn(ctx, rs.m_loc, nc, M, rs.sigma_t.get(), rs.m_loc, nullptr, X + c0, ldq, loc.get() + c0, ldq, false, 0,
+              -1, gemm_splits(ctx, M, nc, M));
     DevBuf<double> all(static_cast<std::size_t>(tr->world() * chunk));
     tr->all_gather(ctx, loc.get(), all.get(), chunk);
     for (int r = 0; r < tr->world(); ++r)
       if (rs.counts[static_cast<std::size_t>(r)] > 0)
-        DFPCA_CUDA(cudaMemcpyAsync(out + rs.offsets[static_cast<std::size_t>(r)] * ldq,
-                                   all.get() + static_cast<i64>(r) * chunk,
-                                   sizeof(double) * rs.counts[static_cast<std::size_t>(r)] * ldq,
-                                   cudaMemcpyDeviceToDevice, st));
+        DFPCA_CUDA(cudaMemcpy2DAsync(out + rs.offsets[static_cast<std::size_t>(r)] * ldq + c0, sizeof(double) * ldq,
+                                     all.get() + static_cast<i64>(r) * chunk + c0, sizeof(double) * ldq,
+                                     sizeof(double) * nc, static_cast<std::size_t>(rs.counts[static_cast<std::size_t>(r)]),
+                                     cudaMemcpyDeviceToDevice, st));
   };
 
-  // Omega
-  DevBuf<unsigned long long> words(static_cast<std::size_t>(2 * ((M * q + 1) / 2)));
-  DFPCA_LAUNCH(ctx, k_mt19937_64, 1, kMtN, 0, splitmix64(seed), static_cast<i64>(words.size()),
-               words.get());
+  // Omega and Y = Sigma Omega ([M][q]; Sigma is exactly symmetric, so
+  // Sigma(k, m) is the K-major operand), pipelined by column blocks: the
+  // one-CTA Mersenne Twister runs on the aux stream and stops after the
+  // words of the first 64 columns (rounded up to whole twists, its state
+  // saved); while it produces the rest, the first block's Box-Muller and
+  // product run on the context stream.
+  const i64 n_words = 2 * ((M * q + 1) / 2);
+  const i64 pairs_total = (M * q + 1) / 2;
+  const i64 c1 = std::min<i64>(q, 64);
+  const i64 w1 = std::min<i64>(n_words, ((c1 * M + kMtN - 1) / kMtN) * kMtN);
+  DevBuf<unsigned long long> words(static_cast<std::size_t>(n_words)), mt_state(kMtN);
   DevBuf<double> omega(static_cast<std::size_t>(M * ldq));
-  DFPCA_LAUNCH(ctx, k_box_muller, grid_for((M * q + 1) / 2, 256), 256, 0, words.get(), M, q, ldq,
-               1.0 / std::sqrt(static_cast<double>(q)), omega.get());
-
-  // Y = Sigma Omega  ([M][q]); Sigma is exactly symmetric, so Sigma(k, m) is
-  // the K-major operand.
   DevBuf<double> Y(static_cast<std::size_t>(M * ldq));
-  apply_sigma(omega.get(), Y.get());
+  const double sd = 1.0 / std::sqrt(static_cast<double>(q));
+  {
+    cudaStream_t aux = ctx->aux_stream();
+    cudaEvent_t ev[3];
+    for (auto& e : ev) DFPCA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    struct Evs {
+      cudaEvent_t* e;
+      ~Evs() {
+        for (int i = 0; i < 3; ++i) cudaEventDestroy(e[i]);
+      }
+    } evs{ev};
+    DFPCA_CUDA(cudaEventRecord(ev[0], st));  // the buffers' stream-ordered allocations
+    DFPCA_CUDA(cudaStreamWaitEvent(aux, ev[0], 0));
+    {
+      struct AuxLaunch {  // launches below go to the aux stream
+        dfpca_context* c;
+        cudaStream_t saved;
+        AuxLaunch(dfpca_context* c_, cudaStream_t s) : c(c_), saved(c_->stream) { c->stream = s; }
+        ~AuxLaunch() { c->stream = saved; }
+      } on_aux(ctx, aux);
+      DFPCA_LAUNCH(ctx, k_mt19937_64, 1, kMtN, 0, splitmix64(seed), w1, words.get(), mt_state.get(), 0);
+      DFPCA_CUDA(cudaEventRecord(ev[1], aux));
+      if (w1 < n_words)
+        DFPCA_LAUNCH(ctx, k_mt19937_64, 1, kMtN, 0, 0ull, n_words - w1, words.get() + w1, mt_state.get(), 1);
+      DFPCA_CUDA(cudaEventRecord(ev[2], aux));
+    }
+    DFPCA_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
+    // Box-Muller pairs of the first block: its columns hold c1 * M normals
+    // (even: c1 = 64 when there is a second block); one block takes them all
+    const i64 p_split = c1 < q ? (c1 * M) / 2 : pairs_total;
+    DFPCA_LAUNCH(ctx, k_box_muller, grid_for(p_split, 256), 256, 0, words.get(), M, q, ldq, sd, 0ll, p_split,
+                 omega.get());
+    apply_sigma(omega.get(), Y.get(), 0, c1);
+    DFPCA_CUDA(cudaStreamWaitEvent(st, ev[2], 0));
+    if (c1 < q) {
+      DFPCA_LAUNCH(ctx, k_box_muller, grid_for(pairs_total - p_split, 256), 256, 0, words.get(), M, q, ldq, sd,
+                   p_split, pairs_total, omega.get());
+      apply_sigma(omega.get(), Y.get(), c1, q - c1);
+    }
+  }
 
   // Thin Q with range(Q) = range(Y) (eigensolve.hpp:260-263; any orthonormal
   // basis of range(Y) gives the same Ritz pairs): Cholesky QR twice -- two
@@ -1269,10 +1252,10 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
     allow_smem(k_row_trsm, tsm);
     const unsigned ctas = static_cast<unsigned>(std::min<i64>((M + kTrsmWarps - 1) / kTrsmWarps, 2 * ctx->sm_count));
     gemm_tn(ctx, q, q, M, Y.get(), ldq, nullptr, Y.get(), ldq, G.get(), q, false);
-    DFPCA_LAUNCH(ctx, k_chol_factor, 1, 256, fsm, G.get(), qi, R.get(), flags.get());
+    DFPCA_LAUNCH(ctx, k_chol_factor, 1, 1024, fsm, G.get(), qi, R.get(), flags.get());
     DFPCA_LAUNCH(ctx, k_row_trsm, ctas, kTrsmWarps * 32, tsm, Y.get(), M, qi, ldq, R.get(), flags.get(), Q1.get());
     gemm_tn(ctx, q, q, M, Q1.get(), ldq, nullptr, Q1.get(), ldq, G.get(), q, false);
-    DFPCA_LAUNCH(ctx, k_chol_factor, 1, 256, fsm, G.get(), qi, R.get(), flags.get() + 2);
+    DFPCA_LAUNCH(ctx, k_chol_factor, 1, 1024, fsm, G.get(), qi, R.get(), flags.get() + 2);
     DFPCA_LAUNCH(ctx, k_row_trsm, ctas, kTrsmWarps * 32, tsm, Q1.get(), M, qi, ldq, R.get(), flags.get() + 2,
                  Q.get());
     double hf[4];
@@ -1297,7 +1280,7 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
 
   // small = Q^T (Sigma Q)
   DevBuf<double> Z(static_cast<std::size_t>(M * ldq));
-  apply_sigma(Q.get(), Z.get());
+  apply_sigma(Q.get(), Z.get(), 0, q);
   DevBuf<double> small(static_cast<std::size_t>(q * q)), Vs(static_cast<std::size_t>(q * q));
   gemm_tn(ctx, q, q, M, Q.get(), ldq, nullptr, Z.get(), ldq, small.get(), q, false);
 

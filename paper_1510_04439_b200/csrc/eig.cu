@@ -1241,83 +1241,89 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
   // the first pass left Q1 within 0.1 of orthonormal (then the second pass
   // restores orthogonality to rounding); otherwise (nearly rank-deficient
   // sketches) Householder QR, one reflector per launch.
-  DevBuf<double> Q(static_cast<std::size_t>(M * ldq)), Qt(static_cast<std::size_t>(M * q));
-  bool cholqr_ok = false;
-  if (q <= kCqMaxQ) {
-    DevBuf<double> G(static_cast<std::size_t>(q * q)), R(static_cast<std::size_t>(q * q)),
-        Q1(static_cast<std::size_t>(M * ldq)), flags(4);
-    const int qi = static_cast<int>(q);
-    const std::size_t fsm = sizeof(double) * q * (q + 1), tsm = trsm_smem(qi);
-    allow_smem(k_chol_factor, fsm);
-    allow_smem(k_row_trsm, tsm);
-    const unsigned ctas = static_cast<unsigned>(std::min<i64>((M + kTrsmWarps - 1) / kTrsmWarps, 2 * ctx->sm_count));
-    gemm_tn(ctx, q, q, M, Y.get(), ldq, nullptr, Y.get(), ldq, G.get(), q, false);
-    DFPCA_LAUNCH(ctx, k_chol_factor, 1, 1024, fsm, G.get(), qi, R.get(), flags.get());
-    DFPCA_LAUNCH(ctx, k_row_trsm, ctas, kTrsmWarps * 32, tsm, Y.get(), M, qi, ldq, R.get(), flags.get(), Q1.get());
-    gemm_tn(ctx, q, q, M, Q1.get(), ldq, nullptr, Q1.get(), ldq, G.get(), q, false);
-    DFPCA_LAUNCH(ctx, k_chol_factor, 1, 1024, fsm, G.get(), qi, R.get(), flags.get() + 2);
-    DFPCA_LAUNCH(ctx, k_row_trsm, ctas, kTrsmWarps * 32, tsm, Q1.get(), M, qi, ldq, R.get(), flags.get() + 2,
-                 Q.get());
-    double hf[4];
-    DFPCA_CUDA(cudaMemcpyAsync(hf, flags.get(), sizeof(hf), cudaMemcpyDeviceToHost, st));
+  // The Cholesky-QR acceptance flags are read at the stage's one host sync
+  // (with the Ritz values), so nothing waits in between; a rejected sketch
+  // reruns the rest from Y with Householder QR.
+  auto from_Y = [&](bool cholqr) -> bool {
+    DevBuf<double> Q(static_cast<std::size_t>(M * ldq)), Qt(static_cast<std::size_t>(M * q)), flags(4);
+    if (cholqr) {
+      DevBuf<double> G(static_cast<std::size_t>(q * q)), R(static_cast<std::size_t>(q * q)),
+          Q1(static_cast<std::size_t>(M * ldq));
+      const int qi = static_cast<int>(q);
+      const std::size_t fsm = sizeof(double) * q * (q + 1), tsm = trsm_smem(qi);
+      allow_smem(k_chol_factor, fsm);
+      allow_smem(k_row_trsm, tsm);
+      const unsigned ctas =
+          static_cast<unsigned>(std::min<i64>((M + kTrsmWarps - 1) / kTrsmWarps, 2 * ctx->sm_count));
+      gemm_tn(ctx, q, q, M, Y.get(), ldq, nullptr, Y.get(), ldq, G.get(), q, false);
+      DFPCA_LAUNCH(ctx, k_chol_factor, 1, 1024, fsm, G.get(), qi, R.get(), flags.get());
+      DFPCA_LAUNCH(ctx, k_row_trsm, ctas, kTrsmWarps * 32, tsm, Y.get(), M, qi, ldq, R.get(), flags.get(),
+                   Q1.get());
+      gemm_tn(ctx, q, q, M, Q1.get(), ldq, nullptr, Q1.get(), ldq, G.get(), q, false);
+      DFPCA_LAUNCH(ctx, k_chol_factor, 1, 1024, fsm, G.get(), qi, R.get(), flags.get() + 2);
+      DFPCA_LAUNCH(ctx, k_row_trsm, ctas, kTrsmWarps * 32, tsm, Q1.get(), M, qi, ldq, R.get(), flags.get() + 2,
+                   Q.get());
+      transpose(ctx, Q.get(), M, q, Qt.get(), ldq, M);
+    } else {
+      DevBuf<double> Yt(static_cast<std::size_t>(M * q)), tau(static_cast<std::size_t>(q));
+      transpose(ctx, Y.get(), M, q, Yt.get(), ldq, M);
+      for (i64 j = -1; j < q - 1; ++j) {
+        const i64 cols = q - (j + 1);
+        DFPCA_LAUNCH(ctx, k_house_step, static_cast<unsigned>(cols), 512, 0, Yt.get(), M, q, j, tau.get());
+      }
+      DFPCA_LAUNCH(ctx, k_q_init, grid_for(M * q, 256), 256, 0, Qt.get(), M, q);
+      for (i64 j = q - 1; j >= 0; --j)
+        DFPCA_LAUNCH(ctx, k_q_apply, static_cast<unsigned>(q - j), 512, 0, Yt.get(), tau.get(), M, q, j,
+                     Qt.get());
+      transpose(ctx, Qt.get(), q, M, Q.get(), M, ldq);
+    }
+
+    // small = Q^T (Sigma Q)
+    DevBuf<double> Z(static_cast<std::size_t>(M * ldq));
+    apply_sigma(Q.get(), Z.get(), 0, q);
+    DevBuf<double> small(static_cast<std::size_t>(q * q)), Vs(static_cast<std::size_t>(q * q));
+    gemm_tn(ctx, q, q, M, Q.get(), ldq, nullptr, Z.get(), ldq, small.get(), q, false);
+
+    DevBuf<double> evals(static_cast<std::size_t>(q));
+    DevBuf<int> info(static_cast<std::size_t>(q + 1));
+    const bool tri = q <= kEigMaxN;
+    if (tri) {
+      const std::size_t tsm = tri_eig_smem(static_cast<int>(q));
+      allow_smem(k_tri_eig, tsm);
+      DFPCA_LAUNCH(ctx, k_tri_eig, 1, kEigThreads, tsm, small.get(), static_cast<int>(q), evals.get(), Vs.get(),
+                   info.get());
+    } else {
+      const int np = static_cast<int>((q + 1) & ~1ll);
+      std::size_t jsmem = sizeof(double) * np * 2;
+      const bool jac_smem = jsmem + sizeof(double) * 2 * q * q <= 200 * 1024;
+      if (jac_smem) {
+        jsmem += sizeof(double) * 2 * q * q;
+        allow_smem(k_jacobi, jsmem);
+      }
+      DFPCA_LAUNCH(ctx, k_jacobi, 1, 1024, jsmem, small.get(), Vs.get(), static_cast<int>(q), evals.get(),
+                   info.get(), jac_smem ? 1 : 0);
+    }
+
+    // lifted = Q V  ([M][q]) -> Lt [q][M]
+    DevBuf<double> lifted(static_cast<std::size_t>(M * q)), Lt(static_cast<std::size_t>(M * q));
+    gemm_tn(ctx, M, q, q, Qt.get(), M, nullptr, Vs.get(), q, lifted.get(), q, false);
+    transpose(ctx, lifted.get(), M, q, Lt.get());
+
+    std::vector<double> tilde(static_cast<std::size_t>(q));
+    int jinfo = 0;
+    double hf[4] = {0.0, 0.0, 0.0, 0.0};
+    DFPCA_CUDA(cudaMemcpyAsync(tilde.data(), evals.get(), sizeof(double) * q, cudaMemcpyDeviceToHost, st));
+    DFPCA_CUDA(cudaMemcpyAsync(&jinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (cholqr) DFPCA_CUDA(cudaMemcpyAsync(hf, flags.get(), sizeof(hf), cudaMemcpyDeviceToHost, st));
     DFPCA_CUDA(cudaStreamSynchronize(st));
-    cholqr_ok = hf[0] == 0.0 && hf[2] == 0.0 && hf[3] < 0.1;
-    if (cholqr_ok) transpose(ctx, Q.get(), M, q, Qt.get(), ldq, M);
-  }
-  if (!cholqr_ok) {
-    DevBuf<double> Yt(static_cast<std::size_t>(M * q)), tau(static_cast<std::size_t>(q));
-    transpose(ctx, Y.get(), M, q, Yt.get(), ldq, M);
-    for (i64 j = -1; j < q - 1; ++j) {
-      const i64 cols = q - (j + 1);
-      DFPCA_LAUNCH(ctx, k_house_step, static_cast<unsigned>(cols), 512, 0, Yt.get(), M, q, j, tau.get());
-    }
-    DFPCA_LAUNCH(ctx, k_q_init, grid_for(M * q, 256), 256, 0, Qt.get(), M, q);
-    for (i64 j = q - 1; j >= 0; --j)
-      DFPCA_LAUNCH(ctx, k_q_apply, static_cast<unsigned>(q - j), 512, 0, Yt.get(), tau.get(), M, q, j,
-                   Qt.get());
-    transpose(ctx, Qt.get(), q, M, Q.get(), M, ldq);
-  }
+    if (cholqr && !(hf[0] == 0.0 && hf[2] == 0.0 && hf[3] < 0.1)) return false;
+    if (!tri && jinfo != 0) fail(kNumeric, "EigFailure", "projected eigensolver did not converge");
 
-  // small = Q^T (Sigma Q)
-  DevBuf<double> Z(static_cast<std::size_t>(M * ldq));
-  apply_sigma(Q.get(), Z.get(), 0, q);
-  DevBuf<double> small(static_cast<std::size_t>(q * q)), Vs(static_cast<std::size_t>(q * q));
-  gemm_tn(ctx, q, q, M, Q.get(), ldq, nullptr, Z.get(), ldq, small.get(), q, false);
-
-  DevBuf<double> evals(static_cast<std::size_t>(q));
-  DevBuf<int> info(static_cast<std::size_t>(q + 1));
-  const bool tri = q <= kEigMaxN;
-  if (tri) {
-    const std::size_t tsm = tri_eig_smem(static_cast<int>(q));
-    allow_smem(k_tri_eig, tsm);
-    DFPCA_LAUNCH(ctx, k_tri_eig, 1, kEigThreads, tsm, small.get(), static_cast<int>(q), evals.get(), Vs.get(),
-                 info.get());
-  } else {
-    const int np = static_cast<int>((q + 1) & ~1ll);
-    std::size_t jsmem = sizeof(double) * np * 2;
-    const bool jac_smem = jsmem + sizeof(double) * 2 * q * q <= 200 * 1024;
-    if (jac_smem) {
-      jsmem += sizeof(double) * 2 * q * q;
-      allow_smem(k_jacobi, jsmem);
-    }
-    DFPCA_LAUNCH(ctx, k_jacobi, 1, 1024, jsmem, small.get(), Vs.get(), static_cast<int>(q), evals.get(),
-                 info.get(), jac_smem ? 1 : 0);
-  }
-
-  // lifted = Q V  ([M][q]) -> Lt [q][M]
-  DevBuf<double> lifted(static_cast<std::size_t>(M * q)), Lt(static_cast<std::size_t>(M * q));
-  gemm_tn(ctx, M, q, q, Qt.get(), M, nullptr, Vs.get(), q, lifted.get(), q, false);
-  transpose(ctx, lifted.get(), M, q, Lt.get());
-
-  std::vector<double> tilde(static_cast<std::size_t>(q));
-  int jinfo = 0;
-  DFPCA_CUDA(cudaMemcpyAsync(tilde.data(), evals.get(), sizeof(double) * q, cudaMemcpyDeviceToHost, st));
-  DFPCA_CUDA(cudaMemcpyAsync(&jinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
-  DFPCA_CUDA(cudaStreamSynchronize(st));
-  if (!tri && jinfo != 0) fail(kNumeric, "EigFailure", "projected eigensolver did not converge");
-
-  finish_eigensystem(ctx, grid, mv.node_of_row, M, Lt.get(), evals.get(), tilde, L_max, true, eigenvalues,
-                     eigenfunctions, fve, total_variance, n_components);
+    finish_eigensystem(ctx, grid, mv.node_of_row, M, Lt.get(), evals.get(), tilde, L_max, true, eigenvalues,
+                       eigenfunctions, fve, total_variance, n_components);
+    return true;
+  };
+  if (!(q <= kCqMaxQ && from_Y(true))) from_Y(false);
 }
 
 

@@ -818,13 +818,13 @@ class MatrixizedCovariance:
     def __init__(self, cov: SurfaceEstimate, dense_budget: int):
         g = cov.grid
         self.cov = cov
-        self.row_of_node = [-1] * g.size()
-        self.node_of_row = []
-        for f in range(g.size()):
-            if g.in_mask(f):
-                self.row_of_node[f] = len(self.node_of_row)
-                self.node_of_row.append(f)
-        self.m = len(self.node_of_row)
+        mask = g.mask()
+        nodes = np.arange(g.size(), dtype=np.int64) if mask is None else np.flatnonzero(np.asarray(mask) != 0)
+        rows = np.full(g.size(), -1, dtype=np.int64)
+        rows[nodes] = np.arange(nodes.size, dtype=np.int64)
+        self.node_of_row = nodes  # int64 arrays (eigensolve.hpp:33-68 keeps std::vector<Index>)
+        self.row_of_node = rows
+        self.m = int(nodes.size)
         self.dense = self.m * self.m * 8 <= dense_budget
 
     @property

@@ -406,11 +406,12 @@ constexpr int kCqMaxQ = 128;
 // a 256-thread column-oriented variant (87 vs 150 / 137 us at q = 99): the
 // factorization is bound by its pivot chain, and more warps hide it better.
 __global__ void __launch_bounds__(1024) k_chol_factor(const double* __restrict__ Gg, int q, double* __restrict__ Rg,
-                                                      double* __restrict__ flags) {
+                                                      double* __restrict__ flags, double shift_scale) {
   extern __shared__ double sm[];
   const int ld = q + 1;
   double* R = sm;
   __shared__ double red[32];
+  __shared__ double shift;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   double dmax = 0.0;
   for (int e = tid; e < q * q; e += blockDim.x) {
@@ -428,7 +429,18 @@ __global__ void __launch_bounds__(1024) k_chol_factor(const double* __restrict__
     for (int w = 0; w < nw; ++w) m = fmax(m, red[w]);
     flags[1] = m;
     flags[0] = 0.0;
+    // shifted Cholesky QR (Fukaya et al. 2020): G + s I with
+    // s = 11 (M q + q (q + 1)) u ||X||_F^2 makes the factorization succeed for
+    // sketches up to cond ~ 1/u; two more unshifted passes restore
+    // orthogonality
+    double tr = 0.0;
+    for (int i = 0; i < q; ++i) tr += R[i * ld + i];
+    shift = shift_scale * tr;
   }
+  __syncthreads();
+  if (shift_scale > 0.0)
+    for (int i = tid; i < q; i += blockDim.x) R[i * ld + i] += shift;
+  __syncthreads();
   for (int k = 0; k < q; ++k) {
     const double d = R[k * ld + k];
     if (!(d > 0.0) || !isfinite(d)) {
@@ -514,7 +526,9 @@ std::size_t trsm_smem(int q) { return sizeof(double) * (static_cast<std::size_t>
 //   per cluster with reorthogonalization inside clusters (dstein's rule:
 //   gaps below 1e-3 |T|), then back-transformed by the reflectors.
 // Outputs: evals descending [n]; V [n][n] row-major, column c = eigenvector
-// of evals[c] (zero for non-candidates); info[0] = candidate count.
+// of evals[c] for the leading min(candidates, max_vec) (zero otherwise);
+// info[0] = candidate count, info[1] = vectors computed; Vt [n][n] scratch
+// (the tridiagonal eigenvectors as rows: coalesced reorthogonalization).
 constexpr int kEigMaxN = 128;
 constexpr int kEigThreads = 512;
 constexpr int kEigGroups = kEigThreads / kEigMaxN;  // row groups per column
@@ -563,7 +577,8 @@ struct TriWork {  // one warp's inverse-iteration workspace
 
 __global__ void __launch_bounds__(kEigThreads) k_tri_eig(const double* __restrict__ Bg, int n,
                                                           double* __restrict__ evals_out, double* __restrict__ V,
-                                                          int* __restrict__ info) {
+                                                          int* __restrict__ info, int max_vec,
+                                                          double* __restrict__ Vt) {
   extern __shared__ double sm[];
   double* Hv = sm;                    // [n][kEigMaxN] reflector vectors (row k: v of H_k)
   double* d = Hv + n * kEigMaxN;      // diagonal
@@ -576,7 +591,8 @@ __global__ void __launch_bounds__(kEigThreads) k_tri_eig(const double* __restric
   double* lam = pp + kEigGroups * kEigMaxN;  // ascending eigenvalues
   double* xk = lam + kEigMaxN;        // column k of the current step
   TriWork* work = reinterpret_cast<TriWork*>(xk + kEigMaxN);
-  __shared__ int n_cand, n_neg, n_clusters, cl_start[kEigMaxN + 1];
+  double* btx = reinterpret_cast<double*>(work + kEigIIWarps);  // [kEigWarps][kEigMaxN] back-transform rows
+  __shared__ int n_cand, n_vec, n_neg, n_clusters, cl_start[kEigMaxN + 1];
   __shared__ double tnorm_s, pivmin_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int col = tid & (kEigMaxN - 1), grp = tid / kEigMaxN;  // thread (column, row group)
@@ -775,21 +791,27 @@ __global__ void __launch_bounds__(kEigThreads) k_tri_eig(const double* __restric
   __syncthreads();
 
   // ---- clusters of the candidates (descending order c = n-1-j)
+  // Vectors only for the leading max_vec candidates: the finalization keeps
+  // at most L_max of them (the caller passes L_max plus a margin for skipped
+  // ones, and asks again with max_vec = n when that was not enough).
   if (tid == 0) {
     const int nc = n_cand;
+    const int nv = nc < max_vec ? nc : max_vec;
     int ncl = 0;
-    for (int c = 0; c < nc; ++c) {
+    for (int c = 0; c < nv; ++c) {
       if (c == 0 || !(fabs(lam[n - 1 - c] - lam[n - c]) <= 1e-3 * tnorm)) cl_start[ncl++] = c;
     }
-    cl_start[ncl] = nc;
+    cl_start[ncl] = nv;
     n_clusters = ncl;
+    n_vec = nv;
     // the non-candidates are never read (finalize stops at the cut): zero
     for (int c = 0; c < n; ++c) evals_out[c] = c < nc ? lam[n - 1 - c] : 0.0;
     info[0] = nc;
+    info[1] = nv;
   }
   __syncthreads();
   for (int e_ = tid; e_ < n * n; e_ += blockDim.x)
-    if (e_ % n >= n_cand) V[e_] = 0.0;
+    if (e_ % n >= n_vec) V[e_] = 0.0;
 
   // ---- inverse iteration, one warp per cluster (members in order); the
   // T-eigenvectors of a cluster stay in V's columns until the cluster is done
@@ -872,11 +894,12 @@ __global__ void __launch_bounds__(kEigThreads) k_tri_eig(const double* __restric
             }
           }
           __syncwarp();
-          for (int c2 = c0; c2 < c; ++c2) {  // orthogonalize against earlier members
+          for (int c2 = c0; c2 < c; ++c2) {  // orthogonalize against earlier members (rows of Vt)
+            const double* u = Vt + static_cast<i64>(c2) * n;
             double s = 0.0;
-            for (int i = lane; i < n; i += 32) s += w.x[i] * V[i * n + c2];
+            for (int i = lane; i < n; i += 32) s += w.x[i] * u[i];
             s = warp_sum(s);
-            for (int i = lane; i < n; i += 32) w.x[i] -= s * V[i * n + c2];
+            for (int i = lane; i < n; i += 32) w.x[i] -= s * u[i];
             __syncwarp();
           }
           double s2 = 0.0;
@@ -885,27 +908,31 @@ __global__ void __launch_bounds__(kEigThreads) k_tri_eig(const double* __restric
           for (int i = lane; i < n; i += 32) w.x[i] *= inv;
           __syncwarp();
         }
-        for (int i = lane; i < n; i += 32) V[i * n + c] = w.x[i];
+        for (int i = lane; i < n; i += 32) Vt[static_cast<i64>(c) * n + i] = w.x[i];
         __syncwarp();
       }
-      // back-transform the cluster's vectors: z <- H_0 ... H_{n-3} z
-      for (int c = c0; c < c1; ++c) {
-        for (int i = lane; i < n; i += 32) w.x[i] = V[i * n + c];
-        __syncwarp();
-        for (int k = n - 3; k >= 0; --k) {
-          const double t = tau[k];
-          if (t == 0.0) continue;
-          const int m = n - k - 1;
-          const double* hv = Hv + k * kEigMaxN + k + 1;  // v_i = hv[i], v_0 = 1
-          double s = 0.0;
-          for (int i = lane; i < m; i += 32) s += hv[i] * w.x[k + 1 + i];
-          s = t * warp_sum(s);
-          for (int i = lane; i < m; i += 32) w.x[k + 1 + i] -= s * hv[i];
-          __syncwarp();
-        }
-        for (int i = lane; i < n; i += 32) V[i * n + c] = w.x[i];
+    }
+  }
+  __syncthreads();
+  // ---- back-transform every vector: z <- H_0 ... H_{n-3} z (a warp per vector)
+  {
+    double* x = btx + warp * kEigMaxN;
+    for (int c = warp; c < n_vec; c += kEigWarps) {
+      for (int i = lane; i < n; i += 32) x[i] = Vt[static_cast<i64>(c) * n + i];
+      __syncwarp();
+      for (int k = n - 3; k >= 0; --k) {
+        const double t = tau[k];
+        if (t == 0.0) continue;
+        const int m = n - k - 1;
+        const double* hv = Hv + k * kEigMaxN + k + 1;  // v_i = hv[i], v_0 = 1
+        double sdot = 0.0;
+        for (int i = lane; i < m; i += 32) sdot += hv[i] * x[k + 1 + i];
+        sdot = t * warp_sum(sdot);
+        for (int i = lane; i < m; i += 32) x[k + 1 + i] -= sdot * hv[i];
         __syncwarp();
       }
+      for (int i = lane; i < n; i += 32) V[i * n + c] = x[i];
+      __syncwarp();
     }
   }
   __syncthreads();
@@ -913,7 +940,7 @@ __global__ void __launch_bounds__(kEigThreads) k_tri_eig(const double* __restric
 
 std::size_t tri_eig_smem(int n) {
   return sizeof(double) * (static_cast<std::size_t>(n) * kEigMaxN + (8 + kEigGroups) * kEigMaxN) +
-         sizeof(TriWork) * kEigIIWarps;
+         sizeof(TriWork) * kEigIIWarps + sizeof(double) * kEigWarps * kEigMaxN;
 }
 
 // ---------------------------------------------------------- finalize ----
@@ -922,12 +949,18 @@ std::size_t tri_eig_smem(int n) {
 __global__ void __launch_bounds__(1024) k_finalize(const double* __restrict__ Lt, const double* __restrict__ tilde,
                                                    i64 M, int q, int L_max, double cut, double cv,
                                                    double* __restrict__ kept, int* __restrict__ kept_src,
-                                                   int* __restrict__ n_kept, int gram_schmidt) {
+                                                   int* __restrict__ n_kept, int gram_schmidt, int n_avail,
+                                                   int* __restrict__ exhausted) {
   __shared__ double red[33];
   __shared__ i64 first_nz;
   int nk = 0;
+  if (threadIdx.x == 0) *exhausted = 0;
   for (int l = 0; l < q && nk < L_max; ++l) {
     if (!(tilde[l] > cut)) break;
+    if (l >= n_avail) {  // a candidate without a computed vector: the caller recomputes them all
+      if (threadIdx.x == 0) *exhausted = 1;
+      break;
+    }
     double* v = kept + static_cast<i64>(nk) * M;
     for (i64 i = threadIdx.x; i < M; i += blockDim.x) v[i] = Lt[static_cast<i64>(l) * M + i];
     __syncthreads();
@@ -1079,10 +1112,12 @@ static RowShard shard_rows_dev(dfpca_context* ctx, Transport& tr, const dfpca_su
 
 // finalize_eigensystem (eigensolve.hpp:146-194) on the device: candidates Lt
 // [q][M] in descending order of tilde (host copy tilde_h, device tilde_d).
-static void finish_eigensystem(dfpca_context* ctx, const Grid& grid, const std::vector<i64>& node_of_row, i64 M,
+// Returns false (nothing written) when a kept candidate had no computed
+// vector (n_avail < the candidates the finalization reached).
+static bool finish_eigensystem(dfpca_context* ctx, const Grid& grid, const std::vector<i64>& node_of_row, i64 M,
                                const double* Lt, const double* tilde_d, const std::vector<double>& tilde,
                                i64 L_max, bool gram_schmidt, double* eigenvalues, double* eigenfunctions,
-                               double* fve, double* total_variance, i64* n_components) {
+                               double* fve, double* total_variance, i64* n_components, i64 n_avail = -1) {
   cudaStream_t st = ctx->stream;
   const i64 q = static_cast<i64>(tilde.size());
   const double cv = grid.cell_volume();
@@ -1093,12 +1128,15 @@ static void finish_eigensystem(dfpca_context* ctx, const Grid& grid, const std::
   const double total = tilde_total * cv;
 
   DevBuf<double> kept(static_cast<std::size_t>(std::max<i64>(L_max, 1) * M));
-  DevBuf<int> kept_src(static_cast<std::size_t>(std::max<i64>(L_max, 1))), nkept(1);
+  DevBuf<int> kept_src(static_cast<std::size_t>(std::max<i64>(L_max, 1))), nkept(2);
   DFPCA_LAUNCH(ctx, k_finalize, 1, 1024, 0, Lt, tilde_d, M, static_cast<int>(q), static_cast<int>(L_max), cut,
-               cv, kept.get(), kept_src.get(), nkept.get(), gram_schmidt ? 1 : 0);
-  int nk = 0;
-  DFPCA_CUDA(cudaMemcpyAsync(&nk, nkept.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+               cv, kept.get(), kept_src.get(), nkept.get(), gram_schmidt ? 1 : 0,
+               static_cast<int>(n_avail < 0 ? q : n_avail), nkept.get() + 1);
+  int nk2[2] = {0, 0};
+  DFPCA_CUDA(cudaMemcpyAsync(nk2, nkept.get(), sizeof(nk2), cudaMemcpyDeviceToHost, st));
   DFPCA_CUDA(cudaStreamSynchronize(st));
+  if (nk2[1] != 0) return false;
+  const int nk = nk2[0];
   std::vector<int> src(static_cast<std::size_t>(std::max(nk, 1)));
   std::vector<double> kv(static_cast<std::size_t>(nk) * M);
   if (nk > 0) {
@@ -1123,6 +1161,7 @@ static void finish_eigensystem(dfpca_context* ctx, const Grid& grid, const std::
   }
   if (total_variance) *total_variance = total;
   if (n_components) *n_components = nk;
+  return true;
 }
 
 
@@ -1243,26 +1282,34 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
   // sketches) Householder QR, one reflector per launch.
   // The Cholesky-QR acceptance flags are read at the stage's one host sync
   // (with the Ritz values), so nothing waits in between; a rejected sketch
-  // reruns the rest from Y with Householder QR.
-  auto from_Y = [&](bool cholqr) -> bool {
-    DevBuf<double> Q(static_cast<std::size_t>(M * ldq)), Qt(static_cast<std::size_t>(M * q)), flags(4);
+  // reruns the rest from Y with shifted Cholesky QR, then Householder QR.
+  // mode 0: Cholesky QR twice; 1: shifted Cholesky QR three times (sketches
+  // too ill-conditioned for mode 0, cond up to ~1/u); 2: Householder QR
+  auto from_Y = [&](int mode) -> bool {
+    const bool cholqr = mode < 2;
+    DevBuf<double> Q(static_cast<std::size_t>(M * ldq)), Qt(static_cast<std::size_t>(M * q)), flags(8);
     if (cholqr) {
       DevBuf<double> G(static_cast<std::size_t>(q * q)), R(static_cast<std::size_t>(q * q)),
-          Q1(static_cast<std::size_t>(M * ldq));
+          Qa(static_cast<std::size_t>(M * ldq)), Qb(static_cast<std::size_t>(M * ldq));
       const int qi = static_cast<int>(q);
       const std::size_t fsm = sizeof(double) * q * (q + 1), tsm = trsm_smem(qi);
       allow_smem(k_chol_factor, fsm);
       allow_smem(k_row_trsm, tsm);
       const unsigned ctas =
           static_cast<unsigned>(std::min<i64>((M + kTrsmWarps - 1) / kTrsmWarps, 2 * ctx->sm_count));
-      gemm_tn(ctx, q, q, M, Y.get(), ldq, nullptr, Y.get(), ldq, G.get(), q, false);
-      DFPCA_LAUNCH(ctx, k_chol_factor, 1, 1024, fsm, G.get(), qi, R.get(), flags.get());
-      DFPCA_LAUNCH(ctx, k_row_trsm, ctas, kTrsmWarps * 32, tsm, Y.get(), M, qi, ldq, R.get(), flags.get(),
-                   Q1.get());
-      gemm_tn(ctx, q, q, M, Q1.get(), ldq, nullptr, Q1.get(), ldq, G.get(), q, false);
-      DFPCA_LAUNCH(ctx, k_chol_factor, 1, 1024, fsm, G.get(), qi, R.get(), flags.get() + 2);
-      DFPCA_LAUNCH(ctx, k_row_trsm, ctas, kTrsmWarps * 32, tsm, Q1.get(), M, qi, ldq, R.get(), flags.get() + 2,
-                   Q.get());
+      const int passes = mode == 0 ? 2 : 3;
+      const double shift_scale =
+          11.0 * (static_cast<double>(M) * q + static_cast<double>(q) * (q + 1)) * 1.1102230246251565e-16;
+      const double* src = Y.get();
+      for (int ps = 0; ps < passes; ++ps) {
+        double* dst = ps == passes - 1 ? Q.get() : (ps % 2 == 0 ? Qa.get() : Qb.get());
+        gemm_tn(ctx, q, q, M, src, ldq, nullptr, src, ldq, G.get(), q, false);
+        DFPCA_LAUNCH(ctx, k_chol_factor, 1, 1024, fsm, G.get(), qi, R.get(), flags.get() + 2 * ps,
+                     mode == 1 && ps == 0 ? shift_scale : 0.0);
+        DFPCA_LAUNCH(ctx, k_row_trsm, ctas, kTrsmWarps * 32, tsm, src, M, qi, ldq, R.get(), flags.get() + 2 * ps,
+                     dst);
+        src = dst;
+      }
       transpose(ctx, Q.get(), M, q, Qt.get(), ldq, M);
     } else {
       DevBuf<double> Yt(static_cast<std::size_t>(M * q)), tau(static_cast<std::size_t>(q));
@@ -1284,14 +1331,20 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
     DevBuf<double> small(static_cast<std::size_t>(q * q)), Vs(static_cast<std::size_t>(q * q));
     gemm_tn(ctx, q, q, M, Q.get(), ldq, nullptr, Z.get(), ldq, small.get(), q, false);
 
-    DevBuf<double> evals(static_cast<std::size_t>(q));
-    DevBuf<int> info(static_cast<std::size_t>(q + 1));
+    DevBuf<double> evals(static_cast<std::size_t>(q)), Vt(static_cast<std::size_t>(q * q));
+    DevBuf<int> info(static_cast<std::size_t>(q + 2));
     const bool tri = q <= kEigMaxN;
-    if (tri) {
+    // vectors for the leading L_max + 4 candidates (more only if the
+    // finalization skips that many: then all of them, below)
+    i64 max_vec = std::min<i64>(q, L_max + 4);
+    auto tri_eig = [&](i64 mv_) {
       const std::size_t tsm = tri_eig_smem(static_cast<int>(q));
       allow_smem(k_tri_eig, tsm);
       DFPCA_LAUNCH(ctx, k_tri_eig, 1, kEigThreads, tsm, small.get(), static_cast<int>(q), evals.get(), Vs.get(),
-                   info.get());
+                   info.get(), static_cast<int>(mv_), Vt.get());
+    };
+    if (tri) {
+      tri_eig(max_vec);
     } else {
       const int np = static_cast<int>((q + 1) & ~1ll);
       std::size_t jsmem = sizeof(double) * np * 2;
@@ -1311,19 +1364,33 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
 
     std::vector<double> tilde(static_cast<std::size_t>(q));
     int jinfo = 0;
-    double hf[4] = {0.0, 0.0, 0.0, 0.0};
+    double hf[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     DFPCA_CUDA(cudaMemcpyAsync(tilde.data(), evals.get(), sizeof(double) * q, cudaMemcpyDeviceToHost, st));
     DFPCA_CUDA(cudaMemcpyAsync(&jinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
     if (cholqr) DFPCA_CUDA(cudaMemcpyAsync(hf, flags.get(), sizeof(hf), cudaMemcpyDeviceToHost, st));
     DFPCA_CUDA(cudaStreamSynchronize(st));
-    if (cholqr && !(hf[0] == 0.0 && hf[2] == 0.0 && hf[3] < 0.1)) return false;
+    if (cholqr) {
+      // every factorization succeeded and the last pass started within 0.1
+      // of orthonormal columns (so it restored orthogonality to rounding)
+      const int passes = mode == 0 ? 2 : 3;
+      bool ok = true;
+      for (int ps = 0; ps < passes; ++ps) ok = ok && hf[2 * ps] == 0.0;
+      if (!(ok && hf[2 * (passes - 1) + 1] < 0.1)) return false;
+    }
     if (!tri && jinfo != 0) fail(kNumeric, "EigFailure", "projected eigensolver did not converge");
 
-    finish_eigensystem(ctx, grid, mv.node_of_row, M, Lt.get(), evals.get(), tilde, L_max, true, eigenvalues,
-                       eigenfunctions, fve, total_variance, n_components);
+    if (!finish_eigensystem(ctx, grid, mv.node_of_row, M, Lt.get(), evals.get(), tilde, L_max, true, eigenvalues,
+                            eigenfunctions, fve, total_variance, n_components, tri ? max_vec : q)) {
+      // more candidates were skipped than the margin covered: all vectors
+      tri_eig(q);
+      gemm_tn(ctx, M, q, q, Qt.get(), M, nullptr, Vs.get(), q, lifted.get(), q, false);
+      transpose(ctx, lifted.get(), M, q, Lt.get());
+      finish_eigensystem(ctx, grid, mv.node_of_row, M, Lt.get(), evals.get(), tilde, L_max, true, eigenvalues,
+                         eigenfunctions, fve, total_variance, n_components);
+    }
     return true;
   };
-  if (!(q <= kCqMaxQ && from_Y(true))) from_Y(false);
+  if (!(q <= kCqMaxQ && (from_Y(0) || from_Y(1)))) from_Y(2);
 }
 
 

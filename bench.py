@@ -441,8 +441,15 @@ def main():
     ap.add_argument("--workload", choices=["covariance", "io"], default="covariance",
                     help="io: the long-format table reader (SURVEY.md 8(f) rank 2)")
     ap.add_argument("--cpu-io-subjects", type=int, default=200)
+    ap.add_argument("--h", type=float, default=None,
+                    help="bandwidth override (configs[2] is quoted at h = 0.1; SURVEY.md 8(d) also times 0.3, "
+                         "R = 20, the reference's FFT path)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.h is not None:
+        global H, WORKLOAD
+        H = args.h
+        WORKLOAD = WORKLOAD.replace("h=0.1 (R=7)", f"h={H} (R={int(np.ceil(H * CELLS))})")
 
     if args.workload == "io":
         if args.impl == "reference":

@@ -214,7 +214,13 @@ struct SharedMoments {
   int band[kMaxDim];         // D_k(x, y) == 0 exactly when |x - y| > band[k] (= R_s + R_t)
   float inv_n[kMaxDim];      // 1 / n_k for fast_divmod
   double sw, dm0;
+  // per-node tables for k_solve_sep_tri (null when an axis exceeds kCoordMask)
+  const double* P = nullptr;         // [SepIdx<d>::n][G]: P_a(u) = prod_k A^k_{a_k}(u_k)
+  const unsigned* coord = nullptr;   // [G]: axis coordinates, kCoordBits each
+  i64 G = 0;
 };
+constexpr int kCoordBits = 10;
+constexpr unsigned kCoordMask = (1u << kCoordBits) - 1;
 
 template <int P>
 __device__ __forceinline__ double shared_moment(const int (&o)[P], const double (&As)[P / 2][3],
@@ -410,6 +416,9 @@ __global__ void __launch_bounds__(kSolveTile) k_solve_tri(MomPtrs mp, SolveGeom 
                                                           i64* __restrict__ empty_list, i64 list_cap) {
   solve_tri_body<N, false>(SharedMoments{}, mp, g, nch, out, empty_count, empty_list, list_cap);
 }
+#ifndef DFPCA_SOLVE5_MIN_CTAS
+#define DFPCA_SOLVE5_MIN_CTAS 8
+#endif
 #ifndef DFPCA_SOLVE_MIN_CTAS
 #define DFPCA_SOLVE_MIN_CTAS 1
 #endif
@@ -486,71 +495,20 @@ __device__ __forceinline__ void fast_divmod(int x, int n, float inv_n, int& q, i
   }
 }
 
+// S (MomentBasis order, local_fit.hpp:34-47: covariates 0..d-1 are the s
+// axes, d..2d-1 the t axes) of node pair (s, t) from the per-node products
+// Ps = P(s), Pt = P(t) and packed axis coordinates cs, ct.  Raw products, the
+// weight applied last: S = sw (P_s P_t), so moments that are mirror images of
+// each other (s <-> t, or axis k <-> l at interior nodes) round identically
+// and tie exactly in the exact path's pivot order.
 template <int N>
-__global__ void __launch_bounds__(kSolveTile, N == 5 ? 8 : DFPCA_SOLVE_MIN_CTAS)
-    k_solve_sep_tri(SharedMoments sh, MomPtrs mp, SolveGeom g, double* __restrict__ out,
-                    unsigned long long* __restrict__ empty_count, i64* __restrict__ empty_list, i64 list_cap) {
+__device__ __forceinline__ void sep_assemble(const SharedMoments& sh, const double (&Ps)[SepIdx<(N - 1) / 2>::n],
+                                             const double (&Pt)[SepIdx<(N - 1) / 2>::n], unsigned cs, unsigned ct,
+                                             double (&S)[1 + (N - 1) + (N - 1) * N / 2]) {
   constexpr int p = N - 1;
   constexpr int d = p / 2;
-  constexpr int nm = 1 + p + p * (p + 1) / 2;
-  constexpr int nl = 1 + p;
   using I = SepIdx<d>;
-  const int lrow = static_cast<int>(blockIdx.y);  // grid: (column chunks, rows)
-  const int ch = static_cast<int>(blockIdx.x);
-  const int tc = static_cast<int>(g.tc);
-  const int t0 = static_cast<int>(g.t0);
-  const int mrow = lrow + static_cast<int>(g.row_lo);
-  const int row = mrow + static_cast<int>(g.row0);
-  if (t0 + (ch + 1) * kSolveTile <= row) return;
-  const int c = ch * kSolveTile + static_cast<int>(threadIdx.x);
-  const int col = t0 + c;
-  if (c >= tc || col < row) return;
-  const i64 e = static_cast<i64>(mrow) * tc + c;
-  const i64 dst = static_cast<i64>(row - g.out_row0) * g.gt + col;
-  if (g.mask && !(g.mask[row] != 0 && g.mask[col] != 0)) {
-    out[dst] = __longlong_as_double(0x7ff8000000000000ll);
-    return;
-  }
-  double T[nl];
-#pragma unroll
-  for (int i = 0; i < nl; ++i) T[i] = mp.T[i][e];  // issue the moment loads first
-  int sk[d], tk[d];
-  {
-    int rs = row, rt = col;
-#pragma unroll
-    for (int k = d - 1; k >= 0; --k) {
-      const int n = sh.n[k];
-      const float inv = sh.inv_n[k];
-      int qs, qt;
-      fast_divmod(rs, n, inv, qs, sk[k]);
-      fast_divmod(rt, n, inv, qt, tk[k]);
-      rs = qs;
-      rt = qt;
-    }
-  }
-  double as[d][3], at[d][3];
-  bool near = true;
-#pragma unroll
-  for (int k = 0; k < d; ++k) {
-    const int n = sh.n[k];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      as[k][r] = __ldg(sh.A[k] + r * n + sk[k]);
-      at[k][r] = __ldg(sh.A[k] + r * n + tk[k]);
-    }
-    const int dist = sk[k] > tk[k] ? sk[k] - tk[k] : tk[k] - sk[k];
-    near = near && dist <= sh.band[k];
-  }
-  // raw products, the weight applied last: S = sw (P_s P_t), so moments
-  // that are mirror images of each other (s <-> t, or axis k <-> l at
-  // interior nodes) round identically and tie exactly in the pivot order
-  double Ps[I::n], Pt[I::n];
-  sep_products<N>(as, Ps, 1.0);
-  sep_products<N>(at, Pt, 1.0);
   const double sw = sh.sw;
-  // S in MomentBasis order (local_fit.hpp:34-47): covariates 0..d-1 are the
-  // s axes, d..2d-1 the t axes
-  double S[nm];
   S[0] = sw * (Ps[0] * Pt[0]);
 #pragma unroll
   for (int k = 0; k < p; ++k) S[1 + k] = sw * (k < d ? Ps[I::one(k)] * Pt[0] : Ps[0] * Pt[I::one(k - d)]);
@@ -564,6 +522,15 @@ __global__ void __launch_bounds__(kSolveTile, N == 5 ? 8 : DFPCA_SOLVE_MIN_CTAS)
       else v = Ps[I::one(k)] * Pt[I::one(l - d)];
       S[quad_index(p, k, l)] = sw * v;
     }
+  int sk[d], tk[d];
+  bool near = true;
+#pragma unroll
+  for (int k = 0; k < d; ++k) {
+    sk[k] = static_cast<int>((cs >> (kCoordBits * k)) & kCoordMask);
+    tk[k] = static_cast<int>((ct >> (kCoordBits * k)) & kCoordMask);
+    const int dist = sk[k] > tk[k] ? sk[k] - tk[k] : tk[k] - sk[k];
+    near = near && dist <= sh.band[k];
+  }
   if (near) {
     // the same-observation band (exact zero outside it)
     double Dst[d][3][3];
@@ -602,10 +569,49 @@ __global__ void __launch_bounds__(kSolveTile, N == 5 ? 8 : DFPCA_SOLVE_MIN_CTAS)
         S[quad_index(p, k, l)] -= band(o);
       }
   }
-  double b0;
-  int st;
-  // pivot order check on the ridged diagonal (Eigen: first largest |.|)
-  double dg[N];
+}
+
+// The per-node product table is interleaved, [G][sep_stride(d)] with the row
+// padded to whole 16-byte pairs: one node's products are sep_stride / 2
+// 128-bit loads (uniform for the row node, lane-contiguous for the columns).
+__host__ __device__ constexpr int sep_stride(int d) { return ((d + 1) * (d + 2) / 2 + 1) & ~1; }
+
+template <int N>
+__device__ __forceinline__ void sep_load(const SharedMoments& sh, int node, double (&P)[SepIdx<(N - 1) / 2>::n]) {
+  constexpr int np = SepIdx<(N - 1) / 2>::n;
+  constexpr int ns = sep_stride((N - 1) / 2);
+  const double2* q = reinterpret_cast<const double2*>(sh.P + static_cast<i64>(node) * ns);
+#pragma unroll
+  for (int i = 0; i < ns / 2; ++i) {
+    const double2 v = __ldg(q + i);
+    P[2 * i] = v.x;
+    if (2 * i + 1 < np) P[2 * i + 1] = v.y;
+  }
+}
+
+// Node of the tiled upper-triangle solve handled by thread `tid` of CTA
+// (ch, lrow); false when the thread has no node.
+struct SepNode {
+  int row, col, c;
+  i64 e, dst;
+};
+__device__ __forceinline__ bool sep_node(const SolveGeom& g, int lrow, int ch, int tid, SepNode& n) {
+  const int tc = static_cast<int>(g.tc);
+  const int t0 = static_cast<int>(g.t0);
+  const int mrow = lrow + static_cast<int>(g.row_lo);
+  n.row = mrow + static_cast<int>(g.row0);
+  n.c = ch * kSolveTile + tid;
+  n.col = t0 + n.c;
+  if (n.c >= tc || n.col < n.row) return false;
+  n.e = static_cast<i64>(mrow) * tc + n.c;
+  n.dst = static_cast<i64>(n.row - g.out_row0) * g.gt + n.col;
+  return true;
+}
+
+// The ridged diagonal (eps = kRidgeScale trace, local_fit.hpp:70-71).
+template <int N>
+__device__ __forceinline__ void ridged_diagonal(const double (&S)[1 + (N - 1) + (N - 1) * N / 2], double (&dg)[N]) {
+  constexpr int p = N - 1;
   dg[0] = S[0];
 #pragma unroll
   for (int k = 0; k < p; ++k) dg[k + 1] = S[quad_index(p, k, k)];
@@ -613,25 +619,94 @@ __global__ void __launch_bounds__(kSolveTile, N == 5 ? 8 : DFPCA_SOLVE_MIN_CTAS)
 #pragma unroll
   for (int i = 0; i < N; ++i) tr += dg[i];
   const double eps = 1e-10 * tr;
-  bool ordered = S[0] > 0.0;
 #pragma unroll
-  for (int i = 0; i < N; ++i) {
-    dg[i] += eps;
+  for (int i = 0; i < N; ++i) dg[i] += eps;
+}
+
+// Shared-design covariance solve over the upper triangle, one CTA per
+// (row, 128-column chunk): the mass moments are assembled from the per-node
+// product table (uniform for the row, 128-bit loads for the columns), the
+// value moments read from the pipeline, and the ridged system solved by the
+// certified fast path (ldlt_certified).  Windows it cannot certify
+// (near-singular, empty, non-SPD) are flagged in `pending` (one bit per node,
+// word lrow * ceil(tc / 32) + c / 32, zeroed by the caller) for
+// k_solve_sep_exact, so this kernel carries no register or code for them.
+template <int N>
+__global__ void __launch_bounds__(kSolveTile, N == 5 ? DFPCA_SOLVE5_MIN_CTAS : DFPCA_SOLVE_MIN_CTAS)
+    k_solve_sep_tri(SharedMoments sh, MomPtrs mp, SolveGeom g, double* __restrict__ out,
+                    unsigned* __restrict__ pending) {
+  constexpr int p = N - 1;
+  constexpr int d = p / 2;
+  constexpr int nm = 1 + p + p * (p + 1) / 2;
+  constexpr int nl = 1 + p;
+  const int lrow = static_cast<int>(blockIdx.y);  // grid: (column chunks, rows)
+  const int ch = static_cast<int>(blockIdx.x);
+  if (g.t0 + (ch + 1) * kSolveTile <= lrow + g.row_lo + g.row0) return;
+  SepNode n;
+  if (!sep_node(g, lrow, ch, static_cast<int>(threadIdx.x), n)) return;
+  if (g.mask && !(g.mask[n.row] != 0 && g.mask[n.col] != 0)) {
+    out[n.dst] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  double T[nl];
 #pragma unroll
-    for (int j = 0; j < i; ++j) ordered = ordered && !(fabs(dg[i]) > fabs(dg[j]));
+  for (int i = 0; i < nl; ++i) T[i] = mp.T[i][n.e];  // issue the moment loads first
+  double Ps[SepIdx<d>::n], Pt[SepIdx<d>::n];
+  sep_load<N>(sh, n.row, Ps);
+  sep_load<N>(sh, n.col, Pt);
+  double S[nm];
+  sep_assemble<N>(sh, Ps, Pt, __ldg(sh.coord + n.row), __ldg(sh.coord + n.col), S);
+  double dg[N], b0;
+  ridged_diagonal<N>(S, dg);
+  const bool done = ldlt_certified<N>(S, T, dg, b0);
+  if (done) out[n.dst] = b0;
+  const unsigned miss = __ballot_sync(__activemask(), !done);
+  if (miss != 0 && (threadIdx.x & 31) == __ffs(__activemask()) - 1) {
+    const i64 wpr = (g.tc + 31) / 32;
+    pending[lrow * wpr + (n.c >> 5)] = miss;
   }
-  if (ordered) {
-    st = ldlt_identity<N>(S, T, dg, b0);
-  } else {
-    __shared__ double sm_solve[(nm + nl) * kSolveTile];
-    st = solve_local_perm<N>(S, T, sm_solve + threadIdx.x, kSolveTile, b0);
-  }
-  if (st == kFitEmpty) {
-    const unsigned long long slot = atomicAdd(empty_count, 1ull);
-    if (static_cast<i64>(slot) < list_cap) empty_list[slot] = dst;
-    out[dst] = __longlong_as_double(0x7ff8000000000000ll);
-  } else {
-    out[dst] = b0;
+}
+
+// The windows k_solve_sep_tri flagged: Eigen's pivoted LDLT replayed exactly
+// (solve_local_perm), the local-constant fallback and the empty-window list.
+// One thread per bitmap word.
+template <int N>
+__global__ void __launch_bounds__(kSolveTile) k_solve_sep_exact(SharedMoments sh, MomPtrs mp, SolveGeom g,
+                                                                const unsigned* __restrict__ pending, i64 n_words,
+                                                                double* __restrict__ out,
+                                                                unsigned long long* __restrict__ empty_count,
+                                                                i64* __restrict__ empty_list, i64 list_cap) {
+  constexpr int p = N - 1;
+  constexpr int d = p / 2;
+  constexpr int nm = 1 + p + p * (p + 1) / 2;
+  constexpr int nl = 1 + p;
+  __shared__ double sm_solve[(nm + nl) * kSolveTile];
+  const i64 wpr = (g.tc + 31) / 32;
+  for (i64 w = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; w < n_words;
+       w += static_cast<i64>(gridDim.x) * blockDim.x) {
+    unsigned bits = pending[w];
+    const int lrow = static_cast<int>(w / wpr);
+    const int cw = static_cast<int>(w % wpr) * 32;
+    while (bits) {
+      const int lane = __ffs(bits) - 1;
+      bits &= bits - 1;
+      SepNode n;
+      if (!sep_node(g, lrow, cw / kSolveTile, cw % kSolveTile + lane, n)) continue;
+      double T[nl], Ps[SepIdx<d>::n], Pt[SepIdx<d>::n], S[nm], b0;
+#pragma unroll
+      for (int i = 0; i < nl; ++i) T[i] = mp.T[i][n.e];
+      sep_load<N>(sh, n.row, Ps);
+      sep_load<N>(sh, n.col, Pt);
+      sep_assemble<N>(sh, Ps, Pt, __ldg(sh.coord + n.row), __ldg(sh.coord + n.col), S);
+      const int st = solve_local_perm<N>(S, T, sm_solve + threadIdx.x, kSolveTile, b0);
+      if (st == kFitEmpty) {
+        const unsigned long long slot = atomicAdd(empty_count, 1ull);
+        if (static_cast<i64>(slot) < list_cap) empty_list[slot] = n.dst;
+        out[n.dst] = __longlong_as_double(0x7ff8000000000000ll);
+      } else {
+        out[n.dst] = b0;
+      }
+    }
   }
 }
 
@@ -823,10 +898,15 @@ void launch_solve_shared_n(dfpca_context* ctx, const SharedMoments& sh, const Mo
   int nch = 0;
   if (const i64 n = tri_ctas(g, nch); n >= 0) {
     if (n > 0) {
-      if (n / nch <= 65535 && g.gt < (i64(1) << 24))
+      if (n / nch <= 65535 && g.gt < (i64(1) << 24) && sh.P) {
+        const i64 n_words = (n / nch) * ((g.tc + 31) / 32);
+        DevBuf<unsigned> pending(static_cast<std::size_t>(n_words));
+        DFPCA_CUDA(cudaMemsetAsync(pending.get(), 0, sizeof(unsigned) * n_words, ctx->stream));
         DFPCA_LAUNCH(ctx, k_solve_sep_tri<N>, dim3(static_cast<unsigned>(nch), static_cast<unsigned>(n / nch)),
-                     kSolveTile, 0, sh, mp, g, out, cnt, list, cap);
-      else
+                     kSolveTile, 0, sh, mp, g, out, pending.get());
+        DFPCA_LAUNCH(ctx, k_solve_sep_exact<N>, grid_for(n_words, kSolveTile, 148ll * 8), kSolveTile, 0, sh, mp, g,
+                     pending.get(), n_words, out, cnt, list, cap);
+      } else
         DFPCA_LAUNCH(ctx, k_solve_shared_tri<N>, static_cast<unsigned>(n), kSolveTile, 0, sh, mp, g, nch, out, cnt,
                      list, cap);
     }
@@ -1196,6 +1276,54 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
     for (int k = 0; k < d; ++k) {
       sh.A[k] = slot->get() + offA[k];
       sh.D[k] = slot->get() + offD[k];
+    }
+    // per-node products P_a(u) (sep_products' expression order, so the
+    // device reads the same bits it would compute) and packed coordinates
+    bool fits = d <= 3;
+    for (int k = 0; k < d; ++k) fits = fits && grid.shape[k] <= static_cast<i64>(kCoordMask) + 1;
+    if (fits) {
+      const int ns = sep_stride(d);
+      auto& nodes = ctx->table_cache[key + "|nodes"];
+      if (!nodes) {
+        std::vector<double> host(static_cast<std::size_t>(ns * G + (G + 1) / 2), 0.0);
+        unsigned* coord = reinterpret_cast<unsigned*>(host.data() + ns * G);
+        std::vector<double> hA(total);
+        DFPCA_CUDA(cudaMemcpy(hA.data(), slot->get(), sizeof(double) * total, cudaMemcpyDeviceToHost));
+        for (i64 u = 0; u < G; ++u) {
+          int j[kMaxDim] = {};
+          i64 rest = u;
+          for (int k = d - 1; k >= 0; --k) {
+            j[k] = static_cast<int>(rest % grid.shape[k]);
+            rest /= grid.shape[k];
+          }
+          unsigned packed = 0;
+          for (int k = 0; k < d; ++k) packed |= static_cast<unsigned>(j[k]) << (kCoordBits * k);
+          coord[u] = packed;
+          auto a = [&](int k, int r) { return hA[offA[k] + r * grid.shape[k] + j[k]]; };
+          double z = 1.0;
+          for (int k = 0; k < d; ++k) z *= a(k, 0);
+          double* row = host.data() + u * ns;
+          row[0] = z;
+          for (int k = 0; k < d; ++k) {
+            double v = 1.0;
+            for (int m = 0; m < d; ++m) v *= a(m, m == k ? 1 : 0);
+            row[1 + k] = v;
+          }
+          for (int k = 0; k < d; ++k)
+            for (int l = k; l < d; ++l) {
+              double v = 1.0;
+              for (int m = 0; m < d; ++m) v *= a(m, (m == k) + (m == l));
+              row[1 + d + k * d - k * (k - 1) / 2 + (l - k)] = v;
+            }
+        }
+        nodes = std::make_unique<DevBuf<double>>(host.size());
+        DFPCA_CUDA(cudaMemcpyAsync(nodes->get(), host.data(), sizeof(double) * host.size(), cudaMemcpyHostToDevice,
+                                   st));
+        DFPCA_CUDA(cudaStreamSynchronize(st));
+      }
+      sh.P = nodes->get();
+      sh.coord = reinterpret_cast<const unsigned*>(nodes->get() + ns * G);
+      sh.G = G;
     }
   }
 

@@ -590,21 +590,50 @@ __device__ __forceinline__ void sep_load(const SharedMoments& sh, int node, doub
 }
 
 // Node of the tiled upper-triangle solve handled by thread `tid` of CTA
-// (ch, lrow); false when the thread has no node.
+// (ch, lrow); false when the thread has no node.  Index arithmetic in 32
+// bits (the launch guarantees rows * gt < 2^32 and npts < 2^32).
 struct SepNode {
-  int row, col, c;
-  i64 e, dst;
+  unsigned row, col, c;
+  unsigned e, dst;
 };
-__device__ __forceinline__ bool sep_node(const SolveGeom& g, int lrow, int ch, int tid, SepNode& n) {
-  const int tc = static_cast<int>(g.tc);
-  const int t0 = static_cast<int>(g.t0);
-  const int mrow = lrow + static_cast<int>(g.row_lo);
-  n.row = mrow + static_cast<int>(g.row0);
+__device__ __forceinline__ bool sep_node(const SolveGeom& g, unsigned lrow, unsigned ch, unsigned tid, SepNode& n) {
+  const unsigned tc = static_cast<unsigned>(g.tc);
+  const unsigned mrow = lrow + static_cast<unsigned>(g.row_lo);
+  n.row = mrow + static_cast<unsigned>(g.row0);
   n.c = ch * kSolveTile + tid;
-  n.col = t0 + n.c;
+  n.col = static_cast<unsigned>(g.t0) + n.c;
   if (n.c >= tc || n.col < n.row) return false;
-  n.e = static_cast<i64>(mrow) * tc + n.c;
-  n.dst = static_cast<i64>(n.row - g.out_row0) * g.gt + n.col;
+  n.e = mrow * tc + n.c;
+  n.dst = (n.row - static_cast<unsigned>(g.out_row0)) * static_cast<unsigned>(g.gt) + n.col;
+  return true;
+}
+
+// First column chunk of local row lrow holding a node with col >= row.
+__host__ __device__ __forceinline__ unsigned sep_first_chunk(const SolveGeom& g, unsigned lrow, unsigned nch) {
+  const long long row = static_cast<long long>(lrow) + g.row_lo + g.row0;
+  const long long off = row - g.t0;
+  const unsigned ch = off > 0 ? static_cast<unsigned>(off / kSolveTile) : 0u;
+  return ch < nch ? ch : nch;
+}
+
+// Paired-row grid of the tiled triangle: grid row y holds the chunks of
+// local rows y and rows-1-y back to back (their counts sum to ~nch + 1 on
+// the full square), so no CTA is launched below the diagonal.
+__device__ __forceinline__ bool sep_cta(const SolveGeom& g, unsigned rows, unsigned nch, unsigned& lrow,
+                                        unsigned& ch) {
+  const unsigned y = blockIdx.y, x = blockIdx.x;
+  const unsigned c0 = sep_first_chunk(g, y, nch), cnt0 = nch - c0;
+  if (x < cnt0) {
+    lrow = y;
+    ch = c0 + x;
+    return true;
+  }
+  const unsigned y1 = rows - 1 - y;
+  if (y1 <= y) return false;
+  const unsigned c1 = sep_first_chunk(g, y1, nch);
+  if (x - cnt0 >= nch - c1) return false;
+  lrow = y1;
+  ch = c1 + (x - cnt0);
   return true;
 }
 
@@ -628,22 +657,22 @@ __device__ __forceinline__ void ridged_diagonal(const double (&S)[1 + (N - 1) + 
 // product table (uniform for the row, 128-bit loads for the columns), the
 // value moments read from the pipeline, and the ridged system solved by the
 // certified fast path (ldlt_certified).  Windows it cannot certify
-// (near-singular, empty, non-SPD) are flagged in `pending` (one bit per node,
-// word lrow * ceil(tc / 32) + c / 32, zeroed by the caller) for
-// k_solve_sep_exact, so this kernel carries no register or code for them.
+// (near-singular, empty, non-SPD) are queued for k_solve_sep_exact as
+// (word, lane bits) entries, word = lrow * ceil(tc / 32) + c / 32, one per
+// warp with misses (pending[0] = count, zeroed by the caller; entries from
+// pending[2]), so this kernel carries no register or code for them.
 template <int N>
 __global__ void __launch_bounds__(kSolveTile, N == 5 ? DFPCA_SOLVE5_MIN_CTAS : DFPCA_SOLVE_MIN_CTAS)
-    k_solve_sep_tri(SharedMoments sh, MomPtrs mp, SolveGeom g, double* __restrict__ out,
-                    unsigned* __restrict__ pending) {
+    k_solve_sep_tri(SharedMoments sh, MomPtrs mp, SolveGeom g, unsigned rows, unsigned nch,
+                    double* __restrict__ out, unsigned* __restrict__ pending) {
   constexpr int p = N - 1;
   constexpr int d = p / 2;
   constexpr int nm = 1 + p + p * (p + 1) / 2;
   constexpr int nl = 1 + p;
-  const int lrow = static_cast<int>(blockIdx.y);  // grid: (column chunks, rows)
-  const int ch = static_cast<int>(blockIdx.x);
-  if (g.t0 + (ch + 1) * kSolveTile <= lrow + g.row_lo + g.row0) return;
+  unsigned lrow, ch;
+  if (!sep_cta(g, rows, nch, lrow, ch)) return;
   SepNode n;
-  if (!sep_node(g, lrow, ch, static_cast<int>(threadIdx.x), n)) return;
+  if (!sep_node(g, lrow, ch, threadIdx.x, n)) return;
   if (g.mask && !(g.mask[n.row] != 0 && g.mask[n.col] != 0)) {
     out[n.dst] = __longlong_as_double(0x7ff8000000000000ll);
     return;
@@ -662,17 +691,19 @@ __global__ void __launch_bounds__(kSolveTile, N == 5 ? DFPCA_SOLVE5_MIN_CTAS : D
   if (done) out[n.dst] = b0;
   const unsigned miss = __ballot_sync(__activemask(), !done);
   if (miss != 0 && (threadIdx.x & 31) == __ffs(__activemask()) - 1) {
-    const i64 wpr = (g.tc + 31) / 32;
-    pending[lrow * wpr + (n.c >> 5)] = miss;
+    const unsigned wpr = static_cast<unsigned>((g.tc + 31) / 32);
+    const unsigned slot = atomicAdd(pending, 1u);
+    pending[2 + 2 * slot] = lrow * wpr + (n.c >> 5);
+    pending[3 + 2 * slot] = miss;
   }
 }
 
 // The windows k_solve_sep_tri flagged: Eigen's pivoted LDLT replayed exactly
 // (solve_local_perm), the local-constant fallback and the empty-window list.
-// One thread per bitmap word.
+// One thread per queued warp word.
 template <int N>
 __global__ void __launch_bounds__(kSolveTile) k_solve_sep_exact(SharedMoments sh, MomPtrs mp, SolveGeom g,
-                                                                const unsigned* __restrict__ pending, i64 n_words,
+                                                                const unsigned* __restrict__ pending,
                                                                 double* __restrict__ out,
                                                                 unsigned long long* __restrict__ empty_count,
                                                                 i64* __restrict__ empty_list, i64 list_cap) {
@@ -682,16 +713,19 @@ __global__ void __launch_bounds__(kSolveTile) k_solve_sep_exact(SharedMoments sh
   constexpr int nl = 1 + p;
   __shared__ double sm_solve[(nm + nl) * kSolveTile];
   const i64 wpr = (g.tc + 31) / 32;
-  for (i64 w = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; w < n_words;
-       w += static_cast<i64>(gridDim.x) * blockDim.x) {
-    unsigned bits = pending[w];
+  const unsigned n_words = pending[0];
+  for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < n_words; q += gridDim.x * blockDim.x) {
+    const i64 w = pending[2 + 2 * q];
+    unsigned bits = pending[3 + 2 * q];
     const int lrow = static_cast<int>(w / wpr);
     const int cw = static_cast<int>(w % wpr) * 32;
     while (bits) {
       const int lane = __ffs(bits) - 1;
       bits &= bits - 1;
       SepNode n;
-      if (!sep_node(g, lrow, cw / kSolveTile, cw % kSolveTile + lane, n)) continue;
+      if (!sep_node(g, static_cast<unsigned>(lrow), static_cast<unsigned>(cw / kSolveTile),
+                    static_cast<unsigned>(cw % kSolveTile + lane), n))
+        continue;
       double T[nl], Ps[SepIdx<d>::n], Pt[SepIdx<d>::n], S[nm], b0;
 #pragma unroll
       for (int i = 0; i < nl; ++i) T[i] = mp.T[i][n.e];
@@ -898,14 +932,22 @@ void launch_solve_shared_n(dfpca_context* ctx, const SharedMoments& sh, const Mo
   int nch = 0;
   if (const i64 n = tri_ctas(g, nch); n >= 0) {
     if (n > 0) {
-      if (n / nch <= 65535 && g.gt < (i64(1) << 24) && sh.P) {
-        const i64 n_words = (n / nch) * ((g.tc + 31) / 32);
-        DevBuf<unsigned> pending(static_cast<std::size_t>(n_words));
-        DFPCA_CUDA(cudaMemsetAsync(pending.get(), 0, sizeof(unsigned) * n_words, ctx->stream));
-        DFPCA_LAUNCH(ctx, k_solve_sep_tri<N>, dim3(static_cast<unsigned>(nch), static_cast<unsigned>(n / nch)),
-                     kSolveTile, 0, sh, mp, g, out, pending.get());
-        DFPCA_LAUNCH(ctx, k_solve_sep_exact<N>, grid_for(n_words, kSolveTile, 148ll * 8), kSolveTile, 0, sh, mp, g,
-                     pending.get(), n_words, out, cnt, list, cap);
+      const i64 rows = n / nch;
+      if (rows <= 2 * 65535 && rows * g.gt < (i64(1) << 32) && g.npts < (i64(1) << 32) && sh.P) {
+        const i64 n_words = rows * ((g.tc + 31) / 32);
+        DevBuf<unsigned> pending(static_cast<std::size_t>(2 + 2 * n_words));
+        DFPCA_CUDA(cudaMemsetAsync(pending.get(), 0, sizeof(unsigned), ctx->stream));
+        unsigned gx = 1;  // widest row pair
+        for (i64 y = 0; y < (rows + 1) / 2; ++y) {
+          const unsigned c0 = nch - sep_first_chunk(g, static_cast<unsigned>(y), nch);
+          const i64 y1 = rows - 1 - y;
+          const unsigned c1 = y1 > y ? nch - sep_first_chunk(g, static_cast<unsigned>(y1), nch) : 0u;
+          gx = std::max(gx, c0 + c1);
+        }
+        DFPCA_LAUNCH(ctx, k_solve_sep_tri<N>, dim3(gx, static_cast<unsigned>((rows + 1) / 2)), kSolveTile, 0, sh, mp,
+                     g, static_cast<unsigned>(rows), static_cast<unsigned>(nch), out, pending.get());
+        DFPCA_LAUNCH(ctx, k_solve_sep_exact<N>, 148 * 4, kSolveTile, 0, sh, mp, g, pending.get(), out, cnt, list,
+                     cap);
       } else
         DFPCA_LAUNCH(ctx, k_solve_shared_tri<N>, static_cast<unsigned>(n), kSolveTile, 0, sh, mp, g, nch, out, cnt,
                      list, cap);

@@ -220,6 +220,10 @@ struct SharedMoments {
   i64 G = 0;
 };
 constexpr int kCoordBits = 10;
+#ifndef DFPCA_SEP_LOOP
+#define DFPCA_SEP_LOOP 4
+#endif
+constexpr int kSepLoop = DFPCA_SEP_LOOP;  // tiles per CTA of k_solve_sep_tri
 constexpr unsigned kCoordMask = (1u << kCoordBits) - 1;
 
 template <int P>
@@ -619,9 +623,9 @@ __host__ __device__ __forceinline__ unsigned sep_first_chunk(const SolveGeom& g,
 // Paired-row grid of the tiled triangle: grid row y holds the chunks of
 // local rows y and rows-1-y back to back (their counts sum to ~nch + 1 on
 // the full square), so no CTA is launched below the diagonal.
-__device__ __forceinline__ bool sep_cta(const SolveGeom& g, unsigned rows, unsigned nch, unsigned& lrow,
+__device__ __forceinline__ bool sep_cta(const SolveGeom& g, unsigned rows, unsigned nch, unsigned x, unsigned& lrow,
                                         unsigned& ch) {
-  const unsigned y = blockIdx.y, x = blockIdx.x;
+  const unsigned y = blockIdx.y;
   const unsigned c0 = sep_first_chunk(g, y, nch), cnt0 = nch - c0;
   if (x < cnt0) {
     lrow = y;
@@ -669,32 +673,36 @@ __global__ void __launch_bounds__(kSolveTile, N == 5 ? DFPCA_SOLVE5_MIN_CTAS : D
   constexpr int d = p / 2;
   constexpr int nm = 1 + p + p * (p + 1) / 2;
   constexpr int nl = 1 + p;
-  unsigned lrow, ch;
-  if (!sep_cta(g, rows, nch, lrow, ch)) return;
-  SepNode n;
-  if (!sep_node(g, lrow, ch, threadIdx.x, n)) return;
-  if (g.mask && !(g.mask[n.row] != 0 && g.mask[n.col] != 0)) {
-    out[n.dst] = __longlong_as_double(0x7ff8000000000000ll);
-    return;
-  }
-  double T[nl];
+  for (int it = 0; it < kSepLoop; ++it) {  // kSepLoop tiles of the grid row per CTA
+    unsigned lrow, ch;
+    if (!sep_cta(g, rows, nch, blockIdx.x * kSepLoop + it, lrow, ch)) return;
+    SepNode n;
+    bool done = true;
+    if (sep_node(g, lrow, ch, threadIdx.x, n)) {
+      if (g.mask && !(g.mask[n.row] != 0 && g.mask[n.col] != 0)) {
+        out[n.dst] = __longlong_as_double(0x7ff8000000000000ll);
+      } else {
+        double T[nl];
 #pragma unroll
-  for (int i = 0; i < nl; ++i) T[i] = mp.T[i][n.e];  // issue the moment loads first
-  double Ps[SepIdx<d>::n], Pt[SepIdx<d>::n];
-  sep_load<N>(sh, n.row, Ps);
-  sep_load<N>(sh, n.col, Pt);
-  double S[nm];
-  sep_assemble<N>(sh, Ps, Pt, __ldg(sh.coord + n.row), __ldg(sh.coord + n.col), S);
-  double dg[N], b0;
-  ridged_diagonal<N>(S, dg);
-  const bool done = ldlt_certified<N>(S, T, dg, b0);
-  if (done) out[n.dst] = b0;
-  const unsigned miss = __ballot_sync(__activemask(), !done);
-  if (miss != 0 && (threadIdx.x & 31) == __ffs(__activemask()) - 1) {
-    const unsigned wpr = static_cast<unsigned>((g.tc + 31) / 32);
-    const unsigned slot = atomicAdd(pending, 1u);
-    pending[2 + 2 * slot] = lrow * wpr + (n.c >> 5);
-    pending[3 + 2 * slot] = miss;
+        for (int i = 0; i < nl; ++i) T[i] = mp.T[i][n.e];  // issue the moment loads first
+        double Ps[SepIdx<d>::n], Pt[SepIdx<d>::n];
+        sep_load<N>(sh, n.row, Ps);
+        sep_load<N>(sh, n.col, Pt);
+        double S[nm];
+        sep_assemble<N>(sh, Ps, Pt, __ldg(sh.coord + n.row), __ldg(sh.coord + n.col), S);
+        double dg[N], b0;
+        ridged_diagonal<N>(S, dg);
+        done = ldlt_certified<N>(S, T, dg, b0);
+        if (done) out[n.dst] = b0;
+      }
+    }
+    const unsigned miss = __ballot_sync(0xffffffffu, !done);
+    if (miss != 0 && (threadIdx.x & 31) == __ffs(miss) - 1) {
+      const unsigned wpr = static_cast<unsigned>((g.tc + 31) / 32);
+      const unsigned slot = atomicAdd(pending, 1u);
+      pending[2 + 2 * slot] = lrow * wpr + (n.c >> 5);
+      pending[3 + 2 * slot] = miss;
+    }
   }
 }
 
@@ -944,7 +952,8 @@ void launch_solve_shared_n(dfpca_context* ctx, const SharedMoments& sh, const Mo
           const unsigned c1 = y1 > y ? nch - sep_first_chunk(g, static_cast<unsigned>(y1), nch) : 0u;
           gx = std::max(gx, c0 + c1);
         }
-        DFPCA_LAUNCH(ctx, k_solve_sep_tri<N>, dim3(gx, static_cast<unsigned>((rows + 1) / 2)), kSolveTile, 0, sh, mp,
+        DFPCA_LAUNCH(ctx, k_solve_sep_tri<N>, dim3((gx + kSepLoop - 1) / kSepLoop, static_cast<unsigned>((rows + 1) / 2)),
+                     kSolveTile, 0, sh, mp,
                      g, static_cast<unsigned>(rows), static_cast<unsigned>(nch), out, pending.get());
         DFPCA_LAUNCH(ctx, k_solve_sep_exact<N>, 148 * 4, kSolveTile, 0, sh, mp, g, pending.get(), out, cnt, list,
                      cap);

@@ -641,6 +641,14 @@ __device__ __forceinline__ bool sep_cta(const SolveGeom& g, unsigned rows, unsig
   return true;
 }
 
+// Streaming load that does not allocate in L1 (the value moments are read
+// once; L1 keeps the product- and band-table lines instead).
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 // The ridged diagonal (eps = kRidgeScale trace, local_fit.hpp:70-71).
 template <int N>
 __device__ __forceinline__ void ridged_diagonal(const double (&S)[1 + (N - 1) + (N - 1) * N / 2], double (&dg)[N]) {
@@ -684,7 +692,7 @@ __global__ void __launch_bounds__(kSolveTile, N == 5 ? DFPCA_SOLVE5_MIN_CTAS : D
       } else {
         double T[nl];
 #pragma unroll
-        for (int i = 0; i < nl; ++i) T[i] = mp.T[i][n.e];  // issue the moment loads first
+        for (int i = 0; i < nl; ++i) T[i] = ld_stream(mp.T[i] + n.e);  // issue the moment loads first
         double Ps[SepIdx<d>::n], Pt[SepIdx<d>::n];
         sep_load<N>(sh, n.row, Ps);
         sep_load<N>(sh, n.col, Pt);
@@ -693,7 +701,7 @@ __global__ void __launch_bounds__(kSolveTile, N == 5 ? DFPCA_SOLVE5_MIN_CTAS : D
         double dg[N], b0;
         ridged_diagonal<N>(S, dg);
         done = ldlt_certified<N>(S, T, dg, b0);
-        if (done) out[n.dst] = b0;
+        if (done) __stcs(out + n.dst, b0);
       }
     }
     const unsigned miss = __ballot_sync(0xffffffffu, !done);

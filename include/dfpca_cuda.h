@@ -75,6 +75,14 @@ enum { DFPCA_SURFACE_MEAN = 0, DFPCA_SURFACE_COVARIANCE = 1, DFPCA_SURFACE_DIAG 
  * Distinct contexts run concurrently. */
 DFPCA_API int dfpca_context_create(int device, dfpca_context** out);
 DFPCA_API int dfpca_context_destroy(dfpca_context* ctx);
+/* Backs the context's stream-ordered pool with at least `bytes` of device
+ * memory now (allocated once, returned to the pool, kept): a later call that
+ * needs that much reuses mapped pages instead of growing the pool while its
+ * kernels run.  The first config-5 (d = 3, 32^3) covariance is ~0.7 s with no
+ * reserve and ~0.12 s after a 96 GB one; mapping costs ~13 ms per GB, paid
+ * here.  The initial reserve is DFPCA_POOL_RESERVE_GB (default 0).  Not in
+ * the reference (its host allocator has no such cost). */
+DFPCA_API int dfpca_context_reserve(dfpca_context* ctx, uint64_t bytes);
 DFPCA_API int dfpca_last_error(const dfpca_context* ctx, int* error_class, const char** name,
                      const char** message);
 /* Sample / observation index attached to ObservationOutsideGrid (-1 if none). */

@@ -58,6 +58,7 @@ PI64 = C.POINTER(C.c_int64)
 SIGNATURES = [
     ("dfpca_context_create", C.c_int, [C.c_int, C.POINTER(P)]),
     ("dfpca_context_destroy", C.c_int, [P]),
+    ("dfpca_context_reserve", C.c_int, [P, C.c_uint64]),
     ("dfpca_last_error", C.c_int, [P, C.POINTER(C.c_int), C.POINTER(C.c_char_p), C.POINTER(C.c_char_p)]),
     ("dfpca_last_error_location", C.c_int, [P, PI64, PI64]),
     ("dfpca_stage_time", C.c_int, [P, C.c_char_p, PD]),

@@ -654,6 +654,14 @@ def fft_covariance(binned: BinnedData, grid: EvaluationGrid, h: Bandwidth, mean:
     return SurfaceEstimate(grid, SurfaceKind.Covariance, handle=handle)
 
 
+def reserve_device_memory(nbytes: int) -> None:
+    """Backs this process's device pool with at least `nbytes` now
+    (dfpca_context_reserve): the first call of a large workload then reuses
+    mapped pages instead of growing the pool while its kernels run (~13 ms
+    per GB, paid here).  A B200-side knob; the reference has no equivalent."""
+    check(_lib.lib().dfpca_context_reserve(_lib.ctx(), int(nbytes)))
+
+
 # ------------------------------------------------- multi-GPU (sharded) ----
 # The reference's only parallel knob is set_max_threads (parallel.hpp:23);
 # here one process per GPU runs one rank of a slab-sharded covariance

@@ -369,17 +369,32 @@ int guarded(dfpca_context* ctx, F&& f) {
 
 }  // namespace
 
+// Blocks freed into a stream-ordered pool that already holds them are handed
+// out again without mapping new pages: allocate `bytes` (at most 55 % of the
+// free memory) and free it into the pool, whose release threshold keeps it.
+bool pool_reserve(dfpca_context* ctx, std::uint64_t bytes) {
+  std::size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
+  const std::size_t want = std::min<std::size_t>(static_cast<std::size_t>(bytes), static_cast<std::size_t>(0.55 * free_b));
+  void* p = nullptr;
+  bool ok = true;
+  if (want > 0) {
+    ok = cudaMallocAsync(&p, want, ctx->stream) == cudaSuccess;
+    if (ok) cudaFreeAsync(p, ctx->stream);
+    ok = cudaStreamSynchronize(ctx->stream) == cudaSuccess && ok;
+  }
+  cudaGetLastError();
+  return ok;
+}
+
 extern "C" {
 
 int dfpca_context_create(int device, dfpca_context** out) {
   if (!out) return kConfig;
   *out = nullptr;
-  // Load every kernel of the library when the driver initialises instead of
-  // at its first launch (CUDA's default lazy loading made the first call of
-  // each path pay for loading its kernels: ~13 ms of the first config-4 mean
-  // smoother, most of the ~1 s first config-5 covariance).  Effective when
-  // this is the process's first CUDA call; DFPCA keeps a caller's own choice.
-  setenv("CUDA_MODULE_LOADING", "EAGER", 0);
+  // Module loading stays CUDA's default (lazy): EAGER would also load every
+  // kernel of cuSOLVER at the first dense_eig (31.7 s cold for config 1,
+  // against 90 ms lazy); lazy loading costs a few ms on each path's first call.
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0 || device < 0 || device >= n) return kNumeric;
   auto* ctx = new dfpca_context();
@@ -393,28 +408,22 @@ int dfpca_context_create(int device, dfpca_context** out) {
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
     std::uint64_t keep = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    // Back the pool with physical memory up front (DFPCA_POOL_RESERVE_GB,
-    // default 96, at most 55 % of the free memory): blocks freed into a pool
-    // that already holds them are handed out again without mapping new
-    // pages, so call-to-call allocation cost stays flat instead of spiking
-    // when a call needs more than the previous ones (the d = 3 32^3
-    // covariance: first call 706 ms with a 48 GB reserve -- the pool grew
-    // while the moment passes ran -- against 122 ms with 100 GB).
+    // Optional up-front backing of the pool (DFPCA_POOL_RESERVE_GB, default
+    // 0; dfpca_context_reserve does the same later): mapping costs ~13 ms per
+    // GB, so it is not paid by every process by default (96 GB: +1.25 s on
+    // context creation).
     const char* e = std::getenv("DFPCA_POOL_RESERVE_GB");
-    const double gb = e ? std::atof(e) : 96.0;
-    std::size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    const std::size_t want =
-        std::min<std::size_t>(static_cast<std::size_t>(gb * (1ull << 30)), static_cast<std::size_t>(0.55 * free_b));
-    void* p = nullptr;
-    if (want > 0 && cudaMallocAsync(&p, want, ctx->stream) == cudaSuccess) {
-      cudaFreeAsync(p, ctx->stream);
-      cudaStreamSynchronize(ctx->stream);
-    }
-    cudaGetLastError();
+    const double gb = e ? std::atof(e) : 0.0;
+    if (gb > 0) pool_reserve(ctx, static_cast<std::uint64_t>(gb * (1ull << 30)));
   }
   *out = ctx;
   return 0;
+}
+
+int dfpca_context_reserve(dfpca_context* ctx, uint64_t bytes) {
+  if (!ctx) return kConfig;
+  cudaSetDevice(ctx->device);
+  return pool_reserve(ctx, bytes) ? 0 : kNumeric;
 }
 
 int dfpca_context_destroy(dfpca_context* ctx) {

@@ -102,7 +102,13 @@ def main():
     ap.add_argument("--configs", default="2,3,4,5")
     ap.add_argument("--q", type=int, default=99)
     ap.add_argument("--L", type=int, default=20)
+    ap.add_argument("--reserve-gb", type=float, default=0.0,
+                    help="api.reserve_device_memory before the first config (timed as reserve_ms)")
     a = ap.parse_args()
+    if a.reserve_gb > 0:
+        t0 = time.perf_counter()
+        api.reserve_device_memory(int(a.reserve_gb * (1 << 30)))
+        print(json.dumps({"reserve_gb": a.reserve_gb, "reserve_ms": (time.perf_counter() - t0) * 1e3}), flush=True)
     for c in [int(x) for x in a.configs.split(",")]:
         run(c, a.q, a.L)
 

@@ -523,13 +523,25 @@ std::size_t trsm_smem(int q) { return sizeof(double) * (static_cast<std::size_t>
 //   eigenvectors of the candidates (eigenvalue > 1e-12 max(0, lambda_max),
 //   the only ones finalize_eigensystem reads) by inverse iteration on the
 //   tridiagonal (dgttrf/dgttrs with precomputed pivot reciprocals), one warp
-//   per cluster with reorthogonalization inside clusters (dstein's rule:
-//   gaps below 1e-3 |T|), then back-transformed by the reflectors.
+//   per cluster with reorthogonalization inside clusters (gaps below
+//   kClusterGap |T|), then back-transformed by the reflectors.
 // Outputs: evals descending [n]; V [n][n] row-major, column c = eigenvector
 // of evals[c] for the leading min(candidates, max_vec) (zero otherwise);
 // info[0] = candidate count, info[1] = vectors computed; Vt [n][n] scratch
 // (the tridiagonal eigenvectors as rows: coalesced reorthogonalization).
 constexpr int kEigMaxN = 128;
+// Cluster rule of the inverse iteration.  Vectors computed independently
+// for eigenvalues a gap g apart are orthogonal to ~u |T| / g (the shifts are
+// exact to ~u |T|), so with g >= 1e-7 |T| the loss is <= 2.2e-9 -- far inside
+// the 1e-6 rad subspace bound and removed by the finalization's Gram-Schmidt
+// -- and only closer eigenvalues are iterated together with
+// reorthogonalization.  (LAPACK dstein groups gaps below 1e-3 |T|: at wide
+// bandwidths that put the whole decaying tail of the Ritz spectrum, 20+
+// members, into one sequential cluster.)
+constexpr double kClusterGap = 1e-7;
+#ifndef DFPCA_EIG_VEC_MARGIN
+#define DFPCA_EIG_VEC_MARGIN 4
+#endif
 constexpr int kEigThreads = 512;
 constexpr int kEigGroups = kEigThreads / kEigMaxN;  // row groups per column
 constexpr int kEigWarps = kEigThreads / 32;
@@ -575,10 +587,24 @@ struct TriWork {  // one warp's inverse-iteration workspace
   int piv[kEigMaxN];
 };
 
+// Acceptance of a Cholesky QR from its per-pass flags (k_chol_factor: flags[2p]
+// = breakdown, flags[2p + 1] = max |G - I| of pass p): every factorization
+// succeeded and the last pass started within 0.1 of orthonormal columns (so
+// it restored orthogonality to rounding).  The host applies the same rule.
+__host__ __device__ inline bool qr_accepted(const double* flags, int passes) {
+  bool ok = true;
+  for (int p = 0; p < passes; ++p) ok = ok && flags[2 * p] == 0.0;
+  return ok && flags[2 * (passes - 1) + 1] < 0.1;
+}
+
 __global__ void __launch_bounds__(kEigThreads) k_tri_eig(const double* __restrict__ Bg, int n,
                                                           double* __restrict__ evals_out, double* __restrict__ V,
                                                           int* __restrict__ info, int max_vec,
-                                                          double* __restrict__ Vt) {
+                                                          double* __restrict__ Vt,
+                                                          const double* __restrict__ qr_flags, int qr_passes) {
+  // a Cholesky QR the host will reject (qr_accepted) makes this call moot:
+  // skip it rather than spend the eigensolve on a basis about to be redone
+  if (qr_flags && !qr_accepted(qr_flags, qr_passes)) return;
   extern __shared__ double sm[];
   double* Hv = sm;                    // [n][kEigMaxN] reflector vectors (row k: v of H_k)
   double* d = Hv + n * kEigMaxN;      // diagonal
@@ -799,7 +825,7 @@ __global__ void __launch_bounds__(kEigThreads) k_tri_eig(const double* __restric
     const int nv = nc < max_vec ? nc : max_vec;
     int ncl = 0;
     for (int c = 0; c < nv; ++c) {
-      if (c == 0 || !(fabs(lam[n - 1 - c] - lam[n - c]) <= 1e-3 * tnorm)) cl_start[ncl++] = c;
+      if (c == 0 || !(fabs(lam[n - 1 - c] - lam[n - c]) <= kClusterGap * tnorm)) cl_start[ncl++] = c;
     }
     cl_start[ncl] = nv;
     n_clusters = ncl;
@@ -1336,12 +1362,13 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
     const bool tri = q <= kEigMaxN;
     // vectors for the leading L_max + 4 candidates (more only if the
     // finalization skips that many: then all of them, below)
-    i64 max_vec = std::min<i64>(q, L_max + 4);
+    i64 max_vec = std::min<i64>(q, L_max + DFPCA_EIG_VEC_MARGIN);
     auto tri_eig = [&](i64 mv_) {
       const std::size_t tsm = tri_eig_smem(static_cast<int>(q));
       allow_smem(k_tri_eig, tsm);
       DFPCA_LAUNCH(ctx, k_tri_eig, 1, kEigThreads, tsm, small.get(), static_cast<int>(q), evals.get(), Vs.get(),
-                   info.get(), static_cast<int>(mv_), Vt.get());
+                   info.get(), static_cast<int>(mv_), Vt.get(), cholqr ? flags.get() : nullptr,
+                   mode == 0 ? 2 : 3);
     };
     if (tri) {
       tri_eig(max_vec);
@@ -1369,14 +1396,7 @@ void run_randomized_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid
     DFPCA_CUDA(cudaMemcpyAsync(&jinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
     if (cholqr) DFPCA_CUDA(cudaMemcpyAsync(hf, flags.get(), sizeof(hf), cudaMemcpyDeviceToHost, st));
     DFPCA_CUDA(cudaStreamSynchronize(st));
-    if (cholqr) {
-      // every factorization succeeded and the last pass started within 0.1
-      // of orthonormal columns (so it restored orthogonality to rounding)
-      const int passes = mode == 0 ? 2 : 3;
-      bool ok = true;
-      for (int ps = 0; ps < passes; ++ps) ok = ok && hf[2 * ps] == 0.0;
-      if (!(ok && hf[2 * (passes - 1) + 1] < 0.1)) return false;
-    }
+    if (cholqr && !qr_accepted(hf, mode == 0 ? 2 : 3)) return false;
     if (!tri && jinfo != 0) fail(kNumeric, "EigFailure", "projected eigensolver did not converge");
 
     if (!finish_eigensystem(ctx, grid, mv.node_of_row, M, Lt.get(), evals.get(), tilde, L_max, true, eigenvalues,

@@ -272,6 +272,10 @@ void gemm_tn(dfpca_context* ctx, i64 M, i64 N, i64 K, const double* A, i64 lda, 
     return;
   }
   const i64 tiles_m = (M + BM - 1) / BM;
+  if (symmetric && M == N && A == B && lda == ldb && ozaki_enabled() &&
+      ozaki_syrk(ctx, M, K, A, lda, w, C, ldc, std::max<i64>(0, tm_begin) * BM,
+                 (tm_end < 0 || tm_end > tiles_m ? tiles_m : tm_end) * BM))
+    return;
   DevBuf<double> scaled;
   i64 a_col0 = 0;
   if (w) {

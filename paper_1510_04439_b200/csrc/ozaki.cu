@@ -1,0 +1,435 @@
+// FP64 SYRK of the pair grids (K2) on the int8 tensor cores: the Ozaki
+// scheme with tcgen05.mma kind::i8.
+//
+// pv[s][t] = sum_i w_i Y_i(s) Y_i(t) (and pw alike) is the symmetric product
+// X^T Y of X = w * Y and Y, both K x G (K = subjects, G = grid nodes).  FP64
+// has no tcgen05 kind and DMMA runs at the DFMA rate (37 TFLOP/s, gemm.cu);
+// the int8 kind runs ~120x faster per MAC, so the product is computed from
+// exact integer products of 7-bit slices:
+//
+//   per node column m, e_m with max_k |X[k][m]| 2^-e_m <= 127/128, and
+//   X[k][m] = 2^e_m (sum_{a=1..S} 2^-7a x_a[m][k] + r),  |r| <= 2^-7S / 2,
+//   x_1 in [-127, 127], x_a in [-64, 64] (round-to-nearest signed digits,
+//   every step exact in double); the same for Y with e'_m, y_b.
+//
+//   X^T Y [s][t] ~ 2^(e_s + e'_t) sum_{d=2..S+1} 2^-7d P_d[s][t],
+//   P_d = sum_{a+b=d} x_a y_b^T  (int8 x int8 -> int32, exact: at most S terms
+//   of K * 127^2 each, so K <= 16384 keeps every sum below 2^31).
+//
+// The dropped pairs (a + b > S + 1) and the slice remainders are each below
+// ~K 2^-7S of max |X| max |Y| per column pair; with S = 8 that is ~3e-14
+// relative at K = 2000 -- the order of an FP64 dot product's own rounding
+// bound (K u sum |x y| ~ 2e-13), far inside the 1e-10 surface tolerance.
+// Zero products stay exactly zero (all digits zero).
+//
+// Kernel: one CTA per SM (the 8 int32 accumulators of a 128 x 64 output tile
+// fill all 512 TMEM columns), persistent over the upper tiles.  Per 64-byte K
+// chunk the CTA stages the S slices of its 128 s-rows and 64 t-rows (96 KB,
+// no-swizzle K-major core-matrix layout, cp.async, double-buffered); one
+// thread issues the 36 slice pairs x 2 K-halves = 72 MMAs (M 128, N 64, K 32)
+// into accumulator d = a + b - 2 and commits them to the stage's mbarrier.
+// The epilogue (4 warps, one TMEM lane = one s row each) converts the 8
+// int32 accumulators to double, scales, and writes every upper-triangle entry
+// of the tile and its mirror (entries s > t are written only by the tile
+// owning (t, s), so the result is exactly symmetric and deterministic).
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "gemm.cuh"
+
+namespace dfpca_gpu {
+namespace {
+
+constexpr int kOzS = 8;           // 7-bit slices
+constexpr int kOzM = 128;         // tile rows (s), UMMA M
+constexpr int kOzN = 64;          // tile columns (t), UMMA N
+constexpr int kOzKc = 32;         // K bytes per stage = one MMA's K
+constexpr int kOzStages = 4;
+constexpr int kOzMaxK = 16384;
+constexpr int kOzBlkA = kOzS * kOzM * kOzKc;   // 32 KB: one (row block, K chunk) of the X slices
+constexpr int kOzBlkB = kOzS * kOzN * kOzKc;   // 16 KB: the same of the Y slices
+constexpr int kOzStage = kOzBlkA + kOzBlkB;    // 48 KB
+constexpr int kOzSmem = kOzStages * kOzStage + 1024;
+// warps: 0 producer (bulk copies), 1 MMA issuer, 2..5 epilogue (TMEM lane
+// quadrants 2, 3, 0, 1)
+constexpr int kOzThreads = 192;
+
+__device__ inline unsigned oz_smem(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+
+__device__ inline void oz_mbar_wait(std::uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "OZ_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra OZ_DONE;\n\t"
+      "bra OZ_WAIT;\n"
+      "OZ_DONE:\n\t}\n" ::"r"(oz_smem(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ inline void oz_mbar_init_n(std::uint64_t* bar, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(oz_smem(bar)), "r"(n));
+}
+__device__ inline void oz_mbar_arrive(std::uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(oz_smem(bar)) : "memory");
+}
+__device__ inline void oz_mbar_expect(std::uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(oz_smem(bar)), "r"(bytes) : "memory");
+}
+__device__ inline void oz_bulk(void* dst, const void* src, unsigned bytes, std::uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(oz_smem(dst)),
+      "l"(src), "r"(bytes), "r"(oz_smem(bar))
+      : "memory");
+}
+
+__device__ inline bool oz_elect() {
+  unsigned p;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}\n"
+      : "=r"(p));
+  return p != 0u;
+}
+
+// Shared-memory matrix descriptor (SM100 UMMA): K-major, 32-byte swizzle:
+// rows of 32 K bytes, 8-row atoms of 256 bytes (`sbo` = 256 between atoms;
+// `lbo` unused, 16).
+__device__ inline std::uint64_t oz_desc(unsigned addr, unsigned lbo, unsigned sbo) {
+  std::uint64_t d = 0;
+  d |= static_cast<std::uint64_t>((addr >> 4) & 0x3fffu);
+  d |= static_cast<std::uint64_t>((lbo >> 4) & 0x3fffu) << 16;
+  d |= static_cast<std::uint64_t>((sbo >> 4) & 0x3fffu) << 32;
+  d |= static_cast<std::uint64_t>(1) << 46;  // descriptor version (SM100)
+  d |= static_cast<std::uint64_t>(6) << 61;  // SWIZZLE_32B
+  return d;                                  // base offset 0 (1024-byte aligned atoms)
+}
+
+// Instruction descriptor of kind::i8: D s32, A and B signed int8, both
+// K-major, M = 128, N = 64.
+constexpr std::uint32_t kOzIdesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<std::uint32_t>(kOzN >> 3) << 17) |
+                                   (static_cast<std::uint32_t>(kOzM >> 4) << 24);
+
+__device__ inline void oz_mma(unsigned tmem_d, std::uint64_t da, std::uint64_t db, bool accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kOzIdesc), "r"(accumulate ? 1 : 0));
+}
+__device__ inline void oz_commit_mbar(std::uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(oz_smem(bar))
+               : "memory");
+}
+
+// 32 consecutive int32 columns of this thread's TMEM lane.
+__device__ inline void oz_tmem_ld32(unsigned taddr, int (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+
+// ---- slicing ---------------------------------------------------------------
+
+// Column scale exponents of both operands in one pass over A: ex[m] / ey[m]
+// hold the bits of max_k |w_k A[k][m]| / max_k |A[k][m]|, combined across CTAs
+// with an integer atomicMax (non-negative doubles order like their bits).
+__global__ void k_oz_colmax(const double* __restrict__ A, i64 K, i64 M, i64 lda, const double* __restrict__ w,
+                            unsigned long long* __restrict__ ex, unsigned long long* __restrict__ ey) {
+  const i64 m = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (m >= M) return;
+  double mx = 0.0, my = 0.0;
+  for (i64 k = blockIdx.y; k < K; k += gridDim.y) {
+    const double a = A[k * lda + m];
+    mx = fmax(mx, fabs(__dmul_rn(w[k], a)));
+    my = fmax(my, fabs(a));
+  }
+  if (mx > 0.0) atomicMax(ex + m, static_cast<unsigned long long>(__double_as_longlong(mx)));
+  if (my > 0.0) atomicMax(ey + m, static_cast<unsigned long long>(__double_as_longlong(my)));
+}
+
+// exp2 scale of column m: the smallest e with max |X| 2^-e <= 127/128.
+__device__ inline int oz_exponent(unsigned long long maxbits) {
+  const double mx = __longlong_as_double(static_cast<long long>(maxbits));
+  if (!(mx > 0.0)) return 0;
+  int e;
+  const double f = frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1)
+  return f > 127.0 / 128.0 ? e + 1 : e;
+}
+
+// Slices of X = w * A (or A) in the product kernel's staging layout: for row
+// block rb (R rows: 128 for the s operand, 64 for the t operand) and 32-byte
+// K chunk c, one contiguous block [a][r][32 bytes] (slice a, row r) in the
+// 32-byte-swizzled K-major layout the MMA descriptors read (the two 16-byte
+// halves of row r swapped when r / 4 is odd), so one bulk copy stages it.  CTA = 32 nodes x 64
+// subjects; digits through shared memory, global writes in 16-byte segments.
+__device__ inline void oz_digits(double x, int ex, std::int8_t (&d)[kOzS]) {
+  double r = ldexp(x, -ex);  // |r| <= 127/128
+#pragma unroll
+  for (int a = 0; a < kOzS; ++a) {
+    const double t = r * 128.0;
+    const double dgt = rint(t);
+    r = t - dgt;
+    d[a] = static_cast<std::int8_t>(static_cast<int>(dgt));
+  }
+}
+
+// X (the weighted operand, 128-row blocks) covers global rows [row0, row1)
+// from local row 0; Y (64-row blocks) covers every row.
+__global__ void __launch_bounds__(256) k_oz_slice(const double* __restrict__ A, i64 K, i64 M, i64 lda,
+                                                  const double* __restrict__ w,
+                                                  const unsigned long long* __restrict__ ex,
+                                                  const unsigned long long* __restrict__ ey,
+                                                  std::int8_t* __restrict__ xs, std::int8_t* __restrict__ ys,
+                                                  i64 rows_x, i64 rows_y, i64 nch, i64 row0, i64 row1) {
+  __shared__ __align__(16) std::int8_t dig[2][kOzS][32][64 + 16];
+  const i64 m0 = static_cast<i64>(blockIdx.x) * 32, k0 = static_cast<i64>(blockIdx.y) * 64;
+  for (int e = threadIdx.x; e < 32 * 64; e += blockDim.x) {
+    const int kk = e / 32, mm = e % 32;
+    const i64 m = m0 + mm, k = k0 + kk;
+    double a = 0.0, aw = 0.0;
+    int eA = 0, eW = 0;
+    if (m < M && k < K) {
+      a = A[k * lda + m];
+      eA = oz_exponent(ey[m]);
+    }
+    const i64 mx = row0 + m;
+    if (mx < row1 && k < K) {
+      aw = __dmul_rn(w[k], A[k * lda + mx]);
+      eW = oz_exponent(ex[mx]);
+    }
+    std::int8_t dx[kOzS], dy[kOzS];
+    oz_digits(aw, eW, dx);
+    oz_digits(a, eA, dy);
+#pragma unroll
+    for (int s = 0; s < kOzS; ++s) {
+      dig[0][s][mm][kk] = dx[s];
+      dig[1][s][mm][kk] = dy[s];
+    }
+  }
+  __syncthreads();
+  // per operand: 8 slices x 32 rows x 4 segments of 16 bytes (2 chunks of 2)
+  for (int e = threadIdx.x; e < 2 * kOzS * 32 * 4; e += blockDim.x) {
+    const int op = e / (kOzS * 128), a = (e / 128) % kOzS, mm = (e / 4) % 32, sg = e % 4;
+    const i64 m = m0 + mm;
+    const int R = op == 0 ? kOzM : kOzN;
+    if (m >= (op == 0 ? rows_x : rows_y)) continue;
+    const i64 rb = m / R, r = m % R, c = (k0 >> 5) + (sg >> 1), g = sg & 1;
+    const int4 v = *reinterpret_cast<const int4*>(&dig[op][a][mm][sg * 16]);
+    std::int8_t* base = op == 0 ? xs : ys;
+    // row r holds its 32 K bytes contiguously; 32-byte swizzle: the 16-byte
+    // half g is stored at g ^ (r / 4 % 2)
+    *reinterpret_cast<int4*>(base + ((rb * nch + c) * kOzS + a) * (R * 32) + r * 32 + ((g ^ ((r >> 2) & 1)) << 4)) = v;
+  }
+}
+
+__global__ void k_oz_scales(const unsigned long long* __restrict__ emax, i64 M, double* __restrict__ scale) {
+  const i64 m = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (m < M) scale[m] = ldexp(1.0, oz_exponent(emax[m]));
+}
+
+// ---- the product -----------------------------------------------------------
+
+// tiles[i] = (I, J): s rows [128 I, 128 I + 128), t columns [64 J, 64 J + 64).
+// Warp-specialized: warp 0 (one lane) streams the (tile, chunk) blocks into a
+// 4-stage ring with bulk copies; warp 1 (one lane) issues the 36 slice-pair
+// MMAs of each chunk and commits them to the stage's "empty" barrier, and the
+// tile's last chunk to "tmem full"; warps 2..5 drain the 8 accumulators
+// (tcgen05.ld), convert, scale and store, then release TMEM for the next tile.
+__global__ void __launch_bounds__(kOzThreads, 1)
+    k_oz_syrk(const std::int8_t* __restrict__ xs, const std::int8_t* __restrict__ ys, i64 nch,
+              const double* __restrict__ sx, const double* __restrict__ sy, i64 M, double* __restrict__ C, i64 ldc,
+              const int2* __restrict__ tiles, int n_tiles, i64 row0, i64 row1) {
+  extern __shared__ __align__(16) std::uint8_t oz_sm[];
+  __shared__ __align__(8) std::uint64_t full[kOzStages], empty[kOzStages], tmem_full, tmem_empty;
+  __shared__ unsigned tmem_base_sh;
+  std::uint8_t* sm = reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(oz_sm) + 1023) &
+                                                     ~static_cast<std::uintptr_t>(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(oz_smem(&tmem_base_sh)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 32) {
+    for (int i = 0; i < kOzStages; ++i) {
+      oz_mbar_init_n(&full[i], 1);
+      oz_mbar_init_n(&empty[i], 1);
+    }
+    oz_mbar_init_n(&tmem_full, 1);
+    oz_mbar_init_n(&tmem_empty, 4);  // one arrival per epilogue warp
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const unsigned tmem = tmem_base_sh;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer
+      int st = 0;
+      unsigned ph = 0;
+      for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
+        const int2 tl = tiles[ti];
+        const std::int8_t* xa = xs + static_cast<i64>(tl.x) * nch * kOzBlkA;
+        const std::int8_t* yb = ys + static_cast<i64>(tl.y) * nch * kOzBlkB;
+        for (i64 c = 0; c < nch; ++c) {
+          oz_mbar_wait(&empty[st], ph ^ 1u);  // first pass: passes at once
+          std::uint8_t* dst = sm + st * kOzStage;
+          oz_mbar_expect(&full[st], kOzStage);
+          oz_bulk(dst, xa + c * kOzBlkA, kOzBlkA, &full[st]);
+          oz_bulk(dst + kOzBlkA, yb + c * kOzBlkB, kOzBlkB, &full[st]);
+          if (++st == kOzStages) {
+            st = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // MMA issuer: the whole warp runs the loop (so the descriptors and TMEM
+    // addresses stay warp-uniform, in uniform registers) and one elected lane
+    // issues the instructions
+    const unsigned tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const unsigned smem0 = __shfl_sync(0xffffffffu, oz_smem(sm), 0);
+    int st = 0;
+    unsigned ph = 0, tph = 0;
+    for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
+      oz_mbar_wait(&tmem_empty, tph ^ 1u);  // the epilogue has drained the previous tile
+      tph ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      for (i64 c = 0; c < nch; ++c) {
+        oz_mbar_wait(&full[st], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        const unsigned a_base = smem0 + st * kOzStage, b_base = a_base + kOzBlkA;
+        const std::uint64_t da0 = oz_desc(a_base, 16, 256), db0 = oz_desc(b_base, 16, 256);
+        const bool first = c == 0;
+        if (oz_elect()) {
+#pragma unroll
+          for (int xa = 0; xa < kOzS; ++xa)
+#pragma unroll
+            for (int yb = 0; yb < kOzS; ++yb) {
+              if (xa + yb > kOzS - 1) continue;  // a + b <= S + 1 (1-based)
+              const int d = xa + yb;
+              // chunk 0: the first pair of each accumulator (xa == 0) overwrites it
+              const bool acc = !(first && xa == 0);
+              oz_mma(tm + d * kOzN, da0 + ((xa * kOzM * 32) >> 4), db0 + ((yb * kOzN * 32) >> 4), acc);
+            }
+          oz_commit_mbar(&empty[st]);
+          if (c == nch - 1) oz_commit_mbar(&tmem_full);
+        }
+        __syncwarp();
+        if (++st == kOzStages) {
+          st = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+  } else {  // epilogue warps 2..5: TMEM lane quadrant q = warp % 4
+    const int q = warp & 3;
+    unsigned tph = 0;
+    for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
+      const int2 tl = tiles[ti];
+      const i64 s0 = row0 + static_cast<i64>(tl.x) * kOzM, t0 = static_cast<i64>(tl.y) * kOzN;
+      oz_mbar_wait(&tmem_full, tph);
+      tph ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      const i64 s = s0 + q * 32 + lane;
+      // read all 8 accumulators out (64 columns of this lane) and combine:
+      // acc = sum_d 2^-7(d+2) P_d, in ascending d (deterministic)
+      double acc[kOzN];
+#pragma unroll
+      for (int n = 0; n < kOzN; ++n) acc[n] = 0.0;
+#pragma unroll 1
+      for (int d = 0; d < kOzS; ++d) {
+        int v0[32], v1[32];
+        const unsigned ta = tmem + (static_cast<unsigned>(q * 32) << 16) + d * kOzN;
+        oz_tmem_ld32(ta, v0);
+        oz_tmem_ld32(ta + 32, v1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        const double pw = ldexp(1.0, -7 * (d + 2));
+#pragma unroll
+        for (int n = 0; n < 32; ++n) {
+          acc[n] = fma(static_cast<double>(v0[n]), pw, acc[n]);
+          acc[32 + n] = fma(static_cast<double>(v1[n]), pw, acc[32 + n]);
+        }
+      }
+      // TMEM read out: the MMA warp may start the next tile while this one stores
+      asm volatile("tcgen05.fence::before_thread_sync;\n");
+      __syncwarp();
+      if (lane == 0) oz_mbar_arrive(&tmem_empty);
+      // row s of the slab: every t >= s; the mirror (t, s) when row t is in
+      // the slab too (C's row 0 is global row row0)
+      if (s < row1) {
+        const double fs = sx[s];
+#pragma unroll 8
+        for (int n = 0; n < kOzN; ++n) {
+          const i64 t = t0 + n;
+          if (t < M && s <= t) {
+            const double val = acc[n] * fs * sy[t];
+            C[(s - row0) * ldc + t] = val;
+            if (t < row1) C[(t - row0) * ldc + s] = val;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
+}  // namespace
+
+bool ozaki_enabled() {
+  const char* e = std::getenv("DFPCA_SYRK");
+  return !(e && std::string(e) == "dmma");
+}
+
+bool ozaki_syrk(dfpca_context* ctx, i64 G, i64 K, const double* A, i64 lda, const double* w, double* C, i64 ldc,
+                i64 row0, i64 row1) {
+  if (K <= 0 || K > kOzMaxK || G <= 0 || !w) return false;
+  row1 = std::min(row1, G);
+  if (row0 >= row1) return true;
+  const i64 Kp = (K + 63) / 64 * 64;
+  const i64 nch = Kp / kOzKc;
+  const i64 RA = (row1 - row0 + kOzM - 1) / kOzM, RB = (G + kOzN - 1) / kOzN;  // row blocks of X (slab), Y
+  DevBuf<std::int8_t> xs(static_cast<std::size_t>(RA * nch * kOzBlkA)), ys(static_cast<std::size_t>(RB * nch * kOzBlkB));
+  DevBuf<unsigned long long> ex(static_cast<std::size_t>(G)), ey(static_cast<std::size_t>(G));
+  DevBuf<double> sx(static_cast<std::size_t>(G)), sy(static_cast<std::size_t>(G));
+  cudaStream_t st = ctx->stream;
+  DFPCA_CUDA(cudaMemsetAsync(ex.get(), 0, sizeof(unsigned long long) * G, st));
+  DFPCA_CUDA(cudaMemsetAsync(ey.get(), 0, sizeof(unsigned long long) * G, st));
+  const dim3 gmax(static_cast<unsigned>((G + 255) / 256), static_cast<unsigned>(std::min<i64>(K, 64)));
+  DFPCA_LAUNCH(ctx, k_oz_colmax, gmax, 256, 0, A, K, G, lda, w, ex.get(), ey.get());
+  // every row of the padded row blocks is written (zeros past the rows and past K)
+  const i64 rows_x = RA * kOzM, rows_y = RB * kOzN;
+  const dim3 gs(static_cast<unsigned>((std::max(rows_x, rows_y) + 31) / 32), static_cast<unsigned>(Kp / 64));
+  DFPCA_LAUNCH(ctx, k_oz_slice, gs, 256, 0, A, K, G, lda, w, ex.get(), ey.get(), xs.get(), ys.get(), rows_x, rows_y,
+               nch, row0, row1);
+  DFPCA_LAUNCH(ctx, k_oz_scales, grid_for(G, 256), 256, 0, ex.get(), G, sx.get());
+  DFPCA_LAUNCH(ctx, k_oz_scales, grid_for(G, 256), 256, 0, ey.get(), G, sy.get());
+  // tiles: I (128 slab rows from row0), J (64 columns) holding some t >= s
+  std::vector<int2> tiles;
+  for (i64 I = 0; I < RA; ++I)
+    for (i64 J = 0; J < RB; ++J)
+      if (J * kOzN + kOzN - 1 >= row0 + I * kOzM) tiles.push_back(make_int2(static_cast<int>(I), static_cast<int>(J)));
+  DevBuf<int2> d_tiles(tiles.size());
+  DFPCA_CUDA(cudaMemcpyAsync(d_tiles.get(), tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, st));
+  allow_smem(k_oz_syrk, kOzSmem);
+  const unsigned grid = static_cast<unsigned>(std::min<i64>(static_cast<i64>(tiles.size()), ctx->sm_count));
+  DFPCA_LAUNCH(ctx, k_oz_syrk, grid, kOzThreads, kOzSmem, xs.get(), ys.get(), nch, sx.get(), sy.get(), G, C, ldc,
+               d_tiles.get(), static_cast<int>(tiles.size()), row0, row1);
+  return true;
+}
+
+}  // namespace dfpca_gpu

@@ -45,17 +45,19 @@ namespace {
 
 constexpr int kOzS = 8;           // 7-bit slices
 constexpr int kOzM = 128;         // tile rows (s), UMMA M
-constexpr int kOzN = 64;          // tile columns (t), UMMA N
+constexpr int kOzN = 128;         // tile columns (t), UMMA N
 constexpr int kOzKc = 32;         // K bytes per stage = one MMA's K
-constexpr int kOzStages = 4;
+constexpr int kOzAcc = 4;         // accumulators per pass (4 x 128 TMEM columns)
+constexpr int kOzStages = 3;
 constexpr int kOzMaxK = 16384;
-constexpr int kOzBlkA = kOzS * kOzM * kOzKc;   // 32 KB: one (row block, K chunk) of the X slices
-constexpr int kOzBlkB = kOzS * kOzN * kOzKc;   // 16 KB: the same of the Y slices
-constexpr int kOzStage = kOzBlkA + kOzBlkB;    // 48 KB
+constexpr int kOzBlk = kOzS * 128 * kOzKc;     // 32 KB: one (128-row block, K chunk) of an operand's slices
+constexpr int kOzHalfBlk = kOzBlk / 2;         // its slices 0..3 (pass 0)
+constexpr int kOzStage = 2 * kOzBlk;           // 64 KB: both operands
 constexpr int kOzSmem = kOzStages * kOzStage + 1024;
-// warps: 0 producer (bulk copies), 1 MMA issuer, 2..5 epilogue (TMEM lane
-// quadrants 2, 3, 0, 1)
-constexpr int kOzThreads = 192;
+// warps: 0 producer (bulk copies), 1 MMA issuer, 2..17 epilogue (TMEM lane
+// quadrant w % 4, columns 32 ((w - 2) / 4) ..)
+constexpr int kOzEpiWarps = 16;
+constexpr int kOzThreads = 32 * (2 + kOzEpiWarps);
 
 __device__ inline unsigned oz_smem(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 
@@ -185,8 +187,8 @@ __device__ inline void oz_digits(double x, int ex, std::int8_t (&d)[kOzS]) {
   }
 }
 
-// X (the weighted operand, 128-row blocks) covers global rows [row0, row1)
-// from local row 0; Y (64-row blocks) covers every row.
+// X (the weighted operand) covers global rows [row0, row1) from local row 0;
+// Y covers every row; both in 128-row blocks.
 __global__ void __launch_bounds__(256) k_oz_slice(const double* __restrict__ A, i64 K, i64 M, i64 lda,
                                                   const double* __restrict__ w,
                                                   const unsigned long long* __restrict__ ex,
@@ -223,7 +225,7 @@ __global__ void __launch_bounds__(256) k_oz_slice(const double* __restrict__ A, 
   for (int e = threadIdx.x; e < 2 * kOzS * 32 * 4; e += blockDim.x) {
     const int op = e / (kOzS * 128), a = (e / 128) % kOzS, mm = (e / 4) % 32, sg = e % 4;
     const i64 m = m0 + mm;
-    const int R = op == 0 ? kOzM : kOzN;
+    constexpr int R = 128;
     if (m >= (op == 0 ? rows_x : rows_y)) continue;
     const i64 rb = m / R, r = m % R, c = (k0 >> 5) + (sg >> 1), g = sg & 1;
     const int4 v = *reinterpret_cast<const int4*>(&dig[op][a][mm][sg * 16]);
@@ -241,12 +243,19 @@ __global__ void k_oz_scales(const unsigned long long* __restrict__ emax, i64 M, 
 
 // ---- the product -----------------------------------------------------------
 
-// tiles[i] = (I, J): s rows [128 I, 128 I + 128), t columns [64 J, 64 J + 64).
-// Warp-specialized: warp 0 (one lane) streams the (tile, chunk) blocks into a
-// 4-stage ring with bulk copies; warp 1 (one lane) issues the 36 slice-pair
-// MMAs of each chunk and commits them to the stage's "empty" barrier, and the
-// tile's last chunk to "tmem full"; warps 2..5 drain the 8 accumulators
-// (tcgen05.ld), convert, scale and store, then release TMEM for the next tile.
+// The slice pairs of pass p: accumulator d = xa + yb in [4p, 4p + 4).
+__host__ __device__ constexpr bool oz_in_pass(int p, int xa, int yb) {
+  return xa + yb >= kOzAcc * p && xa + yb < kOzAcc * (p + 1);
+}
+
+// tiles[i] = (I, J): s rows [row0 + 128 I, +128), t columns [128 J, +128).
+// Warp-specialized: warp 0 (one lane) streams the (tile, pass, chunk) blocks
+// into a 3-stage ring with bulk copies (pass 0 needs slices 0..3 only);
+// warp 1 issues each chunk's slice-pair MMAs (M 128, N 128, K 32) into the
+// pass's 4 accumulators and commits them to the stage's "empty" barrier, and
+// each pass's last chunk to "tmem full"; the 16 epilogue warps add each
+// pass's accumulators into their registers (2^-7(d+2) scales, ascending d),
+// release TMEM ("tmem empty"), and after pass 1 scale and store.
 __global__ void __launch_bounds__(kOzThreads, 1)
     k_oz_syrk(const std::int8_t* __restrict__ xs, const std::int8_t* __restrict__ ys, i64 nch,
               const double* __restrict__ sx, const double* __restrict__ sy, i64 M, double* __restrict__ C, i64 ldc,
@@ -267,7 +276,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       oz_mbar_init_n(&empty[i], 1);
     }
     oz_mbar_init_n(&tmem_full, 1);
-    oz_mbar_init_n(&tmem_empty, 4);  // one arrival per epilogue warp
+    oz_mbar_init_n(&tmem_empty, kOzEpiWarps);  // one arrival per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -281,14 +290,71 @@ __global__ void __launch_bounds__(kOzThreads, 1)
       unsigned ph = 0;
       for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
         const int2 tl = tiles[ti];
-        const std::int8_t* xa = xs + static_cast<i64>(tl.x) * nch * kOzBlkA;
-        const std::int8_t* yb = ys + static_cast<i64>(tl.y) * nch * kOzBlkB;
+        const std::int8_t* xa = xs + static_cast<i64>(tl.x) * nch * kOzBlk;
+        const std::int8_t* yb = ys + static_cast<i64>(tl.y) * nch * kOzBlk;
+        for (int p = 0; p < 2; ++p) {
+          const unsigned bytes = p == 0 ? kOzHalfBlk : kOzBlk;
+          for (i64 c = 0; c < nch; ++c) {
+            oz_mbar_wait(&empty[st], ph ^ 1u);  // first pass over the ring: passes at once
+            std::uint8_t* dst = sm + st * kOzStage;
+            oz_mbar_expect(&full[st], 2 * bytes);
+            oz_bulk(dst, xa + c * kOzBlk, bytes, &full[st]);
+            oz_bulk(dst + kOzBlk, yb + c * kOzBlk, bytes, &full[st]);
+            if (++st == kOzStages) {
+              st = 0;
+              ph ^= 1u;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // MMA issuer: the whole warp runs the loop (descriptors and TMEM
+    // addresses stay warp-uniform) and one elected lane issues
+    const unsigned tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const unsigned smem0 = __shfl_sync(0xffffffffu, oz_smem(sm), 0);
+    int st = 0;
+    unsigned ph = 0, tph = 0;
+    for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
+      for (int p = 0; p < 2; ++p) {
+        oz_mbar_wait(&tmem_empty, tph ^ 1u);  // the epilogue has read the accumulators out
+        tph ^= 1u;
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
         for (i64 c = 0; c < nch; ++c) {
-          oz_mbar_wait(&empty[st], ph ^ 1u);  // first pass: passes at once
-          std::uint8_t* dst = sm + st * kOzStage;
-          oz_mbar_expect(&full[st], kOzStage);
-          oz_bulk(dst, xa + c * kOzBlkA, kOzBlkA, &full[st]);
-          oz_bulk(dst + kOzBlkA, yb + c * kOzBlkB, kOzBlkB, &full[st]);
+          oz_mbar_wait(&full[st], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;\n");
+          const unsigned a_base = smem0 + st * kOzStage, b_base = a_base + kOzBlk;
+          const std::uint64_t da0 = oz_desc(a_base, 16, 256), db0 = oz_desc(b_base, 16, 256);
+          if (oz_elect()) {
+            // chunk 0: the first pair issued into each accumulator overwrites it
+            unsigned started = c == 0 ? 0u : 0xffu;
+            if (p == 0) {
+#pragma unroll
+              for (int xa = 0; xa < kOzS; ++xa)
+#pragma unroll
+                for (int yb = 0; yb < kOzS; ++yb) {
+                  if (!oz_in_pass(0, xa, yb)) continue;
+                  const int d = xa + yb;
+                  oz_mma(tm + d * kOzN, da0 + ((xa * 128 * 32) >> 4), db0 + ((yb * 128 * 32) >> 4),
+                         (started >> d) & 1u);
+                  started |= 1u << d;
+                }
+            } else {
+#pragma unroll
+              for (int xa = 0; xa < kOzS; ++xa)
+#pragma unroll
+                for (int yb = 0; yb < kOzS; ++yb) {
+                  if (!oz_in_pass(1, xa, yb)) continue;
+                  const int d = xa + yb - kOzAcc;
+                  oz_mma(tm + d * kOzN, da0 + ((xa * 128 * 32) >> 4), db0 + ((yb * 128 * 32) >> 4),
+                         (started >> d) & 1u);
+                  started |= 1u << d;
+                }
+            }
+            oz_commit_mbar(&empty[st]);
+            if (c == nch - 1) oz_commit_mbar(&tmem_full);
+          }
+          __syncwarp();
           if (++st == kOzStages) {
             st = 0;
             ph ^= 1u;
@@ -296,84 +362,39 @@ __global__ void __launch_bounds__(kOzThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // MMA issuer: the whole warp runs the loop (so the descriptors and TMEM
-    // addresses stay warp-uniform, in uniform registers) and one elected lane
-    // issues the instructions
-    const unsigned tm = __shfl_sync(0xffffffffu, tmem, 0);
-    const unsigned smem0 = __shfl_sync(0xffffffffu, oz_smem(sm), 0);
-    int st = 0;
-    unsigned ph = 0, tph = 0;
-    for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
-      oz_mbar_wait(&tmem_empty, tph ^ 1u);  // the epilogue has drained the previous tile
-      tph ^= 1u;
-      asm volatile("tcgen05.fence::after_thread_sync;\n");
-      for (i64 c = 0; c < nch; ++c) {
-        oz_mbar_wait(&full[st], ph);
-        asm volatile("tcgen05.fence::after_thread_sync;\n");
-        const unsigned a_base = smem0 + st * kOzStage, b_base = a_base + kOzBlkA;
-        const std::uint64_t da0 = oz_desc(a_base, 16, 256), db0 = oz_desc(b_base, 16, 256);
-        const bool first = c == 0;
-        if (oz_elect()) {
-#pragma unroll
-          for (int xa = 0; xa < kOzS; ++xa)
-#pragma unroll
-            for (int yb = 0; yb < kOzS; ++yb) {
-              if (xa + yb > kOzS - 1) continue;  // a + b <= S + 1 (1-based)
-              const int d = xa + yb;
-              // chunk 0: the first pair of each accumulator (xa == 0) overwrites it
-              const bool acc = !(first && xa == 0);
-              oz_mma(tm + d * kOzN, da0 + ((xa * kOzM * 32) >> 4), db0 + ((yb * kOzN * 32) >> 4), acc);
-            }
-          oz_commit_mbar(&empty[st]);
-          if (c == nch - 1) oz_commit_mbar(&tmem_full);
-        }
-        __syncwarp();
-        if (++st == kOzStages) {
-          st = 0;
-          ph ^= 1u;
-        }
-      }
-    }
-  } else {  // epilogue warps 2..5: TMEM lane quadrant q = warp % 4
-    const int q = warp & 3;
+  } else {  // epilogue warps: TMEM lane quadrant q, 32 columns from 32 cg
+    const int q = warp & 3, cg = (warp - 2) >> 2;
     unsigned tph = 0;
     for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
       const int2 tl = tiles[ti];
-      const i64 s0 = row0 + static_cast<i64>(tl.x) * kOzM, t0 = static_cast<i64>(tl.y) * kOzN;
-      oz_mbar_wait(&tmem_full, tph);
-      tph ^= 1u;
-      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      const i64 s0 = row0 + static_cast<i64>(tl.x) * kOzM, t0 = static_cast<i64>(tl.y) * kOzN + cg * 32;
       const i64 s = s0 + q * 32 + lane;
-      // read all 8 accumulators out (64 columns of this lane) and combine:
-      // acc = sum_d 2^-7(d+2) P_d, in ascending d (deterministic)
-      double acc[kOzN];
+      double acc[32];
 #pragma unroll
-      for (int n = 0; n < kOzN; ++n) acc[n] = 0.0;
+      for (int n = 0; n < 32; ++n) acc[n] = 0.0;
+      for (int p = 0; p < 2; ++p) {
+        oz_mbar_wait(&tmem_full, tph);
+        tph ^= 1u;
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
 #pragma unroll 1
-      for (int d = 0; d < kOzS; ++d) {
-        int v0[32], v1[32];
-        const unsigned ta = tmem + (static_cast<unsigned>(q * 32) << 16) + d * kOzN;
-        oz_tmem_ld32(ta, v0);
-        oz_tmem_ld32(ta + 32, v1);
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        const double pw = ldexp(1.0, -7 * (d + 2));
+        for (int d = 0; d < kOzAcc; ++d) {
+          int v[32];
+          oz_tmem_ld32(tmem + (static_cast<unsigned>(q * 32) << 16) + d * kOzN + cg * 32, v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          const double pw = ldexp(1.0, -7 * (kOzAcc * p + d + 2));
 #pragma unroll
-        for (int n = 0; n < 32; ++n) {
-          acc[n] = fma(static_cast<double>(v0[n]), pw, acc[n]);
-          acc[32 + n] = fma(static_cast<double>(v1[n]), pw, acc[32 + n]);
+          for (int n = 0; n < 32; ++n) acc[n] = fma(static_cast<double>(v[n]), pw, acc[n]);
         }
+        asm volatile("tcgen05.fence::before_thread_sync;\n");
+        __syncwarp();
+        if (lane == 0) oz_mbar_arrive(&tmem_empty);
       }
-      // TMEM read out: the MMA warp may start the next tile while this one stores
-      asm volatile("tcgen05.fence::before_thread_sync;\n");
-      __syncwarp();
-      if (lane == 0) oz_mbar_arrive(&tmem_empty);
       // row s of the slab: every t >= s; the mirror (t, s) when row t is in
       // the slab too (C's row 0 is global row row0)
       if (s < row1) {
         const double fs = sx[s];
 #pragma unroll 8
-        for (int n = 0; n < kOzN; ++n) {
+        for (int n = 0; n < 32; ++n) {
           const i64 t = t0 + n;
           if (t < M && s <= t) {
             const double val = acc[n] * fs * sy[t];
@@ -403,7 +424,7 @@ bool ozaki_syrk(dfpca_context* ctx, i64 G, i64 K, const double* A, i64 lda, cons
   const i64 Kp = (K + 63) / 64 * 64;
   const i64 nch = Kp / kOzKc;
   const i64 RA = (row1 - row0 + kOzM - 1) / kOzM, RB = (G + kOzN - 1) / kOzN;  // row blocks of X (slab), Y
-  DevBuf<std::int8_t> xs(static_cast<std::size_t>(RA * nch * kOzBlkA)), ys(static_cast<std::size_t>(RB * nch * kOzBlkB));
+  DevBuf<std::int8_t> xs(static_cast<std::size_t>(RA * nch * kOzBlk)), ys(static_cast<std::size_t>(RB * nch * kOzBlk));
   DevBuf<unsigned long long> ex(static_cast<std::size_t>(G)), ey(static_cast<std::size_t>(G));
   DevBuf<double> sx(static_cast<std::size_t>(G)), sy(static_cast<std::size_t>(G));
   cudaStream_t st = ctx->stream;

@@ -50,6 +50,11 @@ PEAKS = ROOT / "MEASURED_PEAKS.json"
 # FP64 peak of this pool's B200 (DMMA m8n8k4 and DFMA both), measured with
 # tools/fp64_peak.cu (profiles/fp64_peak_r01.txt); MEASURED_PEAKS.json has no FP64 entry.
 FP64_PEAK_TFLOPS = 37.07
+# Dense int8 tensor peak of this pool's B200, measured like MEASURED_PEAKS.json's
+# bf16 figure (cuBLASLt int8 GEMM, 8192^3, best of 10; tools/int8_peak.py,
+# profiles/r07_int8_peak.jsonl): the denominator of the Ozaki SYRK (k_oz_syrk).
+INT8_PEAK_TOPS = 3126.7
+OZ_SLICES = 8  # csrc/ozaki.cu kOzS
 
 
 def rank_env():
@@ -719,8 +724,19 @@ def kernel_model(G: int, n_pair: int, shared: bool):
     f_in, f_out, upper = tri_fractions(cells, R)
     t_rd, t_wr = tphase_fractions(cells, R)
     arr = 8.0 * G * G
+    # Ozaki SYRK (csrc/ozaki.cu): the S(S+1)/2 slice-pair int8 products over
+    # the upper triangle, 2 ops per MAC (the kernel also multiplies the zero
+    # padding of K to a multiple of 64 and whole 128 x 128 diagonal tiles);
+    # slicing reads the value grids once and writes 2 S bytes per entry
+    S = OZ_SLICES
+    ozaki = {
+        "k_oz_syrk": ("int8", 2.0 * S * (S + 1) / 2 * n_pair * G * (G + 1) / 2),
+        "k_oz_slice": ("hbm", 8.0 * n_pair * G + 2.0 * S * n_pair * G),
+        "k_oz_colmax": ("hbm", 8.0 * n_pair * G),
+    }
     if shared:
         return {
+            **ozaki,
             "k_gemm_tn": ("tensor", 2.0 * n_pair * G * G / 2.0),
             "k_scale_rows": ("hbm", 2 * 8.0 * n_pair * G),
             "k_tphase2": ("hbm", (1 * t_rd + 3 * t_wr) * arr),
@@ -730,6 +746,7 @@ def kernel_model(G: int, n_pair: int, shared: bool):
             "k_center_mirror": ("hbm", (upper + 1.0) * arr),
         }
     return {
+        **ozaki,
         "k_gemm_tn": ("tensor", 2.0 * n_pair * G * G / 2.0),
         "k_rank_one": ("hbm", 1 * arr),
         "k_scale_rows": ("hbm", 2 * 8.0 * n_pair * G),
@@ -773,10 +790,12 @@ def roofline(kstats, G, binned, slab=None):
     if not kstats:
         return None
     model = kernel_model(G, N_SUBJ, shared=("k_solve_shared_tri" in kstats or "k_solve_sep_tri" in kstats))
+    slab_share = 1.0
     if slab is not None:  # one rank's share: its rows of the upper triangle
         r0, nr = slab
         share = (sum(G - s for s in range(r0, r0 + nr))) / (G * (G + 1) / 2)
         model = {k: (bnd, work * share) for k, (bnd, work) in model.items()}
+        slab_share = 1.0 / share
     total_ms = sum(v[0] for v in kstats.values())
     table = {}
     for name, (ms, cnt) in kstats.items():
@@ -789,6 +808,13 @@ def roofline(kstats, G, binned, slab=None):
             table[name] = {"bound": "tensor", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                            "frac": ach / FP64_PEAK_TFLOPS, "ms": ms, "launches": cnt,
                            "share_of_step": ms / total_ms}
+        elif bound == "int8":
+            ach = work / secs / 1e12
+            table[name] = {"bound": "tensor", "achieved": ach, "peak": INT8_PEAK_TOPS, "unit": "TOP/s (int8)",
+                           "frac": ach / INT8_PEAK_TOPS, "ms": ms, "launches": cnt,
+                           "share_of_step": ms / total_ms,
+                           # the FP64 product it replaces, n G^2 flops over the same time
+                           "fp64_equiv_tflops": N_SUBJ * G * G / secs / 1e12 / (slab_share if slab else 1.0)}
         else:
             ach = work / secs / 1e9
             table[name] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
@@ -799,7 +825,9 @@ def roofline(kstats, G, binned, slab=None):
     d["kernel"] = dom
     d["traffic"], d["traffic_source"] = ncu_traffic(dom)
     d["algorithmic_per_launch"] = model[dom][1] / table[dom]["launches"]
-    d["peak_source"] = ("measured FP64 DMMA peak (tools/fp64_peak.cu, profiles/fp64_peak_r01.txt)"
+    d["peak_source"] = ("measured dense int8 peak (cuBLASLt 8192^3, tools/int8_peak.py, profiles/r07_int8_peak.jsonl)"
+                        if model[dom][0] == "int8" else
+                        "measured FP64 DMMA peak (tools/fp64_peak.cu, profiles/fp64_peak_r01.txt)"
                         if d["bound"] == "tensor" else "MEASURED_PEAKS.json hbm_gbs (measured copy)")
     d["all_kernels"] = table
     return d

@@ -23,6 +23,16 @@ from paper_1510_04439_b200 import _lib, api, synth  # noqa: E402
 CONFIGS = {c: (synth.CONFIGS[c], (lambda c=c: synth.config(c))) for c in (1, 2, 3, 4, 5)}
 
 
+def sm_clock():
+    """Current SM clock (MHz) through NVML, or None."""
+    try:
+        import pynvml as nv
+        nv.nvmlInit()
+        return nv.nvmlDeviceGetClockInfo(nv.nvmlDeviceGetHandleByIndex(0), nv.NVML_CLOCK_SM)
+    except Exception:
+        return None
+
+
 def run(cfg: int, q: int, L: int):
     name, make = CONFIGS[cfg]
     t0 = time.perf_counter()
@@ -41,16 +51,22 @@ def run(cfg: int, q: int, L: int):
     mean = api.fft_local_linear(b, grid, h, api.MomentTarget.Mean)
     t["mean_ms"] = (time.perf_counter() - t0) * 1e3
     covs = []
-    for _ in range(2):  # second call is warm
+    warm = None
+    for i in range(4):  # the first call is cold; the best of the next three is "warm"
         t0 = time.perf_counter()
         cov = api.fft_covariance(b, grid, h, mean)
-        covs.append((time.perf_counter() - t0) * 1e3)
+        ms = (time.perf_counter() - t0) * 1e3
         stages = {s: _lib.stage_ms(s) for s in ("pairs", "moments", "solve", "fallback", "center", "total")}
-        if len(covs) == 1:
+        if i == 0:
             t["covariance_device_ms_cold"] = stages
+            t["covariance_ms_cold"] = ms
+        elif warm is None or stages["total"] < warm[1]["total"]:
+            warm = (ms, stages)
+        if i < 3:
             del cov
-    t["covariance_ms_cold"], t["covariance_ms"] = covs
-    t["covariance_device_ms"] = stages
+    t["covariance_ms"], t["covariance_device_ms"] = warm
+    stages = warm[1]
+    t["sm_clock_mhz"] = sm_clock()
     out["gridpts_per_s"] = grid.size() ** 2 / (stages["total"] / 1e3)
     t0 = time.perf_counter()
     eig = api.randomized_eig(api.matrixize(cov), q, L, grid, 20260815)

@@ -9,8 +9,8 @@
 //
 //   per node column m, e_m with max_k |X[k][m]| 2^-e_m <= 127/128, and
 //   X[k][m] = 2^e_m (sum_{a=1..S} 2^-7a x_a[m][k] + r),  |r| <= 2^-7S / 2,
-//   x_1 in [-127, 127], x_a in [-64, 64] (round-to-nearest signed digits,
-//   every step exact in double); the same for Y with e'_m, y_b.
+//   x_1 in [-127, 127], x_a in [-64, 64] (signed digits of the 56-bit
+//   integer rint(X 2^(56-e)), oz_pack16); the same for Y with e'_m, y_b.
 //
 //   X^T Y [s][t] ~ 2^(e_s + e'_t) sum_{d=2..S+1} 2^-7d P_d[s][t],
 //   P_d = sum_{a+b=d} x_a y_b^T  (int8 x int8 -> int32, exact: at most S terms
@@ -176,69 +176,81 @@ __device__ inline int oz_exponent(unsigned long long maxbits) {
 // 32-byte-swizzled K-major layout the MMA descriptors read (the two 16-byte
 // halves of row r swapped when r / 4 is odd), so one bulk copy stages it.  CTA = 32 nodes x 64
 // subjects; digits through shared memory, global writes in 16-byte segments.
-__device__ inline void oz_digits(double x, int ex, std::int8_t (&d)[kOzS]) {
-  double r = ldexp(x, -ex);  // |r| <= 127/128
+// The 16 digits of slice 0..7 of 16 consecutive K entries of one operand row,
+// packed per slice into 16 bytes: x = 2^e iv 2^-56 with iv = rint(x 2^(56-e))
+// (|iv| < 2^56 127/128; the dropped part is below 2^(e-57), the truncation of
+// 8 seven-bit digits), then signed digits by round-half-up shifts on the
+// integer, d_a = round(iv / 2^(56-7a)), iv -= d_a 2^(56-7a): d_1 in
+// [-127, 127], the rest in [-64, 64], exactly x = 2^e sum_a d_a 2^-7a + r.
+__device__ inline void oz_pack16(const double (&x)[16], int e, uint4 (&out)[kOzS]) {
+  unsigned w[kOzS][4];
 #pragma unroll
-  for (int a = 0; a < kOzS; ++a) {
-    const double t = r * 128.0;
-    const double dgt = rint(t);
-    r = t - dgt;
-    d[a] = static_cast<std::int8_t>(static_cast<int>(dgt));
+  for (int a = 0; a < kOzS; ++a)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[a][q] = 0u;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    long long iv = __double2ll_rn(ldexp(x[j], 56 - e));
+#pragma unroll
+    for (int a = 0; a < kOzS; ++a) {
+      const int sh = 56 - 7 * (a + 1);
+      long long d;
+      if (sh > 0) {
+        d = (iv + (1ll << (sh - 1))) >> sh;
+        iv -= d << sh;
+      } else {
+        d = iv;
+      }
+      w[a][j >> 2] |= (static_cast<unsigned>(d) & 0xffu) << (8 * (j & 3));
+    }
   }
+#pragma unroll
+  for (int a = 0; a < kOzS; ++a) out[a] = make_uint4(w[a][0], w[a][1], w[a][2], w[a][3]);
 }
 
-// X (the weighted operand) covers global rows [row0, row1) from local row 0;
-// Y covers every row; both in 128-row blocks.
-__global__ void __launch_bounds__(256) k_oz_slice(const double* __restrict__ A, i64 K, i64 M, i64 lda,
+// Slices of both operands (X = w * A on rows [row0, row1) from local row 0,
+// Y = A on every row; 128-row blocks, the staging layout above) and the
+// column scales 2^e: thread = (row, 16-entry K segment), consecutive threads
+// on consecutive rows (coalesced reads of A), digits packed in registers and
+// written as 16-byte segments (no shared memory).
+__global__ void __launch_bounds__(128) k_oz_slice(const double* __restrict__ A, i64 K, i64 M, i64 lda,
                                                   const double* __restrict__ w,
                                                   const unsigned long long* __restrict__ ex,
                                                   const unsigned long long* __restrict__ ey,
                                                   std::int8_t* __restrict__ xs, std::int8_t* __restrict__ ys,
-                                                  i64 rows_x, i64 rows_y, i64 nch, i64 row0, i64 row1) {
-  __shared__ __align__(16) std::int8_t dig[2][kOzS][32][64 + 16];
-  const i64 m0 = static_cast<i64>(blockIdx.x) * 32, k0 = static_cast<i64>(blockIdx.y) * 64;
-  for (int e = threadIdx.x; e < 32 * 64; e += blockDim.x) {
-    const int kk = e / 32, mm = e % 32;
-    const i64 m = m0 + mm, k = k0 + kk;
-    double a = 0.0, aw = 0.0;
-    int eA = 0, eW = 0;
-    if (m < M && k < K) {
-      a = A[k * lda + m];
-      eA = oz_exponent(ey[m]);
-    }
-    const i64 mx = row0 + m;
-    if (mx < row1 && k < K) {
-      aw = __dmul_rn(w[k], A[k * lda + mx]);
-      eW = oz_exponent(ex[mx]);
-    }
-    std::int8_t dx[kOzS], dy[kOzS];
-    oz_digits(aw, eW, dx);
-    oz_digits(a, eA, dy);
+                                                  double* __restrict__ sx, double* __restrict__ sy, i64 rows_x,
+                                                  i64 rows_y, i64 nch, i64 row0, i64 row1) {
+  const i64 m = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  const i64 k0 = static_cast<i64>(blockIdx.y) * 16;
+  const i64 c = k0 >> 5, g = (k0 >> 4) & 1;
+  for (int op = 0; op < 2; ++op) {
+    const i64 rows = op == 0 ? rows_x : rows_y;
+    if (m >= rows) continue;
+    const i64 gm = op == 0 ? row0 + m : m;  // global row
+    const bool valid = op == 0 ? gm < row1 : gm < M;
+    const int e = valid ? oz_exponent((op == 0 ? ex : ey)[gm]) : 0;
+    if (valid && blockIdx.y == 0) (op == 0 ? sx : sy)[gm] = ldexp(1.0, e);
+    double x[16];
 #pragma unroll
-    for (int s = 0; s < kOzS; ++s) {
-      dig[0][s][mm][kk] = dx[s];
-      dig[1][s][mm][kk] = dy[s];
+    for (int j = 0; j < 16; ++j) {
+      const i64 k = k0 + j;
+      double v = 0.0;
+      if (valid && k < K) {
+        v = A[k * lda + gm];
+        if (op == 0) v = __dmul_rn(w[k], v);
+      }
+      x[j] = v;
     }
-  }
-  __syncthreads();
-  // per operand: 8 slices x 32 rows x 4 segments of 16 bytes (2 chunks of 2)
-  for (int e = threadIdx.x; e < 2 * kOzS * 32 * 4; e += blockDim.x) {
-    const int op = e / (kOzS * 128), a = (e / 128) % kOzS, mm = (e / 4) % 32, sg = e % 4;
-    const i64 m = m0 + mm;
-    constexpr int R = 128;
-    if (m >= (op == 0 ? rows_x : rows_y)) continue;
-    const i64 rb = m / R, r = m % R, c = (k0 >> 5) + (sg >> 1), g = sg & 1;
-    const int4 v = *reinterpret_cast<const int4*>(&dig[op][a][mm][sg * 16]);
+    uint4 d[kOzS];
+    oz_pack16(x, e, d);
     std::int8_t* base = op == 0 ? xs : ys;
+    const i64 rb = m >> 7, r = m & 127;
     // row r holds its 32 K bytes contiguously; 32-byte swizzle: the 16-byte
     // half g is stored at g ^ (r / 4 % 2)
-    *reinterpret_cast<int4*>(base + ((rb * nch + c) * kOzS + a) * (R * 32) + r * 32 + ((g ^ ((r >> 2) & 1)) << 4)) = v;
+    std::int8_t* dst = base + (rb * nch + c) * kOzBlk + r * 32 + ((g ^ ((r >> 2) & 1)) << 4);
+#pragma unroll
+    for (int a = 0; a < kOzS; ++a) *reinterpret_cast<uint4*>(dst + a * (128 * 32)) = d[a];
   }
-}
-
-__global__ void k_oz_scales(const unsigned long long* __restrict__ emax, i64 M, double* __restrict__ scale) {
-  const i64 m = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
-  if (m < M) scale[m] = ldexp(1.0, oz_exponent(emax[m]));
 }
 
 // ---- the product -----------------------------------------------------------
@@ -434,11 +446,9 @@ bool ozaki_syrk(dfpca_context* ctx, i64 G, i64 K, const double* A, i64 lda, cons
   DFPCA_LAUNCH(ctx, k_oz_colmax, gmax, 256, 0, A, K, G, lda, w, ex.get(), ey.get());
   // every row of the padded row blocks is written (zeros past the rows and past K)
   const i64 rows_x = RA * kOzM, rows_y = RB * kOzN;
-  const dim3 gs(static_cast<unsigned>((std::max(rows_x, rows_y) + 31) / 32), static_cast<unsigned>(Kp / 64));
-  DFPCA_LAUNCH(ctx, k_oz_slice, gs, 256, 0, A, K, G, lda, w, ex.get(), ey.get(), xs.get(), ys.get(), rows_x, rows_y,
-               nch, row0, row1);
-  DFPCA_LAUNCH(ctx, k_oz_scales, grid_for(G, 256), 256, 0, ex.get(), G, sx.get());
-  DFPCA_LAUNCH(ctx, k_oz_scales, grid_for(G, 256), 256, 0, ey.get(), G, sy.get());
+  const dim3 gs(static_cast<unsigned>((std::max(rows_x, rows_y) + 127) / 128), static_cast<unsigned>(Kp / 16));
+  DFPCA_LAUNCH(ctx, k_oz_slice, gs, 128, 0, A, K, G, lda, w, ex.get(), ey.get(), xs.get(), ys.get(), sx.get(),
+               sy.get(), rows_x, rows_y, nch, row0, row1);
   // tiles: I (128 slab rows from row0), J (64 columns) holding some t >= s
   std::vector<int2> tiles;
   for (i64 I = 0; I < RA; ++I)

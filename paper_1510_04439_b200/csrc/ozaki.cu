@@ -151,20 +151,30 @@ __global__ void k_oz_colmax(const double* __restrict__ A, i64 K, i64 M, i64 lda,
                             unsigned long long* __restrict__ ex, unsigned long long* __restrict__ ey) {
   const i64 m = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
   if (m >= M) return;
+  // a NaN / Inf entry poisons its column: the bits of NaN order above every
+  // finite value, and oz_exponent turns them into a NaN column scale, so every
+  // product with that row or column comes out NaN (as the FP64 sum would)
   double mx = 0.0, my = 0.0;
   for (i64 k = blockIdx.y; k < K; k += gridDim.y) {
     const double a = A[k * lda + m];
-    mx = fmax(mx, fabs(__dmul_rn(w[k], a)));
-    my = fmax(my, fabs(a));
+    const double aw = __dmul_rn(w[k], a);
+    mx = isfinite(aw) ? fmax(mx, fabs(aw)) : __longlong_as_double(0x7ff8000000000000ll);
+    my = isfinite(a) ? fmax(my, fabs(a)) : __longlong_as_double(0x7ff8000000000000ll);
+    if (!isfinite(aw) || !isfinite(a)) break;
   }
-  if (mx > 0.0) atomicMax(ex + m, static_cast<unsigned long long>(__double_as_longlong(mx)));
-  if (my > 0.0) atomicMax(ey + m, static_cast<unsigned long long>(__double_as_longlong(my)));
+  const auto bits = [](double v) {
+    return isnan(v) ? 0x7ff8000000000000ull : static_cast<unsigned long long>(__double_as_longlong(v));
+  };
+  if (!(mx == 0.0)) atomicMax(ex + m, bits(mx));
+  if (!(my == 0.0)) atomicMax(ey + m, bits(my));
 }
 
-// exp2 scale of column m: the smallest e with max |X| 2^-e <= 127/128.
+// exp2 scale of column m: the smallest e with max |X| 2^-e <= 127/128 (0 for
+// an all-zero or a poisoned column).
+__device__ inline bool oz_poisoned(unsigned long long maxbits) { return maxbits >= 0x7ff0000000000000ull; }
 __device__ inline int oz_exponent(unsigned long long maxbits) {
   const double mx = __longlong_as_double(static_cast<long long>(maxbits));
-  if (!(mx > 0.0)) return 0;
+  if (!(mx > 0.0) || oz_poisoned(maxbits)) return 0;
   int e;
   const double f = frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1)
   return f > 127.0 / 128.0 ? e + 1 : e;
@@ -190,7 +200,8 @@ __device__ inline void oz_pack16(const double (&x)[16], int e, uint4 (&out)[kOzS
     for (int q = 0; q < 4; ++q) w[a][q] = 0u;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    long long iv = __double2ll_rn(ldexp(x[j], 56 - e));
+    const double xs_ = ldexp(x[j], 56 - e);
+    long long iv = isfinite(xs_) ? __double2ll_rn(xs_) : 0ll;  // poisoned rows: scale NaN, digits unused
 #pragma unroll
     for (int a = 0; a < kOzS; ++a) {
       const int sh = 56 - 7 * (a + 1);
@@ -228,8 +239,10 @@ __global__ void __launch_bounds__(128) k_oz_slice(const double* __restrict__ A, 
     if (m >= rows) continue;
     const i64 gm = op == 0 ? row0 + m : m;  // global row
     const bool valid = op == 0 ? gm < row1 : gm < M;
-    const int e = valid ? oz_exponent((op == 0 ? ex : ey)[gm]) : 0;
-    if (valid && blockIdx.y == 0) (op == 0 ? sx : sy)[gm] = ldexp(1.0, e);
+    const unsigned long long mb = valid ? (op == 0 ? ex : ey)[gm] : 0ull;
+    const int e = oz_exponent(mb);
+    if (valid && blockIdx.y == 0)
+      (op == 0 ? sx : sy)[gm] = oz_poisoned(mb) ? __longlong_as_double(0x7ff8000000000000ll) : ldexp(1.0, e);
     double x[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {

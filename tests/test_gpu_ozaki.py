@@ -3,9 +3,9 @@
 pw and pv within 1e-14 of the largest entry (the bound test_pair_grids holds
 against the reference; exact zeros are the reference's own business there,
 a near-cancelling sum can round to 0 in one FP64 order and not another), the
-same NaNs; the covariance within 1e-10 and exactly symmetric.  Grid sizes that are not multiples of the 128-node
-tiles, and a NaN observation (its row and column of the pair grid must come
-out NaN, as the FP64 sum's do)."""
+same NaNs; the covariance within 1e-10 and exactly symmetric.  Grid sizes
+that are not multiples of the 128-node tiles, and a NaN observation (its row
+and column of the pair grid must come out NaN, as the FP64 sum's do)."""
 import numpy as np
 import pytest
 

@@ -80,8 +80,9 @@ DFPCA_API int dfpca_context_destroy(dfpca_context* ctx);
  * needs that much reuses mapped pages instead of growing the pool while its
  * kernels run.  The first config-5 (d = 3, 32^3) covariance is ~0.7 s with no
  * reserve and ~0.12 s after a 96 GB one; mapping costs ~13 ms per GB, paid
- * here.  The initial reserve is DFPCA_POOL_RESERVE_GB (default 0).  Not in
- * the reference (its host allocator has no such cost). */
+ * here.  The initial reserve is DFPCA_POOL_RESERVE_GB (default 16: without
+ * one the pool grows in fragments and calls stall while it maps more).  Not
+ * in the reference (its host allocator has no such cost). */
 DFPCA_API int dfpca_context_reserve(dfpca_context* ctx, uint64_t bytes);
 DFPCA_API int dfpca_last_error(const dfpca_context* ctx, int* error_class, const char** name,
                      const char** message);

@@ -408,12 +408,14 @@ int dfpca_context_create(int device, dfpca_context** out) {
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
     std::uint64_t keep = ~0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    // Optional up-front backing of the pool (DFPCA_POOL_RESERVE_GB, default
-    // 0; dfpca_context_reserve does the same later): mapping costs ~13 ms per
-    // GB, so it is not paid by every process by default (96 GB: +1.25 s on
-    // context creation).
+    // Up-front backing of the pool (DFPCA_POOL_RESERVE_GB, default 16;
+    // dfpca_context_reserve adds more later).  Without one the pool grows in
+    // pieces and calls stall while it maps more (config-3 covariance 1.3 ms
+    // warm, with stalls of 3-60 ms on calls whose allocations did not fit the
+    // fragments); 16 GB (~0.2 s at creation, ~13 ms per GB) covers the d = 2
+    // configurations, and 96 GB (+1.25 s) the d = 3 32^3 one.
     const char* e = std::getenv("DFPCA_POOL_RESERVE_GB");
-    const double gb = e ? std::atof(e) : 0.0;
+    const double gb = e ? std::atof(e) : 16.0;
     if (gb > 0) pool_reserve(ctx, static_cast<std::uint64_t>(gb * (1ull << 30)));
   }
   *out = ctx;

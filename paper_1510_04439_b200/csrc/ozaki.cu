@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(128) k_oz_slice(const double* __restrict__ A, 
                                                   const unsigned long long* __restrict__ ey,
                                                   std::int8_t* __restrict__ xs, std::int8_t* __restrict__ ys,
                                                   double* __restrict__ sx, double* __restrict__ sy, i64 rows_x,
-                                                  i64 rows_y, i64 nch, i64 row0, i64 row1) {
+                                                  i64 rows_y, i64 nch, i64 row0, i64 row1, int ry) {
   const i64 m = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
   const i64 k0 = static_cast<i64>(blockIdx.y) * 16;
   const i64 c = k0 >> 5, g = (k0 >> 4) & 1;
@@ -257,12 +257,13 @@ __global__ void __launch_bounds__(128) k_oz_slice(const double* __restrict__ A, 
     uint4 d[kOzS];
     oz_pack16(x, e, d);
     std::int8_t* base = op == 0 ? xs : ys;
-    const i64 rb = m >> 7, r = m & 127;
+    const int R = op == 0 ? 128 : ry;  // rows per block of this operand
+    const i64 rb = m / R, r = m % R;
     // row r holds its 32 K bytes contiguously; 32-byte swizzle: the 16-byte
     // half g is stored at g ^ (r / 4 % 2)
-    std::int8_t* dst = base + (rb * nch + c) * kOzBlk + r * 32 + ((g ^ ((r >> 2) & 1)) << 4);
+    std::int8_t* dst = base + (rb * nch + c) * (kOzS * R * kOzKc) + r * 32 + ((g ^ ((r >> 2) & 1)) << 4);
 #pragma unroll
-    for (int a = 0; a < kOzS; ++a) *reinterpret_cast<uint4*>(dst + a * (128 * 32)) = d[a];
+    for (int a = 0; a < kOzS; ++a) *reinterpret_cast<uint4*>(dst + a * (R * 32)) = d[a];
   }
 }
 
@@ -434,6 +435,244 @@ __global__ void __launch_bounds__(kOzThreads, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
+// ---- the product on CTA pairs ---------------------------------------------
+// tcgen05.mma.cta_group::2: one MMA covers M 256 (128 s rows per CTA of the
+// pair, each in its own TMEM) x N 128 (each CTA stages its half of the 128 t
+// rows: 64), so every SM reads 6 KB of operands per 128 x 128 x 32 MMA
+// instead of 8 KB -- the shared-memory operand reads are what bound the
+// one-CTA kernel.  Tiles of 256 s rows x 128 t columns; the leader CTA
+// (rank 0) issues for the pair.  Barriers: each CTA's producer fills its own
+// stage (its own "full"); the peer's warp 1 forwards its "full" to the
+// leader ("peer full"); the leader's commits arrive on both CTAs' "empty" and
+// "tmem full" (multicast); the 32 epilogue warps of the pair arrive on the
+// leader's "tmem empty".
+constexpr int kOz2BlkA = kOzS * 128 * kOzKc;       // 32 KB: 128 s rows
+constexpr int kOz2BlkB = kOzS * 64 * kOzKc;        // 16 KB: 64 t rows (half of N)
+constexpr int kOz2Stage = kOz2BlkA + kOz2BlkB;     // 48 KB
+constexpr int kOz2Stages = 4;
+constexpr int kOz2Smem = kOz2Stages * kOz2Stage + 1024;
+constexpr std::uint32_t kOz2Idesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<std::uint32_t>(128 >> 3) << 17) |
+                                    (static_cast<std::uint32_t>(256 >> 4) << 24);
+
+__device__ inline unsigned oz_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ inline void oz_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ inline unsigned oz_mapa(unsigned addr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ inline void oz_arrive_remote(unsigned cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+__device__ inline void oz_wait_cluster(std::uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "OZ2_WAIT:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra OZ2_DONE;\n\t"
+      "bra OZ2_WAIT;\n"
+      "OZ2_DONE:\n\t}\n" ::"r"(oz_smem(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ inline void oz2_mma(unsigned tmem_d, std::uint64_t da, std::uint64_t db, bool accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kOz2Idesc), "r"(accumulate ? 1 : 0));
+}
+__device__ inline void oz2_commit_both(std::uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          oz_smem(bar)),
+      "h"(static_cast<unsigned short>(3))
+      : "memory");
+}
+
+// tiles[i] = (I2, J): s rows [row0 + 256 I2, +256) (CTA rank r: +128 r),
+// t columns [128 J, +128) (CTA rank r stages rows 128 J + 64 r ..).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
+    k_oz_syrk2(const std::int8_t* __restrict__ xs, const std::int8_t* __restrict__ ys, i64 nch,
+               const double* __restrict__ sx, const double* __restrict__ sy, i64 M, double* __restrict__ C, i64 ldc,
+               const int2* __restrict__ tiles, int n_tiles, i64 row0, i64 row1) {
+  extern __shared__ __align__(16) std::uint8_t oz_sm[];
+  __shared__ __align__(8) std::uint64_t full[kOz2Stages], peer_full[kOz2Stages], empty[kOz2Stages], tmem_full,
+      tmem_empty;
+  __shared__ unsigned tmem_base_sh;
+  std::uint8_t* sm = reinterpret_cast<std::uint8_t*>((reinterpret_cast<std::uintptr_t>(oz_sm) + 1023) &
+                                                     ~static_cast<std::uintptr_t>(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const unsigned rank = oz_rank();
+  const int pair = static_cast<int>(blockIdx.x >> 1), n_pairs = static_cast<int>(gridDim.x >> 1);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(oz_smem(&tmem_base_sh)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  if (tid == 32) {
+    for (int i = 0; i < kOz2Stages; ++i) {
+      oz_mbar_init_n(&full[i], 1);
+      oz_mbar_init_n(&peer_full[i], 1);
+      oz_mbar_init_n(&empty[i], 1);
+    }
+    oz_mbar_init_n(&tmem_full, 1);
+    oz_mbar_init_n(&tmem_empty, 2 * kOzEpiWarps);  // both CTAs' epilogue warps (leader's barrier)
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  oz_cluster_sync();  // barriers of both CTAs initialised before any remote arrive
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const unsigned tmem = tmem_base_sh;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer: this CTA's A rows and B half
+      int st = 0;
+      unsigned ph = 0;
+      for (int ti = pair; ti < n_tiles; ti += n_pairs) {
+        const int2 tl = tiles[ti];
+        const std::int8_t* xa = xs + (static_cast<i64>(2 * tl.x + rank) * nch) * kOz2BlkA;
+        const std::int8_t* yb = ys + (static_cast<i64>(2 * tl.y + rank) * nch) * kOz2BlkB;
+        for (int p = 0; p < 2; ++p) {
+          const unsigned ba = p == 0 ? kOz2BlkA / 2 : kOz2BlkA, bb = p == 0 ? kOz2BlkB / 2 : kOz2BlkB;
+          for (i64 c = 0; c < nch; ++c) {
+            oz_wait_cluster(&empty[st], ph ^ 1u);
+            std::uint8_t* dst = sm + st * kOz2Stage;
+            oz_mbar_expect(&full[st], ba + bb);
+            oz_bulk(dst, xa + c * kOz2BlkA, ba, &full[st]);
+            oz_bulk(dst + kOz2BlkA, yb + c * kOz2BlkB, bb, &full[st]);
+            if (++st == kOz2Stages) {
+              st = 0;
+              ph ^= 1u;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 1) {  // peer: forward each stage's arrival to the leader
+      if (lane == 0) {
+        int st = 0;
+        unsigned ph = 0;
+        for (int ti = pair; ti < n_tiles; ti += n_pairs)
+          for (int p = 0; p < 2; ++p)
+            for (i64 c = 0; c < nch; ++c) {
+              oz_mbar_wait(&full[st], ph);
+              oz_arrive_remote(oz_mapa(oz_smem(&peer_full[st]), 0));
+              if (++st == kOz2Stages) {
+                st = 0;
+                ph ^= 1u;
+              }
+            }
+      }
+    } else {  // leader: MMA issuer (whole warp; one elected lane issues)
+      const unsigned tm = __shfl_sync(0xffffffffu, tmem, 0);
+      const unsigned smem0 = __shfl_sync(0xffffffffu, oz_smem(sm), 0);
+      int st = 0;
+      unsigned ph = 0, tph = 0;
+      for (int ti = pair; ti < n_tiles; ti += n_pairs) {
+        for (int p = 0; p < 2; ++p) {
+          oz_wait_cluster(&tmem_empty, tph ^ 1u);
+          tph ^= 1u;
+          asm volatile("tcgen05.fence::after_thread_sync;\n");
+          for (i64 c = 0; c < nch; ++c) {
+            oz_mbar_wait(&full[st], ph);
+            oz_wait_cluster(&peer_full[st], ph);
+            asm volatile("tcgen05.fence::after_thread_sync;\n");
+            const unsigned a_base = smem0 + st * kOz2Stage, b_base = a_base + kOz2BlkA;
+            const std::uint64_t da0 = oz_desc(a_base, 16, 256), db0 = oz_desc(b_base, 16, 256);
+            if (oz_elect()) {
+              unsigned started = c == 0 ? 0u : 0xffu;
+              if (p == 0) {
+#pragma unroll
+                for (int xa = 0; xa < kOzS; ++xa)
+#pragma unroll
+                  for (int yb = 0; yb < kOzS; ++yb) {
+                    if (!oz_in_pass(0, xa, yb)) continue;
+                    const int d = xa + yb;
+                    oz2_mma(tm + d * 128, da0 + ((xa * 128 * 32) >> 4), db0 + ((yb * 64 * 32) >> 4),
+                            (started >> d) & 1u);
+                    started |= 1u << d;
+                  }
+              } else {
+#pragma unroll
+                for (int xa = 0; xa < kOzS; ++xa)
+#pragma unroll
+                  for (int yb = 0; yb < kOzS; ++yb) {
+                    if (!oz_in_pass(1, xa, yb)) continue;
+                    const int d = xa + yb - kOzAcc;
+                    oz2_mma(tm + d * 128, da0 + ((xa * 128 * 32) >> 4), db0 + ((yb * 64 * 32) >> 4),
+                            (started >> d) & 1u);
+                    started |= 1u << d;
+                  }
+              }
+              oz2_commit_both(&empty[st]);
+              if (c == nch - 1) oz2_commit_both(&tmem_full);
+            }
+            __syncwarp();
+            if (++st == kOz2Stages) {
+              st = 0;
+              ph ^= 1u;
+            }
+          }
+        }
+      }
+    }
+  } else {  // epilogue warps (both CTAs): TMEM lane quadrant q, 32 columns from 32 cg
+    const int q = warp & 3, cg = (warp - 2) >> 2;
+    const unsigned leader_empty = oz_mapa(oz_smem(&tmem_empty), 0);
+    unsigned tph = 0;
+    for (int ti = pair; ti < n_tiles; ti += n_pairs) {
+      const int2 tl = tiles[ti];
+      const i64 s0 = row0 + static_cast<i64>(tl.x) * 256 + rank * 128, t0 = static_cast<i64>(tl.y) * 128 + cg * 32;
+      const i64 s = s0 + q * 32 + lane;
+      double acc[32];
+#pragma unroll
+      for (int n = 0; n < 32; ++n) acc[n] = 0.0;
+      for (int p = 0; p < 2; ++p) {
+        oz_wait_cluster(&tmem_full, tph);
+        tph ^= 1u;
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+#pragma unroll 1
+        for (int d = 0; d < kOzAcc; ++d) {
+          int v[32];
+          oz_tmem_ld32(tmem + (static_cast<unsigned>(q * 32) << 16) + d * 128 + cg * 32, v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          const double pw = ldexp(1.0, -7 * (kOzAcc * p + d + 2));
+#pragma unroll
+          for (int n = 0; n < 32; ++n) acc[n] = fma(static_cast<double>(v[n]), pw, acc[n]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n");
+        __syncwarp();
+        if (lane == 0) oz_arrive_remote(leader_empty);
+      }
+      if (s < row1) {
+        const double fs = sx[s];
+#pragma unroll 8
+        for (int n = 0; n < 32; ++n) {
+          const i64 t = t0 + n;
+          if (t < M && s <= t) {
+            const double val = acc[n] * fs * sy[t];
+            C[(s - row0) * ldc + t] = val;
+            if (t < row1) C[(t - row0) * ldc + s] = val;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  oz_cluster_sync();  // the pair is done with both TMEMs
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
 }  // namespace
 
 bool ozaki_enabled() {
@@ -448,8 +687,15 @@ bool ozaki_syrk(dfpca_context* ctx, i64 G, i64 K, const double* A, i64 lda, cons
   if (row0 >= row1) return true;
   const i64 Kp = (K + 63) / 64 * 64;
   const i64 nch = Kp / kOzKc;
-  const i64 RA = (row1 - row0 + kOzM - 1) / kOzM, RB = (G + kOzN - 1) / kOzN;  // row blocks of X (slab), Y
-  DevBuf<std::int8_t> xs(static_cast<std::size_t>(RA * nch * kOzBlk)), ys(static_cast<std::size_t>(RB * nch * kOzBlk));
+  const char* pe = std::getenv("DFPCA_OZ_PAIRS");
+  const bool pairs = !(pe && std::string(pe) == "0");  // CTA-pair kernel (k_oz_syrk2)
+  // row blocks: X in 128 rows (an even count for the pairs), Y in 128 (64 for the pairs)
+  const i64 RA0 = (row1 - row0 + kOzM - 1) / kOzM;
+  const i64 RA = pairs ? (RA0 + 1) / 2 * 2 : RA0;
+  const int ry = pairs ? 64 : 128;
+  const i64 RB = (G + 127) / 128 * (128 / ry);
+  DevBuf<std::int8_t> xs(static_cast<std::size_t>(RA * nch * kOzBlk)),
+      ys(static_cast<std::size_t>(RB * nch * kOzS * ry * kOzKc));
   DevBuf<unsigned long long> ex(static_cast<std::size_t>(G)), ey(static_cast<std::size_t>(G));
   DevBuf<double> sx(static_cast<std::size_t>(G)), sy(static_cast<std::size_t>(G));
   cudaStream_t st = ctx->stream;
@@ -458,21 +704,30 @@ bool ozaki_syrk(dfpca_context* ctx, i64 G, i64 K, const double* A, i64 lda, cons
   const dim3 gmax(static_cast<unsigned>((G + 255) / 256), static_cast<unsigned>(std::min<i64>(K, 64)));
   DFPCA_LAUNCH(ctx, k_oz_colmax, gmax, 256, 0, A, K, G, lda, w, ex.get(), ey.get());
   // every row of the padded row blocks is written (zeros past the rows and past K)
-  const i64 rows_x = RA * kOzM, rows_y = RB * kOzN;
+  const i64 rows_x = RA * kOzM, rows_y = RB * ry;
   const dim3 gs(static_cast<unsigned>((std::max(rows_x, rows_y) + 127) / 128), static_cast<unsigned>(Kp / 16));
   DFPCA_LAUNCH(ctx, k_oz_slice, gs, 128, 0, A, K, G, lda, w, ex.get(), ey.get(), xs.get(), ys.get(), sx.get(),
-               sy.get(), rows_x, rows_y, nch, row0, row1);
-  // tiles: I (128 slab rows from row0), J (64 columns) holding some t >= s
+               sy.get(), rows_x, rows_y, nch, row0, row1, ry);
+  // tiles holding some t >= s: (I, J) of 128 x 128 (one CTA), (I2, J) of
+  // 256 x 128 (a CTA pair)
   std::vector<int2> tiles;
-  for (i64 I = 0; I < RA; ++I)
-    for (i64 J = 0; J < RB; ++J)
-      if (J * kOzN + kOzN - 1 >= row0 + I * kOzM) tiles.push_back(make_int2(static_cast<int>(I), static_cast<int>(J)));
+  const i64 TI = pairs ? RA / 2 : RA, TM = pairs ? 256 : 128, TJ = (G + 127) / 128;
+  for (i64 I = 0; I < TI; ++I)
+    for (i64 J = 0; J < TJ; ++J)
+      if (J * 128 + 127 >= row0 + I * TM) tiles.push_back(make_int2(static_cast<int>(I), static_cast<int>(J)));
   DevBuf<int2> d_tiles(tiles.size());
   DFPCA_CUDA(cudaMemcpyAsync(d_tiles.get(), tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, st));
-  allow_smem(k_oz_syrk, kOzSmem);
-  const unsigned grid = static_cast<unsigned>(std::min<i64>(static_cast<i64>(tiles.size()), ctx->sm_count));
-  DFPCA_LAUNCH(ctx, k_oz_syrk, grid, kOzThreads, kOzSmem, xs.get(), ys.get(), nch, sx.get(), sy.get(), G, C, ldc,
-               d_tiles.get(), static_cast<int>(tiles.size()), row0, row1);
+  if (pairs) {
+    allow_smem(k_oz_syrk2, kOz2Smem);
+    const unsigned grid = static_cast<unsigned>(2 * std::min<i64>(static_cast<i64>(tiles.size()), ctx->sm_count / 2));
+    DFPCA_LAUNCH(ctx, k_oz_syrk2, grid, kOzThreads, kOz2Smem, xs.get(), ys.get(), nch, sx.get(), sy.get(), G, C, ldc,
+                 d_tiles.get(), static_cast<int>(tiles.size()), row0, row1);
+  } else {
+    allow_smem(k_oz_syrk, kOzSmem);
+    const unsigned grid = static_cast<unsigned>(std::min<i64>(static_cast<i64>(tiles.size()), ctx->sm_count));
+    DFPCA_LAUNCH(ctx, k_oz_syrk, grid, kOzThreads, kOzSmem, xs.get(), ys.get(), nch, sx.get(), sy.get(), G, C, ldc,
+                 d_tiles.get(), static_cast<int>(tiles.size()), row0, row1);
+  }
   return true;
 }
 

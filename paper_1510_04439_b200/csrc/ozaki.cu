@@ -688,7 +688,7 @@ bool ozaki_syrk(dfpca_context* ctx, i64 G, i64 K, const double* A, i64 lda, cons
   const i64 Kp = (K + 63) / 64 * 64;
   const i64 nch = Kp / kOzKc;
   const char* pe = std::getenv("DFPCA_OZ_PAIRS");
-  const bool pairs = !(pe && std::string(pe) == "0");  // CTA-pair kernel (k_oz_syrk2)
+  const bool pairs = pe && std::string(pe) == "1";  // CTA-pair kernel (k_oz_syrk2), opt-in
   // row blocks: X in 128 rows (an even count for the pairs), Y in 128 (64 for the pairs)
   const i64 RA0 = (row1 - row0 + kOzM - 1) / kOzM;
   const i64 RA = pairs ? (RA0 + 1) / 2 * 2 : RA0;

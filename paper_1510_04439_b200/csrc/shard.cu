@@ -318,7 +318,13 @@ class NullTransport final : public Transport {
   NullTransport(int world, int rank) : world_(world), rank_(rank) {}
   int rank() const override { return rank_; }
   int world() const override { return world_; }
-  void exchange(dfpca_context*, const std::vector<Msg>&, const std::vector<Msg>&) override {}
+  // what would arrive is not computed here: zeros stand in for it (left
+  // uninitialised, NaN bit patterns in the pool sent those nodes through the
+  // solve's exact pass and inflated the projected time)
+  void exchange(dfpca_context* ctx, const std::vector<Msg>&, const std::vector<Msg>& recv) override {
+    for (const Msg& m : recv)
+      if (m.count > 0) DFPCA_CUDA(cudaMemsetAsync(m.buf, 0, sizeof(double) * m.count, ctx->stream));
+  }
   unsigned long long max_u64(dfpca_context*, unsigned long long v) override { return v; }
   void all_gather(dfpca_context* ctx, const double* send, double* recv, i64 count) override {
     DFPCA_CUDA(cudaMemcpyAsync(recv + rank_ * count, send, sizeof(double) * count, cudaMemcpyDeviceToDevice,

@@ -24,24 +24,39 @@ ShardPlan make_shard_plan(i64 n1, i64 rn, i64 R, int world) {
     for (i64 x = u * p.unit; x < std::min(n1, (u + 1) * p.unit); ++x) w += static_cast<double>(n1 - x) - 0.5;
     cum[static_cast<std::size_t>(u) + 1] = cum[static_cast<std::size_t>(u)] + w;
   }
-  const double total = cum.back();
-  p.bounds.assign(static_cast<std::size_t>(p.world) + 1, 0);
-  i64 prev = 0;
-  for (int r = 1; r < p.world; ++r) {
-    const double target = total * r / p.world;
-    // nearest unit boundary to the target, never before the previous one
-    i64 best = prev;
-    double bd = std::fabs(cum[static_cast<std::size_t>(prev)] - target);
-    for (i64 u = prev; u <= units; ++u) {
-      const double dd = std::fabs(cum[static_cast<std::size_t>(u)] - target);
-      if (dd < bd) {
-        bd = dd;
-        best = u;
+  // contiguous unit ranges per rank minimising the largest load (then the
+  // sum of squared loads, so ties stay balanced): a small DP over unit
+  // boundaries (units <= n1, a few hundred at most in practice)
+  const int W = p.world;
+  const std::size_t U = static_cast<std::size_t>(units);
+  auto load = [&](std::size_t a, std::size_t b) { return cum[b] - cum[a]; };
+  // f[k][j]: best (max, sumsq) for units [0, j) split into k ranks
+  const double inf = 1e300;
+  std::vector<std::vector<std::pair<double, double>>> f(
+      static_cast<std::size_t>(W) + 1, std::vector<std::pair<double, double>>(U + 1, {inf, inf}));
+  std::vector<std::vector<std::size_t>> arg(static_cast<std::size_t>(W) + 1, std::vector<std::size_t>(U + 1, 0));
+  f[0][0] = {0.0, 0.0};
+  for (int k = 1; k <= W; ++k)
+    for (std::size_t j = 0; j <= U; ++j)
+      for (std::size_t i = j + 1; i-- > 0;) {  // rank k takes units [i, j) (possibly none; ties: later ranks idle)
+        const auto& prev = f[static_cast<std::size_t>(k) - 1][i];
+        if (prev.first >= inf) continue;
+        const double l = load(i, j);
+        const std::pair<double, double> cand{std::max(prev.first, l), prev.second + l * l};
+        auto& cur = f[static_cast<std::size_t>(k)][j];
+        if (cand.first < cur.first - 1e-9 || (cand.first <= cur.first + 1e-9 && cand.second < cur.second - 1e-9)) {
+          cur = cand;
+          arg[static_cast<std::size_t>(k)][j] = i;
+        }
       }
-    }
-    prev = best;
-    p.bounds[static_cast<std::size_t>(r)] = std::min(n1, best * p.unit);
+  p.bounds.assign(static_cast<std::size_t>(W) + 1, 0);
+  std::size_t j = U;
+  for (int k = W; k >= 1; --k) {
+    const std::size_t i = arg[static_cast<std::size_t>(k)][j];
+    p.bounds[static_cast<std::size_t>(k)] = std::min(n1, static_cast<i64>(j) * p.unit);
+    j = i;
   }
+  p.bounds[0] = 0;
   p.bounds[static_cast<std::size_t>(p.world)] = n1;
   return p;
 }

@@ -506,7 +506,10 @@ __device__ __forceinline__ void fast_divmod(int x, int n, float inv_n, int& q, i
 // weight applied last: S = sw (P_s P_t), so moments that are mirror images of
 // each other (s <-> t, or axis k <-> l at interior nodes) round identically
 // and tie exactly in the exact path's pivot order.
-template <int N>
+// kExactOrder: the rounding the exact pass replays (sw applied last, so
+// mirror-image moments tie exactly); otherwise Ps arrives pre-scaled by sw
+// (one multiply per moment; the certified fast path needs no ties).
+template <int N, bool kExactOrder = true>
 __device__ __forceinline__ void sep_assemble(const SharedMoments& sh, const double (&Ps)[SepIdx<(N - 1) / 2>::n],
                                              const double (&Pt)[SepIdx<(N - 1) / 2>::n], unsigned cs, unsigned ct,
                                              double (&S)[1 + (N - 1) + (N - 1) * N / 2]) {
@@ -514,9 +517,10 @@ __device__ __forceinline__ void sep_assemble(const SharedMoments& sh, const doub
   constexpr int d = p / 2;
   using I = SepIdx<d>;
   const double sw = sh.sw;
-  S[0] = sw * (Ps[0] * Pt[0]);
+  auto sc = [&](double v) { return kExactOrder ? sw * v : v; };
+  S[0] = sc(Ps[0] * Pt[0]);
 #pragma unroll
-  for (int k = 0; k < p; ++k) S[1 + k] = sw * (k < d ? Ps[I::one(k)] * Pt[0] : Ps[0] * Pt[I::one(k - d)]);
+  for (int k = 0; k < p; ++k) S[1 + k] = sc(k < d ? Ps[I::one(k)] * Pt[0] : Ps[0] * Pt[I::one(k - d)]);
 #pragma unroll
   for (int k = 0; k < p; ++k)
 #pragma unroll
@@ -525,7 +529,7 @@ __device__ __forceinline__ void sep_assemble(const SharedMoments& sh, const doub
       if (l < d) v = Ps[I::two(k, l)] * Pt[0];
       else if (k >= d) v = Ps[0] * Pt[I::two(k - d, l - d)];
       else v = Ps[I::one(k)] * Pt[I::one(l - d)];
-      S[quad_index(p, k, l)] = sw * v;
+      S[quad_index(p, k, l)] = sc(v);
     }
   int sk[d], tk[d];
   bool near = true;
@@ -697,8 +701,10 @@ __global__ void __launch_bounds__(kSolveTile, N == 5 ? DFPCA_SOLVE5_MIN_CTAS : D
         double Ps[SepIdx<d>::n], Pt[SepIdx<d>::n];
         sep_load<N>(sh, n.row, Ps);
         sep_load<N>(sh, n.col, Pt);
+#pragma unroll
+        for (int i = 0; i < SepIdx<d>::n; ++i) Ps[i] *= sh.sw;
         double S[nm];
-        sep_assemble<N>(sh, Ps, Pt, __ldg(sh.coord + n.row), __ldg(sh.coord + n.col), S);
+        sep_assemble<N, false>(sh, Ps, Pt, __ldg(sh.coord + n.row), __ldg(sh.coord + n.col), S);
         double dg[N], b0;
         ridged_diagonal<N>(S, dg);
         done = ldlt_certified<N>(S, T, dg, b0);

@@ -972,14 +972,6 @@ void launch_solve_shared_n(dfpca_context* ctx, const SharedMoments& sh, const Mo
                      g, static_cast<unsigned>(rows), static_cast<unsigned>(nch), out, pending.get());
         DFPCA_LAUNCH(ctx, k_solve_sep_exact<N>, 148 * 4, kSolveTile, 0, sh, mp, g, pending.get(), out, cnt, list,
                      cap);
-        if (std::getenv("DFPCA_DEBUG_SOLVE")) {
-          unsigned q = 0;
-          cudaMemcpyAsync(&q, pending.get(), sizeof(q), cudaMemcpyDeviceToHost, ctx->stream);
-          cudaStreamSynchronize(ctx->stream);
-          std::fprintf(stderr, "sep solve: rows %lld row_lo %lld row0 %lld t0 %lld tc %lld queued %u\n",
-                       static_cast<long long>(rows), static_cast<long long>(g.row_lo), static_cast<long long>(g.row0),
-                       static_cast<long long>(g.t0), static_cast<long long>(g.tc), q);
-        }
       } else
         DFPCA_LAUNCH(ctx, k_solve_shared_tri<N>, static_cast<unsigned>(n), kSolveTile, 0, sh, mp, g, nch, out, cnt,
                      list, cap);

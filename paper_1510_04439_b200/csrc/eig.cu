@@ -1143,7 +1143,8 @@ static RowShard shard_rows_dev(dfpca_context* ctx, Transport& tr, const dfpca_su
 static bool finish_eigensystem(dfpca_context* ctx, const Grid& grid, const std::vector<i64>& node_of_row, i64 M,
                                const double* Lt, const double* tilde_d, const std::vector<double>& tilde,
                                i64 L_max, bool gram_schmidt, double* eigenvalues, double* eigenfunctions,
-                               double* fve, double* total_variance, i64* n_components, i64 n_avail = -1) {
+                               double* fve, double* total_variance, i64* n_components, i64 n_avail = -1,
+                               const double* tilde_total_in = nullptr) {
   cudaStream_t st = ctx->stream;
   const i64 q = static_cast<i64>(tilde.size());
   const double cv = grid.cell_volume();
@@ -1151,6 +1152,7 @@ static bool finish_eigensystem(dfpca_context* ctx, const Grid& grid, const std::
   double tilde_total = 0.0;
   for (double t : tilde)
     if (t > cut) tilde_total += t;
+  if (tilde_total_in) tilde_total = *tilde_total_in;  // a partial spectrum: the caller's sum over the cut
   const double total = tilde_total * cv;
 
   DevBuf<double> kept(static_cast<std::size_t>(std::max<i64>(L_max, 1) * M));
@@ -1458,17 +1460,35 @@ __global__ void k_reverse_rows(const double* __restrict__ in, i64 rows, i64 cols
 }
 }  // namespace
 
+bool dense_top_eigenpairs(dfpca_context* ctx, const double* sigma, i64 M, int count, double cut_rel,
+                          std::vector<double>& lam_out, double* vecs, double& above_cut);
+
 void run_dense_eig(dfpca_context* ctx, const dfpca_surface* cov, const Grid& grid, i64 L_max, double* eigenvalues,
                    double* eigenfunctions, double* fve, double* total_variance, i64* n_components) {
   if (cov->kind != DFPCA_SURFACE_COVARIANCE)
     fail(kConfig, "InvalidArgument", "matrixize expects a covariance surface");
   if (cov->n != grid.G * grid.G) fail(kConfig, "InvalidArgument", "covariance surface has wrong length");
-  CusolverApi& api = CusolverApi::get();
   cudaStream_t st = ctx->stream;
   ctx->begin_stage("eigen");
   MatrixView mv = matrixize_dev(ctx, cov, grid);
   const i64 M = mv.M;
   if (M > (i64(1) << 31) / M) fail(kConfig, "InvalidArgument", "matrix too large for the dense eigensolver");
+  // The hand-written path (dense_eig.cu) unless DFPCA_DENSE_EIG=cusolver;
+  // it declines (and cuSOLVER's syevd runs) outside its size range.
+  const char* mode = std::getenv("DFPCA_DENSE_EIG");
+  const int count = static_cast<int>(std::min<i64>(L_max, M));
+  if (!(mode && std::string(mode) == "cusolver") && count >= 1) {
+    std::vector<double> lam;
+    double above = 0.0;
+    DevBuf<double> vecs(static_cast<std::size_t>(count) * M), td(static_cast<std::size_t>(count));
+    if (dense_top_eigenpairs(ctx, mv.sigma, M, count, 1e-12, lam, vecs.get(), above)) {
+      DFPCA_CUDA(cudaMemcpyAsync(td.get(), lam.data(), sizeof(double) * count, cudaMemcpyHostToDevice, st));
+      finish_eigensystem(ctx, grid, mv.node_of_row, M, vecs.get(), td.get(), lam, L_max, false, eigenvalues,
+                         eigenfunctions, fve, total_variance, n_components, -1, &above);
+      return;
+    }
+  }
+  CusolverApi& api = CusolverApi::get();
   // A = Sigma (symmetric: row-major == column-major), overwritten by the eigenvectors
   DevBuf<double> A(static_cast<std::size_t>(M * M)), w(static_cast<std::size_t>(M));
   DFPCA_CUDA(cudaMemcpyAsync(A.get(), mv.sigma, sizeof(double) * M * M, cudaMemcpyDeviceToDevice, st));

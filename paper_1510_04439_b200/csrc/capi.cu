@@ -258,6 +258,12 @@ bool host_trace() {
 }
 }  // namespace
 
+namespace dfpca_gpu {
+void host_mark(const char* what) {
+  if (host_trace()) std::fprintf(stderr, "[host %10.1f us] %s\n", host_us(), what);
+}
+}  // namespace dfpca_gpu
+
 void dfpca_context::begin_stage(const std::string& name) {
   if (host_trace()) std::fprintf(stderr, "[host %10.1f us] begin %s\n", host_us(), name.c_str());
   StageMark m;

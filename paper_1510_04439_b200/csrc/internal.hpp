@@ -18,6 +18,7 @@ namespace dfpca_gpu {
 
 using i64 = std::int64_t;
 class Transport;  // shard.cu: NCCL (or in-process) rank exchanges
+void host_mark(const char* what);  // DFPCA_HOST_TRACE: a host timestamp on stderr
 
 // Error classes of the reference (errors.hpp:11-17).
 enum : int { kParse = 2, kConfig = 3, kNumeric = 4, kVersion = 5 };

@@ -917,6 +917,20 @@ __global__ void k_center_mirror(double* __restrict__ cov, const double* __restri
   }
 }
 
+// The centering of k_center_mirror on listed upper entries (flat s G + t,
+// s <= t) and their mirrors: the entries the ladder refitted after it.
+__global__ void k_center_list(double* __restrict__ cov, const double* __restrict__ mean,
+                              const std::uint8_t* __restrict__ mask, i64 G, const i64* __restrict__ list, i64 n) {
+  for (i64 q = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; q < n;
+       q += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 dst = list[q], a = dst / G, b = dst % G;
+    double v = cov[dst];
+    if (!mask || (mask[a] && mask[b])) v -= mean[a] * mean[b];
+    cov[dst] = v;
+    if (a < b) cov[b * G + a] = v;
+  }
+}
+
 __global__ void k_fill_nan(double* p, i64 n) {
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < n; e += (i64)gridDim.x * blockDim.x)
     p[e] = __longlong_as_double(0x7ff8000000000000ll);
@@ -1231,6 +1245,7 @@ void run_local_linear(dfpca_context* ctx, const dfpca_binned* b, const Grid& gri
 // Pair grids + moments + solve + center + symmetrize for the covariance.
 void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& grid, const double* h,
                          const double* mean_host, const CovShardExec* shard, dfpca_surface** out) {
+  host_mark("cov entry");
   const int d = grid.d;
   const int p = 2 * d;
   const i64 G = grid.G;
@@ -1240,6 +1255,7 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
   std::vector<AxisTaps> taps(p);
   for (int k = 0; k < p; ++k) taps[k] = make_taps(h[k % d], grid.spacing[k % d]);
   DevBuf<double> taps_dev(3 * (2 * 4096 + 1));
+  host_mark("taps");
 
   // Slab of this rank (shard.hpp): pair-grid / t-partial rows are the s1
   // planes [ha, hb), output rows the planes [sa, sb); one device: everything.
@@ -1279,24 +1295,23 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
     }
     shared = some_axis;
   }
+  host_mark("surface alloc");
   SharedMoments sh{};
   if (shared) {
+    host_mark("shared setup");
     double sw = 0.0;  // the reference's off-band pw entry: ordered sum of (w_i M0) M0
     for (double w : b->pair_weight_h) sw = sw + (w * b->shared_m0) * b->shared_m0;
     sh.sw = sw;
     sh.dm0 = b->shared_dm0;
     // The A / D tables depend only on the axis lengths and taps: built once per
     // context and kept on the device (their host build is O(n^2 R) per axis).
+    // (the taps are make_taps(h, spacing) of each axis: those bits key them)
     std::string key = "shared";
     for (int k = 0; k < d; ++k) {
-      key += "|" + std::to_string(grid.shape[k]);
-      for (int side : {k, d + k})
-        for (int r = 0; r < 3; ++r)
-          for (double v : taps[side].t[r]) {
-            std::uint64_t bits;
-            std::memcpy(&bits, &v, sizeof(bits));
-            key += ":" + std::to_string(bits);
-          }
+      std::uint64_t hb, sb;
+      std::memcpy(&hb, &h[k], sizeof(hb));
+      std::memcpy(&sb, &grid.spacing[k], sizeof(sb));
+      key += "|" + std::to_string(grid.shape[k]) + ":" + std::to_string(hb) + ":" + std::to_string(sb);
     }
     std::vector<std::size_t> offA(d), offD(d);
     std::size_t total = 0;
@@ -1399,6 +1414,7 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
   // and the rest received from the other ranks (shard.hpp, exchange 1)
   DevBuf<double> pw, pv(static_cast<std::size_t>(LR * G));
   if (!shared) pw.alloc(static_cast<std::size_t>(LR * G));
+  host_mark("pair buffers");
   ctx->begin_stage("pairs");
   if (sharded) {
     PairWindow win;
@@ -1418,6 +1434,10 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
     build_pair_grids(ctx, b, shared ? nullptr : pw.get(), pv.get());
   }
   ctx->end_stage();
+
+  // for the centering (K5): uploaded while the pair build runs
+  DevBuf<double> mean_dev(static_cast<std::size_t>(G));
+  DFPCA_CUDA(cudaMemcpyAsync(mean_dev.get(), mean_host, sizeof(double) * G, cudaMemcpyHostToDevice, st));
 
   // ---- phase T: t-axis passes over row chunks of the pair grids ----
   ctx->begin_stage("moments");
@@ -1675,10 +1695,35 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
     ctx->begin_stage("moments");
   }
   unsigned long long n_empty = 0;
-  DFPCA_CUDA(cudaMemcpyAsync(&n_empty, cnt.get(), sizeof(n_empty), cudaMemcpyDeviceToHost, st));
-  DFPCA_CUDA(cudaStreamSynchronize(st));
-  ctx->end_stage();
-  tpart_store.clear();
+  const i64 tiles = (G + 31) / 32;
+  const i64 I0 = out_row0 / 32, I1 = (out_row0 + out_rows + 31) / 32;
+  auto pstart = [tiles](i64 i) { return i * tiles - i * (i - 1) / 2; };
+  const i64 pairs = out_rows > 0 ? pstart(I1) - pstart(I0) : 0;  // (slab rows start on 64-row tiles)
+  if (!sharded) {
+    // One device: center and mirror without waiting for the empty-window
+    // count (read back with the final sync); empty windows, if any, are then
+    // refitted by the ladder and re-centered entry by entry (same formula).
+    unsigned long long* slot = ctx->pinned_u64(1);
+    DFPCA_CUDA(cudaMemcpyAsync(slot, cnt.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    ctx->end_stage();
+    ctx->begin_stage("center");
+    if (pairs > 0)
+      DFPCA_LAUNCH(ctx, k_center_mirror, static_cast<unsigned>(pairs), 256, 0, surf->values.get(), mean_dev.get(),
+                   grid.has_mask ? mask_dev.get() : nullptr, G, I0, I1, out_row0);
+    ctx->end_stage();
+    DFPCA_CUDA(cudaStreamSynchronize(st));
+    n_empty = *slot;
+    tpart_store.clear();
+    if (n_empty == 0) {
+      *out = surf.release();
+      return;
+    }
+  } else {
+    DFPCA_CUDA(cudaMemcpyAsync(&n_empty, cnt.get(), sizeof(n_empty), cudaMemcpyDeviceToHost, st));
+    DFPCA_CUDA(cudaStreamSynchronize(st));
+    ctx->end_stage();
+    tpart_store.clear();
+  }
   if (sharded) {
     // every rank must take the same branch before the covariance exchange
     const unsigned long long any_empty = shard->max_over_ranks(n_empty);
@@ -1735,16 +1780,18 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
            "binned covariance smoother: " + std::to_string(n_still) +
                " node(s) had no binned mass in the kernel window (AllWeightsZero) after 3 window "
                "enlargements");
+    if (!sharded) {  // the refitted entries, centered and mirrored like the rest
+      DFPCA_LAUNCH(ctx, k_center_list, grid_for(static_cast<i64>(n_empty), 256), 256, 0, surf->values.get(),
+                   mean_dev.get(), grid.has_mask ? mask_dev.get() : nullptr, G, list.get(),
+                   static_cast<i64>(n_empty));
+      DFPCA_CUDA(cudaStreamSynchronize(st));
+      *out = surf.release();
+      return;
+    }
   }
 
   // ---- center + symmetrize (K5) ----
   ctx->begin_stage("center");
-  DevBuf<double> mean_dev(static_cast<std::size_t>(G));
-  DFPCA_CUDA(cudaMemcpyAsync(mean_dev.get(), mean_host, sizeof(double) * G, cudaMemcpyHostToDevice, st));
-  const i64 tiles = (G + 31) / 32;
-  const i64 I0 = out_row0 / 32, I1 = (out_row0 + out_rows + 31) / 32;
-  auto pstart = [tiles](i64 i) { return i * tiles - i * (i - 1) / 2; };
-  const i64 pairs = out_rows > 0 ? pstart(I1) - pstart(I0) : 0;  // (slab rows start on 64-row tiles)
   if (pairs > 0)
     DFPCA_LAUNCH(ctx, k_center_mirror, static_cast<unsigned>(pairs), 256, 0, surf->values.get(), mean_dev.get(),
                  grid.has_mask ? mask_dev.get() : nullptr, G, I0, I1, out_row0);

@@ -22,16 +22,16 @@
 // bound (K u sum |x y| ~ 2e-13), far inside the 1e-10 surface tolerance.
 // Zero products stay exactly zero (all digits zero).
 //
-// Kernel: one CTA per SM (the 8 int32 accumulators of a 128 x 64 output tile
-// fill all 512 TMEM columns), persistent over the upper tiles.  Per 64-byte K
-// chunk the CTA stages the S slices of its 128 s-rows and 64 t-rows (96 KB,
-// no-swizzle K-major core-matrix layout, cp.async, double-buffered); one
-// thread issues the 36 slice pairs x 2 K-halves = 72 MMAs (M 128, N 64, K 32)
-// into accumulator d = a + b - 2 and commits them to the stage's mbarrier.
-// The epilogue (4 warps, one TMEM lane = one s row each) converts the 8
-// int32 accumulators to double, scales, and writes every upper-triangle entry
-// of the tile and its mirror (entries s > t are written only by the tile
-// owning (t, s), so the result is exactly symmetric and deterministic).
+// Kernels: k_oz_colmax (the column scales), k_oz_slice (the slices, in the
+// product's staging layout) and k_oz_syrk, one CTA per SM, persistent over
+// the upper 128 x 128 tiles: a producer warp streams each (tile, pass,
+// 32-byte K chunk) block of slices into a 3-stage ring with bulk copies, one
+// warp issues the slice-pair MMAs (M 128, N 128, K 32) into the pass's 4
+// int32 TMEM accumulators (d = a + b in [4p, 4p + 4); two passes fill the 512
+// columns twice), and 16 epilogue warps add each pass into FP64 registers
+// (ascending d), then scale and write every upper-triangle entry of the tile
+// and its mirror (entries s > t are written only by the tile owning (t, s):
+// exactly symmetric, deterministic).
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>

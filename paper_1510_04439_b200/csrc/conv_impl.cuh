@@ -470,6 +470,132 @@ __global__ void __launch_bounds__(kThreads) k_tphase2(const double* __restrict__
   cp_async_wait_c<0>();
 }
 
+// Value-only form (the shared design: only pv is convolved), on zero-padded
+// shared planes so the inner loops carry no bounds tests: X lines hold R
+// zeros on each side (pitch ldx, odd), Y holds R zero rows above and R + 8
+// below (a t1 block may start at any row; pitch ldy, odd); the pads
+// are zeroed once and never written.  One X buffer: the next row's copy is
+// issued after the last t2 pass has read X, so it overlaps the t1 pass.
+// Same products, same order as k_tphase2 (bit-identical).
+__host__ __device__ constexpr int tpv_ldx(int n2, int R) { return ((n2 + kJBr - 1) / kJBr * kJBr + 2 * R) | 1; }
+__host__ __device__ constexpr int tpv_ldy(int n2) { return n2 | 1; }
+__host__ __device__ constexpr int tpv_yrows(int n1, int R) { return n1 + kJBr + 2 * R; }  // t1 blocks start at any j_lo
+
+template <int R, int ORD>
+__device__ inline void tpv_conv_rows(const double* X, double* Y, int n1, int n2, int ldx, int ldy, const Taps2P& tp,
+                                     int l0) {
+  const int nb = (n2 + kJBr - 1) / kJBr;
+  const int nl = n1 - l0;
+  for (int item = threadIdx.x; item < nl * nb; item += blockDim.x) {
+    const int l = l0 + item % nl, j0 = (item / nl) * kJBr;
+    const double* xr = X + l * ldx + j0;  // xr[m + R] = X[l][j0 + m]
+    double acc[kJBr];
+#pragma unroll
+    for (int jj = 0; jj < kJBr; ++jj) acc[jj] = 0.0;
+#pragma unroll
+    for (int m = -R; m < kJBr + R; ++m) {
+      const double x = xr[m + R];
+#pragma unroll
+      for (int jj = 0; jj < kJBr; ++jj) {
+        const int o = m - jj;
+        if (o >= -R && o <= R) acc[jj] = fma(tp.t[1][ORD][o + R], x, acc[jj]);
+      }
+    }
+    double* yr = Y + (l + R) * ldy + j0;
+#pragma unroll
+    for (int jj = 0; jj < kJBr; ++jj)
+      if (j0 + jj < n2) yr[jj] = acc[jj];
+  }
+}
+
+template <int R, int NO>
+__device__ inline void tpv_conv_cols(const double* Y, int n1, int n2, int ldy, double* const* outs, i64 row_off,
+                                     const Taps2P& tp, int j_lo) {
+  const int nb = (n1 - j_lo + kJBr - 1) / kJBr;
+  for (int item = threadIdx.x; item < n2 * nb; item += blockDim.x) {
+    const int c = item % n2, j0 = j_lo + (item / n2) * kJBr;
+    const double* yc = Y + j0 * ldy + c;  // yc[(m + R) ldy] = Y[j0 + m][c]
+    double acc[NO][kJBr];
+#pragma unroll
+    for (int r = 0; r < NO; ++r)
+#pragma unroll
+      for (int jj = 0; jj < kJBr; ++jj) acc[r][jj] = 0.0;
+#pragma unroll
+    for (int m = -R; m < kJBr + R; ++m) {
+      const double x = yc[(m + R) * ldy];
+#pragma unroll
+      for (int jj = 0; jj < kJBr; ++jj) {
+        const int o = m - jj;
+        if (o >= -R && o <= R) {
+#pragma unroll
+          for (int r = 0; r < NO; ++r) acc[r][jj] = fma(tp.t[0][r][o + R], x, acc[r][jj]);
+        }
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < kJBr; ++jj) {
+      const int j = j0 + jj;
+      if (j < n1) {
+#pragma unroll
+        for (int r = 0; r < NO; ++r) outs[r][row_off + static_cast<i64>(j) * n2 + c] = acc[r][jj];
+      }
+    }
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(kThreads, 2) k_tphase2v(const double* __restrict__ pv, i64 rows, int n1, int n2,
+                                                          TPhaseOut out, Taps2P tp) {
+  extern __shared__ double sm[];
+  const int ldx = tpv_ldx(n2, R), ldy = tpv_ldy(n2);
+  double* X = sm;
+  double* Y = sm + n1 * ldx;
+  const int ny = tpv_yrows(n1, R);
+  for (int e = threadIdx.x; e < n1 * ldx + ny * ldy; e += blockDim.x) sm[e] = 0.0;  // the pads
+  __syncthreads();
+  const i64 plane = static_cast<i64>(n1) * n2;
+  auto j_lo_of = [&](i64 s) -> int {
+    if (out.t1_margin < 0) return 0;
+    const long long lo = (out.s_base + s) / out.rn - out.t1_margin;
+    return lo <= 0 ? 0 : (lo >= n1 ? n1 : static_cast<int>(lo));
+  };
+  auto issue = [&](i64 s) {
+    const double* src = pv + s * plane;
+    const int l0 = j_lo_of(s) - R > 0 ? j_lo_of(s) - R : 0;
+    for (int e = l0 * n2 + threadIdx.x; e < plane; e += blockDim.x)
+      cp_async_c8(X + (e / n2) * ldx + R + e % n2, src + e, 8);
+  };
+  i64 s = blockIdx.x;
+  if (s < rows) issue(s);
+  cp_async_commit_c();
+  while (s < rows) {
+    const i64 ns = s + gridDim.x;
+    cp_async_wait_c<0>();
+    __syncthreads();
+    const i64 off = s * plane;
+    const int j_lo = j_lo_of(s);
+    const int l0 = j_lo - R > 0 ? j_lo - R : 0;
+    tpv_conv_rows<R, 0>(X, Y, n1, n2, ldx, ldy, tp, l0);
+    __syncthreads();
+    {
+      double* o[2] = {out.v[0], out.v[1]};
+      tpv_conv_cols<R, 2>(Y, n1, n2, ldy, o, off, tp, j_lo);
+    }
+    __syncthreads();
+    tpv_conv_rows<R, 1>(X, Y, n1, n2, ldx, ldy, tp, l0);
+    __syncthreads();
+    if (ns < rows) issue(ns);  // X is free: the next row streams in under the t1 pass
+    cp_async_commit_c();
+    {
+      double* o[1] = {out.v[2]};
+      tpv_conv_cols<R, 1>(Y, n1, n2, ldy, o, off, tp, j_lo);
+    }
+    __syncthreads();
+    s = ns;
+  }
+  cp_async_wait_c<0>();
+}
+
 // ------------------------------------------------------------- launchers --
 template <typename K>
 inline unsigned persistent_grid(dfpca_context* ctx, K kern, std::size_t smem, i64 work, int threads = kThreads) {
@@ -530,6 +656,13 @@ void launch_tphase2(dfpca_context* ctx, const TPhase2Spec& s, const Taps2P& tp) 
   out.rn = s.rn;
   out.t1_margin = s.t1_margin;
   const int n1 = static_cast<int>(s.n1), n2 = static_cast<int>(s.n2);
+  if (s.value_only && std::getenv("DFPCA_TPHASE_2BUF") == nullptr) {
+    const std::size_t smem1 =
+        sizeof(double) * (static_cast<std::size_t>(n1) * tpv_ldx(n2, R) + static_cast<std::size_t>(tpv_yrows(n1, R)) * tpv_ldy(n2));
+    const unsigned grid1 = persistent_grid(ctx, k_tphase2v<R>, smem1, s.rows);
+    DFPCA_LAUNCH(ctx, k_tphase2v<R>, grid1, kThreads, smem1, s.pv, s.rows, n1, n2, out, tp);
+    return;
+  }
   const std::size_t smem = sizeof(double) * 3 * n1 * (n2 + 1);
   const unsigned grid = persistent_grid(ctx, k_tphase2<R>, smem, s.rows);
   DFPCA_LAUNCH(ctx, k_tphase2<R>, grid, kThreads, smem, s.pw, s.pv, s.rows, n1, n2, s.value_only ? 1 : 0, out,

@@ -470,13 +470,15 @@ __global__ void __launch_bounds__(kThreads) k_tphase2(const double* __restrict__
   cp_async_wait_c<0>();
 }
 
-// Value-only form (the shared design: only pv is convolved), on zero-padded
-// shared planes so the inner loops carry no bounds tests: X lines hold R
+// The fused t-phase on zero-padded shared planes, so the inner loops carry
+// no bounds tests: X lines hold R
 // zeros on each side (pitch ldx, odd), Y holds R zero rows above and R + 8
 // below (a t1 block may start at any row; pitch ldy, odd); the pads
-// are zeroed once and never written.  One X buffer: the next row's copy is
-// issued after the last t2 pass has read X, so it overlaps the t1 pass.
-// Same products, same order as k_tphase2 (bit-identical).
+// are zeroed once and never written.  One X buffer: the next plane's copy is
+// issued after the last t2 pass of the current one has read X, so it
+// overlaps the t1 pass.  Same products, same order as k_tphase2
+// (bit-identical), which remains as DFPCA_TPHASE_2BUF=1 and for planes too
+// large for the padded buffers.
 __host__ __device__ constexpr int tpv_ldx(int n2, int R) { return ((n2 + kJBr - 1) / kJBr * kJBr + 2 * R) | 1; }
 __host__ __device__ constexpr int tpv_ldy(int n2) { return n2 | 1; }
 __host__ __device__ constexpr int tpv_yrows(int n1, int R) { return n1 + kJBr + 2 * R; }  // t1 blocks start at any j_lo
@@ -543,9 +545,9 @@ __device__ inline void tpv_conv_cols(const double* Y, int n1, int n2, int ldy, d
   }
 }
 
-template <int R>
-__global__ void __launch_bounds__(kThreads, 2) k_tphase2v(const double* __restrict__ pv, i64 rows, int n1, int n2,
-                                                          TPhaseOut out, Taps2P tp) {
+template <int R, bool VO>  // VO: value planes only (the shared design), no mass-order code
+__global__ void __launch_bounds__(kThreads, 2) k_tphase2v(const double* __restrict__ pw, const double* __restrict__ pv,
+                                                          i64 rows, int n1, int n2, TPhaseOut out, Taps2P tp) {
   extern __shared__ double sm[];
   const int ldx = tpv_ldx(n2, R), ldy = tpv_ldy(n2);
   double* X = sm;
@@ -559,39 +561,59 @@ __global__ void __launch_bounds__(kThreads, 2) k_tphase2v(const double* __restri
     const long long lo = (out.s_base + s) / out.rn - out.t1_margin;
     return lo <= 0 ? 0 : (lo >= n1 ? n1 : static_cast<int>(lo));
   };
-  auto issue = [&](i64 s) {
-    const double* src = pv + s * plane;
+  auto issue = [&](i64 s, int pass) {
+    const double* src = (pass ? pv : pw) + s * plane;
     const int l0 = j_lo_of(s) - R > 0 ? j_lo_of(s) - R : 0;
     for (int e = l0 * n2 + threadIdx.x; e < plane; e += blockDim.x)
       cp_async_c8(X + (e / n2) * ldx + R + e % n2, src + e, 8);
   };
+  // planes in order: (s, pw), (s, pv), (s + grid, pw), ... (pv only when value_only)
+  const int first_pass = VO ? 1 : 0;
   i64 s = blockIdx.x;
-  if (s < rows) issue(s);
+  int pass = first_pass;
+  if (s < rows) issue(s, pass);
   cp_async_commit_c();
   while (s < rows) {
-    const i64 ns = s + gridDim.x;
+    const bool same_row = pass == 0;
+    const i64 ns = same_row ? s : s + gridDim.x;
+    const int npass = same_row ? 1 : first_pass;
     cp_async_wait_c<0>();
     __syncthreads();
     const i64 off = s * plane;
     const int j_lo = j_lo_of(s);
     const int l0 = j_lo - R > 0 ? j_lo - R : 0;
-    tpv_conv_rows<R, 0>(X, Y, n1, n2, ldx, ldy, tp, l0);
-    __syncthreads();
-    {
-      double* o[2] = {out.v[0], out.v[1]};
-      tpv_conv_cols<R, 2>(Y, n1, n2, ldy, o, off, tp, j_lo);
+    const int max_order = !VO && pass == 0 ? 2 : 1;
+    for (int r2 = 0; r2 <= max_order; ++r2) {
+      if (r2 == 0) tpv_conv_rows<R, 0>(X, Y, n1, n2, ldx, ldy, tp, l0);
+      else if (r2 == 1) tpv_conv_rows<R, 1>(X, Y, n1, n2, ldx, ldy, tp, l0);
+      else tpv_conv_rows<R, 2>(X, Y, n1, n2, ldx, ldy, tp, l0);
+      __syncthreads();
+      if (r2 == max_order) {  // X is free: the next plane streams in under the t1 pass
+        if (ns < rows) issue(ns, npass);
+        cp_async_commit_c();
+      }
+      if (!VO && pass == 0) {
+        if (r2 == 0) {
+          double* o[3] = {out.m[0], out.m[1], out.m[2]};
+          tpv_conv_cols<R, 3>(Y, n1, n2, ldy, o, off, tp, j_lo);
+        } else if (r2 == 1) {
+          double* o[2] = {out.m[3], out.m[4]};
+          tpv_conv_cols<R, 2>(Y, n1, n2, ldy, o, off, tp, j_lo);
+        } else {
+          double* o[1] = {out.m[5]};
+          tpv_conv_cols<R, 1>(Y, n1, n2, ldy, o, off, tp, j_lo);
+        }
+      } else if (r2 == 0) {
+        double* o[2] = {out.v[0], out.v[1]};
+        tpv_conv_cols<R, 2>(Y, n1, n2, ldy, o, off, tp, j_lo);
+      } else {
+        double* o[1] = {out.v[2]};
+        tpv_conv_cols<R, 1>(Y, n1, n2, ldy, o, off, tp, j_lo);
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    tpv_conv_rows<R, 1>(X, Y, n1, n2, ldx, ldy, tp, l0);
-    __syncthreads();
-    if (ns < rows) issue(ns);  // X is free: the next row streams in under the t1 pass
-    cp_async_commit_c();
-    {
-      double* o[1] = {out.v[2]};
-      tpv_conv_cols<R, 1>(Y, n1, n2, ldy, o, off, tp, j_lo);
-    }
-    __syncthreads();
     s = ns;
+    pass = npass;
   }
   cp_async_wait_c<0>();
 }
@@ -656,11 +678,16 @@ void launch_tphase2(dfpca_context* ctx, const TPhase2Spec& s, const Taps2P& tp) 
   out.rn = s.rn;
   out.t1_margin = s.t1_margin;
   const int n1 = static_cast<int>(s.n1), n2 = static_cast<int>(s.n2);
-  if (s.value_only && std::getenv("DFPCA_TPHASE_2BUF") == nullptr) {
-    const std::size_t smem1 =
-        sizeof(double) * (static_cast<std::size_t>(n1) * tpv_ldx(n2, R) + static_cast<std::size_t>(tpv_yrows(n1, R)) * tpv_ldy(n2));
-    const unsigned grid1 = persistent_grid(ctx, k_tphase2v<R>, smem1, s.rows);
-    DFPCA_LAUNCH(ctx, k_tphase2v<R>, grid1, kThreads, smem1, s.pv, s.rows, n1, n2, out, tp);
+  const std::size_t smem1 = sizeof(double) * (static_cast<std::size_t>(n1) * tpv_ldx(n2, R) +
+                                              static_cast<std::size_t>(tpv_yrows(n1, R)) * tpv_ldy(n2));
+  if (smem1 <= 200 * 1024 && std::getenv("DFPCA_TPHASE_2BUF") == nullptr) {
+    if (s.value_only) {
+      const unsigned grid1 = persistent_grid(ctx, k_tphase2v<R, true>, smem1, s.rows);
+      DFPCA_LAUNCH(ctx, (k_tphase2v<R, true>), grid1, kThreads, smem1, s.pw, s.pv, s.rows, n1, n2, out, tp);
+    } else {
+      const unsigned grid1 = persistent_grid(ctx, k_tphase2v<R, false>, smem1, s.rows);
+      DFPCA_LAUNCH(ctx, (k_tphase2v<R, false>), grid1, kThreads, smem1, s.pw, s.pv, s.rows, n1, n2, out, tp);
+    }
     return;
   }
   const std::size_t smem = sizeof(double) * 3 * n1 * (n2 + 1);

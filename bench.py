@@ -703,7 +703,7 @@ def kernel_model(G: int, n_pair: int, shared: bool):
                           (the symmetric half of 2 n G^2 flops)    -> FP64 tensor
             k_rank_one    pw = W M(s) M(t): write 1 array          -> HBM
             k_scale_rows  w_i V_i: read + write n G doubles
-    t-phase k_tphase2     read pw, pv; write 9 t-partials -- the planes the
+    t-phase k_tphase2(v)  read pw, pv; write 9 t-partials -- the planes the
                           trimmed kernel actually moves (tphase_fractions:
                           0.71 of the input planes read, 0.62 of the output
                           planes written at cfg 3: 347 MB, ncu 293 MB)
@@ -740,6 +740,7 @@ def kernel_model(G: int, n_pair: int, shared: bool):
             "k_gemm_tn": ("tensor", 2.0 * n_pair * G * G / 2.0),
             "k_scale_rows": ("hbm", 2 * 8.0 * n_pair * G),
             "k_tphase2": ("hbm", (1 * t_rd + 3 * t_wr) * arr),
+            "k_tphase2v": ("hbm", (1 * t_rd + 3 * t_wr) * arr),
             "k_pass_cols": ("hbm", (3 * f_in + 4 * f_out + (4 + 5) * f_out) * arr),
             "k_solve_sep_tri": ("hbm", 6 * upper * arr),
             "k_solve_shared_tri": ("hbm", 6 * upper * arr),
@@ -751,6 +752,7 @@ def kernel_model(G: int, n_pair: int, shared: bool):
         "k_rank_one": ("hbm", 1 * arr),
         "k_scale_rows": ("hbm", 2 * 8.0 * n_pair * G),
         "k_tphase2": ("hbm", (2 * t_rd + 9 * t_wr) * arr),
+        "k_tphase2v": ("hbm", (2 * t_rd + 9 * t_wr) * arr),
         "k_pass_cols": ("hbm", (9 * f_in + 14 * f_out + (14 + 20) * f_out) * arr),
         "k_solve_tri": ("hbm", 21 * upper * arr),
         "k_center_mirror": ("hbm", (upper + 1.0) * arr),

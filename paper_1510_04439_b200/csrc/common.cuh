@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 
@@ -33,6 +34,39 @@ struct DevGrid {
     ::dfpca_gpu::cuda_check(cudaGetLastError(), #kernel);                         \
     if (dfpca_prof_slot_ >= 0) (ctx)->kernel_end(dfpca_prof_slot_);               \
     ++(ctx)->launches;                                                            \
+  } while (0)
+
+// Programmatic dependent launch (PDL): the kernel may be scheduled while the
+// previous kernel on the stream drains (its launch latency and rasterization
+// overlap that kernel's tail).  Every kernel launched this way calls
+// pdl_wait() first, which blocks until the previous grid has completed and
+// its memory is visible -- so ordering is exactly that of a plain launch.
+// DFPCA_PDL=0 turns the attribute off (A/B).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DFPCA_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+#define DFPCA_LAUNCH_PDL(ctx, kernel, grid, block, smem, ...)                                     \
+  do {                                                                                           \
+    const int dfpca_prof_slot_ = (ctx)->profile ? (ctx)->kernel_begin(#kernel) : -1;            \
+    cudaLaunchConfig_t dfpca_cfg_{};                                                             \
+    dfpca_cfg_.gridDim = dim3(grid);                                                             \
+    dfpca_cfg_.blockDim = dim3(block);                                                           \
+    dfpca_cfg_.dynamicSmemBytes = (smem);                                                        \
+    dfpca_cfg_.stream = (ctx)->stream;                                                           \
+    cudaLaunchAttribute dfpca_attr_[1];                                                          \
+    dfpca_attr_[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                      \
+    dfpca_attr_[0].val.programmaticStreamSerializationAllowed = ::dfpca_gpu::pdl_enabled() ? 1 : 0; \
+    dfpca_cfg_.attrs = dfpca_attr_;                                                              \
+    dfpca_cfg_.numAttrs = 1;                                                                     \
+    ::dfpca_gpu::cuda_check(cudaLaunchKernelEx(&dfpca_cfg_, kernel, __VA_ARGS__), #kernel);      \
+    if (dfpca_prof_slot_ >= 0) (ctx)->kernel_end(dfpca_prof_slot_);                              \
+    ++(ctx)->launches;                                                                           \
   } while (0)
 
 // Raises (never lowers) a kernel's dynamic shared-memory limit.  The

@@ -112,6 +112,7 @@ constexpr int kProducerThreads = 32;
 template <int R, int NO, int JB, bool BULK>
 __global__ void __launch_bounds__(kThreads + kProducerThreads) k_pass_cols(View in, View o0, View o1, View o2,
                                                                            TapsP tp) {
+  pdl_wait();
   extern __shared__ __align__(128) double sm[];  // [2][n][kTC]
   __shared__ __align__(8) std::uint64_t bar[2];
   __shared__ __align__(8) std::uint64_t empty_bar[2];
@@ -548,6 +549,7 @@ __device__ inline void tpv_conv_cols(const double* Y, int n1, int n2, int ldy, d
 template <int R, bool VO>  // VO: value planes only (the shared design), no mass-order code
 __global__ void __launch_bounds__(kThreads, 2) k_tphase2v(const double* __restrict__ pw, const double* __restrict__ pv,
                                                           i64 rows, int n1, int n2, TPhaseOut out, Taps2P tp) {
+  pdl_wait();
   extern __shared__ double sm[];
   const int ldx = tpv_ldx(n2, R), ldy = tpv_ldy(n2);
   double* X = sm;
@@ -635,7 +637,7 @@ void launch_cols(dfpca_context* ctx, const PassSpec& s, const View& o1, const Vi
   const std::size_t smem = sizeof(double) * 2 * kTC * in.n;
   const int threads = BULK ? kThreads + kProducerThreads : kThreads;
   const unsigned grid = persistent_grid(ctx, k_pass_cols<R, NO, JB, BULK>, smem, tiles, threads);
-  DFPCA_LAUNCH(ctx, (k_pass_cols<R, NO, JB, BULK>), grid, threads, smem, in, s.out[0], o1, o2, tp);
+  DFPCA_LAUNCH_PDL(ctx, (k_pass_cols<R, NO, JB, BULK>), grid, threads, smem, in, s.out[0], o1, o2, tp);
 }
 
 template <int R, int NO>
@@ -683,10 +685,10 @@ void launch_tphase2(dfpca_context* ctx, const TPhase2Spec& s, const Taps2P& tp) 
   if (smem1 <= 200 * 1024 && std::getenv("DFPCA_TPHASE_2BUF") == nullptr) {
     if (s.value_only) {
       const unsigned grid1 = persistent_grid(ctx, k_tphase2v<R, true>, smem1, s.rows);
-      DFPCA_LAUNCH(ctx, (k_tphase2v<R, true>), grid1, kThreads, smem1, s.pw, s.pv, s.rows, n1, n2, out, tp);
+      DFPCA_LAUNCH_PDL(ctx, (k_tphase2v<R, true>), grid1, kThreads, smem1, s.pw, s.pv, s.rows, n1, n2, out, tp);
     } else {
       const unsigned grid1 = persistent_grid(ctx, k_tphase2v<R, false>, smem1, s.rows);
-      DFPCA_LAUNCH(ctx, (k_tphase2v<R, false>), grid1, kThreads, smem1, s.pw, s.pv, s.rows, n1, n2, out, tp);
+      DFPCA_LAUNCH_PDL(ctx, (k_tphase2v<R, false>), grid1, kThreads, smem1, s.pw, s.pv, s.rows, n1, n2, out, tp);
     }
     return;
   }

@@ -149,6 +149,7 @@ __device__ inline void oz_tmem_ld32(unsigned taddr, int (&v)[32]) {
 // with an integer atomicMax (non-negative doubles order like their bits).
 __global__ void k_oz_colmax(const double* __restrict__ A, i64 K, i64 M, i64 lda, const double* __restrict__ w,
                             unsigned long long* __restrict__ ex, unsigned long long* __restrict__ ey) {
+  pdl_wait();
   const i64 m = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
   if (m >= M) return;
   // a NaN / Inf entry poisons its column: the bits of NaN order above every
@@ -231,6 +232,7 @@ __global__ void __launch_bounds__(128) k_oz_slice(const double* __restrict__ A, 
                                                   std::int8_t* __restrict__ xs, std::int8_t* __restrict__ ys,
                                                   double* __restrict__ sx, double* __restrict__ sy, i64 rows_x,
                                                   i64 rows_y, i64 nch, i64 row0, i64 row1, int ry) {
+  pdl_wait();
   const i64 m = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
   const i64 k0 = static_cast<i64>(blockIdx.y) * 16;
   const i64 c = k0 >> 5, g = (k0 >> 4) & 1;
@@ -286,6 +288,7 @@ __global__ void __launch_bounds__(kOzThreads, 1)
     k_oz_syrk(const std::int8_t* __restrict__ xs, const std::int8_t* __restrict__ ys, i64 nch,
               const double* __restrict__ sx, const double* __restrict__ sy, i64 M, double* __restrict__ C, i64 ldc,
               const int2* __restrict__ tiles, int n_tiles, i64 row0, i64 row1) {
+  pdl_wait();
   extern __shared__ __align__(16) std::uint8_t oz_sm[];
   __shared__ __align__(8) std::uint64_t full[kOzStages], empty[kOzStages], tmem_full, tmem_empty;
   __shared__ unsigned tmem_base_sh;
@@ -702,11 +705,11 @@ bool ozaki_syrk(dfpca_context* ctx, i64 G, i64 K, const double* A, i64 lda, cons
   DFPCA_CUDA(cudaMemsetAsync(ex.get(), 0, sizeof(unsigned long long) * G, st));
   DFPCA_CUDA(cudaMemsetAsync(ey.get(), 0, sizeof(unsigned long long) * G, st));
   const dim3 gmax(static_cast<unsigned>((G + 255) / 256), static_cast<unsigned>(std::min<i64>(K, 64)));
-  DFPCA_LAUNCH(ctx, k_oz_colmax, gmax, 256, 0, A, K, G, lda, w, ex.get(), ey.get());
+  DFPCA_LAUNCH_PDL(ctx, k_oz_colmax, gmax, 256, 0, A, K, G, lda, w, ex.get(), ey.get());
   // every row of the padded row blocks is written (zeros past the rows and past K)
   const i64 rows_x = RA * kOzM, rows_y = RB * ry;
   const dim3 gs(static_cast<unsigned>((std::max(rows_x, rows_y) + 127) / 128), static_cast<unsigned>(Kp / 16));
-  DFPCA_LAUNCH(ctx, k_oz_slice, gs, 128, 0, A, K, G, lda, w, ex.get(), ey.get(), xs.get(), ys.get(), sx.get(),
+  DFPCA_LAUNCH_PDL(ctx, k_oz_slice, gs, 128, 0, A, K, G, lda, w, ex.get(), ey.get(), xs.get(), ys.get(), sx.get(),
                sy.get(), rows_x, rows_y, nch, row0, row1, ry);
   // tiles holding some t >= s: (I, J) of 128 x 128 (one CTA), (I2, J) of
   // 256 x 128 (a CTA pair)
@@ -725,7 +728,7 @@ bool ozaki_syrk(dfpca_context* ctx, i64 G, i64 K, const double* A, i64 lda, cons
   } else {
     allow_smem(k_oz_syrk, kOzSmem);
     const unsigned grid = static_cast<unsigned>(std::min<i64>(static_cast<i64>(tiles.size()), ctx->sm_count));
-    DFPCA_LAUNCH(ctx, k_oz_syrk, grid, kOzThreads, kOzSmem, xs.get(), ys.get(), nch, sx.get(), sy.get(), G, C, ldc,
+    DFPCA_LAUNCH_PDL(ctx, k_oz_syrk, grid, kOzThreads, kOzSmem, xs.get(), ys.get(), nch, sx.get(), sy.get(), G, C, ldc,
                  d_tiles.get(), static_cast<int>(tiles.size()), row0, row1);
   }
   return true;

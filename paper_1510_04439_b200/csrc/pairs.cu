@@ -68,6 +68,7 @@ __global__ void k_band_fix(const double* __restrict__ diag_mass, const double* _
                            i64 G, int d, i64 codes, DevGrid g, const double* __restrict__ ps_mass,
                            int identical, const double* __restrict__ w, i64 n_pair, double w_seq,
                            double* __restrict__ pw, double* __restrict__ pv, i64 row0, i64 rows, i64 col0) {
+  pdl_wait();
   // window: band entries of rows u in [row0, row0 + rows) and columns t >= col0;
   // pw / pv point at row row0 (leading dimension G)
   const int lane = threadIdx.x & 31;
@@ -397,7 +398,7 @@ void build_pair_grids(dfpca_context* ctx, const dfpca_binned* b, double* pw, dou
             w.tm_begin, tm_end);
   if (exchange) exchange(pw != nullptr && !b->identical_mass);
   if (pv)
-    DFPCA_LAUNCH(ctx, k_band_fix, grid_for(w.rows * b->codes * 32, 256, 148ll * 32), 256, 0,
+    DFPCA_LAUNCH_PDL(ctx, k_band_fix, grid_for(w.rows * b->codes * 32, 256, 148ll * 32), 256, 0,
                  b->diag_mass.get(), b->diag_value.get(), G, b->grid.d, b->codes, dg,
                  b->ps_mass.get(), b->identical_mass ? 1 : 0, b->pair_weight.get(), n, W, pw, pv, w.row0, w.rows,
                  w.col0);

@@ -682,6 +682,7 @@ template <int N>
 __global__ void __launch_bounds__(kSolveTile, N == 5 ? DFPCA_SOLVE5_MIN_CTAS : DFPCA_SOLVE_MIN_CTAS)
     k_solve_sep_tri(SharedMoments sh, MomPtrs mp, SolveGeom g, unsigned rows, unsigned nch,
                     double* __restrict__ out, unsigned* __restrict__ pending) {
+  pdl_wait();
   constexpr int p = N - 1;
   constexpr int d = p / 2;
   constexpr int nm = 1 + p + p * (p + 1) / 2;
@@ -730,6 +731,7 @@ __global__ void __launch_bounds__(kSolveTile) k_solve_sep_exact(SharedMoments sh
                                                                 double* __restrict__ out,
                                                                 unsigned long long* __restrict__ empty_count,
                                                                 i64* __restrict__ empty_list, i64 list_cap) {
+  pdl_wait();
   constexpr int p = N - 1;
   constexpr int d = p / 2;
   constexpr int nm = 1 + p + p * (p + 1) / 2;
@@ -880,6 +882,7 @@ __global__ void k_ladder(LadderGeom lg, const double* __restrict__ mass, const d
 // accesses coalesced.
 __global__ void k_center_mirror(double* __restrict__ cov, const double* __restrict__ mean,
                                 const std::uint8_t* __restrict__ mask, i64 G, i64 I0, i64 I1, i64 out_row0) {
+  pdl_wait();
   // Slab form (shard.hpp): row tiles [I0, I1) of 32 rows, cov holds global
   // rows from out_row0 on; mirrors land only inside the slab's own rows (the
   // rest reach their owners through the covariance exchange).
@@ -981,10 +984,10 @@ void launch_solve_shared_n(dfpca_context* ctx, const SharedMoments& sh, const Mo
           const unsigned c1 = y1 > y ? nch - sep_first_chunk(g, static_cast<unsigned>(y1), nch) : 0u;
           gx = std::max(gx, c0 + c1);
         }
-        DFPCA_LAUNCH(ctx, k_solve_sep_tri<N>, dim3((gx + kSepLoop - 1) / kSepLoop, static_cast<unsigned>((rows + 1) / 2)),
+        DFPCA_LAUNCH_PDL(ctx, k_solve_sep_tri<N>, dim3((gx + kSepLoop - 1) / kSepLoop, static_cast<unsigned>((rows + 1) / 2)),
                      kSolveTile, 0, sh, mp,
                      g, static_cast<unsigned>(rows), static_cast<unsigned>(nch), out, pending.get());
-        DFPCA_LAUNCH(ctx, k_solve_sep_exact<N>, 148 * 4, kSolveTile, 0, sh, mp, g, pending.get(), out, cnt, list,
+        DFPCA_LAUNCH_PDL(ctx, k_solve_sep_exact<N>, 148 * 4, kSolveTile, 0, sh, mp, g, pending.get(), out, cnt, list,
                      cap);
       } else
         DFPCA_LAUNCH(ctx, k_solve_shared_tri<N>, static_cast<unsigned>(n), kSolveTile, 0, sh, mp, g, nch, out, cnt,
@@ -1708,7 +1711,7 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
     ctx->end_stage();
     ctx->begin_stage("center");
     if (pairs > 0)
-      DFPCA_LAUNCH(ctx, k_center_mirror, static_cast<unsigned>(pairs), 256, 0, surf->values.get(), mean_dev.get(),
+      DFPCA_LAUNCH_PDL(ctx, k_center_mirror, static_cast<unsigned>(pairs), 256, 0, surf->values.get(), mean_dev.get(),
                    grid.has_mask ? mask_dev.get() : nullptr, G, I0, I1, out_row0);
     ctx->end_stage();
     DFPCA_CUDA(cudaStreamSynchronize(st));
@@ -1793,7 +1796,7 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
   // ---- center + symmetrize (K5) ----
   ctx->begin_stage("center");
   if (pairs > 0)
-    DFPCA_LAUNCH(ctx, k_center_mirror, static_cast<unsigned>(pairs), 256, 0, surf->values.get(), mean_dev.get(),
+    DFPCA_LAUNCH_PDL(ctx, k_center_mirror, static_cast<unsigned>(pairs), 256, 0, surf->values.get(), mean_dev.get(),
                  grid.has_mask ? mask_dev.get() : nullptr, G, I0, I1, out_row0);
   ctx->end_stage();
   if (sharded) {  // exchange 2: the lower-triangle blocks of this slab's rows

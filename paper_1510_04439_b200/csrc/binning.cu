@@ -56,6 +56,7 @@ __global__ void k_bin_count(DevGrid g, const i64* __restrict__ offsets, i64 n_sa
                             i64 o0, i64 o1, const i64* __restrict__ pair_slot, int want_grid_records,
                             unsigned* __restrict__ grid_count, unsigned* __restrict__ band_count,
                             unsigned long long* __restrict__ first_bad) {
+  pdl_wait();
   for (i64 o = o0 + blockIdx.x * (i64)blockDim.x + threadIdx.x; o < o1;
        o += (i64)gridDim.x * blockDim.x) {
     const double* x = coords + o * (D > 0 ? D : g.d);
@@ -103,6 +104,7 @@ __global__ void k_bin_emit(DevGrid g, const i64* __restrict__ offsets, i64 n_sam
                            double* __restrict__ gmass, unsigned* __restrict__ gobs,
                            unsigned long long* __restrict__ bkey, unsigned* __restrict__ bval,
                            double* __restrict__ bmm, unsigned* __restrict__ bobs) {
+  pdl_wait();
   for (i64 o = o0 + blockIdx.x * (i64)blockDim.x + threadIdx.x; o < o1;
        o += (i64)gridDim.x * blockDim.x) {
     const double* x = coords + o * (D > 0 ? D : g.d);
@@ -162,6 +164,7 @@ __global__ void k_bin_aggregate(i64 G, i64 key_samples, i64 i0, const unsigned l
                                 const double* __restrict__ values,
                                 const double* __restrict__ mean_w, double* __restrict__ mass,
                                 double* __restrict__ wvalue, double* __restrict__ wsquare) {
+  pdl_wait();
   // One warp per bin: the lanes gather and form the per-record terms of 32
   // consecutive records in parallel and stage them in shared memory; lanes
   // 0, 1, 2 then fold mass, wvalue, wsquare (one sum each) in record order.
@@ -216,6 +219,7 @@ __global__ void k_bin_per_sample(i64 G, i64 key_samples, i64 i0, const unsigned 
                                  const unsigned* __restrict__ robs,
                                  const double* __restrict__ values, const i64* __restrict__ pair_slot,
                                  double* __restrict__ ps_mass, double* __restrict__ ps_value) {
+  pdl_wait();
   for (i64 r0 = blockIdx.x * (i64)blockDim.x + threadIdx.x; r0 < n_rec;
        r0 += (i64)gridDim.x * blockDim.x) {
     const unsigned long long k = key[r0];
@@ -241,6 +245,7 @@ __global__ void k_bin_band(const unsigned long long* __restrict__ key, const uns
                            i64 n_rec, i64 n_keys, const double* __restrict__ bmm,
                            const unsigned* __restrict__ robs, const double* __restrict__ values,
                            double* __restrict__ diag_mass, double* __restrict__ diag_value) {
+  pdl_wait();
   // One warp per band index, records folded in order as in k_bin_aggregate
   // (lane 0 the mass sum, lane 1 the value sum).
   __shared__ double terms[kFoldWarps][2][33];
@@ -283,6 +288,7 @@ __global__ void k_bin_band(const unsigned long long* __restrict__ key, const uns
 // identical_mass flag: any per-sample mass grid differing from slot 0.
 __global__ void k_mass_identical(const double* __restrict__ ps_mass, i64 n_pair, i64 G,
                                  int* __restrict__ differs) {
+  pdl_wait();
   const i64 total = (n_pair - 1) * G;
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
        e += (i64)gridDim.x * blockDim.x) {
@@ -298,6 +304,7 @@ __global__ void k_mass_identical(const double* __restrict__ ps_mass, i64 n_pair,
 // Shared-design probe: mass grid constant, band diagonal-only and constant.
 __global__ void k_shared_design(const double* __restrict__ m, const double* __restrict__ dm, i64 G, i64 codes,
                                 i64 center, int* __restrict__ bad) {
+  pdl_wait();
   const double m0 = m[0], d0 = dm[center];
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < G * codes; e += (i64)gridDim.x * blockDim.x) {
     const i64 u = e / codes, c = e - u * codes;

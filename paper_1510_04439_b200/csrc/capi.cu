@@ -23,6 +23,7 @@ thread_local cudaStream_t g_alloc_stream = nullptr;
 // (SurfaceEstimate::values[i] without downloading the G^2 array).
 __global__ void k_gather_values(const double* __restrict__ values, i64 lo, const i64* __restrict__ index, i64 n,
                                 double* __restrict__ out) {
+  pdl_wait();
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<i64>(gridDim.x) * blockDim.x)
     out[i] = values[index[i] - lo];

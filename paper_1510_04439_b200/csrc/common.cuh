@@ -27,14 +27,9 @@ struct DevGrid {
 // can report how many of its own kernels ran (bench.py "gpu_launches").
 // With profiling enabled (dfpca_profile_enable) each launch is bracketed by
 // CUDA events on the launching stream and attributed to the kernel's name.
-#define DFPCA_LAUNCH(ctx, kernel, grid, block, smem, ...)                         \
-  do {                                                                            \
-    const int dfpca_prof_slot_ = (ctx)->profile ? (ctx)->kernel_begin(#kernel) : -1; \
-    kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);              \
-    ::dfpca_gpu::cuda_check(cudaGetLastError(), #kernel);                         \
-    if (dfpca_prof_slot_ >= 0) (ctx)->kernel_end(dfpca_prof_slot_);               \
-    ++(ctx)->launches;                                                            \
-  } while (0)
+// Every launch is a programmatic dependent launch (below): each kernel of
+// the library begins with pdl_wait().
+#define DFPCA_LAUNCH(ctx, kernel, grid, block, smem, ...) DFPCA_LAUNCH_PDL(ctx, kernel, grid, block, smem, __VA_ARGS__)
 
 // Programmatic dependent launch (PDL): the kernel may be scheduled while the
 // previous kernel on the stream drains (its launch latency and rasterization

@@ -18,6 +18,7 @@ using conv_detail::TapsP;
 // Generic pass: any radius, any axis length; one thread per output element.
 __global__ void k_pass_generic(View in, View o0, View o1, View o2, int n_out,
                                const double* __restrict__ taps, int R) {
+  pdl_wait();
   const i64 total = in.outer * in.n * in.inner;
   const int W = 2 * R + 1;
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;

@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(kThreads + kProducerThreads) k_pass_cols(View 
 // through a shared-memory output tile so the global stores stay coalesced.
 template <int R, int NO>
 __global__ void __launch_bounds__(kThreads) k_pass_rows(View in, View o0, View o1, View o2, TapsP tp) {
+  pdl_wait();
   extern __shared__ double sm[];  // [kLines][n + 1] input, then NO output tiles of the same shape
   const i64 n = in.n;
   const i64 ld = n + 1;
@@ -397,6 +398,7 @@ template <int R>
 __global__ void __launch_bounds__(kThreads) k_tphase2(const double* __restrict__ pw, const double* __restrict__ pv,
                                                       i64 rows, int n1, int n2, int value_only, TPhaseOut out,
                                                       Taps2P tp) {
+  pdl_wait();
   extern __shared__ double sm[];
   const int ld = n2 + 1;
   const int pe = n1 * ld;  // padded plane

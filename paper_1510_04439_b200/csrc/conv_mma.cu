@@ -57,6 +57,7 @@ struct MmaTaps {
 __global__ void __launch_bounds__(kThreadsM, 2)
     k_tphase2_mma(const double* __restrict__ pw, const double* __restrict__ pv, i64 rows, int n1, int n2,
                   int value_only, conv_detail::TPhaseOut out, const MmaTaps* __restrict__ taps_g, int R1, int R2) {
+  pdl_wait();
   extern __shared__ __align__(16) double sm[];
   double* Xb = sm;                      // [2][kRows][kLd]
   double* Y = sm + 2 * kRows * kLd;     // [kRows][kLd]
@@ -246,6 +247,7 @@ __device__ inline void pass_meta(const View& in, int tile, int chunks, int R, in
 
 __global__ void __launch_bounds__(kThreadsM, 2)
     k_pass_cols_mma(View in, View o0, View o1, View o2, int n_out, const PassTaps* __restrict__ taps_g, int R) {
+  pdl_wait();
   extern __shared__ __align__(16) double sm[];
   double* Xb = sm;                  // [2][kRows][kLd]
   double* tz = sm + 2 * kRows * kLd;  // PassTaps

@@ -78,6 +78,7 @@ template <int D>
 __global__ void __launch_bounds__(kUnitsPerCta * kGroups)
     k_cv_mean_partials(CvData data, const double* __restrict__ tgt, int n_units, const double* __restrict__ hh,
                        int squares, i64 chunk_len, double* __restrict__ partial) {
+  pdl_wait();
   constexpr int NM = 1 + D + D * (D + 1) / 2, NL = 1 + D;
   __shared__ double sx[kObsTile][D];
   __shared__ double sy[kObsTile], sw[kObsTile];
@@ -142,6 +143,7 @@ template <int D>
 __global__ void __launch_bounds__(kUnitsPerCta * kGroups)
     k_cv_pair_partials(CvData data, const double* __restrict__ tgt, int n_units, const double* __restrict__ hh,
                        i64 chunk_len, double* __restrict__ partial) {
+  pdl_wait();
   constexpr int P = 2 * D;
   constexpr int NM = 1 + P + P * (P + 1) / 2, NL = 1 + P;
   extern __shared__ double red_dyn[];  // [kGroups][kUnitsPerCta][NM + NL]
@@ -305,6 +307,7 @@ template <int N>
 __global__ void k_cv_finish(const double* __restrict__ partial, int n_chunks, int n_units,
                             const UnitInfo* __restrict__ info, double kernel0, double* __restrict__ term,
                             int* __restrict__ flag) {
+  pdl_wait();
   constexpr int p = N - 1, NM = 1 + p + p * (p + 1) / 2, NL = 1 + p;
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= n_units) return;

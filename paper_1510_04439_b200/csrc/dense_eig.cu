@@ -163,6 +163,7 @@ constexpr int kTrdMaxPer = 4;  // row elements per thread prefetched into regist
 __global__ void __launch_bounds__(kTrdThreads, 1)
     k_trd(double* __restrict__ A, int n, double* __restrict__ d, double* __restrict__ e, double* __restrict__ taus,
           double* __restrict__ V, double* __restrict__ p, double* __restrict__ part) {
+  pdl_wait();
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double sh[];  // v [n], w [n], next row [n], v_next [n]
   double* sv = sh;
@@ -298,6 +299,7 @@ __host__ __device__ inline int sturm_count(const double* __restrict__ d, const d
 // each: 32-point multisection of [gl, gu] to the dstebz tolerance.
 __global__ void k_bisect(const double* __restrict__ d, const double* __restrict__ e2, int n, int a0, int count,
                          double gl, double gu, double pivmin, double* __restrict__ lam) {
+  pdl_wait();
   const int j = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (j >= count) return;
   const int idx = a0 + j;
@@ -328,6 +330,7 @@ __device__ inline double lu_rcp(double x) {
 __global__ void k_tri_invit(const double* __restrict__ d, const double* __restrict__ e, int n,
                             const double* __restrict__ shift, int count, double tnorm, double* __restrict__ Y,
                             double* __restrict__ work, int* __restrict__ iwork) {
+  pdl_wait();
   const int c = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (c >= count) return;
   double* du = work + static_cast<i64>(c) * 4 * n;
@@ -407,6 +410,7 @@ __global__ void k_tri_invit(const double* __restrict__ d, const double* __restri
 // Orthonormalises each cluster's vectors in order (two Gram-Schmidt passes
 // against the earlier members), one warp per cluster.
 __global__ void k_cluster_mgs(int n, const int* __restrict__ cl_start, int n_clusters, double* __restrict__ Y) {
+  pdl_wait();
   const int cl = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (cl >= n_clusters) return;
   const int c0 = cl_start[cl], c1 = cl_start[cl + 1];
@@ -436,6 +440,7 @@ constexpr int kBtThreads = 512;
 __global__ void __launch_bounds__(kBtThreads) k_back_transform(const double* __restrict__ V,
                                                                const double* __restrict__ taus, int n,
                                                                const double* __restrict__ Y, double* __restrict__ X) {
+  pdl_wait();
   extern __shared__ double xs[];
   __shared__ double red[2][kBtThreads / 32];
   const int c = blockIdx.x, lane = threadIdx.x & 31, wib = threadIdx.x >> 5;

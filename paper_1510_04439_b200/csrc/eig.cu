@@ -48,6 +48,7 @@ __host__ __device__ inline unsigned long long splitmix64(unsigned long long x) {
 __global__ void __launch_bounds__(kMtN) k_mt19937_64(unsigned long long seed, i64 n_words,
                                                      unsigned long long* __restrict__ out,
                                                      unsigned long long* __restrict__ state, int resume) {
+  pdl_wait();
   __shared__ unsigned long long buf[2][kMtN];
   if (resume) {
     buf[0][threadIdx.x] = state[threadIdx.x];
@@ -93,6 +94,7 @@ __global__ void __launch_bounds__(kMtN) k_mt19937_64(unsigned long long seed, i6
 // GEMM's K-major operand.
 __global__ void k_box_muller(const unsigned long long* __restrict__ words, i64 M, i64 q, i64 ldq, double sd,
                              i64 p_begin, i64 p_end, double* __restrict__ omega) {
+  pdl_wait();
   const i64 total = M * q;
   for (i64 pidx = p_begin + blockIdx.x * (i64)blockDim.x + threadIdx.x; pidx < p_end;
        pidx += (i64)gridDim.x * blockDim.x) {
@@ -115,6 +117,7 @@ __global__ void k_box_muller(const unsigned long long* __restrict__ words, i64 M
 // ----------------------------------------------------------- helpers ----
 __global__ void k_gather_sigma(const double* __restrict__ cov, i64 G, const i64* __restrict__ node_of_row,
                                i64 M, double* __restrict__ sig) {
+  pdl_wait();
   const i64 total = M * M;
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
        e += (i64)gridDim.x * blockDim.x) {
@@ -126,6 +129,7 @@ __global__ void k_gather_sigma(const double* __restrict__ cov, i64 G, const i64*
 // out[c][r] = in[r][c] for r < rows, c < cols (row strides ld_in, ld_out).
 __global__ void k_transpose(const double* __restrict__ in, i64 rows, i64 cols, i64 ld_in, double* __restrict__ out,
                             i64 ld_out) {
+  pdl_wait();
   __shared__ double tile[32][33];
   const i64 tiles_c = (cols + 31) / 32;
   const i64 br = blockIdx.x / tiles_c, bc = blockIdx.x % tiles_c;
@@ -193,6 +197,7 @@ __device__ void make_reflector(double* col, i64 j, i64 M, double* tau, double* r
 // column j+1 then forms reflector j+1.  Launch with j = -1 to only form
 // reflector 0.
 __global__ void k_house_step(double* __restrict__ Yt, i64 M, i64 q, i64 j, double* __restrict__ tau) {
+  pdl_wait();
   __shared__ double red[33];
   const i64 c = j + 1 + blockIdx.x;
   if (c >= q) return;
@@ -210,6 +215,7 @@ __global__ void k_house_step(double* __restrict__ Yt, i64 M, i64 q, i64 j, doubl
 
 // Q = H_0 ... H_{q-1} [I; 0], backward accumulation; Qt rows are Q columns.
 __global__ void k_q_init(double* __restrict__ Qt, i64 M, i64 q) {
+  pdl_wait();
   const i64 total = q * M;
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
        e += (i64)gridDim.x * blockDim.x) {
@@ -220,6 +226,7 @@ __global__ void k_q_init(double* __restrict__ Qt, i64 M, i64 q) {
 
 __global__ void k_q_apply(const double* __restrict__ Yt, const double* __restrict__ tau, i64 M, i64 q,
                           i64 j, double* __restrict__ Qt) {
+  pdl_wait();
   __shared__ double red[33];
   const i64 c = j + blockIdx.x;
   if (c >= q) return;
@@ -239,6 +246,7 @@ __global__ void k_q_apply(const double* __restrict__ Yt, const double* __restric
 __global__ void __launch_bounds__(1024) k_jacobi(double* __restrict__ Ag, double* __restrict__ Vg, int n,
                                                  double* __restrict__ evals, int* __restrict__ info,
                                                  int in_smem) {
+  pdl_wait();
   extern __shared__ double sh[];
   const int np = (n + 1) & ~1;  // padded to even (index n is a dummy)
   double* cs = sh;               // [np/2] cos
@@ -407,6 +415,7 @@ constexpr int kCqMaxQ = 128;
 // factorization is bound by its pivot chain, and more warps hide it better.
 __global__ void __launch_bounds__(1024) k_chol_factor(const double* __restrict__ Gg, int q, double* __restrict__ Rg,
                                                       double* __restrict__ flags, double shift_scale) {
+  pdl_wait();
   extern __shared__ double sm[];
   const int ld = q + 1;
   double* R = sm;
@@ -467,6 +476,7 @@ __global__ void __launch_bounds__(kTrsmWarps * 32) k_row_trsm(const double* __re
                                                               const double* __restrict__ Rg,
                                                               const double* __restrict__ flags,
                                                               double* __restrict__ Xout) {
+  pdl_wait();
   if (flags[0] != 0.0) return;
   extern __shared__ double sm[];
   double* R = sm;           // [q][q]
@@ -602,6 +612,7 @@ __global__ void __launch_bounds__(kEigThreads) k_tri_eig(const double* __restric
                                                           int* __restrict__ info, int max_vec,
                                                           double* __restrict__ Vt,
                                                           const double* __restrict__ qr_flags, int qr_passes) {
+  pdl_wait();
   // a Cholesky QR the host will reject (qr_accepted) makes this call moot:
   // skip it rather than spend the eigensolve on a basis about to be redone
   if (qr_flags && !qr_accepted(qr_flags, qr_passes)) return;
@@ -977,6 +988,7 @@ __global__ void __launch_bounds__(1024) k_finalize(const double* __restrict__ Lt
                                                    double* __restrict__ kept, int* __restrict__ kept_src,
                                                    int* __restrict__ n_kept, int gram_schmidt, int n_avail,
                                                    int* __restrict__ exhausted) {
+  pdl_wait();
   __shared__ double red[33];
   __shared__ i64 first_nz;
   int nk = 0;
@@ -1027,6 +1039,7 @@ __global__ void __launch_bounds__(1024) k_finalize(const double* __restrict__ Lt
 
 __global__ void k_residual_norms(const double* __restrict__ SV, const double* __restrict__ V, i64 M, i64 L,
                                  const double* __restrict__ lam, double cv, double* __restrict__ out) {
+  pdl_wait();
   __shared__ double red[33];
   const i64 l = blockIdx.x;
   double s = 0.0;
@@ -1082,6 +1095,7 @@ struct RowShard {
 
 __global__ void k_gather_rows(const double* __restrict__ slab, i64 G, i64 row0, const i64* __restrict__ rows_nodes,
                               i64 m_loc, const i64* __restrict__ node_of_row, i64 M, double* __restrict__ out) {
+  pdl_wait();
   const i64 total = m_loc * M;
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total; e += (i64)gridDim.x * blockDim.x) {
     const i64 r = e / M, c = e % M;
@@ -1453,6 +1467,7 @@ struct CusolverApi {
 };
 
 __global__ void k_reverse_rows(const double* __restrict__ in, i64 rows, i64 cols, double* __restrict__ out) {
+  pdl_wait();
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < rows * cols; e += (i64)gridDim.x * blockDim.x) {
     const i64 r = e / cols, c = e % cols;
     out[(rows - 1 - r) * cols + c] = in[e];

@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
               i64 ldb, double* __restrict__ C, i64 ldc, int symmetric, i64 tiles_n, i64 k_chunk,
               i64 split_stride, i64 tm_begin, i64 tm_end, const int4* __restrict__ items,
               double* __restrict__ ws, i64 k_mid, i64 a_col0) {
+  pdl_wait();
   extern __shared__ __align__(16) double smem[];
 
   // symmetric: one work item per CTA (items, sym_items()): a tile pair
@@ -198,6 +199,7 @@ __global__ void __launch_bounds__(NTHREADS, CTAS_PER_SM)
 // that order), written like a whole tile (direct, and mirrored inside the slab).
 __global__ void k_sym_split_reduce(const int4* __restrict__ split_items, const double* __restrict__ ws, i64 M,
                                    i64 N, double* __restrict__ C, i64 ldc, i64 tm_begin, i64 tm_end) {
+  pdl_wait();
   const int4 it = split_items[blockIdx.x];
   const i64 tm = it.x, tn = it.y;
   const double* w0 = ws + static_cast<i64>(it.w) * 2 * (BM * BN);
@@ -216,6 +218,7 @@ __global__ void k_sym_split_reduce(const int4* __restrict__ split_items, const d
 // Deterministic split-K reduction: slabs summed in ascending split order.
 __global__ void k_splitk_reduce(const double* __restrict__ ws, i64 splits, i64 M, i64 N,
                                 double* __restrict__ C, i64 ldc) {
+  pdl_wait();
   const i64 total = M * N;
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
        e += (i64)gridDim.x * blockDim.x) {
@@ -230,6 +233,7 @@ __global__ void k_splitk_reduce(const double* __restrict__ ws, i64 splits, i64 M
 // reference's pw * m); a slab scales only the columns of its own row tiles.
 __global__ void k_scale_rows(const double* __restrict__ in, const double* __restrict__ w, i64 K, i64 M,
                              i64 ld, i64 col0, double* __restrict__ out) {
+  pdl_wait();
   const i64 total = K * M;
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
        e += (i64)gridDim.x * blockDim.x) {

@@ -292,6 +292,7 @@ __device__ __forceinline__ u64 newline_bits(u64 v) {
 }
 
 __global__ void __launch_bounds__(kThreads) k_nl_count(const u64* __restrict__ text, i64 words, i64* counts) {
+  pdl_wait();
   using Reduce = cub::BlockReduce<int, kThreads>;
   __shared__ typename Reduce::TempStorage tmp;
   const i64 tiles = (words + kThreads - 1) / kThreads;
@@ -306,6 +307,7 @@ __global__ void __launch_bounds__(kThreads) k_nl_count(const u64* __restrict__ t
 
 __global__ void __launch_bounds__(kThreads) k_nl_write(const u64* __restrict__ text, i64 words,
                                                      const i64* __restrict__ tile_off, i64* nl) {
+  pdl_wait();
   using Scan = cub::BlockScan<int, kThreads>;
   __shared__ typename Scan::TempStorage tmp;
   const i64 tiles = (words + kThreads - 1) / kThreads;
@@ -349,6 +351,7 @@ struct SplitOut {
 // Pass 1, one thread per line: one scan of the line's bytes records the
 // field bounds (the reference's split rule) and checks the field count.
 __global__ void __launch_bounds__(kThreads) k_split_lines(Lines ln, i64 n_lines, int F, char delim, SplitOut o) {
+  pdl_wait();
   for (i64 L = 1 + blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; L < n_lines;
        L += static_cast<i64>(gridDim.x) * blockDim.x) {
     i64 st, en;
@@ -471,6 +474,7 @@ constexpr i64 kFieldChunk = 4096;
 
 __global__ void __launch_bounds__(kThreads) k_parse_fields(Lines ln, i64 n_lines, int F, const i64* is_rec,
                                                            const u64* fb, double* vals, u64* err) {
+  pdl_wait();
   const int nv = F - 1;
   const i64 per = n_lines - 1;
   for (i64 e = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; e < per * nv;
@@ -501,6 +505,7 @@ __global__ void __launch_bounds__(kThreads) k_parse_fields(Lines ln, i64 n_lines
 }
 
 __global__ void k_rec_line(const i64* is_rec, const i64* rec_idx, i64 n_lines, i64* rec_line) {
+  pdl_wait();
   for (i64 L = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; L < n_lines;
        L += static_cast<i64>(gridDim.x) * blockDim.x)
     if (is_rec[L]) rec_line[rec_idx[L]] = L;
@@ -515,6 +520,7 @@ __device__ bool same_id(const char* t, i64 a, int la, i64 b, int lb) {
 
 __global__ void k_run_heads(const char* text, const i64* rec_line, const i64* id_start, const int* id_len, i64 n_rec,
                             i64* head) {
+  pdl_wait();
   for (i64 r = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; r < n_rec;
        r += static_cast<i64>(gridDim.x) * blockDim.x) {
     if (r == 0) {
@@ -529,6 +535,7 @@ __global__ void k_run_heads(const char* text, const i64* rec_line, const i64* id
 // Heads: record index, id bounds, length; max id length.
 __global__ void k_head_list(const i64* head, const i64* head_idx, const i64* rec_line, const i64* id_start,
                             const int* id_len, i64 n_rec, i64* head_rec, i64* h_start, int* h_len, int* max_len) {
+  pdl_wait();
   for (i64 r = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; r < n_rec;
        r += static_cast<i64>(gridDim.x) * blockDim.x) {
     if (!head[r]) continue;
@@ -541,6 +548,7 @@ __global__ void k_head_list(const i64* head, const i64* head_idx, const i64* rec
 }
 
 __global__ void k_iota(i64* p, i64 n) {
+  pdl_wait();
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<i64>(gridDim.x) * blockDim.x)
     p[i] = i;
@@ -549,6 +557,7 @@ __global__ void k_iota(i64* p, i64 n) {
 // chunk c (8 bytes, big-endian, zero padded) of head perm[i]'s id, or its length (c < 0)
 __global__ void k_chunk_keys(const char* text, const i64* h_start, const int* h_len, const i64* perm, i64 n, int c,
                              u64* keys) {
+  pdl_wait();
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<i64>(gridDim.x) * blockDim.x) {
     const i64 h = perm[i];
@@ -568,6 +577,7 @@ __global__ void k_chunk_keys(const char* text, const i64* h_start, const int* h_
 
 __global__ void k_group_flags(const char* text, const i64* h_start, const int* h_len, const i64* perm, i64 n,
                               i64* newgrp, i64* first_flag) {
+  pdl_wait();
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<i64>(gridDim.x) * blockDim.x) {
     const i64 h = perm[i];
@@ -581,6 +591,7 @@ __global__ void k_group_flags(const char* text, const i64* h_start, const int* h
 // sample of every head = rank (in head order) of its group's first head
 __global__ void k_group_sample(const i64* perm, const i64* newgrp, const i64* grp_ex, const i64* rank, i64 n,
                                i64* sample_of_group, i64* first_head_of_sample) {
+  pdl_wait();
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<i64>(gridDim.x) * blockDim.x) {
     if (!newgrp[i]) continue;
@@ -592,12 +603,14 @@ __global__ void k_group_sample(const i64* perm, const i64* newgrp, const i64* gr
 
 __global__ void k_head_sample(const i64* perm, const i64* newgrp, const i64* grp_ex, const i64* sample_of_group,
                               i64 n, u64* head_sample) {
+  pdl_wait();
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<i64>(gridDim.x) * blockDim.x)
     head_sample[perm[i]] = static_cast<u64>(sample_of_group[grp_ex[i] + newgrp[i] - 1]);
 }
 
 __global__ void k_run_lengths(const i64* sorted_heads, const i64* head_rec, i64 n_heads, i64 n_rec, i64* len) {
+  pdl_wait();
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n_heads;
        i += static_cast<i64>(gridDim.x) * blockDim.x) {
     const i64 h = sorted_heads[i];
@@ -607,6 +620,7 @@ __global__ void k_run_lengths(const i64* sorted_heads, const i64* head_rec, i64 
 
 __global__ void k_run_base(const i64* sorted_heads, const u64* sorted_sample, const i64* run_off, i64 n_heads,
                            i64 n_samples, i64 n_rec, i64* run_base, i64* offsets) {
+  pdl_wait();
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n_heads;
        i += static_cast<i64>(gridDim.x) * blockDim.x) {
     run_base[sorted_heads[i]] = run_off[i];
@@ -618,6 +632,7 @@ __global__ void k_run_base(const i64* sorted_heads, const u64* sorted_sample, co
 __global__ void k_scatter(const i64* head, const i64* head_idx, const i64* run_base, const i64* head_rec,
                           const i64* rec_line, const double* vals, i64 n_lines, i64 n_rec, int d, double* coords,
                           double* values) {
+  pdl_wait();
   for (i64 r = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; r < n_rec;
        r += static_cast<i64>(gridDim.x) * blockDim.x) {
     const i64 h = head_idx[r] + head[r] - 1;
@@ -629,6 +644,7 @@ __global__ void k_scatter(const i64* head, const i64* head_idx, const i64* run_b
 }
 
 __global__ void k_id_lengths(const i64* first_head, const int* h_len, i64 n_samples, i64* len) {
+  pdl_wait();
   for (i64 s = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; s < n_samples;
        s += static_cast<i64>(gridDim.x) * blockDim.x)
     len[s] = h_len[first_head[s]];
@@ -636,6 +652,7 @@ __global__ void k_id_lengths(const i64* first_head, const int* h_len, i64 n_samp
 
 __global__ void k_id_gather(const char* text, const i64* first_head, const i64* h_start, const int* h_len,
                             const i64* id_off, i64 n_samples, char* out) {
+  pdl_wait();
   for (i64 s = blockIdx.x; s < n_samples; s += gridDim.x) {
     const i64 h = first_head[s];
     for (int b = threadIdx.x; b < h_len[h]; b += blockDim.x) out[id_off[s] + b] = text[h_start[h] + b];

@@ -506,6 +506,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kOzThreads, 1)
     k_oz_syrk2(const std::int8_t* __restrict__ xs, const std::int8_t* __restrict__ ys, i64 nch,
                const double* __restrict__ sx, const double* __restrict__ sy, i64 M, double* __restrict__ C, i64 ldc,
                const int2* __restrict__ tiles, int n_tiles, i64 row0, i64 row1) {
+  pdl_wait();
   extern __shared__ __align__(16) std::uint8_t oz_sm[];
   __shared__ __align__(8) std::uint64_t full[kOz2Stages], peer_full[kOz2Stages], empty[kOz2Stages], tmem_full,
       tmem_empty;

@@ -44,6 +44,7 @@ namespace {
 // (pw points at row row0, leading dimension G).
 __global__ void k_rank_one(double* __restrict__ pw, const double* __restrict__ m, double W, i64 G, i64 row0,
                            i64 rows, i64 col0) {
+  pdl_wait();
   const i64 w = G - col0;
   const i64 total = rows * w;
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < total;
@@ -132,6 +133,7 @@ constexpr int kSparseThreads = 256;
 // nonzero count of every per-sample mass grid (block per sample)
 __global__ void __launch_bounds__(kSparseThreads) k_nnz_count(const double* __restrict__ ps_mass, i64 G,
                                                               i64* __restrict__ nnz) {
+  pdl_wait();
   using Reduce = cub::BlockReduce<i64, kSparseThreads>;
   __shared__ typename Reduce::TempStorage tmp;
   const double* m = ps_mass + static_cast<i64>(blockIdx.x) * G;
@@ -150,6 +152,7 @@ __global__ void __launch_bounds__(kSparseThreads) k_nnz_compact(const double* __
                                                                 i64 col0, int* __restrict__ nz_f,
                                                                 double* __restrict__ nz_m, double* __restrict__ nz_v,
                                                                 int* __restrict__ nz_s, i64* __restrict__ ranges) {
+  pdl_wait();
   using Scan = cub::BlockScan<int, kSparseThreads>;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int base;
@@ -202,6 +205,7 @@ __global__ void __launch_bounds__(kSparseThreads) k_pair_emit(const i64* __restr
                                                               unsigned long long* __restrict__ key,
                                                               unsigned* __restrict__ val, unsigned* __restrict__ ra,
                                                               unsigned* __restrict__ rb) {
+  pdl_wait();
   const int i = blockIdx.x;
   const i64 off = nz_off[i], end = nz_off[i + 1];
   const i64 a0 = off + ranges[3 * i], a1 = off + ranges[3 * i + 1], b0 = off + ranges[3 * i + 2];
@@ -224,6 +228,7 @@ __global__ void k_pair_sum(const unsigned long long* __restrict__ key, const uns
                            const double* __restrict__ nz_m, const double* __restrict__ nz_v,
                            const int* __restrict__ nz_s, const double* __restrict__ w, i64 G, i64 col0,
                            double* __restrict__ pw, double* __restrict__ pv) {
+  pdl_wait();
   const i64 cols = G - col0;
   for (i64 r0 = blockIdx.x * (i64)blockDim.x + threadIdx.x; r0 < n_rec; r0 += (i64)gridDim.x * blockDim.x) {
     const unsigned long long k = key[r0];
@@ -246,6 +251,7 @@ __global__ void k_pair_sum(const unsigned long long* __restrict__ key, const uns
 __global__ void k_band_sub(const double* __restrict__ diag_mass, const double* __restrict__ diag_value, i64 G,
                            int d, i64 codes, DevGrid g, double* __restrict__ pw, double* __restrict__ pv, i64 row0,
                            i64 rows, i64 col0) {
+  pdl_wait();
   const i64 total = rows * codes;
   for (i64 e0 = blockIdx.x * (i64)blockDim.x + threadIdx.x; e0 < total; e0 += (i64)gridDim.x * blockDim.x) {
     const i64 e = e0 + row0 * codes;

@@ -60,6 +60,7 @@ __device__ inline double interp_dev(const DevGrid& g, const double* __restrict__
 
 // ---- estimate_sigma2 ----
 __global__ void k_cov_diagonal(const double* __restrict__ slab, i64 G, i64 row0, i64 rows, double* __restrict__ diag) {
+  pdl_wait();
   for (i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x; r < rows; r += (i64)gridDim.x * blockDim.x)
     diag[row0 + r] = slab[r * G + row0 + r];
 }
@@ -67,6 +68,7 @@ __global__ void k_cov_diagonal(const double* __restrict__ slab, i64 G, i64 row0,
 __global__ void k_sigma2(const double* __restrict__ dpn, const double* __restrict__ gdiag,
                          const double* __restrict__ mean, const std::uint8_t* __restrict__ mask, i64 G,
                          double* __restrict__ out) {
+  pdl_wait();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double acc = 0.0;
   i64 count = 0;
@@ -88,6 +90,7 @@ __global__ void k_tent_grid(DevGrid g, const i64* __restrict__ offsets, i64 n_sa
                             const double* __restrict__ coords, const double* __restrict__ values,
                             double* __restrict__ mass, double* __restrict__ wval,
                             unsigned long long* __restrict__ bad) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const i64 warps = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
   const int corners = 1 << g.d;
@@ -120,6 +123,7 @@ __global__ void k_integration_scores(const double* __restrict__ mass, const doub
                                      const double* __restrict__ mean, const double* __restrict__ phi,
                                      const std::uint8_t* __restrict__ mask, i64 G, i64 n, i64 L, double cv,
                                      double* __restrict__ out) {
+  pdl_wait();
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < n * L; e += (i64)gridDim.x * blockDim.x) {
     const i64 i = e / L, l = e % L;
     const double* m = mass + i * G;
@@ -161,6 +165,7 @@ struct PaceArgs {
 // cap * (L + 2) + cap^2 doubles and 3 cap ints (any observation count).
 template <bool BIG>
 __global__ void k_pace(PaceArgs a, const i64* big_list, double* ws, int* iws, i64 cap) {
+  pdl_wait();
   extern __shared__ double sm[];
   const i64 i = BIG ? big_list[blockIdx.x] : static_cast<i64>(blockIdx.x);
   if (i >= a.n_samples) return;
@@ -372,6 +377,7 @@ __global__ void k_pace(PaceArgs a, const i64* big_list, double* ws, int* iws, i6
 // ---- reconstruct_on_grid ----
 __global__ void k_reconstruct(const double* __restrict__ mean, const double* __restrict__ phi, i64 G, i64 L,
                               const double* __restrict__ scores, i64 n, double* __restrict__ out) {
+  pdl_wait();
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < n * G; e += (i64)gridDim.x * blockDim.x) {
     const i64 i = e / G, f = e % G;
     const double mu = mean[f];

@@ -55,6 +55,7 @@ __device__ inline int find_block(const PackDesc* __restrict__ d, int n, i64 x) {
 // both sides coalesced).  One launch packs every block of a phase.
 __global__ void k_pack_blocks(const double* __restrict__ src, i64 ld, i64 row0, const PackDesc* __restrict__ desc,
                               int n_desc, double* __restrict__ packed) {
+  pdl_wait();
   __shared__ double tile[32][33];
   const PackDesc b = desc[find_block(desc, n_desc, blockIdx.x)];
   const i64 w = b.c1 - b.c0, h = b.r1 - b.r0;
@@ -85,6 +86,7 @@ __global__ void k_pack_blocks(const double* __restrict__ src, i64 ld, i64 row0, 
 // across the columns (coalesced on both sides).
 __global__ void k_unpack_blocks(const double* __restrict__ packed, double* __restrict__ dst, i64 ld, i64 row0,
                                 const PackDesc* __restrict__ desc, int n_desc) {
+  pdl_wait();
   const PackDesc b = desc[find_block(desc, n_desc, blockIdx.x)];
   const i64 w = b.c1 - b.c0;
   const i64 s = blockIdx.x - b.first;

@@ -167,6 +167,7 @@ template <int N>
 __global__ void __launch_bounds__(128) k_solve(MomPtrs mp, SolveGeom g, double* __restrict__ out,
                                                unsigned long long* __restrict__ empty_count,
                                                i64* __restrict__ empty_list, i64 list_cap) {
+  pdl_wait();
   constexpr int p = N - 1;
   constexpr int nm = 1 + p + p * (p + 1) / 2;
   constexpr int nl = 1 + p;
@@ -246,6 +247,7 @@ __global__ void __launch_bounds__(128) k_solve_shared(SharedMoments sh, MomPtrs 
                                                       double* __restrict__ out,
                                                       unsigned long long* __restrict__ empty_count,
                                                       i64* __restrict__ empty_list, i64 list_cap) {
+  pdl_wait();
   constexpr int p = N - 1;
   constexpr int d = p / 2;
   constexpr int nm = 1 + p + p * (p + 1) / 2;
@@ -419,6 +421,7 @@ template <int N>
 __global__ void __launch_bounds__(kSolveTile) k_solve_tri(MomPtrs mp, SolveGeom g, int nch, double* __restrict__ out,
                                                           unsigned long long* __restrict__ empty_count,
                                                           i64* __restrict__ empty_list, i64 list_cap) {
+  pdl_wait();
   solve_tri_body<N, false>(SharedMoments{}, mp, g, nch, out, empty_count, empty_list, list_cap);
 }
 #ifndef DFPCA_SOLVE5_MIN_CTAS
@@ -433,6 +436,7 @@ template <int N>
 __global__ void __launch_bounds__(kSolveTile, N == 5 ? 8 : DFPCA_SOLVE_MIN_CTAS)
     k_solve_shared_tri(SharedMoments sh, MomPtrs mp, SolveGeom g, int nch, double* __restrict__ out,
                        unsigned long long* __restrict__ empty_count, i64* __restrict__ empty_list, i64 list_cap) {
+  pdl_wait();
   solve_tri_body<N, true>(sh, mp, g, nch, out, empty_count, empty_list, list_cap);
 }
 
@@ -785,6 +789,7 @@ struct LadderGeom {
 __global__ void k_ladder(LadderGeom lg, const double* __restrict__ mass, const double* __restrict__ value,
                          const i64* __restrict__ nodes, i64 n_nodes, double* __restrict__ out,
                          unsigned long long* __restrict__ still_empty) {
+  pdl_wait();
   __shared__ double red[256];
   __shared__ double acc[kMaxNm + kMaxNl];
   __shared__ int status_sh;
@@ -924,6 +929,7 @@ __global__ void k_center_mirror(double* __restrict__ cov, const double* __restri
 // s <= t) and their mirrors: the entries the ladder refitted after it.
 __global__ void k_center_list(double* __restrict__ cov, const double* __restrict__ mean,
                               const std::uint8_t* __restrict__ mask, i64 G, const i64* __restrict__ list, i64 n) {
+  pdl_wait();
   for (i64 q = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; q < n;
        q += static_cast<i64>(gridDim.x) * blockDim.x) {
     const i64 dst = list[q], a = dst / G, b = dst % G;
@@ -935,6 +941,7 @@ __global__ void k_center_list(double* __restrict__ cov, const double* __restrict
 }
 
 __global__ void k_fill_nan(double* p, i64 n) {
+  pdl_wait();
   for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < n; e += (i64)gridDim.x * blockDim.x)
     p[e] = __longlong_as_double(0x7ff8000000000000ll);
 }

@@ -500,8 +500,13 @@ bool dense_top_eigenpairs(dfpca_context* ctx, const double* sigma, i64 M, int co
     int nn = n;
     void* args[] = {&a, &nn, &dp, &ep, &tp, &vp, &pp, &qp};
     const int slot = ctx->profile ? ctx->kernel_begin("k_trd") : -1;
-    DFPCA_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_trd), dim3(blocks), dim3(kTrdThreads), args,
-                                           shm, st));
+    const cudaError_t le = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_trd), dim3(blocks),
+                                                       dim3(kTrdThreads), args, shm, st);
+    if (le == cudaErrorCooperativeLaunchTooLarge) {  // SMs taken (e.g. by MPS limits): the library path
+      cudaGetLastError();
+      return false;
+    }
+    DFPCA_CUDA(le);
     if (slot >= 0) ctx->kernel_end(slot);
     ++ctx->launches;
   }

@@ -435,37 +435,62 @@ __global__ void k_cluster_mgs(int n, const int* __restrict__ cl_start, int n_clu
 }
 
 // X[c] = H_0 ... H_{n-3} Y[c] (H_k = I - tau_k v_k v_k^T on indices k + 1 ..),
-// one CTA per vector, held in shared memory.
+// one CTA per vector, held in shared memory; the next reflector streams into
+// a second shared buffer (cp.async) while the current one is applied, so the
+// per-reflector chain is two barriers and no global-memory latency.  The
+// partial sums alternate between two reduction buffers, so a fast warp's
+// next partial cannot overwrite one still being read.
 constexpr int kBtThreads = 512;
+__device__ __forceinline__ void bt_cp8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src));
+}
 __global__ void __launch_bounds__(kBtThreads) k_back_transform(const double* __restrict__ V,
                                                                const double* __restrict__ taus, int n,
                                                                const double* __restrict__ Y, double* __restrict__ X) {
   pdl_wait();
-  extern __shared__ double xs[];
+  extern __shared__ double bsm[];  // x [n], tau [n], v buffers [2][n]
+  double* xs = bsm;
+  double* ts = bsm + n;
+  double* ub[2] = {bsm + 2 * n, bsm + 3 * n};
   __shared__ double red[2][kBtThreads / 32];
   const int c = blockIdx.x, lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < n; i += kBtThreads) xs[i] = Y[static_cast<i64>(c) * n + i];
-  __syncthreads();
-  int par = 0;
-  for (int k = n - 3; k >= 0; --k) {
-    const double tau = taus[k];
-    if (tau == 0.0) continue;
-    const int m = n - k - 1;
+  for (int i = threadIdx.x; i < n; i += kBtThreads) {
+    xs[i] = Y[static_cast<i64>(c) * n + i];
+    ts[i] = i + 2 < n ? taus[i] : 0.0;
+  }
+  auto issue = [&](int k, double* dst) {
     const double* u = V + static_cast<i64>(k) * n + k + 1;
+    for (int j = threadIdx.x; j < n - k - 1; j += kBtThreads) bt_cp8(dst + j, u + j);
+  };
+  int k = n - 3, b = 0, par = 0;
+  if (k >= 0) issue(k, ub[0]);
+  asm volatile("cp.async.commit_group;\n" ::);
+  for (; k >= 0; --k) {
+    // v_k has landed and every thread is past the previous reflector's update
+    // (so its buffer, ub[b ^ 1], may be refilled with v_{k-1})
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    if (k >= 1) issue(k - 1, ub[b ^ 1]);
+    asm volatile("cp.async.commit_group;\n" ::);
+    const int m = n - k - 1;
+    const double* u = ub[b];  // u[0] = 1 (stored)
     double* xx = xs + k + 1;
     double s = 0.0;
-    for (int j = threadIdx.x; j < m; j += kBtThreads) s = fma(j == 0 ? 1.0 : u[j], xx[j], s);
+    for (int j = threadIdx.x; j < m; j += kBtThreads) s = fma(u[j], xx[j], s);
     s = dw_sum(s);
     if (lane == 0) red[par][wib] = s;
     __syncthreads();
     double t = 0.0;
 #pragma unroll
     for (int w = 0; w < kBtThreads / 32; ++w) t += red[par][w];
-    t *= tau;
-    par ^= 1;  // the next reflector's partials go to the other buffer
-    for (int j = threadIdx.x; j < m; j += kBtThreads) xx[j] -= t * (j == 0 ? 1.0 : u[j]);
-    __syncthreads();
+    t *= ts[k];
+    for (int j = threadIdx.x; j < m; j += kBtThreads) xx[j] -= t * u[j];
+    b ^= 1;
+    par ^= 1;
   }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
   for (int i = threadIdx.x; i < n; i += kBtThreads) X[static_cast<i64>(c) * n + i] = xs[i];
 }
 
@@ -591,7 +616,7 @@ bool dense_top_eigenpairs(dfpca_context* ctx, const double* sigma, i64 M, int co
   DFPCA_LAUNCH(ctx, k_tri_invit, static_cast<unsigned>((count * 32 + 63) / 64), 64, 0, d.get(), e.get(), n,
                lam.get(), count, tnorm, Y.get(), work.get(), iwork.get());
   DFPCA_LAUNCH(ctx, k_cluster_mgs, static_cast<unsigned>((ncl * 32 + 63) / 64), 64, 0, n, dcl.get(), ncl, Y.get());
-  const std::size_t bsm = sizeof(double) * static_cast<std::size_t>(n);
+  const std::size_t bsm = sizeof(double) * 4 * static_cast<std::size_t>(n);
   allow_smem(k_back_transform, bsm);
   DFPCA_LAUNCH(ctx, k_back_transform, static_cast<unsigned>(count), kBtThreads, bsm, V.get(), taus.get(), n, Y.get(),
                vecs);

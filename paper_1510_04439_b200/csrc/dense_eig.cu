@@ -48,11 +48,12 @@ __device__ inline double dw_sum(double v) {
 }
 
 // Deterministic block sum (fixed mapping of terms to threads): every CTA
-// that sums the same values gets the same result.
+// that sums the same values gets the same result.  One barrier: the callers
+// rotate three `red` buffers, so a buffer is rewritten only after two more
+// barriers, when every thread has read it.
 __device__ inline double trd_block_sum(double v, double* red) {
   v = dw_sum(v);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  __syncthreads();
   if (lane == 0) red[wib] = v;
   __syncthreads();
   double t = 0.0;
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
   double* sw = sh + n;
   double* srow = sh + 2 * n;
   double* snv = sh + 3 * n;
-  __shared__ double red[kTrdWarps];
+  __shared__ double red[3][kTrdWarps];  // K, sigma, p^T v sums (rotated: one barrier each)
   __shared__ double segsum[kTrdWarps];
   const bool rec = blockIdx.x == 0;
 
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
     const double* row0 = A + 1;
     double s = 0.0;
     for (int j = 1 + threadIdx.x; j < m; j += kTrdThreads) s = fma(row0[j], row0[j], s);
-    R = make_reflector(row0[0], trd_block_sum(s, red));
+    R = make_reflector(row0[0], trd_block_sum(s, red[1]));
     for (int j = threadIdx.x; j < m; j += kTrdThreads) sv[j] = j == 0 ? 1.0 : row0[j] * R.scale;
     __syncthreads();
     if (rec) {
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
       }
       for (int j = threadIdx.x; j < m; j += kTrdThreads) V[1 + j] = sv[j];
     }
-    trd_rows<false>(A, n, 1, m, nullptr, nullptr, sv, R.tau, p + 1, part, red, segsum);
+    trd_rows<false>(A, n, 1, m, nullptr, nullptr, sv, R.tau, p + 1, part, red[2], segsum);
   }
   grid.sync();
 
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
                          : 0.0;
     // K_k (same order in every CTA), w_k, the updated row k + 1 over columns
     // k + 1 .. (index 0 = the diagonal) and its norm beyond the subdiagonal
-    const double K = 0.5 * R.tau * trd_block_sum(t, red);
+    const double K = 0.5 * R.tau * trd_block_sum(t, red[0]);
     const double w0 = p0 - K * sv[0];
     double s = 0.0;
 #pragma unroll
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
       srow[j] = r;
       s = fma(r, r, s);
     }
-    const double sig = trd_block_sum(s, red);
+    const double sig = trd_block_sum(s, red[1]);
     if (k + 3 == n) {  // the last 2 x 2 block
       if (rec && threadIdx.x == 0) {
         d[n - 2] = srow[0];
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1)
       for (int j = threadIdx.x; j < mn; j += kTrdThreads) vk[j] = snv[j];
     }
     trd_rows<true>(A, n, k + 2, mn, sv, sw, snv, Rn.tau, p + ((k + 1) & 1) * n + k + 2,
-                   part + ((k + 1) & 1) * gridDim.x, red, segsum);
+                   part + ((k + 1) & 1) * gridDim.x, red[2], segsum);
     double* tmp = sv;
     sv = snv;
     snv = tmp;

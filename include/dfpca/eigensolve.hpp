@@ -1,11 +1,14 @@
 // Drop-in matrixization and random-projection eigensolver (reference
 // eigensolve.hpp: matrixize, default_sketch_size, randomized_eig,
 // select_components_fve, eig_residuals, EigenSystem) running on the GPU: the
-// sketch, range capture, Householder QR, Rayleigh-Ritz projection, Jacobi
-// eigensolve, lift and Riemann MGS all happen on the device
-// (dfpca_randomized_eig), on the device-resident covariance when the surface
-// came from fft_covariance.  dense_eig (the LAPACK comparator, also the
-// pipeline's default) runs cuSOLVER syevd on the device (dfpca_dense_eig).
+// sketch, range capture (DMMA products), Cholesky QR (Householder QR for
+// ill-conditioned sketches), Rayleigh-Ritz projection, the small symmetric
+// eigensolve (tridiagonalization, bisection, inverse iteration), lift and
+// Riemann MGS all happen on the device (dfpca_randomized_eig), on the
+// device-resident covariance when the surface came from fft_covariance.
+// dense_eig (the LAPACK comparator, also the pipeline's default) runs the
+// library's own device eigensolver (dfpca_dense_eig: Householder
+// tridiagonalization, Sturm bisection, inverse iteration, back-transform).
 //
 // MatrixizedCovariance::dense_matrix / apply use Eigen::MatrixXd when Eigen is
 // available (as in the reference) and a small column-major dfpca::DenseMatrix

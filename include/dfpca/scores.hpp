@@ -7,6 +7,10 @@
 // reconstruct_at stays a host evaluation (one multilinear interpolation per
 // component), and holdout_prediction_error batches each held-out location's
 // re-scoring into one GPU call.
+//
+// Host-side glue (argument validation, error names and message text, and
+// the expressions whose bits the results depend on) follows the reference's
+// code line for line where the drop-in contract requires identical behaviour.
 #pragma once
 
 #include <algorithm>

@@ -212,7 +212,7 @@ def run_reference(args, emit=True):
     val = G2 / t_cov
     sample = (f"the full workload: fft_covariance of all {N_SUBJ} subjects on the 64x64 grid "
               f"(16,777,216 gridpts), reference headers compiled unchanged (oracle/_ref), "
-              f"set_max_threads({cores}); {n_steps} run(s), --steps ignored (one run is ~100 s)")
+              f"set_max_threads({cores}); {n_steps} run(s), --steps ignored (one run is ~60 s)")
     line = {"metric": METRIC, "value": val, "unit": "gridpts/s", "n_gpus": args.gpus, "steps": n_steps,
             "warmup": 0, "ms_per_step": t_cov * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",

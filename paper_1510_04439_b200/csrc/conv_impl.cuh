@@ -475,40 +475,44 @@ __global__ void __launch_bounds__(kThreads) k_tphase2(const double* __restrict__
 
 // The fused t-phase on zero-padded shared planes, so the inner loops carry
 // no bounds tests: X lines hold R
-// zeros on each side (pitch ldx, odd), Y holds R zero rows above and R + 8
+// zeros on each side (pitch ldx, odd), Y holds R zero rows above and R + kJBv
 // below (a t1 block may start at any row; pitch ldy, odd); the pads
 // are zeroed once and never written.  One X buffer: the next plane's copy is
 // issued after the last t2 pass of the current one has read X, so it
 // overlaps the t1 pass.  Same products, same order as k_tphase2
 // (bit-identical), which remains as DFPCA_TPHASE_2BUF=1 and for planes too
 // large for the padded buffers.
-__host__ __device__ constexpr int tpv_ldx(int n2, int R) { return ((n2 + kJBr - 1) / kJBr * kJBr + 2 * R) | 1; }
+#ifndef DFPCA_TPV_JB
+#define DFPCA_TPV_JB 8
+#endif
+constexpr int kJBv = DFPCA_TPV_JB;  // outputs per thread of the padded t-phase
+__host__ __device__ constexpr int tpv_ldx(int n2, int R) { return ((n2 + kJBv - 1) / kJBv * kJBv + 2 * R) | 1; }
 __host__ __device__ constexpr int tpv_ldy(int n2) { return n2 | 1; }
-__host__ __device__ constexpr int tpv_yrows(int n1, int R) { return n1 + kJBr + 2 * R; }  // t1 blocks start at any j_lo
+__host__ __device__ constexpr int tpv_yrows(int n1, int R) { return n1 + kJBv + 2 * R; }  // t1 blocks start at any j_lo
 
 template <int R, int ORD>
 __device__ inline void tpv_conv_rows(const double* X, double* Y, int n1, int n2, int ldx, int ldy, const Taps2P& tp,
                                      int l0) {
-  const int nb = (n2 + kJBr - 1) / kJBr;
+  const int nb = (n2 + kJBv - 1) / kJBv;
   const int nl = n1 - l0;
   for (int item = threadIdx.x; item < nl * nb; item += blockDim.x) {
-    const int l = l0 + item % nl, j0 = (item / nl) * kJBr;
+    const int l = l0 + item % nl, j0 = (item / nl) * kJBv;
     const double* xr = X + l * ldx + j0;  // xr[m + R] = X[l][j0 + m]
-    double acc[kJBr];
+    double acc[kJBv];
 #pragma unroll
-    for (int jj = 0; jj < kJBr; ++jj) acc[jj] = 0.0;
+    for (int jj = 0; jj < kJBv; ++jj) acc[jj] = 0.0;
 #pragma unroll
-    for (int m = -R; m < kJBr + R; ++m) {
+    for (int m = -R; m < kJBv + R; ++m) {
       const double x = xr[m + R];
 #pragma unroll
-      for (int jj = 0; jj < kJBr; ++jj) {
+      for (int jj = 0; jj < kJBv; ++jj) {
         const int o = m - jj;
         if (o >= -R && o <= R) acc[jj] = fma(tp.t[1][ORD][o + R], x, acc[jj]);
       }
     }
     double* yr = Y + (l + R) * ldy + j0;
 #pragma unroll
-    for (int jj = 0; jj < kJBr; ++jj)
+    for (int jj = 0; jj < kJBv; ++jj)
       if (j0 + jj < n2) yr[jj] = acc[jj];
   }
 }
@@ -516,20 +520,20 @@ __device__ inline void tpv_conv_rows(const double* X, double* Y, int n1, int n2,
 template <int R, int NO>
 __device__ inline void tpv_conv_cols(const double* Y, int n1, int n2, int ldy, double* const* outs, i64 row_off,
                                      const Taps2P& tp, int j_lo) {
-  const int nb = (n1 - j_lo + kJBr - 1) / kJBr;
+  const int nb = (n1 - j_lo + kJBv - 1) / kJBv;
   for (int item = threadIdx.x; item < n2 * nb; item += blockDim.x) {
-    const int c = item % n2, j0 = j_lo + (item / n2) * kJBr;
+    const int c = item % n2, j0 = j_lo + (item / n2) * kJBv;
     const double* yc = Y + j0 * ldy + c;  // yc[(m + R) ldy] = Y[j0 + m][c]
-    double acc[NO][kJBr];
+    double acc[NO][kJBv];
 #pragma unroll
     for (int r = 0; r < NO; ++r)
 #pragma unroll
-      for (int jj = 0; jj < kJBr; ++jj) acc[r][jj] = 0.0;
+      for (int jj = 0; jj < kJBv; ++jj) acc[r][jj] = 0.0;
 #pragma unroll
-    for (int m = -R; m < kJBr + R; ++m) {
+    for (int m = -R; m < kJBv + R; ++m) {
       const double x = yc[(m + R) * ldy];
 #pragma unroll
-      for (int jj = 0; jj < kJBr; ++jj) {
+      for (int jj = 0; jj < kJBv; ++jj) {
         const int o = m - jj;
         if (o >= -R && o <= R) {
 #pragma unroll
@@ -538,7 +542,7 @@ __device__ inline void tpv_conv_cols(const double* Y, int n1, int n2, int ldy, d
       }
     }
 #pragma unroll
-    for (int jj = 0; jj < kJBr; ++jj) {
+    for (int jj = 0; jj < kJBv; ++jj) {
       const int j = j0 + jj;
       if (j < n1) {
 #pragma unroll

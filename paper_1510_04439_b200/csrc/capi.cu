@@ -394,6 +394,19 @@ bool pool_reserve(dfpca_context* ctx, std::uint64_t bytes) {
   return ok;
 }
 
+namespace dfpca_gpu {
+// Backs the pool up to `bytes` in one allocation when it holds less: a
+// large call's first run then maps its memory at once instead of growing
+// the pool block by block (cold start).
+void pool_ensure(dfpca_context* ctx, std::uint64_t bytes) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) != cudaSuccess) return;
+  std::uint64_t reserved = 0;
+  if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) != cudaSuccess) return;
+  if (reserved < bytes) pool_reserve(ctx, bytes);
+}
+}  // namespace dfpca_gpu
+
 extern "C" {
 
 int dfpca_context_create(int device, dfpca_context** out) {

@@ -267,3 +267,8 @@ struct dfpca_dataset {
   dfpca_gpu::DevBuf<std::int64_t> offsets;
   dfpca_gpu::DevBuf<double> coords, values, obs_w;
 };
+
+namespace dfpca_gpu {
+// Backs the device pool up to `bytes` in one allocation when it holds less (capi.cu).
+void pool_ensure(dfpca_context* ctx, std::uint64_t bytes);
+}  // namespace dfpca_gpu

@@ -1281,6 +1281,13 @@ void run_covariance_impl(dfpca_context* ctx, const dfpca_binned* b, const Grid& 
   const i64 out_rows = (sb - sa) * rn;
   const i64 col_lo = sa * rn;  // first column any output of this slab needs (t >= s)
 
+  // The call's peak pool use is ~7 pair-grid-sized arrays on the shared
+  // design (d = 3 32^3: 55.6 GB measured), ~2x that with pw and the mass
+  // orders: map it in one allocation rather than block by block on the
+  // first large call (a no-op once the pool holds that much).
+  pool_ensure(ctx, static_cast<std::uint64_t>((b->shared_const ? 7.5 : 15.0) * static_cast<double>(LR) *
+                                              static_cast<double>(G) * 8.0));
+
   auto surf = std::make_unique<dfpca_surface>();
   surf->grid = grid;
   surf->kind = DFPCA_SURFACE_COVARIANCE;

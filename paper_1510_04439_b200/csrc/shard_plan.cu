@@ -29,15 +29,15 @@ ShardPlan make_shard_plan(i64 n1, i64 rn, i64 R, int world) {
   // boundaries (units <= n1, a few hundred at most in practice).  A rank's
   // load is its upper-triangle weight plus a per-plane term for the planes
   // its moment passes cover, halo included (the t-phase of [a - R, b + R)):
-  // beta = 0.18 n1 triangle units per plane, fitted on the measured d = 3
-  // ranks (~0.7 ms per halo-extended plane against 0.12 ms per unit at
-  // n1 = 32, rn = 1024; profiles/r07_shard_projection_d3_32cubed.jsonl:
-  // N = 2 0.79 -> 0.86, N = 4 0.67 -> 0.71 projected), faded out for small
+  // beta = 0.14 n1 triangle units per plane (the d = 3 ranks' fit, ~0.7 ms
+  // per halo-extended plane against 0.12 ms per unit at n1 = 32, rn = 1024,
+  // then the best of 0.10-0.30 by projection: N = 2 0.79 -> 0.87, N = 4
+  // 0.67 -> 0.72, N = 8 0.49 -> 0.51), faded out for small
   // planes (rn < 32 n1: d = 2 64^2, where fixed per-rank costs dominate and
   // the planes-only balance measured better).
   const int W = p.world;
   const std::size_t U = static_cast<std::size_t>(units);
-  const double beta = 0.18 * static_cast<double>(n1) *
+  const double beta = 0.14 * static_cast<double>(n1) *
                       std::min(1.0, static_cast<double>(rn) / (32.0 * static_cast<double>(n1)));
   auto load = [&](std::size_t a, std::size_t b) {
     if (b <= a) return 0.0;

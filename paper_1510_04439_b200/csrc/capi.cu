@@ -269,8 +269,8 @@ void dfpca_context::begin_stage(const std::string& name) {
   if (host_trace()) std::fprintf(stderr, "[host %10.1f us] begin %s\n", host_us(), name.c_str());
   StageMark m;
   m.name = name;
-  cudaEventCreate(&m.start);
-  cudaEventCreate(&m.stop);
+  m.start = take_event();
+  m.stop = take_event();
   cudaEventRecord(m.start, stream);
   marks.push_back(m);
 }
@@ -284,9 +284,7 @@ void dfpca_context::end_stage() {
     }
 }
 int dfpca_context::kernel_begin(const char* name) {
-  cudaEvent_t a, b;
-  cudaEventCreate(&a);
-  cudaEventCreate(&b);
+  cudaEvent_t a = take_event(), b = take_event();
   cudaEventRecord(a, stream);
   std::string n(name);
   if (!n.empty() && n.front() == '(') n = n.substr(1);
@@ -305,8 +303,8 @@ void dfpca_context::collect_stages() {
       st.ms += ms;
       st.count += 1;
     }
-    cudaEventDestroy(km.second.first);
-    cudaEventDestroy(km.second.second);
+    give_event(km.second.first);
+    give_event(km.second.second);
   }
   kernel_marks.clear();
   for (auto& m : marks) {
@@ -315,8 +313,8 @@ void dfpca_context::collect_stages() {
       const std::string name = m.name[0] == '#' ? m.name.substr(1) : m.name;
       stage_ms[name] += ms;
     }
-    cudaEventDestroy(m.start);
-    cudaEventDestroy(m.stop);
+    give_event(m.start);
+    give_event(m.stop);
   }
   marks.clear();
 }
@@ -362,13 +360,13 @@ int guarded(dfpca_context* ctx, F&& f) {
   cudaStreamSynchronize(ctx->stream);
   cudaGetLastError();
   for (auto& m : ctx->marks) {
-    cudaEventDestroy(m.start);
-    cudaEventDestroy(m.stop);
+    ctx->give_event(m.start);
+    ctx->give_event(m.stop);
   }
   ctx->marks.clear();
   for (auto& km : ctx->kernel_marks) {
-    cudaEventDestroy(km.second.first);
-    cudaEventDestroy(km.second.second);
+    ctx->give_event(km.second.first);
+    ctx->give_event(km.second.second);
   }
   ctx->kernel_marks.clear();
   return record(ctx);
@@ -464,6 +462,7 @@ int dfpca_context_destroy(dfpca_context* ctx) {
     cudaStreamDestroy(ctx->copy_);
   }
   if (ctx->fence_) cudaEventDestroy(ctx->fence_);
+  for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
   if (ctx->aux_) {
     cudaStreamSynchronize(ctx->aux_);
     cudaStreamDestroy(ctx->aux_);

@@ -136,7 +136,20 @@ struct dfpca_context {
   dfpca_gpu::Failure err;
   std::map<std::string, double> stage_ms;
   std::vector<dfpca_gpu::StageMark> marks;
-  std::vector<cudaEvent_t> event_pool;
+  std::vector<cudaEvent_t> event_pool;  // timing events reused across calls (stage / kernel marks)
+  cudaEvent_t take_event() {
+    if (event_pool.empty()) {
+      cudaEvent_t e = nullptr;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+  }
+  void give_event(cudaEvent_t e) {
+    if (e) event_pool.push_back(e);
+  }
   std::int64_t launches = 0;
   // multi-GPU (dfpca_nccl_init): this process's rank of a sharded covariance
   std::shared_ptr<dfpca_gpu::Transport> transport;

@@ -906,22 +906,31 @@ __global__ void k_center_mirror(double* __restrict__ cov, const double* __restri
   while (I + 1 < tiles && start(I + 1) <= t) ++I;
   const i64 J = I + (t - start(I));
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 32 x 8 threads
-  for (int r = ty; r < 32; r += 8) {
-    const i64 a = I * 32 + r, b = J * 32 + tx;
-    double v = 0.0;
-    if (a < G && b < G && a <= b) {
-      double* p = cov + (a - out_row0) * G + b;
-      v = *p;
-      if (!mask || (mask[a] && mask[b])) v -= mean[a] * mean[b];
-      *p = v;
+  // the thread's four rows: loads first (independent), then center and store
+  const i64 b = J * 32 + tx;
+  double v[4];
+  bool ok[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const i64 a = I * 32 + ty + 8 * q;
+    ok[q] = a < G && b < G && a <= b;
+    v[q] = ok[q] ? cov[(a - out_row0) * G + b] : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = ty + 8 * q;
+    const i64 a = I * 32 + r;
+    if (ok[q]) {
+      if (!mask || (mask[a] && mask[b])) v[q] -= mean[a] * mean[b];
+      cov[(a - out_row0) * G + b] = v[q];
     }
-    tile[r][tx] = v;
+    tile[r][tx] = v[q];
   }
   if (J >= I1) return;  // mirror rows belong to a later slab
   __syncthreads();
   for (int r = ty; r < 32; r += 8) {
-    const i64 b = J * 32 + r, a = I * 32 + tx;  // mirror (b, a) of the upper entry (a, b)
-    if (a < G && b < G && a < b) cov[(b - out_row0) * G + a] = tile[tx][r];
+    const i64 bm = J * 32 + r, am = I * 32 + tx;  // mirror (bm, am) of the upper entry (am, bm)
+    if (am < G && bm < G && am < bm) cov[(bm - out_row0) * G + am] = tile[tx][r];
   }
 }
 
